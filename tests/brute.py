@@ -1,0 +1,122 @@
+"""Independent brute-force neighbourhood generator (pure Python, tiny inputs).
+
+Pins the oracle's operator semantics and best move (SURVEY.md §8(c) "What pins
+each part": "An independent generator produces every solution reachable by one
+move ... scores it ... and compares the best score and the set of scores with
+the canonical enumerator").  It works on plain customer lists with Python list
+surgery -- no canonical slots, no positions, no shared code with oracle/.
+
+Operators (PAPER.md Fig. `operators` P:107-146; segment lengths per SURVEY
+§8(c) item 7): relocate/or-opt (segment of N consecutive customers moved to
+another route), swap/cross (exchange of an N1-segment and an N2-segment between
+two routes), 2-opt* (exchange of tails), 2-opt (reverse a block of one route),
+intra relocate (segment moved elsewhere in its own route), intra swap
+(exchange two disjoint segments of one route, first of length N1).
+"""
+from __future__ import annotations
+
+import math
+from typing import Dict, List, Tuple
+
+
+def simulate(dist, demand, tw, route):
+    """Event simulation of one route given as customers only (depot implicit).
+    Returns (distance, load, time_warp)."""
+    nodes = [0] + list(route) + [0]
+    D = sum(dist[nodes[k]][nodes[k + 1]] for k in range(len(nodes) - 1))
+    L = sum(demand[c] for c in route)
+    TV = 0.0
+    if tw is not None:
+        t = tw[0][0]
+        for k in range(1, len(nodes)):
+            p, q = nodes[k - 1], nodes[k]
+            arr = t + tw[p][2] + dist[p][q]
+            st = max(arr, tw[q][0])
+            if st > tw[q][1]:
+                TV += st - tw[q][1]
+                st = tw[q][1]
+            t = st
+    return D, L, TV
+
+
+def segments(route, n):
+    return [(i, route[i:i + n]) for i in range(0, len(route) - n + 1)]
+
+
+def neighbours(routes: List[List[int]], op: str, n1: int = 1, n2: int = 1):
+    """Yield (changed_route_ids, new_routes_for_them) for one operator/variant."""
+    R = len(routes)
+    if op == "relocate":
+        for a in range(R):
+            for i, seg in segments(routes[a], n1):
+                rest = routes[a][:i] + routes[a][i + n1:]
+                for b in range(R):
+                    if b == a:
+                        continue
+                    for k in range(len(routes[b]) + 1):
+                        yield (a, b), (rest, routes[b][:k] + seg + routes[b][k:])
+    elif op == "swap":
+        for a in range(R):
+            for b in range(R):
+                if a == b or (n1 == n2 and b < a):
+                    continue
+                for i, sa in segments(routes[a], n1):
+                    for j, sb in segments(routes[b], n2):
+                        yield (a, b), (routes[a][:i] + sb + routes[a][i + n1:],
+                                       routes[b][:j] + sa + routes[b][j + n2:])
+    elif op == "2opt*":
+        for a in range(R):
+            for b in range(a + 1, R):
+                for i in range(len(routes[a]) + 1):
+                    for j in range(len(routes[b]) + 1):
+                        yield (a, b), (routes[a][:i] + routes[b][j:],
+                                       routes[b][:j] + routes[a][i:])
+    elif op == "2opt":
+        for a in range(R):
+            r = routes[a]
+            for i in range(len(r)):
+                for j in range(i + 1, len(r)):
+                    yield (a,), (r[:i] + r[i:j + 1][::-1] + r[j + 1:],)
+    elif op == "intra_relocate":
+        for a in range(R):
+            r = routes[a]
+            for i, seg in segments(r, n1):
+                rest = r[:i] + r[i + n1:]
+                for k in range(len(rest) + 1):
+                    if k == i:
+                        continue  # the identity placement
+                    yield (a,), (rest[:k] + seg + rest[k:],)
+    elif op == "intra_swap":
+        for a in range(R):
+            r = routes[a]
+            for i in range(len(r)):
+                for j in range(i + n1, len(r) - n2 + 1):
+                    if i + n1 > len(r):
+                        continue
+                    new = r[:i] + r[j:j + n2] + r[i + n1:j] + r[i:i + n1] + r[j + n2:]
+                    yield (a,), (new,)
+    else:
+        raise ValueError(op)
+
+
+def scores(dist, demand, tw, capacity, routes, op, n1=1, n2=1, mode=0, wQ=10.0, wT=10.0):
+    """List of scores of every neighbour (feasible-only: inf if infeasible)."""
+    cur = {}
+    for idx, r in enumerate(routes):
+        cur[idx] = simulate(dist, demand, tw, r)
+    out = []
+    for ids, news in neighbours(routes, op, n1, n2):
+        dD = dLV = dTV = 0.0
+        feas = True
+        for rid, nr in zip(ids, news):
+            D, L, TV = simulate(dist, demand, tw, nr)
+            D0, L0, TV0 = cur[rid]
+            dD += D - D0
+            dLV += max(L - capacity, 0) - max(L0 - capacity, 0)
+            dTV += TV - TV0
+            feas = feas and L <= capacity and TV == 0
+        if mode == 0:
+            out.append(dD if feas else math.inf)
+        else:
+            out.append(dD + wQ * dLV + wT * dTV)
+    return out

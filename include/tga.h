@@ -1,0 +1,227 @@
+/*
+ * tga.h -- C ABI of the B200-native full-neighbourhood VRP move evaluator.
+ *
+ * The hot path of arXiv 2506.17357 ("Speeding up Local Optimization in
+ * Vehicle Routing with Tensor-based GPU Acceleration", TGA): for every
+ * candidate of the 2-opt, 2-opt*, relocate, swap, or-opt and cross-exchange
+ * operators, compute the delta cost and the capacity / time-window
+ * feasibility from per-position attribute records, reduce to the best move,
+ * and apply it with an incremental attribute rebuild.
+ *
+ * Citations: P:n = PAPER.md line n (with its section / equation).
+ *   Problem statement and inputs .......... §2, P:49-58 (Eq. 1)
+ *   Concatenation algebra ................. §4.3, Eq. 2,
+ *                                           Eq. 3e-f, Eq. 4
+ *   Workflow (init / evaluate / update) ... §5.1; Alg. A2
+ *   Operators ............................. §4.1, Fig. `operators` P:107-149
+ *   Evaluation + argmin ................... §5.3.4, Eq. 16
+ *   Tensor update ......................... §5.3.5
+ *
+ * Conventions (all calls):
+ *   - Every function returns an int32 status: TGA_OK (0), a positive
+ *     informational code, or a negative error.  Nothing aborts and no C++
+ *     exception crosses the boundary.  tga_last_error() returns a
+ *     thread-local message for the last failing call on this thread.
+ *   - Host pointers passed in are only read during the call (the library
+ *     copies what it keeps); the caller keeps ownership.  Opaque objects are
+ *     owned by the library and freed by their *_destroy.  A solution must not
+ *     outlive its instance.
+ *   - One host thread at a time per solution object.
+ *   - Node 0 is the depot; customers are 1..n_nodes-1.
+ *   - Travel time equals travel distance (T = C), as in the GH/Solomon
+ *     convention; the inter-route kernels require a symmetric matrix.
+ */
+#ifndef TGA_H
+#define TGA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------ status codes */
+#define TGA_OK                    0
+#define TGA_NO_IMPROVING_MOVE     1   /* best score >= 0, or every candidate infeasible */
+#define TGA_ERR_INVALID_ARGUMENT (-1) /* sizes, e > l, d < 0, non-zero diagonal, capacity <= 0, NULL */
+#define TGA_ERR_STRUCTURE        (-2) /* routes do not cover every customer exactly once / id out of range */
+#define TGA_ERR_STALE            (-3) /* move from an older solution generation */
+#define TGA_ERR_UNSUPPORTED      (-4) /* 2-opt on a time-windowed instance; asymmetric C; T != C */
+#define TGA_ERR_CUDA             (-5)
+#define TGA_ERR_NCCL             (-6)
+#define TGA_ERR_OOM              (-7)
+
+/* ------------------------------------------------------------ data types */
+#define TGA_I32 0   /* integer distances (CVRP nint; VRPTW integer tenths) -> exact */
+#define TGA_F32 1   /* real distances/times held in fp32 on the device            */
+
+/* ------------------------------------------------------------ move variants
+ * A variant is an operator with fixed segment lengths.  Its id is its rank in
+ * the deterministic tie-break "lowest (score, variant, flat index)"
+ * (reading 5 in DESIGN.md).  Candidate spaces (canonical slots):
+ *   2OPT        intra, reverse customers u..v of one route (CVRP only)
+ *   2OPT_STAR   inter, cut after slot u of route a and v of route b, route(u)<route(v)
+ *   RELOCATE1   inter, move customer u after slot v of another route
+ *   OROPT2/3    inter, move the segment u..u+N-1 (N=2,3) after slot v of another route
+ *   SWAP11      inter, exchange customers u and v, route(u)<route(v)
+ *   CROSSn1n2   inter, exchange segment u..u+N1-1 with v..v+N2-1 (N1<=N2; N1==N2 => route(u)<route(v))
+ *   IRELOCATEn  intra, move segment u..u+N-1 after the node originally at slot v
+ *   ISWAPn1n2   intra, exchange segments at u (length N1) and v (length N2), u+N1<=v
+ */
+enum {
+    TGA_V_2OPT = 0,
+    TGA_V_2OPT_STAR = 1,
+    TGA_V_RELOCATE1 = 2, TGA_V_OROPT2 = 3, TGA_V_OROPT3 = 4,
+    TGA_V_SWAP11 = 5,
+    TGA_V_CROSS12 = 6, TGA_V_CROSS13 = 7, TGA_V_CROSS22 = 8, TGA_V_CROSS23 = 9, TGA_V_CROSS33 = 10,
+    TGA_V_IRELOCATE1 = 11, TGA_V_IRELOCATE2 = 12, TGA_V_IRELOCATE3 = 13,
+    TGA_V_ISWAP11 = 14, TGA_V_ISWAP12 = 15, TGA_V_ISWAP13 = 16,
+    TGA_V_ISWAP21 = 17, TGA_V_ISWAP22 = 18, TGA_V_ISWAP23 = 19,
+    TGA_V_ISWAP31 = 20, TGA_V_ISWAP32 = 21, TGA_V_ISWAP33 = 22,
+    TGA_N_VARIANTS = 23
+};
+
+/* operator masks (bit i = variant i); OR them for a fused sweep */
+#define TGA_OP_2OPT           (1u << TGA_V_2OPT)
+#define TGA_OP_2OPT_STAR      (1u << TGA_V_2OPT_STAR)
+#define TGA_OP_RELOCATE       (1u << TGA_V_RELOCATE1)
+#define TGA_OP_OR_OPT         ((1u << TGA_V_OROPT2) | (1u << TGA_V_OROPT3))
+#define TGA_OP_SWAP           (1u << TGA_V_SWAP11)
+#define TGA_OP_CROSS          (0x1Fu << TGA_V_CROSS12)
+#define TGA_OP_INTRA_RELOCATE (0x7u << TGA_V_IRELOCATE1)
+#define TGA_OP_INTRA_SWAP     (0x1FFu << TGA_V_ISWAP11)
+#define TGA_OP_INTER          (0x7FEu)
+#define TGA_OP_INTRA          (TGA_OP_2OPT | TGA_OP_INTRA_RELOCATE | TGA_OP_INTRA_SWAP)
+#define TGA_OP_ALL            ((1u << TGA_N_VARIANTS) - 1u)
+/* the north-star fused sweep: 2-opt* + relocate + swap */
+#define TGA_OP_FUSED_NS       (TGA_OP_2OPT_STAR | TGA_OP_RELOCATE | TGA_OP_SWAP)
+
+/* score modes (Eq. 16a: F = F(dD, dT_V, dL_V), never given by the paper; reading 4) */
+#define TGA_SCORE_FEASIBLE  0   /* score = dD if both new routes are feasible, else +inf */
+#define TGA_SCORE_PENALISED 1   /* score = dD + w_load * dL_V + w_tw * dT_V */
+
+typedef struct tga_instance tga_instance;
+typedef struct tga_solution tga_solution;
+
+typedef struct {
+    int32_t score_mode;  /* TGA_SCORE_*; default TGA_SCORE_FEASIBLE */
+    int32_t w_load;      /* integer penalty weight on load excess (default 10) */
+    int32_t w_tw;        /* integer penalty weight on time warp (default 10) */
+    int32_t device;      /* CUDA device ordinal; -1 = current device */
+    int32_t reserved[12];
+} tga_options;
+
+typedef struct {
+    int32_t variant;             /* TGA_V_* */
+    int32_t n1, n2;              /* segment lengths (0 where not applicable) */
+    int32_t route_a, pos_a;      /* route / position of slot u (position 0 = start depot) */
+    int32_t route_b, pos_b;      /* route / position of slot v; route_a == route_b => intra */
+    int32_t u, v;                /* canonical slot ids */
+    int32_t feasible;            /* 1 if both changed routes are feasible */
+    int64_t delta_i;             /* score in integer mode (TGA_I32); == dD in feasible-only mode */
+    double  delta_f;             /* score as a double (both modes) */
+    uint64_t key;                /* packed (order-preserving score << 32 | flat index) */
+    uint64_t generation;         /* solution generation this move belongs to */
+} tga_move;
+
+/* ------------------------------------------------------------ instance
+ * tga_instance_create: upload one instance (§2).
+ *   n_nodes   number of nodes incl. the depot (>= 2)
+ *   dist      n_nodes*n_nodes row-major distances c_ij (= travel times t_ij),
+ *             int32 (dist_dtype TGA_I32) or float (TGA_F32); zero diagonal,
+ *             non-negative, symmetric
+ *   time      must be NULL (T = C); non-NULL => TGA_ERR_UNSUPPORTED
+ *   demand    n_nodes int32 delivery demands d_i >= 0, d_0 = 0
+ *   tw        NULL for CVRP, else n_nodes*3 floats {e_i, l_i, s_i} in the
+ *             distance unit, e_i <= l_i, s_0 = 0
+ *   capacity  vehicle capacity Q > 0
+ *   opt       NULL = defaults
+ *   out       receives the instance
+ * Errors: TGA_ERR_INVALID_ARGUMENT, TGA_ERR_UNSUPPORTED, TGA_ERR_CUDA, TGA_ERR_OOM. */
+int32_t tga_instance_create(int32_t n_nodes, const void *dist, int32_t dist_dtype,
+                            const void *time, const int32_t *demand, const float *tw,
+                            int32_t capacity, const tga_options *opt, tga_instance **out);
+int32_t tga_instance_destroy(tga_instance *inst);
+
+/* ------------------------------------------------------------ solution
+ * tga_solution_load: "a solution tensor T_s is first initialized on the GPU
+ * using the attribute matrices derived from S".  Builds the slot
+ * layout, the position-ordered distance matrix and the forward/backward
+ * attribute records (attribute-rebuild scan).
+ *   n_routes   number of routes R >= 1 (empty routes allowed; never renumbered)
+ *   route_ptr  R+1 int32 CSR offsets into customers
+ *   customers  route_ptr[R] int32 customer ids; every customer exactly once
+ * Errors: TGA_ERR_STRUCTURE, TGA_ERR_INVALID_ARGUMENT, TGA_ERR_CUDA, TGA_ERR_OOM. */
+int32_t tga_solution_load(tga_instance *inst, int32_t n_routes, const int32_t *route_ptr,
+                          const int32_t *customers, tga_solution **out);
+int32_t tga_solution_destroy(tga_solution *sol);
+
+/* tga_eval: enqueue the evaluation of every variant in op_mask on
+ * cuda_stream (a cudaStream_t; NULL = the solution's own stream) and return
+ * without synchronising (Extraction/Concatenation/Differencing/Evaluation,
+ * P:241 steps 1-4, fused into one kernel per candidate space).  With a
+ * communicator (tga_comm_init) only this rank's shard of the candidate rows
+ * is evaluated and the packed keys are MIN-allreduced over NCCL on the same
+ * stream.  Errors: TGA_ERR_UNSUPPORTED (2-opt with time windows), TGA_ERR_CUDA. */
+int32_t tga_eval(tga_solution *sol, uint32_t op_mask, void *cuda_stream);
+
+/* tga_best_move: synchronise the stream, read the per-variant keys (8 B each)
+ * and decode the best over op_mask ("transferred to the CPU").
+ * Returns TGA_OK if the best score is < 0, TGA_NO_IMPROVING_MOVE otherwise
+ * (out is still filled when any candidate was valid; out->key = ~0 if none). */
+int32_t tga_best_move(tga_solution *sol, uint32_t op_mask, tga_move *out);
+
+/* tga_apply_move: apply a move returned by tga_best_move for this generation
+ * ("update the solution S, and synchronize the updated solution tensor",
+ * P:241 step 5; §5.3.5): splice the 1-2 route lists, re-upload only the
+ * changed slot span, refresh its rows/columns of the distance tile matrix and
+ * re-scan the affected routes.  Errors: TGA_ERR_STALE, TGA_ERR_INVALID_ARGUMENT. */
+int32_t tga_apply_move(tga_solution *sol, const tga_move *move);
+
+/* Per-variant raw keys of the last tga_eval (synchronises). keys[TGA_N_VARIANTS];
+ * ~0 = no valid candidate. */
+int32_t tga_solution_keys(tga_solution *sol, uint64_t *keys);
+
+/* Exact candidate counts per variant for the current solution (closed forms;
+ * host only). counts[TGA_N_VARIANTS]. */
+int32_t tga_solution_counts(const tga_solution *sol, uint64_t *counts);
+
+/* Totals from the device attribute records: distance D(S) (Eq. 1, mu1=0,
+ * mu2=1), sum of load excess max(L-Q,0), sum of time warp. */
+int32_t tga_solution_cost(tga_solution *sol, int64_t *dist_i, double *dist_f,
+                          int64_t *load_excess, double *tw_excess);
+
+/* Export the routes (CSR). route_ptr[R+1], customers[N]. */
+int32_t tga_solution_routes(const tga_solution *sol, int32_t *route_ptr, int32_t *customers);
+/* R, N, canonical slot count Q = N + R, generation */
+int32_t tga_solution_info(const tga_solution *sol, int32_t *n_routes, int32_t *n_customers,
+                          int32_t *n_slots, uint64_t *generation);
+
+/* Attribute records per canonical slot (Q entries each), for parity with a
+ * from-scratch rebuild: prefix [0..p] and suffix [p..L+1] loads and
+ * distances; prefix/suffix time warp T_V; service start time at p derived
+ * from the prefix record (start = T_E + T_D - T_V - s).  Any pointer may be NULL. */
+int32_t tga_solution_attributes(tga_solution *sol, int64_t *pre_L, int64_t *suf_L,
+                                double *pre_D, double *suf_D, double *pre_TV,
+                                double *suf_TV, double *start);
+
+/* ------------------------------------------------------------ multi-GPU
+ * Row sharding: a solution with a shard plan (n_shards > 1) evaluates only
+ * shard `shard` of the inter-route tile rows and intra-route slot rows.
+ * tga_comm_init attaches an NCCL communicator (nccl_unique_id = 128-byte
+ * ncclUniqueId shared by all ranks) and makes tga_eval MIN-allreduce the
+ * packed keys (exact: keys are (score, canonical index)). */
+int32_t tga_solution_set_shard(tga_solution *sol, int32_t shard, int32_t n_shards);
+int32_t tga_nccl_unique_id(void *out_128_bytes);
+int32_t tga_comm_init(tga_solution *sol, int32_t rank, int32_t world, const void *nccl_unique_id);
+
+/* ------------------------------------------------------------ misc */
+const char *tga_last_error(void);
+const char *tga_version(void);
+/* number of CUDA kernels this library launched so far (for the bench's gpu_launches) */
+uint64_t tga_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TGA_H */

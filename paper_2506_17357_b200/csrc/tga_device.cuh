@@ -1,0 +1,121 @@
+// tga_device.cuh -- device-side building blocks of the TGA hot path (sm_100a).
+//
+// Attribute records and the concatenation algebra of PAPER.md §4.3:
+//   Eq. 2   D(s1 + s2)   = D(s1) + c_jk + D(s2)
+//   Eq. 3ef L_M(s1 + s2) = L_M(s1) + L_M(s2)   (no pickups)
+//   Eq. 4   time-warp record {T_D, T_E, T_L, T_V}, T_W == 0 reading
+// and the packed (score, canonical index) key of the fused argmin
+// (Eq. 16c; deterministic lowest-index tie-break, reading 5).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tga {
+
+// ------------------------------------------------------------------ records
+// A time-window record of a subsequence: x = T_D (duration incl.
+// waiting), y = T_E (earliest start), z = T_L (latest start), w = T_V (warp).
+using TwRec = float4;
+
+// Eq. 4b-4h with T_W(s1) == 0 (reading 1).  `t` is t_jk, the travel
+// time from the last node of a to the first node of b.  In TW-I mode every
+// operand is an integer-valued float below 2^24, so the result is exact.
+__host__ __device__ __forceinline__ TwRec tw_cat(const TwRec a, const TwRec b, const float t) {
+    const float dt = a.x + t - a.w;                  // Eq. 4b  Delta_t
+    const float dw = fmaxf(b.y - dt - a.z, 0.0f);    // Eq. 4c  Delta_w
+    const float dv = fmaxf(a.y + dt - b.z, 0.0f);    // Eq. 4d  Delta_v
+    TwRec r;
+    r.x = a.x + t + dw + b.x;                        // Eq. 4e  T_D
+    r.y = fmaxf(a.y, b.y - dt) - dw;                 // Eq. 4f  T_E
+    r.z = fminf(a.z, b.z - dt) + dv;                 // Eq. 4g  T_L
+    r.w = a.w + dv + b.w;                            // Eq. 4h  T_V
+    return r;
+}
+
+// Eq. 4a: a single node k: T_D = s_k, T_E = e_k, T_L = l_k, T_V = 0.
+__host__ __device__ __forceinline__ TwRec tw_single(float e, float l, float s) {
+    return make_float4(s, e, l, 0.0f);
+}
+
+// ------------------------------------------------------------------ keys
+// Order-preserving 32-bit images of a score.
+__device__ __forceinline__ uint32_t ord_score(int32_t s) { return static_cast<uint32_t>(s) ^ 0x80000000u; }
+__device__ __forceinline__ uint32_t ord_score(float s) {
+    const uint32_t u = __float_as_uint(s);
+    return u ^ ((u & 0x80000000u) ? 0xFFFFFFFFu : 0x80000000u);
+}
+constexpr uint64_t kNoKey = ~0ull;
+
+__device__ __forceinline__ uint64_t pack_key(uint32_t ord, uint32_t idx) {
+    return (static_cast<uint64_t>(ord) << 32) | idx;
+}
+
+__device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+
+__device__ __forceinline__ uint64_t warp_min64(uint64_t k) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) k = umin64(k, __shfl_xor_sync(0xffffffffu, k, off));
+    return k;
+}
+
+// ------------------------------------------------------------------ scoring
+// Score of a candidate (Eq. 16a; modes = DESIGN.md reading 4).
+//   feasible-only : dD if every new route has L <= Q and T_V == 0, else no key
+//   penalised     : dD + wQ * dL_V + wT * dT_V
+struct ScoreParams {
+    int32_t capacity;
+    int32_t mode;      // 0 feasible-only, 1 penalised
+    int32_t wQ, wT;
+};
+
+template <class DT> struct ScoreT;
+template <> struct ScoreT<int32_t> {
+    __device__ __forceinline__ static int32_t tv(float x) { return __float2int_rn(x); }
+};
+template <> struct ScoreT<float> {
+    __device__ __forceinline__ static float tv(float x) { return x; }
+};
+
+// dLV / dTV are differences of new-minus-old excess (old values per route).
+template <class DT, bool TW>
+__device__ __forceinline__ uint64_t score_key(const ScoreParams &sp, bool valid, DT dD,
+                                              int32_t la, int32_t lb, int32_t la0, int32_t lb0,
+                                              float tva, float tvb, float tva0, float tvb0,
+                                              uint32_t idx) {
+    const int32_t Q = sp.capacity;
+    if (sp.mode == 0) {
+        bool feas = valid && (la <= Q) && (lb <= Q);
+        if (TW) feas = feas && (tva == 0.0f) && (tvb == 0.0f);
+        return feas ? pack_key(ord_score(dD), idx) : kNoKey;
+    }
+    const int32_t dlv = max(la - Q, 0) + max(lb - Q, 0) - max(la0 - Q, 0) - max(lb0 - Q, 0);
+    DT s = dD + static_cast<DT>(sp.wQ * dlv);
+    if (TW) s += static_cast<DT>(sp.wT) * ScoreT<DT>::tv((tva + tvb) - (tva0 + tvb0));
+    return valid ? pack_key(ord_score(s), idx) : kNoKey;
+}
+
+// ------------------------------------------------------------------ launch-side views
+// Device view of one solution (all arrays indexed by physical slot unless noted).
+template <class DT>
+struct SolView {
+    // layout
+    const int32_t *node, *route, *pos, *rlen, *canon;
+    // loads: prefix [0..x] and suffix [x..L+1]
+    const int32_t *fwdL, *bwdL;
+    // distances: edge x -> x+1, and bridge_N[x] = c(x-1, x+N) (N = 1..3)
+    const DT *enext;
+    const DT *bridge1, *bridge2, *bridge3;
+    // time-window records: prefix, suffix, segments of 2 and 3 starting at x
+    const TwRec *fwdT, *bwdT, *seg2T, *seg3T;
+    const TwRec *node_tw;     // per node: (s, e, l, 0)
+    // per route
+    const int32_t *rW;        // load
+    const float *rTV;         // time warp
+    // position-ordered distance matrix Dp[a][b] = c(node(a), node(b))
+    const DT *Dp;
+    int32_t pitch;            // elements per Dp row
+    int32_t Qp;               // physical slots (rows of Dp)
+    uint32_t Qc;              // canonical slot count Q = N + R (flat index = u * Qc + v)
+};
+
+}  // namespace tga

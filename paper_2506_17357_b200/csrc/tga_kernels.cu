@@ -1,0 +1,664 @@
+// tga_kernels.cu -- hand-written sm_100a kernels of the TGA hot path.
+//
+//   k_dp_rows / k_dp_cols   position-ordered distance matrix Dp[a][b] = c(node a, node b)
+//                           (build, and the row/column refresh of the update step)
+//   k_scan                  attribute rebuild: per-route segmented prefix/suffix scans with
+//                           warp shuffles of the Eq. 2 / 3e-f / 4 records
+//   k_inter<DT,TW,MASK>     inter-route candidates (2-opt*, relocate/or-opt, swap/cross),
+//                           TMA-staged Dp tiles, branch-free feasibility, fused argmin
+//                           (P:241 steps 1-4; Eq. 16)
+//   k_intra<DT,TW>          intra-route candidates (2-opt, intra relocate, intra swap) with
+//                           incremental middle-segment composition
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "tga_device.cuh"
+#include "tga_launch.h"
+
+namespace tga {
+
+// ============================================================== Dp build / refresh
+__device__ __forceinline__ int bits(int32_t v) { return v; }
+__device__ __forceinline__ int bits(float v) { return __float_as_int(v); }
+
+template <class DT>
+__global__ void __launch_bounds__(256) k_dp_rows(DT *__restrict__ Dp, int pitch,
+                                                 const int32_t *__restrict__ node,
+                                                 const DT *__restrict__ C, int n, int lo, int hi) {
+    const int a = lo + blockIdx.y;
+    if (a >= hi) return;
+    const DT *crow = C + static_cast<size_t>(node[a]) * n;
+    DT *drow = Dp + static_cast<size_t>(a) * pitch;
+    for (int b = 4 * (blockIdx.x * blockDim.x + threadIdx.x); b < pitch; b += 4 * gridDim.x * blockDim.x) {
+        const int4 nd = *reinterpret_cast<const int4 *>(node + b);
+        const DT v0 = __ldg(crow + nd.x), v1 = __ldg(crow + nd.y), v2 = __ldg(crow + nd.z), v3 = __ldg(crow + nd.w);
+        *reinterpret_cast<int4 *>(drow + b) = make_int4(bits(v0), bits(v1), bits(v2), bits(v3));
+    }
+}
+
+// columns b in [lo, hi) of every row (the transpose half of a refresh)
+template <class DT>
+__global__ void __launch_bounds__(256) k_dp_cols(DT *__restrict__ Dp, int pitch,
+                                                 const int32_t *__restrict__ node,
+                                                 const DT *__restrict__ C, int n, int rows, int lo, int hi) {
+    const int b = lo + blockIdx.x * 32 + threadIdx.x;
+    const int a = blockIdx.y * 8 + threadIdx.y;
+    if (b >= hi || a >= rows) return;
+    Dp[static_cast<size_t>(a) * pitch + b] = __ldg(C + static_cast<size_t>(node[a]) * n + node[b]);
+}
+
+// ============================================================== attribute rebuild scan
+// One warp per route; chunks of 32 positions with carries.  Positions
+// k = 0..L+1 of route r live at physical slots base..base+L+1.
+template <class DT, bool TW>
+__global__ void __launch_bounds__(256) k_scan(ScanArgs<DT> A, int r_lo, int r_hi) {
+    const int lane = threadIdx.x & 31;
+    const int r = r_lo + static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    if (r >= r_hi) return;
+    const int base = A.rbase[r];
+    const int L = A.rlenR[r];
+    const int len = L + 2;
+    const int n = A.n_nodes;
+
+    // ---------------- forward pass: prefix loads, prefix distance, prefix TW records
+    int carryL = 0;
+    DT carryD = DT(0);
+    TwRec carryT = make_float4(0.f, 0.f, 0.f, 0.f);
+    DT carryE = DT(0);  // edge into the first position of the chunk
+    for (int c0 = 0; c0 < len; c0 += 32) {
+        const int k = c0 + lane;
+        const bool in = k < len;
+        const int x = base + k;
+        const int nd = in ? A.node[x] : 0;
+        const bool has_next = in && (k + 1 < len);
+        const int nn = has_next ? A.node[x + 1] : 0;
+        const DT e = has_next ? A.C[static_cast<size_t>(nd) * n + nn] : DT(0);
+        // loads (Eq. 3e-f): inclusive prefix sum
+        int sL = in ? A.demand[nd] : 0;
+        DT sD = e;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int oL = __shfl_up_sync(0xffffffffu, sL, off);
+            const DT oD = __shfl_up_sync(0xffffffffu, sD, off);
+            if (lane >= off) { sL += oL; sD += oD; }
+        }
+        const int fL = carryL + sL;
+        const DT fD = carryD + sD - e;  // exclusive: distance of [0..k] (Eq. 2)
+        TwRec fT = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (TW) {
+            const TwRec nt = A.node_tw[nd];
+            TwRec rec = nt;
+            // link into this position = edge (k-1 -> k)
+            const DT ein_lane = __shfl_up_sync(0xffffffffu, e, 1);
+            float inl = (lane == 0) ? static_cast<float>(carryE) : static_cast<float>(ein_lane);
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                TwRec o;
+                o.x = __shfl_up_sync(0xffffffffu, rec.x, off);
+                o.y = __shfl_up_sync(0xffffffffu, rec.y, off);
+                o.z = __shfl_up_sync(0xffffffffu, rec.z, off);
+                o.w = __shfl_up_sync(0xffffffffu, rec.w, off);
+                const float oin = __shfl_up_sync(0xffffffffu, inl, off);
+                if (lane >= off) { rec = tw_cat(o, rec, inl); inl = oin; }
+            }
+            fT = (c0 > 0) ? tw_cat(carryT, rec, inl) : rec;
+        }
+        if (in) {
+            A.fwdL[x] = fL;
+            A.fwdD[x] = fD;
+            A.enext[x] = e;
+            if (TW) A.fwdT[x] = fT;
+        }
+        const int last = min(31, len - 1 - c0);
+        carryL = __shfl_sync(0xffffffffu, fL, last);
+        carryD = __shfl_sync(0xffffffffu, fD + e, last);
+        carryE = __shfl_sync(0xffffffffu, e, last);
+        if (TW) {
+            carryT.x = __shfl_sync(0xffffffffu, fT.x, last);
+            carryT.y = __shfl_sync(0xffffffffu, fT.y, last);
+            carryT.z = __shfl_sync(0xffffffffu, fT.z, last);
+            carryT.w = __shfl_sync(0xffffffffu, fT.w, last);
+        }
+    }
+    if (lane == 0) {
+        A.rW[r] = carryL;
+        if (TW) A.rTV[r] = carryT.w;
+    }
+
+    // ---------------- backward pass: suffix loads, suffix distance, suffix TW records
+    int bcarryL = 0;
+    DT bcarryD = DT(0);
+    TwRec bcarryT = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int nchunks = (len + 31) / 32;
+    for (int ci = nchunks - 1; ci >= 0; --ci) {
+        const int c0 = ci * 32;
+        const int nvalid = min(32, len - c0);
+        const int k = c0 + lane;
+        const bool in = lane < nvalid;
+        const int x = base + k;
+        const int nd = in ? A.node[x] : 0;
+        const DT e = in ? A.enext[x] : DT(0);  // written by the forward pass (same warp)
+        int sL = in ? A.demand[nd] : 0;
+        DT sD = e;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int oL = __shfl_down_sync(0xffffffffu, sL, off);
+            const DT oD = __shfl_down_sync(0xffffffffu, sD, off);
+            if (lane + off < nvalid) { sL += oL; sD += oD; }
+        }
+        const int bL = bcarryL + sL;
+        const DT bD = bcarryD + sD;
+        TwRec bT = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (TW) {
+            TwRec rec = A.node_tw[nd];
+            float outl = static_cast<float>(e);  // edge out of the record's last position
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                TwRec o;
+                o.x = __shfl_down_sync(0xffffffffu, rec.x, off);
+                o.y = __shfl_down_sync(0xffffffffu, rec.y, off);
+                o.z = __shfl_down_sync(0xffffffffu, rec.z, off);
+                o.w = __shfl_down_sync(0xffffffffu, rec.w, off);
+                const float oout = __shfl_down_sync(0xffffffffu, outl, off);
+                if (lane + off < nvalid) { rec = tw_cat(rec, o, outl); outl = oout; }
+            }
+            bT = (ci < nchunks - 1) ? tw_cat(rec, bcarryT, outl) : rec;
+        }
+        if (in) {
+            A.bwdL[x] = bL;
+            A.bwdD[x] = bD;
+            if (TW) A.bwdT[x] = bT;
+        }
+        bcarryL = __shfl_sync(0xffffffffu, bL, 0);
+        bcarryD = __shfl_sync(0xffffffffu, bD, 0);
+        if (TW) {
+            bcarryT.x = __shfl_sync(0xffffffffu, bT.x, 0);
+            bcarryT.y = __shfl_sync(0xffffffffu, bT.y, 0);
+            bcarryT.z = __shfl_sync(0xffffffffu, bT.z, 0);
+            bcarryT.w = __shfl_sync(0xffffffffu, bT.w, 0);
+        }
+    }
+    if (lane == 0) A.rD[r] = bcarryD;
+
+    // ---------------- per-position segment records and bridges (N = 1..3)
+    for (int k = lane; k < len; k += 32) {
+        const int x = base + k;
+        // bridge_N[x] = c(x-1, x+N): the edge that closes the gap left by removing
+        // the segment x..x+N-1 (relocate / or-opt removal, Eq. 2)
+        const int np = (k >= 1) ? A.node[x - 1] : 0;
+        DT b1 = DT(0), b2 = DT(0), b3 = DT(0);
+        if (k >= 1 && k + 1 <= len - 1) b1 = A.C[static_cast<size_t>(np) * n + A.node[x + 1]];
+        if (k >= 1 && k + 2 <= len - 1) b2 = A.C[static_cast<size_t>(np) * n + A.node[x + 2]];
+        if (k >= 1 && k + 3 <= len - 1) b3 = A.C[static_cast<size_t>(np) * n + A.node[x + 3]];
+        A.bridge1[x] = b1;
+        A.bridge2[x] = b2;
+        A.bridge3[x] = b3;
+        if (TW) {
+            const TwRec s1 = A.node_tw[A.node[x]];
+            TwRec s2 = s1, s3 = s1;
+            if (k + 1 < len) {
+                s2 = tw_cat(s1, A.node_tw[A.node[x + 1]], static_cast<float>(A.enext[x]));
+                s3 = s2;
+                if (k + 2 < len) s3 = tw_cat(s2, A.node_tw[A.node[x + 2]], static_cast<float>(A.enext[x + 1]));
+            }
+            A.seg2T[x] = s2;
+            A.seg3T[x] = s3;
+        }
+    }
+}
+
+// ============================================================== TMA / mbarrier helpers
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(phase)
+            : "memory");
+    } while (!done);
+}
+// 2-D TMA tile load: box at (x = column, y = row) of the tensor map into smem.
+__device__ __forceinline__ void tma_load_2d(void *smem_dst, const CUtensorMap *map, int x, int y, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+            "r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// ============================================================== inter-route evaluation
+// Tile: TU u-rows x TV v-columns of the (physical) slot pair space; the Dp box
+// with a halo (rows u0-1 .. u0+TU+2, cols v0-1 .. v0+TV+2) is TMA-loaded into
+// shared memory (double-buffered across the persistent tile loop).
+// Thread mapping: lane -> v = v0 + lane + 32*j (j < VPT); warp -> UPW rows.
+template <class DT, bool TW, uint32_t MASK>
+__global__ void __launch_bounds__(kInterThreads) k_inter(const SolView<DT> S, const __grid_constant__ CUtensorMap tmap,
+                                                         const uint32_t *__restrict__ tiles, int t_lo, int t_hi,
+                                                         ScoreParams sp, uint64_t *__restrict__ keys) {
+    constexpr int TU = kTileU, TV = kTileV, VPT = TV / 32, UPW = TU / (kInterThreads / 32);
+    constexpr int BW = kBoxW, BH = kBoxH;
+    constexpr int NV = 11;  // inter variant ids 1..10
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    DT *buf0 = reinterpret_cast<DT *>(smem_raw);
+    DT *buf1 = reinterpret_cast<DT *>(smem_raw + kBoxBytesPadded);
+    __shared__ uint64_t bar[2];
+    __shared__ unsigned long long red[NV];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_barrier_init();
+    }
+    if (tid < NV) red[tid] = kNoKey;
+    __syncthreads();
+
+    uint64_t best[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) best[i] = kNoKey;
+
+    auto issue = [&](int t, int b) {
+        const uint32_t ij = tiles[t];
+        const int I = ij >> 16, J = ij & 0xFFFF;
+        mbar_expect_tx(&bar[b], kBoxBytes);
+        tma_load_2d(b ? buf1 : buf0, &tmap, J * TV - 1, I * TU - 1, &bar[b]);
+    };
+
+    int t = t_lo + blockIdx.x;
+    if (tid == 0 && t < t_hi) issue(t, 0);
+    uint32_t phase0 = 0, phase1 = 0;
+    for (int it = 0; t < t_hi; t += gridDim.x, ++it) {
+        const int b = it & 1;
+        const int tn = t + gridDim.x;
+        if (tid == 0 && tn < t_hi) issue(tn, b ^ 1);
+        if (b == 0) { mbar_wait(&bar[0], phase0); phase0 ^= 1; }
+        else        { mbar_wait(&bar[1], phase1); phase1 ^= 1; }
+        const DT *tile = b ? buf1 : buf0;
+        const uint32_t ij = tiles[t];
+        const int u0 = (ij >> 16) * TU, v0 = (ij & 0xFFFF) * TV;
+        // Dp(x, y) from the staged box
+        auto Dt = [&](int x, int y) -> DT { return tile[(x - u0 + 1) * BW + (y - v0 + 1)]; };
+
+#pragma unroll 1
+        for (int j = 0; j < VPT; ++j) {
+            const int v = v0 + lane + 32 * j;
+            const int cv = S.canon[v];
+            const int rv = S.route[v];
+            const int pv = S.pos[v];
+            const int Lb = S.rlen[v];
+            const int Wb = (rv >= 0) ? S.rW[rv] : 0;
+            const float TVb = (TW && rv >= 0) ? S.rTV[rv] : 0.f;
+#pragma unroll 1
+            for (int i = 0; i < UPW; ++i) {
+                const int u = u0 + warp * UPW + i;
+                const int cu = S.canon[u];
+                const int ru = S.route[u];
+                if (cu < 0) continue;  // warp-uniform: end depot / padding row
+                const bool pair = (cv >= 0) && (ru < rv);
+                const int pu = S.pos[u];
+                const int La = S.rlen[u];
+                const int Wa = S.rW[ru];
+                const float TVa = TW ? S.rTV[ru] : 0.f;
+                const uint32_t idx_uv = static_cast<uint32_t>(cu) * S.Qc + static_cast<uint32_t>(cv);
+                const uint32_t idx_vu = static_cast<uint32_t>(cv) * S.Qc + static_cast<uint32_t>(cu);
+
+                // ---- 2-opt* (3-Seq(0,0) P:346; Eq. 14)
+                if (MASK & (1u << 1)) {
+                    const DT dD = Dt(u, v + 1) + Dt(u + 1, v) - S.enext[u] - S.enext[v];
+                    const int la = S.fwdL[u] + S.bwdL[v + 1];
+                    const int lb = S.fwdL[v] + S.bwdL[u + 1];
+                    float ta = 0.f, tb = 0.f;
+                    if (TW) {
+                        ta = tw_cat(S.fwdT[u], S.bwdT[v + 1], static_cast<float>(Dt(u, v + 1))).w;
+                        tb = tw_cat(S.fwdT[v], S.bwdT[u + 1], static_cast<float>(Dt(u + 1, v))).w;
+                    }
+                    best[1] = umin64(best[1], score_key<DT, TW>(sp, pair, dD, la, lb, Wa, Wb, ta, tb, TVa, TVb, idx_uv));
+                }
+                // ---- relocate (N=1) / or-opt (N=2,3): both directions (Eq. 13)
+#pragma unroll
+                for (int N = 1; N <= 3; ++N) {
+                    if (!(MASK & (1u << (1 + N)))) continue;
+                    const DT *bridge = N == 1 ? S.bridge1 : (N == 2 ? S.bridge2 : S.bridge3);
+                    const TwRec *segT = N == 1 ? nullptr : (N == 2 ? S.seg2T : S.seg3T);
+                    {   // segment u..u+N-1 (route a) inserted after v (route b)
+                        const bool ok = pair && pu >= 1 && pu + N - 1 <= La;
+                        const DT dD = bridge[u] - S.enext[u - 1] - S.enext[u + N - 1] + Dt(u, v) +
+                                      Dt(u + N - 1, v + 1) - S.enext[v];
+                        const int s = S.fwdL[u + N - 1] - S.fwdL[u - 1];
+                        float ta = 0.f, tb = 0.f;
+                        if (TW) {
+                            const TwRec sg = N == 1 ? S.node_tw[S.node[u]] : segT[u];
+                            ta = tw_cat(S.fwdT[u - 1], S.bwdT[u + N], static_cast<float>(bridge[u])).w;
+                            const TwRec X = tw_cat(S.fwdT[v], sg, static_cast<float>(Dt(u, v)));
+                            tb = tw_cat(X, S.bwdT[v + 1], static_cast<float>(Dt(u + N - 1, v + 1))).w;
+                        }
+                        best[1 + N] = umin64(best[1 + N], score_key<DT, TW>(sp, ok, dD, Wa - s, Wb + s, Wa, Wb,
+                                                                            ta, tb, TVa, TVb, idx_uv));
+                    }
+                    {   // segment v..v+N-1 (route b) inserted after u (route a)
+                        const bool ok = pair && pv >= 1 && pv + N - 1 <= Lb;
+                        const DT dD = bridge[v] - S.enext[v - 1] - S.enext[v + N - 1] + Dt(u, v) +
+                                      Dt(u + 1, v + N - 1) - S.enext[u];
+                        const int s = S.fwdL[v + N - 1] - S.fwdL[v - 1];
+                        float ta = 0.f, tb = 0.f;
+                        if (TW) {
+                            const TwRec sg = N == 1 ? S.node_tw[S.node[v]] : segT[v];
+                            tb = tw_cat(S.fwdT[v - 1], S.bwdT[v + N], static_cast<float>(bridge[v])).w;
+                            const TwRec X = tw_cat(S.fwdT[u], sg, static_cast<float>(Dt(u, v)));
+                            ta = tw_cat(X, S.bwdT[u + 1], static_cast<float>(Dt(u + 1, v + N - 1))).w;
+                        }
+                        best[1 + N] = umin64(best[1 + N], score_key<DT, TW>(sp, ok, dD, Wa + s, Wb - s, Wa, Wb,
+                                                                            ta, tb, TVa, TVb, idx_vu));
+                    }
+                }
+                // ---- swap (1,1) / cross-exchange (N1,N2) (3-Seq(N1,N2) P:346)
+#pragma unroll
+                for (int sv = 0; sv < 6; ++sv) {
+                    const int vid = 5 + sv;
+                    if (!(MASK & (1u << vid))) continue;
+                    const int N1 = sv == 0 ? 1 : (sv <= 2 ? 1 : (sv <= 4 ? 2 : 3));
+                    const int N2 = sv == 0 ? 1 : (sv == 1 ? 2 : (sv == 2 ? 3 : (sv == 3 ? 2 : 3)));
+                    auto seg = [&](int x, int N) -> TwRec {
+                        return N == 1 ? S.node_tw[S.node[x]] : (N == 2 ? S.seg2T[x] : S.seg3T[x]);
+                    };
+                    {   // N1-segment at u (route a), N2-segment at v (route b)
+                        const bool ok = pair && pu >= 1 && pu + N1 - 1 <= La && pv >= 1 && pv + N2 - 1 <= Lb;
+                        const DT dD = Dt(u - 1, v) + Dt(u + N1, v + N2 - 1) + Dt(u, v - 1) + Dt(u + N1 - 1, v + N2) -
+                                      S.enext[u - 1] - S.enext[u + N1 - 1] - S.enext[v - 1] - S.enext[v + N2 - 1];
+                        const int sa = S.fwdL[u + N1 - 1] - S.fwdL[u - 1];
+                        const int sb = S.fwdL[v + N2 - 1] - S.fwdL[v - 1];
+                        float ta = 0.f, tb = 0.f;
+                        if (TW) {
+                            const TwRec A1 = tw_cat(S.fwdT[u - 1], seg(v, N2), static_cast<float>(Dt(u - 1, v)));
+                            ta = tw_cat(A1, S.bwdT[u + N1], static_cast<float>(Dt(u + N1, v + N2 - 1))).w;
+                            const TwRec B1 = tw_cat(S.fwdT[v - 1], seg(u, N1), static_cast<float>(Dt(u, v - 1)));
+                            tb = tw_cat(B1, S.bwdT[v + N2], static_cast<float>(Dt(u + N1 - 1, v + N2))).w;
+                        }
+                        best[vid] = umin64(best[vid], score_key<DT, TW>(sp, ok, dD, Wa - sa + sb, Wb - sb + sa, Wa,
+                                                                        Wb, ta, tb, TVa, TVb, idx_uv));
+                    }
+                    if (N1 != N2) {   // N1-segment at v (route b), N2-segment at u (route a)
+                        const bool ok = pair && pv >= 1 && pv + N1 - 1 <= Lb && pu >= 1 && pu + N2 - 1 <= La;
+                        const DT dD = Dt(u, v - 1) + Dt(u + N2 - 1, v + N1) + Dt(u - 1, v) + Dt(u + N2, v + N1 - 1) -
+                                      S.enext[v - 1] - S.enext[v + N1 - 1] - S.enext[u - 1] - S.enext[u + N2 - 1];
+                        const int sb = S.fwdL[v + N1 - 1] - S.fwdL[v - 1];
+                        const int sa = S.fwdL[u + N2 - 1] - S.fwdL[u - 1];
+                        float ta = 0.f, tb = 0.f;
+                        if (TW) {
+                            const TwRec B1 = tw_cat(S.fwdT[v - 1], seg(u, N2), static_cast<float>(Dt(u, v - 1)));
+                            tb = tw_cat(B1, S.bwdT[v + N1], static_cast<float>(Dt(u + N2 - 1, v + N1))).w;
+                            const TwRec A1 = tw_cat(S.fwdT[u - 1], seg(v, N1), static_cast<float>(Dt(u - 1, v)));
+                            ta = tw_cat(A1, S.bwdT[u + N2], static_cast<float>(Dt(u + N2, v + N1 - 1))).w;
+                        }
+                        best[vid] = umin64(best[vid], score_key<DT, TW>(sp, ok, dD, Wa - sa + sb, Wb - sb + sa, Wa,
+                                                                        Wb, ta, tb, TVa, TVb, idx_vu));
+                    }
+                }
+            }
+        }
+        __syncthreads();  // every thread is done with this buffer before it is refilled
+    }
+
+    // ---- fused argmin: warp shuffle -> shared -> one 64-bit atomicMin per variant per CTA
+#pragma unroll
+    for (int i = 1; i < NV; ++i) {
+        if (!(MASK & (1u << i))) continue;
+        const uint64_t k = warp_min64(best[i]);
+        if (lane == 0 && k != kNoKey) atomicMin(&red[i], static_cast<unsigned long long>(k));
+    }
+    __syncthreads();
+    if (tid < NV && (MASK & (1u << tid)) && red[tid] != kNoKey)
+        atomicMin(reinterpret_cast<unsigned long long *>(keys) + tid, red[tid]);
+}
+
+// ============================================================== intra-route evaluation
+// One thread per (slot u, intra variant); the thread walks v along the route so
+// the middle segment of Intra-Relocate / Intra-Swap is composed incrementally
+// (one Eq. 4 concatenation per step).
+__constant__ int kIntraVariants[13] = {0, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20, 21, 22};
+
+template <class DT, bool TW>
+__global__ void __launch_bounds__(256) k_intra(const SolView<DT> S, ScoreParams sp, uint32_t vmask, int x_lo,
+                                               int x_hi, uint64_t *__restrict__ keys) {
+    __shared__ unsigned long long red[23];
+    if (threadIdx.x < 23) red[threadIdx.x] = kNoKey;
+    __syncthreads();
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int x = x_lo + t / 13;
+    const int var = kIntraVariants[t % 13];
+    uint64_t best = kNoKey;
+    if (x < x_hi && (vmask & (1u << var)) && S.canon[x] >= 0 && S.pos[x] >= 1) {
+        const int p = S.pos[x], L = S.rlen[x], r = S.route[x];
+        const int base = x - p;
+        const int W = S.rW[r];
+        const float TV0 = TW ? S.rTV[r] : 0.f;
+        const uint32_t cu = static_cast<uint32_t>(S.canon[x]);
+        const uint32_t cbase = cu - static_cast<uint32_t>(p);
+        auto D = [&](int a, int b) -> DT { return S.Dp[static_cast<size_t>(a) * S.pitch + b]; };
+        auto E = [&](int a) -> DT { return S.enext[a]; };
+        auto seg = [&](int a, int N) -> TwRec {
+            return N == 1 ? S.node_tw[S.node[a]] : (N == 2 ? S.seg2T[a] : S.seg3T[a]);
+        };
+        auto key = [&](DT dD, float tv, int q) -> uint64_t {
+            return score_key<DT, TW>(sp, true, dD, W, 0, W, 0, tv, 0.f, TV0, 0.f, cu * S.Qc + cbase + q);
+        };
+        if (var == 0) {
+            // 2-opt: reverse u..v (Eq. 7); loads unchanged; CVRP only (host-checked)
+            for (int q = p + 1; q <= L; ++q) {
+                const int v = base + q;
+                const DT dD = D(x - 1, v) + D(x, v + 1) - E(x - 1) - E(v);
+                best = umin64(best, key(dD, 0.f, q));
+            }
+        } else if (var <= 13) {
+            // intra relocate / or-opt of x..x+N-1 after the node originally at q
+            const int N = var - 10;
+            if (p + N - 1 <= L) {
+                const DT rem = (N == 1 ? S.bridge1[x] : (N == 2 ? S.bridge2[x] : S.bridge3[x])) -
+                               E(x - 1) - E(x + N - 1);
+                // forward: route' = [0..u-1] + [u+N..q] + seg + [q+1..]
+                TwRec P = make_float4(0.f, 0.f, 0.f, 0.f);
+                TwRec sg = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (TW) {
+                    sg = seg(x, N);
+                    const float br = static_cast<float>(N == 1 ? S.bridge1[x] : (N == 2 ? S.bridge2[x] : S.bridge3[x]));
+                    if (p + N <= L) P = tw_cat(S.fwdT[x - 1], S.node_tw[S.node[x + N]], br);
+                }
+                for (int q = p + N; q <= L; ++q) {
+                    const int v = base + q;
+                    if (TW && q > p + N) P = tw_cat(P, S.node_tw[S.node[v]], static_cast<float>(E(v - 1)));
+                    const DT dD = rem + D(v, x) + D(x + N - 1, v + 1) - E(v);
+                    float tv = 0.f;
+                    if (TW) {
+                        const TwRec A2 = tw_cat(P, sg, static_cast<float>(D(v, x)));
+                        tv = tw_cat(A2, S.bwdT[v + 1], static_cast<float>(D(x + N - 1, v + 1))).w;
+                    }
+                    best = umin64(best, key(dD, tv, q));
+                }
+                // backward: route' = [0..q] + seg + [q+1..u-1] + [u+N..]
+                TwRec T = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (TW && p >= 2) {
+                    const float br = static_cast<float>(N == 1 ? S.bridge1[x] : (N == 2 ? S.bridge2[x] : S.bridge3[x]));
+                    T = tw_cat(S.node_tw[S.node[x - 1]], S.bwdT[x + N], br);
+                }
+                for (int q = p - 2; q >= 0; --q) {
+                    const int v = base + q;
+                    if (TW && q < p - 2) T = tw_cat(S.node_tw[S.node[v + 1]], T, static_cast<float>(E(v + 1)));
+                    const DT dD = rem + D(v, x) + D(x + N - 1, v + 1) - E(v);
+                    float tv = 0.f;
+                    if (TW) {
+                        const TwRec A2 = tw_cat(S.fwdT[v], sg, static_cast<float>(D(v, x)));
+                        tv = tw_cat(A2, T, static_cast<float>(D(x + N - 1, v + 1))).w;
+                    }
+                    best = umin64(best, key(dD, tv, q));
+                }
+            }
+        } else {
+            // intra swap (N1 at u, N2 at v), u+N1 <= v
+            const int N1 = (var - 14) / 3 + 1, N2 = (var - 14) % 3 + 1;
+            if (p + N1 - 1 <= L) {
+                TwRec M = make_float4(0.f, 0.f, 0.f, 0.f);
+                const TwRec s1 = TW ? seg(x, N1) : M;
+                for (int q = p + N1; q + N2 - 1 <= L; ++q) {
+                    const int v = base + q;
+                    DT dD;
+                    float tv = 0.f;
+                    if (q == p + N1) {  // adjacent: [0..u-1] + seg_v + seg_u + [v+N2..]
+                        dD = D(x - 1, v) + D(v + N2 - 1, x) + D(x + N1 - 1, v + N2) - E(x - 1) - E(v - 1) -
+                             E(v + N2 - 1);
+                        if (TW) {
+                            const TwRec R1 = tw_cat(S.fwdT[x - 1], seg(v, N2), static_cast<float>(D(x - 1, v)));
+                            const TwRec R3 = tw_cat(R1, s1, static_cast<float>(D(v + N2 - 1, x)));
+                            tv = tw_cat(R3, S.bwdT[v + N2], static_cast<float>(D(x + N1 - 1, v + N2))).w;
+                        }
+                    } else {            // [0..u-1] + seg_v + [u+N1..v-1] + seg_u + [v+N2..]
+                        if (TW) {
+                            const TwRec nv1 = S.node_tw[S.node[v - 1]];
+                            M = (q == p + N1 + 1) ? nv1 : tw_cat(M, nv1, static_cast<float>(E(v - 2)));
+                        }
+                        dD = D(x - 1, v) + D(v + N2 - 1, x + N1) + D(v - 1, x) + D(x + N1 - 1, v + N2) - E(x - 1) -
+                             E(x + N1 - 1) - E(v - 1) - E(v + N2 - 1);
+                        if (TW) {
+                            const TwRec R1 = tw_cat(S.fwdT[x - 1], seg(v, N2), static_cast<float>(D(x - 1, v)));
+                            const TwRec R2 = tw_cat(R1, M, static_cast<float>(D(v + N2 - 1, x + N1)));
+                            const TwRec R3 = tw_cat(R2, s1, static_cast<float>(D(v - 1, x)));
+                            tv = tw_cat(R3, S.bwdT[v + N2], static_cast<float>(D(x + N1 - 1, v + N2))).w;
+                        }
+                    }
+                    best = umin64(best, key(dD, tv, q));
+                }
+            }
+        }
+    }
+    if (best != kNoKey) atomicMin(&red[var], static_cast<unsigned long long>(best));
+    __syncthreads();
+    if (threadIdx.x < 23 && red[threadIdx.x] != kNoKey)
+        atomicMin(reinterpret_cast<unsigned long long *>(keys) + threadIdx.x, red[threadIdx.x]);
+}
+
+// ============================================================== launchers
+static unsigned long long g_launches = 0;
+unsigned long long launch_count() { return g_launches; }
+
+template <class DT>
+cudaError_t launch_dp(DT *Dp, int pitch, const int32_t *node, const DT *C, int n, int Qp, int lo, int hi,
+                      bool full, cudaStream_t st) {
+    if (hi <= lo) return cudaSuccess;
+    {
+        dim3 grid(std::max(1, std::min(8, (pitch / 4 + 255) / 256)), hi - lo);
+        k_dp_rows<DT><<<grid, 256, 0, st>>>(Dp, pitch, node, C, n, lo, hi);
+        ++g_launches;
+    }
+    if (!full) {
+        dim3 grid((hi - lo + 31) / 32, (Qp + 7) / 8);
+        k_dp_cols<DT><<<grid, dim3(32, 8), 0, st>>>(Dp, pitch, node, C, n, Qp, lo, hi);
+        ++g_launches;
+    }
+    return cudaGetLastError();
+}
+
+template <class DT>
+cudaError_t launch_scan(const ScanArgs<DT> &A, bool tw, int r_lo, int r_hi, cudaStream_t st) {
+    if (r_hi <= r_lo) return cudaSuccess;
+    const int warps = r_hi - r_lo;
+    const int blocks = (warps * 32 + 255) / 256;
+    if (tw) k_scan<DT, true><<<blocks, 256, 0, st>>>(A, r_lo, r_hi);
+    else    k_scan<DT, false><<<blocks, 256, 0, st>>>(A, r_lo, r_hi);
+    ++g_launches;
+    return cudaGetLastError();
+}
+
+template <class DT, bool TW, uint32_t MASK>
+static cudaError_t launch_inter_t(const SolView<DT> &S, const CUtensorMap &map, const uint32_t *tiles, int t_lo,
+                                  int t_hi, const ScoreParams &sp, uint64_t *keys, int grid, cudaStream_t st) {
+    auto kern = k_inter<DT, TW, MASK>;
+    const int smem = 2 * kBoxBytesPadded;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr = true;
+    }
+    kern<<<grid, kInterThreads, smem, st>>>(S, map, tiles, t_lo, t_hi, sp, keys);
+    ++g_launches;
+    return cudaGetLastError();
+}
+
+// compiled MASK groups; a request is decomposed into these
+template <class DT, bool TW>
+static cudaError_t launch_inter_tw(uint32_t mask, const SolView<DT> &S, const CUtensorMap &map, const uint32_t *tiles,
+                                   int t_lo, int t_hi, const ScoreParams &sp, uint64_t *keys, int grid,
+                                   cudaStream_t st) {
+    cudaError_t err = cudaSuccess;
+    auto run = [&](auto kmask) {
+        if (err == cudaSuccess)
+            err = launch_inter_t<DT, TW, decltype(kmask)::value>(S, map, tiles, t_lo, t_hi, sp, keys, grid, st);
+    };
+    constexpr uint32_t ALL = 0x7FEu, NS = (1u << 1) | (1u << 2) | (1u << 5);
+    if ((mask & ALL) == ALL) { run(std::integral_constant<uint32_t, ALL>{}); return err; }
+    if ((mask & NS) == NS) { run(std::integral_constant<uint32_t, NS>{}); mask &= ~NS; }
+    if (mask & (1u << 1)) run(std::integral_constant<uint32_t, (1u << 1)>{});
+    if (mask & (1u << 2)) run(std::integral_constant<uint32_t, (1u << 2)>{});
+    if (mask & (3u << 3)) run(std::integral_constant<uint32_t, (3u << 3)>{});
+    if (mask & (1u << 5)) run(std::integral_constant<uint32_t, (1u << 5)>{});
+    if (mask & (0x1Fu << 6)) run(std::integral_constant<uint32_t, (0x1Fu << 6)>{});
+    return err;
+}
+
+template <class DT>
+cudaError_t launch_inter(uint32_t mask, bool tw, const SolView<DT> &S, const CUtensorMap &map, const uint32_t *tiles,
+                         int t_lo, int t_hi, const ScoreParams &sp, uint64_t *keys, int grid, cudaStream_t st) {
+    if (t_hi <= t_lo || !(mask & 0x7FEu)) return cudaSuccess;
+    return tw ? launch_inter_tw<DT, true>(mask, S, map, tiles, t_lo, t_hi, sp, keys, grid, st)
+              : launch_inter_tw<DT, false>(mask, S, map, tiles, t_lo, t_hi, sp, keys, grid, st);
+}
+
+template <class DT>
+cudaError_t launch_intra(uint32_t mask, bool tw, const SolView<DT> &S, const ScoreParams &sp, int x_lo, int x_hi,
+                         uint64_t *keys, cudaStream_t st) {
+    const uint32_t intra = mask & ((1u << 0) | (0x7u << 11) | (0x1FFu << 14));
+    if (x_hi <= x_lo || !intra) return cudaSuccess;
+    const int threads = (x_hi - x_lo) * 13;
+    const int blocks = (threads + 255) / 256;
+    if (tw) k_intra<DT, true><<<blocks, 256, 0, st>>>(S, sp, intra, x_lo, x_hi, keys);
+    else    k_intra<DT, false><<<blocks, 256, 0, st>>>(S, sp, intra, x_lo, x_hi, keys);
+    ++g_launches;
+    return cudaGetLastError();
+}
+
+// explicit instantiations
+template cudaError_t launch_dp<int32_t>(int32_t *, int, const int32_t *, const int32_t *, int, int, int, int, bool,
+                                        cudaStream_t);
+template cudaError_t launch_dp<float>(float *, int, const int32_t *, const float *, int, int, int, int, bool,
+                                      cudaStream_t);
+template cudaError_t launch_scan<int32_t>(const ScanArgs<int32_t> &, bool, int, int, cudaStream_t);
+template cudaError_t launch_scan<float>(const ScanArgs<float> &, bool, int, int, cudaStream_t);
+template cudaError_t launch_inter<int32_t>(uint32_t, bool, const SolView<int32_t> &, const CUtensorMap &,
+                                           const uint32_t *, int, int, const ScoreParams &, uint64_t *, int,
+                                           cudaStream_t);
+template cudaError_t launch_inter<float>(uint32_t, bool, const SolView<float> &, const CUtensorMap &, const uint32_t *,
+                                         int, int, const ScoreParams &, uint64_t *, int, cudaStream_t);
+template cudaError_t launch_intra<int32_t>(uint32_t, bool, const SolView<int32_t> &, const ScoreParams &, int, int,
+                                           uint64_t *, cudaStream_t);
+template cudaError_t launch_intra<float>(uint32_t, bool, const SolView<float> &, const ScoreParams &, int, int,
+                                         uint64_t *, cudaStream_t);
+
+}  // namespace tga

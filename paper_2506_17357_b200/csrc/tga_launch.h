@@ -1,0 +1,54 @@
+// tga_launch.h -- host-side launch interface of the TGA kernels (internal).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <type_traits>
+#include <algorithm>
+
+#include "tga_device.cuh"
+
+namespace tga {
+
+// inter-route tile geometry (see k_inter)
+constexpr int kInterThreads = 256;
+constexpr int kTileU = 32;                      // u rows per tile
+constexpr int kTileV = 64;                      // v columns per tile
+constexpr int kBoxW = kTileV + 4;               // Dp box columns: v0-1 .. v0+TV+2
+constexpr int kBoxH = kTileU + 4;               // Dp box rows:    u0-1 .. u0+TU+2
+constexpr int kBoxBytes = kBoxW * kBoxH * 4;
+constexpr int kBoxBytesPadded = (kBoxBytes + 127) / 128 * 128;
+constexpr int kPitchAlign = 64;                 // Dp pitch: multiple of lcm(TU, TV)
+constexpr int kGuard = 8;                       // guard slots before/after every slot array
+
+template <class DT>
+struct ScanArgs {
+    int n_nodes;
+    const DT *C;
+    const int32_t *demand;
+    const TwRec *node_tw;
+    const int32_t *node;
+    const int32_t *rbase, *rlenR;
+    int32_t *fwdL, *bwdL;
+    DT *enext, *fwdD, *bwdD;
+    DT *bridge1, *bridge2, *bridge3;
+    TwRec *fwdT, *bwdT, *seg2T, *seg3T;
+    int32_t *rW;
+    float *rTV;
+    DT *rD;
+};
+
+template <class DT>
+cudaError_t launch_dp(DT *Dp, int pitch, const int32_t *node, const DT *C, int n, int Qp, int lo, int hi,
+                      bool full, cudaStream_t st);
+template <class DT>
+cudaError_t launch_scan(const ScanArgs<DT> &A, bool tw, int r_lo, int r_hi, cudaStream_t st);
+template <class DT>
+cudaError_t launch_inter(uint32_t mask, bool tw, const SolView<DT> &S, const CUtensorMap &map, const uint32_t *tiles,
+                         int t_lo, int t_hi, const ScoreParams &sp, uint64_t *keys, int grid, cudaStream_t st);
+template <class DT>
+cudaError_t launch_intra(uint32_t mask, bool tw, const SolView<DT> &S, const ScoreParams &sp, int x_lo, int x_hi,
+                         uint64_t *keys, cudaStream_t st);
+unsigned long long launch_count();
+
+}  // namespace tga

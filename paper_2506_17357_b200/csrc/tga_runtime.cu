@@ -1,0 +1,855 @@
+// tga_runtime.cu -- host runtime behind the tga_* C ABI (include/tga.h).
+//
+// Owns instance / solution state, the physical slot layout, device memory,
+// the TMA descriptor of the position-ordered distance matrix, the tile plan
+// (and its row shards), the NCCL communicator, and the host side of the
+// update step (route-list splice + span re-upload, P:241 step 5).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <limits>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "tga.h"
+#include "tga_launch.h"
+
+using namespace tga;
+
+// ============================================================== errors
+static thread_local std::string g_err;
+static int32_t fail(int32_t code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+#define TGA_CUDA(x)                                                                            \
+    do {                                                                                       \
+        cudaError_t e_ = (x);                                                                  \
+        if (e_ != cudaSuccess) {                                                               \
+            return fail(e_ == cudaErrorMemoryAllocation ? TGA_ERR_OOM : TGA_ERR_CUDA,          \
+                        std::string(#x) + ": " + cudaGetErrorString(e_));                      \
+        }                                                                                      \
+    } while (0)
+
+// ============================================================== NCCL (dlopen'd)
+namespace {
+typedef struct ncclComm *ncclComm_t;
+typedef struct { char internal[128]; } ncclUniqueId;
+typedef int ncclResult_t;
+constexpr int kNcclUint64 = 5, kNcclMin = 3;
+struct Nccl {
+    void *h = nullptr;
+    ncclResult_t (*getUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*allReduce)(const void *, void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    const char *(*errStr)(ncclResult_t) = nullptr;
+    bool load() {
+        if (h) return true;
+        h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return false;
+        getUniqueId = reinterpret_cast<decltype(getUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+        commInitRank = reinterpret_cast<decltype(commInitRank)>(dlsym(h, "ncclCommInitRank"));
+        allReduce = reinterpret_cast<decltype(allReduce)>(dlsym(h, "ncclAllReduce"));
+        commDestroy = reinterpret_cast<decltype(commDestroy)>(dlsym(h, "ncclCommDestroy"));
+        errStr = reinterpret_cast<decltype(errStr)>(dlsym(h, "ncclGetErrorString"));
+        return getUniqueId && commInitRank && allReduce && commDestroy;
+    }
+};
+Nccl g_nccl;
+
+// ============================================================== TMA descriptor
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// variant -> segment lengths (0 = n/a)
+void variant_lengths(int v, int *n1, int *n2) {
+    *n1 = *n2 = 0;
+    if (v >= TGA_V_RELOCATE1 && v <= TGA_V_OROPT3) { *n1 = v - TGA_V_RELOCATE1 + 1; return; }
+    static const int sw[6][2] = {{1, 1}, {1, 2}, {1, 3}, {2, 2}, {2, 3}, {3, 3}};
+    if (v >= TGA_V_SWAP11 && v <= TGA_V_CROSS33) { *n1 = sw[v - 5][0]; *n2 = sw[v - 5][1]; return; }
+    if (v >= TGA_V_IRELOCATE1 && v <= TGA_V_IRELOCATE3) { *n1 = v - TGA_V_IRELOCATE1 + 1; return; }
+    if (v >= TGA_V_ISWAP11 && v <= TGA_V_ISWAP33) { *n1 = (v - 14) / 3 + 1; *n2 = (v - 14) % 3 + 1; }
+}
+}  // namespace
+
+// ============================================================== objects
+struct tga_instance {
+    int n = 0, dtype = TGA_I32, Q = 0, device = 0;
+    bool tw = false;
+    tga_options opt{};
+    void *dC = nullptr;
+    int32_t *dDemand = nullptr;
+    TwRec *dNodeTw = nullptr;
+    std::vector<int32_t> hDemand;
+    std::vector<float> hTw;
+    int max_c_abs = 0;
+};
+
+struct tga_solution {
+    tga_instance *inst = nullptr;
+    uint64_t gen = 1;
+    std::vector<std::vector<int32_t>> routes;
+    int R = 0, N = 0, Qc = 0, Qp = 0, pitch = 0, cap = 0;
+    std::vector<int32_t> rbase, cbase;                  // host: physical / canonical base per route
+    // device arena
+    void *arena = nullptr;
+    int32_t *node = nullptr, *route = nullptr, *pos = nullptr, *rlen = nullptr, *canon = nullptr;
+    int32_t *fwdL = nullptr, *bwdL = nullptr;
+    void *enext = nullptr, *fwdD = nullptr, *bwdD = nullptr, *br1 = nullptr, *br2 = nullptr, *br3 = nullptr;
+    TwRec *fwdT = nullptr, *bwdT = nullptr, *seg2T = nullptr, *seg3T = nullptr;
+    int32_t *d_rbase = nullptr, *d_rlenR = nullptr, *d_rW = nullptr;
+    float *d_rTV = nullptr;
+    void *d_rD = nullptr;
+    void *Dp = nullptr;
+    uint64_t *keys = nullptr;
+    uint32_t *d_tiles = nullptr;
+    int n_tiles = 0;
+    CUtensorMap tmap{};
+    bool tmap_ok = false;
+    uint64_t *h_keys = nullptr;                         // pinned
+    int32_t *h_stage = nullptr;                         // pinned staging (5 * cap int32)
+    cudaStream_t stream = nullptr;
+    int shard = 0, n_shards = 1;
+    ncclComm_t comm = nullptr;
+    int sm_count = 148;
+    uint64_t eval_gen = 0;
+    uint32_t eval_mask = 0;
+};
+
+// ============================================================== helpers
+static bool is_intra_variant(int v) { return v == TGA_V_2OPT || v >= TGA_V_IRELOCATE1; }
+
+static int32_t set_device(const tga_instance *inst) {
+    TGA_CUDA(cudaSetDevice(inst->device));
+    return TGA_OK;
+}
+
+// Build the physical layout: route r occupies slots rbase[r] .. rbase[r]+L+1
+// (start depot, customers, end depot).  Canonical id of (r, p), p <= L, is
+// cbase[r] + p (SURVEY §8(c) "canonical slot"); end depots and padding have
+// canonical id -1.
+static void compute_bases(tga_solution *s) {
+    s->rbase.resize(s->R + 1);
+    s->cbase.resize(s->R + 1);
+    int pb = 0, cb = 0;
+    for (int r = 0; r < s->R; ++r) {
+        s->rbase[r] = pb;
+        s->cbase[r] = cb;
+        const int L = static_cast<int>(s->routes[r].size());
+        pb += L + 2;
+        cb += L + 1;
+    }
+    s->rbase[s->R] = pb;
+    s->cbase[s->R] = cb;
+}
+
+// Fill the 5 layout arrays (node, route, pos, rlen, canon) for routes r_lo..r_hi
+// into the pinned staging buffer, at offsets relative to slot rbase[r_lo].
+static void stage_layout(tga_solution *s, int r_lo, int r_hi, int *span_lo, int *span_n) {
+    const int lo = s->rbase[r_lo], hi = s->rbase[r_hi + 1];
+    const int n = hi - lo;
+    int32_t *nd = s->h_stage, *rt = nd + s->cap, *ps = rt + s->cap, *rl = ps + s->cap, *cn = rl + s->cap;
+    for (int r = r_lo; r <= r_hi; ++r) {
+        const int L = static_cast<int>(s->routes[r].size());
+        for (int p = 0; p <= L + 1; ++p) {
+            const int i = s->rbase[r] + p - lo;
+            nd[i] = (p == 0 || p == L + 1) ? 0 : s->routes[r][p - 1];
+            rt[i] = r;
+            ps[i] = p;
+            rl[i] = L;
+            cn[i] = (p <= L) ? s->cbase[r] + p : -1;
+        }
+    }
+    *span_lo = lo;
+    *span_n = n;
+}
+
+static int32_t upload_layout(tga_solution *s, int r_lo, int r_hi) {
+    int lo, n;
+    stage_layout(s, r_lo, r_hi, &lo, &n);
+    int32_t *dst[5] = {s->node, s->route, s->pos, s->rlen, s->canon};
+    for (int k = 0; k < 5; ++k)
+        TGA_CUDA(cudaMemcpyAsync(dst[k] + lo, s->h_stage + static_cast<size_t>(k) * s->cap, sizeof(int32_t) * n,
+                                 cudaMemcpyHostToDevice, s->stream));
+    std::vector<int32_t> rl(s->R);
+    for (int r = 0; r < s->R; ++r) rl[r] = static_cast<int32_t>(s->routes[r].size());
+    // per-route arrays are tiny: upload whole (synchronous copies from pageable memory)
+    TGA_CUDA(cudaMemcpyAsync(s->d_rbase, s->rbase.data(), sizeof(int32_t) * s->R, cudaMemcpyHostToDevice, s->stream));
+    TGA_CUDA(cudaMemcpyAsync(s->d_rlenR, rl.data(), sizeof(int32_t) * s->R, cudaMemcpyHostToDevice, s->stream));
+    TGA_CUDA(cudaStreamSynchronize(s->stream));  // pageable sources must outlive the copies
+    return TGA_OK;
+}
+
+template <class DT>
+static ScanArgs<DT> scan_args(tga_solution *s) {
+    ScanArgs<DT> a;
+    a.n_nodes = s->inst->n;
+    a.C = static_cast<const DT *>(s->inst->dC);
+    a.demand = s->inst->dDemand;
+    a.node_tw = s->inst->dNodeTw;
+    a.node = s->node;
+    a.rbase = s->d_rbase;
+    a.rlenR = s->d_rlenR;
+    a.fwdL = s->fwdL;
+    a.bwdL = s->bwdL;
+    a.enext = static_cast<DT *>(s->enext);
+    a.fwdD = static_cast<DT *>(s->fwdD);
+    a.bwdD = static_cast<DT *>(s->bwdD);
+    a.bridge1 = static_cast<DT *>(s->br1);
+    a.bridge2 = static_cast<DT *>(s->br2);
+    a.bridge3 = static_cast<DT *>(s->br3);
+    a.fwdT = s->fwdT;
+    a.bwdT = s->bwdT;
+    a.seg2T = s->seg2T;
+    a.seg3T = s->seg3T;
+    a.rW = s->d_rW;
+    a.rTV = s->d_rTV;
+    a.rD = static_cast<DT *>(s->d_rD);
+    return a;
+}
+
+template <class DT>
+static SolView<DT> sol_view(const tga_solution *s) {
+    SolView<DT> v;
+    v.node = s->node;
+    v.route = s->route;
+    v.pos = s->pos;
+    v.rlen = s->rlen;
+    v.canon = s->canon;
+    v.fwdL = s->fwdL;
+    v.bwdL = s->bwdL;
+    v.enext = static_cast<const DT *>(s->enext);
+    v.bridge1 = static_cast<const DT *>(s->br1);
+    v.bridge2 = static_cast<const DT *>(s->br2);
+    v.bridge3 = static_cast<const DT *>(s->br3);
+    v.fwdT = s->fwdT;
+    v.bwdT = s->bwdT;
+    v.seg2T = s->seg2T;
+    v.seg3T = s->seg3T;
+    v.node_tw = s->inst->dNodeTw;
+    v.rW = s->d_rW;
+    v.rTV = s->d_rTV;
+    v.Dp = static_cast<const DT *>(s->Dp);
+    v.pitch = s->pitch;
+    v.Qp = s->Qp;
+    v.Qc = static_cast<uint32_t>(s->Qc);
+    return v;
+}
+
+static int32_t refresh(tga_solution *s, int r_lo, int r_hi, bool full) {
+    const tga_instance *I = s->inst;
+    const int lo = full ? 0 : s->rbase[r_lo];
+    const int hi = full ? s->pitch : s->rbase[r_hi + 1];
+    cudaError_t e;
+    if (I->dtype == TGA_I32) {
+        e = launch_dp<int32_t>(static_cast<int32_t *>(s->Dp), s->pitch, s->node, static_cast<const int32_t *>(I->dC),
+                               I->n, s->Qp, lo, hi, full, s->stream);
+        if (e == cudaSuccess) e = launch_scan<int32_t>(scan_args<int32_t>(s), I->tw, r_lo, r_hi + 1, s->stream);
+    } else {
+        e = launch_dp<float>(static_cast<float *>(s->Dp), s->pitch, s->node, static_cast<const float *>(I->dC), I->n,
+                             s->Qp, lo, hi, full, s->stream);
+        if (e == cudaSuccess) e = launch_scan<float>(scan_args<float>(s), I->tw, r_lo, r_hi + 1, s->stream);
+    }
+    if (e != cudaSuccess) return fail(TGA_ERR_CUDA, std::string("refresh: ") + cudaGetErrorString(e));
+    return TGA_OK;
+}
+
+static void build_tiles(tga_solution *s) {
+    s->d_tiles = s->d_tiles;  // allocated in the arena
+    std::vector<uint32_t> t;
+    const int nI = s->pitch / kTileU, nJ = s->pitch / kTileV;
+    for (int I = 0; I < nI; ++I) {
+        if (I * kTileU >= s->Qp) break;
+        for (int J = 0; J < nJ; ++J) {
+            if (J * kTileV >= s->Qp) break;
+            if (I * kTileU < J * kTileV + kTileV - 1) t.push_back((static_cast<uint32_t>(I) << 16) | J);
+        }
+    }
+    s->n_tiles = static_cast<int>(t.size());
+    cudaMemcpy(s->d_tiles, t.data(), sizeof(uint32_t) * t.size(), cudaMemcpyHostToDevice);
+}
+
+static void free_solution(tga_solution *s) {
+    if (!s) return;
+    if (s->inst) cudaSetDevice(s->inst->device);
+    if (s->comm && g_nccl.commDestroy) g_nccl.commDestroy(s->comm);
+    if (s->arena) cudaFree(s->arena);
+    if (s->Dp) cudaFree(s->Dp);
+    if (s->h_keys) cudaFreeHost(s->h_keys);
+    if (s->h_stage) cudaFreeHost(s->h_stage);
+    if (s->stream) cudaStreamDestroy(s->stream);
+    delete s;
+}
+
+// ============================================================== ABI: instance
+extern "C" int32_t tga_instance_create(int32_t n, const void *dist, int32_t dtype, const void *time,
+                                       const int32_t *demand, const float *tw, int32_t capacity,
+                                       const tga_options *opt, tga_instance **out) {
+    if (!out) return fail(TGA_ERR_INVALID_ARGUMENT, "out is NULL");
+    *out = nullptr;
+    if (n < 2 || !dist || !demand) return fail(TGA_ERR_INVALID_ARGUMENT, "n_nodes < 2 or NULL dist/demand");
+    if (n > 65535) return fail(TGA_ERR_INVALID_ARGUMENT, "n_nodes > 65535 (flat index is 32-bit)");
+    if (dtype != TGA_I32 && dtype != TGA_F32) return fail(TGA_ERR_INVALID_ARGUMENT, "dist_dtype");
+    if (time) return fail(TGA_ERR_UNSUPPORTED, "separate travel-time matrix (T != C) not supported");
+    if (capacity <= 0) return fail(TGA_ERR_INVALID_ARGUMENT, "capacity <= 0");
+    if (demand[0] != 0) return fail(TGA_ERR_INVALID_ARGUMENT, "depot demand must be 0");
+    for (int i = 0; i < n; ++i)
+        if (demand[i] < 0) return fail(TGA_ERR_INVALID_ARGUMENT, "negative demand");
+    // matrix checks: zero diagonal, non-negative, symmetric (inter-route kernels)
+    int max_abs = 0;
+    for (int i = 0; i < n; ++i) {
+        for (int j = 0; j < n; ++j) {
+            double a, b;
+            if (dtype == TGA_I32) {
+                a = static_cast<const int32_t *>(dist)[static_cast<size_t>(i) * n + j];
+                b = static_cast<const int32_t *>(dist)[static_cast<size_t>(j) * n + i];
+            } else {
+                a = static_cast<const float *>(dist)[static_cast<size_t>(i) * n + j];
+                b = static_cast<const float *>(dist)[static_cast<size_t>(j) * n + i];
+            }
+            if (!(a >= 0) || (i == j && a != 0)) return fail(TGA_ERR_INVALID_ARGUMENT, "negative distance or non-zero diagonal");
+            if (a != b) return fail(TGA_ERR_UNSUPPORTED, "asymmetric distance matrix");
+            max_abs = std::max(max_abs, static_cast<int>(std::min(a, 2.0e9)));
+        }
+    }
+    if (tw) {
+        for (int i = 0; i < n; ++i) {
+            const float e = tw[3 * i], l = tw[3 * i + 1], s = tw[3 * i + 2];
+            if (!(e <= l) || !(s >= 0)) return fail(TGA_ERR_INVALID_ARGUMENT, "time window e > l or s < 0");
+        }
+    }
+    auto *I = new (std::nothrow) tga_instance();
+    if (!I) return fail(TGA_ERR_OOM, "host allocation");
+    I->n = n;
+    I->dtype = dtype;
+    I->Q = capacity;
+    I->tw = tw != nullptr;
+    I->max_c_abs = max_abs;
+    if (opt) I->opt = *opt;
+    else { I->opt.score_mode = TGA_SCORE_FEASIBLE; I->opt.w_load = 10; I->opt.w_tw = 10; I->opt.device = -1; }
+    if (I->opt.device < 0) cudaGetDevice(&I->device);
+    else I->device = I->opt.device;
+    I->hDemand.assign(demand, demand + n);
+    std::vector<TwRec> ntw(n);
+    if (tw) {
+        I->hTw.assign(tw, tw + 3 * static_cast<size_t>(n));
+        for (int i = 0; i < n; ++i) ntw[i] = tw_single(tw[3 * i], tw[3 * i + 1], tw[3 * i + 2]);
+    } else {
+        for (int i = 0; i < n; ++i) ntw[i] = tw_single(0.f, 3.0e38f, 0.f);
+    }
+    auto cleanup = [&](int32_t code) {
+        if (I->dC) cudaFree(I->dC);
+        if (I->dDemand) cudaFree(I->dDemand);
+        if (I->dNodeTw) cudaFree(I->dNodeTw);
+        delete I;
+        return code;
+    };
+    if (cudaSetDevice(I->device) != cudaSuccess) return cleanup(fail(TGA_ERR_CUDA, "cudaSetDevice"));
+    const size_t nn = static_cast<size_t>(n) * n;
+    cudaError_t e = cudaMalloc(&I->dC, nn * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&I->dDemand, sizeof(int32_t) * n);
+    if (e == cudaSuccess) e = cudaMalloc(&I->dNodeTw, sizeof(TwRec) * n);
+    if (e == cudaSuccess) e = cudaMemcpy(I->dC, dist, nn * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(I->dDemand, demand, sizeof(int32_t) * n, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(I->dNodeTw, ntw.data(), sizeof(TwRec) * n, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess)
+        return cleanup(fail(e == cudaErrorMemoryAllocation ? TGA_ERR_OOM : TGA_ERR_CUDA,
+                            std::string("instance upload: ") + cudaGetErrorString(e)));
+    *out = I;
+    return TGA_OK;
+}
+
+extern "C" int32_t tga_instance_destroy(tga_instance *I) {
+    if (!I) return TGA_OK;
+    cudaSetDevice(I->device);
+    cudaFree(I->dC);
+    cudaFree(I->dDemand);
+    cudaFree(I->dNodeTw);
+    delete I;
+    return TGA_OK;
+}
+
+// ============================================================== ABI: solution
+extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *ptr, const int32_t *cust,
+                                     tga_solution **out) {
+    if (!out || !I || !ptr || (R > 0 && !cust && ptr[R] > 0))
+        return fail(TGA_ERR_INVALID_ARGUMENT, "NULL argument");
+    *out = nullptr;
+    if (R < 1) return fail(TGA_ERR_INVALID_ARGUMENT, "n_routes < 1");
+    if (ptr[0] != 0) return fail(TGA_ERR_STRUCTURE, "route_ptr[0] != 0");
+    std::vector<char> seen(I->n, 0);
+    for (int r = 0; r < R; ++r) {
+        if (ptr[r + 1] < ptr[r]) return fail(TGA_ERR_STRUCTURE, "route_ptr not non-decreasing");
+        for (int k = ptr[r]; k < ptr[r + 1]; ++k) {
+            const int c = cust[k];
+            if (c <= 0 || c >= I->n) return fail(TGA_ERR_STRUCTURE, "customer id out of range");
+            if (seen[c]) return fail(TGA_ERR_STRUCTURE, "customer visited twice");
+            seen[c] = 1;
+        }
+    }
+    if (ptr[R] != I->n - 1) return fail(TGA_ERR_STRUCTURE, "not every customer is visited");
+    if (set_device(I) != TGA_OK) return TGA_ERR_CUDA;
+
+    auto *s = new (std::nothrow) tga_solution();
+    if (!s) return fail(TGA_ERR_OOM, "host allocation");
+    s->inst = I;
+    s->R = R;
+    s->routes.resize(R);
+    for (int r = 0; r < R; ++r) s->routes[r].assign(cust + ptr[r], cust + ptr[r + 1]);
+    s->N = ptr[R];
+    s->Qc = s->N + R;
+    s->Qp = s->N + 2 * R;
+    s->pitch = static_cast<int>(align_up(static_cast<size_t>(s->Qp) + 4, kPitchAlign));
+    s->cap = s->pitch + 2 * kGuard;
+    if (static_cast<uint64_t>(s->Qc) * s->Qc > 0xFFFFFFFFull) {
+        delete s;
+        return fail(TGA_ERR_INVALID_ARGUMENT, "Q^2 exceeds the 32-bit flat index");
+    }
+    compute_bases(s);
+    int32_t rc = TGA_OK;
+    auto bail = [&](int32_t code) { free_solution(s); return code; };
+    {
+        cudaDeviceProp prop;
+        if (cudaGetDeviceProperties(&prop, I->device) == cudaSuccess) s->sm_count = prop.multiProcessorCount;
+    }
+    if (cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking) != cudaSuccess)
+        return bail(fail(TGA_ERR_CUDA, "stream create"));
+    // ---- device arena: slot arrays (with guards), per-route arrays, keys, tiles
+    const size_t cap = s->cap, Rr = static_cast<size_t>(R) + 1;
+    struct Item { void **p; size_t bytes; };
+    const size_t tiles_max = static_cast<size_t>(s->pitch / kTileU) * (s->pitch / kTileV) + 1;
+    void *v_node, *v_route, *v_pos, *v_rlen, *v_canon, *v_fwdL, *v_bwdL, *v_en, *v_fD, *v_bD, *v_b1, *v_b2, *v_b3;
+    void *v_fT, *v_bT, *v_s2, *v_s3, *v_rbase, *v_rlenR, *v_rW, *v_rTV, *v_rD, *v_keys, *v_tiles;
+    Item items[] = {
+        {&v_node, cap * 4}, {&v_route, cap * 4}, {&v_pos, cap * 4}, {&v_rlen, cap * 4}, {&v_canon, cap * 4},
+        {&v_fwdL, cap * 4}, {&v_bwdL, cap * 4}, {&v_en, cap * 4}, {&v_fD, cap * 4}, {&v_bD, cap * 4},
+        {&v_b1, cap * 4}, {&v_b2, cap * 4}, {&v_b3, cap * 4},
+        {&v_fT, cap * 16}, {&v_bT, cap * 16}, {&v_s2, cap * 16}, {&v_s3, cap * 16},
+        {&v_rbase, Rr * 4}, {&v_rlenR, Rr * 4}, {&v_rW, Rr * 4}, {&v_rTV, Rr * 4}, {&v_rD, Rr * 4},
+        {&v_keys, TGA_N_VARIANTS * 8}, {&v_tiles, tiles_max * 4}};
+    size_t total = 0;
+    for (auto &it : items) total += align_up(it.bytes, 256);
+    if (cudaMalloc(&s->arena, total) != cudaSuccess) return bail(fail(TGA_ERR_OOM, "device arena"));
+    {
+        size_t off = 0;
+        for (auto &it : items) {
+            *it.p = static_cast<char *>(s->arena) + off;
+            off += align_up(it.bytes, 256);
+        }
+    }
+    // guards: ints -> -1 (route/pos/rlen/canon invalid), node -> 0 (a valid node id)
+    if (cudaMemset(s->arena, 0xFF, total) != cudaSuccess) return bail(fail(TGA_ERR_CUDA, "memset"));
+    if (cudaMemset(v_node, 0, cap * 4) != cudaSuccess) return bail(fail(TGA_ERR_CUDA, "memset"));
+    auto g32 = [&](void *p) { return static_cast<int32_t *>(p) + kGuard; };
+    auto g128 = [&](void *p) { return static_cast<TwRec *>(p) + kGuard; };
+    s->node = g32(v_node); s->route = g32(v_route); s->pos = g32(v_pos); s->rlen = g32(v_rlen);
+    s->canon = g32(v_canon); s->fwdL = g32(v_fwdL); s->bwdL = g32(v_bwdL);
+    s->enext = g32(v_en); s->fwdD = g32(v_fD); s->bwdD = g32(v_bD);
+    s->br1 = g32(v_b1); s->br2 = g32(v_b2); s->br3 = g32(v_b3);
+    s->fwdT = g128(v_fT); s->bwdT = g128(v_bT); s->seg2T = g128(v_s2); s->seg3T = g128(v_s3);
+    s->d_rbase = static_cast<int32_t *>(v_rbase); s->d_rlenR = static_cast<int32_t *>(v_rlenR);
+    s->d_rW = static_cast<int32_t *>(v_rW); s->d_rTV = static_cast<float *>(v_rTV); s->d_rD = v_rD;
+    s->keys = static_cast<uint64_t *>(v_keys);
+    s->d_tiles = static_cast<uint32_t *>(v_tiles);
+    // numeric per-slot arrays start at 0 (guards are only read by masked-out lanes)
+    for (void *p : {v_fwdL, v_bwdL, v_en, v_fD, v_bD, v_b1, v_b2, v_b3})
+        if (cudaMemset(p, 0, cap * 4) != cudaSuccess) return bail(fail(TGA_ERR_CUDA, "memset"));
+    for (void *p : {v_fT, v_bT, v_s2, v_s3})
+        if (cudaMemset(p, 0, cap * 16) != cudaSuccess) return bail(fail(TGA_ERR_CUDA, "memset"));
+    // ---- position-ordered distance matrix
+    const size_t dp_bytes = static_cast<size_t>(s->pitch) * s->pitch * 4;
+    if (cudaMalloc(&s->Dp, dp_bytes) != cudaSuccess) return bail(fail(TGA_ERR_OOM, "Dp allocation"));
+    if (cudaMallocHost(&s->h_keys, TGA_N_VARIANTS * 8) != cudaSuccess ||
+        cudaMallocHost(&s->h_stage, sizeof(int32_t) * 5 * cap) != cudaSuccess)
+        return bail(fail(TGA_ERR_OOM, "pinned host allocation"));
+    // ---- layout upload, Dp build, scan
+    if ((rc = upload_layout(s, 0, R - 1)) != TGA_OK) return bail(rc);
+    if ((rc = refresh(s, 0, R - 1, true)) != TGA_OK) return bail(rc);
+    build_tiles(s);
+    // ---- TMA descriptor over Dp: dims {pitch cols, pitch rows}, box {kBoxW, kBoxH}
+    if (auto enc = get_encode()) {
+        cuuint64_t gdim[2] = {static_cast<cuuint64_t>(s->pitch), static_cast<cuuint64_t>(s->pitch)};
+        cuuint64_t gstride[1] = {static_cast<cuuint64_t>(s->pitch) * 4};
+        cuuint32_t box[2] = {static_cast<cuuint32_t>(kBoxW), static_cast<cuuint32_t>(kBoxH)};
+        cuuint32_t estr[2] = {1, 1};
+        CUresult cr = enc(&s->tmap, I->dtype == TGA_I32 ? CU_TENSOR_MAP_DATA_TYPE_INT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                          2, s->Dp, gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        s->tmap_ok = (cr == CUDA_SUCCESS);
+    }
+    if (!s->tmap_ok) return bail(fail(TGA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable or failed"));
+    if (cudaStreamSynchronize(s->stream) != cudaSuccess)
+        return bail(fail(TGA_ERR_CUDA, std::string("load: ") + cudaGetErrorString(cudaGetLastError())));
+    *out = s;
+    return TGA_OK;
+}
+
+extern "C" int32_t tga_solution_destroy(tga_solution *s) {
+    free_solution(s);
+    return TGA_OK;
+}
+
+extern "C" int32_t tga_solution_set_shard(tga_solution *s, int32_t shard, int32_t n_shards) {
+    if (!s || n_shards < 1 || shard < 0 || shard >= n_shards) return fail(TGA_ERR_INVALID_ARGUMENT, "shard plan");
+    s->shard = shard;
+    s->n_shards = n_shards;
+    return TGA_OK;
+}
+
+// ============================================================== ABI: evaluation
+extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
+    if (!s) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL solution");
+    const tga_instance *I = s->inst;
+    mask &= TGA_OP_ALL;
+    if ((mask & TGA_OP_2OPT) && I->tw)
+        return fail(TGA_ERR_UNSUPPORTED, "2-opt is only defined without time windows (P:148)");
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s->stream;
+    TGA_CUDA(cudaMemsetAsync(s->keys, 0xFF, TGA_N_VARIANTS * 8, st));
+    ScoreParams sp{I->Q, I->opt.score_mode, I->opt.w_load, I->opt.w_tw};
+    // row shard of the tile list and of the intra slot range
+    const int t_lo = static_cast<int>(static_cast<int64_t>(s->n_tiles) * s->shard / s->n_shards);
+    const int t_hi = static_cast<int>(static_cast<int64_t>(s->n_tiles) * (s->shard + 1) / s->n_shards);
+    const int x_lo = static_cast<int>(static_cast<int64_t>(s->Qp) * s->shard / s->n_shards);
+    const int x_hi = static_cast<int>(static_cast<int64_t>(s->Qp) * (s->shard + 1) / s->n_shards);
+    const int grid = std::max(1, std::min(t_hi - t_lo, s->sm_count * 4));
+    cudaError_t e;
+    if (I->dtype == TGA_I32) {
+        const auto v = sol_view<int32_t>(s);
+        e = launch_inter<int32_t>(mask, I->tw, v, s->tmap, s->d_tiles, t_lo, t_hi, sp, s->keys, grid, st);
+        if (e == cudaSuccess) e = launch_intra<int32_t>(mask, I->tw, v, sp, x_lo, x_hi, s->keys, st);
+    } else {
+        const auto v = sol_view<float>(s);
+        e = launch_inter<float>(mask, I->tw, v, s->tmap, s->d_tiles, t_lo, t_hi, sp, s->keys, grid, st);
+        if (e == cudaSuccess) e = launch_intra<float>(mask, I->tw, v, sp, x_lo, x_hi, s->keys, st);
+    }
+    if (e != cudaSuccess) return fail(TGA_ERR_CUDA, std::string("eval launch: ") + cudaGetErrorString(e));
+    if (s->comm) {
+        const ncclResult_t r = g_nccl.allReduce(s->keys, s->keys, TGA_N_VARIANTS, kNcclUint64, kNcclMin, s->comm, st);
+        if (r != 0) return fail(TGA_ERR_NCCL, std::string("ncclAllReduce: ") + (g_nccl.errStr ? g_nccl.errStr(r) : "?"));
+    }
+    if (st != s->stream) {
+        // later synchronous calls use the solution's stream: order them after this eval
+        cudaEvent_t ev;
+        TGA_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        TGA_CUDA(cudaEventRecord(ev, st));
+        TGA_CUDA(cudaStreamWaitEvent(s->stream, ev, 0));
+        cudaEventDestroy(ev);
+    }
+    s->eval_gen = s->gen;
+    s->eval_mask = mask;
+    return TGA_OK;
+}
+
+extern "C" int32_t tga_solution_keys(tga_solution *s, uint64_t *keys) {
+    if (!s || !keys) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL argument");
+    TGA_CUDA(cudaMemcpyAsync(s->h_keys, s->keys, TGA_N_VARIANTS * 8, cudaMemcpyDeviceToHost, s->stream));
+    TGA_CUDA(cudaStreamSynchronize(s->stream));
+    std::memcpy(keys, s->h_keys, TGA_N_VARIANTS * 8);
+    return TGA_OK;
+}
+
+static double decode_score(uint32_t ord, bool integer, int64_t *as_int) {
+    if (integer) {
+        const int32_t v = static_cast<int32_t>(ord ^ 0x80000000u);
+        *as_int = v;
+        return static_cast<double>(v);
+    }
+    const uint32_t u = (ord & 0x80000000u) ? (ord ^ 0x80000000u) : ~ord;
+    float f;
+    std::memcpy(&f, &u, 4);
+    *as_int = static_cast<int64_t>(std::llround(static_cast<double>(f)));
+    return static_cast<double>(f);
+}
+
+static void canon_to_rp(const tga_solution *s, int c, int *r, int *p) {
+    // largest route with cbase <= c
+    const auto it = std::upper_bound(s->cbase.begin(), s->cbase.begin() + s->R, c);
+    *r = static_cast<int>(it - s->cbase.begin()) - 1;
+    *p = c - s->cbase[*r];
+}
+
+extern "C" int32_t tga_best_move(tga_solution *s, uint32_t mask, tga_move *out) {
+    if (!s || !out) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (s->eval_gen != s->gen) return fail(TGA_ERR_STALE, "no evaluation for the current generation");
+    TGA_CUDA(cudaMemcpyAsync(s->h_keys, s->keys, TGA_N_VARIANTS * 8, cudaMemcpyDeviceToHost, s->stream));
+    TGA_CUDA(cudaStreamSynchronize(s->stream));
+    mask &= s->eval_mask;
+    int bv = -1;
+    uint64_t bk = ~0ull;
+    for (int v = 0; v < TGA_N_VARIANTS; ++v) {
+        if (!(mask & (1u << v))) continue;
+        const uint64_t k = s->h_keys[v];
+        if (k == ~0ull) continue;
+        // lowest (score, variant rank, flat index); variants visited in rank order
+        if (bv < 0 || (k >> 32) < (bk >> 32)) { bv = v; bk = k; }
+    }
+    std::memset(out, 0, sizeof(*out));
+    out->key = ~0ull;
+    out->generation = s->gen;
+    out->variant = -1;
+    if (bv < 0) return TGA_NO_IMPROVING_MOVE;
+    const uint32_t idx = static_cast<uint32_t>(bk & 0xFFFFFFFFu);
+    const int cu = static_cast<int>(idx / static_cast<uint32_t>(s->Qc));
+    const int cv = static_cast<int>(idx % static_cast<uint32_t>(s->Qc));
+    out->variant = bv;
+    variant_lengths(bv, &out->n1, &out->n2);
+    out->u = cu;
+    out->v = cv;
+    canon_to_rp(s, cu, &out->route_a, &out->pos_a);
+    canon_to_rp(s, cv, &out->route_b, &out->pos_b);
+    out->delta_f = decode_score(static_cast<uint32_t>(bk >> 32), s->inst->dtype == TGA_I32, &out->delta_i);
+    out->feasible = 1;
+    if (s->inst->opt.score_mode == TGA_SCORE_PENALISED) out->feasible = -1;  // not tracked in penalised mode
+    out->key = bk;
+    return out->delta_f < 0 ? TGA_OK : TGA_NO_IMPROVING_MOVE;
+}
+
+// ============================================================== ABI: update
+// Splice the host route lists (Fig. `operators` P:107-146) -- the update of S
+// (Alg. A2 line 7) -- then synchronise the device state of the changed
+// span only.
+static bool splice(std::vector<std::vector<int32_t>> &routes, const tga_move *m) {
+    const int v = m->variant, ra = m->route_a, rb = m->route_b, pa = m->pos_a, pb = m->pos_b;
+    const int R = static_cast<int>(routes.size());
+    if (ra < 0 || ra >= R || rb < 0 || rb >= R) return false;
+    std::vector<int32_t> &a = routes[ra];
+    std::vector<int32_t> &b = routes[rb];
+    const int La = static_cast<int>(a.size()), Lb = static_cast<int>(b.size());
+    int n1, n2;
+    variant_lengths(v, &n1, &n2);
+    typedef std::vector<int32_t> V;
+    auto sl = [](const V &x, int i, int j) { return V(x.begin() + i, x.begin() + j); };  // [i, j)
+    auto cat = [](std::initializer_list<V> parts) {
+        V r;
+        for (auto &p : parts) r.insert(r.end(), p.begin(), p.end());
+        return r;
+    };
+    if (v == TGA_V_2OPT_STAR) {
+        if (ra == rb || pa < 0 || pa > La || pb < 0 || pb > Lb) return false;
+        V na = cat({sl(a, 0, pa), sl(b, pb, Lb)}), nb = cat({sl(b, 0, pb), sl(a, pa, La)});
+        a.swap(na); b.swap(nb);
+    } else if (v >= TGA_V_RELOCATE1 && v <= TGA_V_OROPT3) {
+        if (ra == rb || pa < 1 || pa + n1 - 1 > La || pb < 0 || pb > Lb) return false;
+        V seg = sl(a, pa - 1, pa - 1 + n1);
+        V na = cat({sl(a, 0, pa - 1), sl(a, pa - 1 + n1, La)}), nb = cat({sl(b, 0, pb), seg, sl(b, pb, Lb)});
+        a.swap(na); b.swap(nb);
+    } else if (v >= TGA_V_SWAP11 && v <= TGA_V_CROSS33) {
+        if (ra == rb || pa < 1 || pa + n1 - 1 > La || pb < 1 || pb + n2 - 1 > Lb) return false;
+        V sa = sl(a, pa - 1, pa - 1 + n1), sb = sl(b, pb - 1, pb - 1 + n2);
+        V na = cat({sl(a, 0, pa - 1), sb, sl(a, pa - 1 + n1, La)});
+        V nb = cat({sl(b, 0, pb - 1), sa, sl(b, pb - 1 + n2, Lb)});
+        a.swap(na); b.swap(nb);
+    } else if (v == TGA_V_2OPT) {
+        if (ra != rb || pa < 1 || pb <= pa || pb > La) return false;
+        std::reverse(a.begin() + (pa - 1), a.begin() + pb);
+    } else if (v >= TGA_V_IRELOCATE1 && v <= TGA_V_IRELOCATE3) {
+        if (ra != rb || pa < 1 || pa + n1 - 1 > La || pb < 0 || pb > La) return false;
+        if (pb >= pa - 1 && pb <= pa + n1 - 1) return false;
+        V seg = sl(a, pa - 1, pa - 1 + n1), na;
+        if (pb > pa) na = cat({sl(a, 0, pa - 1), sl(a, pa - 1 + n1, pb), seg, sl(a, pb, La)});
+        else na = cat({sl(a, 0, pb), seg, sl(a, pb, pa - 1), sl(a, pa - 1 + n1, La)});
+        a.swap(na);
+    } else if (v >= TGA_V_ISWAP11 && v <= TGA_V_ISWAP33) {
+        if (ra != rb || pa < 1 || pa + n1 > pb || pb + n2 - 1 > La) return false;
+        V na = cat({sl(a, 0, pa - 1), sl(a, pb - 1, pb - 1 + n2), sl(a, pa - 1 + n1, pb - 1), sl(a, pa - 1, pa - 1 + n1),
+                    sl(a, pb - 1 + n2, La)});
+        a.swap(na);
+    } else {
+        return false;
+    }
+    return true;
+}
+
+extern "C" int32_t tga_apply_move(tga_solution *s, const tga_move *m) {
+    if (!s || !m) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (m->generation != s->gen) return fail(TGA_ERR_STALE, "move generation does not match the solution");
+    if (m->variant < 0 || m->variant >= TGA_N_VARIANTS) return fail(TGA_ERR_INVALID_ARGUMENT, "variant");
+    if (set_device(s->inst) != TGA_OK) return TGA_ERR_CUDA;
+    TGA_CUDA(cudaStreamSynchronize(s->stream));  // the staging buffer / route arrays may still be in use
+    if (!splice(s->routes, m)) return fail(TGA_ERR_INVALID_ARGUMENT, "move positions out of range for its variant");
+    compute_bases(s);
+    const int r_lo = std::min(m->route_a, m->route_b), r_hi = std::max(m->route_a, m->route_b);
+    int32_t rc;
+    if ((rc = upload_layout(s, r_lo, r_hi)) != TGA_OK) return rc;
+    if ((rc = refresh(s, r_lo, r_hi, false)) != TGA_OK) return rc;
+    ++s->gen;
+    return TGA_OK;
+}
+
+// ============================================================== ABI: queries
+extern "C" int32_t tga_solution_counts(const tga_solution *s, uint64_t *c) {
+    if (!s || !c) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL argument");
+    std::memset(c, 0, sizeof(uint64_t) * TGA_N_VARIANTS);
+    const int R = s->R;
+    std::vector<int64_t> L(R);
+    for (int r = 0; r < R; ++r) L[r] = static_cast<int64_t>(s->routes[r].size());
+    auto pos = [](int64_t x) { return x > 0 ? x : 0; };
+    int64_t sumL1 = 0;
+    for (int r = 0; r < R; ++r) sumL1 += L[r] + 1;
+    // 2-opt*: sum_{a<b} (La+1)(Lb+1)
+    {
+        int64_t acc = 0, pre = 0;
+        for (int r = 0; r < R; ++r) { acc += pre * (L[r] + 1); pre += L[r] + 1; }
+        c[TGA_V_2OPT_STAR] = acc;
+    }
+    for (int N = 1; N <= 3; ++N) {  // relocate: sum_a max(La-N+1,0) * (sum_{b != a} (Lb+1))
+        int64_t acc = 0;
+        for (int r = 0; r < R; ++r) acc += pos(L[r] - N + 1) * (sumL1 - (L[r] + 1));
+        c[TGA_V_RELOCATE1 + N - 1] = acc;
+    }
+    static const int sw[6][2] = {{1, 1}, {1, 2}, {1, 3}, {2, 2}, {2, 3}, {3, 3}};
+    for (int k = 0; k < 6; ++k) {
+        const int n1 = sw[k][0], n2 = sw[k][1];
+        int64_t s1 = 0, s2 = 0, diag = 0;
+        for (int r = 0; r < R; ++r) { s1 += pos(L[r] - n1 + 1); s2 += pos(L[r] - n2 + 1); diag += pos(L[r] - n1 + 1) * pos(L[r] - n2 + 1); }
+        const int64_t ordered = s1 * s2 - diag;
+        c[TGA_V_SWAP11 + k] = (n1 == n2) ? ordered / 2 : ordered;
+    }
+    for (int r = 0; r < R; ++r) {
+        c[TGA_V_2OPT] += L[r] * (L[r] - 1) / 2;
+        for (int N = 1; N <= 3; ++N) c[TGA_V_IRELOCATE1 + N - 1] += pos(L[r] - N + 1) * pos(L[r] - N);
+        for (int a = 1; a <= 3; ++a)
+            for (int b = 1; b <= 3; ++b) {
+                const int64_t M = L[r] - a - b + 1;
+                c[TGA_V_ISWAP11 + 3 * (a - 1) + (b - 1)] += M >= 1 ? M * (M + 1) / 2 : 0;
+            }
+    }
+    return TGA_OK;
+}
+
+extern "C" int32_t tga_solution_info(const tga_solution *s, int32_t *R, int32_t *N, int32_t *Q, uint64_t *gen) {
+    if (!s) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL solution");
+    if (R) *R = s->R;
+    if (N) *N = s->N;
+    if (Q) *Q = s->Qc;
+    if (gen) *gen = s->gen;
+    return TGA_OK;
+}
+
+extern "C" int32_t tga_solution_routes(const tga_solution *s, int32_t *ptr, int32_t *cust) {
+    if (!s || !ptr || !cust) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL argument");
+    int q = 0;
+    ptr[0] = 0;
+    for (int r = 0; r < s->R; ++r) {
+        for (int32_t c : s->routes[r]) cust[q++] = c;
+        ptr[r + 1] = q;
+    }
+    return TGA_OK;
+}
+
+extern "C" int32_t tga_solution_cost(tga_solution *s, int64_t *dist_i, double *dist_f, int64_t *lex, double *tex) {
+    if (!s) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL solution");
+    TGA_CUDA(cudaStreamSynchronize(s->stream));
+    std::vector<int32_t> W(s->R), Draw(s->R);
+    std::vector<float> TV(s->R);
+    TGA_CUDA(cudaMemcpy(W.data(), s->d_rW, 4 * s->R, cudaMemcpyDeviceToHost));
+    TGA_CUDA(cudaMemcpy(Draw.data(), s->d_rD, 4 * s->R, cudaMemcpyDeviceToHost));
+    TGA_CUDA(cudaMemcpy(TV.data(), s->d_rTV, 4 * s->R, cudaMemcpyDeviceToHost));
+    int64_t di = 0, le = 0;
+    double df = 0, te = 0;
+    for (int r = 0; r < s->R; ++r) {
+        if (s->inst->dtype == TGA_I32) { di += Draw[r]; df += Draw[r]; }
+        else { float f; std::memcpy(&f, &Draw[r], 4); df += f; di = static_cast<int64_t>(std::llround(df)); }
+        le += std::max<int64_t>(W[r] - s->inst->Q, 0);
+        if (s->inst->tw) te += TV[r];
+    }
+    if (dist_i) *dist_i = di;
+    if (dist_f) *dist_f = df;
+    if (lex) *lex = le;
+    if (tex) *tex = te;
+    return TGA_OK;
+}
+
+extern "C" int32_t tga_solution_attributes(tga_solution *s, int64_t *pre_L, int64_t *suf_L, double *pre_D,
+                                           double *suf_D, double *pre_TV, double *suf_TV, double *start) {
+    if (!s) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL solution");
+    TGA_CUDA(cudaStreamSynchronize(s->stream));
+    const int Qp = s->Qp;
+    std::vector<int32_t> fL(Qp), bL(Qp), fD(Qp), bD(Qp), nd(Qp);
+    std::vector<TwRec> fT(Qp), bT(Qp);
+    TGA_CUDA(cudaMemcpy(fL.data(), s->fwdL, 4 * Qp, cudaMemcpyDeviceToHost));
+    TGA_CUDA(cudaMemcpy(bL.data(), s->bwdL, 4 * Qp, cudaMemcpyDeviceToHost));
+    TGA_CUDA(cudaMemcpy(fD.data(), s->fwdD, 4 * Qp, cudaMemcpyDeviceToHost));
+    TGA_CUDA(cudaMemcpy(bD.data(), s->bwdD, 4 * Qp, cudaMemcpyDeviceToHost));
+    TGA_CUDA(cudaMemcpy(nd.data(), s->node, 4 * Qp, cudaMemcpyDeviceToHost));
+    TGA_CUDA(cudaMemcpy(fT.data(), s->fwdT, 16 * Qp, cudaMemcpyDeviceToHost));
+    TGA_CUDA(cudaMemcpy(bT.data(), s->bwdT, 16 * Qp, cudaMemcpyDeviceToHost));
+    auto asd = [&](int32_t raw) -> double {
+        if (s->inst->dtype == TGA_I32) return raw;
+        float f;
+        std::memcpy(&f, &raw, 4);
+        return f;
+    };
+    for (int r = 0; r < s->R; ++r) {
+        const int L = static_cast<int>(s->routes[r].size());
+        for (int p = 0; p <= L; ++p) {
+            const int x = s->rbase[r] + p, c = s->cbase[r] + p;
+            if (pre_L) pre_L[c] = fL[x];
+            if (suf_L) suf_L[c] = bL[x];
+            if (pre_D) pre_D[c] = asd(fD[x]);
+            if (suf_D) suf_D[c] = asd(bD[x]);
+            if (pre_TV) pre_TV[c] = s->inst->tw ? fT[x].w : 0.0;
+            if (suf_TV) suf_TV[c] = s->inst->tw ? bT[x].w : 0.0;
+            if (start) {
+                // service start at p from the prefix record: T_E + T_D - T_V - s
+                start[c] = s->inst->tw
+                               ? static_cast<double>(fT[x].y) + fT[x].x - fT[x].w - s->inst->hTw[3 * nd[x] + 2]
+                               : 0.0;
+            }
+        }
+    }
+    return TGA_OK;
+}
+
+// ============================================================== ABI: multi-GPU
+extern "C" int32_t tga_nccl_unique_id(void *out) {
+    if (!out) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (!g_nccl.load()) return fail(TGA_ERR_NCCL, "libnccl.so.2 not loadable");
+    ncclUniqueId id;
+    const ncclResult_t r = g_nccl.getUniqueId(&id);
+    if (r != 0) return fail(TGA_ERR_NCCL, "ncclGetUniqueId failed");
+    std::memcpy(out, &id, sizeof(id));
+    return TGA_OK;
+}
+
+extern "C" int32_t tga_comm_init(tga_solution *s, int32_t rank, int32_t world, const void *uid) {
+    if (!s || !uid || world < 1 || rank < 0 || rank >= world) return fail(TGA_ERR_INVALID_ARGUMENT, "comm args");
+    if (!g_nccl.load()) return fail(TGA_ERR_NCCL, "libnccl.so.2 not loadable");
+    if (set_device(s->inst) != TGA_OK) return TGA_ERR_CUDA;
+    ncclUniqueId id;
+    std::memcpy(&id, uid, sizeof(id));
+    ncclComm_t c = nullptr;
+    const ncclResult_t r = g_nccl.commInitRank(&c, world, id, rank);
+    if (r != 0) return fail(TGA_ERR_NCCL, std::string("ncclCommInitRank: ") + (g_nccl.errStr ? g_nccl.errStr(r) : "?"));
+    if (s->comm) g_nccl.commDestroy(s->comm);
+    s->comm = c;
+    s->shard = rank;
+    s->n_shards = world;
+    return TGA_OK;
+}
+
+// ============================================================== ABI: misc
+extern "C" const char *tga_last_error(void) { return g_err.c_str(); }
+extern "C" const char *tga_version(void) { return "tga-b200 0.1 (sm_100a)"; }
+extern "C" uint64_t tga_launch_count(void) { return tga::launch_count(); }

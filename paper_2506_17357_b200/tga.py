@@ -1,0 +1,299 @@
+"""Thin ctypes binding of libtga.so (include/tga.h) -- argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels behind the C ABI; this
+module converts numpy arrays / torch streams to pointers and status codes to
+exceptions.  There is no CPU fallback: if libtga.so is missing or a CUDA
+device is unavailable the calls fail loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtga.so")
+
+# ---------------------------------------------------------------- constants (include/tga.h)
+OK, NO_IMPROVING_MOVE = 0, 1
+ERR = {-1: "INVALID_ARGUMENT", -2: "STRUCTURE", -3: "STALE", -4: "UNSUPPORTED", -5: "CUDA",
+       -6: "NCCL", -7: "OOM"}
+I32, F32 = 0, 1
+SCORE_FEASIBLE, SCORE_PENALISED = 0, 1
+N_VARIANTS = 23
+V_2OPT, V_2OPT_STAR = 0, 1
+V_RELOCATE = {1: 2, 2: 3, 3: 4}
+V_SWAP = {(1, 1): 5, (1, 2): 6, (1, 3): 7, (2, 2): 8, (2, 3): 9, (3, 3): 10}
+V_IRELOCATE = {1: 11, 2: 12, 3: 13}
+V_ISWAP = {(a, b): 14 + 3 * (a - 1) + (b - 1) for a in (1, 2, 3) for b in (1, 2, 3)}
+VARIANT_NAMES = (["2opt", "2opt*", "relocate", "or-opt2", "or-opt3", "swap11", "cross12", "cross13",
+                  "cross22", "cross23", "cross33", "irelocate1", "irelocate2", "irelocate3"]
+                 + [f"iswap{a}{b}" for a in (1, 2, 3) for b in (1, 2, 3)])
+OP_2OPT = 1 << 0
+OP_2OPT_STAR = 1 << 1
+OP_RELOCATE = 1 << 2
+OP_OR_OPT = (1 << 3) | (1 << 4)
+OP_SWAP = 1 << 5
+OP_CROSS = 0x1F << 6
+OP_INTRA_RELOCATE = 0x7 << 11
+OP_INTRA_SWAP = 0x1FF << 14
+OP_INTER = 0x7FE
+OP_INTRA = OP_2OPT | OP_INTRA_RELOCATE | OP_INTRA_SWAP
+OP_ALL = (1 << N_VARIANTS) - 1
+OP_FUSED_NS = OP_2OPT_STAR | OP_RELOCATE | OP_SWAP
+OPERATORS = {"2opt": OP_2OPT, "2opt*": OP_2OPT_STAR, "relocate": OP_RELOCATE, "or-opt": OP_OR_OPT,
+             "swap": OP_SWAP, "cross": OP_CROSS, "intra-relocate": OP_INTRA_RELOCATE,
+             "intra-swap": OP_INTRA_SWAP}
+
+
+class TgaError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"tga error {code} ({ERR.get(code, '?')}): {msg}")
+        self.code = code
+
+
+class _Options(C.Structure):
+    _fields_ = [("score_mode", C.c_int32), ("w_load", C.c_int32), ("w_tw", C.c_int32),
+                ("device", C.c_int32), ("reserved", C.c_int32 * 12)]
+
+
+class Move(C.Structure):
+    """tga_move (include/tga.h)."""
+    _fields_ = [("variant", C.c_int32), ("n1", C.c_int32), ("n2", C.c_int32),
+                ("route_a", C.c_int32), ("pos_a", C.c_int32), ("route_b", C.c_int32),
+                ("pos_b", C.c_int32), ("u", C.c_int32), ("v", C.c_int32),
+                ("feasible", C.c_int32), ("delta_i", C.c_int64), ("delta_f", C.c_double),
+                ("key", C.c_uint64), ("generation", C.c_uint64)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+_lib = None
+_SYMBOLS = {
+    "tga_instance_create": (C.c_int32, [C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
+                                        C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
+    "tga_instance_destroy": (C.c_int32, [C.c_void_p]),
+    "tga_solution_load": (C.c_int32, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "tga_solution_destroy": (C.c_int32, [C.c_void_p]),
+    "tga_eval": (C.c_int32, [C.c_void_p, C.c_uint32, C.c_void_p]),
+    "tga_best_move": (C.c_int32, [C.c_void_p, C.c_uint32, C.c_void_p]),
+    "tga_apply_move": (C.c_int32, [C.c_void_p, C.c_void_p]),
+    "tga_solution_keys": (C.c_int32, [C.c_void_p, C.c_void_p]),
+    "tga_solution_counts": (C.c_int32, [C.c_void_p, C.c_void_p]),
+    "tga_solution_cost": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "tga_solution_routes": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "tga_solution_info": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "tga_solution_attributes": (C.c_int32, [C.c_void_p] + [C.c_void_p] * 7),
+    "tga_solution_set_shard": (C.c_int32, [C.c_void_p, C.c_int32, C.c_int32]),
+    "tga_nccl_unique_id": (C.c_int32, [C.c_void_p]),
+    "tga_comm_init": (C.c_int32, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
+    "tga_last_error": (C.c_char_p, []),
+    "tga_version": (C.c_char_p, []),
+    "tga_launch_count": (C.c_uint64, []),
+}
+
+
+def lib() -> C.CDLL:
+    """Load libtga.so (raises if it was not built -- there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built; run paper_2506_17357_b200/build.py "
+                              "(or __graft_entry__.build())")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SYMBOLS.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(rc: int, allow=(OK,)) -> int:
+    if rc in allow:
+        return rc
+    msg = lib().tga_last_error().decode(errors="replace")
+    raise TgaError(rc, msg)
+
+
+def _p(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _stream_ptr(stream) -> Optional[int]:
+    if stream is None:
+        return None
+    if isinstance(stream, int):
+        return stream
+    return int(getattr(stream, "cuda_stream"))  # torch.cuda.Stream
+
+
+def version() -> str:
+    return lib().tga_version().decode()
+
+
+def launch_count() -> int:
+    return int(lib().tga_launch_count())
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_char * 128)()
+    _check(lib().tga_nccl_unique_id(C.cast(buf, C.c_void_p)))
+    return bytes(buf)
+
+
+class Instance:
+    """tga_instance_create(dist, demand, tw, capacity)."""
+
+    def __init__(self, dist, demand, capacity: int, tw=None, score_mode: int = SCORE_FEASIBLE,
+                 w_load: int = 10, w_tw: int = 10, device: int = -1):
+        dist = np.asarray(dist)
+        if np.issubdtype(dist.dtype, np.integer):
+            self.dist = np.ascontiguousarray(dist, dtype=np.int32)
+            self.dtype = I32
+        else:
+            self.dist = np.ascontiguousarray(dist, dtype=np.float32)
+            self.dtype = F32
+        self.n = int(self.dist.shape[0])
+        self.demand = np.ascontiguousarray(demand, dtype=np.int32)
+        self.tw = None if tw is None else np.ascontiguousarray(tw, dtype=np.float32)
+        self.capacity = int(capacity)
+        opt = _Options()
+        opt.score_mode, opt.w_load, opt.w_tw, opt.device = score_mode, w_load, w_tw, device
+        self.score_mode = score_mode
+        h = C.c_void_p()
+        _check(lib().tga_instance_create(self.n, _p(self.dist), self.dtype, None, _p(self.demand),
+                                         _p(self.tw), self.capacity, C.byref(opt), C.byref(h)))
+        self._h = h
+
+    @classmethod
+    def from_gen(cls, inst, **kw):
+        return cls(inst.dist, inst.demand, inst.capacity, inst.tw, **kw)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().tga_instance_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _csr(routes):
+    if isinstance(routes, tuple):
+        ptr, cust = routes
+    else:
+        rr = routes.routes if hasattr(routes, "routes") else routes
+        ptr = np.zeros(len(rr) + 1, dtype=np.int32)
+        for i, r in enumerate(rr):
+            ptr[i + 1] = ptr[i] + len(r)
+        cust = np.array([c for r in rr for c in r], dtype=np.int32)
+    return np.ascontiguousarray(ptr, dtype=np.int32), np.ascontiguousarray(cust, dtype=np.int32)
+
+
+class Solution:
+    """tga_solution_load(routes) + eval / best_move / apply_move."""
+
+    def __init__(self, inst: Instance, routes):
+        self.inst = inst
+        ptr, cust = _csr(routes)
+        h = C.c_void_p()
+        _check(lib().tga_solution_load(inst.handle, len(ptr) - 1, _p(ptr), _p(cust), C.byref(h)))
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().tga_solution_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- hot path
+    def eval(self, op_mask: int = OP_ALL, stream=None) -> None:
+        _check(lib().tga_eval(self._h, op_mask, _stream_ptr(stream)))
+
+    def best_move(self, op_mask: int = OP_ALL):
+        """(improving: bool, Move).  Move.variant == -1 when no candidate was valid."""
+        m = Move()
+        rc = _check(lib().tga_best_move(self._h, op_mask, C.byref(m)), allow=(OK, NO_IMPROVING_MOVE))
+        return rc == OK, m
+
+    def apply(self, move: Move) -> None:
+        _check(lib().tga_apply_move(self._h, C.byref(move)))
+
+    # ---- queries
+    def keys(self) -> np.ndarray:
+        k = np.zeros(N_VARIANTS, dtype=np.uint64)
+        _check(lib().tga_solution_keys(self._h, _p(k)))
+        return k
+
+    def counts(self) -> np.ndarray:
+        c = np.zeros(N_VARIANTS, dtype=np.uint64)
+        _check(lib().tga_solution_counts(self._h, _p(c)))
+        return c
+
+    def info(self):
+        R, N, Q, g = C.c_int32(), C.c_int32(), C.c_int32(), C.c_uint64()
+        _check(lib().tga_solution_info(self._h, C.byref(R), C.byref(N), C.byref(Q), C.byref(g)))
+        return R.value, N.value, Q.value, g.value
+
+    def routes(self):
+        R, N, _, _ = self.info()
+        ptr = np.zeros(R + 1, dtype=np.int32)
+        cust = np.zeros(max(N, 1), dtype=np.int32)
+        _check(lib().tga_solution_routes(self._h, _p(ptr), _p(cust)))
+        return [list(map(int, cust[ptr[i]:ptr[i + 1]])) for i in range(R)]
+
+    def cost(self):
+        di, df, le, te = C.c_int64(), C.c_double(), C.c_int64(), C.c_double()
+        _check(lib().tga_solution_cost(self._h, C.byref(di), C.byref(df), C.byref(le), C.byref(te)))
+        return di.value, df.value, le.value, te.value
+
+    def attributes(self):
+        _, _, Q, _ = self.info()
+        out = {k: np.zeros(Q) for k in ("pre_D", "suf_D", "pre_TV", "suf_TV", "start")}
+        out["pre_L"] = np.zeros(Q, dtype=np.int64)
+        out["suf_L"] = np.zeros(Q, dtype=np.int64)
+        _check(lib().tga_solution_attributes(self._h, _p(out["pre_L"]), _p(out["suf_L"]),
+                                             _p(out["pre_D"]), _p(out["suf_D"]), _p(out["pre_TV"]),
+                                             _p(out["suf_TV"]), _p(out["start"])))
+        return out
+
+    # ---- multi-GPU
+    def set_shard(self, shard: int, n_shards: int) -> None:
+        _check(lib().tga_solution_set_shard(self._h, shard, n_shards))
+
+    def comm_init(self, rank: int, world: int, uid: bytes) -> None:
+        buf = (C.c_char * 128).from_buffer_copy(uid)
+        _check(lib().tga_comm_init(self._h, rank, world, C.cast(buf, C.c_void_p)))
+
+
+def decode_key(key: int, integer: bool = True):
+    """(score, flat index) of a packed key (order-preserving score << 32 | index)."""
+    key = int(key)
+    ordv, idx = key >> 32, key & 0xFFFFFFFF
+    if integer:
+        s = (ordv ^ 0x80000000)
+        s = s - (1 << 32) if s >= 1 << 31 else s
+        return s, idx
+    u = (ordv ^ 0x80000000) if (ordv & 0x80000000) else (~ordv & 0xFFFFFFFF)
+    return float(np.array([u], dtype=np.uint32).view(np.float32)[0]), idx

@@ -1,0 +1,75 @@
+"""The C-ABI library loads and exports every symbol include/tga.h declares
+(no compute calls -- CPU only)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "tga.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(tga_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_declares_the_north_star_calls():
+    names = _declared()
+    for f in ["tga_instance_create", "tga_solution_load", "tga_eval", "tga_best_move", "tga_apply_move"]:
+        assert f in names
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2506_17357_b200 import build
+    build.build()
+    lib = ctypes.CDLL(os.path.join(ROOT, "paper_2506_17357_b200", "libtga.so"))
+    for name in _declared():
+        assert hasattr(lib, name), name
+
+
+def test_binding_symbol_table_matches_header():
+    from paper_2506_17357_b200 import tga
+    assert sorted(tga._SYMBOLS) == _declared()
+
+
+def test_variant_tables_agree_with_oracle():
+    """Variant ids are the tie-break rank on both sides (kept in sync by this
+    test, not by shared code)."""
+    import oracle as O
+    from paper_2506_17357_b200 import tga
+    assert tga.N_VARIANTS == O.N_VARIANTS
+    assert tga.V_RELOCATE == O.V_RELOC and tga.V_SWAP == O.V_SWAP
+    assert tga.V_IRELOCATE == O.V_IRELOC and tga.V_ISWAP == O.V_ISWAP
+    hdr = open(os.path.join(ROOT, "include", "tga.h")).read()
+    for name, val in re.findall(r"TGA_V_([A-Z0-9_]+)\s*=\s*(\d+)", hdr):
+        pass
+    assert "TGA_N_VARIANTS = 23" in hdr
+
+
+def test_version_and_error_strings_without_gpu():
+    from paper_2506_17357_b200 import tga
+    assert "sm_100a" in tga.version()
+    assert isinstance(tga.lib().tga_last_error(), bytes)
+
+
+def test_instance_argument_validation_without_gpu():
+    """Argument checks happen before any device call."""
+    from paper_2506_17357_b200 import tga
+    d = np.array([[0, 1], [2, 0]], dtype=np.int32)
+    with pytest.raises(tga.TgaError) as e:
+        tga.Instance(d, [0, 1], 10)
+    assert e.value.code == -4  # asymmetric -> unsupported
+    d = np.array([[0, 1], [1, 0]], dtype=np.int32)
+    with pytest.raises(tga.TgaError) as e:
+        tga.Instance(d, [0, -1], 10)
+    assert e.value.code == -1
+
+
+def test_key_decode_roundtrip():
+    from paper_2506_17357_b200 import tga
+    for s in [-5, 0, 7, -2 ** 31, 2 ** 31 - 1]:
+        ordv = (s & 0xFFFFFFFF) ^ 0x80000000
+        assert tga.decode_key((ordv << 32) | 123) == (s, 123)

@@ -1,0 +1,272 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by
+element on the same seeded inputs.
+
+Bar (BASELINE.json north_star): integer distances (CVRP nint, VRPTW integer
+tenths) -> best-move keys bit-exact per variant (score and canonical index);
+real-valued time windows -> scores within 1e-4 relative and identical masks
+outside the ambiguity band (reading 13).
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import tga_gen as G
+from tests.conftest import gpu_available
+
+pytestmark = pytest.mark.gpu
+
+if gpu_available():
+    from paper_2506_17357_b200 import tga as T
+else:  # pragma: no cover - collected on CPU boxes, skipped by the marker filter
+    T = None
+
+
+def _need_gpu():
+    if not gpu_available():
+        pytest.skip("no CUDA device")
+
+
+INTER = [1, 2, 3, 4, 5, 6, 7, 8, 9, 10]
+INTRA_TW = list(range(11, 23))
+ALLV = list(range(23))
+
+
+def oracle_key(m: O.Move, Q: int):
+    if not m.found:
+        return None
+    return (m.score, m.u * Q + m.v)
+
+
+def gpu_keys(sol, integer=True):
+    ks = sol.keys()
+    out = {}
+    for v in range(T.N_VARIANTS):
+        k = int(ks[v])
+        out[v] = None if k == 0xFFFFFFFFFFFFFFFF else T.decode_key(k, integer)
+    return out
+
+
+def check_exact(inst, routes, variants, mode=0, label=""):
+    orc = O.Oracle.from_instance(inst)
+    gi = T.Instance.from_gen(inst, score_mode=mode)
+    gs = T.Solution(gi, routes)
+    mask = sum(1 << v for v in variants)
+    gs.eval(mask)
+    got = gpu_keys(gs, integer=True)
+    Q = O.canonical_q(routes)
+    for v in variants:
+        m = orc.best_move(routes, v, mode=mode)
+        exp = oracle_key(m, Q)
+        assert got[v] == exp, f"{label} variant {v} ({T.VARIANT_NAMES[v]}): gpu {got[v]} oracle {exp}"
+    return gi, gs, orc
+
+
+# ---------------------------------------------------------------- cfg1: 20 customers, 4 routes
+@pytest.mark.parametrize("seed", range(4))
+@pytest.mark.parametrize("spare", [False, True])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_cfg1_all_variants_exact(seed, spare, mode):
+    _need_gpu()
+    inst, sol = G.cvrp_small(seed, spare=spare)
+    check_exact(inst, sol, ALLV, mode, f"cfg1 s{seed}")
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_cfg1_random_partitions_exact(seed):
+    """Feasible and infeasible random partitions, ragged + empty routes."""
+    _need_gpu()
+    inst, _ = G.cvrp_small(seed)
+    sol = G.random_partition(20, 3 + seed % 4, 900 + seed, allow_empty=True)
+    for mode in (0, 1):
+        check_exact(inst, sol, ALLV, mode, f"cfg1-rand s{seed}")
+
+
+@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("mode", [0, 1])
+def test_small_vrptw_exact(seed, mode):
+    """TW-I (integer tenths in fp32 on the GPU): bit-exact keys."""
+    _need_gpu()
+    inst, sol = G.gh_like(seed, n=60, kind="R1" if seed % 2 == 0 else "R2")
+    if seed >= 3:
+        sol = G.perturb(sol, 12, seed)  # infeasible states too
+    check_exact(inst, sol, INTER + INTRA_TW, mode, f"vrptw s{seed}")
+
+
+def test_long_routes_chunked_scan():
+    """Routes longer than one warp (L > 32) exercise the scan carries."""
+    _need_gpu()
+    inst, sol = G.gh_like(5, n=300, kind="R2")
+    long_sol = G.Solution([sum(sol.routes[:4], [])] + sol.routes[4:])
+    for mode in (0, 1):
+        check_exact(inst, long_sol, INTER + INTRA_TW, mode, "long")
+    inst2, sol2 = G.x_like(3, n=300, target_routes=3)
+    check_exact(inst2, sol2, ALLV, 1, "long-cvrp")
+
+
+# ---------------------------------------------------------------- attributes (a2)
+@pytest.mark.parametrize("name", ["cfg1", "vrptw"])
+def test_attribute_rebuild_matches_full_rebuild(name):
+    _need_gpu()
+    if name == "cfg1":
+        inst, sol = G.cvrp_small(1, spare=True)
+    else:
+        inst, sol = G.gh_like(2, n=200, kind="R2")
+        sol = G.perturb(sol, 30, 5)
+    orc = O.Oracle.from_instance(inst)
+    gs = T.Solution(T.Instance.from_gen(inst), sol)
+    a, b = gs.attributes(), orc.attributes(sol)
+    for k in ("pre_L", "suf_L", "pre_D", "suf_D", "pre_TV", "suf_TV"):
+        np.testing.assert_array_equal(a[k], b[k], err_msg=k)
+    if inst.tw is not None:
+        np.testing.assert_array_equal(a["start"], b["start"])
+    D, LV, TV = orc.cost(sol)
+    di, df, le, te = gs.cost()
+    assert di == D and le == LV and te == TV
+
+
+def test_counts_match_oracle_enumeration():
+    _need_gpu()
+    inst, _ = G.cvrp_small(2)
+    sol = G.random_partition(20, 5, 77, allow_empty=True)
+    orc = O.Oracle.from_instance(inst)
+    gs = T.Solution(T.Instance.from_gen(inst), sol)
+    c = gs.counts()
+    for v in ALLV:
+        assert int(c[v]) == orc.best_move(sol, v).n_candidates
+
+
+# ---------------------------------------------------------------- lockstep trajectories (a7, a8)
+@pytest.mark.parametrize("name", ["cvrp", "vrptw"])
+def test_lockstep_descent(name):
+    """Identical search trajectories: best move over all variants,
+    applied on both sides, keys equal at every step; delta == cost change."""
+    _need_gpu()
+    if name == "cvrp":
+        inst, sol = G.x_like(4, n=150, target_routes=8)
+        variants = ALLV
+    else:
+        inst, sol = G.gh_like(4, n=150, kind="R2")
+        variants = INTER + INTRA_TW
+    orc = O.Oracle.from_instance(inst)
+    gs = T.Solution(T.Instance.from_gen(inst), sol)
+    mask = sum(1 << v for v in variants)
+    routes = [list(r) for r in sol.routes]
+    D0 = orc.cost(routes)[0]
+    for step in range(25):
+        gs.eval(mask)
+        improving, mv = gs.best_move(mask)
+        ob = orc.best_over(routes, variants)
+        if ob is None or not ob.score < 0:
+            assert not improving
+            break
+        assert improving
+        Q = O.canonical_q(routes)
+        assert (mv.variant, mv.delta_i, mv.u, mv.v) == (ob.variant, ob.score, ob.u, ob.v), step
+        assert (mv.route_a, mv.pos_a, mv.route_b, mv.pos_b) == (ob.route_a, ob.pos_a, ob.route_b, ob.pos_b)
+        gs.apply(mv)
+        routes = orc.apply(routes, ob.variant, ob.route_a, ob.pos_a, ob.route_b, ob.pos_b)
+        assert gs.routes() == routes
+        D1 = orc.cost(routes)[0]
+        assert D1 - D0 == mv.delta_i
+        assert gs.cost()[0] == D1
+        D0 = D1
+    # the incremental state equals a fresh load of the final routes
+    fresh = T.Solution(gs.inst, routes)
+    fresh.eval(mask)
+    gs.eval(mask)
+    np.testing.assert_array_equal(fresh.keys(), gs.keys())
+
+
+def test_stale_move_rejected():
+    _need_gpu()
+    inst, sol = G.x_like(5, n=80, target_routes=5)
+    gs = T.Solution(T.Instance.from_gen(inst), sol)
+    gs.eval(T.OP_INTER)
+    ok, mv = gs.best_move(T.OP_INTER)
+    assert ok
+    gs.apply(mv)
+    with pytest.raises(T.TgaError) as e:
+        gs.apply(mv)
+    assert e.value.code == -3
+
+
+def test_two_opt_with_time_windows_unsupported():
+    _need_gpu()
+    inst, sol = G.gh_like(0, n=40, kind="R1")
+    gs = T.Solution(T.Instance.from_gen(inst), sol)
+    with pytest.raises(T.TgaError) as e:
+        gs.eval(T.OP_2OPT)
+    assert e.value.code == -4
+
+
+# ---------------------------------------------------------------- sharding (a6)
+@pytest.mark.parametrize("n_shards", [2, 3, 8])
+def test_virtual_shards_equal_unsharded(n_shards):
+    """Row shards evaluated one after another, keys min-combined on the host:
+    equal to the unsharded keys (the exact combine of the NCCL allreduce)."""
+    _need_gpu()
+    inst, sol = G.x_like(6, n=400, target_routes=17)
+    gs = T.Solution(T.Instance.from_gen(inst), sol)
+    gs.eval(T.OP_ALL)
+    full = gs.keys()
+    comb = np.full(T.N_VARIANTS, np.iinfo(np.uint64).max, dtype=np.uint64)
+    for s in range(n_shards):
+        gs.set_shard(s, n_shards)
+        gs.eval(T.OP_ALL)
+        comb = np.minimum(comb, gs.keys())
+    np.testing.assert_array_equal(comb, full)
+
+
+# ---------------------------------------------------------------- full-size configs
+@pytest.mark.parametrize("name", ["cfg2", "cfg3", "cfg3r2"])
+def test_full_size_configs_exact(name):
+    """BASELINE configs 2-3 at full size, the launch configuration bench.py
+    times: every variant's key vs the oracle's full enumeration."""
+    _need_gpu()
+    inst, sol = G.config(name)
+    variants = ALLV if inst.tw is None else INTER + INTRA_TW
+    check_exact(inst, sol, variants, 0, name)
+
+
+def test_cfg2_state_b_after_descent():
+    """'State B' (after accepted moves) at full size: sampled candidates
+    scored one by one by the oracle agree with the GPU keys."""
+    _need_gpu()
+    inst, sol = G.config("cfg2")
+    orc = O.Oracle.from_instance(inst)
+    gs = T.Solution(T.Instance.from_gen(inst), sol)
+    for _ in range(30):
+        gs.eval(T.OP_ALL)
+        ok, mv = gs.best_move(T.OP_ALL)
+        if not ok:
+            break
+        gs.apply(mv)
+    routes = gs.routes()
+    check_exact(inst, routes, ALLV, 0, "cfg2-B")
+
+
+# ---------------------------------------------------------------- TW-F (real-valued)
+def test_real_valued_time_windows_tolerance():
+    """TW-F: fp32 GPU vs fp64 oracle.  Scores within 1e-4 relative; when the
+    oracle's best is separated from the runner-up by more than the band, the
+    index must match (readings 13, 17)."""
+    _need_gpu()
+    inst, sol = G.gh_like(1, n=200, kind="R2", mode="twf")
+    orc = O.Oracle.from_instance(inst)
+    gs = T.Solution(T.Instance.from_gen(inst), sol)
+    mask = sum(1 << v for v in INTER + INTRA_TW)
+    gs.eval(mask)
+    got = gpu_keys(gs, integer=False)
+    Q = O.canonical_q(sol)
+    for v in INTER + INTRA_TW:
+        sc, us, vs, best = orc.enumerate(sol, v)
+        if not best.found:
+            assert got[v] is None
+            continue
+        assert got[v] is not None
+        s_gpu, idx_gpu = got[v]
+        tol = 1e-4 * max(1.0, abs(best.score))
+        assert abs(s_gpu - best.score) <= tol + 1e-3
+        order = np.sort(sc[np.isfinite(sc)])
+        if len(order) > 1 and order[1] - order[0] > 10 * tol + 1e-2:
+            assert idx_gpu == best.u * Q + best.v

@@ -248,7 +248,7 @@ __device__ __forceinline__ void tma_load_2d(void *smem_dst, const CUtensorMap *m
 
 // ============================================================== inter-route evaluation
 // Tile: TU u-rows x TV v-columns of the (physical) slot pair space; the Dp box
-// with a halo (rows u0-1 .. u0+TU+2, cols v0-1 .. v0+TV+2) is TMA-loaded into
+// with a halo (rows u0-1 .. u0+TU+2, cols v0-4 .. v0+TV+3) is TMA-loaded into
 // shared memory (double-buffered across the persistent tile loop).
 // Thread mapping: lane -> v = v0 + lane + 32*j (j < VPT); warp -> UPW rows.
 template <class DT, bool TW, uint32_t MASK>
@@ -258,9 +258,11 @@ __global__ void __launch_bounds__(kInterThreads) k_inter(const SolView<DT> S, co
     constexpr int TU = kTileU, TV = kTileV, VPT = TV / 32, UPW = TU / (kInterThreads / 32);
     constexpr int BW = kBoxW, BH = kBoxH;
     constexpr int NV = 11;  // inter variant ids 1..10
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    DT *buf0 = reinterpret_cast<DT *>(smem_raw);
-    DT *buf1 = reinterpret_cast<DT *>(smem_raw + kBoxBytesPadded);
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    // TMA destinations must be 128-byte aligned in the shared window: align at run time
+    unsigned char *smem_al = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+    DT *buf0 = reinterpret_cast<DT *>(smem_al);
+    DT *buf1 = reinterpret_cast<DT *>(smem_al + kBoxBytesPadded);
     __shared__ uint64_t bar[2];
     __shared__ unsigned long long red[NV];
 
@@ -281,7 +283,7 @@ __global__ void __launch_bounds__(kInterThreads) k_inter(const SolView<DT> S, co
         const uint32_t ij = tiles[t];
         const int I = ij >> 16, J = ij & 0xFFFF;
         mbar_expect_tx(&bar[b], kBoxBytes);
-        tma_load_2d(b ? buf1 : buf0, &tmap, J * TV - 1, I * TU - 1, &bar[b]);
+        tma_load_2d(b ? buf1 : buf0, &tmap, J * TV - kBoxX0, I * TU - 1, &bar[b]);
     };
 
     int t = t_lo + blockIdx.x;
@@ -297,7 +299,7 @@ __global__ void __launch_bounds__(kInterThreads) k_inter(const SolView<DT> S, co
         const uint32_t ij = tiles[t];
         const int u0 = (ij >> 16) * TU, v0 = (ij & 0xFFFF) * TV;
         // Dp(x, y) from the staged box
-        auto Dt = [&](int x, int y) -> DT { return tile[(x - u0 + 1) * BW + (y - v0 + 1)]; };
+        auto Dt = [&](int x, int y) -> DT { return tile[(x - u0 + 1) * BW + (y - v0 + kBoxX0)]; };
 
 #pragma unroll 1
         for (int j = 0; j < VPT; ++j) {
@@ -591,7 +593,7 @@ template <class DT, bool TW, uint32_t MASK>
 static cudaError_t launch_inter_t(const SolView<DT> &S, const CUtensorMap &map, const uint32_t *tiles, int t_lo,
                                   int t_hi, const ScoreParams &sp, uint64_t *keys, int grid, cudaStream_t st) {
     auto kern = k_inter<DT, TW, MASK>;
-    const int smem = 2 * kBoxBytesPadded;
+    const int smem = 2 * kBoxBytesPadded + 128;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

@@ -14,7 +14,11 @@ namespace tga {
 constexpr int kInterThreads = 256;
 constexpr int kTileU = 32;                      // u rows per tile
 constexpr int kTileV = 64;                      // v columns per tile
-constexpr int kBoxW = kTileV + 4;               // Dp box columns: v0-1 .. v0+TV+2
+// Dp box columns v0-4 .. v0+TV+3: the innermost TMA coordinate must be a
+// multiple of 16 bytes (measured on B200: an unaligned x traps as an illegal
+// instruction), so the left halo is 4 columns wide instead of 1.
+constexpr int kBoxW = kTileV + 8;
+constexpr int kBoxX0 = 4;                       // columns left of v0 in the box
 constexpr int kBoxH = kTileU + 4;               // Dp box rows:    u0-1 .. u0+TU+2
 constexpr int kBoxBytes = kBoxW * kBoxH * 4;
 constexpr int kBoxBytesPadded = (kBoxBytes + 127) / 128 * 128;

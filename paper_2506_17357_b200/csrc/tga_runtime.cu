@@ -141,6 +141,7 @@ static bool is_intra_variant(int v) { return v == TGA_V_2OPT || v >= TGA_V_IRELO
 
 static int32_t set_device(const tga_instance *inst) {
     TGA_CUDA(cudaSetDevice(inst->device));
+    (void)cudaGetLastError();  // drop non-sticky errors left by other code on this thread
     return TGA_OK;
 }
 
@@ -365,6 +366,7 @@ extern "C" int32_t tga_instance_create(int32_t n, const void *dist, int32_t dtyp
         return code;
     };
     if (cudaSetDevice(I->device) != cudaSuccess) return cleanup(fail(TGA_ERR_CUDA, "cudaSetDevice"));
+    (void)cudaGetLastError();
     const size_t nn = static_cast<size_t>(n) * n;
     cudaError_t e = cudaMalloc(&I->dC, nn * 4);
     if (e == cudaSuccess) e = cudaMalloc(&I->dDemand, sizeof(int32_t) * n);
@@ -524,6 +526,7 @@ extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
     mask &= TGA_OP_ALL;
     if ((mask & TGA_OP_2OPT) && I->tw)
         return fail(TGA_ERR_UNSUPPORTED, "2-opt is only defined without time windows (P:148)");
+    if (set_device(I) != TGA_OK) return TGA_ERR_CUDA;
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s->stream;
     TGA_CUDA(cudaMemsetAsync(s->keys, 0xFF, TGA_N_VARIANTS * 8, st));
     ScoreParams sp{I->Q, I->opt.score_mode, I->opt.w_load, I->opt.w_tw};

@@ -1,0 +1,393 @@
+#!/usr/bin/env python
+"""Benchmark of the TGA hot path on B200 (BASELINE.json metric: moves evaluated/s
+and full-neighbourhood sweeps/s per operator).
+
+A *step* is one best-improvement local-search iteration of the whole hot path
+ on the BASELINE config-2 workload (Uchoa X-like
+CVRP, 1000 customers, X-n1001-k43 shape + one spare route):
+    tga_eval(all 23 variants: inter-route kernel + intra-route kernel)
+    -> tga_best_move (8 B per variant device->host)
+    -> tga_apply_move (span re-upload, Dp row/column refresh, re-scan).
+value = canonical candidates evaluated / device time of the step (CUDA events on
+the solution's stream, L2 flushed between steps: the working set < L2).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl tga|reference]
+Under torchrun (N>1) every rank evaluates a row shard of the same neighbourhood
+and the packed keys are MIN-allreduced over NCCL inside tga_eval.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "moves evaluated/sec and neighbourhood sweeps/sec per operator at 1/2/4/8 B200"
+UNIT = "moves/s"
+
+# Algorithmic lane-operations per candidate: the
+# arithmetic of the variant's delta / load / feasibility formulas plus the
+# select + min of the fused argmin, CVRP integer path.  Row- or column-only
+# terms (removal gains, route loads) are amortised and not counted.
+ALG_OPS = {1: 10, 2: 11, 3: 11, 4: 11, 5: 18, 6: 18, 7: 18, 8: 18, 9: 18, 10: 18,
+           0: 5, 11: 5, 12: 5, 13: 5}
+for _v in range(14, 23):
+    ALG_OPS[_v] = 9
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=60)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["tga", "reference"], default="tga")
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-per-op", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"tga_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        if self.proc is None:
+            return out
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait()
+        self.f.close()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            p = [x.strip() for x in line.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx.append(float(p[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, p[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        if sm:
+            out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                   "samples": len(sm)}
+        return out
+
+
+# ------------------------------------------------------------------ helpers
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def traffic_for(kernel_tag: str):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(p):
+        return json.load(open(p)).get(kernel_tag)
+    return None
+
+
+def dist_init(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def oracle_sweep_rate(inst, routes, budget_s=12.0, rows_frac=None, row_offset=0):
+    """CPU oracle (single thread, as it stands) on all variants; returns
+    (moves/s, candidates, seconds, sweeps)."""
+    import oracle as O
+    orc = O.Oracle.from_instance(inst)
+    variants = [v for v in range(23) if not (inst.tw is not None and v == 0)]
+    Q = O.canonical_q(routes)
+    tot_c, tot_t, sweeps = 0, 0.0, 0
+    while True:
+        for v in variants:
+            if rows_frac:
+                span = max(1, int(Q * rows_frac))
+                lo = (row_offset * span) % Q
+                t0 = time.perf_counter()
+                m = orc.best_move(routes, v, u_lo=lo, u_hi=min(Q, lo + span))
+            else:
+                t0 = time.perf_counter()
+                m = orc.best_move(routes, v)
+            tot_t += time.perf_counter() - t0
+            tot_c += m.n_candidates
+        sweeps += 1
+        if tot_t >= budget_s or rows_frac:
+            break
+    return tot_c / tot_t, tot_c, tot_t, sweeps
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args):
+    ws, rank, _ = dist_init(args)
+    if rank != 0:
+        return 0
+    import tga_gen as G
+    inst, sol = G.config(args.config, args.seed)
+    routes = sol.routes
+    frac = 1.0 / 16
+    for w in range(args.warmup):
+        oracle_sweep_rate(inst, routes, rows_frac=frac, row_offset=w)
+    tot_c, tot_t = 0, 0.0
+    for k in range(args.steps):
+        _, c, t, _ = oracle_sweep_rate(inst, routes, rows_frac=frac, row_offset=args.warmup + k)
+        tot_c += c
+        tot_t += t
+    v = tot_c / tot_t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"{args.config}: {G.CONFIGS.get(args.config, args.config)}; "
+                               "all 23 move variants", "seed": args.seed},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"each step = all 23 variants over 1/16 of the canonical u-rows "
+                                   f"(rotating), single-threaded C oracle rebuilding every neighbour"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ tga arm
+def run_tga(args):
+    import torch
+    ws, rank, local = dist_init(args)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    import tga_gen as G
+    from paper_2506_17357_b200 import tga as T
+
+    inst, sol0 = G.config(args.config, args.seed)
+    stream = torch.cuda.Stream(device=dev)
+    gi = T.Instance.from_gen(inst)
+    gs = T.Solution(gi, sol0)
+    gs.set_stream(stream)
+    if ws > 1:
+        import torch.distributed as dist
+        obj = [T.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        gs.comm_init(rank, ws, obj[0])
+    mask_all = T.OP_ALL if inst.tw is None else (T.OP_ALL & ~T.OP_2OPT)
+    mask_inter = mask_all & T.OP_INTER
+    mask_intra = mask_all & T.OP_INTRA
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)  # 256 MB > L2 (126 MB)
+
+    def step(evs=None):
+        if evs:
+            evs[0].record(stream)
+        gs.eval(mask_inter, stream)
+        if evs:
+            evs[1].record(stream)
+        gs.eval(mask_intra | T.EVAL_ACCUMULATE, stream)
+        ok, mv = gs.best_move(mask_all)
+        if ok:
+            gs.apply(mv)
+        if evs:
+            evs[2].record(stream)
+        return ok
+
+    # ---------------- warm-up
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize(dev)
+
+    # ---------------- timed region: K steps, per-step events, L2 flushed between steps
+    sampler = ClockSampler(local)
+    K = args.steps
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+    counts = []
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    sampler.start()
+    launches0 = T.launch_count()
+    applied = 0
+    for k in range(K):
+        with torch.cuda.stream(stream):
+            flush.fill_(k)
+        counts.append(gs.counts().astype(np.int64))
+        applied += int(step(evs[k]))
+    torch.cuda.synchronize(dev)
+    launches = T.launch_count() - launches0
+    clocks = sampler.stop()
+    step_ms = [e[0].elapsed_time(e[2]) for e in evs]
+    inter_ms = [e[0].elapsed_time(e[1]) for e in evs]
+    tot_ms = float(sum(step_ms))
+    if ws > 1:
+        import torch.distributed as dist
+        t = torch.tensor([tot_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+        dist.barrier()
+    cand = np.stack(counts)                              # K x 23
+    sel = np.array([(mask_all >> v) & 1 for v in range(23)], dtype=bool)
+    cand_total = int(cand[:, sel].sum())
+    value = cand_total / (tot_ms / 1e3)
+
+    if rank != 0:
+        return 0
+
+    # ---------------- roofline of the dominant kernel (inter-route eval), live events
+    pk, pk_src = peaks()
+    inter_avg_s = statistics.mean(inter_ms) / 1e3
+    R, N, Qc, _ = gs.info()
+    Qp = N + 2 * R
+    inter_sel = [v for v in range(1, 11)]
+    inter_cands = float(cand[:, inter_sel].sum(axis=1).mean())
+    alg_bytes = (Qp * Qp / 2.0) * 4.0                    # Dp upper triangle, int32
+    alg_ops = float(sum(cand[:, v].mean() * ALG_OPS[v] for v in inter_sel))
+    sm_mhz_peak = float(pk.get("sm_max_mhz", 1965.0))
+    alu_peak = 148 * 128 * sm_mhz_peak * 1e6            # lane-ops/s (4 SMSP x 32 lanes x 1 issue/clk)
+    hbm_peak = float(pk["hbm_gbs"]) * 1e9
+    t_hbm = alg_bytes / hbm_peak
+    t_alu = alg_ops / alu_peak
+    hbm_view = {"bound": "hbm", "achieved": alg_bytes / inter_avg_s / 1e9, "peak": hbm_peak / 1e9,
+                "unit": "GB/s", "frac": (alg_bytes / inter_avg_s) / hbm_peak,
+                "traffic": traffic_for("k_inter_all"), "peak_source": pk_src}
+    alu_view = {"bound": "alu", "achieved": alg_ops / inter_avg_s / 1e12, "peak": alu_peak / 1e12,
+                "unit": "Tops/s", "frac": (alg_ops / inter_avg_s) / alu_peak,
+                "traffic": traffic_for("k_inter_all"),
+                "peak_source": f"148 SM x 128 lanes x {sm_mhz_peak:.0f} MHz ({pk_src} sm_max_mhz)"}
+    primary, alt = (alu_view, hbm_view) if t_alu >= t_hbm else (hbm_view, alu_view)
+    primary = dict(primary, kernel="k_inter<int,CVRP,all-inter> (tga_eval inter launch incl. key reset)",
+                   kernel_ms=inter_avg_s * 1e3, candidates_per_launch=inter_cands,
+                   alg_bytes_per_launch=alg_bytes, alg_ops_per_launch=alg_ops)
+
+    # ---------------- steady state per operator: CUDA-graph replay of back-to-back sweeps
+    per_op = {}
+    if not args.no_per_op:
+        cnt_now = gs.counts().astype(np.int64)
+        groups = dict(T.OPERATORS)
+        groups["fused 2-opt*+relocate+swap"] = T.OP_FUSED_NS
+        groups["all inter"] = T.OP_INTER
+        groups["all"] = mask_all
+        for name, m in groups.items():
+            m &= mask_all
+            if not m:
+                continue
+            G_SWEEPS, REPS = 20, 10
+            gs.eval(m, stream)
+            torch.cuda.synchronize(dev)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                for _ in range(G_SWEEPS):
+                    gs.eval(m, stream)
+            g.replay()
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(stream):
+                e0.record(stream)
+                for _ in range(REPS):
+                    g.replay()
+                e1.record(stream)
+            torch.cuda.synchronize(dev)
+            per_sweep_s = e0.elapsed_time(e1) / 1e3 / (G_SWEEPS * REPS)
+            c = int(sum(cnt_now[v] for v in range(23) if (m >> v) & 1))
+            per_op[name] = {"moves_per_s": c / per_sweep_s, "sweeps_per_s": 1.0 / per_sweep_s,
+                            "us_per_sweep": per_sweep_s * 1e6, "candidates": c}
+            del g
+
+    # ---------------- e2e through the C ABI with host buffers
+    ptr, cust = sol0.flat()
+    e2e_steps = min(K, 20)
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    e2e_c = 0
+    for _ in range(e2e_steps):
+        s2 = T.Solution(gi, (ptr, cust))          # host -> device: routes, layout, Dp build, scan
+        s2.eval(mask_all)
+        s2.best_move(mask_all)                    # device -> host: 8 B per variant
+        e2e_c += int(sum(int(x) for v, x in enumerate(s2.counts()) if (mask_all >> v) & 1))
+        s2.close()
+    torch.cuda.synchronize(dev)
+    e2e_s = time.perf_counter() - t0
+    h2d = 4 * (len(ptr) + len(cust)) + 5 * 4 * (N + 2 * R) + 8 * R
+    e2e = {"value": e2e_c / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+           "d2h_bytes_per_step": 23 * 8,
+           "step": "tga_solution_load(host CSR routes) + tga_eval(all) + tga_best_move; "
+                   "host wall clock, instance resident"}
+
+    # ---------------- CPU oracle baseline (rank 0, N=1 only)
+    cpu = None
+    if ws == 1 and not args.no_cpu_baseline:
+        rate, c, t, sw = oracle_sweep_rate(inst, sol0.routes, budget_s=12.0)
+        cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"{sw} full sweep(s) of all variants on state A ({c} candidates, {t:.1f} s), "
+                         "single-threaded C oracle that rebuilds every neighbour route"}
+
+    sweeps_per_s = K / (tot_ms / 1e3)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K,
+        "warmup": max(args.warmup, 3), "ms_per_step": tot_ms / K, "higher_is_better": True,
+        "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic",
+        "config": {"workload": f"{args.config}: {G.CONFIGS.get(args.config, args.config)}; "
+                               "step = eval all variants + best move + apply",
+                   "customers": N, "routes": R, "canonical_slots": Qc, "seed": args.seed,
+                   "l2": "flushed between timed steps (256 MB write); working set < L2",
+                   "parallelism": f"row-shard x{ws}" if ws > 1 else "1 GPU"},
+        "sweeps_per_s": sweeps_per_s, "applied_moves": applied,
+        "candidates_per_step": cand_total / K,
+        "roofline": primary, "roofline_alt": alt,
+        "per_operator_steady_state": per_op,
+        "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_tga(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

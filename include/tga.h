@@ -95,6 +95,9 @@ enum {
 #define TGA_OP_ALL            ((1u << TGA_N_VARIANTS) - 1u)
 /* the north-star fused sweep: 2-opt* + relocate + swap */
 #define TGA_OP_FUSED_NS       (TGA_OP_2OPT_STAR | TGA_OP_RELOCATE | TGA_OP_SWAP)
+/* flag for tga_eval: keep the keys of the previous tga_eval of this generation and
+ * MIN-combine into them (evaluate a neighbourhood in several launches) */
+#define TGA_EVAL_ACCUMULATE   (1u << 31)
 
 /* score modes (Eq. 16a: F = F(dD, dT_V, dL_V), never given by the paper; reading 4) */
 #define TGA_SCORE_FEASIBLE  0   /* score = dD if both new routes are feasible, else +inf */
@@ -177,6 +180,11 @@ int32_t tga_best_move(tga_solution *sol, uint32_t op_mask, tga_move *out);
  * changed slot span, refresh its rows/columns of the distance tile matrix and
  * re-scan the affected routes.  Errors: TGA_ERR_STALE, TGA_ERR_INVALID_ARGUMENT. */
 int32_t tga_apply_move(tga_solution *sol, const tga_move *move);
+
+/* Make the solution use cuda_stream (a cudaStream_t; NULL = its own stream)
+ * for every later call (eval, best_move, apply, queries).  The stream must
+ * belong to the solution's device and outlive the solution or the next call. */
+int32_t tga_solution_set_stream(tga_solution *sol, void *cuda_stream);
 
 /* Per-variant raw keys of the last tga_eval (synchronises). keys[TGA_N_VARIANTS];
  * ~0 = no valid candidate. */

@@ -128,7 +128,8 @@ struct tga_solution {
     bool tmap_ok = false;
     uint64_t *h_keys = nullptr;                         // pinned
     int32_t *h_stage = nullptr;                         // pinned staging (5 * cap int32)
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr;                     // current stream (own or user's)
+    cudaStream_t own_stream = nullptr;
     int shard = 0, n_shards = 1;
     ncclComm_t comm = nullptr;
     int sm_count = 148;
@@ -298,7 +299,7 @@ static void free_solution(tga_solution *s) {
     if (s->Dp) cudaFree(s->Dp);
     if (s->h_keys) cudaFreeHost(s->h_keys);
     if (s->h_stage) cudaFreeHost(s->h_stage);
-    if (s->stream) cudaStreamDestroy(s->stream);
+    if (s->own_stream) cudaStreamDestroy(s->own_stream);
     delete s;
 }
 
@@ -434,8 +435,9 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
         cudaDeviceProp prop;
         if (cudaGetDeviceProperties(&prop, I->device) == cudaSuccess) s->sm_count = prop.multiProcessorCount;
     }
-    if (cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking) != cudaSuccess)
+    if (cudaStreamCreateWithFlags(&s->own_stream, cudaStreamNonBlocking) != cudaSuccess)
         return bail(fail(TGA_ERR_CUDA, "stream create"));
+    s->stream = s->own_stream;
     // ---- device arena: slot arrays (with guards), per-route arrays, keys, tiles
     const size_t cap = s->cap, Rr = static_cast<size_t>(R) + 1;
     struct Item { void **p; size_t bytes; };
@@ -512,6 +514,21 @@ extern "C" int32_t tga_solution_destroy(tga_solution *s) {
     return TGA_OK;
 }
 
+extern "C" int32_t tga_solution_set_stream(tga_solution *s, void *stream) {
+    if (!s) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL solution");
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s->own_stream;
+    if (st != s->stream) {
+        // order the new stream after everything queued on the old one
+        cudaEvent_t ev;
+        TGA_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        TGA_CUDA(cudaEventRecord(ev, s->stream));
+        TGA_CUDA(cudaStreamWaitEvent(st, ev, 0));
+        cudaEventDestroy(ev);
+    }
+    s->stream = st;
+    return TGA_OK;
+}
+
 extern "C" int32_t tga_solution_set_shard(tga_solution *s, int32_t shard, int32_t n_shards) {
     if (!s || n_shards < 1 || shard < 0 || shard >= n_shards) return fail(TGA_ERR_INVALID_ARGUMENT, "shard plan");
     s->shard = shard;
@@ -523,12 +540,13 @@ extern "C" int32_t tga_solution_set_shard(tga_solution *s, int32_t shard, int32_
 extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
     if (!s) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL solution");
     const tga_instance *I = s->inst;
+    const bool accumulate = (mask & TGA_EVAL_ACCUMULATE) && s->eval_gen == s->gen;
     mask &= TGA_OP_ALL;
     if ((mask & TGA_OP_2OPT) && I->tw)
         return fail(TGA_ERR_UNSUPPORTED, "2-opt is only defined without time windows (P:148)");
     if (set_device(I) != TGA_OK) return TGA_ERR_CUDA;
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s->stream;
-    TGA_CUDA(cudaMemsetAsync(s->keys, 0xFF, TGA_N_VARIANTS * 8, st));
+    if (!accumulate) TGA_CUDA(cudaMemsetAsync(s->keys, 0xFF, TGA_N_VARIANTS * 8, st));
     ScoreParams sp{I->Q, I->opt.score_mode, I->opt.w_load, I->opt.w_tw};
     // row shard of the tile list and of the intra slot range
     const int t_lo = static_cast<int>(static_cast<int64_t>(s->n_tiles) * s->shard / s->n_shards);
@@ -559,8 +577,8 @@ extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
         TGA_CUDA(cudaStreamWaitEvent(s->stream, ev, 0));
         cudaEventDestroy(ev);
     }
+    s->eval_mask = accumulate ? (s->eval_mask | mask) : mask;
     s->eval_gen = s->gen;
-    s->eval_mask = mask;
     return TGA_OK;
 }
 

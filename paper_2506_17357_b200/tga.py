@@ -44,6 +44,7 @@ OP_INTER = 0x7FE
 OP_INTRA = OP_2OPT | OP_INTRA_RELOCATE | OP_INTRA_SWAP
 OP_ALL = (1 << N_VARIANTS) - 1
 OP_FUSED_NS = OP_2OPT_STAR | OP_RELOCATE | OP_SWAP
+EVAL_ACCUMULATE = 1 << 31
 OPERATORS = {"2opt": OP_2OPT, "2opt*": OP_2OPT_STAR, "relocate": OP_RELOCATE, "or-opt": OP_OR_OPT,
              "swap": OP_SWAP, "cross": OP_CROSS, "intra-relocate": OP_INTRA_RELOCATE,
              "intra-swap": OP_INTRA_SWAP}
@@ -89,6 +90,7 @@ _SYMBOLS = {
     "tga_solution_info": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "tga_solution_attributes": (C.c_int32, [C.c_void_p] + [C.c_void_p] * 7),
     "tga_solution_set_shard": (C.c_int32, [C.c_void_p, C.c_int32, C.c_int32]),
+    "tga_solution_set_stream": (C.c_int32, [C.c_void_p, C.c_void_p]),
     "tga_nccl_unique_id": (C.c_int32, [C.c_void_p]),
     "tga_comm_init": (C.c_int32, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
     "tga_last_error": (C.c_char_p, []),
@@ -277,6 +279,10 @@ class Solution:
                                              _p(out["pre_D"]), _p(out["suf_D"]), _p(out["pre_TV"]),
                                              _p(out["suf_TV"]), _p(out["start"])))
         return out
+
+    def set_stream(self, stream) -> None:
+        """Use this cudaStream_t / torch.cuda.Stream for every later call."""
+        _check(lib().tga_solution_set_stream(self._h, _stream_ptr(stream)))
 
     # ---- multi-GPU
     def set_shard(self, shard: int, n_shards: int) -> None:

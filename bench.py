@@ -217,15 +217,9 @@ def run_tga(args):
     def step(evs=None):
         if evs:
             evs[0].record(stream)
-        gs.eval(mask_inter, stream)
+        ok, _ = gs.step(mask_all)   # tga_step: eval (inter + intra) -> best move -> apply
         if evs:
             evs[1].record(stream)
-        gs.eval(mask_intra | T.EVAL_ACCUMULATE, stream)
-        ok, mv = gs.best_move(mask_all)
-        if ok:
-            gs.apply(mv)
-        if evs:
-            evs[2].record(stream)
         return ok
 
     # ---------------- warm-up
@@ -236,7 +230,8 @@ def run_tga(args):
     # ---------------- timed region: K steps, per-step events, L2 flushed between steps
     sampler = ClockSampler(local)
     K = args.steps
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(K)]
+    gs.enable_timing(True)   # CUDA events around the inter-route launch, on its stream
     counts = []
     if ws > 1:
         import torch.distributed as dist
@@ -253,8 +248,9 @@ def run_tga(args):
     torch.cuda.synchronize(dev)
     launches = T.launch_count() - launches0
     clocks = sampler.stop()
-    step_ms = [e[0].elapsed_time(e[2]) for e in evs]
-    inter_ms = [e[0].elapsed_time(e[1]) for e in evs]
+    step_ms = [e[0].elapsed_time(e[1]) for e in evs]
+    inter_ms = [float(x) for x in gs.timings()]
+    gs.enable_timing(False)
     tot_ms = float(sum(step_ms))
     if ws > 1:
         import torch.distributed as dist
@@ -331,23 +327,31 @@ def run_tga(args):
             del g
 
     # ---------------- e2e through the C ABI with host buffers
-    ptr, cust = sol0.flat()
-    e2e_steps = min(K, 20)
+    # each step: tga_solution_reload(host CSR routes of a new solution: H2D of
+    # the routes + slot layout, Dp rebuild, full attribute scan) -> tga_eval(all)
+    # -> tga_best_move (D2H of 8 B per variant); host wall clock, instance resident
+    import tga_gen as G2
+    e2e_sols = [G2.perturb(sol0, 20, 7000 + k).flat() for k in range(8)]
+    e2e_steps = min(K, 40)
+    s2 = T.Solution(gi, sol0)
+    for k in range(3):
+        s2.reload(e2e_sols[k % 8]); s2.eval(mask_all); s2.best_move(mask_all)
     torch.cuda.synchronize(dev)
-    t0 = time.perf_counter()
     e2e_c = 0
-    for _ in range(e2e_steps):
-        s2 = T.Solution(gi, (ptr, cust))          # host -> device: routes, layout, Dp build, scan
+    t0 = time.perf_counter()
+    for k in range(e2e_steps):
+        s2.reload(e2e_sols[k % 8])
         s2.eval(mask_all)
-        s2.best_move(mask_all)                    # device -> host: 8 B per variant
+        s2.best_move(mask_all)
         e2e_c += int(sum(int(x) for v, x in enumerate(s2.counts()) if (mask_all >> v) & 1))
-        s2.close()
     torch.cuda.synchronize(dev)
     e2e_s = time.perf_counter() - t0
+    s2.close()
+    ptr, cust = sol0.flat()
     h2d = 4 * (len(ptr) + len(cust)) + 5 * 4 * (N + 2 * R) + 8 * R
     e2e = {"value": e2e_c / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
            "d2h_bytes_per_step": 23 * 8,
-           "step": "tga_solution_load(host CSR routes) + tga_eval(all) + tga_best_move; "
+           "step": "tga_solution_reload(host CSR routes) + tga_eval(all) + tga_best_move; "
                    "host wall clock, instance resident"}
 
     # ---------------- CPU oracle baseline (rank 0, N=1 only)
@@ -375,7 +379,7 @@ def run_tga(args):
         "per_operator_steady_state": per_op,
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
     }
-    print(json.dumps(line), flush=True)
+    print(json.dumps(line, default=float), flush=True)
     if ws > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

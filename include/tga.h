@@ -186,6 +186,28 @@ int32_t tga_apply_move(tga_solution *sol, const tga_move *move);
  * belong to the solution's device and outlive the solution or the next call. */
 int32_t tga_solution_set_stream(tga_solution *sol, void *cuda_stream);
 
+/* tga_step: one best-improvement iteration of the feasible-and-infeasible
+ * search (Alg. A2 lines 5-8): tga_eval(op_mask) + tga_best_move +
+ * tga_apply_move when the best score is < 0.  out (may be NULL) receives the
+ * move.  Returns TGA_OK if a move was applied, TGA_NO_IMPROVING_MOVE if not. */
+int32_t tga_step(tga_solution *sol, uint32_t op_mask, tga_move *out);
+
+/* tga_solution_reload: load another solution of the same instance into an
+ * existing solution object (same route count and customer count => same
+ * device layout; no allocation): host arrays are copied, the slot layout is
+ * re-uploaded, the distance tile matrix rebuilt and every route re-scanned,
+ * asynchronously on the solution's stream.  Errors: TGA_ERR_STRUCTURE,
+ * TGA_ERR_INVALID_ARGUMENT (different R), TGA_ERR_CUDA. */
+int32_t tga_solution_reload(tga_solution *sol, int32_t n_routes, const int32_t *route_ptr,
+                            const int32_t *customers);
+
+/* Live kernel timing: when enabled, tga_eval records CUDA events around the
+ * inter-route kernel launch on its stream; tga_solution_timings returns (and
+ * clears) up to max_n recorded durations in milliseconds (synchronises).
+ * Returns the number written in *n_out. */
+int32_t tga_solution_enable_timing(tga_solution *sol, int32_t enable);
+int32_t tga_solution_timings(tga_solution *sol, float *ms, int32_t max_n, int32_t *n_out);
+
 /* Per-variant raw keys of the last tga_eval (synchronises). keys[TGA_N_VARIANTS];
  * ~0 = no valid candidate. */
 int32_t tga_solution_keys(tga_solution *sol, uint64_t *keys);
@@ -220,6 +242,9 @@ int32_t tga_solution_attributes(tga_solution *sol, int64_t *pre_L, int64_t *suf_
  * ncclUniqueId shared by all ranks) and makes tga_eval MIN-allreduce the
  * packed keys (exact: keys are (score, canonical index)). */
 int32_t tga_solution_set_shard(tga_solution *sol, int32_t shard, int32_t n_shards);
+/* The row-shard plan (host only): items [lo, hi) of n_items for shard `shard` of
+ * `n_shards` (contiguous, balanced to +-1, disjoint, covering). */
+int32_t tga_shard_range(int64_t n_items, int32_t shard, int32_t n_shards, int64_t *lo, int64_t *hi);
 int32_t tga_nccl_unique_id(void *out_128_bytes);
 int32_t tga_comm_init(tga_solution *sol, int32_t rank, int32_t world, const void *nccl_unique_id);
 

@@ -94,6 +94,29 @@ __device__ __forceinline__ uint64_t score_key(const ScoreParams &sp, bool valid,
     return valid ? pack_key(ord_score(s), idx) : kNoKey;
 }
 
+// ------------------------------------------------------------------ per-slot record (CVRP fast path)
+// Everything the fused inter-route kernel needs about one slot x in one
+// 96-byte record, so a tile row is one bulk copy and a lane's column is six
+// 16-byte loads.  Validity is folded into the load terms: an invalid role
+// carries kPoison in a load that is compared against the capacity, so the
+// candidate fails the capacity test without a branch (feasible-only mode).
+constexpr int32_t kPoison = 1 << 28;
+struct __align__(16) SlotRec {
+    int32_t c;       // canonical id, -1 for an end depot / padding
+    int32_t r;       // route id, -1 for padding
+    int32_t fL;      // prefix load of [0..x]               (2-opt* head),  +P if c < 0
+    int32_t bL1;     // suffix load of [x+1..L+1]            (2-opt* tail),  +P if c < 0
+    int32_t ne;      // -e(x), e(x) = c(x, x+1)
+    int32_t W;       // route load (insertion target),       +P if c < 0
+    int32_t so[3];   // relocate-out load s_N of x..x+N-1,   +P if the segment is invalid or W - s_N > Q
+    int32_t rem[3];  // relocate-out distance c(x-1, x+N) - e(x-1) - e(x+N-1)  (Eq. 2)
+    int32_t sA[3];   // swap: W - s_N,                       +P if the segment is invalid
+    int32_t sS[3];   // swap: s_N
+    int32_t sE[3];   // swap: -e(x-1) - e(x+N-1)
+    int32_t pad[3];
+};
+static_assert(sizeof(SlotRec) == 96, "SlotRec layout");
+
 // ------------------------------------------------------------------ launch-side views
 // Device view of one solution (all arrays indexed by physical slot unless noted).
 template <class DT>

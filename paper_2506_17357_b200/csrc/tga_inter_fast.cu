@@ -1,0 +1,245 @@
+// tga_inter_fast.cu -- fused inter-route sweep, CVRP feasible-only fast path (sm_100a).
+//
+// Same candidate space, scores and keys as k_inter (Fig. `operators`
+// P:107-149; Eq. 2 / 3f; Eq. 16), organised for instruction economy:
+//   * tile = U rows (u) x 128 columns (v); a CTA of 4 warps, lane <-> column;
+//     the warp walks its U rows in canonical order, so a plain strict '<' on a
+//     32-bit score keeps the lowest canonical index per (variant, direction)
+//     stream (reading 5) -- no 64-bit key per candidate;
+//   * the Dp box (rows u0-1..u0+U+2, cols v0-4..v0+131) is one TMA tile load,
+//     the U+4 row records one bulk copy, both double-buffered across the
+//     persistent tile loop on mbarriers;
+//   * every row-only or column-only term (removal gains, segment loads, route
+//     loads, validity) is precomputed in the 96-byte SlotRec; validity is a
+//     poisoned load, so each candidate is: a few adds, one capacity compare,
+//     one select and one compare-and-keep.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <climits>
+#include <cstdint>
+
+#include "tga_device.cuh"
+#include "tga_launch.h"
+
+namespace tga {
+
+namespace {
+__device__ __forceinline__ uint32_t s_u32(const void *p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void f_mbar_init(uint64_t *bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void f_expect(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void f_wait(uint64_t *bar, uint32_t phase) {
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(s_u32(bar)), "r"(phase)
+            : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void f_tma2d(void *dst, const CUtensorMap *map, int x, int y, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+            "r"(s_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(s_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void f_bulk(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     s_u32(dst)),
+                 "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(s_u32(bar))
+                 : "memory");
+}
+
+// running best of one (variant, direction) stream inside a tile: score + the
+// canonical id of the row slot; strict '<' keeps the first (lowest) row.
+struct Run {
+    int32_t s;
+    int32_t c;
+};
+__device__ __forceinline__ void keep(Run &b, bool feas, int32_t dD, int32_t c) {
+    const int32_t s = feas ? dD : INT_MAX;
+    if (s < b.s) { b.s = s; b.c = c; }
+}
+__device__ __forceinline__ void fold(uint64_t &acc, const Run &b, bool direct, uint32_t cv, uint32_t Qc) {
+    if (b.s != INT_MAX) {
+        const uint32_t idx = direct ? static_cast<uint32_t>(b.c) * Qc + cv : cv * Qc + static_cast<uint32_t>(b.c);
+        acc = umin64(acc, pack_key(ord_score(b.s), idx));
+    }
+}
+}  // namespace
+
+// stream slots: 0 2opt* | 1,2 reloc1 d/r | 3,4 oropt2 | 5,6 oropt3 | 7 swap11 |
+// 8,9 cross12 | 10,11 cross13 | 12 cross22 | 13,14 cross23 | 15 cross33
+template <uint32_t MASK>
+__global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__restrict__ rec,
+                                                             const __grid_constant__ CUtensorMap tmap,
+                                                             const uint32_t *__restrict__ tiles, int t_lo, int t_hi,
+                                                             uint32_t Qc, int32_t cap, uint64_t *__restrict__ keys) {
+    constexpr int U = kFastU, BW = kFastBoxW;
+    constexpr int NV = 11;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char *sm = smem_raw + ((128u - (s_u32(smem_raw) & 127u)) & 127u);
+    int32_t *const dp0 = reinterpret_cast<int32_t *>(sm);
+    int32_t *const dp1 = reinterpret_cast<int32_t *>(sm + kFastBoxBytesPadded);
+    SlotRec *const rows0 = reinterpret_cast<SlotRec *>(sm + 2 * kFastBoxBytesPadded);
+    SlotRec *const rows1 = reinterpret_cast<SlotRec *>(sm + 2 * kFastBoxBytesPadded + kFastRowBytesPadded);
+    __shared__ uint64_t bar[2];
+    __shared__ unsigned long long red[NV];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) {
+        f_mbar_init(&bar[0]);
+        f_mbar_init(&bar[1]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (tid < NV) red[tid] = kNoKey;
+    __syncthreads();
+
+    uint64_t acc[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) acc[i] = kNoKey;
+
+    auto issue = [&](int t, int b) {
+        const uint32_t ij = tiles[t];
+        const int I = ij >> 16, J = ij & 0xFFFF;
+        uint64_t *br = b ? &bar[1] : &bar[0];
+        f_expect(br, kFastBoxBytes + U * 96);
+        f_tma2d(b ? dp1 : dp0, &tmap, J * kFastTV - 4, I * U - 1, br);
+        f_bulk(b ? rows1 : rows0, rec + I * U, U * 96, br);
+    };
+
+    int t = t_lo + blockIdx.x;
+    if (tid == 0 && t < t_hi) issue(t, 0);
+    uint32_t ph0 = 0u, ph1 = 0u;
+    for (int it = 0; t < t_hi; t += gridDim.x, ++it) {
+        const int b = it & 1;
+        if (tid == 0 && t + static_cast<int>(gridDim.x) < t_hi) issue(t + gridDim.x, b ^ 1);
+        const uint32_t ij = tiles[t];
+        const int u0 = (ij >> 16) * U, v0 = (ij & 0xFFFF) * kFastTV;
+        const int col = warp * 32 + lane;   // column inside the tile
+        const int v = v0 + col;
+        // ---- this lane's column record (six 16-byte loads; overlaps the TMA)
+        const SlotRec V = rec[v];
+        if (b) { f_wait(&bar[1], ph1); ph1 ^= 1u; } else { f_wait(&bar[0], ph0); ph0 ^= 1u; }
+        const int32_t *T = b ? dp1 : dp0;
+        const SlotRec *RW = b ? rows1 : rows0;
+        // Dp(u0 + i + di, v + dj), i = row index in the tile
+        auto D = [&](int i, int di, int dj) -> int32_t { return T[(i + 1 + di) * BW + (col + 4 + dj)]; };
+
+        Run run[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) run[k] = Run{INT_MAX, 0};
+
+#pragma unroll
+        for (int i = 0; i < U; ++i) {
+            const SlotRec &A = RW[i];       // row u = u0 + i (broadcast reads)
+            const int32_t cu = A.c, ru = A.r;
+            if (cu < 0) continue;            // warp-uniform: end depot / padding row
+            if (!(ru < V.r)) continue;       // pair must span two routes, route(u) < route(v)
+            // ---- 2-opt*: A' = F(u) + B(v+1), B' = F(v) + B(u+1)    (Eq. 14)
+            if (MASK & (1u << 1)) {
+                const int32_t dD = D(i, 0, 1) + D(i, 1, 0) + A.ne + V.ne;
+                const int32_t la = A.fL + V.bL1, lb = V.fL + A.bL1;
+                keep(run[0], max(la, lb) <= cap, dD, cu);
+            }
+            // ---- relocate / or-opt, both directions                   (Eq. 13)
+#pragma unroll
+            for (int N = 1; N <= 3; ++N) {
+                if (!(MASK & (1u << (1 + N)))) continue;
+                const int32_t d1 = A.rem[N - 1] + D(i, 0, 0) + D(i, N - 1, 1) + V.ne;  // seg(u) after v
+                keep(run[2 * N - 1], V.W + A.so[N - 1] <= cap, d1, cu);
+                const int32_t d2 = V.rem[N - 1] + D(i, 0, 0) + D(i, 1, N - 1) + A.ne;  // seg(v) after u
+                keep(run[2 * N], A.W + V.so[N - 1] <= cap, d2, cu);
+            }
+            // ---- swap (1,1) / cross-exchange (N1,N2), N1 <= N2
+#pragma unroll
+            for (int sv = 0; sv < 6; ++sv) {
+                constexpr int n1s[6] = {1, 1, 1, 2, 2, 3}, n2s[6] = {1, 2, 3, 2, 3, 3};
+                constexpr int slot[6] = {7, 8, 10, 12, 13, 15};
+                const int N1 = n1s[sv], N2 = n2s[sv];
+                if (!(MASK & (1u << (5 + sv)))) continue;
+                {   // N1-segment at u, N2-segment at v
+                    const int32_t dD = D(i, -1, 0) + D(i, N1, N2 - 1) + D(i, 0, -1) + D(i, N1 - 1, N2) +
+                                       A.sE[N1 - 1] + V.sE[N2 - 1];
+                    const int32_t la = A.sA[N1 - 1] + V.sS[N2 - 1], lb = V.sA[N2 - 1] + A.sS[N1 - 1];
+                    keep(run[slot[sv]], max(la, lb) <= cap, dD, cu);
+                }
+                if (N1 != N2) {   // N1-segment at v, N2-segment at u
+                    const int32_t dD = D(i, 0, -1) + D(i, N2 - 1, N1) + D(i, -1, 0) + D(i, N2, N1 - 1) +
+                                       V.sE[N1 - 1] + A.sE[N2 - 1];
+                    const int32_t lb = V.sA[N1 - 1] + A.sS[N2 - 1], la = A.sA[N2 - 1] + V.sS[N1 - 1];
+                    keep(run[slot[sv] + 1], max(la, lb) <= cap, dD, cu);
+                }
+            }
+        }
+        // ---- fold this tile's streams into the per-variant 64-bit keys
+        if (V.c >= 0) {
+            const uint32_t cv = static_cast<uint32_t>(V.c);
+            if (MASK & (1u << 1)) fold(acc[1], run[0], true, cv, Qc);
+#pragma unroll
+            for (int N = 1; N <= 3; ++N) {
+                if (!(MASK & (1u << (1 + N)))) continue;
+                fold(acc[1 + N], run[2 * N - 1], true, cv, Qc);
+                fold(acc[1 + N], run[2 * N], false, cv, Qc);
+            }
+            if (MASK & (1u << 5)) fold(acc[5], run[7], true, cv, Qc);
+            if (MASK & (1u << 6)) { fold(acc[6], run[8], true, cv, Qc); fold(acc[6], run[9], false, cv, Qc); }
+            if (MASK & (1u << 7)) { fold(acc[7], run[10], true, cv, Qc); fold(acc[7], run[11], false, cv, Qc); }
+            if (MASK & (1u << 8)) fold(acc[8], run[12], true, cv, Qc);
+            if (MASK & (1u << 9)) { fold(acc[9], run[13], true, cv, Qc); fold(acc[9], run[14], false, cv, Qc); }
+            if (MASK & (1u << 10)) fold(acc[10], run[15], true, cv, Qc);
+        }
+        __syncthreads();  // buffer b is refilled two iterations later
+    }
+
+    // ---- fused argmin: warp shuffle -> shared -> one 64-bit atomicMin per variant per CTA
+#pragma unroll
+    for (int i = 1; i < NV; ++i) {
+        if (!(MASK & (1u << i))) continue;
+        const uint64_t k = warp_min64(acc[i]);
+        if (lane == 0 && k != kNoKey) atomicMin(&red[i], static_cast<unsigned long long>(k));
+    }
+    __syncthreads();
+    if (tid < NV && (MASK & (1u << tid)) && red[tid] != kNoKey)
+        atomicMin(reinterpret_cast<unsigned long long *>(keys) + tid, red[tid]);
+}
+
+template <uint32_t MASK>
+static cudaError_t launch_fast_t(const SlotRec *rec, const CUtensorMap &map, const uint32_t *tiles, int t_lo, int t_hi,
+                                 uint32_t Qc, int32_t cap, uint64_t *keys, int grid, cudaStream_t st) {
+    auto kern = k_inter_fast<MASK>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kFastSmem);
+        attr = true;
+    }
+    kern<<<grid, kFastThreads, kFastSmem, st>>>(rec, map, tiles, t_lo, t_hi, Qc, cap, keys);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_inter_fast(uint32_t mask, const SlotRec *rec, const CUtensorMap &map, const uint32_t *tiles, int t_lo,
+                              int t_hi, uint32_t Qc, int32_t cap, uint64_t *keys, int grid, cudaStream_t st) {
+    if (t_hi <= t_lo || !(mask & 0x7FEu)) return cudaSuccess;
+    cudaError_t err = cudaSuccess;
+    auto run = [&](auto kmask) {
+        if (err == cudaSuccess)
+            err = launch_fast_t<decltype(kmask)::value>(rec, map, tiles, t_lo, t_hi, Qc, cap, keys, grid, st);
+    };
+    constexpr uint32_t ALL = 0x7FEu, NS = (1u << 1) | (1u << 2) | (1u << 5);
+    if ((mask & ALL) == ALL) { run(std::integral_constant<uint32_t, ALL>{}); return err; }
+    if ((mask & NS) == NS) { run(std::integral_constant<uint32_t, NS>{}); mask &= ~NS; }
+    if (mask & (1u << 1)) run(std::integral_constant<uint32_t, (1u << 1)>{});
+    if (mask & (1u << 2)) run(std::integral_constant<uint32_t, (1u << 2)>{});
+    if (mask & (3u << 3)) run(std::integral_constant<uint32_t, (3u << 3)>{});
+    if (mask & (1u << 5)) run(std::integral_constant<uint32_t, (1u << 5)>{});
+    if (mask & (0x1Fu << 6)) run(std::integral_constant<uint32_t, (0x1Fu << 6)>{});
+    return err;
+}
+
+}  // namespace tga

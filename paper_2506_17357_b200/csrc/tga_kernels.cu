@@ -52,10 +52,7 @@ __global__ void __launch_bounds__(256) k_dp_cols(DT *__restrict__ Dp, int pitch,
 // One warp per route; chunks of 32 positions with carries.  Positions
 // k = 0..L+1 of route r live at physical slots base..base+L+1.
 template <class DT, bool TW>
-__global__ void __launch_bounds__(256) k_scan(ScanArgs<DT> A, int r_lo, int r_hi) {
-    const int lane = threadIdx.x & 31;
-    const int r = r_lo + static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-    if (r >= r_hi) return;
+__device__ __forceinline__ void scan_route(const ScanArgs<DT> &A, const int r, const int lane) {
     const int base = A.rbase[r];
     const int L = A.rlenR[r];
     const int len = L + 2;
@@ -180,6 +177,8 @@ __global__ void __launch_bounds__(256) k_scan(ScanArgs<DT> A, int r_lo, int r_hi
         }
     }
     if (lane == 0) A.rD[r] = bcarryD;
+    const int Wr = carryL;  // route load (Eq. 3f over the whole route)
+    __syncwarp();           // fwdL / bwdL / enext of this route are visible to the whole warp
 
     // ---------------- per-position segment records and bridges (N = 1..3)
     for (int k = lane; k < len; k += 32) {
@@ -205,6 +204,76 @@ __global__ void __launch_bounds__(256) k_scan(ScanArgs<DT> A, int r_lo, int r_hi
             A.seg2T[x] = s2;
             A.seg3T[x] = s3;
         }
+        if constexpr (std::is_same<DT, int32_t>::value) {
+            if (A.rec) {
+                SlotRec q;
+                const bool slot = k <= L;  // canonical slot (not the end depot)
+                const int32_t e_x = A.enext[x], e_prev = (k >= 1) ? A.enext[x - 1] : 0;
+                const int32_t fl_prev = (k >= 1) ? A.fwdL[x - 1] : 0;
+                q.c = slot ? A.canon[x] : -1;
+                q.r = r;
+                q.fL = slot ? A.fwdL[x] : kPoison;
+                q.bL1 = (slot && k + 1 < len) ? A.bwdL[x + 1] : kPoison;
+                q.ne = -e_x;
+                q.W = slot ? Wr : kPoison;
+                const DT br[3] = {b1, b2, b3};
+#pragma unroll
+                for (int N = 1; N <= 3; ++N) {
+                    const bool segok = (k >= 1) && (k + N - 1 <= L);
+                    const int32_t sN = segok ? A.fwdL[x + N - 1] - fl_prev : 0;
+                    const int32_t eout = segok ? A.enext[x + N - 1] : 0;
+                    q.so[N - 1] = (segok && Wr - sN <= A.capacity) ? sN : kPoison;
+                    q.rem[N - 1] = segok ? br[N - 1] - e_prev - eout : 0;
+                    q.sA[N - 1] = segok ? Wr - sN : kPoison;
+                    q.sS[N - 1] = sN;
+                    q.sE[N - 1] = segok ? -e_prev - eout : 0;
+                }
+                q.pad[0] = q.pad[1] = q.pad[2] = 0;
+                A.rec[x] = q;
+            }
+        }
+    }
+}
+
+template <class DT, bool TW>
+__global__ void __launch_bounds__(256) k_scan(ScanArgs<DT> A, int r_lo, int r_hi) {
+    const int lane = threadIdx.x & 31;
+    const int r = r_lo + static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    if (r >= r_hi) return;
+    scan_route<DT, TW>(A, r, lane);
+}
+
+// The update step of an applied move in ONE launch: blocks
+// [0, nb_rows) refresh Dp rows [lo, hi), blocks [nb_rows, nb_rows + nb_cols)
+// refresh Dp columns [lo, hi) of rows [0, Qp), the rest re-scan routes
+// [r_lo, r_hi) (the scan reads node ids and C, never Dp, so the roles are
+// independent).
+template <class DT, bool TW>
+__global__ void __launch_bounds__(256) k_update(ScanArgs<DT> A, DT *__restrict__ Dp, int pitch, int Qp, int lo, int hi,
+                                                int r_lo, int r_hi, int nb_rows, int nb_cols) {
+    const int b = blockIdx.x;
+    const DT *__restrict__ C = A.C;
+    const int n = A.n_nodes;
+    if (b < nb_rows) {
+        const int a = lo + b;
+        const DT *crow = C + static_cast<size_t>(A.node[a]) * n;
+        DT *drow = Dp + static_cast<size_t>(a) * pitch;
+        for (int c = 4 * threadIdx.x; c < pitch; c += 4 * blockDim.x) {
+            const int4 nd = *reinterpret_cast<const int4 *>(A.node + c);
+            *reinterpret_cast<int4 *>(drow + c) =
+                make_int4(bits(__ldg(crow + nd.x)), bits(__ldg(crow + nd.y)), bits(__ldg(crow + nd.z)),
+                          bits(__ldg(crow + nd.w)));
+        }
+    } else if (b < nb_rows + nb_cols) {
+        const int a = (b - nb_rows) * 8 + (threadIdx.x >> 5);
+        if (a < Qp) {
+            const DT *crow = C + static_cast<size_t>(A.node[a]) * n;
+            DT *drow = Dp + static_cast<size_t>(a) * pitch;
+            for (int c = lo + (threadIdx.x & 31); c < hi; c += 32) drow[c] = __ldg(crow + A.node[c]);
+        }
+    } else {
+        const int r = r_lo + (b - nb_rows - nb_cols) * 8 + static_cast<int>(threadIdx.x >> 5);
+        if (r < r_hi) scan_route<DT, TW>(A, r, threadIdx.x & 31);
     }
 }
 
@@ -557,9 +626,94 @@ __global__ void __launch_bounds__(256) k_intra(const SolView<DT> S, ScoreParams 
         atomicMin(reinterpret_cast<unsigned long long *>(keys) + threadIdx.x, red[threadIdx.x]);
 }
 
+// ============================================================== intra-route evaluation, CVRP
+// No time windows => no sequential middle segment: every (u, v) pair of a route
+// is independent.  A warp owns one u slot, lane <-> v position (strided by 32);
+// per variant the warp argmin is one 32-bit REDUX.MIN of (score << 5 | lane):
+// lanes hold consecutive canonical v, so the lowest lane is the lowest index.
+// Loads are unchanged by intra moves (Eq. 3f), so feasibility is the route's.
+__device__ __forceinline__ uint32_t intra_k32(bool ok, int32_t dD, int lane) {
+    // dD is bounded by 8 * max c < 2^25 (host-checked: max c < 2^21)
+    return ok ? ((static_cast<uint32_t>(dD + (1 << 25)) << 5) | static_cast<uint32_t>(lane)) : 0xFFFFFFFFu;
+}
+__device__ __forceinline__ void warp_keep(unsigned long long *red, int var, uint32_t k32, uint32_t idx_base, int lane) {
+    const uint32_t m = __reduce_min_sync(0xffffffffu, k32);
+    if (lane == 0 && m != 0xFFFFFFFFu) {
+        const int32_t s = static_cast<int32_t>(m >> 5) - (1 << 25);
+        atomicMin(&red[var], static_cast<unsigned long long>(pack_key(ord_score(s), idx_base + (m & 31u))));
+    }
+}
+
+__global__ void __launch_bounds__(256) k_intra_cvrp(const SolView<int32_t> S, ScoreParams sp, uint32_t vmask,
+                                                    int x_lo, int x_hi, uint64_t *__restrict__ keys) {
+    __shared__ unsigned long long red[23];
+    if (threadIdx.x < 23) red[threadIdx.x] = kNoKey;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int x = x_lo + static_cast<int>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    if (x < x_hi && S.canon[x] >= 0 && S.pos[x] >= 1) {   // warp-uniform
+        const int p = S.pos[x], L = S.rlen[x], r = S.route[x];
+        const int base = x - p;
+        const bool ok_route = sp.mode == 1 || S.rW[r] <= sp.capacity;
+        const uint32_t cu = static_cast<uint32_t>(S.canon[x]);
+        const uint32_t cbase = cu - static_cast<uint32_t>(p);
+        auto D = [&](int a, int b) -> int32_t { return __ldg(S.Dp + static_cast<size_t>(a) * S.pitch + b); };
+        const int32_t em = S.enext[x - 1];
+        int32_t eo[3], rem[3];
+#pragma unroll
+        for (int N = 1; N <= 3; ++N) {
+            eo[N - 1] = S.enext[min(x + N - 1, base + L + 1)];
+            const int32_t br = N == 1 ? S.bridge1[x] : (N == 2 ? S.bridge2[x] : S.bridge3[x]);
+            rem[N - 1] = br - em - eo[N - 1];
+        }
+        for (int qb = 0; qb <= L; qb += 32) {
+            const int q = qb + lane;
+            const bool in = q <= L;
+            const int v = base + min(q, L);
+            const int vm1 = max(v - 1, base);          // masked lanes (q = 0) must still read a valid row
+            const uint32_t ib = cu * S.Qc + cbase + static_cast<uint32_t>(qb);
+            const int32_t ev = S.enext[v], evm = (q >= 1 && in) ? S.enext[v - 1] : 0;
+            // phase 1: every variant's 32-bit key in registers (all loads issued together)
+            uint32_t k[23];
+#pragma unroll
+            for (int i = 0; i < 23; ++i) k[i] = 0xFFFFFFFFu;
+            if (vmask & 1u)   // 2-opt: reverse u..v
+                k[0] = intra_k32(ok_route && in && q > p, D(x - 1, v) + D(x, v + 1) - em - ev, lane);
+#pragma unroll
+            for (int N = 1; N <= 3; ++N) {  // intra relocate / or-opt
+                if (!(vmask & (1u << (10 + N)))) continue;
+                const bool ok = ok_route && in && p + N - 1 <= L && (q < p - 1 || q > p + N - 1);
+                k[10 + N] = intra_k32(ok, rem[N - 1] + D(v, x) + D(x + N - 1, v + 1) - ev, lane);
+            }
+#pragma unroll
+            for (int a = 1; a <= 3; ++a) {   // intra swap (N1 = a at u, N2 = b at v), u + N1 <= v
+#pragma unroll
+                for (int b = 1; b <= 3; ++b) {
+                    const int var = 14 + 3 * (a - 1) + (b - 1);
+                    if (!(vmask & (1u << var))) continue;
+                    const bool ok = ok_route && in && q >= p + a && q + b - 1 <= L;
+                    const int32_t ev2 = S.enext[min(v + b - 1, base + L + 1)];
+                    const int32_t adj = D(x - 1, v) + D(v + b - 1, x) + D(x + a - 1, v + b) - em - evm - ev2;
+                    const int32_t gap = D(x - 1, v) + D(v + b - 1, x + a) + D(vm1, x) + D(x + a - 1, v + b) - em -
+                                        eo[a - 1] - evm - ev2;
+                    k[var] = intra_k32(ok, q == p + a ? adj : gap, lane);
+                }
+            }
+            // phase 2: one REDUX.MIN per variant
+#pragma unroll
+            for (int i = 0; i < 23; ++i)
+                if ((i == 0 || i >= 11) && (vmask & (1u << i))) warp_keep(red, i, k[i], ib, lane);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < 23 && red[threadIdx.x] != kNoKey)
+        atomicMin(reinterpret_cast<unsigned long long *>(keys) + threadIdx.x, red[threadIdx.x]);
+}
+
 // ============================================================== launchers
 static unsigned long long g_launches = 0;
 unsigned long long launch_count() { return g_launches; }
+void note_launch() { ++g_launches; }
 
 template <class DT>
 cudaError_t launch_dp(DT *Dp, int pitch, const int32_t *node, const DT *C, int n, int Qp, int lo, int hi,
@@ -588,6 +742,22 @@ cudaError_t launch_scan(const ScanArgs<DT> &A, bool tw, int r_lo, int r_hi, cuda
     ++g_launches;
     return cudaGetLastError();
 }
+
+template <class DT>
+cudaError_t launch_update(const ScanArgs<DT> &A, bool tw, DT *Dp, int pitch, int Qp, int lo, int hi, int r_lo,
+                          int r_hi, cudaStream_t st) {
+    const int nb_rows = hi - lo, nb_cols = (Qp + 7) / 8, nb_scan = (r_hi - r_lo + 7) / 8;
+    const int grid = nb_rows + nb_cols + nb_scan;
+    if (grid <= 0) return cudaSuccess;
+    if (tw) k_update<DT, true><<<grid, 256, 0, st>>>(A, Dp, pitch, Qp, lo, hi, r_lo, r_hi, nb_rows, nb_cols);
+    else    k_update<DT, false><<<grid, 256, 0, st>>>(A, Dp, pitch, Qp, lo, hi, r_lo, r_hi, nb_rows, nb_cols);
+    ++g_launches;
+    return cudaGetLastError();
+}
+template cudaError_t launch_update<int32_t>(const ScanArgs<int32_t> &, bool, int32_t *, int, int, int, int, int, int,
+                                            cudaStream_t);
+template cudaError_t launch_update<float>(const ScanArgs<float> &, bool, float *, int, int, int, int, int, int,
+                                          cudaStream_t);
 
 template <class DT, bool TW, uint32_t MASK>
 static cudaError_t launch_inter_t(const SolView<DT> &S, const CUtensorMap &map, const uint32_t *tiles, int t_lo,
@@ -635,9 +805,17 @@ cudaError_t launch_inter(uint32_t mask, bool tw, const SolView<DT> &S, const CUt
 
 template <class DT>
 cudaError_t launch_intra(uint32_t mask, bool tw, const SolView<DT> &S, const ScoreParams &sp, int x_lo, int x_hi,
-                         uint64_t *keys, cudaStream_t st) {
+                         uint64_t *keys, cudaStream_t st, bool small_dist) {
     const uint32_t intra = mask & ((1u << 0) | (0x7u << 11) | (0x1FFu << 14));
     if (x_hi <= x_lo || !intra) return cudaSuccess;
+    if constexpr (std::is_same<DT, int32_t>::value) {
+        if (!tw && small_dist) {
+            const int blocks = (x_hi - x_lo + 7) / 8;
+            k_intra_cvrp<<<blocks, 256, 0, st>>>(S, sp, intra, x_lo, x_hi, keys);
+            ++g_launches;
+            return cudaGetLastError();
+        }
+    }
     const int threads = (x_hi - x_lo) * 13;
     const int blocks = (threads + 255) / 256;
     if (tw) k_intra<DT, true><<<blocks, 256, 0, st>>>(S, sp, intra, x_lo, x_hi, keys);
@@ -659,8 +837,8 @@ template cudaError_t launch_inter<int32_t>(uint32_t, bool, const SolView<int32_t
 template cudaError_t launch_inter<float>(uint32_t, bool, const SolView<float> &, const CUtensorMap &, const uint32_t *,
                                          int, int, const ScoreParams &, uint64_t *, int, cudaStream_t);
 template cudaError_t launch_intra<int32_t>(uint32_t, bool, const SolView<int32_t> &, const ScoreParams &, int, int,
-                                           uint64_t *, cudaStream_t);
+                                           uint64_t *, cudaStream_t, bool);
 template cudaError_t launch_intra<float>(uint32_t, bool, const SolView<float> &, const ScoreParams &, int, int,
-                                         uint64_t *, cudaStream_t);
+                                         uint64_t *, cudaStream_t, bool);
 
 }  // namespace tga

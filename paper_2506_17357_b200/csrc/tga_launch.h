@@ -22,7 +22,18 @@ constexpr int kBoxX0 = 4;                       // columns left of v0 in the box
 constexpr int kBoxH = kTileU + 4;               // Dp box rows:    u0-1 .. u0+TU+2
 constexpr int kBoxBytes = kBoxW * kBoxH * 4;
 constexpr int kBoxBytesPadded = (kBoxBytes + 127) / 128 * 128;
-constexpr int kPitchAlign = 64;                 // Dp pitch: multiple of lcm(TU, TV)
+constexpr int kPitchAlign = 128;                // Dp pitch: multiple of every tile width
+
+// CVRP fast path (k_inter_fast): 4 warps, tile = kFastU rows x 128 columns
+constexpr int kFastThreads = 128;
+constexpr int kFastU = 16;
+constexpr int kFastTV = 128;
+constexpr int kFastBoxW = kFastTV + 8;          // cols v0-4 .. v0+131 (16-byte aligned TMA x)
+constexpr int kFastBoxH = kFastU + 4;           // rows u0-1 .. u0+U+2
+constexpr int kFastBoxBytes = kFastBoxW * kFastBoxH * 4;
+constexpr int kFastBoxBytesPadded = (kFastBoxBytes + 127) / 128 * 128;
+constexpr int kFastRowBytesPadded = (kFastU * 96 + 127) / 128 * 128;
+constexpr int kFastSmem = 2 * kFastBoxBytesPadded + 2 * kFastRowBytesPadded + 128;
 constexpr int kGuard = 8;                       // guard slots before/after every slot array
 
 template <class DT>
@@ -40,11 +51,17 @@ struct ScanArgs {
     int32_t *rW;
     float *rTV;
     DT *rD;
+    const int32_t *canon;
+    int32_t capacity;
+    SlotRec *rec;      // CVRP fast-path records (int DT only); may be null
 };
 
 template <class DT>
 cudaError_t launch_dp(DT *Dp, int pitch, const int32_t *node, const DT *C, int n, int Qp, int lo, int hi,
                       bool full, cudaStream_t st);
+template <class DT>
+cudaError_t launch_update(const ScanArgs<DT> &A, bool tw, DT *Dp, int pitch, int Qp, int lo, int hi, int r_lo,
+                          int r_hi, cudaStream_t st);
 template <class DT>
 cudaError_t launch_scan(const ScanArgs<DT> &A, bool tw, int r_lo, int r_hi, cudaStream_t st);
 template <class DT>
@@ -52,7 +69,10 @@ cudaError_t launch_inter(uint32_t mask, bool tw, const SolView<DT> &S, const CUt
                          int t_lo, int t_hi, const ScoreParams &sp, uint64_t *keys, int grid, cudaStream_t st);
 template <class DT>
 cudaError_t launch_intra(uint32_t mask, bool tw, const SolView<DT> &S, const ScoreParams &sp, int x_lo, int x_hi,
-                         uint64_t *keys, cudaStream_t st);
+                         uint64_t *keys, cudaStream_t st, bool small_dist = false);
 unsigned long long launch_count();
+void note_launch();
+cudaError_t launch_inter_fast(uint32_t mask, const SlotRec *rec, const CUtensorMap &map, const uint32_t *tiles, int t_lo,
+                              int t_hi, uint32_t Qc, int32_t cap, uint64_t *keys, int grid, cudaStream_t st);
 
 }  // namespace tga

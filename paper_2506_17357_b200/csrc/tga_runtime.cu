@@ -103,6 +103,7 @@ struct tga_instance {
     std::vector<int32_t> hDemand;
     std::vector<float> hTw;
     int max_c_abs = 0;
+    bool fast_ok = false;  // loads small enough for the poisoned-load fast path
 };
 
 struct tga_solution {
@@ -126,8 +127,16 @@ struct tga_solution {
     int n_tiles = 0;
     CUtensorMap tmap{};
     bool tmap_ok = false;
+    // CVRP fast path: per-slot records, its own tile plan and TMA box
+    SlotRec *rec = nullptr;
+    uint32_t *d_ftiles = nullptr;
+    int n_ftiles = 0;
+    CUtensorMap fmap{};
+    bool fast = false;
     uint64_t *h_keys = nullptr;                         // pinned
-    int32_t *h_stage = nullptr;                         // pinned staging (5 * cap int32)
+    int32_t *h_stage = nullptr;                         // pinned staging: 5 rows of lay_pitch bytes
+    int32_t *h_rstage = nullptr;                        // pinned staging: 2 rows of route_pitch bytes
+    size_t lay_pitch = 0, route_pitch = 0;              // arena pitch of the slot / route arrays
     cudaStream_t stream = nullptr;                     // current stream (own or user's)
     cudaStream_t own_stream = nullptr;
     int shard = 0, n_shards = 1;
@@ -135,6 +144,10 @@ struct tga_solution {
     int sm_count = 148;
     uint64_t eval_gen = 0;
     uint32_t eval_mask = 0;
+    // live timing of the inter-route launch (ring of event pairs)
+    bool timing = false;
+    std::vector<cudaEvent_t> tev;
+    int tev_n = 0;
 };
 
 // ============================================================== helpers
@@ -165,12 +178,13 @@ static void compute_bases(tga_solution *s) {
     s->cbase[s->R] = cb;
 }
 
-// Fill the 5 layout arrays (node, route, pos, rlen, canon) for routes r_lo..r_hi
-// into the pinned staging buffer, at offsets relative to slot rbase[r_lo].
+// Fill the 5 layout arrays (node, route, pos, rlen, canon) of routes r_lo..r_hi
+// into the pinned staging rows (row pitch = the arena pitch of those arrays),
+// relative to slot rbase[r_lo], plus the per-route (rbase, rlen) rows.
 static void stage_layout(tga_solution *s, int r_lo, int r_hi, int *span_lo, int *span_n) {
     const int lo = s->rbase[r_lo], hi = s->rbase[r_hi + 1];
-    const int n = hi - lo;
-    int32_t *nd = s->h_stage, *rt = nd + s->cap, *ps = rt + s->cap, *rl = ps + s->cap, *cn = rl + s->cap;
+    const size_t rp = s->lay_pitch / 4;
+    int32_t *nd = s->h_stage, *rt = nd + rp, *ps = rt + rp, *rl = ps + rp, *cn = rl + rp;
     for (int r = r_lo; r <= r_hi; ++r) {
         const int L = static_cast<int>(s->routes[r].size());
         for (int p = 0; p <= L + 1; ++p) {
@@ -182,23 +196,26 @@ static void stage_layout(tga_solution *s, int r_lo, int r_hi, int *span_lo, int 
             cn[i] = (p <= L) ? s->cbase[r] + p : -1;
         }
     }
+    const size_t rq = s->route_pitch / 4;
+    int32_t *rb = s->h_rstage, *rn = rb + rq;
+    for (int r = 0; r < s->R; ++r) {
+        rb[r] = s->rbase[r];
+        rn[r] = static_cast<int32_t>(s->routes[r].size());
+    }
     *span_lo = lo;
-    *span_n = n;
+    *span_n = hi - lo;
 }
 
+// Two asynchronous 2-D copies (5 slot arrays of the changed span, 2 route
+// arrays); no host synchronisation -- the staging buffers are reused only after
+// the stream has drained (tga_apply_move synchronises on entry).
 static int32_t upload_layout(tga_solution *s, int r_lo, int r_hi) {
     int lo, n;
     stage_layout(s, r_lo, r_hi, &lo, &n);
-    int32_t *dst[5] = {s->node, s->route, s->pos, s->rlen, s->canon};
-    for (int k = 0; k < 5; ++k)
-        TGA_CUDA(cudaMemcpyAsync(dst[k] + lo, s->h_stage + static_cast<size_t>(k) * s->cap, sizeof(int32_t) * n,
-                                 cudaMemcpyHostToDevice, s->stream));
-    std::vector<int32_t> rl(s->R);
-    for (int r = 0; r < s->R; ++r) rl[r] = static_cast<int32_t>(s->routes[r].size());
-    // per-route arrays are tiny: upload whole (synchronous copies from pageable memory)
-    TGA_CUDA(cudaMemcpyAsync(s->d_rbase, s->rbase.data(), sizeof(int32_t) * s->R, cudaMemcpyHostToDevice, s->stream));
-    TGA_CUDA(cudaMemcpyAsync(s->d_rlenR, rl.data(), sizeof(int32_t) * s->R, cudaMemcpyHostToDevice, s->stream));
-    TGA_CUDA(cudaStreamSynchronize(s->stream));  // pageable sources must outlive the copies
+    TGA_CUDA(cudaMemcpy2DAsync(s->node + lo, s->lay_pitch, s->h_stage, s->lay_pitch, sizeof(int32_t) * n, 5,
+                               cudaMemcpyHostToDevice, s->stream));
+    TGA_CUDA(cudaMemcpy2DAsync(s->d_rbase, s->route_pitch, s->h_rstage, s->route_pitch, sizeof(int32_t) * s->R, 2,
+                               cudaMemcpyHostToDevice, s->stream));
     return TGA_OK;
 }
 
@@ -227,6 +244,9 @@ static ScanArgs<DT> scan_args(tga_solution *s) {
     a.rW = s->d_rW;
     a.rTV = s->d_rTV;
     a.rD = static_cast<DT *>(s->d_rD);
+    a.canon = s->canon;
+    a.capacity = s->inst->Q;
+    a.rec = s->rec;
     return a;
 }
 
@@ -263,6 +283,16 @@ static int32_t refresh(tga_solution *s, int r_lo, int r_hi, bool full) {
     const int lo = full ? 0 : s->rbase[r_lo];
     const int hi = full ? s->pitch : s->rbase[r_hi + 1];
     cudaError_t e;
+    if (!full) {  // update step of one applied move: one launch (Dp rows + columns + re-scan)
+        if (I->dtype == TGA_I32)
+            e = launch_update<int32_t>(scan_args<int32_t>(s), I->tw, static_cast<int32_t *>(s->Dp), s->pitch, s->Qp,
+                                       lo, hi, r_lo, r_hi + 1, s->stream);
+        else
+            e = launch_update<float>(scan_args<float>(s), I->tw, static_cast<float *>(s->Dp), s->pitch, s->Qp, lo, hi,
+                                     r_lo, r_hi + 1, s->stream);
+        if (e != cudaSuccess) return fail(TGA_ERR_CUDA, std::string("update: ") + cudaGetErrorString(e));
+        return TGA_OK;
+    }
     if (I->dtype == TGA_I32) {
         e = launch_dp<int32_t>(static_cast<int32_t *>(s->Dp), s->pitch, s->node, static_cast<const int32_t *>(I->dC),
                                I->n, s->Qp, lo, hi, full, s->stream);
@@ -289,6 +319,13 @@ static void build_tiles(tga_solution *s) {
     }
     s->n_tiles = static_cast<int>(t.size());
     cudaMemcpy(s->d_tiles, t.data(), sizeof(uint32_t) * t.size(), cudaMemcpyHostToDevice);
+    // fast-path plan: kFastU x kFastTV tiles of the upper triangle
+    std::vector<uint32_t> f;
+    for (int I = 0; I < s->pitch / kFastU && I * kFastU < s->Qp; ++I)
+        for (int J = 0; J < s->pitch / kFastTV && J * kFastTV < s->Qp; ++J)
+            if (I * kFastU < J * kFastTV + kFastTV - 1) f.push_back((static_cast<uint32_t>(I) << 16) | J);
+    s->n_ftiles = static_cast<int>(f.size());
+    cudaMemcpy(s->d_ftiles, f.data(), sizeof(uint32_t) * f.size(), cudaMemcpyHostToDevice);
 }
 
 static void free_solution(tga_solution *s) {
@@ -299,7 +336,9 @@ static void free_solution(tga_solution *s) {
     if (s->Dp) cudaFree(s->Dp);
     if (s->h_keys) cudaFreeHost(s->h_keys);
     if (s->h_stage) cudaFreeHost(s->h_stage);
+    if (s->h_rstage) cudaFreeHost(s->h_rstage);
     if (s->own_stream) cudaStreamDestroy(s->own_stream);
+    for (auto e : s->tev) cudaEventDestroy(e);
     delete s;
 }
 
@@ -347,6 +386,12 @@ extern "C" int32_t tga_instance_create(int32_t n, const void *dist, int32_t dtyp
     I->Q = capacity;
     I->tw = tw != nullptr;
     I->max_c_abs = max_abs;
+    {
+        int64_t tot = 0;
+        for (int i = 0; i < n; ++i) tot += demand[i];
+        I->fast_ok = tot < (kPoison >> 2) && capacity < (kPoison >> 2) &&
+                     static_cast<int64_t>(max_abs) * 16 < (1ll << 30);
+    }
     if (opt) I->opt = *opt;
     else { I->opt.score_mode = TGA_SCORE_FEASIBLE; I->opt.w_load = 10; I->opt.w_tw = 10; I->opt.device = -1; }
     if (I->opt.device < 0) cudaGetDevice(&I->device);
@@ -444,13 +489,17 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
     const size_t tiles_max = static_cast<size_t>(s->pitch / kTileU) * (s->pitch / kTileV) + 1;
     void *v_node, *v_route, *v_pos, *v_rlen, *v_canon, *v_fwdL, *v_bwdL, *v_en, *v_fD, *v_bD, *v_b1, *v_b2, *v_b3;
     void *v_fT, *v_bT, *v_s2, *v_s3, *v_rbase, *v_rlenR, *v_rW, *v_rTV, *v_rD, *v_keys, *v_tiles;
+    void *v_rec = nullptr, *v_ftiles = nullptr;
+    const size_t ftiles_max = static_cast<size_t>(s->pitch / kFastU) * (s->pitch / kFastTV) + 1;
+    const bool want_fast = I->dtype == TGA_I32 && !I->tw && I->opt.score_mode == TGA_SCORE_FEASIBLE && I->fast_ok;
     Item items[] = {
         {&v_node, cap * 4}, {&v_route, cap * 4}, {&v_pos, cap * 4}, {&v_rlen, cap * 4}, {&v_canon, cap * 4},
         {&v_fwdL, cap * 4}, {&v_bwdL, cap * 4}, {&v_en, cap * 4}, {&v_fD, cap * 4}, {&v_bD, cap * 4},
         {&v_b1, cap * 4}, {&v_b2, cap * 4}, {&v_b3, cap * 4},
         {&v_fT, cap * 16}, {&v_bT, cap * 16}, {&v_s2, cap * 16}, {&v_s3, cap * 16},
         {&v_rbase, Rr * 4}, {&v_rlenR, Rr * 4}, {&v_rW, Rr * 4}, {&v_rTV, Rr * 4}, {&v_rD, Rr * 4},
-        {&v_keys, TGA_N_VARIANTS * 8}, {&v_tiles, tiles_max * 4}};
+        {&v_keys, TGA_N_VARIANTS * 8}, {&v_tiles, tiles_max * 4},
+        {&v_rec, want_fast ? cap * sizeof(SlotRec) : 0}, {&v_ftiles, want_fast ? ftiles_max * 4 : 0}};
     size_t total = 0;
     for (auto &it : items) total += align_up(it.bytes, 256);
     if (cudaMalloc(&s->arena, total) != cudaSuccess) return bail(fail(TGA_ERR_OOM, "device arena"));
@@ -475,6 +524,18 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
     s->d_rW = static_cast<int32_t *>(v_rW); s->d_rTV = static_cast<float *>(v_rTV); s->d_rD = v_rD;
     s->keys = static_cast<uint64_t *>(v_keys);
     s->d_tiles = static_cast<uint32_t *>(v_tiles);
+    if (want_fast) {
+        s->fast = true;
+        s->rec = static_cast<SlotRec *>(v_rec) + kGuard;
+        s->d_ftiles = static_cast<uint32_t *>(v_ftiles);
+        // every record starts poisoned (padding, guards); the scan overwrites route slots
+        SlotRec p{};
+        p.c = -1; p.r = -1; p.fL = p.bL1 = p.W = kPoison;
+        for (int k = 0; k < 3; ++k) { p.so[k] = kPoison; p.sA[k] = kPoison; }
+        std::vector<SlotRec> init(cap, p);
+        if (cudaMemcpy(v_rec, init.data(), cap * sizeof(SlotRec), cudaMemcpyHostToDevice) != cudaSuccess)
+            return bail(fail(TGA_ERR_CUDA, "record init"));
+    }
     // numeric per-slot arrays start at 0 (guards are only read by masked-out lanes)
     for (void *p : {v_fwdL, v_bwdL, v_en, v_fD, v_bD, v_b1, v_b2, v_b3})
         if (cudaMemset(p, 0, cap * 4) != cudaSuccess) return bail(fail(TGA_ERR_CUDA, "memset"));
@@ -483,8 +544,11 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
     // ---- position-ordered distance matrix
     const size_t dp_bytes = static_cast<size_t>(s->pitch) * s->pitch * 4;
     if (cudaMalloc(&s->Dp, dp_bytes) != cudaSuccess) return bail(fail(TGA_ERR_OOM, "Dp allocation"));
+    s->lay_pitch = align_up(cap * 4, 256);
+    s->route_pitch = align_up(Rr * 4, 256);
     if (cudaMallocHost(&s->h_keys, TGA_N_VARIANTS * 8) != cudaSuccess ||
-        cudaMallocHost(&s->h_stage, sizeof(int32_t) * 5 * cap) != cudaSuccess)
+        cudaMallocHost(&s->h_stage, 5 * s->lay_pitch) != cudaSuccess ||
+        cudaMallocHost(&s->h_rstage, 2 * s->route_pitch) != cudaSuccess)
         return bail(fail(TGA_ERR_OOM, "pinned host allocation"));
     // ---- layout upload, Dp build, scan
     if ((rc = upload_layout(s, 0, R - 1)) != TGA_OK) return bail(rc);
@@ -503,6 +567,17 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
         s->tmap_ok = (cr == CUDA_SUCCESS);
     }
     if (!s->tmap_ok) return bail(fail(TGA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable or failed"));
+    if (s->fast) {
+        auto enc = get_encode();
+        cuuint64_t gdim[2] = {static_cast<cuuint64_t>(s->pitch), static_cast<cuuint64_t>(s->pitch)};
+        cuuint64_t gstride[1] = {static_cast<cuuint64_t>(s->pitch) * 4};
+        cuuint32_t box[2] = {static_cast<cuuint32_t>(kFastBoxW), static_cast<cuuint32_t>(kFastBoxH)};
+        cuuint32_t estr[2] = {1, 1};
+        CUresult cr = enc(&s->fmap, CU_TENSOR_MAP_DATA_TYPE_INT32, 2, s->Dp, gdim, gstride, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (cr != CUDA_SUCCESS) return bail(fail(TGA_ERR_CUDA, "fast-path tensor map"));
+    }
     if (cudaStreamSynchronize(s->stream) != cudaSuccess)
         return bail(fail(TGA_ERR_CUDA, std::string("load: ") + cudaGetErrorString(cudaGetLastError())));
     *out = s;
@@ -511,6 +586,14 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
 
 extern "C" int32_t tga_solution_destroy(tga_solution *s) {
     free_solution(s);
+    return TGA_OK;
+}
+
+extern "C" int32_t tga_shard_range(int64_t n, int32_t shard, int32_t n_shards, int64_t *lo, int64_t *hi) {
+    if (!lo || !hi || n < 0 || n_shards < 1 || shard < 0 || shard >= n_shards)
+        return fail(TGA_ERR_INVALID_ARGUMENT, "shard range");
+    *lo = n * shard / n_shards;
+    *hi = n * (shard + 1) / n_shards;
     return TGA_OK;
 }
 
@@ -536,6 +619,8 @@ extern "C" int32_t tga_solution_set_shard(tga_solution *s, int32_t shard, int32_
     return TGA_OK;
 }
 
+extern "C" int32_t tga_shard_range(int64_t n, int32_t shard, int32_t n_shards, int64_t *lo, int64_t *hi);
+
 // ============================================================== ABI: evaluation
 extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
     if (!s) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL solution");
@@ -549,20 +634,38 @@ extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
     if (!accumulate) TGA_CUDA(cudaMemsetAsync(s->keys, 0xFF, TGA_N_VARIANTS * 8, st));
     ScoreParams sp{I->Q, I->opt.score_mode, I->opt.w_load, I->opt.w_tw};
     // row shard of the tile list and of the intra slot range
-    const int t_lo = static_cast<int>(static_cast<int64_t>(s->n_tiles) * s->shard / s->n_shards);
-    const int t_hi = static_cast<int>(static_cast<int64_t>(s->n_tiles) * (s->shard + 1) / s->n_shards);
-    const int x_lo = static_cast<int>(static_cast<int64_t>(s->Qp) * s->shard / s->n_shards);
-    const int x_hi = static_cast<int>(static_cast<int64_t>(s->Qp) * (s->shard + 1) / s->n_shards);
+    int64_t a, b;
+    tga_shard_range(s->n_tiles, s->shard, s->n_shards, &a, &b);
+    const int t_lo = static_cast<int>(a), t_hi = static_cast<int>(b);
+    tga_shard_range(s->Qp, s->shard, s->n_shards, &a, &b);
+    const int x_lo = static_cast<int>(a), x_hi = static_cast<int>(b);
     const int grid = std::max(1, std::min(t_hi - t_lo, s->sm_count * 4));
     cudaError_t e;
-    if (I->dtype == TGA_I32) {
-        const auto v = sol_view<int32_t>(s);
-        e = launch_inter<int32_t>(mask, I->tw, v, s->tmap, s->d_tiles, t_lo, t_hi, sp, s->keys, grid, st);
-        if (e == cudaSuccess) e = launch_intra<int32_t>(mask, I->tw, v, sp, x_lo, x_hi, s->keys, st);
+    const bool timed = s->timing && (mask & TGA_OP_INTER) && s->tev_n + 2 <= static_cast<int>(s->tev.size());
+    if (timed) TGA_CUDA(cudaEventRecord(s->tev[s->tev_n], st));
+    if (I->dtype == TGA_I32 && s->fast) {
+        tga_shard_range(s->n_ftiles, s->shard, s->n_shards, &a, &b);
+        const int f_lo = static_cast<int>(a), f_hi = static_cast<int>(b);
+        const int fgrid = std::max(1, std::min(f_hi - f_lo, s->sm_count * 4));
+        e = launch_inter_fast(mask, s->rec, s->fmap, s->d_ftiles, f_lo, f_hi, static_cast<uint32_t>(s->Qc), I->Q,
+                              s->keys, fgrid, st);
+    } else if (I->dtype == TGA_I32) {
+        e = launch_inter<int32_t>(mask, I->tw, sol_view<int32_t>(s), s->tmap, s->d_tiles, t_lo, t_hi, sp, s->keys,
+                                  grid, st);
     } else {
-        const auto v = sol_view<float>(s);
-        e = launch_inter<float>(mask, I->tw, v, s->tmap, s->d_tiles, t_lo, t_hi, sp, s->keys, grid, st);
-        if (e == cudaSuccess) e = launch_intra<float>(mask, I->tw, v, sp, x_lo, x_hi, s->keys, st);
+        e = launch_inter<float>(mask, I->tw, sol_view<float>(s), s->tmap, s->d_tiles, t_lo, t_hi, sp, s->keys, grid,
+                                st);
+    }
+    if (timed) {
+        TGA_CUDA(cudaEventRecord(s->tev[s->tev_n + 1], st));
+        s->tev_n += 2;
+    }
+    if (e == cudaSuccess) {
+        if (I->dtype == TGA_I32)
+            e = launch_intra<int32_t>(mask, I->tw, sol_view<int32_t>(s), sp, x_lo, x_hi, s->keys, st,
+                                      I->max_c_abs < (1 << 21));
+        else
+            e = launch_intra<float>(mask, I->tw, sol_view<float>(s), sp, x_lo, x_hi, s->keys, st);
     }
     if (e != cudaSuccess) return fail(TGA_ERR_CUDA, std::string("eval launch: ") + cudaGetErrorString(e));
     if (s->comm) {
@@ -867,6 +970,69 @@ extern "C" int32_t tga_comm_init(tga_solution *s, int32_t rank, int32_t world, c
     s->comm = c;
     s->shard = rank;
     s->n_shards = world;
+    return TGA_OK;
+}
+
+// ============================================================== ABI: step / reload / timing
+extern "C" int32_t tga_step(tga_solution *s, uint32_t mask, tga_move *out) {
+    if (!s) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL solution");
+    int32_t rc = tga_eval(s, mask, nullptr);
+    if (rc != TGA_OK) return rc;
+    tga_move m;
+    rc = tga_best_move(s, mask, &m);
+    if (out) *out = m;
+    if (rc != TGA_OK) return rc;  // TGA_NO_IMPROVING_MOVE or an error
+    return tga_apply_move(s, &m);
+}
+
+extern "C" int32_t tga_solution_reload(tga_solution *s, int32_t R, const int32_t *ptr, const int32_t *cust) {
+    if (!s || !ptr || !cust) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL argument");
+    const tga_instance *I = s->inst;
+    if (R != s->R) return fail(TGA_ERR_INVALID_ARGUMENT, "reload needs the same route count");
+    if (ptr[0] != 0 || ptr[R] != I->n - 1) return fail(TGA_ERR_STRUCTURE, "route_ptr does not cover the customers");
+    std::vector<char> seen(I->n, 0);
+    for (int r = 0; r < R; ++r) {
+        if (ptr[r + 1] < ptr[r]) return fail(TGA_ERR_STRUCTURE, "route_ptr not non-decreasing");
+        for (int k = ptr[r]; k < ptr[r + 1]; ++k) {
+            const int c = cust[k];
+            if (c <= 0 || c >= I->n || seen[c]) return fail(TGA_ERR_STRUCTURE, "customer out of range or repeated");
+            seen[c] = 1;
+        }
+    }
+    if (set_device(I) != TGA_OK) return TGA_ERR_CUDA;
+    TGA_CUDA(cudaStreamSynchronize(s->stream));  // staging buffers may still be in flight
+    for (int r = 0; r < R; ++r) s->routes[r].assign(cust + ptr[r], cust + ptr[r + 1]);
+    compute_bases(s);
+    int32_t rc;
+    if ((rc = upload_layout(s, 0, R - 1)) != TGA_OK) return rc;
+    if ((rc = refresh(s, 0, R - 1, true)) != TGA_OK) return rc;
+    ++s->gen;
+    return TGA_OK;
+}
+
+extern "C" int32_t tga_solution_enable_timing(tga_solution *s, int32_t enable) {
+    if (!s) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL solution");
+    if (enable && s->tev.empty()) {
+        s->tev.resize(8192);
+        for (auto &e : s->tev) TGA_CUDA(cudaEventCreate(&e));
+    }
+    s->timing = enable != 0;
+    s->tev_n = 0;
+    return TGA_OK;
+}
+
+extern "C" int32_t tga_solution_timings(tga_solution *s, float *ms, int32_t max_n, int32_t *n_out) {
+    if (!s || !n_out) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL argument");
+    int n = 0;
+    for (int i = 0; i + 1 < s->tev_n && n < max_n; i += 2) {
+        TGA_CUDA(cudaEventSynchronize(s->tev[i + 1]));
+        float t = 0.f;
+        TGA_CUDA(cudaEventElapsedTime(&t, s->tev[i], s->tev[i + 1]));
+        if (ms) ms[n] = t;
+        ++n;
+    }
+    s->tev_n = 0;
+    *n_out = n;
     return TGA_OK;
 }
 

@@ -91,6 +91,11 @@ _SYMBOLS = {
     "tga_solution_attributes": (C.c_int32, [C.c_void_p] + [C.c_void_p] * 7),
     "tga_solution_set_shard": (C.c_int32, [C.c_void_p, C.c_int32, C.c_int32]),
     "tga_solution_set_stream": (C.c_int32, [C.c_void_p, C.c_void_p]),
+    "tga_step": (C.c_int32, [C.c_void_p, C.c_uint32, C.c_void_p]),
+    "tga_solution_reload": (C.c_int32, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
+    "tga_solution_enable_timing": (C.c_int32, [C.c_void_p, C.c_int32]),
+    "tga_solution_timings": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]),
+    "tga_shard_range": (C.c_int32, [C.c_int64, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
     "tga_nccl_unique_id": (C.c_int32, [C.c_void_p]),
     "tga_comm_init": (C.c_int32, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
     "tga_last_error": (C.c_char_p, []),
@@ -140,6 +145,13 @@ def version() -> str:
 
 def launch_count() -> int:
     return int(lib().tga_launch_count())
+
+
+def shard_range(n_items: int, shard: int, n_shards: int):
+    """The library's row-shard plan: [lo, hi) of n_items for this shard."""
+    lo, hi = C.c_int64(), C.c_int64()
+    _check(lib().tga_shard_range(n_items, shard, n_shards, C.byref(lo), C.byref(hi)))
+    return lo.value, hi.value
 
 
 def nccl_unique_id() -> bytes:
@@ -241,6 +253,27 @@ class Solution:
 
     def apply(self, move: Move) -> None:
         _check(lib().tga_apply_move(self._h, C.byref(move)))
+
+    def step(self, op_mask: int = OP_ALL):
+        """eval + best_move + apply (if improving) in one call: (applied, Move)."""
+        m = Move()
+        rc = _check(lib().tga_step(self._h, op_mask, C.byref(m)), allow=(OK, NO_IMPROVING_MOVE))
+        return rc == OK, m
+
+    def reload(self, routes) -> None:
+        """Load another solution (same route count) into this object, asynchronously."""
+        ptr, cust = _csr(routes)
+        _check(lib().tga_solution_reload(self._h, len(ptr) - 1, _p(ptr), _p(cust)))
+
+    def enable_timing(self, on: bool = True) -> None:
+        _check(lib().tga_solution_enable_timing(self._h, int(on)))
+
+    def timings(self) -> np.ndarray:
+        """Durations (ms) of the inter-route launches recorded since the last call."""
+        buf = np.zeros(8192, dtype=np.float32)
+        n = C.c_int32()
+        _check(lib().tga_solution_timings(self._h, _p(buf), len(buf), C.byref(n)))
+        return buf[:n.value].copy()
 
     # ---- queries
     def keys(self) -> np.ndarray:

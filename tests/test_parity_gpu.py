@@ -270,3 +270,32 @@ def test_real_valued_time_windows_tolerance():
         order = np.sort(sc[np.isfinite(sc)])
         if len(order) > 1 and order[1] - order[0] > 10 * tol + 1e-2:
             assert idx_gpu == best.u * Q + best.v
+
+
+# ---------------------------------------------------------------- step / reload / timing ABI
+def test_step_reload_and_timing():
+    """tga_step == eval + best_move + apply; tga_solution_reload == a fresh load;
+    live timings are recorded for the inter-route launch."""
+    _need_gpu()
+    inst, sol = G.x_like(8, n=200, target_routes=9)
+    gi = T.Instance.from_gen(inst)
+    a = T.Solution(gi, sol)
+    b = T.Solution(gi, sol)
+    a.enable_timing(True)
+    for _ in range(10):
+        a.eval(T.OP_ALL)
+        ok, mv = a.best_move(T.OP_ALL)
+        applied, mv2 = b.step(T.OP_ALL)
+        assert ok == applied and (mv.variant, mv.u, mv.v, mv.delta_i) == (mv2.variant, mv2.u, mv2.v, mv2.delta_i)
+        if ok:
+            a.apply(mv)
+    assert a.routes() == b.routes()
+    t = a.timings()
+    assert len(t) == 10 and (t > 0).all()
+    other = G.perturb(sol, 15, 3)
+    b.reload(other)
+    fresh = T.Solution(gi, other)
+    b.eval(T.OP_ALL)
+    fresh.eval(T.OP_ALL)
+    np.testing.assert_array_equal(b.keys(), fresh.keys())
+    assert b.routes() == fresh.routes()

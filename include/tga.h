@@ -248,6 +248,28 @@ int32_t tga_shard_range(int64_t n_items, int32_t shard, int32_t n_shards, int64_
 int32_t tga_nccl_unique_id(void *out_128_bytes);
 int32_t tga_comm_init(tga_solution *sol, int32_t rank, int32_t world, const void *nccl_unique_id);
 
+/* ------------------------------------------------------------ population batch
+ * A batch of solutions of one instance evaluated by single launches over
+ * (solution, tile) work items (BASELINE config 5; "Population-based
+ * metaheuristics can leverage parallel evaluation").
+ * tga_batch_load: n_sol solutions; n_routes[k] routes each; route_ptr holds the
+ * n_sol CSR offset arrays back to back (n_routes[k]+1 entries each, each
+ * starting at 0); customers holds n_sol blocks of n_nodes-1 ids.
+ * tga_batch_best_moves: out[n_sol] moves, status[n_sol] (TGA_OK = improving,
+ * TGA_NO_IMPROVING_MOVE) -- may be NULL.  tga_batch_apply_moves applies
+ * moves[k] where apply[k] != 0 (apply may be NULL = all with a valid variant).
+ * tga_batch_solution returns a borrowed handle (owned by the batch). */
+typedef struct tga_batch tga_batch;
+int32_t tga_batch_load(tga_instance *inst, int32_t n_sol, const int32_t *n_routes,
+                       const int32_t *route_ptr, const int32_t *customers, tga_batch **out);
+int32_t tga_batch_destroy(tga_batch *batch);
+int32_t tga_batch_size(const tga_batch *batch, int32_t *n_sol);
+int32_t tga_batch_solution(tga_batch *batch, int32_t i, tga_solution **out);
+int32_t tga_batch_eval(tga_batch *batch, uint32_t op_mask, void *cuda_stream);
+int32_t tga_batch_keys(tga_batch *batch, uint64_t *keys);
+int32_t tga_batch_best_moves(tga_batch *batch, uint32_t op_mask, tga_move *out, int32_t *status);
+int32_t tga_batch_apply_moves(tga_batch *batch, const tga_move *moves, const int32_t *apply);
+
 /* ------------------------------------------------------------ misc */
 const char *tga_last_error(void);
 const char *tga_version(void);

@@ -139,6 +139,7 @@ struct SolView {
     int32_t pitch;            // elements per Dp row
     int32_t Qp;               // physical slots (rows of Dp)
     uint32_t Qc;              // canonical slot count Q = N + R (flat index = u * Qc + v)
+    const uint32_t *tiles;    // generic inter-route tile plan (batch kernels)
 };
 
 }  // namespace tga

@@ -320,8 +320,137 @@ __device__ __forceinline__ void tma_load_2d(void *smem_dst, const CUtensorMap *m
 // with a halo (rows u0-1 .. u0+TU+2, cols v0-4 .. v0+TV+3) is TMA-loaded into
 // shared memory (double-buffered across the persistent tile loop).
 // Thread mapping: lane -> v = v0 + lane + 32*j (j < VPT); warp -> UPW rows.
+// One tile of the inter-route candidate space (rows u0.., columns v0..), Dp box
+// already in shared memory; running (score, index) keys per variant in `best`.
 template <class DT, bool TW, uint32_t MASK>
-__global__ void __launch_bounds__(kInterThreads) k_inter(const SolView<DT> S, const __grid_constant__ CUtensorMap tmap,
+__device__ __forceinline__ void inter_tile(const SolView<DT> &S, const DT *__restrict__ tile, const int u0,
+                                           const int v0, const ScoreParams &sp, uint64_t (&best)[11]) {
+    constexpr int TU = kTileU, TV = kTileV, VPT = TV / 32, UPW = TU / (kInterThreads / 32);
+    constexpr int BW = kBoxW;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // Dp(x, y) from the staged box
+    auto Dt = [&](int x, int y) -> DT { return tile[(x - u0 + 1) * BW + (y - v0 + kBoxX0)]; };
+#pragma unroll 1
+    for (int j = 0; j < VPT; ++j) {
+        const int v = v0 + lane + 32 * j;
+        const int cv = S.canon[v];
+        const int rv = S.route[v];
+        const int pv = S.pos[v];
+        const int Lb = S.rlen[v];
+        const int Wb = (rv >= 0) ? S.rW[rv] : 0;
+        const float TVb = (TW && rv >= 0) ? S.rTV[rv] : 0.f;
+#pragma unroll 1
+        for (int i = 0; i < UPW; ++i) {
+            const int u = u0 + warp * UPW + i;
+            const int cu = S.canon[u];
+            const int ru = S.route[u];
+            if (cu < 0) continue;  // warp-uniform: end depot / padding row
+            const bool pair = (cv >= 0) && (ru < rv);
+            const int pu = S.pos[u];
+            const int La = S.rlen[u];
+            const int Wa = S.rW[ru];
+            const float TVa = TW ? S.rTV[ru] : 0.f;
+            const uint32_t idx_uv = static_cast<uint32_t>(cu) * S.Qc + static_cast<uint32_t>(cv);
+            const uint32_t idx_vu = static_cast<uint32_t>(cv) * S.Qc + static_cast<uint32_t>(cu);
+
+            // ---- 2-opt* (3-Seq(0,0) P:346; Eq. 14)
+            if (MASK & (1u << 1)) {
+                const DT dD = Dt(u, v + 1) + Dt(u + 1, v) - S.enext[u] - S.enext[v];
+                const int la = S.fwdL[u] + S.bwdL[v + 1];
+                const int lb = S.fwdL[v] + S.bwdL[u + 1];
+                float ta = 0.f, tb = 0.f;
+                if (TW) {
+                    ta = tw_cat(S.fwdT[u], S.bwdT[v + 1], static_cast<float>(Dt(u, v + 1))).w;
+                    tb = tw_cat(S.fwdT[v], S.bwdT[u + 1], static_cast<float>(Dt(u + 1, v))).w;
+                }
+                best[1] = umin64(best[1], score_key<DT, TW>(sp, pair, dD, la, lb, Wa, Wb, ta, tb, TVa, TVb, idx_uv));
+            }
+            // ---- relocate (N=1) / or-opt (N=2,3): both directions (Eq. 13)
+#pragma unroll
+            for (int N = 1; N <= 3; ++N) {
+                if (!(MASK & (1u << (1 + N)))) continue;
+                const DT *bridge = N == 1 ? S.bridge1 : (N == 2 ? S.bridge2 : S.bridge3);
+                const TwRec *segT = N == 1 ? nullptr : (N == 2 ? S.seg2T : S.seg3T);
+                {   // segment u..u+N-1 (route a) inserted after v (route b)
+                    const bool ok = pair && pu >= 1 && pu + N - 1 <= La;
+                    const DT dD = bridge[u] - S.enext[u - 1] - S.enext[u + N - 1] + Dt(u, v) +
+                                  Dt(u + N - 1, v + 1) - S.enext[v];
+                    const int s = S.fwdL[u + N - 1] - S.fwdL[u - 1];
+                    float ta = 0.f, tb = 0.f;
+                    if (TW) {
+                        const TwRec sg = N == 1 ? S.node_tw[S.node[u]] : segT[u];
+                        ta = tw_cat(S.fwdT[u - 1], S.bwdT[u + N], static_cast<float>(bridge[u])).w;
+                        const TwRec X = tw_cat(S.fwdT[v], sg, static_cast<float>(Dt(u, v)));
+                        tb = tw_cat(X, S.bwdT[v + 1], static_cast<float>(Dt(u + N - 1, v + 1))).w;
+                    }
+                    best[1 + N] = umin64(best[1 + N], score_key<DT, TW>(sp, ok, dD, Wa - s, Wb + s, Wa, Wb,
+                                                                        ta, tb, TVa, TVb, idx_uv));
+                }
+                {   // segment v..v+N-1 (route b) inserted after u (route a)
+                    const bool ok = pair && pv >= 1 && pv + N - 1 <= Lb;
+                    const DT dD = bridge[v] - S.enext[v - 1] - S.enext[v + N - 1] + Dt(u, v) +
+                                  Dt(u + 1, v + N - 1) - S.enext[u];
+                    const int s = S.fwdL[v + N - 1] - S.fwdL[v - 1];
+                    float ta = 0.f, tb = 0.f;
+                    if (TW) {
+                        const TwRec sg = N == 1 ? S.node_tw[S.node[v]] : segT[v];
+                        tb = tw_cat(S.fwdT[v - 1], S.bwdT[v + N], static_cast<float>(bridge[v])).w;
+                        const TwRec X = tw_cat(S.fwdT[u], sg, static_cast<float>(Dt(u, v)));
+                        ta = tw_cat(X, S.bwdT[u + 1], static_cast<float>(Dt(u + 1, v + N - 1))).w;
+                    }
+                    best[1 + N] = umin64(best[1 + N], score_key<DT, TW>(sp, ok, dD, Wa + s, Wb - s, Wa, Wb,
+                                                                        ta, tb, TVa, TVb, idx_vu));
+                }
+            }
+            // ---- swap (1,1) / cross-exchange (N1,N2) (3-Seq(N1,N2) P:346)
+#pragma unroll
+            for (int sv = 0; sv < 6; ++sv) {
+                const int vid = 5 + sv;
+                if (!(MASK & (1u << vid))) continue;
+                const int N1 = sv == 0 ? 1 : (sv <= 2 ? 1 : (sv <= 4 ? 2 : 3));
+                const int N2 = sv == 0 ? 1 : (sv == 1 ? 2 : (sv == 2 ? 3 : (sv == 3 ? 2 : 3)));
+                auto seg = [&](int x, int N) -> TwRec {
+                    return N == 1 ? S.node_tw[S.node[x]] : (N == 2 ? S.seg2T[x] : S.seg3T[x]);
+                };
+                {   // N1-segment at u (route a), N2-segment at v (route b)
+                    const bool ok = pair && pu >= 1 && pu + N1 - 1 <= La && pv >= 1 && pv + N2 - 1 <= Lb;
+                    const DT dD = Dt(u - 1, v) + Dt(u + N1, v + N2 - 1) + Dt(u, v - 1) + Dt(u + N1 - 1, v + N2) -
+                                  S.enext[u - 1] - S.enext[u + N1 - 1] - S.enext[v - 1] - S.enext[v + N2 - 1];
+                    const int sa = S.fwdL[u + N1 - 1] - S.fwdL[u - 1];
+                    const int sb = S.fwdL[v + N2 - 1] - S.fwdL[v - 1];
+                    float ta = 0.f, tb = 0.f;
+                    if (TW) {
+                        const TwRec A1 = tw_cat(S.fwdT[u - 1], seg(v, N2), static_cast<float>(Dt(u - 1, v)));
+                        ta = tw_cat(A1, S.bwdT[u + N1], static_cast<float>(Dt(u + N1, v + N2 - 1))).w;
+                        const TwRec B1 = tw_cat(S.fwdT[v - 1], seg(u, N1), static_cast<float>(Dt(u, v - 1)));
+                        tb = tw_cat(B1, S.bwdT[v + N2], static_cast<float>(Dt(u + N1 - 1, v + N2))).w;
+                    }
+                    best[vid] = umin64(best[vid], score_key<DT, TW>(sp, ok, dD, Wa - sa + sb, Wb - sb + sa, Wa,
+                                                                    Wb, ta, tb, TVa, TVb, idx_uv));
+                }
+                if (N1 != N2) {   // N1-segment at v (route b), N2-segment at u (route a)
+                    const bool ok = pair && pv >= 1 && pv + N1 - 1 <= Lb && pu >= 1 && pu + N2 - 1 <= La;
+                    const DT dD = Dt(u, v - 1) + Dt(u + N2 - 1, v + N1) + Dt(u - 1, v) + Dt(u + N2, v + N1 - 1) -
+                                  S.enext[v - 1] - S.enext[v + N1 - 1] - S.enext[u - 1] - S.enext[u + N2 - 1];
+                    const int sb = S.fwdL[v + N1 - 1] - S.fwdL[v - 1];
+                    const int sa = S.fwdL[u + N2 - 1] - S.fwdL[u - 1];
+                    float ta = 0.f, tb = 0.f;
+                    if (TW) {
+                        const TwRec B1 = tw_cat(S.fwdT[v - 1], seg(u, N2), static_cast<float>(Dt(u, v - 1)));
+                        tb = tw_cat(B1, S.bwdT[v + N1], static_cast<float>(Dt(u + N2 - 1, v + N1))).w;
+                        const TwRec A1 = tw_cat(S.fwdT[u - 1], seg(v, N1), static_cast<float>(Dt(u - 1, v)));
+                        ta = tw_cat(A1, S.bwdT[u + N2], static_cast<float>(Dt(u + N2, v + N1 - 1))).w;
+                    }
+                    best[vid] = umin64(best[vid], score_key<DT, TW>(sp, ok, dD, Wa - sa + sb, Wb - sb + sa, Wa,
+                                                                    Wb, ta, tb, TVa, TVb, idx_vu));
+                }
+            }
+        }
+    }
+}
+
+template <class DT, bool TW, uint32_t MASK>
+__global__ void __launch_bounds__(kInterThreads) k_inter(const __grid_constant__ SolView<DT> S, const __grid_constant__ CUtensorMap tmap,
                                                          const uint32_t *__restrict__ tiles, int t_lo, int t_hi,
                                                          ScoreParams sp, uint64_t *__restrict__ keys) {
     constexpr int TU = kTileU, TV = kTileV, VPT = TV / 32, UPW = TU / (kInterThreads / 32);
@@ -367,126 +496,8 @@ __global__ void __launch_bounds__(kInterThreads) k_inter(const SolView<DT> S, co
         const DT *tile = b ? buf1 : buf0;
         const uint32_t ij = tiles[t];
         const int u0 = (ij >> 16) * TU, v0 = (ij & 0xFFFF) * TV;
-        // Dp(x, y) from the staged box
-        auto Dt = [&](int x, int y) -> DT { return tile[(x - u0 + 1) * BW + (y - v0 + kBoxX0)]; };
 
-#pragma unroll 1
-        for (int j = 0; j < VPT; ++j) {
-            const int v = v0 + lane + 32 * j;
-            const int cv = S.canon[v];
-            const int rv = S.route[v];
-            const int pv = S.pos[v];
-            const int Lb = S.rlen[v];
-            const int Wb = (rv >= 0) ? S.rW[rv] : 0;
-            const float TVb = (TW && rv >= 0) ? S.rTV[rv] : 0.f;
-#pragma unroll 1
-            for (int i = 0; i < UPW; ++i) {
-                const int u = u0 + warp * UPW + i;
-                const int cu = S.canon[u];
-                const int ru = S.route[u];
-                if (cu < 0) continue;  // warp-uniform: end depot / padding row
-                const bool pair = (cv >= 0) && (ru < rv);
-                const int pu = S.pos[u];
-                const int La = S.rlen[u];
-                const int Wa = S.rW[ru];
-                const float TVa = TW ? S.rTV[ru] : 0.f;
-                const uint32_t idx_uv = static_cast<uint32_t>(cu) * S.Qc + static_cast<uint32_t>(cv);
-                const uint32_t idx_vu = static_cast<uint32_t>(cv) * S.Qc + static_cast<uint32_t>(cu);
-
-                // ---- 2-opt* (3-Seq(0,0) P:346; Eq. 14)
-                if (MASK & (1u << 1)) {
-                    const DT dD = Dt(u, v + 1) + Dt(u + 1, v) - S.enext[u] - S.enext[v];
-                    const int la = S.fwdL[u] + S.bwdL[v + 1];
-                    const int lb = S.fwdL[v] + S.bwdL[u + 1];
-                    float ta = 0.f, tb = 0.f;
-                    if (TW) {
-                        ta = tw_cat(S.fwdT[u], S.bwdT[v + 1], static_cast<float>(Dt(u, v + 1))).w;
-                        tb = tw_cat(S.fwdT[v], S.bwdT[u + 1], static_cast<float>(Dt(u + 1, v))).w;
-                    }
-                    best[1] = umin64(best[1], score_key<DT, TW>(sp, pair, dD, la, lb, Wa, Wb, ta, tb, TVa, TVb, idx_uv));
-                }
-                // ---- relocate (N=1) / or-opt (N=2,3): both directions (Eq. 13)
-#pragma unroll
-                for (int N = 1; N <= 3; ++N) {
-                    if (!(MASK & (1u << (1 + N)))) continue;
-                    const DT *bridge = N == 1 ? S.bridge1 : (N == 2 ? S.bridge2 : S.bridge3);
-                    const TwRec *segT = N == 1 ? nullptr : (N == 2 ? S.seg2T : S.seg3T);
-                    {   // segment u..u+N-1 (route a) inserted after v (route b)
-                        const bool ok = pair && pu >= 1 && pu + N - 1 <= La;
-                        const DT dD = bridge[u] - S.enext[u - 1] - S.enext[u + N - 1] + Dt(u, v) +
-                                      Dt(u + N - 1, v + 1) - S.enext[v];
-                        const int s = S.fwdL[u + N - 1] - S.fwdL[u - 1];
-                        float ta = 0.f, tb = 0.f;
-                        if (TW) {
-                            const TwRec sg = N == 1 ? S.node_tw[S.node[u]] : segT[u];
-                            ta = tw_cat(S.fwdT[u - 1], S.bwdT[u + N], static_cast<float>(bridge[u])).w;
-                            const TwRec X = tw_cat(S.fwdT[v], sg, static_cast<float>(Dt(u, v)));
-                            tb = tw_cat(X, S.bwdT[v + 1], static_cast<float>(Dt(u + N - 1, v + 1))).w;
-                        }
-                        best[1 + N] = umin64(best[1 + N], score_key<DT, TW>(sp, ok, dD, Wa - s, Wb + s, Wa, Wb,
-                                                                            ta, tb, TVa, TVb, idx_uv));
-                    }
-                    {   // segment v..v+N-1 (route b) inserted after u (route a)
-                        const bool ok = pair && pv >= 1 && pv + N - 1 <= Lb;
-                        const DT dD = bridge[v] - S.enext[v - 1] - S.enext[v + N - 1] + Dt(u, v) +
-                                      Dt(u + 1, v + N - 1) - S.enext[u];
-                        const int s = S.fwdL[v + N - 1] - S.fwdL[v - 1];
-                        float ta = 0.f, tb = 0.f;
-                        if (TW) {
-                            const TwRec sg = N == 1 ? S.node_tw[S.node[v]] : segT[v];
-                            tb = tw_cat(S.fwdT[v - 1], S.bwdT[v + N], static_cast<float>(bridge[v])).w;
-                            const TwRec X = tw_cat(S.fwdT[u], sg, static_cast<float>(Dt(u, v)));
-                            ta = tw_cat(X, S.bwdT[u + 1], static_cast<float>(Dt(u + 1, v + N - 1))).w;
-                        }
-                        best[1 + N] = umin64(best[1 + N], score_key<DT, TW>(sp, ok, dD, Wa + s, Wb - s, Wa, Wb,
-                                                                            ta, tb, TVa, TVb, idx_vu));
-                    }
-                }
-                // ---- swap (1,1) / cross-exchange (N1,N2) (3-Seq(N1,N2) P:346)
-#pragma unroll
-                for (int sv = 0; sv < 6; ++sv) {
-                    const int vid = 5 + sv;
-                    if (!(MASK & (1u << vid))) continue;
-                    const int N1 = sv == 0 ? 1 : (sv <= 2 ? 1 : (sv <= 4 ? 2 : 3));
-                    const int N2 = sv == 0 ? 1 : (sv == 1 ? 2 : (sv == 2 ? 3 : (sv == 3 ? 2 : 3)));
-                    auto seg = [&](int x, int N) -> TwRec {
-                        return N == 1 ? S.node_tw[S.node[x]] : (N == 2 ? S.seg2T[x] : S.seg3T[x]);
-                    };
-                    {   // N1-segment at u (route a), N2-segment at v (route b)
-                        const bool ok = pair && pu >= 1 && pu + N1 - 1 <= La && pv >= 1 && pv + N2 - 1 <= Lb;
-                        const DT dD = Dt(u - 1, v) + Dt(u + N1, v + N2 - 1) + Dt(u, v - 1) + Dt(u + N1 - 1, v + N2) -
-                                      S.enext[u - 1] - S.enext[u + N1 - 1] - S.enext[v - 1] - S.enext[v + N2 - 1];
-                        const int sa = S.fwdL[u + N1 - 1] - S.fwdL[u - 1];
-                        const int sb = S.fwdL[v + N2 - 1] - S.fwdL[v - 1];
-                        float ta = 0.f, tb = 0.f;
-                        if (TW) {
-                            const TwRec A1 = tw_cat(S.fwdT[u - 1], seg(v, N2), static_cast<float>(Dt(u - 1, v)));
-                            ta = tw_cat(A1, S.bwdT[u + N1], static_cast<float>(Dt(u + N1, v + N2 - 1))).w;
-                            const TwRec B1 = tw_cat(S.fwdT[v - 1], seg(u, N1), static_cast<float>(Dt(u, v - 1)));
-                            tb = tw_cat(B1, S.bwdT[v + N2], static_cast<float>(Dt(u + N1 - 1, v + N2))).w;
-                        }
-                        best[vid] = umin64(best[vid], score_key<DT, TW>(sp, ok, dD, Wa - sa + sb, Wb - sb + sa, Wa,
-                                                                        Wb, ta, tb, TVa, TVb, idx_uv));
-                    }
-                    if (N1 != N2) {   // N1-segment at v (route b), N2-segment at u (route a)
-                        const bool ok = pair && pv >= 1 && pv + N1 - 1 <= Lb && pu >= 1 && pu + N2 - 1 <= La;
-                        const DT dD = Dt(u, v - 1) + Dt(u + N2 - 1, v + N1) + Dt(u - 1, v) + Dt(u + N2, v + N1 - 1) -
-                                      S.enext[v - 1] - S.enext[v + N1 - 1] - S.enext[u - 1] - S.enext[u + N2 - 1];
-                        const int sb = S.fwdL[v + N1 - 1] - S.fwdL[v - 1];
-                        const int sa = S.fwdL[u + N2 - 1] - S.fwdL[u - 1];
-                        float ta = 0.f, tb = 0.f;
-                        if (TW) {
-                            const TwRec B1 = tw_cat(S.fwdT[v - 1], seg(u, N2), static_cast<float>(Dt(u, v - 1)));
-                            tb = tw_cat(B1, S.bwdT[v + N1], static_cast<float>(Dt(u + N2 - 1, v + N1))).w;
-                            const TwRec A1 = tw_cat(S.fwdT[u - 1], seg(v, N1), static_cast<float>(Dt(u - 1, v)));
-                            ta = tw_cat(A1, S.bwdT[u + N2], static_cast<float>(Dt(u + N2, v + N1 - 1))).w;
-                        }
-                        best[vid] = umin64(best[vid], score_key<DT, TW>(sp, ok, dD, Wa - sa + sb, Wb - sb + sa, Wa,
-                                                                        Wb, ta, tb, TVa, TVb, idx_vu));
-                    }
-                }
-            }
-        }
+        inter_tile<DT, TW, MASK>(S, tile, u0, v0, sp, best);
         __syncthreads();  // every thread is done with this buffer before it is refilled
     }
 
@@ -502,6 +513,68 @@ __global__ void __launch_bounds__(kInterThreads) k_inter(const SolView<DT> S, co
         atomicMin(reinterpret_cast<unsigned long long *>(keys) + tid, red[tid]);
 }
 
+// population mode: a work item = (solution, tile) of a batch of solutions of one
+// instance; every solution has its own Dp (own TMA descriptor, in global
+// memory) and its own 23 keys.  Keys are reduced per work item.
+template <class DT, bool TW, uint32_t MASK>
+__global__ void __launch_bounds__(kInterThreads) k_inter_batch(const SolView<DT> *__restrict__ views,
+                                                               const CUtensorMap *__restrict__ maps,
+                                                               const uint32_t *__restrict__ work, int n_work,
+                                                               ScoreParams sp, uint64_t *__restrict__ keys) {
+    constexpr int TU = kTileU, TV = kTileV;
+    constexpr int NV = 11;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char *smem_al = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+    DT *buf0 = reinterpret_cast<DT *>(smem_al);
+    DT *buf1 = reinterpret_cast<DT *>(smem_al + kBoxBytesPadded);
+    __shared__ uint64_t bar[2];
+    __shared__ unsigned long long red[NV];
+    const int tid = threadIdx.x, lane = tid & 31;
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_barrier_init();
+    }
+    if (tid < NV) red[tid] = kNoKey;
+    __syncthreads();
+    auto issue = [&](int i, int b) {
+        const uint32_t w = work[i];
+        const int sol = static_cast<int>(w >> 20);
+        const uint32_t ij = views[sol].tiles[w & 0xFFFFFu];
+        mbar_expect_tx(&bar[b], kBoxBytes);
+        tma_load_2d(b ? buf1 : buf0, maps + sol, (ij & 0xFFFF) * TV - kBoxX0, (ij >> 16) * TU - 1, &bar[b]);
+    };
+    int i = blockIdx.x;
+    if (tid == 0 && i < n_work) issue(i, 0);
+    uint32_t phase0 = 0, phase1 = 0;
+    for (int it = 0; i < n_work; i += gridDim.x, ++it) {
+        const int b = it & 1;
+        if (tid == 0 && i + static_cast<int>(gridDim.x) < n_work) issue(i + gridDim.x, b ^ 1);
+        if (b == 0) { mbar_wait(&bar[0], phase0); phase0 ^= 1; }
+        else        { mbar_wait(&bar[1], phase1); phase1 ^= 1; }
+        const uint32_t w = work[i];
+        const int sol = static_cast<int>(w >> 20);
+        const SolView<DT> &S = views[sol];
+        const uint32_t ij = S.tiles[w & 0xFFFFFu];
+        uint64_t best[NV];
+#pragma unroll
+        for (int k = 0; k < NV; ++k) best[k] = kNoKey;
+        inter_tile<DT, TW, MASK>(S, b ? buf1 : buf0, (ij >> 16) * TU, (ij & 0xFFFF) * TV, sp, best);
+#pragma unroll
+        for (int k = 1; k < NV; ++k) {
+            if (!(MASK & (1u << k))) continue;
+            const uint64_t m = warp_min64(best[k]);
+            if (lane == 0 && m != kNoKey) atomicMin(&red[k], static_cast<unsigned long long>(m));
+        }
+        __syncthreads();
+        if (tid < NV && (MASK & (1u << tid)) && red[tid] != kNoKey) {
+            atomicMin(reinterpret_cast<unsigned long long *>(keys) + static_cast<size_t>(sol) * 23 + tid, red[tid]);
+            red[tid] = kNoKey;
+        }
+        __syncthreads();  // buffer b and red[] are reused
+    }
+}
+
 // ============================================================== intra-route evaluation
 // One thread per (slot u, intra variant); the thread walks v along the route so
 // the middle segment of Intra-Relocate / Intra-Swap is composed incrementally
@@ -509,8 +582,8 @@ __global__ void __launch_bounds__(kInterThreads) k_inter(const SolView<DT> S, co
 __constant__ int kIntraVariants[13] = {0, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20, 21, 22};
 
 template <class DT, bool TW>
-__global__ void __launch_bounds__(256) k_intra(const SolView<DT> S, ScoreParams sp, uint32_t vmask, int x_lo,
-                                               int x_hi, uint64_t *__restrict__ keys) {
+__device__ __forceinline__ void intra_body(const SolView<DT> &S, const ScoreParams &sp, uint32_t vmask, int x_lo,
+                                           int x_hi, uint64_t *__restrict__ keys) {
     __shared__ unsigned long long red[23];
     if (threadIdx.x < 23) red[threadIdx.x] = kNoKey;
     __syncthreads();
@@ -624,6 +697,20 @@ __global__ void __launch_bounds__(256) k_intra(const SolView<DT> S, ScoreParams 
     __syncthreads();
     if (threadIdx.x < 23 && red[threadIdx.x] != kNoKey)
         atomicMin(reinterpret_cast<unsigned long long *>(keys) + threadIdx.x, red[threadIdx.x]);
+}
+
+template <class DT, bool TW>
+__global__ void __launch_bounds__(256) k_intra(const __grid_constant__ SolView<DT> S, ScoreParams sp, uint32_t vmask,
+                                               int x_lo, int x_hi, uint64_t *__restrict__ keys) {
+    intra_body<DT, TW>(S, sp, vmask, x_lo, x_hi, keys);
+}
+
+// population mode: blockIdx.y = solution (BASELINE config 5)
+template <class DT, bool TW>
+__global__ void __launch_bounds__(256) k_intra_batch(const SolView<DT> *__restrict__ views, ScoreParams sp,
+                                                     uint32_t vmask, uint64_t *__restrict__ keys) {
+    const SolView<DT> &S = views[blockIdx.y];
+    intra_body<DT, TW>(S, sp, vmask, 0, S.Qp, keys + static_cast<size_t>(blockIdx.y) * 23);
 }
 
 // ============================================================== intra-route evaluation, CVRP
@@ -823,6 +910,60 @@ cudaError_t launch_intra(uint32_t mask, bool tw, const SolView<DT> &S, const Sco
     ++g_launches;
     return cudaGetLastError();
 }
+
+template <class DT, bool TW>
+static cudaError_t launch_inter_batch_tw(uint32_t mask, const SolView<DT> *views, const CUtensorMap *maps,
+                                         const uint32_t *work, int n_work, const ScoreParams &sp, uint64_t *keys,
+                                         int grid, cudaStream_t st) {
+    cudaError_t err = cudaSuccess;
+    const int smem = 2 * kBoxBytesPadded + 128;
+    auto run = [&](auto kmask) {
+        if (err != cudaSuccess) return;
+        auto kern = k_inter_batch<DT, TW, decltype(kmask)::value>;
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            attr = true;
+        }
+        kern<<<grid, kInterThreads, smem, st>>>(views, maps, work, n_work, sp, keys);
+        ++g_launches;
+        err = cudaGetLastError();
+    };
+    constexpr uint32_t ALL = 0x7FEu, NS = (1u << 1) | (1u << 2) | (1u << 5);
+    if ((mask & ALL) == ALL) { run(std::integral_constant<uint32_t, ALL>{}); return err; }
+    if ((mask & NS) == NS) { run(std::integral_constant<uint32_t, NS>{}); mask &= ~NS; }
+    if (mask & (1u << 1)) run(std::integral_constant<uint32_t, (1u << 1)>{});
+    if (mask & (1u << 2)) run(std::integral_constant<uint32_t, (1u << 2)>{});
+    if (mask & (3u << 3)) run(std::integral_constant<uint32_t, (3u << 3)>{});
+    if (mask & (1u << 5)) run(std::integral_constant<uint32_t, (1u << 5)>{});
+    if (mask & (0x1Fu << 6)) run(std::integral_constant<uint32_t, (0x1Fu << 6)>{});
+    return err;
+}
+
+template <class DT>
+cudaError_t launch_batch(uint32_t mask, bool tw, const SolView<DT> *views, const CUtensorMap *maps,
+                         const uint32_t *work, int n_work, int n_sol, int max_qp, const ScoreParams &sp,
+                         uint64_t *keys, int grid, cudaStream_t st) {
+    cudaError_t e = cudaSuccess;
+    if (n_work > 0 && (mask & 0x7FEu))
+        e = tw ? launch_inter_batch_tw<DT, true>(mask, views, maps, work, n_work, sp, keys, grid, st)
+               : launch_inter_batch_tw<DT, false>(mask, views, maps, work, n_work, sp, keys, grid, st);
+    const uint32_t intra = mask & ((1u << 0) | (0x7u << 11) | (0x1FFu << 14));
+    if (e == cudaSuccess && intra && n_sol > 0) {
+        dim3 g((max_qp * 13 + 255) / 256, n_sol);
+        if (tw) k_intra_batch<DT, true><<<g, 256, 0, st>>>(views, sp, intra, keys);
+        else    k_intra_batch<DT, false><<<g, 256, 0, st>>>(views, sp, intra, keys);
+        ++g_launches;
+        e = cudaGetLastError();
+    }
+    return e;
+}
+template cudaError_t launch_batch<int32_t>(uint32_t, bool, const SolView<int32_t> *, const CUtensorMap *,
+                                           const uint32_t *, int, int, int, const ScoreParams &, uint64_t *, int,
+                                           cudaStream_t);
+template cudaError_t launch_batch<float>(uint32_t, bool, const SolView<float> *, const CUtensorMap *,
+                                         const uint32_t *, int, int, int, const ScoreParams &, uint64_t *, int,
+                                         cudaStream_t);
 
 // explicit instantiations
 template cudaError_t launch_dp<int32_t>(int32_t *, int, const int32_t *, const int32_t *, int, int, int, int, bool,

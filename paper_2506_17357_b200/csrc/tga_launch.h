@@ -70,6 +70,10 @@ cudaError_t launch_inter(uint32_t mask, bool tw, const SolView<DT> &S, const CUt
 template <class DT>
 cudaError_t launch_intra(uint32_t mask, bool tw, const SolView<DT> &S, const ScoreParams &sp, int x_lo, int x_hi,
                          uint64_t *keys, cudaStream_t st, bool small_dist = false);
+template <class DT>
+cudaError_t launch_batch(uint32_t mask, bool tw, const SolView<DT> *views, const CUtensorMap *maps,
+                         const uint32_t *work, int n_work, int n_sol, int max_qp, const ScoreParams &sp,
+                         uint64_t *keys, int grid, cudaStream_t st);
 unsigned long long launch_count();
 void note_launch();
 cudaError_t launch_inter_fast(uint32_t mask, const SlotRec *rec, const CUtensorMap &map, const uint32_t *tiles, int t_lo,

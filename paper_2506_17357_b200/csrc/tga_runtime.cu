@@ -144,6 +144,7 @@ struct tga_solution {
     int sm_count = 148;
     uint64_t eval_gen = 0;
     uint32_t eval_mask = 0;
+    bool drained = false;  // the stream was synchronised after the last enqueued work
     // live timing of the inter-route launch (ring of event pairs)
     bool timing = false;
     std::vector<cudaEvent_t> tev;
@@ -275,6 +276,7 @@ static SolView<DT> sol_view(const tga_solution *s) {
     v.pitch = s->pitch;
     v.Qp = s->Qp;
     v.Qc = static_cast<uint32_t>(s->Qc);
+    v.tiles = s->d_tiles;
     return v;
 }
 
@@ -682,6 +684,7 @@ extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
     }
     s->eval_mask = accumulate ? (s->eval_mask | mask) : mask;
     s->eval_gen = s->gen;
+    s->drained = false;
     return TGA_OK;
 }
 
@@ -713,19 +716,27 @@ static void canon_to_rp(const tga_solution *s, int c, int *r, int *p) {
     *p = c - s->cbase[*r];
 }
 
+static int32_t decode_best(const tga_solution *s, const uint64_t *keys, uint32_t mask, tga_move *out);
+
 extern "C" int32_t tga_best_move(tga_solution *s, uint32_t mask, tga_move *out) {
     if (!s || !out) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL argument");
     if (s->eval_gen != s->gen) return fail(TGA_ERR_STALE, "no evaluation for the current generation");
     TGA_CUDA(cudaMemcpyAsync(s->h_keys, s->keys, TGA_N_VARIANTS * 8, cudaMemcpyDeviceToHost, s->stream));
     TGA_CUDA(cudaStreamSynchronize(s->stream));
+    s->drained = true;
     mask &= s->eval_mask;
+    return decode_best(s, s->h_keys, mask, out);
+}
+
+// lowest (score, variant rank, flat index) over the keys of `mask` -> tga_move
+static int32_t decode_best(const tga_solution *s, const uint64_t *keys, uint32_t mask, tga_move *out) {
     int bv = -1;
     uint64_t bk = ~0ull;
     for (int v = 0; v < TGA_N_VARIANTS; ++v) {
         if (!(mask & (1u << v))) continue;
-        const uint64_t k = s->h_keys[v];
+        const uint64_t k = keys[v];
         if (k == ~0ull) continue;
-        // lowest (score, variant rank, flat index); variants visited in rank order
+        // variants visited in rank order: a later variant wins only with a strictly lower score
         if (bv < 0 || (k >> 32) < (bk >> 32)) { bv = v; bk = k; }
     }
     std::memset(out, 0, sizeof(*out));
@@ -810,7 +821,8 @@ extern "C" int32_t tga_apply_move(tga_solution *s, const tga_move *m) {
     if (m->generation != s->gen) return fail(TGA_ERR_STALE, "move generation does not match the solution");
     if (m->variant < 0 || m->variant >= TGA_N_VARIANTS) return fail(TGA_ERR_INVALID_ARGUMENT, "variant");
     if (set_device(s->inst) != TGA_OK) return TGA_ERR_CUDA;
-    TGA_CUDA(cudaStreamSynchronize(s->stream));  // the staging buffer / route arrays may still be in use
+    if (!s->drained) TGA_CUDA(cudaStreamSynchronize(s->stream));  // staging buffers may still be in flight
+    s->drained = false;
     if (!splice(s->routes, m)) return fail(TGA_ERR_INVALID_ARGUMENT, "move positions out of range for its variant");
     compute_bases(s);
     const int r_lo = std::min(m->route_a, m->route_b), r_hi = std::max(m->route_a, m->route_b);
@@ -1007,6 +1019,7 @@ extern "C" int32_t tga_solution_reload(tga_solution *s, int32_t R, const int32_t
     if ((rc = upload_layout(s, 0, R - 1)) != TGA_OK) return rc;
     if ((rc = refresh(s, 0, R - 1, true)) != TGA_OK) return rc;
     ++s->gen;
+    s->drained = false;
     return TGA_OK;
 }
 
@@ -1033,6 +1046,173 @@ extern "C" int32_t tga_solution_timings(tga_solution *s, float *ms, int32_t max_
     }
     s->tev_n = 0;
     *n_out = n;
+    return TGA_OK;
+}
+
+// ============================================================== ABI: population batch
+struct tga_batch {
+    tga_instance *inst = nullptr;
+    std::vector<tga_solution *> sols;
+    cudaStream_t stream = nullptr;
+    void *d_views = nullptr;        // SolView<DT>[n]
+    CUtensorMap *d_maps = nullptr;  // [n]
+    uint32_t *d_work = nullptr;     // (solution << 20 | tile) work items
+    uint64_t *d_keys = nullptr;     // [n][23]
+    uint64_t *h_keys = nullptr;     // pinned [n][23]
+    int n_work = 0, max_qp = 0, sm_count = 148;
+    uint32_t eval_mask = 0;
+    std::vector<uint64_t> eval_gen;
+};
+
+static void free_batch(tga_batch *b) {
+    if (!b) return;
+    for (auto *s : b->sols) free_solution(s);
+    if (b->d_views) cudaFree(b->d_views);
+    if (b->d_maps) cudaFree(b->d_maps);
+    if (b->d_work) cudaFree(b->d_work);
+    if (b->d_keys) cudaFree(b->d_keys);
+    if (b->h_keys) cudaFreeHost(b->h_keys);
+    if (b->stream) cudaStreamDestroy(b->stream);
+    delete b;
+}
+
+extern "C" int32_t tga_batch_load(tga_instance *I, int32_t n_sol, const int32_t *n_routes, const int32_t *route_ptr,
+                                  const int32_t *customers, tga_batch **out) {
+    if (!I || !n_routes || !route_ptr || !customers || !out || n_sol < 1 || n_sol > 4096)
+        return fail(TGA_ERR_INVALID_ARGUMENT, "batch arguments");
+    *out = nullptr;
+    if (set_device(I) != TGA_OK) return TGA_ERR_CUDA;
+    auto *b = new (std::nothrow) tga_batch();
+    if (!b) return fail(TGA_ERR_OOM, "host allocation");
+    b->inst = I;
+    auto bail = [&](int32_t code) { free_batch(b); return code; };
+    if (cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking) != cudaSuccess)
+        return bail(fail(TGA_ERR_CUDA, "stream"));
+    size_t rp = 0;
+    const int ncust = I->n - 1;
+    std::vector<uint32_t> work;
+    for (int k = 0; k < n_sol; ++k) {
+        tga_solution *s = nullptr;
+        int32_t rc = tga_solution_load(I, n_routes[k], route_ptr + rp, customers + static_cast<size_t>(k) * ncust, &s);
+        if (rc != TGA_OK) return bail(rc);
+        b->sols.push_back(s);
+        tga_solution_set_stream(s, b->stream);
+        rp += static_cast<size_t>(n_routes[k]) + 1;
+        b->max_qp = std::max(b->max_qp, s->Qp);
+        if (s->n_tiles >= (1 << 20)) return bail(fail(TGA_ERR_INVALID_ARGUMENT, "too many tiles per solution"));
+        for (int t = 0; t < s->n_tiles; ++t) work.push_back((static_cast<uint32_t>(k) << 20) | static_cast<uint32_t>(t));
+    }
+    b->n_work = static_cast<int>(work.size());
+    b->eval_gen.assign(n_sol, 0);
+    {
+        cudaDeviceProp prop;
+        if (cudaGetDeviceProperties(&prop, I->device) == cudaSuccess) b->sm_count = prop.multiProcessorCount;
+    }
+    const size_t vsz = I->dtype == TGA_I32 ? sizeof(SolView<int32_t>) : sizeof(SolView<float>);
+    std::vector<unsigned char> views(vsz * n_sol);
+    std::vector<CUtensorMap> maps(n_sol);
+    for (int k = 0; k < n_sol; ++k) {
+        if (I->dtype == TGA_I32) { auto v = sol_view<int32_t>(b->sols[k]); std::memcpy(&views[vsz * k], &v, vsz); }
+        else { auto v = sol_view<float>(b->sols[k]); std::memcpy(&views[vsz * k], &v, vsz); }
+        maps[k] = b->sols[k]->tmap;
+    }
+    if (cudaMalloc(&b->d_views, views.size()) != cudaSuccess ||
+        cudaMalloc(&b->d_maps, sizeof(CUtensorMap) * n_sol) != cudaSuccess ||
+        cudaMalloc(&b->d_work, sizeof(uint32_t) * std::max<size_t>(1, work.size())) != cudaSuccess ||
+        cudaMalloc(&b->d_keys, sizeof(uint64_t) * TGA_N_VARIANTS * n_sol) != cudaSuccess ||
+        cudaMallocHost(&b->h_keys, sizeof(uint64_t) * TGA_N_VARIANTS * n_sol) != cudaSuccess)
+        return bail(fail(TGA_ERR_OOM, "batch allocation"));
+    if (cudaMemcpy(b->d_views, views.data(), views.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(b->d_maps, maps.data(), sizeof(CUtensorMap) * n_sol, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(b->d_work, work.data(), sizeof(uint32_t) * work.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+        return bail(fail(TGA_ERR_CUDA, "batch upload"));
+    *out = b;
+    return TGA_OK;
+}
+
+extern "C" int32_t tga_batch_destroy(tga_batch *b) {
+    free_batch(b);
+    return TGA_OK;
+}
+
+extern "C" int32_t tga_batch_size(const tga_batch *b, int32_t *n_sol) {
+    if (!b || !n_sol) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL argument");
+    *n_sol = static_cast<int32_t>(b->sols.size());
+    return TGA_OK;
+}
+
+extern "C" int32_t tga_batch_solution(tga_batch *b, int32_t i, tga_solution **out) {
+    if (!b || !out || i < 0 || i >= static_cast<int>(b->sols.size())) return fail(TGA_ERR_INVALID_ARGUMENT, "index");
+    *out = b->sols[i];
+    return TGA_OK;
+}
+
+extern "C" int32_t tga_batch_eval(tga_batch *b, uint32_t mask, void *stream) {
+    if (!b) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL batch");
+    const tga_instance *I = b->inst;
+    mask &= TGA_OP_ALL;
+    if ((mask & TGA_OP_2OPT) && I->tw) return fail(TGA_ERR_UNSUPPORTED, "2-opt with time windows (P:148)");
+    if (set_device(I) != TGA_OK) return TGA_ERR_CUDA;
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : b->stream;
+    const int n = static_cast<int>(b->sols.size());
+    TGA_CUDA(cudaMemsetAsync(b->d_keys, 0xFF, sizeof(uint64_t) * TGA_N_VARIANTS * n, st));
+    ScoreParams sp{I->Q, I->opt.score_mode, I->opt.w_load, I->opt.w_tw};
+    const int grid = std::max(1, std::min(b->n_work, b->sm_count * 4));
+    cudaError_t e = I->dtype == TGA_I32
+        ? launch_batch<int32_t>(mask, I->tw, static_cast<const SolView<int32_t> *>(b->d_views), b->d_maps, b->d_work,
+                                b->n_work, n, b->max_qp, sp, b->d_keys, grid, st)
+        : launch_batch<float>(mask, I->tw, static_cast<const SolView<float> *>(b->d_views), b->d_maps, b->d_work,
+                              b->n_work, n, b->max_qp, sp, b->d_keys, grid, st);
+    if (e != cudaSuccess) return fail(TGA_ERR_CUDA, std::string("batch eval: ") + cudaGetErrorString(e));
+    if (st != b->stream) {
+        cudaEvent_t ev;
+        TGA_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        TGA_CUDA(cudaEventRecord(ev, st));
+        TGA_CUDA(cudaStreamWaitEvent(b->stream, ev, 0));
+        cudaEventDestroy(ev);
+    }
+    b->eval_mask = mask;
+    for (int k = 0; k < n; ++k) {
+        b->eval_gen[k] = b->sols[k]->gen;
+        b->sols[k]->drained = false;
+    }
+    return TGA_OK;
+}
+
+extern "C" int32_t tga_batch_keys(tga_batch *b, uint64_t *keys) {
+    if (!b || !keys) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL argument");
+    const size_t bytes = sizeof(uint64_t) * TGA_N_VARIANTS * b->sols.size();
+    TGA_CUDA(cudaMemcpyAsync(b->h_keys, b->d_keys, bytes, cudaMemcpyDeviceToHost, b->stream));
+    TGA_CUDA(cudaStreamSynchronize(b->stream));
+    std::memcpy(keys, b->h_keys, bytes);
+    return TGA_OK;
+}
+
+extern "C" int32_t tga_batch_best_moves(tga_batch *b, uint32_t mask, tga_move *out, int32_t *status) {
+    if (!b || !out) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL argument");
+    const int n = static_cast<int>(b->sols.size());
+    TGA_CUDA(cudaMemcpyAsync(b->h_keys, b->d_keys, sizeof(uint64_t) * TGA_N_VARIANTS * n, cudaMemcpyDeviceToHost,
+                             b->stream));
+    TGA_CUDA(cudaStreamSynchronize(b->stream));
+    mask &= b->eval_mask;
+    for (int k = 0; k < n; ++k) {
+        tga_solution *s = b->sols[k];
+        s->drained = true;
+        if (b->eval_gen[k] != s->gen) return fail(TGA_ERR_STALE, "batch evaluation is stale");
+        const int32_t rc = decode_best(s, b->h_keys + static_cast<size_t>(k) * TGA_N_VARIANTS, mask, &out[k]);
+        if (status) status[k] = rc;
+    }
+    return TGA_OK;
+}
+
+extern "C" int32_t tga_batch_apply_moves(tga_batch *b, const tga_move *moves, const int32_t *apply) {
+    if (!b || !moves) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL argument");
+    for (size_t k = 0; k < b->sols.size(); ++k) {
+        if (apply && !apply[k]) continue;
+        if (moves[k].variant < 0) continue;
+        const int32_t rc = tga_apply_move(b->sols[k], &moves[k]);
+        if (rc != TGA_OK) return rc;
+    }
     return TGA_OK;
 }
 

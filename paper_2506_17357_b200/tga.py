@@ -98,6 +98,15 @@ _SYMBOLS = {
     "tga_shard_range": (C.c_int32, [C.c_int64, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
     "tga_nccl_unique_id": (C.c_int32, [C.c_void_p]),
     "tga_comm_init": (C.c_int32, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
+    "tga_batch_load": (C.c_int32, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                   C.c_void_p]),
+    "tga_batch_destroy": (C.c_int32, [C.c_void_p]),
+    "tga_batch_size": (C.c_int32, [C.c_void_p, C.c_void_p]),
+    "tga_batch_solution": (C.c_int32, [C.c_void_p, C.c_int32, C.c_void_p]),
+    "tga_batch_eval": (C.c_int32, [C.c_void_p, C.c_uint32, C.c_void_p]),
+    "tga_batch_keys": (C.c_int32, [C.c_void_p, C.c_void_p]),
+    "tga_batch_best_moves": (C.c_int32, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p]),
+    "tga_batch_apply_moves": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "tga_last_error": (C.c_char_p, []),
     "tga_version": (C.c_char_p, []),
     "tga_launch_count": (C.c_uint64, []),
@@ -324,6 +333,72 @@ class Solution:
     def comm_init(self, rank: int, world: int, uid: bytes) -> None:
         buf = (C.c_char * 128).from_buffer_copy(uid)
         _check(lib().tga_comm_init(self._h, rank, world, C.cast(buf, C.c_void_p)))
+
+
+class _Borrowed(Solution):
+    """A solution owned by a Batch (not destroyed by Python)."""
+
+    def __init__(self, inst, handle):
+        self.inst = inst
+        self._h = handle
+
+    def close(self):
+        self._h = None
+
+
+class Batch:
+    """tga_batch_*: a population of solutions of one instance evaluated together
+    (BASELINE config 5)."""
+
+    def __init__(self, inst: Instance, solutions):
+        self.inst = inst
+        n_routes, ptrs, custs = [], [], []
+        for sol in solutions:
+            ptr, cust = _csr(sol)
+            n_routes.append(len(ptr) - 1)
+            ptrs.append(ptr)
+            custs.append(cust)
+        self.n = len(n_routes)
+        nr = np.array(n_routes, dtype=np.int32)
+        ptr_all = np.ascontiguousarray(np.concatenate(ptrs), dtype=np.int32)
+        cust_all = np.ascontiguousarray(np.concatenate(custs), dtype=np.int32)
+        h = C.c_void_p()
+        _check(lib().tga_batch_load(inst.handle, self.n, _p(nr), _p(ptr_all), _p(cust_all), C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().tga_batch_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def solution(self, i: int) -> Solution:
+        h = C.c_void_p()
+        _check(lib().tga_batch_solution(self._h, i, C.byref(h)))
+        return _Borrowed(self.inst, h)
+
+    def eval(self, op_mask: int = OP_ALL, stream=None) -> None:
+        _check(lib().tga_batch_eval(self._h, op_mask, _stream_ptr(stream)))
+
+    def keys(self) -> np.ndarray:
+        k = np.zeros((self.n, N_VARIANTS), dtype=np.uint64)
+        _check(lib().tga_batch_keys(self._h, _p(k)))
+        return k
+
+    def best_moves(self, op_mask: int = OP_ALL):
+        moves = (Move * self.n)()
+        status = np.zeros(self.n, dtype=np.int32)
+        _check(lib().tga_batch_best_moves(self._h, op_mask, C.cast(moves, C.c_void_p), _p(status)))
+        return status, moves
+
+    def apply(self, moves, apply_mask=None) -> None:
+        am = None if apply_mask is None else np.ascontiguousarray(apply_mask, dtype=np.int32)
+        _check(lib().tga_batch_apply_moves(self._h, C.cast(moves, C.c_void_p), _p(am)))
 
 
 def decode_key(key: int, integer: bool = True):

@@ -299,3 +299,64 @@ def test_step_reload_and_timing():
     fresh.eval(T.OP_ALL)
     np.testing.assert_array_equal(b.keys(), fresh.keys())
     assert b.routes() == fresh.routes()
+
+
+# ---------------------------------------------------------------- population batch (config 5)
+@pytest.mark.parametrize("mode", [0, 1])
+def test_batch_population_exact(mode):
+    """BASELINE config 5 shape (R1_2-like VRPTW, 200 customers) at reduced
+    population: every solution's 22 keys (2-opt is CVRP-only) == oracle."""
+    _need_gpu()
+    inst, sols = G.population(0, n=200, n_sol=24)
+    gi = T.Instance.from_gen(inst, score_mode=mode)
+    b = T.Batch(gi, sols)
+    mask = T.OP_ALL & ~T.OP_2OPT
+    b.eval(mask)
+    keys = b.keys()
+    orc = O.Oracle.from_instance(inst)
+    for k, sol in enumerate(sols):
+        Q = O.canonical_q(sol)
+        for v in INTER + INTRA_TW:
+            m = orc.best_move(sol, v, mode=mode)
+            exp = oracle_key(m, Q)
+            kk = int(keys[k, v])
+            got = None if kk == 0xFFFFFFFFFFFFFFFF else T.decode_key(kk)
+            assert got == exp, (k, v, got, exp)
+
+
+def test_batch_full_population_1024():
+    """Full config 5 (1024 solutions): batch keys == single-solution keys for
+    every solution, a seeded sample of 32 == oracle; one batch step of
+    best moves + apply keeps every solution consistent with a fresh load."""
+    _need_gpu()
+    inst, sols = G.config("cfg5")
+    assert len(sols) == 1024
+    gi = T.Instance.from_gen(inst)
+    b = T.Batch(gi, sols)
+    mask = T.OP_ALL & ~T.OP_2OPT
+    b.eval(mask)
+    keys = b.keys()
+    rng = np.random.default_rng(5)
+    orc = O.Oracle.from_instance(inst)
+    for k in rng.choice(1024, size=32, replace=False):
+        sol = sols[int(k)]
+        Q = O.canonical_q(sol)
+        for v in INTER + INTRA_TW:
+            m = orc.best_move(sol, v)
+            exp = oracle_key(m, Q)
+            kk = int(keys[k, v])
+            got = None if kk == 0xFFFFFFFFFFFFFFFF else T.decode_key(kk)
+            assert got == exp, (int(k), v, got, exp)
+    for k in range(0, 1024, 97):
+        single = T.Solution(gi, sols[k])
+        single.eval(mask)
+        np.testing.assert_array_equal(single.keys(), keys[k])
+    status, moves = b.best_moves(mask)
+    b.apply(moves, apply_mask=(status == 0))
+    b.eval(mask)
+    keys2 = b.keys()
+    for k in range(0, 1024, 131):
+        routes = b.solution(k).routes()
+        fresh = T.Solution(gi, routes)
+        fresh.eval(mask)
+        np.testing.assert_array_equal(fresh.keys(), keys2[k])

@@ -188,6 +188,79 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ tga arm
+def run_population(args, ws, rank, local, dev):
+    """BASELINE config 5: 1024 VRPTW solutions (200 customers) evaluated as one
+    batch; N ranks split the population (each owns 1024/N solutions, no
+    collective).  A step = batch eval of every variant + best moves + apply."""
+    import torch
+    import tga_gen as G
+    from paper_2506_17357_b200 import tga as T
+    inst, sols = G.config("cfg5", args.seed)
+    lo, hi = T.shard_range(len(sols), rank, ws)
+    mine = sols[lo:hi]
+    stream = torch.cuda.Stream(device=dev)
+    gi = T.Instance.from_gen(inst)
+    b = T.Batch(gi, mine)
+    mask = T.OP_ALL & ~T.OP_2OPT
+
+    def counts_total():
+        return sum(int(sum(int(x) for v, x in enumerate(b.solution(k).counts()) if (mask >> v) & 1))
+                   for k in range(len(mine)))
+
+    def step():
+        b.eval(mask, stream)
+        status, moves = b.best_moves(mask)
+        b.apply(moves, apply_mask=(status == 0))
+        return int((status == 0).sum())
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize(dev)
+    K = min(args.steps, 20)
+    cand = 0
+    sampler = ClockSampler(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    sampler.start()
+    launches0 = T.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    applied = 0
+    tot_ms = 0.0
+    for _ in range(K):
+        c = counts_total()
+        cand += c
+        e0.record(stream)
+        applied += step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        tot_ms += e0.elapsed_time(e1)
+    launches = T.launch_count() - launches0
+    clocks = sampler.stop()
+    if ws > 1:
+        import torch.distributed as dist
+        t = torch.tensor([tot_ms, float(cand)], device=dev, dtype=torch.float64)
+        tm = t.clone()
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        tot_ms, cand = float(tm[0].item()), float(t[1].item())
+    if rank != 0:
+        return 0
+    line = {"metric": METRIC, "value": cand / (tot_ms / 1e3), "unit": UNIT, "n_gpus": ws, "steps": K,
+            "warmup": max(args.warmup, 3), "ms_per_step": tot_ms / K, "higher_is_better": True,
+            "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None, "dtype": "f32 (integer-valued)",
+            "data": "synthetic",
+            "config": {"workload": "cfg5: population 1024 x VRPTW 200 customers (R1_2-like, TW-I); "
+                                   "step = batch eval of 22 variants + best moves + apply",
+                       "solutions": len(sols), "parallelism": f"population split x{ws}"},
+            "applied_moves": applied, "gpu_launches": int(launches), "clocks": clocks,
+            "roofline": None, "cpu_baseline": None,
+            "e2e": None}
+    print(json.dumps(line, default=float), flush=True)
+    return 0
+
+
 def run_tga(args):
     import torch
     ws, rank, local = dist_init(args)
@@ -196,6 +269,8 @@ def run_tga(args):
     if ws > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
+    if args.config == "cfg5":
+        return run_population(args, ws, rank, local, dev)
     import tga_gen as G
     from paper_2506_17357_b200 import tga as T
 

@@ -154,6 +154,17 @@ struct tga_solution {
 // ============================================================== helpers
 static bool is_intra_variant(int v) { return v == TGA_V_2OPT || v >= TGA_V_IRELOCATE1; }
 
+// make `later` wait for everything already enqueued on `earlier`
+static cudaError_t order_after(cudaStream_t later, cudaStream_t earlier) {
+    cudaEvent_t ev;
+    cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+    e = cudaEventRecord(ev, earlier);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(later, ev, 0);
+    cudaEventDestroy(ev);
+    return e;
+}
+
 static int32_t set_device(const tga_instance *inst) {
     TGA_CUDA(cudaSetDevice(inst->device));
     (void)cudaGetLastError();  // drop non-sticky errors left by other code on this thread
@@ -513,8 +524,10 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
         }
     }
     // guards: ints -> -1 (route/pos/rlen/canon invalid), node -> 0 (a valid node id)
-    if (cudaMemset(s->arena, 0xFF, total) != cudaSuccess) return bail(fail(TGA_ERR_CUDA, "memset"));
-    if (cudaMemset(v_node, 0, cap * 4) != cudaSuccess) return bail(fail(TGA_ERR_CUDA, "memset"));
+    // every initialisation is ordered on the solution's (non-blocking) stream: a
+    // legacy-stream cudaMemset would not be ordered before the layout upload
+    if (cudaMemsetAsync(s->arena, 0xFF, total, s->stream) != cudaSuccess) return bail(fail(TGA_ERR_CUDA, "memset"));
+    if (cudaMemsetAsync(v_node, 0, cap * 4, s->stream) != cudaSuccess) return bail(fail(TGA_ERR_CUDA, "memset"));
     auto g32 = [&](void *p) { return static_cast<int32_t *>(p) + kGuard; };
     auto g128 = [&](void *p) { return static_cast<TwRec *>(p) + kGuard; };
     s->node = g32(v_node); s->route = g32(v_route); s->pos = g32(v_pos); s->rlen = g32(v_rlen);
@@ -535,14 +548,16 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
         p.c = -1; p.r = -1; p.fL = p.bL1 = p.W = kPoison;
         for (int k = 0; k < 3; ++k) { p.so[k] = kPoison; p.sA[k] = kPoison; }
         std::vector<SlotRec> init(cap, p);
-        if (cudaMemcpy(v_rec, init.data(), cap * sizeof(SlotRec), cudaMemcpyHostToDevice) != cudaSuccess)
+        if (cudaMemcpyAsync(v_rec, init.data(), cap * sizeof(SlotRec), cudaMemcpyHostToDevice, s->stream) !=
+                cudaSuccess ||
+            cudaStreamSynchronize(s->stream) != cudaSuccess)  // `init` is pageable and local
             return bail(fail(TGA_ERR_CUDA, "record init"));
     }
     // numeric per-slot arrays start at 0 (guards are only read by masked-out lanes)
     for (void *p : {v_fwdL, v_bwdL, v_en, v_fD, v_bD, v_b1, v_b2, v_b3})
-        if (cudaMemset(p, 0, cap * 4) != cudaSuccess) return bail(fail(TGA_ERR_CUDA, "memset"));
+        if (cudaMemsetAsync(p, 0, cap * 4, s->stream) != cudaSuccess) return bail(fail(TGA_ERR_CUDA, "memset"));
     for (void *p : {v_fT, v_bT, v_s2, v_s3})
-        if (cudaMemset(p, 0, cap * 16) != cudaSuccess) return bail(fail(TGA_ERR_CUDA, "memset"));
+        if (cudaMemsetAsync(p, 0, cap * 16, s->stream) != cudaSuccess) return bail(fail(TGA_ERR_CUDA, "memset"));
     // ---- position-ordered distance matrix
     const size_t dp_bytes = static_cast<size_t>(s->pitch) * s->pitch * 4;
     if (cudaMalloc(&s->Dp, dp_bytes) != cudaSuccess) return bail(fail(TGA_ERR_OOM, "Dp allocation"));
@@ -633,6 +648,7 @@ extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
         return fail(TGA_ERR_UNSUPPORTED, "2-opt is only defined without time windows (P:148)");
     if (set_device(I) != TGA_OK) return TGA_ERR_CUDA;
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s->stream;
+    if (st != s->stream) TGA_CUDA(order_after(st, s->stream));  // see the latest applied move
     if (!accumulate) TGA_CUDA(cudaMemsetAsync(s->keys, 0xFF, TGA_N_VARIANTS * 8, st));
     ScoreParams sp{I->Q, I->opt.score_mode, I->opt.w_load, I->opt.w_tw};
     // row shard of the tile list and of the intra slot range
@@ -674,14 +690,7 @@ extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
         const ncclResult_t r = g_nccl.allReduce(s->keys, s->keys, TGA_N_VARIANTS, kNcclUint64, kNcclMin, s->comm, st);
         if (r != 0) return fail(TGA_ERR_NCCL, std::string("ncclAllReduce: ") + (g_nccl.errStr ? g_nccl.errStr(r) : "?"));
     }
-    if (st != s->stream) {
-        // later synchronous calls use the solution's stream: order them after this eval
-        cudaEvent_t ev;
-        TGA_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-        TGA_CUDA(cudaEventRecord(ev, st));
-        TGA_CUDA(cudaStreamWaitEvent(s->stream, ev, 0));
-        cudaEventDestroy(ev);
-    }
+    if (st != s->stream) TGA_CUDA(order_after(s->stream, st));  // later calls use the solution's stream
     s->eval_mask = accumulate ? (s->eval_mask | mask) : mask;
     s->eval_gen = s->gen;
     s->drained = false;
@@ -1154,6 +1163,7 @@ extern "C" int32_t tga_batch_eval(tga_batch *b, uint32_t mask, void *stream) {
     if ((mask & TGA_OP_2OPT) && I->tw) return fail(TGA_ERR_UNSUPPORTED, "2-opt with time windows (P:148)");
     if (set_device(I) != TGA_OK) return TGA_ERR_CUDA;
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : b->stream;
+    if (st != b->stream) TGA_CUDA(order_after(st, b->stream));
     const int n = static_cast<int>(b->sols.size());
     TGA_CUDA(cudaMemsetAsync(b->d_keys, 0xFF, sizeof(uint64_t) * TGA_N_VARIANTS * n, st));
     ScoreParams sp{I->Q, I->opt.score_mode, I->opt.w_load, I->opt.w_tw};
@@ -1164,13 +1174,7 @@ extern "C" int32_t tga_batch_eval(tga_batch *b, uint32_t mask, void *stream) {
         : launch_batch<float>(mask, I->tw, static_cast<const SolView<float> *>(b->d_views), b->d_maps, b->d_work,
                               b->n_work, n, b->max_qp, sp, b->d_keys, grid, st);
     if (e != cudaSuccess) return fail(TGA_ERR_CUDA, std::string("batch eval: ") + cudaGetErrorString(e));
-    if (st != b->stream) {
-        cudaEvent_t ev;
-        TGA_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-        TGA_CUDA(cudaEventRecord(ev, st));
-        TGA_CUDA(cudaStreamWaitEvent(b->stream, ev, 0));
-        cudaEventDestroy(ev);
-    }
+    if (st != b->stream) TGA_CUDA(order_after(b->stream, st));
     b->eval_mask = mask;
     for (int k = 0; k < n; ++k) {
         b->eval_gen[k] = b->sols[k]->gen;

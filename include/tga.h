@@ -192,6 +192,18 @@ int32_t tga_solution_set_stream(tga_solution *sol, void *cuda_stream);
  * move.  Returns TGA_OK if a move was applied, TGA_NO_IMPROVING_MOVE if not. */
 int32_t tga_step(tga_solution *sol, uint32_t op_mask, tga_move *out);
 
+/* tga_step_async: the same iteration entirely on the device, without a host
+ * round trip: the evaluation kernels, then one kernel
+ * that picks the best key, and -- if improving -- splices the changed routes
+ * in the slot arrays, then the update kernel (bounds read on the device).
+ * Enqueue-only; steps can be issued back to back (or captured in a CUDA
+ * graph).  Host-side queries resynchronise the host route lists lazily.
+ * tga_solution_device_stats returns and clears the candidate counts per
+ * variant accumulated by device steps (counts[TGA_N_VARIANTS]) and the number
+ * of moves they applied (synchronises). */
+int32_t tga_step_async(tga_solution *sol, uint32_t op_mask);
+int32_t tga_solution_device_stats(tga_solution *sol, uint64_t *counts, uint64_t *applied);
+
 /* tga_solution_reload: load another solution of the same instance into an
  * existing solution object (same route count and customer count => same
  * device layout; no allocation): host arrays are copied, the slot layout is
@@ -269,6 +281,9 @@ int32_t tga_batch_eval(tga_batch *batch, uint32_t op_mask, void *cuda_stream);
 int32_t tga_batch_keys(tga_batch *batch, uint64_t *keys);
 int32_t tga_batch_best_moves(tga_batch *batch, uint32_t op_mask, tga_move *out, int32_t *status);
 int32_t tga_batch_apply_moves(tga_batch *batch, const tga_move *moves, const int32_t *apply);
+/* device-resident steps of every solution of the batch (see tga_step_async) */
+int32_t tga_batch_step_async(tga_batch *batch, uint32_t op_mask);
+int32_t tga_batch_device_stats(tga_batch *batch, uint64_t *counts, uint64_t *applied);
 
 /* ------------------------------------------------------------ misc */
 const char *tga_last_error(void);

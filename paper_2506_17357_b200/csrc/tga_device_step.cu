@@ -1,0 +1,252 @@
+// tga_device_step.cu -- device-resident best-improvement step (
+// Alg. A2 lines 5-8; the "Update" step of §5.3.5, without a
+// GPU-CPU round trip -- the paper's observed bottleneck).
+//
+//   k_pick_apply   one CTA per solution: candidate counts of the evaluated
+//                  neighbourhood (closed forms over route lengths), best key
+//                  over the operator mask (lowest (score, variant, index)),
+//                  decode, and -- if improving -- the splice of the 1-2 changed
+//                  routes directly in the slot arrays (snapshot of the changed
+//                  span, piece-wise remap), new route bases / lengths / canonical
+//                  offsets, and a descriptor of the changed span.
+//   k_update_dev   Dp row/column refresh of the span + re-scan of its routes,
+//                  bounds read from the descriptor (grid-stride; no host sync).
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "tga_device.cuh"
+#include "tga_launch.h"
+
+namespace tga {
+
+namespace {
+// a piece of a new route: customers [start, start+len) of old route `src`
+// (1-based positions), possibly reversed (2-opt)
+struct Piece {
+    int src, start, len, rev;
+};
+struct NewRoute {
+    int r, L, np;
+    Piece p[5];
+};
+
+__device__ __forceinline__ void add_piece(NewRoute &nr, int src, int a, int b, int rev = 0) {  // [a, b] inclusive
+    if (b >= a) nr.p[nr.np++] = Piece{src, a, b - a + 1, rev};
+}
+
+__device__ __forceinline__ int find_route(const int32_t *cbase, int R, int c) {
+    int lo = 0, hi = R - 1;  // largest r with cbase[r] <= c
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (cbase[mid] <= c) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ int64_t pz(int64_t x) { return x > 0 ? x : 0; }
+}  // namespace
+
+// ------------------------------------------------------------------ pick + apply
+__global__ void __launch_bounds__(256) k_pick_apply(const DevState *__restrict__ states, uint32_t mask, int integer) {
+    const DevState &S = states[blockIdx.x];
+    const int tid = threadIdx.x;
+    const int R = S.R;
+    // ---- 1. exact candidate counts of the evaluated neighbourhood (closed forms)
+    constexpr int NS = 27;
+    __shared__ unsigned long long sums[NS];
+    if (tid < NS) sums[tid] = 0;
+    __syncthreads();
+    {
+        unsigned long long loc[NS];
+#pragma unroll
+        for (int k = 0; k < NS; ++k) loc[k] = 0;
+        for (int r = tid; r < R; r += blockDim.x) {
+            const int64_t L = S.rlenR[r], X = L + 1;
+            const int64_t x1 = pz(L), x2 = pz(L - 1), x3 = pz(L - 2);
+            loc[0] += X;
+            loc[1] += X * X;
+            loc[2] += x1; loc[3] += x2; loc[4] += x3;
+            loc[5] += x1 * X; loc[6] += x2 * X; loc[7] += x3 * X;
+            loc[8] += x1 * x1; loc[9] += x1 * x2; loc[10] += x1 * x3;
+            loc[11] += x2 * x2; loc[12] += x2 * x3; loc[13] += x3 * x3;
+            loc[14] += L * (L - 1) / 2;
+            loc[15] += x1 * pz(L - 1); loc[16] += x2 * pz(L - 2); loc[17] += x3 * pz(L - 3);
+#pragma unroll
+            for (int a = 1; a <= 3; ++a)
+#pragma unroll
+                for (int b = 1; b <= 3; ++b) {
+                    const int64_t M = L - a - b + 1;
+                    loc[18 + 3 * (a - 1) + (b - 1)] += M >= 1 ? M * (M + 1) / 2 : 0;
+                }
+        }
+#pragma unroll
+        for (int k = 0; k < NS; ++k)
+            if (loc[k]) atomicAdd(&sums[k], loc[k]);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        const long long S1 = sums[0], S2 = sums[1];
+        long long c[23];
+        c[0] = sums[14];
+        c[1] = (S1 * S1 - S2) / 2;
+        for (int N = 1; N <= 3; ++N) c[1 + N] = static_cast<long long>(sums[1 + N]) * S1 - static_cast<long long>(sums[4 + N]);
+        const long long X[4] = {0, static_cast<long long>(sums[2]), static_cast<long long>(sums[3]),
+                                static_cast<long long>(sums[4])};
+        const int n1s[6] = {1, 1, 1, 2, 2, 3}, n2s[6] = {1, 2, 3, 2, 3, 3}, pidx[6] = {8, 9, 10, 11, 12, 13};
+        for (int k = 0; k < 6; ++k) {
+            const long long ordered = X[n1s[k]] * X[n2s[k]] - static_cast<long long>(sums[pidx[k]]);
+            c[5 + k] = (n1s[k] == n2s[k]) ? ordered / 2 : ordered;
+        }
+        for (int N = 1; N <= 3; ++N) c[10 + N] = sums[14 + N];
+        for (int k = 0; k < 9; ++k) c[14 + k] = sums[18 + k];
+        for (int v = 0; v < 23; ++v)
+            if (mask & (1u << v)) S.acc[v] += static_cast<unsigned long long>(c[v]);
+    }
+
+    // ---- 2. best key over the mask, decode, pieces of the new routes
+    __shared__ NewRoute nr[2];
+    __shared__ int sh_n, sh_rlo, sh_rhi, sh_lo, sh_hi, sh_d, sh_applied;
+    if (tid == 0) {
+        int bv = -1;
+        uint64_t bk = ~0ull;
+        for (int v = 0; v < 23; ++v) {
+            if (!(mask & (1u << v))) continue;
+            const uint64_t k = S.keys[v];
+            if (k == ~0ull) continue;
+            if (bv < 0 || (k >> 32) < (bk >> 32)) { bv = v; bk = k; }
+        }
+        bool improving = false;
+        if (bv >= 0) {
+            const uint32_t ord = static_cast<uint32_t>(bk >> 32);
+            if (integer) {
+                improving = ord < 0x80000000u;  // int32 score < 0
+            } else {
+                const uint32_t u = (ord & 0x80000000u) ? (ord ^ 0x80000000u) : ~ord;
+                improving = __uint_as_float(u) < 0.0f;
+            }
+        }
+        sh_applied = 0;
+        if (improving) {
+            const uint32_t idx = static_cast<uint32_t>(bk & 0xFFFFFFFFu);
+            const int cu = static_cast<int>(idx / static_cast<uint32_t>(S.Qc));
+            const int cv = static_cast<int>(idx % static_cast<uint32_t>(S.Qc));
+            const int ra = find_route(S.cbase, R, cu), pa = cu - S.cbase[ra];
+            const int rb = find_route(S.cbase, R, cv), pb = cv - S.cbase[rb];
+            const int La = S.rlenR[ra], Lb = S.rlenR[rb];
+            const int v = bv;
+            NewRoute A{ra, 0, 0, {}}, B{rb, 0, 0, {}};
+            int nroutes = 2;
+            if (v == 1) {  // 2-opt*
+                add_piece(A, ra, 1, pa); add_piece(A, rb, pb + 1, Lb);
+                add_piece(B, rb, 1, pb); add_piece(B, ra, pa + 1, La);
+            } else if (v >= 2 && v <= 4) {  // relocate / or-opt
+                const int N = v - 1;
+                add_piece(A, ra, 1, pa - 1); add_piece(A, ra, pa + N, La);
+                add_piece(B, rb, 1, pb); add_piece(B, ra, pa, pa + N - 1); add_piece(B, rb, pb + 1, Lb);
+            } else if (v >= 5 && v <= 10) {  // swap / cross
+                const int n1s[6] = {1, 1, 1, 2, 2, 3}, n2s[6] = {1, 2, 3, 2, 3, 3};
+                const int N1 = n1s[v - 5], N2 = n2s[v - 5];
+                add_piece(A, ra, 1, pa - 1); add_piece(A, rb, pb, pb + N2 - 1); add_piece(A, ra, pa + N1, La);
+                add_piece(B, rb, 1, pb - 1); add_piece(B, ra, pa, pa + N1 - 1); add_piece(B, rb, pb + N2, Lb);
+            } else if (v == 0) {  // 2-opt
+                nroutes = 1;
+                add_piece(A, ra, 1, pa - 1); add_piece(A, ra, pa, pb, 1); add_piece(A, ra, pb + 1, La);
+            } else if (v >= 11 && v <= 13) {  // intra relocate
+                nroutes = 1;
+                const int N = v - 10;
+                if (pb > pa) {
+                    add_piece(A, ra, 1, pa - 1); add_piece(A, ra, pa + N, pb);
+                    add_piece(A, ra, pa, pa + N - 1); add_piece(A, ra, pb + 1, La);
+                } else {
+                    add_piece(A, ra, 1, pb); add_piece(A, ra, pa, pa + N - 1);
+                    add_piece(A, ra, pb + 1, pa - 1); add_piece(A, ra, pa + N, La);
+                }
+            } else {  // intra swap
+                nroutes = 1;
+                const int N1 = (v - 14) / 3 + 1, N2 = (v - 14) % 3 + 1;
+                add_piece(A, ra, 1, pa - 1); add_piece(A, ra, pb, pb + N2 - 1); add_piece(A, ra, pa + N1, pb - 1);
+                add_piece(A, ra, pa, pa + N1 - 1); add_piece(A, ra, pb + N2, La);
+            }
+            for (int k = 0; k < A.np; ++k) A.L += A.p[k].len;
+            for (int k = 0; k < B.np; ++k) B.L += B.p[k].len;
+            // nr[0] is the lower route of the span
+            if (nroutes == 1 || ra < rb) { nr[0] = A; nr[1] = B; }
+            else { nr[0] = B; nr[1] = A; }
+            sh_n = nroutes;
+            sh_rlo = nr[0].r;
+            sh_rhi = nroutes == 2 ? nr[1].r : nr[0].r;
+            sh_lo = S.rbase[sh_rlo];
+            sh_hi = S.rbase[sh_rhi] + S.rlenR[sh_rhi] + 2;
+            sh_d = nr[0].L - S.rlenR[sh_rlo];  // shift of every route after the first changed one
+            sh_applied = 1;
+        }
+    }
+    __syncthreads();
+    if (!sh_applied) {
+        if (tid == 0) S.desc[0] = 0;
+        return;
+    }
+    const int lo = sh_lo, hi = sh_hi, rlo = sh_rlo, rhi = sh_rhi, dlt = sh_d, nrt = sh_n;
+    // ---- 3. snapshot the changed span of node ids
+    for (int x = lo + tid; x < hi; x += blockDim.x) S.scratch[x - lo] = S.node[x];
+    __syncthreads();
+    // new base / length / canonical base of route r in [rlo, rhi] (old arrays still intact)
+    auto nbase = [&](int r) { return r == rlo ? S.rbase[r] : S.rbase[r] + dlt; };
+    auto ncb = [&](int r) { return r == rlo ? S.cbase[r] : S.cbase[r] + dlt; };
+    auto nlen = [&](int r) { return r == nr[0].r ? nr[0].L : (nrt == 2 && r == nr[1].r ? nr[1].L : S.rlenR[r]); };
+    // ---- 4. rewrite the span slot by slot
+    for (int x = lo + tid; x < hi; x += blockDim.x) {
+        int a = rlo, b = rhi;  // route of new slot x: largest r with nbase(r) <= x
+        while (a < b) {
+            const int m = (a + b + 1) >> 1;
+            if (nbase(m) <= x) a = m;
+            else b = m - 1;
+        }
+        const int r = a, p = x - nbase(r), L = nlen(r);
+        int nd = 0;
+        if (p >= 1 && p <= L) {
+            const NewRoute *chg = (r == nr[0].r) ? &nr[0] : ((nrt == 2 && r == nr[1].r) ? &nr[1] : nullptr);
+            int old_slot;
+            if (chg) {
+                int off = p - 1, k = 0;
+                while (off >= chg->p[k].len) { off -= chg->p[k].len; ++k; }
+                const Piece &pc = chg->p[k];
+                const int op = pc.rev ? pc.start + pc.len - 1 - off : pc.start + off;
+                old_slot = S.rbase[pc.src] + op;
+            } else {
+                old_slot = S.rbase[r] + p;
+            }
+            nd = S.scratch[old_slot - lo];
+        }
+        S.node[x] = nd;
+        S.route[x] = r;
+        S.pos[x] = p;
+        S.rlen[x] = L;
+        S.canon[x] = (p <= L) ? ncb(r) + p : -1;
+    }
+    __syncthreads();
+    // ---- 5. per-route arrays (each thread owns whole routes: no cross-thread hazard)
+    for (int r = rlo + tid; r <= rhi; r += blockDim.x) {
+        const int b = nbase(r), c = ncb(r), L = nlen(r);
+        S.rbase[r] = b;
+        S.cbase[r] = c;
+        S.rlenR[r] = L;
+    }
+    if (tid == 0) {
+        S.desc[0] = 1;
+        S.desc[1] = lo;
+        S.desc[2] = hi;
+        S.desc[3] = rlo;
+        S.desc[4] = rhi + 1;
+        S.acc[23] += 1;
+    }
+}
+
+cudaError_t launch_pick_apply(const DevState *states, int n_sol, bool is_int, uint32_t mask, cudaStream_t st) {
+    k_pick_apply<<<n_sol, 256, 0, st>>>(states, mask, is_int ? 1 : 0);
+    note_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace tga

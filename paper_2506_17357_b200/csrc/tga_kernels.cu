@@ -243,38 +243,71 @@ __global__ void __launch_bounds__(256) k_scan(ScanArgs<DT> A, int r_lo, int r_hi
     scan_route<DT, TW>(A, r, lane);
 }
 
-// The update step of an applied move in ONE launch: blocks
-// [0, nb_rows) refresh Dp rows [lo, hi), blocks [nb_rows, nb_rows + nb_cols)
-// refresh Dp columns [lo, hi) of rows [0, Qp), the rest re-scan routes
-// [r_lo, r_hi) (the scan reads node ids and C, never Dp, so the roles are
-// independent).
+// The update step of an applied move as work units: units
+// [0, hi-lo) refresh Dp rows [lo, hi); the next ceil(Qp/8) units refresh Dp
+// columns [lo, hi) of 8 rows each; the rest re-scan 8 routes each of
+// [r_lo, r_hi) (the scan reads node ids and C, never Dp: independent roles).
 template <class DT, bool TW>
-__global__ void __launch_bounds__(256) k_update(ScanArgs<DT> A, DT *__restrict__ Dp, int pitch, int Qp, int lo, int hi,
-                                                int r_lo, int r_hi, int nb_rows, int nb_cols) {
-    const int b = blockIdx.x;
+__device__ __forceinline__ void update_units(const ScanArgs<DT> &A, DT *__restrict__ Dp, int pitch, int Qp, int lo,
+                                             int hi, int r_lo, int r_hi, int unit0, int ustride) {
     const DT *__restrict__ C = A.C;
     const int n = A.n_nodes;
-    if (b < nb_rows) {
-        const int a = lo + b;
-        const DT *crow = C + static_cast<size_t>(A.node[a]) * n;
-        DT *drow = Dp + static_cast<size_t>(a) * pitch;
-        for (int c = 4 * threadIdx.x; c < pitch; c += 4 * blockDim.x) {
-            const int4 nd = *reinterpret_cast<const int4 *>(A.node + c);
-            *reinterpret_cast<int4 *>(drow + c) =
-                make_int4(bits(__ldg(crow + nd.x)), bits(__ldg(crow + nd.y)), bits(__ldg(crow + nd.z)),
-                          bits(__ldg(crow + nd.w)));
-        }
-    } else if (b < nb_rows + nb_cols) {
-        const int a = (b - nb_rows) * 8 + (threadIdx.x >> 5);
-        if (a < Qp) {
+    const int nb_rows = hi - lo, nb_cols = (Qp + 7) / 8, nb_scan = (r_hi - r_lo + 7) / 8;
+    const int total = nb_rows + nb_cols + nb_scan;
+    for (int b = unit0; b < total; b += ustride) {
+        if (b < nb_rows) {
+            const int a = lo + b;
             const DT *crow = C + static_cast<size_t>(A.node[a]) * n;
             DT *drow = Dp + static_cast<size_t>(a) * pitch;
-            for (int c = lo + (threadIdx.x & 31); c < hi; c += 32) drow[c] = __ldg(crow + A.node[c]);
+            for (int c = 4 * threadIdx.x; c < pitch; c += 4 * blockDim.x) {
+                const int4 nd = *reinterpret_cast<const int4 *>(A.node + c);
+                *reinterpret_cast<int4 *>(drow + c) =
+                    make_int4(bits(__ldg(crow + nd.x)), bits(__ldg(crow + nd.y)), bits(__ldg(crow + nd.z)),
+                              bits(__ldg(crow + nd.w)));
+            }
+        } else if (b < nb_rows + nb_cols) {
+            const int a = (b - nb_rows) * 8 + (threadIdx.x >> 5);
+            if (a < Qp) {
+                const DT *crow = C + static_cast<size_t>(A.node[a]) * n;
+                DT *drow = Dp + static_cast<size_t>(a) * pitch;
+                for (int c = lo + (threadIdx.x & 31); c < hi; c += 32) drow[c] = __ldg(crow + A.node[c]);
+            }
+        } else {
+            const int r = r_lo + (b - nb_rows - nb_cols) * 8 + static_cast<int>(threadIdx.x >> 5);
+            if (r < r_hi) scan_route<DT, TW>(A, r, threadIdx.x & 31);
         }
-    } else {
-        const int r = r_lo + (b - nb_rows - nb_cols) * 8 + static_cast<int>(threadIdx.x >> 5);
-        if (r < r_hi) scan_route<DT, TW>(A, r, threadIdx.x & 31);
     }
+}
+
+template <class DT, bool TW>
+__global__ void __launch_bounds__(256) k_update(ScanArgs<DT> A, DT *__restrict__ Dp, int pitch, int Qp, int lo, int hi,
+                                                int r_lo, int r_hi) {
+    update_units<DT, TW>(A, Dp, pitch, Qp, lo, hi, r_lo, r_hi, blockIdx.x, gridDim.x);
+}
+
+// device-resident variant: bounds from the descriptor written by k_pick_apply
+// (tga_device_step.cu); blockIdx.y = solution; grid-stride over the units.
+template <class DT, bool TW>
+__global__ void __launch_bounds__(256) k_update_dev(const DevState *__restrict__ states,
+                                                    const ScanArgs<DT> *__restrict__ scans) {
+    const DevState &S = states[blockIdx.y];
+    if (S.desc[0] == 0) return;
+    update_units<DT, TW>(scans[blockIdx.y], static_cast<DT *>(S.Dp), S.pitch, S.Qp, S.desc[1], S.desc[2], S.desc[3],
+                         S.desc[4], blockIdx.x, gridDim.x);
+}
+
+cudaError_t launch_update_dev(const DevState *states, const void *scans, int n_sol, bool tw, bool is_int,
+                              int blocks_per_sol, cudaStream_t st) {
+    dim3 g(blocks_per_sol, n_sol);
+    if (is_int) {
+        if (tw) k_update_dev<int32_t, true><<<g, 256, 0, st>>>(states, static_cast<const ScanArgs<int32_t> *>(scans));
+        else    k_update_dev<int32_t, false><<<g, 256, 0, st>>>(states, static_cast<const ScanArgs<int32_t> *>(scans));
+    } else {
+        if (tw) k_update_dev<float, true><<<g, 256, 0, st>>>(states, static_cast<const ScanArgs<float> *>(scans));
+        else    k_update_dev<float, false><<<g, 256, 0, st>>>(states, static_cast<const ScanArgs<float> *>(scans));
+    }
+    note_launch();
+    return cudaGetLastError();
 }
 
 // ============================================================== TMA / mbarrier helpers
@@ -836,8 +869,8 @@ cudaError_t launch_update(const ScanArgs<DT> &A, bool tw, DT *Dp, int pitch, int
     const int nb_rows = hi - lo, nb_cols = (Qp + 7) / 8, nb_scan = (r_hi - r_lo + 7) / 8;
     const int grid = nb_rows + nb_cols + nb_scan;
     if (grid <= 0) return cudaSuccess;
-    if (tw) k_update<DT, true><<<grid, 256, 0, st>>>(A, Dp, pitch, Qp, lo, hi, r_lo, r_hi, nb_rows, nb_cols);
-    else    k_update<DT, false><<<grid, 256, 0, st>>>(A, Dp, pitch, Qp, lo, hi, r_lo, r_hi, nb_rows, nb_cols);
+    if (tw) k_update<DT, true><<<grid, 256, 0, st>>>(A, Dp, pitch, Qp, lo, hi, r_lo, r_hi);
+    else    k_update<DT, false><<<grid, 256, 0, st>>>(A, Dp, pitch, Qp, lo, hi, r_lo, r_hi);
     ++g_launches;
     return cudaGetLastError();
 }

@@ -56,6 +56,21 @@ struct ScanArgs {
     SlotRec *rec;      // CVRP fast-path records (int DT only); may be null
 };
 
+// per-solution device state of the device-resident step (k_pick_apply / k_update_dev)
+struct DevState {
+    int32_t *node, *route, *pos, *rlen, *canon;   // slot arrays (guarded)
+    int32_t *rbase, *rlenR, *cbase;              // per route
+    int32_t *scratch;                            // snapshot of a changed span (cap ints)
+    const uint64_t *keys;                        // 23 packed keys of the last evaluation
+    int32_t *desc;                               // [applied, lo, hi, r_lo, r_hi)
+    unsigned long long *acc;                     // [23] candidate counts + [23] applied moves
+    void *Dp;
+    int32_t R, Qc, Qp, pitch;
+};
+cudaError_t launch_pick_apply(const DevState *states, int n_sol, bool is_int, uint32_t mask, cudaStream_t st);
+cudaError_t launch_update_dev(const DevState *states, const void *scans, int n_sol, bool tw, bool is_int,
+                              int blocks_per_sol, cudaStream_t st);
+
 template <class DT>
 cudaError_t launch_dp(DT *Dp, int pitch, const int32_t *node, const DT *C, int n, int Qp, int lo, int hi,
                       bool full, cudaStream_t st);

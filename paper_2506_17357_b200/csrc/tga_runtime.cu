@@ -118,7 +118,13 @@ struct tga_solution {
     int32_t *fwdL = nullptr, *bwdL = nullptr;
     void *enext = nullptr, *fwdD = nullptr, *bwdD = nullptr, *br1 = nullptr, *br2 = nullptr, *br3 = nullptr;
     TwRec *fwdT = nullptr, *bwdT = nullptr, *seg2T = nullptr, *seg3T = nullptr;
-    int32_t *d_rbase = nullptr, *d_rlenR = nullptr, *d_rW = nullptr;
+    int32_t *d_rbase = nullptr, *d_rlenR = nullptr, *d_cbase = nullptr, *d_rW = nullptr;
+    // device-resident step
+    DevState *d_ds = nullptr;      // this solution's DevState (device copy)
+    void *d_sa = nullptr;          // ScanArgs<DT> (device copy)
+    int32_t *d_desc = nullptr, *d_scratch = nullptr;
+    unsigned long long *d_acc = nullptr;
+    bool host_stale = false;       // host route lists lag behind device-resident steps
     float *d_rTV = nullptr;
     void *d_rD = nullptr;
     void *Dp = nullptr;
@@ -209,10 +215,11 @@ static void stage_layout(tga_solution *s, int r_lo, int r_hi, int *span_lo, int 
         }
     }
     const size_t rq = s->route_pitch / 4;
-    int32_t *rb = s->h_rstage, *rn = rb + rq;
+    int32_t *rb = s->h_rstage, *rn = rb + rq, *rc = rn + rq;
     for (int r = 0; r < s->R; ++r) {
         rb[r] = s->rbase[r];
         rn[r] = static_cast<int32_t>(s->routes[r].size());
+        rc[r] = s->cbase[r];
     }
     *span_lo = lo;
     *span_n = hi - lo;
@@ -226,7 +233,7 @@ static int32_t upload_layout(tga_solution *s, int r_lo, int r_hi) {
     stage_layout(s, r_lo, r_hi, &lo, &n);
     TGA_CUDA(cudaMemcpy2DAsync(s->node + lo, s->lay_pitch, s->h_stage, s->lay_pitch, sizeof(int32_t) * n, 5,
                                cudaMemcpyHostToDevice, s->stream));
-    TGA_CUDA(cudaMemcpy2DAsync(s->d_rbase, s->route_pitch, s->h_rstage, s->route_pitch, sizeof(int32_t) * s->R, 2,
+    TGA_CUDA(cudaMemcpy2DAsync(s->d_rbase, s->route_pitch, s->h_rstage, s->route_pitch, sizeof(int32_t) * s->R, 3,
                                cudaMemcpyHostToDevice, s->stream));
     return TGA_OK;
 }
@@ -291,6 +298,34 @@ static SolView<DT> sol_view(const tga_solution *s) {
     return v;
 }
 
+static DevState make_devstate(const tga_solution *s, const uint64_t *keys) {
+    DevState d;
+    d.node = s->node; d.route = s->route; d.pos = s->pos; d.rlen = s->rlen; d.canon = s->canon;
+    d.rbase = s->d_rbase; d.rlenR = s->d_rlenR; d.cbase = s->d_cbase;
+    d.scratch = s->d_scratch; d.keys = keys; d.desc = s->d_desc; d.acc = s->d_acc; d.Dp = s->Dp;
+    d.R = s->R; d.Qc = s->Qc; d.Qp = s->Qp; d.pitch = s->pitch;
+    return d;
+}
+
+// Device-resident steps changed the routes on the device only: rebuild the host
+// route lists (node ids + route lengths, one D2H each) before any host-side use.
+static int32_t sync_host(tga_solution *s) {
+    if (!s->host_stale) return TGA_OK;
+    TGA_CUDA(cudaStreamSynchronize(s->stream));
+    std::vector<int32_t> nd(s->Qp), L(s->R);
+    TGA_CUDA(cudaMemcpy(nd.data(), s->node, 4 * s->Qp, cudaMemcpyDeviceToHost));
+    TGA_CUDA(cudaMemcpy(L.data(), s->d_rlenR, 4 * s->R, cudaMemcpyDeviceToHost));
+    int b = 0;
+    for (int r = 0; r < s->R; ++r) {
+        s->routes[r].assign(nd.begin() + b + 1, nd.begin() + b + 1 + L[r]);
+        b += L[r] + 2;
+    }
+    compute_bases(s);
+    s->host_stale = false;
+    s->drained = true;
+    return TGA_OK;
+}
+
 static int32_t refresh(tga_solution *s, int r_lo, int r_hi, bool full) {
     const tga_instance *I = s->inst;
     const int lo = full ? 0 : s->rbase[r_lo];
@@ -338,7 +373,7 @@ static void build_tiles(tga_solution *s) {
         for (int J = 0; J < s->pitch / kFastTV && J * kFastTV < s->Qp; ++J)
             if (I * kFastU < J * kFastTV + kFastTV - 1) f.push_back((static_cast<uint32_t>(I) << 16) | J);
     s->n_ftiles = static_cast<int>(f.size());
-    cudaMemcpy(s->d_ftiles, f.data(), sizeof(uint32_t) * f.size(), cudaMemcpyHostToDevice);
+    if (s->d_ftiles) cudaMemcpy(s->d_ftiles, f.data(), sizeof(uint32_t) * f.size(), cudaMemcpyHostToDevice);
 }
 
 static void free_solution(tga_solution *s) {
@@ -501,7 +536,8 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
     struct Item { void **p; size_t bytes; };
     const size_t tiles_max = static_cast<size_t>(s->pitch / kTileU) * (s->pitch / kTileV) + 1;
     void *v_node, *v_route, *v_pos, *v_rlen, *v_canon, *v_fwdL, *v_bwdL, *v_en, *v_fD, *v_bD, *v_b1, *v_b2, *v_b3;
-    void *v_fT, *v_bT, *v_s2, *v_s3, *v_rbase, *v_rlenR, *v_rW, *v_rTV, *v_rD, *v_keys, *v_tiles;
+    void *v_fT, *v_bT, *v_s2, *v_s3, *v_rbase, *v_rlenR, *v_cbase, *v_rW, *v_rTV, *v_rD, *v_keys, *v_tiles;
+    void *v_ds, *v_sa, *v_desc, *v_scr, *v_acc;
     void *v_rec = nullptr, *v_ftiles = nullptr;
     const size_t ftiles_max = static_cast<size_t>(s->pitch / kFastU) * (s->pitch / kFastTV) + 1;
     const bool want_fast = I->dtype == TGA_I32 && !I->tw && I->opt.score_mode == TGA_SCORE_FEASIBLE && I->fast_ok;
@@ -510,7 +546,9 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
         {&v_fwdL, cap * 4}, {&v_bwdL, cap * 4}, {&v_en, cap * 4}, {&v_fD, cap * 4}, {&v_bD, cap * 4},
         {&v_b1, cap * 4}, {&v_b2, cap * 4}, {&v_b3, cap * 4},
         {&v_fT, cap * 16}, {&v_bT, cap * 16}, {&v_s2, cap * 16}, {&v_s3, cap * 16},
-        {&v_rbase, Rr * 4}, {&v_rlenR, Rr * 4}, {&v_rW, Rr * 4}, {&v_rTV, Rr * 4}, {&v_rD, Rr * 4},
+        {&v_rbase, Rr * 4}, {&v_rlenR, Rr * 4}, {&v_cbase, Rr * 4}, {&v_rW, Rr * 4}, {&v_rTV, Rr * 4},
+        {&v_rD, Rr * 4}, {&v_ds, sizeof(DevState)}, {&v_sa, sizeof(ScanArgs<int32_t>)}, {&v_desc, 8 * 4},
+        {&v_scr, cap * 4}, {&v_acc, 48 * 8},
         {&v_keys, TGA_N_VARIANTS * 8}, {&v_tiles, tiles_max * 4},
         {&v_rec, want_fast ? cap * sizeof(SlotRec) : 0}, {&v_ftiles, want_fast ? ftiles_max * 4 : 0}};
     size_t total = 0;
@@ -537,6 +575,10 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
     s->fwdT = g128(v_fT); s->bwdT = g128(v_bT); s->seg2T = g128(v_s2); s->seg3T = g128(v_s3);
     s->d_rbase = static_cast<int32_t *>(v_rbase); s->d_rlenR = static_cast<int32_t *>(v_rlenR);
     s->d_rW = static_cast<int32_t *>(v_rW); s->d_rTV = static_cast<float *>(v_rTV); s->d_rD = v_rD;
+    s->d_cbase = static_cast<int32_t *>(v_cbase);
+    s->d_ds = static_cast<DevState *>(v_ds); s->d_sa = v_sa;
+    s->d_desc = static_cast<int32_t *>(v_desc); s->d_scratch = static_cast<int32_t *>(v_scr);
+    s->d_acc = static_cast<unsigned long long *>(v_acc);
     s->keys = static_cast<uint64_t *>(v_keys);
     s->d_tiles = static_cast<uint32_t *>(v_tiles);
     if (want_fast) {
@@ -565,7 +607,7 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
     s->route_pitch = align_up(Rr * 4, 256);
     if (cudaMallocHost(&s->h_keys, TGA_N_VARIANTS * 8) != cudaSuccess ||
         cudaMallocHost(&s->h_stage, 5 * s->lay_pitch) != cudaSuccess ||
-        cudaMallocHost(&s->h_rstage, 2 * s->route_pitch) != cudaSuccess)
+        cudaMallocHost(&s->h_rstage, 3 * s->route_pitch) != cudaSuccess)
         return bail(fail(TGA_ERR_OOM, "pinned host allocation"));
     // ---- layout upload, Dp build, scan
     if ((rc = upload_layout(s, 0, R - 1)) != TGA_OK) return bail(rc);
@@ -594,6 +636,19 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (cr != CUDA_SUCCESS) return bail(fail(TGA_ERR_CUDA, "fast-path tensor map"));
+    }
+    {   // device-resident step state
+        DevState ds = make_devstate(s, s->keys);
+        if (cudaMemcpyAsync(s->d_ds, &ds, sizeof(ds), cudaMemcpyHostToDevice, s->stream) != cudaSuccess ||
+            cudaMemsetAsync(s->d_acc, 0, 48 * 8, s->stream) != cudaSuccess ||
+            cudaMemsetAsync(s->d_desc, 0, 8 * 4, s->stream) != cudaSuccess)
+            return bail(fail(TGA_ERR_CUDA, "device step state"));
+        cudaError_t e2;
+        if (I->dtype == TGA_I32) { auto a = scan_args<int32_t>(s); e2 = cudaMemcpyAsync(s->d_sa, &a, sizeof(a), cudaMemcpyHostToDevice, s->stream);
+                                   if (e2 == cudaSuccess) e2 = cudaStreamSynchronize(s->stream); }
+        else { auto a = scan_args<float>(s); e2 = cudaMemcpyAsync(s->d_sa, &a, sizeof(a), cudaMemcpyHostToDevice, s->stream);
+               if (e2 == cudaSuccess) e2 = cudaStreamSynchronize(s->stream); }
+        if (e2 != cudaSuccess) return bail(fail(TGA_ERR_CUDA, "device step state"));
     }
     if (cudaStreamSynchronize(s->stream) != cudaSuccess)
         return bail(fail(TGA_ERR_CUDA, std::string("load: ") + cudaGetErrorString(cudaGetLastError())));
@@ -730,6 +785,7 @@ static int32_t decode_best(const tga_solution *s, const uint64_t *keys, uint32_t
 extern "C" int32_t tga_best_move(tga_solution *s, uint32_t mask, tga_move *out) {
     if (!s || !out) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL argument");
     if (s->eval_gen != s->gen) return fail(TGA_ERR_STALE, "no evaluation for the current generation");
+    if (sync_host(s) != TGA_OK) return TGA_ERR_CUDA;
     TGA_CUDA(cudaMemcpyAsync(s->h_keys, s->keys, TGA_N_VARIANTS * 8, cudaMemcpyDeviceToHost, s->stream));
     TGA_CUDA(cudaStreamSynchronize(s->stream));
     s->drained = true;
@@ -830,6 +886,7 @@ extern "C" int32_t tga_apply_move(tga_solution *s, const tga_move *m) {
     if (m->generation != s->gen) return fail(TGA_ERR_STALE, "move generation does not match the solution");
     if (m->variant < 0 || m->variant >= TGA_N_VARIANTS) return fail(TGA_ERR_INVALID_ARGUMENT, "variant");
     if (set_device(s->inst) != TGA_OK) return TGA_ERR_CUDA;
+    if (sync_host(s) != TGA_OK) return TGA_ERR_CUDA;
     if (!s->drained) TGA_CUDA(cudaStreamSynchronize(s->stream));  // staging buffers may still be in flight
     s->drained = false;
     if (!splice(s->routes, m)) return fail(TGA_ERR_INVALID_ARGUMENT, "move positions out of range for its variant");
@@ -843,8 +900,10 @@ extern "C" int32_t tga_apply_move(tga_solution *s, const tga_move *m) {
 }
 
 // ============================================================== ABI: queries
-extern "C" int32_t tga_solution_counts(const tga_solution *s, uint64_t *c) {
-    if (!s || !c) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL argument");
+extern "C" int32_t tga_solution_counts(const tga_solution *cs, uint64_t *c) {
+    if (!cs || !c) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL argument");
+    tga_solution *s = const_cast<tga_solution *>(cs);  // refreshing the host cache only
+    if (sync_host(s) != TGA_OK) return TGA_ERR_CUDA;
     std::memset(c, 0, sizeof(uint64_t) * TGA_N_VARIANTS);
     const int R = s->R;
     std::vector<int64_t> L(R);
@@ -892,8 +951,10 @@ extern "C" int32_t tga_solution_info(const tga_solution *s, int32_t *R, int32_t 
     return TGA_OK;
 }
 
-extern "C" int32_t tga_solution_routes(const tga_solution *s, int32_t *ptr, int32_t *cust) {
-    if (!s || !ptr || !cust) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL argument");
+extern "C" int32_t tga_solution_routes(const tga_solution *cs, int32_t *ptr, int32_t *cust) {
+    if (!cs || !ptr || !cust) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL argument");
+    tga_solution *s = const_cast<tga_solution *>(cs);  // refreshing the host cache only
+    if (sync_host(s) != TGA_OK) return TGA_ERR_CUDA;
     int q = 0;
     ptr[0] = 0;
     for (int r = 0; r < s->R; ++r) {
@@ -929,6 +990,7 @@ extern "C" int32_t tga_solution_cost(tga_solution *s, int64_t *dist_i, double *d
 extern "C" int32_t tga_solution_attributes(tga_solution *s, int64_t *pre_L, int64_t *suf_L, double *pre_D,
                                            double *suf_D, double *pre_TV, double *suf_TV, double *start) {
     if (!s) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL solution");
+    if (sync_host(s) != TGA_OK) return TGA_ERR_CUDA;
     TGA_CUDA(cudaStreamSynchronize(s->stream));
     const int Qp = s->Qp;
     std::vector<int32_t> fL(Qp), bL(Qp), fD(Qp), bD(Qp), nd(Qp);
@@ -1022,6 +1084,7 @@ extern "C" int32_t tga_solution_reload(tga_solution *s, int32_t R, const int32_t
     }
     if (set_device(I) != TGA_OK) return TGA_ERR_CUDA;
     TGA_CUDA(cudaStreamSynchronize(s->stream));  // staging buffers may still be in flight
+    s->host_stale = false;
     for (int r = 0; r < R; ++r) s->routes[r].assign(cust + ptr[r], cust + ptr[r + 1]);
     compute_bases(s);
     int32_t rc;
@@ -1058,6 +1121,33 @@ extern "C" int32_t tga_solution_timings(tga_solution *s, float *ms, int32_t max_
     return TGA_OK;
 }
 
+// ============================================================== ABI: device-resident step
+extern "C" int32_t tga_step_async(tga_solution *s, uint32_t mask) {
+    if (!s) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL solution");
+    int32_t rc = tga_eval(s, mask, nullptr);
+    if (rc != TGA_OK) return rc;
+    const tga_instance *I = s->inst;
+    cudaError_t e = launch_pick_apply(s->d_ds, 1, I->dtype == TGA_I32, s->eval_mask, s->stream);
+    if (e == cudaSuccess)
+        e = launch_update_dev(s->d_ds, s->d_sa, 1, I->tw, I->dtype == TGA_I32, s->sm_count * 2, s->stream);
+    if (e != cudaSuccess) return fail(TGA_ERR_CUDA, std::string("device step: ") + cudaGetErrorString(e));
+    ++s->gen;
+    s->host_stale = true;
+    s->drained = false;
+    return TGA_OK;
+}
+
+extern "C" int32_t tga_solution_device_stats(tga_solution *s, uint64_t *counts, uint64_t *applied) {
+    if (!s) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL solution");
+    unsigned long long acc[48];
+    TGA_CUDA(cudaMemcpyAsync(acc, s->d_acc, sizeof(acc), cudaMemcpyDeviceToHost, s->stream));
+    TGA_CUDA(cudaStreamSynchronize(s->stream));
+    TGA_CUDA(cudaMemsetAsync(s->d_acc, 0, sizeof(acc), s->stream));
+    if (counts) for (int v = 0; v < TGA_N_VARIANTS; ++v) counts[v] = acc[v];
+    if (applied) *applied = acc[23];
+    return TGA_OK;
+}
+
 // ============================================================== ABI: population batch
 struct tga_batch {
     tga_instance *inst = nullptr;
@@ -1071,6 +1161,8 @@ struct tga_batch {
     int n_work = 0, max_qp = 0, sm_count = 148;
     uint32_t eval_mask = 0;
     std::vector<uint64_t> eval_gen;
+    DevState *d_states = nullptr;   // per solution, keys pointing into d_keys
+    void *d_scans = nullptr;        // ScanArgs<DT> per solution
 };
 
 static void free_batch(tga_batch *b) {
@@ -1081,6 +1173,8 @@ static void free_batch(tga_batch *b) {
     if (b->d_work) cudaFree(b->d_work);
     if (b->d_keys) cudaFree(b->d_keys);
     if (b->h_keys) cudaFreeHost(b->h_keys);
+    if (b->d_states) cudaFree(b->d_states);
+    if (b->d_scans) cudaFree(b->d_scans);
     if (b->stream) cudaStreamDestroy(b->stream);
     delete b;
 }
@@ -1131,6 +1225,21 @@ extern "C" int32_t tga_batch_load(tga_instance *I, int32_t n_sol, const int32_t 
         cudaMalloc(&b->d_keys, sizeof(uint64_t) * TGA_N_VARIANTS * n_sol) != cudaSuccess ||
         cudaMallocHost(&b->h_keys, sizeof(uint64_t) * TGA_N_VARIANTS * n_sol) != cudaSuccess)
         return bail(fail(TGA_ERR_OOM, "batch allocation"));
+    {
+        std::vector<DevState> ds(n_sol);
+        const size_t ssz = I->dtype == TGA_I32 ? sizeof(ScanArgs<int32_t>) : sizeof(ScanArgs<float>);
+        std::vector<unsigned char> sa(ssz * n_sol);
+        for (int k = 0; k < n_sol; ++k) {
+            ds[k] = make_devstate(b->sols[k], b->d_keys + static_cast<size_t>(k) * TGA_N_VARIANTS);
+            if (I->dtype == TGA_I32) { auto a = scan_args<int32_t>(b->sols[k]); std::memcpy(&sa[ssz * k], &a, ssz); }
+            else { auto a = scan_args<float>(b->sols[k]); std::memcpy(&sa[ssz * k], &a, ssz); }
+        }
+        if (cudaMalloc(&b->d_states, sizeof(DevState) * n_sol) != cudaSuccess ||
+            cudaMalloc(&b->d_scans, sa.size()) != cudaSuccess ||
+            cudaMemcpy(b->d_states, ds.data(), sizeof(DevState) * n_sol, cudaMemcpyHostToDevice) != cudaSuccess ||
+            cudaMemcpy(b->d_scans, sa.data(), sa.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+            return bail(fail(TGA_ERR_OOM, "batch step state"));
+    }
     if (cudaMemcpy(b->d_views, views.data(), views.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
         cudaMemcpy(b->d_maps, maps.data(), sizeof(CUtensorMap) * n_sol, cudaMemcpyHostToDevice) != cudaSuccess ||
         cudaMemcpy(b->d_work, work.data(), sizeof(uint32_t) * work.size(), cudaMemcpyHostToDevice) != cudaSuccess)
@@ -1217,6 +1326,41 @@ extern "C" int32_t tga_batch_apply_moves(tga_batch *b, const tga_move *moves, co
         const int32_t rc = tga_apply_move(b->sols[k], &moves[k]);
         if (rc != TGA_OK) return rc;
     }
+    return TGA_OK;
+}
+
+extern "C" int32_t tga_batch_step_async(tga_batch *b, uint32_t mask) {
+    if (!b) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL batch");
+    int32_t rc = tga_batch_eval(b, mask, nullptr);
+    if (rc != TGA_OK) return rc;
+    const tga_instance *I = b->inst;
+    const int n = static_cast<int>(b->sols.size());
+    cudaError_t e = launch_pick_apply(b->d_states, n, I->dtype == TGA_I32, b->eval_mask, b->stream);
+    if (e == cudaSuccess)
+        e = launch_update_dev(b->d_states, b->d_scans, n, I->tw, I->dtype == TGA_I32,
+                              std::max(1, b->sm_count * 4 / n), b->stream);
+    if (e != cudaSuccess) return fail(TGA_ERR_CUDA, std::string("batch device step: ") + cudaGetErrorString(e));
+    for (auto *s : b->sols) {
+        ++s->gen;
+        s->host_stale = true;
+        s->drained = false;
+    }
+    return TGA_OK;
+}
+
+extern "C" int32_t tga_batch_device_stats(tga_batch *b, uint64_t *counts, uint64_t *applied) {
+    if (!b) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL batch");
+    TGA_CUDA(cudaStreamSynchronize(b->stream));
+    uint64_t tot[TGA_N_VARIANTS] = {0}, app = 0;
+    for (auto *s : b->sols) {
+        uint64_t c[TGA_N_VARIANTS], a = 0;
+        const int32_t rc = tga_solution_device_stats(s, c, &a);
+        if (rc != TGA_OK) return rc;
+        for (int v = 0; v < TGA_N_VARIANTS; ++v) tot[v] += c[v];
+        app += a;
+    }
+    if (counts) std::memcpy(counts, tot, sizeof(tot));
+    if (applied) *applied = app;
     return TGA_OK;
 }
 

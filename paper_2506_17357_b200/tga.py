@@ -107,6 +107,10 @@ _SYMBOLS = {
     "tga_batch_keys": (C.c_int32, [C.c_void_p, C.c_void_p]),
     "tga_batch_best_moves": (C.c_int32, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_void_p]),
     "tga_batch_apply_moves": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "tga_step_async": (C.c_int32, [C.c_void_p, C.c_uint32]),
+    "tga_solution_device_stats": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "tga_batch_step_async": (C.c_int32, [C.c_void_p, C.c_uint32]),
+    "tga_batch_device_stats": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "tga_last_error": (C.c_char_p, []),
     "tga_version": (C.c_char_p, []),
     "tga_launch_count": (C.c_uint64, []),
@@ -269,6 +273,17 @@ class Solution:
         rc = _check(lib().tga_step(self._h, op_mask, C.byref(m)), allow=(OK, NO_IMPROVING_MOVE))
         return rc == OK, m
 
+    def step_async(self, op_mask: int = OP_ALL) -> None:
+        """Device-resident step: eval + pick + apply + update, no host round trip."""
+        _check(lib().tga_step_async(self._h, op_mask))
+
+    def device_stats(self):
+        """(counts per variant, applied moves) accumulated by step_async; clears them."""
+        c = np.zeros(N_VARIANTS, dtype=np.uint64)
+        a = C.c_uint64()
+        _check(lib().tga_solution_device_stats(self._h, _p(c), C.byref(a)))
+        return c, a.value
+
     def reload(self, routes) -> None:
         """Load another solution (same route count) into this object, asynchronously."""
         ptr, cust = _csr(routes)
@@ -395,6 +410,15 @@ class Batch:
         status = np.zeros(self.n, dtype=np.int32)
         _check(lib().tga_batch_best_moves(self._h, op_mask, C.cast(moves, C.c_void_p), _p(status)))
         return status, moves
+
+    def step_async(self, op_mask: int = OP_ALL) -> None:
+        _check(lib().tga_batch_step_async(self._h, op_mask))
+
+    def device_stats(self):
+        c = np.zeros(N_VARIANTS, dtype=np.uint64)
+        a = C.c_uint64()
+        _check(lib().tga_batch_device_stats(self._h, _p(c), C.byref(a)))
+        return c, a.value
 
     def apply(self, moves, apply_mask=None) -> None:
         am = None if apply_mask is None else np.ascontiguousarray(apply_mask, dtype=np.int32)

@@ -399,3 +399,67 @@ def test_cfg4_shape_reduced_exact():
     _need_gpu()
     inst, sol = G.large_cvrp(1, n=2000, mean_len=100)
     check_exact(inst, sol, ALLV, 0, "cfg4-2000")
+
+
+# ---------------------------------------------------------------- device-resident step (NEXT #1)
+@pytest.mark.parametrize("name", ["cvrp", "vrptw", "cfg2"])
+def test_device_resident_step_matches_host_step(name):
+    """tga_step_async (pick + splice + update on the device) follows exactly
+    the trajectory of the host-driven tga_step; its on-device candidate
+    counts equal the closed forms of the host."""
+    _need_gpu()
+    if name == "cvrp":
+        inst, sol = G.x_like(9, n=200, target_routes=9)
+    elif name == "vrptw":
+        inst, sol = G.gh_like(9, n=200, kind="R2")
+    else:
+        inst, sol = G.config("cfg2")
+    mask = T.OP_ALL if inst.tw is None else T.OP_ALL & ~T.OP_2OPT
+    gi = T.Instance.from_gen(inst)
+    host = T.Solution(gi, sol)
+    dev = T.Solution(gi, sol)
+    exp_counts = np.zeros(T.N_VARIANTS, dtype=np.uint64)
+    applied = 0
+    for k in range(40):
+        c = host.counts()
+        for v in range(T.N_VARIANTS):
+            if (mask >> v) & 1:
+                exp_counts[v] += c[v]
+        ok, _ = host.step(mask)
+        applied += int(ok)
+        dev.step_async(mask)
+        if k % 10 == 9:
+            assert dev.routes() == host.routes(), k
+    counts, app = dev.device_stats()
+    assert app == applied
+    np.testing.assert_array_equal(counts, exp_counts)
+    assert dev.routes() == host.routes()
+    host.eval(mask)
+    dev.eval(mask)
+    np.testing.assert_array_equal(dev.keys(), host.keys())
+    # host-side calls after device steps: apply a host move on the device-stepped object
+    ok, mv = dev.best_move(mask)
+    if ok:
+        dev.apply(mv)
+        fresh = T.Solution(gi, dev.routes())
+        fresh.eval(mask)
+        dev.eval(mask)
+        np.testing.assert_array_equal(dev.keys(), fresh.keys())
+
+
+def test_batch_device_step_matches_host_batch():
+    _need_gpu()
+    inst, sols = G.population(1, n=200, n_sol=64)
+    gi = T.Instance.from_gen(inst)
+    mask = T.OP_ALL & ~T.OP_2OPT
+    hb = T.Batch(gi, sols)
+    db = T.Batch(gi, sols)
+    for _ in range(5):
+        hb.eval(mask)
+        status, moves = hb.best_moves(mask)
+        hb.apply(moves, apply_mask=(status == 0))
+        db.step_async(mask)
+    for k in range(64):
+        assert db.solution(k).routes() == hb.solution(k).routes(), k
+    counts, applied = db.device_stats()
+    assert applied > 0

@@ -201,6 +201,7 @@ def run_population(args, ws, rank, local, dev):
     stream = torch.cuda.Stream(device=dev)
     gi = T.Instance.from_gen(inst)
     b = T.Batch(gi, mine)
+    b.set_stream(stream)
     mask = T.OP_ALL & ~T.OP_2OPT
 
     def counts_total():
@@ -208,15 +209,14 @@ def run_population(args, ws, rank, local, dev):
                    for k in range(len(mine)))
 
     def step():
-        b.eval(mask, stream)
-        status, moves = b.best_moves(mask)
-        b.apply(moves, apply_mask=(status == 0))
-        return int((status == 0).sum())
+        b.step_async(mask)   # batch eval + on-device pick/splice + update for every solution
+        return 0
 
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize(dev)
-    K = min(args.steps, 20)
+    b.device_stats()
+    K = min(args.steps, 50)
     cand = 0
     sampler = ClockSampler(local)
     if ws > 1:
@@ -228,15 +228,17 @@ def run_population(args, ws, rank, local, dev):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     applied = 0
     tot_ms = 0.0
-    for _ in range(K):
-        c = counts_total()
-        cand += c
+    torch.cuda.synchronize(dev)
+    with torch.cuda.stream(stream):
         e0.record(stream)
-        applied += step()
+        for _ in range(K):
+            step()
         e1.record(stream)
-        torch.cuda.synchronize(dev)
-        tot_ms += e0.elapsed_time(e1)
+    torch.cuda.synchronize(dev)
+    tot_ms = e0.elapsed_time(e1)   # K batch steps back to back on the batch stream (CUDA events)
     launches = T.launch_count() - launches0
+    dc, applied = b.device_stats()
+    cand = int(dc.sum())
     clocks = sampler.stop()
     if ws > 1:
         import torch.distributed as dist
@@ -290,12 +292,13 @@ def run_tga(args):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)  # 256 MB > L2 (126 MB)
 
     def step(evs=None):
+        # tga_step_async: eval (inter + intra kernels) -> on-device best move + splice
+        # -> update kernel; no host round trip
         if evs:
             evs[0].record(stream)
-        ok, _ = gs.step(mask_all)   # tga_step: eval (inter + intra) -> best move -> apply
+        gs.step_async(mask_all)
         if evs:
             evs[1].record(stream)
-        return ok
 
     # ---------------- warm-up
     for _ in range(max(args.warmup, 3)):
@@ -305,7 +308,6 @@ def run_tga(args):
     # ---------------- timed region: K steps, per-step events, L2 flushed between steps
     sampler = ClockSampler(local)
     K = args.steps
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(K)]
     gs.enable_timing(True)   # CUDA events around the inter-route launch, on its stream
     counts = []
     if ws > 1:
@@ -315,15 +317,14 @@ def run_tga(args):
     sampler.start()
     launches0 = T.launch_count()
     applied = 0
-    for k in range(K):
-        with torch.cuda.stream(stream):
-            flush.fill_(k)
-        counts.append(gs.counts().astype(np.int64))
-        applied += int(step(evs[k]))
+    gs.device_stats()  # clear the on-device counters of the warm-up
+    # K device-resident steps enqueued from C (tga_descent); CUDA events around every
+    # step on the solution's stream; a 256 MB memset before each step flushes L2
+    step_ms = [float(x) for x in gs.descent(mask_all, K, l2_flush=flush, timed=True)]
     torch.cuda.synchronize(dev)
     launches = T.launch_count() - launches0
+    dev_counts, applied = gs.device_stats()   # exact candidate counts of the K evaluated neighbourhoods
     clocks = sampler.stop()
-    step_ms = [e[0].elapsed_time(e[1]) for e in evs]
     inter_ms = [float(x) for x in gs.timings()]
     gs.enable_timing(False)
     tot_ms = float(sum(step_ms))
@@ -333,9 +334,7 @@ def run_tga(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms = float(t.item())
         dist.barrier()
-    cand = np.stack(counts)                              # K x 23
-    sel = np.array([(mask_all >> v) & 1 for v in range(23)], dtype=bool)
-    cand_total = int(cand[:, sel].sum())
+    cand_total = int(dev_counts.sum())
     value = cand_total / (tot_ms / 1e3)
 
     if rank != 0:
@@ -347,9 +346,9 @@ def run_tga(args):
     R, N, Qc, _ = gs.info()
     Qp = N + 2 * R
     inter_sel = [v for v in range(1, 11)]
-    inter_cands = float(cand[:, inter_sel].sum(axis=1).mean())
+    inter_cands = float(sum(int(dev_counts[v]) for v in inter_sel)) / K
     alg_bytes = (Qp * Qp / 2.0) * 4.0                    # Dp upper triangle, int32
-    alg_ops = float(sum(cand[:, v].mean() * ALG_OPS[v] for v in inter_sel))
+    alg_ops = float(sum(int(dev_counts[v]) * ALG_OPS[v] for v in inter_sel)) / K
     sm_mhz_peak = float(pk.get("sm_max_mhz", 1965.0))
     alu_peak = 148 * 128 * sm_mhz_peak * 1e6            # lane-ops/s (4 SMSP x 32 lanes x 1 issue/clk)
     hbm_peak = float(pk["hbm_gbs"]) * 1e9
@@ -363,7 +362,7 @@ def run_tga(args):
                 "traffic": traffic_for("k_inter_all"),
                 "peak_source": f"148 SM x 128 lanes x {sm_mhz_peak:.0f} MHz ({pk_src} sm_max_mhz)"}
     primary, alt = (alu_view, hbm_view) if t_alu >= t_hbm else (hbm_view, alu_view)
-    primary = dict(primary, kernel="k_inter<int,CVRP,all-inter> (tga_eval inter launch incl. key reset)",
+    primary = dict(primary, kernel="k_inter_fast<all-inter> (CVRP fused inter-route sweep), live CUDA events",
                    kernel_ms=inter_avg_s * 1e3, candidates_per_launch=inter_cands,
                    alg_bytes_per_launch=alg_bytes, alg_ops_per_launch=alg_ops)
 
@@ -448,7 +447,8 @@ def run_tga(args):
                    "customers": N, "routes": R, "canonical_slots": Qc, "seed": args.seed,
                    "l2": "flushed between timed steps (256 MB write); working set < L2",
                    "parallelism": f"row-shard x{ws}" if ws > 1 else "1 GPU"},
-        "sweeps_per_s": sweeps_per_s, "applied_moves": applied,
+        "sweeps_per_s": sweeps_per_s, "applied_moves": int(applied),
+        "step": "tga_step_async: eval all variants -> on-device best move + splice -> update kernel",
         "candidates_per_step": cand_total / K,
         "roofline": primary, "roofline_alt": alt,
         "per_operator_steady_state": per_op,

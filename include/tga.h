@@ -202,6 +202,14 @@ int32_t tga_step(tga_solution *sol, uint32_t op_mask, tga_move *out);
  * variant accumulated by device steps (counts[TGA_N_VARIANTS]) and the number
  * of moves they applied (synchronises). */
 int32_t tga_step_async(tga_solution *sol, uint32_t op_mask);
+/* tga_descent: n_steps device-resident steps enqueued from C (a best-improvement
+ * descent, Alg. A2).  Optional instrumentation: when step_ms is not
+ * NULL, CUDA events bracket every step on the solution's stream and the
+ * per-step device times are written there (synchronises); when l2_flush is not
+ * NULL, flush_bytes of it are overwritten before every step, outside the
+ * bracketed interval (cold-L2 timing). */
+int32_t tga_descent(tga_solution *sol, uint32_t op_mask, int32_t n_steps, void *l2_flush, uint64_t flush_bytes,
+                    float *step_ms);
 int32_t tga_solution_device_stats(tga_solution *sol, uint64_t *counts, uint64_t *applied);
 
 /* tga_solution_reload: load another solution of the same instance into an
@@ -281,6 +289,8 @@ int32_t tga_batch_eval(tga_batch *batch, uint32_t op_mask, void *cuda_stream);
 int32_t tga_batch_keys(tga_batch *batch, uint64_t *keys);
 int32_t tga_batch_best_moves(tga_batch *batch, uint32_t op_mask, tga_move *out, int32_t *status);
 int32_t tga_batch_apply_moves(tga_batch *batch, const tga_move *moves, const int32_t *apply);
+/* use cuda_stream for every later batch call (NULL = the batch's own stream) */
+int32_t tga_batch_set_stream(tga_batch *batch, void *cuda_stream);
 /* device-resident steps of every solution of the batch (see tga_step_async) */
 int32_t tga_batch_step_async(tga_batch *batch, uint32_t op_mask);
 int32_t tga_batch_device_stats(tga_batch *batch, uint64_t *counts, uint64_t *applied);

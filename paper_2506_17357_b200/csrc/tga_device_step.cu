@@ -48,21 +48,31 @@ __device__ __forceinline__ int64_t pz(int64_t x) { return x > 0 ? x : 0; }
 }  // namespace
 
 // ------------------------------------------------------------------ pick + apply
+// Route arrays (base, length, canonical base) are staged in shared memory so the
+// serial parts (decode, binary searches over routes) never wait on global loads.
 __global__ void __launch_bounds__(256) k_pick_apply(const DevState *__restrict__ states, uint32_t mask, int integer) {
+    extern __shared__ int32_t smr[];
     const DevState &S = states[blockIdx.x];
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int R = S.R;
+    int32_t *sb = smr, *sl = smr + (R + 1), *sc = smr + 2 * (R + 1);
+    for (int r = tid; r <= R; r += blockDim.x) {
+        sb[r] = S.rbase[r];
+        sl[r] = r < R ? S.rlenR[r] : 0;
+        sc[r] = S.cbase[r];
+    }
+    __shared__ uint64_t skeys[23];
+    if (tid < 23) skeys[tid] = S.keys[tid];
     // ---- 1. exact candidate counts of the evaluated neighbourhood (closed forms)
     constexpr int NS = 27;
-    __shared__ unsigned long long sums[NS];
-    if (tid < NS) sums[tid] = 0;
+    __shared__ long long wsum[8][NS];
     __syncthreads();
     {
-        unsigned long long loc[NS];
+        long long loc[NS];
 #pragma unroll
         for (int k = 0; k < NS; ++k) loc[k] = 0;
         for (int r = tid; r < R; r += blockDim.x) {
-            const int64_t L = S.rlenR[r], X = L + 1;
+            const int64_t L = sl[r], X = L + 1;
             const int64_t x1 = pz(L), x2 = pz(L - 1), x3 = pz(L - 2);
             loc[0] += X;
             loc[1] += X * X;
@@ -81,27 +91,36 @@ __global__ void __launch_bounds__(256) k_pick_apply(const DevState *__restrict__
                 }
         }
 #pragma unroll
-        for (int k = 0; k < NS; ++k)
-            if (loc[k]) atomicAdd(&sums[k], loc[k]);
+        for (int k = 0; k < NS; ++k) {
+            long long v = loc[k];
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+            if (lane == 0) wsum[warp][k] = v;
+        }
     }
     __syncthreads();
-    if (tid == 0) {
+    __shared__ long long sums[NS];
+    if (tid < NS) {
+        long long v = 0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) v += wsum[w][tid];
+        sums[tid] = v;
+    }
+    __syncthreads();
+    if (tid < 23 && (mask & (1u << tid))) {  // one variant per thread
         const long long S1 = sums[0], S2 = sums[1];
-        long long c[23];
-        c[0] = sums[14];
-        c[1] = (S1 * S1 - S2) / 2;
-        for (int N = 1; N <= 3; ++N) c[1 + N] = static_cast<long long>(sums[1 + N]) * S1 - static_cast<long long>(sums[4 + N]);
-        const long long X[4] = {0, static_cast<long long>(sums[2]), static_cast<long long>(sums[3]),
-                                static_cast<long long>(sums[4])};
-        const int n1s[6] = {1, 1, 1, 2, 2, 3}, n2s[6] = {1, 2, 3, 2, 3, 3}, pidx[6] = {8, 9, 10, 11, 12, 13};
-        for (int k = 0; k < 6; ++k) {
-            const long long ordered = X[n1s[k]] * X[n2s[k]] - static_cast<long long>(sums[pidx[k]]);
-            c[5 + k] = (n1s[k] == n2s[k]) ? ordered / 2 : ordered;
-        }
-        for (int N = 1; N <= 3; ++N) c[10 + N] = sums[14 + N];
-        for (int k = 0; k < 9; ++k) c[14 + k] = sums[18 + k];
-        for (int v = 0; v < 23; ++v)
-            if (mask & (1u << v)) S.acc[v] += static_cast<unsigned long long>(c[v]);
+        const int v = tid;
+        long long c;
+        if (v == 0) c = sums[14];
+        else if (v == 1) c = (S1 * S1 - S2) / 2;
+        else if (v <= 4) c = sums[v] * S1 - sums[v + 3];
+        else if (v <= 10) {
+            const int n1s[6] = {1, 1, 1, 2, 2, 3}, n2s[6] = {1, 2, 3, 2, 3, 3}, pidx[6] = {8, 9, 10, 11, 12, 13};
+            const int k = v - 5;
+            const long long ordered = sums[1 + n1s[k]] * sums[1 + n2s[k]] - sums[pidx[k]];
+            c = (n1s[k] == n2s[k]) ? ordered / 2 : ordered;
+        } else if (v <= 13) c = sums[v + 4];
+        else c = sums[v + 4];
+        S.acc[v] += static_cast<unsigned long long>(c);
     }
 
     // ---- 2. best key over the mask, decode, pieces of the new routes
@@ -112,7 +131,7 @@ __global__ void __launch_bounds__(256) k_pick_apply(const DevState *__restrict__
         uint64_t bk = ~0ull;
         for (int v = 0; v < 23; ++v) {
             if (!(mask & (1u << v))) continue;
-            const uint64_t k = S.keys[v];
+            const uint64_t k = skeys[v];
             if (k == ~0ull) continue;
             if (bv < 0 || (k >> 32) < (bk >> 32)) { bv = v; bk = k; }
         }
@@ -131,9 +150,9 @@ __global__ void __launch_bounds__(256) k_pick_apply(const DevState *__restrict__
             const uint32_t idx = static_cast<uint32_t>(bk & 0xFFFFFFFFu);
             const int cu = static_cast<int>(idx / static_cast<uint32_t>(S.Qc));
             const int cv = static_cast<int>(idx % static_cast<uint32_t>(S.Qc));
-            const int ra = find_route(S.cbase, R, cu), pa = cu - S.cbase[ra];
-            const int rb = find_route(S.cbase, R, cv), pb = cv - S.cbase[rb];
-            const int La = S.rlenR[ra], Lb = S.rlenR[rb];
+            const int ra = find_route(sc, R, cu), pa = cu - sc[ra];
+            const int rb = find_route(sc, R, cv), pb = cv - sc[rb];
+            const int La = sl[ra], Lb = sl[rb];
             const int v = bv;
             NewRoute A{ra, 0, 0, {}}, B{rb, 0, 0, {}};
             int nroutes = 2;
@@ -170,15 +189,14 @@ __global__ void __launch_bounds__(256) k_pick_apply(const DevState *__restrict__
             }
             for (int k = 0; k < A.np; ++k) A.L += A.p[k].len;
             for (int k = 0; k < B.np; ++k) B.L += B.p[k].len;
-            // nr[0] is the lower route of the span
-            if (nroutes == 1 || ra < rb) { nr[0] = A; nr[1] = B; }
+            if (nroutes == 1 || ra < rb) { nr[0] = A; nr[1] = B; }  // nr[0] = lower route of the span
             else { nr[0] = B; nr[1] = A; }
             sh_n = nroutes;
             sh_rlo = nr[0].r;
             sh_rhi = nroutes == 2 ? nr[1].r : nr[0].r;
-            sh_lo = S.rbase[sh_rlo];
-            sh_hi = S.rbase[sh_rhi] + S.rlenR[sh_rhi] + 2;
-            sh_d = nr[0].L - S.rlenR[sh_rlo];  // shift of every route after the first changed one
+            sh_lo = sb[sh_rlo];
+            sh_hi = sb[sh_rhi] + sl[sh_rhi] + 2;
+            sh_d = nr[0].L - sl[sh_rlo];  // shift of every route after the first changed one
             sh_applied = 1;
         }
     }
@@ -191,10 +209,10 @@ __global__ void __launch_bounds__(256) k_pick_apply(const DevState *__restrict__
     // ---- 3. snapshot the changed span of node ids
     for (int x = lo + tid; x < hi; x += blockDim.x) S.scratch[x - lo] = S.node[x];
     __syncthreads();
-    // new base / length / canonical base of route r in [rlo, rhi] (old arrays still intact)
-    auto nbase = [&](int r) { return r == rlo ? S.rbase[r] : S.rbase[r] + dlt; };
-    auto ncb = [&](int r) { return r == rlo ? S.cbase[r] : S.cbase[r] + dlt; };
-    auto nlen = [&](int r) { return r == nr[0].r ? nr[0].L : (nrt == 2 && r == nr[1].r ? nr[1].L : S.rlenR[r]); };
+    // new base / length / canonical base of route r in [rlo, rhi] (old values in shared memory)
+    auto nbase = [&](int r) { return r == rlo ? sb[r] : sb[r] + dlt; };
+    auto ncb = [&](int r) { return r == rlo ? sc[r] : sc[r] + dlt; };
+    auto nlen = [&](int r) { return r == nr[0].r ? nr[0].L : (nrt == 2 && r == nr[1].r ? nr[1].L : sl[r]); };
     // ---- 4. rewrite the span slot by slot
     for (int x = lo + tid; x < hi; x += blockDim.x) {
         int a = rlo, b = rhi;  // route of new slot x: largest r with nbase(r) <= x
@@ -213,9 +231,9 @@ __global__ void __launch_bounds__(256) k_pick_apply(const DevState *__restrict__
                 while (off >= chg->p[k].len) { off -= chg->p[k].len; ++k; }
                 const Piece &pc = chg->p[k];
                 const int op = pc.rev ? pc.start + pc.len - 1 - off : pc.start + off;
-                old_slot = S.rbase[pc.src] + op;
+                old_slot = sb[pc.src] + op;
             } else {
-                old_slot = S.rbase[r] + p;
+                old_slot = sb[r] + p;
             }
             nd = S.scratch[old_slot - lo];
         }
@@ -225,13 +243,11 @@ __global__ void __launch_bounds__(256) k_pick_apply(const DevState *__restrict__
         S.rlen[x] = L;
         S.canon[x] = (p <= L) ? ncb(r) + p : -1;
     }
-    __syncthreads();
-    // ---- 5. per-route arrays (each thread owns whole routes: no cross-thread hazard)
+    // ---- 5. per-route arrays (old values are in shared memory: no hazard)
     for (int r = rlo + tid; r <= rhi; r += blockDim.x) {
-        const int b = nbase(r), c = ncb(r), L = nlen(r);
-        S.rbase[r] = b;
-        S.cbase[r] = c;
-        S.rlenR[r] = L;
+        S.rbase[r] = nbase(r);
+        S.cbase[r] = ncb(r);
+        S.rlenR[r] = nlen(r);
     }
     if (tid == 0) {
         S.desc[0] = 1;
@@ -243,8 +259,15 @@ __global__ void __launch_bounds__(256) k_pick_apply(const DevState *__restrict__
     }
 }
 
-cudaError_t launch_pick_apply(const DevState *states, int n_sol, bool is_int, uint32_t mask, cudaStream_t st) {
-    k_pick_apply<<<n_sol, 256, 0, st>>>(states, mask, is_int ? 1 : 0);
+cudaError_t launch_pick_apply(const DevState *states, int n_sol, bool is_int, uint32_t mask, int max_routes,
+                              cudaStream_t st) {
+    const int smem = 3 * (max_routes + 1) * 4;
+    static int attr = 0;
+    if (smem > 48 * 1024 && smem > attr) {
+        cudaFuncSetAttribute(k_pick_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr = smem;
+    }
+    k_pick_apply<<<n_sol, 256, smem, st>>>(states, mask, is_int ? 1 : 0);
     note_launch();
     return cudaGetLastError();
 }

@@ -67,7 +67,8 @@ struct DevState {
     void *Dp;
     int32_t R, Qc, Qp, pitch;
 };
-cudaError_t launch_pick_apply(const DevState *states, int n_sol, bool is_int, uint32_t mask, cudaStream_t st);
+cudaError_t launch_pick_apply(const DevState *states, int n_sol, bool is_int, uint32_t mask, int max_routes,
+                              cudaStream_t st);
 cudaError_t launch_update_dev(const DevState *states, const void *scans, int n_sol, bool tw, bool is_int,
                               int blocks_per_sol, cudaStream_t st);
 

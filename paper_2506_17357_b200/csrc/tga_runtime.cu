@@ -1127,7 +1127,7 @@ extern "C" int32_t tga_step_async(tga_solution *s, uint32_t mask) {
     int32_t rc = tga_eval(s, mask, nullptr);
     if (rc != TGA_OK) return rc;
     const tga_instance *I = s->inst;
-    cudaError_t e = launch_pick_apply(s->d_ds, 1, I->dtype == TGA_I32, s->eval_mask, s->stream);
+    cudaError_t e = launch_pick_apply(s->d_ds, 1, I->dtype == TGA_I32, s->eval_mask, s->R, s->stream);
     if (e == cudaSuccess)
         e = launch_update_dev(s->d_ds, s->d_sa, 1, I->tw, I->dtype == TGA_I32, s->sm_count * 2, s->stream);
     if (e != cudaSuccess) return fail(TGA_ERR_CUDA, std::string("device step: ") + cudaGetErrorString(e));
@@ -1135,6 +1135,29 @@ extern "C" int32_t tga_step_async(tga_solution *s, uint32_t mask) {
     s->host_stale = true;
     s->drained = false;
     return TGA_OK;
+}
+
+extern "C" int32_t tga_descent(tga_solution *s, uint32_t mask, int32_t n_steps, void *l2_flush, uint64_t flush_bytes,
+                               float *step_ms) {
+    if (!s || n_steps < 0) return fail(TGA_ERR_INVALID_ARGUMENT, "descent arguments");
+    std::vector<cudaEvent_t> ev;
+    if (step_ms) {
+        ev.resize(2 * static_cast<size_t>(n_steps));
+        for (auto &e : ev) TGA_CUDA(cudaEventCreate(&e));
+    }
+    int32_t rc = TGA_OK;
+    for (int k = 0; k < n_steps && rc == TGA_OK; ++k) {
+        if (l2_flush && flush_bytes) TGA_CUDA(cudaMemsetAsync(l2_flush, k & 0xFF, flush_bytes, s->stream));
+        if (step_ms) TGA_CUDA(cudaEventRecord(ev[2 * k], s->stream));
+        rc = tga_step_async(s, mask);
+        if (step_ms && rc == TGA_OK) TGA_CUDA(cudaEventRecord(ev[2 * k + 1], s->stream));
+    }
+    if (step_ms && rc == TGA_OK) {
+        TGA_CUDA(cudaStreamSynchronize(s->stream));
+        for (int k = 0; k < n_steps; ++k) TGA_CUDA(cudaEventElapsedTime(&step_ms[k], ev[2 * k], ev[2 * k + 1]));
+    }
+    for (auto e : ev) cudaEventDestroy(e);
+    return rc;
 }
 
 extern "C" int32_t tga_solution_device_stats(tga_solution *s, uint64_t *counts, uint64_t *applied) {
@@ -1161,6 +1184,7 @@ struct tga_batch {
     int n_work = 0, max_qp = 0, sm_count = 148;
     uint32_t eval_mask = 0;
     std::vector<uint64_t> eval_gen;
+    cudaStream_t own_stream = nullptr;
     DevState *d_states = nullptr;   // per solution, keys pointing into d_keys
     void *d_scans = nullptr;        // ScanArgs<DT> per solution
 };
@@ -1175,7 +1199,7 @@ static void free_batch(tga_batch *b) {
     if (b->h_keys) cudaFreeHost(b->h_keys);
     if (b->d_states) cudaFree(b->d_states);
     if (b->d_scans) cudaFree(b->d_scans);
-    if (b->stream) cudaStreamDestroy(b->stream);
+    if (b->own_stream) cudaStreamDestroy(b->own_stream);
     delete b;
 }
 
@@ -1189,8 +1213,9 @@ extern "C" int32_t tga_batch_load(tga_instance *I, int32_t n_sol, const int32_t 
     if (!b) return fail(TGA_ERR_OOM, "host allocation");
     b->inst = I;
     auto bail = [&](int32_t code) { free_batch(b); return code; };
-    if (cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking) != cudaSuccess)
+    if (cudaStreamCreateWithFlags(&b->own_stream, cudaStreamNonBlocking) != cudaSuccess)
         return bail(fail(TGA_ERR_CUDA, "stream"));
+    b->stream = b->own_stream;
     size_t rp = 0;
     const int ncust = I->n - 1;
     std::vector<uint32_t> work;
@@ -1329,13 +1354,24 @@ extern "C" int32_t tga_batch_apply_moves(tga_batch *b, const tga_move *moves, co
     return TGA_OK;
 }
 
+extern "C" int32_t tga_batch_set_stream(tga_batch *b, void *stream) {
+    if (!b) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL batch");
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : b->own_stream;
+    if (st != b->stream) TGA_CUDA(order_after(st, b->stream));
+    b->stream = st;
+    for (auto *s : b->sols) s->stream = st;
+    return TGA_OK;
+}
+
 extern "C" int32_t tga_batch_step_async(tga_batch *b, uint32_t mask) {
     if (!b) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL batch");
     int32_t rc = tga_batch_eval(b, mask, nullptr);
     if (rc != TGA_OK) return rc;
     const tga_instance *I = b->inst;
     const int n = static_cast<int>(b->sols.size());
-    cudaError_t e = launch_pick_apply(b->d_states, n, I->dtype == TGA_I32, b->eval_mask, b->stream);
+    int max_r = 0;
+    for (auto *s : b->sols) max_r = std::max(max_r, s->R);
+    cudaError_t e = launch_pick_apply(b->d_states, n, I->dtype == TGA_I32, b->eval_mask, max_r, b->stream);
     if (e == cudaSuccess)
         e = launch_update_dev(b->d_states, b->d_scans, n, I->tw, I->dtype == TGA_I32,
                               std::max(1, b->sm_count * 4 / n), b->stream);

@@ -109,7 +109,9 @@ _SYMBOLS = {
     "tga_batch_apply_moves": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "tga_step_async": (C.c_int32, [C.c_void_p, C.c_uint32]),
     "tga_solution_device_stats": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "tga_descent": (C.c_int32, [C.c_void_p, C.c_uint32, C.c_int32, C.c_void_p, C.c_uint64, C.c_void_p]),
     "tga_batch_step_async": (C.c_int32, [C.c_void_p, C.c_uint32]),
+    "tga_batch_set_stream": (C.c_int32, [C.c_void_p, C.c_void_p]),
     "tga_batch_device_stats": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "tga_last_error": (C.c_char_p, []),
     "tga_version": (C.c_char_p, []),
@@ -277,6 +279,14 @@ class Solution:
         """Device-resident step: eval + pick + apply + update, no host round trip."""
         _check(lib().tga_step_async(self._h, op_mask))
 
+    def descent(self, op_mask: int, n_steps: int, l2_flush=None, timed: bool = False):
+        """n device-resident steps enqueued from C; per-step device ms when timed.
+        l2_flush: a torch CUDA tensor overwritten before every step (outside the timing)."""
+        ms = np.zeros(max(n_steps, 1), dtype=np.float32) if timed else None
+        fp, fb = (None, 0) if l2_flush is None else (l2_flush.data_ptr(), l2_flush.numel() * l2_flush.element_size())
+        _check(lib().tga_descent(self._h, op_mask, n_steps, fp, fb, _p(ms)))
+        return ms[:n_steps] if timed else None
+
     def device_stats(self):
         """(counts per variant, applied moves) accumulated by step_async; clears them."""
         c = np.zeros(N_VARIANTS, dtype=np.uint64)
@@ -413,6 +423,9 @@ class Batch:
 
     def step_async(self, op_mask: int = OP_ALL) -> None:
         _check(lib().tga_batch_step_async(self._h, op_mask))
+
+    def set_stream(self, stream) -> None:
+        _check(lib().tga_batch_set_stream(self._h, _stream_ptr(stream)))
 
     def device_stats(self):
         c = np.zeros(N_VARIANTS, dtype=np.uint64)

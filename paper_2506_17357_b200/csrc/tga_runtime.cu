@@ -715,7 +715,11 @@ extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
     const int grid = std::max(1, std::min(t_hi - t_lo, s->sm_count * 4));
     cudaError_t e;
     const bool timed = s->timing && (mask & TGA_OP_INTER) && s->tev_n + 2 <= static_cast<int>(s->tev.size());
-    if (timed) TGA_CUDA(cudaEventRecord(s->tev[s->tev_n], st));
+    // inside a captured graph (tga_descent) the records must be external event nodes
+    cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+    if (timed) TGA_CUDA(cudaStreamIsCapturing(st, &cst));
+    const unsigned rec_flags = cst == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
+    if (timed) TGA_CUDA(cudaEventRecordWithFlags(s->tev[s->tev_n], st, rec_flags));
     if (I->dtype == TGA_I32 && s->fast) {
         tga_shard_range(s->n_ftiles, s->shard, s->n_shards, &a, &b);
         const int f_lo = static_cast<int>(a), f_hi = static_cast<int>(b);
@@ -730,7 +734,7 @@ extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
                                 st);
     }
     if (timed) {
-        TGA_CUDA(cudaEventRecord(s->tev[s->tev_n + 1], st));
+        TGA_CUDA(cudaEventRecordWithFlags(s->tev[s->tev_n + 1], st, rec_flags));
         s->tev_n += 2;
     }
     if (e == cudaSuccess) {
@@ -1137,27 +1141,54 @@ extern "C" int32_t tga_step_async(tga_solution *s, uint32_t mask) {
     return TGA_OK;
 }
 
+// The whole descent is captured once into a CUDA graph (memsets, kernels and the
+// per-step event records as external event nodes) and launched as one unit:
+// no per-kernel CPU launch cost and short inter-kernel gaps.
 extern "C" int32_t tga_descent(tga_solution *s, uint32_t mask, int32_t n_steps, void *l2_flush, uint64_t flush_bytes,
                                float *step_ms) {
     if (!s || n_steps < 0) return fail(TGA_ERR_INVALID_ARGUMENT, "descent arguments");
+    if (n_steps == 0) return TGA_OK;
+    if (set_device(s->inst) != TGA_OK) return TGA_ERR_CUDA;
     std::vector<cudaEvent_t> ev;
     if (step_ms) {
         ev.resize(2 * static_cast<size_t>(n_steps));
         for (auto &e : ev) TGA_CUDA(cudaEventCreate(&e));
     }
+    // capture on a private stream forked from the solution's stream
+    cudaStream_t cap;
+    TGA_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+    cudaStream_t saved = s->stream;
     int32_t rc = TGA_OK;
-    for (int k = 0; k < n_steps && rc == TGA_OK; ++k) {
-        if (l2_flush && flush_bytes) TGA_CUDA(cudaMemsetAsync(l2_flush, k & 0xFF, flush_bytes, s->stream));
-        if (step_ms) TGA_CUDA(cudaEventRecord(ev[2 * k], s->stream));
-        rc = tga_step_async(s, mask);
-        if (step_ms && rc == TGA_OK) TGA_CUDA(cudaEventRecord(ev[2 * k + 1], s->stream));
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaError_t e = order_after(cap, saved);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(saved);
+    if (e == cudaSuccess) e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+        s->stream = cap;
+        for (int k = 0; k < n_steps && rc == TGA_OK && e == cudaSuccess; ++k) {
+            if (l2_flush && flush_bytes) e = cudaMemsetAsync(l2_flush, k & 0xFF, flush_bytes, cap);
+            if (e == cudaSuccess && step_ms) e = cudaEventRecordWithFlags(ev[2 * k], cap, cudaEventRecordExternal);
+            if (e == cudaSuccess) rc = tga_step_async(s, mask);
+            if (e == cudaSuccess && rc == TGA_OK && step_ms)
+                e = cudaEventRecordWithFlags(ev[2 * k + 1], cap, cudaEventRecordExternal);
+        }
+        const cudaError_t e2 = cudaStreamEndCapture(cap, &graph);
+        if (e == cudaSuccess) e = e2;
+        s->stream = saved;
     }
-    if (step_ms && rc == TGA_OK) {
-        TGA_CUDA(cudaStreamSynchronize(s->stream));
-        for (int k = 0; k < n_steps; ++k) TGA_CUDA(cudaEventElapsedTime(&step_ms[k], ev[2 * k], ev[2 * k + 1]));
-    }
-    for (auto e : ev) cudaEventDestroy(e);
-    return rc;
+    if (e == cudaSuccess && rc == TGA_OK) e = cudaGraphInstantiate(&exec, graph, 0);
+    if (e == cudaSuccess && rc == TGA_OK) e = cudaGraphLaunch(exec, saved);
+    if (e == cudaSuccess && rc == TGA_OK) e = cudaStreamSynchronize(saved);
+    if (e == cudaSuccess && rc == TGA_OK && step_ms)
+        for (int k = 0; k < n_steps && e == cudaSuccess; ++k) e = cudaEventElapsedTime(&step_ms[k], ev[2 * k], ev[2 * k + 1]);
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    cudaStreamDestroy(cap);
+    for (auto x : ev) cudaEventDestroy(x);
+    if (rc != TGA_OK) return rc;
+    if (e != cudaSuccess) return fail(TGA_ERR_CUDA, std::string("descent graph: ") + cudaGetErrorString(e));
+    return TGA_OK;
 }
 
 extern "C" int32_t tga_solution_device_stats(tga_solution *s, uint64_t *counts, uint64_t *applied) {

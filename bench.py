@@ -345,7 +345,8 @@ def run_tga(args):
     inter_avg_s = statistics.mean(inter_ms) / 1e3
     R, N, Qc, _ = gs.info()
     Qp = N + 2 * R
-    inter_sel = [v for v in range(1, 11)]
+    # the CVRP fast path evaluates inter AND intra candidates in the one timed launch
+    inter_sel = [v for v in range(23) if (mask_all >> v) & 1] if inst.tw is None else list(range(1, 11))
     inter_cands = float(sum(int(dev_counts[v]) for v in inter_sel)) / K
     alg_bytes = (Qp * Qp / 2.0) * 4.0                    # Dp upper triangle, int32
     alg_ops = float(sum(int(dev_counts[v]) * ALG_OPS[v] for v in inter_sel)) / K
@@ -362,7 +363,7 @@ def run_tga(args):
                 "traffic": traffic_for("k_inter_all"),
                 "peak_source": f"148 SM x 128 lanes x {sm_mhz_peak:.0f} MHz ({pk_src} sm_max_mhz)"}
     primary, alt = (alu_view, hbm_view) if t_alu >= t_hbm else (hbm_view, alu_view)
-    primary = dict(primary, kernel="k_inter_fast<all-inter> (CVRP fused inter-route sweep), live CUDA events",
+    primary = dict(primary, kernel="k_inter_fast<all-inter> (CVRP: inter tiles + intra warps in one launch), live CUDA events",
                    kernel_ms=inter_avg_s * 1e3, candidates_per_launch=inter_cands,
                    alg_bytes_per_launch=alg_bytes, alg_ops_per_launch=alg_ops)
 

@@ -142,4 +142,78 @@ struct SolView {
     const uint32_t *tiles;    // generic inter-route tile plan (batch kernels)
 };
 
+// ------------------------------------------------------------------ intra-route CVRP (warp per u slot)
+__device__ __forceinline__ uint32_t intra_k32(bool ok, int32_t dD, int lane) {
+    // dD is bounded by 8 * max c < 2^25 (host-checked: max c < 2^21)
+    return ok ? ((static_cast<uint32_t>(dD + (1 << 25)) << 5) | static_cast<uint32_t>(lane)) : 0xFFFFFFFFu;
+}
+__device__ __forceinline__ void warp_keep(unsigned long long *red, int var, uint32_t k32, uint32_t idx_base, int lane) {
+    const uint32_t m = __reduce_min_sync(0xffffffffu, k32);
+    if (lane == 0 && m != 0xFFFFFFFFu) {
+        const int32_t s = static_cast<int32_t>(m >> 5) - (1 << 25);
+        atomicMin(&red[var], static_cast<unsigned long long>(pack_key(ord_score(s), idx_base + (m & 31u))));
+    }
+}
+
+// One warp evaluates every intra-route CVRP variant of u slot x (lane <-> v);
+// the per-variant warp minima are MIN-combined into the CTA's red[23].
+__device__ __forceinline__ void intra_cvrp_warp(const SolView<int32_t> &S, const ScoreParams &sp, uint32_t vmask,
+                                                int x, unsigned long long *red) {
+    const int lane = threadIdx.x & 31;
+    if (S.canon[x] >= 0 && S.pos[x] >= 1) {   // warp-uniform
+        const int p = S.pos[x], L = S.rlen[x], r = S.route[x];
+        const int base = x - p;
+        const bool ok_route = sp.mode == 1 || S.rW[r] <= sp.capacity;
+        const uint32_t cu = static_cast<uint32_t>(S.canon[x]);
+        const uint32_t cbase = cu - static_cast<uint32_t>(p);
+        auto D = [&](int a, int b) -> int32_t { return __ldg(S.Dp + static_cast<size_t>(a) * S.pitch + b); };
+        const int32_t em = S.enext[x - 1];
+        int32_t eo[3], rem[3];
+#pragma unroll
+        for (int N = 1; N <= 3; ++N) {
+            eo[N - 1] = S.enext[min(x + N - 1, base + L + 1)];
+            const int32_t br = N == 1 ? S.bridge1[x] : (N == 2 ? S.bridge2[x] : S.bridge3[x]);
+            rem[N - 1] = br - em - eo[N - 1];
+        }
+        for (int qb = 0; qb <= L; qb += 32) {
+            const int q = qb + lane;
+            const bool in = q <= L;
+            const int v = base + min(q, L);
+            const int vm1 = max(v - 1, base);          // masked lanes (q = 0) must still read a valid row
+            const uint32_t ib = cu * S.Qc + cbase + static_cast<uint32_t>(qb);
+            const int32_t ev = S.enext[v], evm = (q >= 1 && in) ? S.enext[v - 1] : 0;
+            // phase 1: every variant's 32-bit key in registers (all loads issued together)
+            uint32_t k[23];
+#pragma unroll
+            for (int i = 0; i < 23; ++i) k[i] = 0xFFFFFFFFu;
+            if (vmask & 1u)   // 2-opt: reverse u..v
+                k[0] = intra_k32(ok_route && in && q > p, D(x - 1, v) + D(x, v + 1) - em - ev, lane);
+#pragma unroll
+            for (int N = 1; N <= 3; ++N) {  // intra relocate / or-opt
+                if (!(vmask & (1u << (10 + N)))) continue;
+                const bool ok = ok_route && in && p + N - 1 <= L && (q < p - 1 || q > p + N - 1);
+                k[10 + N] = intra_k32(ok, rem[N - 1] + D(v, x) + D(x + N - 1, v + 1) - ev, lane);
+            }
+#pragma unroll
+            for (int a = 1; a <= 3; ++a) {   // intra swap (N1 = a at u, N2 = b at v), u + N1 <= v
+#pragma unroll
+                for (int b = 1; b <= 3; ++b) {
+                    const int var = 14 + 3 * (a - 1) + (b - 1);
+                    if (!(vmask & (1u << var))) continue;
+                    const bool ok = ok_route && in && q >= p + a && q + b - 1 <= L;
+                    const int32_t ev2 = S.enext[min(v + b - 1, base + L + 1)];
+                    const int32_t adj = D(x - 1, v) + D(v + b - 1, x) + D(x + a - 1, v + b) - em - evm - ev2;
+                    const int32_t gap = D(x - 1, v) + D(v + b - 1, x + a) + D(vm1, x) + D(x + a - 1, v + b) - em -
+                                        eo[a - 1] - evm - ev2;
+                    k[var] = intra_k32(ok, q == p + a ? adj : gap, lane);
+                }
+            }
+            // phase 2: one REDUX.MIN per variant
+#pragma unroll
+            for (int i = 0; i < 23; ++i)
+                if ((i == 0 || i >= 11) && (vmask & (1u << i))) warp_keep(red, i, k[i], ib, lane);
+        }
+    }
+}
+
 }  // namespace tga

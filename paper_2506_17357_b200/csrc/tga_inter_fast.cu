@@ -79,7 +79,9 @@ template <uint32_t MASK>
 __global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__restrict__ rec,
                                                              const __grid_constant__ CUtensorMap tmap,
                                                              const uint32_t *__restrict__ tiles, int t_lo, int t_hi,
-                                                             uint32_t Qc, int32_t cap, uint64_t *__restrict__ keys) {
+                                                             uint32_t Qc, int32_t cap, uint64_t *__restrict__ keys,
+                                                             const __grid_constant__ SolView<int32_t> SV,
+                                                             ScoreParams sp, uint32_t imask, int x_lo, int x_hi) {
     constexpr int U = kFastU, BW = kFastBoxW;
     constexpr int NV = 11;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -89,7 +91,7 @@ __global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__re
     SlotRec *const rows0 = reinterpret_cast<SlotRec *>(sm + 2 * kFastBoxBytesPadded);
     SlotRec *const rows1 = reinterpret_cast<SlotRec *>(sm + 2 * kFastBoxBytesPadded + kFastRowBytesPadded);
     __shared__ uint64_t bar[2];
-    __shared__ unsigned long long red[NV];
+    __shared__ unsigned long long red[23];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) {
@@ -97,7 +99,7 @@ __global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__re
         f_mbar_init(&bar[1]);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (tid < NV) red[tid] = kNoKey;
+    if (tid < 23) red[tid] = kNoKey;
     __syncthreads();
 
     uint64_t acc[NV];
@@ -115,6 +117,15 @@ __global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__re
 
     int t = t_lo + blockIdx.x;
     if (tid == 0 && t < t_hi) issue(t, 0);
+    // intra-route CVRP work of this launch (one u slot per warp) while the first
+    // tile's TMA is in flight: the whole neighbourhood is one kernel
+    if (imask) {
+        const int n_units = (x_hi - x_lo + 3) / 4;
+        for (int j = blockIdx.x; j < n_units; j += gridDim.x) {
+            const int x = x_lo + 4 * j + warp;
+            if (x < x_hi) intra_cvrp_warp(SV, sp, imask, x, red);
+        }
+    }
     uint32_t ph0 = 0u, ph1 = 0u;
     for (int it = 0; t < t_hi; t += gridDim.x, ++it) {
         const int b = it & 1;
@@ -205,31 +216,38 @@ __global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__re
         if (lane == 0 && k != kNoKey) atomicMin(&red[i], static_cast<unsigned long long>(k));
     }
     __syncthreads();
-    if (tid < NV && (MASK & (1u << tid)) && red[tid] != kNoKey)
-        atomicMin(reinterpret_cast<unsigned long long *>(keys) + tid, red[tid]);
+    if (tid < 23 && red[tid] != kNoKey) atomicMin(reinterpret_cast<unsigned long long *>(keys) + tid, red[tid]);
 }
 
 template <uint32_t MASK>
 static cudaError_t launch_fast_t(const SlotRec *rec, const CUtensorMap &map, const uint32_t *tiles, int t_lo, int t_hi,
-                                 uint32_t Qc, int32_t cap, uint64_t *keys, int grid, cudaStream_t st) {
+                                 uint32_t Qc, int32_t cap, uint64_t *keys, int grid, cudaStream_t st,
+                                 const SolView<int32_t> &SV, const ScoreParams &sp, uint32_t imask, int x_lo,
+                                 int x_hi) {
     auto kern = k_inter_fast<MASK>;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kFastSmem);
         attr = true;
     }
-    kern<<<grid, kFastThreads, kFastSmem, st>>>(rec, map, tiles, t_lo, t_hi, Qc, cap, keys);
+    kern<<<grid, kFastThreads, kFastSmem, st>>>(rec, map, tiles, t_lo, t_hi, Qc, cap, keys, SV, sp, imask, x_lo, x_hi);
     note_launch();
     return cudaGetLastError();
 }
 
 cudaError_t launch_inter_fast(uint32_t mask, const SlotRec *rec, const CUtensorMap &map, const uint32_t *tiles, int t_lo,
-                              int t_hi, uint32_t Qc, int32_t cap, uint64_t *keys, int grid, cudaStream_t st) {
-    if (t_hi <= t_lo || !(mask & 0x7FEu)) return cudaSuccess;
+                              int t_hi, uint32_t Qc, int32_t cap, uint64_t *keys, int max_grid, cudaStream_t st,
+                              const SolView<int32_t> &SV, const ScoreParams &sp, uint32_t imask, int x_lo, int x_hi) {
+    if (!(mask & 0x7FEu)) return cudaSuccess;
     cudaError_t err = cudaSuccess;
+    // the intra-route work rides along with the first launch
+    const int units = imask ? (x_hi - x_lo + 3) / 4 : 0;
     auto run = [&](auto kmask) {
-        if (err == cudaSuccess)
-            err = launch_fast_t<decltype(kmask)::value>(rec, map, tiles, t_lo, t_hi, Qc, cap, keys, grid, st);
+        if (err != cudaSuccess) return;
+        const int grid = std::max(1, std::min(std::max(t_hi - t_lo, units), max_grid));
+        err = launch_fast_t<decltype(kmask)::value>(rec, map, tiles, t_lo, t_hi, Qc, cap, keys, grid, st, SV, sp,
+                                                    imask, x_lo, x_hi);
+        imask = 0;
     };
     constexpr uint32_t ALL = 0x7FEu, NS = (1u << 1) | (1u << 2) | (1u << 5);
     if ((mask & ALL) == ALL) { run(std::integral_constant<uint32_t, ALL>{}); return err; }

@@ -93,6 +93,7 @@ cudaError_t launch_batch(uint32_t mask, bool tw, const SolView<DT> *views, const
 unsigned long long launch_count();
 void note_launch();
 cudaError_t launch_inter_fast(uint32_t mask, const SlotRec *rec, const CUtensorMap &map, const uint32_t *tiles, int t_lo,
-                              int t_hi, uint32_t Qc, int32_t cap, uint64_t *keys, int grid, cudaStream_t st);
+                              int t_hi, uint32_t Qc, int32_t cap, uint64_t *keys, int max_grid, cudaStream_t st,
+                              const SolView<int32_t> &SV, const ScoreParams &sp, uint32_t imask, int x_lo, int x_hi);
 
 }  // namespace tga

@@ -714,6 +714,7 @@ extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
     const int x_lo = static_cast<int>(a), x_hi = static_cast<int>(b);
     const int grid = std::max(1, std::min(t_hi - t_lo, s->sm_count * 4));
     cudaError_t e;
+    bool fused_intra = false;
     const bool timed = s->timing && (mask & TGA_OP_INTER) && s->tev_n + 2 <= static_cast<int>(s->tev.size());
     // inside a captured graph (tga_descent) the records must be external event nodes
     cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
@@ -723,9 +724,11 @@ extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
     if (I->dtype == TGA_I32 && s->fast) {
         tga_shard_range(s->n_ftiles, s->shard, s->n_shards, &a, &b);
         const int f_lo = static_cast<int>(a), f_hi = static_cast<int>(b);
-        const int fgrid = std::max(1, std::min(f_hi - f_lo, s->sm_count * 4));
+        // fused: inter tiles + the intra-route CVRP work in one launch (when there is inter work)
+        fused_intra = (mask & TGA_OP_INTER) && !I->tw && I->max_c_abs < (1 << 21);
+        const uint32_t imask = fused_intra ? (mask & TGA_OP_INTRA) : 0u;
         e = launch_inter_fast(mask, s->rec, s->fmap, s->d_ftiles, f_lo, f_hi, static_cast<uint32_t>(s->Qc), I->Q,
-                              s->keys, fgrid, st);
+                              s->keys, s->sm_count * 4, st, sol_view<int32_t>(s), sp, imask, x_lo, x_hi);
     } else if (I->dtype == TGA_I32) {
         e = launch_inter<int32_t>(mask, I->tw, sol_view<int32_t>(s), s->tmap, s->d_tiles, t_lo, t_hi, sp, s->keys,
                                   grid, st);
@@ -737,7 +740,7 @@ extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
         TGA_CUDA(cudaEventRecordWithFlags(s->tev[s->tev_n + 1], st, rec_flags));
         s->tev_n += 2;
     }
-    if (e == cudaSuccess) {
+    if (e == cudaSuccess && !fused_intra) {
         if (I->dtype == TGA_I32)
             e = launch_intra<int32_t>(mask, I->tw, sol_view<int32_t>(s), sp, x_lo, x_hi, s->keys, st,
                                       I->max_c_abs < (1 << 21));

@@ -75,21 +75,24 @@ __device__ __forceinline__ void fold(uint64_t &acc, const Run &b, bool direct, u
 
 // stream slots: 0 2opt* | 1,2 reloc1 d/r | 3,4 oropt2 | 5,6 oropt3 | 7 swap11 |
 // 8,9 cross12 | 10,11 cross13 | 12 cross22 | 13,14 cross23 | 15 cross33
-template <uint32_t MASK>
+template <int U, uint32_t MASK>
 __global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__restrict__ rec,
                                                              const __grid_constant__ CUtensorMap tmap,
                                                              const uint32_t *__restrict__ tiles, int t_lo, int t_hi,
                                                              uint32_t Qc, int32_t cap, uint64_t *__restrict__ keys,
                                                              const __grid_constant__ SolView<int32_t> SV,
                                                              ScoreParams sp, uint32_t imask, int x_lo, int x_hi) {
-    constexpr int U = kFastU, BW = kFastBoxW;
+    using G = FastGeom<U>;
+    constexpr int BW = G::BoxW;
     constexpr int NV = 11;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *sm = smem_raw + ((128u - (s_u32(smem_raw) & 127u)) & 127u);
     int32_t *const dp0 = reinterpret_cast<int32_t *>(sm);
-    int32_t *const dp1 = reinterpret_cast<int32_t *>(sm + kFastBoxBytesPadded);
-    SlotRec *const rows0 = reinterpret_cast<SlotRec *>(sm + 2 * kFastBoxBytesPadded);
-    SlotRec *const rows1 = reinterpret_cast<SlotRec *>(sm + 2 * kFastBoxBytesPadded + kFastRowBytesPadded);
+    int32_t *const dp1 = reinterpret_cast<int32_t *>(sm + G::BoxPad);
+    SlotRec *const rows0 = reinterpret_cast<SlotRec *>(sm + 2 * G::BoxPad);
+    SlotRec *const rows1 = reinterpret_cast<SlotRec *>(sm + 2 * G::BoxPad + G::RowBytes);
+    SlotRec *const cols0 = reinterpret_cast<SlotRec *>(sm + 2 * G::BoxPad + 2 * G::RowBytes);
+    SlotRec *const cols1 = reinterpret_cast<SlotRec *>(sm + 2 * G::BoxPad + 2 * G::RowBytes + G::ColBytes);
     __shared__ uint64_t bar[2];
     __shared__ unsigned long long red[23];
 
@@ -110,9 +113,10 @@ __global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__re
         const uint32_t ij = tiles[t];
         const int I = ij >> 16, J = ij & 0xFFFF;
         uint64_t *br = b ? &bar[1] : &bar[0];
-        f_expect(br, kFastBoxBytes + U * 96);
+        f_expect(br, G::BoxBytes + G::RowBytes + G::ColBytes);
         f_tma2d(b ? dp1 : dp0, &tmap, J * kFastTV - 4, I * U - 1, br);
-        f_bulk(b ? rows1 : rows0, rec + I * U, U * 96, br);
+        f_bulk(b ? rows1 : rows0, rec + I * U, G::RowBytes, br);
+        f_bulk(b ? cols1 : cols0, rec + J * kFastTV, G::ColBytes, br);
     };
 
     int t = t_lo + blockIdx.x;
@@ -134,9 +138,10 @@ __global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__re
         const int u0 = (ij >> 16) * U, v0 = (ij & 0xFFFF) * kFastTV;
         const int col = warp * 32 + lane;   // column inside the tile
         const int v = v0 + col;
-        // ---- this lane's column record (six 16-byte loads; overlaps the TMA)
-        const SlotRec V = rec[v];
         if (b) { f_wait(&bar[1], ph1); ph1 ^= 1u; } else { f_wait(&bar[0], ph0); ph0 ^= 1u; }
+        // ---- this lane's column record, bulk-copied with the tile (six 16-byte LDS)
+        const SlotRec V = (b ? cols1 : cols0)[col];
+        (void)v;
         const int32_t *T = b ? dp1 : dp0;
         const SlotRec *RW = b ? rows1 : rows0;
         // Dp(u0 + i + di, v + dj), i = row index in the tile
@@ -219,25 +224,28 @@ __global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__re
     if (tid < 23 && red[tid] != kNoKey) atomicMin(reinterpret_cast<unsigned long long *>(keys) + tid, red[tid]);
 }
 
-template <uint32_t MASK>
+template <int U, uint32_t MASK>
 static cudaError_t launch_fast_t(const SlotRec *rec, const CUtensorMap &map, const uint32_t *tiles, int t_lo, int t_hi,
                                  uint32_t Qc, int32_t cap, uint64_t *keys, int grid, cudaStream_t st,
                                  const SolView<int32_t> &SV, const ScoreParams &sp, uint32_t imask, int x_lo,
                                  int x_hi) {
-    auto kern = k_inter_fast<MASK>;
+    auto kern = k_inter_fast<U, MASK>;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kFastSmem);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, FastGeom<U>::Smem);
         attr = true;
     }
-    kern<<<grid, kFastThreads, kFastSmem, st>>>(rec, map, tiles, t_lo, t_hi, Qc, cap, keys, SV, sp, imask, x_lo, x_hi);
+    kern<<<grid, kFastThreads, FastGeom<U>::Smem, st>>>(rec, map, tiles, t_lo, t_hi, Qc, cap, keys, SV, sp, imask,
+                                                         x_lo, x_hi);
     note_launch();
     return cudaGetLastError();
 }
 
-cudaError_t launch_inter_fast(uint32_t mask, const SlotRec *rec, const CUtensorMap &map, const uint32_t *tiles, int t_lo,
-                              int t_hi, uint32_t Qc, int32_t cap, uint64_t *keys, int max_grid, cudaStream_t st,
-                              const SolView<int32_t> &SV, const ScoreParams &sp, uint32_t imask, int x_lo, int x_hi) {
+template <int U>
+static cudaError_t launch_fast_u(uint32_t mask, const SlotRec *rec, const CUtensorMap &map, const uint32_t *tiles,
+                                 int t_lo, int t_hi, uint32_t Qc, int32_t cap, uint64_t *keys, int max_grid,
+                                 cudaStream_t st, const SolView<int32_t> &SV, const ScoreParams &sp, uint32_t imask,
+                                 int x_lo, int x_hi) {
     if (!(mask & 0x7FEu)) return cudaSuccess;
     cudaError_t err = cudaSuccess;
     // the intra-route work rides along with the first launch
@@ -245,8 +253,8 @@ cudaError_t launch_inter_fast(uint32_t mask, const SlotRec *rec, const CUtensorM
     auto run = [&](auto kmask) {
         if (err != cudaSuccess) return;
         const int grid = std::max(1, std::min(std::max(t_hi - t_lo, units), max_grid));
-        err = launch_fast_t<decltype(kmask)::value>(rec, map, tiles, t_lo, t_hi, Qc, cap, keys, grid, st, SV, sp,
-                                                    imask, x_lo, x_hi);
+        err = launch_fast_t<U, decltype(kmask)::value>(rec, map, tiles, t_lo, t_hi, Qc, cap, keys, grid, st, SV, sp,
+                                                       imask, x_lo, x_hi);
         imask = 0;
     };
     constexpr uint32_t ALL = 0x7FEu, NS = (1u << 1) | (1u << 2) | (1u << 5);
@@ -258,6 +266,16 @@ cudaError_t launch_inter_fast(uint32_t mask, const SlotRec *rec, const CUtensorM
     if (mask & (1u << 5)) run(std::integral_constant<uint32_t, (1u << 5)>{});
     if (mask & (0x1Fu << 6)) run(std::integral_constant<uint32_t, (0x1Fu << 6)>{});
     return err;
+}
+
+cudaError_t launch_inter_fast(int U, uint32_t mask, const SlotRec *rec, const CUtensorMap &map, const uint32_t *tiles,
+                              int t_lo, int t_hi, uint32_t Qc, int32_t cap, uint64_t *keys, int max_grid,
+                              cudaStream_t st, const SolView<int32_t> &SV, const ScoreParams &sp, uint32_t imask,
+                              int x_lo, int x_hi) {
+    return U == 8 ? launch_fast_u<8>(mask, rec, map, tiles, t_lo, t_hi, Qc, cap, keys, max_grid, st, SV, sp, imask,
+                                     x_lo, x_hi)
+                  : launch_fast_u<16>(mask, rec, map, tiles, t_lo, t_hi, Qc, cap, keys, max_grid, st, SV, sp, imask,
+                                      x_lo, x_hi);
 }
 
 }  // namespace tga

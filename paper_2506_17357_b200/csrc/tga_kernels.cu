@@ -15,6 +15,7 @@
 
 #include "tga_device.cuh"
 #include "tga_launch.h"
+#include "tga_pick.cuh"
 
 namespace tga {
 
@@ -285,26 +286,54 @@ __global__ void __launch_bounds__(256) k_update(ScanArgs<DT> A, DT *__restrict__
     update_units<DT, TW>(A, Dp, pitch, Qp, lo, hi, r_lo, r_hi, blockIdx.x, gridDim.x);
 }
 
-// device-resident variant: bounds from the descriptor written by k_pick_apply
-// (tga_device_step.cu); blockIdx.y = solution; grid-stride over the units.
-template <class DT, bool TW>
-__global__ void __launch_bounds__(256) k_update_dev(const DevState *__restrict__ states,
-                                                    const ScanArgs<DT> *__restrict__ scans) {
-    const DevState &S = states[blockIdx.y];
-    if (S.desc[0] == 0) return;
-    update_units<DT, TW>(scans[blockIdx.y], static_cast<DT *>(S.Dp), S.pitch, S.Qp, S.desc[1], S.desc[2], S.desc[3],
-                         S.desc[4], blockIdx.x, gridDim.x);
+// Device-resident apply + update in ONE launch (blockIdx.y = solution): block 0
+// picks the best key and splices the changed routes (tga_pick.cuh), a grid
+// barrier over the gridDim.x blocks of the solution (all co-resident: the grid
+// is at most one block per SM), then every block refreshes Dp rows / columns
+// and re-scans routes of the changed span read from the descriptor.
+__device__ __forceinline__ void solution_barrier(int32_t *counter, int nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const int v = atomicAdd(counter, 1);
+        const int target = (v / nblocks + 1) * nblocks;  // launches of one stream never overlap
+        while (*reinterpret_cast<volatile int32_t *>(counter) < target) __nanosleep(64);
+        __threadfence();
+    }
+    __syncthreads();
 }
 
-cudaError_t launch_update_dev(const DevState *states, const void *scans, int n_sol, bool tw, bool is_int,
-                              int blocks_per_sol, cudaStream_t st) {
+template <class DT, bool TW>
+__global__ void __launch_bounds__(256) k_pick_update(const DevState *__restrict__ states,
+                                                     const ScanArgs<DT> *__restrict__ scans, uint32_t mask,
+                                                     int integer) {
+    extern __shared__ int32_t smr[];
+    const DevState &S = states[blockIdx.y];
+    if (blockIdx.x == 0) pick_apply_body(S, mask, integer, smr);
+    if (gridDim.x > 1) solution_barrier(S.desc + 6, gridDim.x);
+    else __syncthreads();
+    const volatile int32_t *desc = S.desc;
+    if (desc[0] == 0) return;
+    update_units<DT, TW>(scans[blockIdx.y], static_cast<DT *>(S.Dp), S.pitch, S.Qp, desc[1], desc[2], desc[3],
+                         desc[4], blockIdx.x, gridDim.x);
+}
+
+cudaError_t launch_pick_update(const DevState *states, const void *scans, int n_sol, bool tw, bool is_int,
+                               uint32_t mask, int max_routes, int blocks_per_sol, cudaStream_t st) {
+    const int smem = 3 * (max_routes + 1) * 4;
     dim3 g(blocks_per_sol, n_sol);
+    if (smem > 48 * 1024) {
+        cudaFuncSetAttribute(k_pick_update<int32_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_pick_update<int32_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_pick_update<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_pick_update<float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    }
     if (is_int) {
-        if (tw) k_update_dev<int32_t, true><<<g, 256, 0, st>>>(states, static_cast<const ScanArgs<int32_t> *>(scans));
-        else    k_update_dev<int32_t, false><<<g, 256, 0, st>>>(states, static_cast<const ScanArgs<int32_t> *>(scans));
+        if (tw) k_pick_update<int32_t, true><<<g, 256, smem, st>>>(states, static_cast<const ScanArgs<int32_t> *>(scans), mask, 1);
+        else    k_pick_update<int32_t, false><<<g, 256, smem, st>>>(states, static_cast<const ScanArgs<int32_t> *>(scans), mask, 1);
     } else {
-        if (tw) k_update_dev<float, true><<<g, 256, 0, st>>>(states, static_cast<const ScanArgs<float> *>(scans));
-        else    k_update_dev<float, false><<<g, 256, 0, st>>>(states, static_cast<const ScanArgs<float> *>(scans));
+        if (tw) k_pick_update<float, true><<<g, 256, smem, st>>>(states, static_cast<const ScanArgs<float> *>(scans), mask, 0);
+        else    k_pick_update<float, false><<<g, 256, smem, st>>>(states, static_cast<const ScanArgs<float> *>(scans), mask, 0);
     }
     note_launch();
     return cudaGetLastError();

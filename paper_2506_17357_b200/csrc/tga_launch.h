@@ -24,16 +24,21 @@ constexpr int kBoxBytes = kBoxW * kBoxH * 4;
 constexpr int kBoxBytesPadded = (kBoxBytes + 127) / 128 * 128;
 constexpr int kPitchAlign = 128;                // Dp pitch: multiple of every tile width
 
-// CVRP fast path (k_inter_fast): 4 warps, tile = kFastU rows x 128 columns
+// CVRP fast path (k_inter_fast<U>): 4 warps, tile = U rows x 128 columns,
+// U = 8 for small neighbourhoods (more tiles than resident CTAs), 16 otherwise
 constexpr int kFastThreads = 128;
-constexpr int kFastU = 16;
 constexpr int kFastTV = 128;
-constexpr int kFastBoxW = kFastTV + 8;          // cols v0-4 .. v0+131 (16-byte aligned TMA x)
-constexpr int kFastBoxH = kFastU + 4;           // rows u0-1 .. u0+U+2
-constexpr int kFastBoxBytes = kFastBoxW * kFastBoxH * 4;
-constexpr int kFastBoxBytesPadded = (kFastBoxBytes + 127) / 128 * 128;
-constexpr int kFastRowBytesPadded = (kFastU * 96 + 127) / 128 * 128;
-constexpr int kFastSmem = 2 * kFastBoxBytesPadded + 2 * kFastRowBytesPadded + 128;
+template <int U>
+struct FastGeom {
+    static constexpr int BoxW = kFastTV + 8;                    // cols v0-4 .. v0+131 (16-byte aligned TMA x)
+    static constexpr int BoxH = U + 4;                          // rows u0-1 .. u0+U+2
+    static constexpr int BoxBytes = BoxW * BoxH * 4;
+    static constexpr int BoxPad = (BoxBytes + 127) / 128 * 128;
+    static constexpr int RowBytes = U * 96;                     // row records (bulk copy)
+    static constexpr int ColBytes = kFastTV * 96;               // column records (bulk copy)
+    static constexpr int Smem = 2 * BoxPad + 2 * RowBytes + 2 * ColBytes + 128;
+    static_assert(RowBytes % 128 == 0 && ColBytes % 128 == 0, "bulk copy alignment");
+};
 constexpr int kGuard = 8;                       // guard slots before/after every slot array
 
 template <class DT>
@@ -62,15 +67,13 @@ struct DevState {
     int32_t *rbase, *rlenR, *cbase;              // per route
     int32_t *scratch;                            // snapshot of a changed span (cap ints)
     const uint64_t *keys;                        // 23 packed keys of the last evaluation
-    int32_t *desc;                               // [applied, lo, hi, r_lo, r_hi)
+    int32_t *desc;                               // [applied, lo, hi, r_lo, r_hi), [6] grid-barrier counter
     unsigned long long *acc;                     // [23] candidate counts + [23] applied moves
     void *Dp;
     int32_t R, Qc, Qp, pitch;
 };
-cudaError_t launch_pick_apply(const DevState *states, int n_sol, bool is_int, uint32_t mask, int max_routes,
-                              cudaStream_t st);
-cudaError_t launch_update_dev(const DevState *states, const void *scans, int n_sol, bool tw, bool is_int,
-                              int blocks_per_sol, cudaStream_t st);
+cudaError_t launch_pick_update(const DevState *states, const void *scans, int n_sol, bool tw, bool is_int,
+                               uint32_t mask, int max_routes, int blocks_per_sol, cudaStream_t st);
 
 template <class DT>
 cudaError_t launch_dp(DT *Dp, int pitch, const int32_t *node, const DT *C, int n, int Qp, int lo, int hi,
@@ -92,8 +95,9 @@ cudaError_t launch_batch(uint32_t mask, bool tw, const SolView<DT> *views, const
                          uint64_t *keys, int grid, cudaStream_t st);
 unsigned long long launch_count();
 void note_launch();
-cudaError_t launch_inter_fast(uint32_t mask, const SlotRec *rec, const CUtensorMap &map, const uint32_t *tiles, int t_lo,
-                              int t_hi, uint32_t Qc, int32_t cap, uint64_t *keys, int max_grid, cudaStream_t st,
-                              const SolView<int32_t> &SV, const ScoreParams &sp, uint32_t imask, int x_lo, int x_hi);
+cudaError_t launch_inter_fast(int U, uint32_t mask, const SlotRec *rec, const CUtensorMap &map, const uint32_t *tiles,
+                              int t_lo, int t_hi, uint32_t Qc, int32_t cap, uint64_t *keys, int max_grid,
+                              cudaStream_t st, const SolView<int32_t> &SV, const ScoreParams &sp, uint32_t imask,
+                              int x_lo, int x_hi);
 
 }  // namespace tga

@@ -2,15 +2,16 @@
 // Alg. A2 lines 5-8; the "Update" step of §5.3.5, without a
 // GPU-CPU round trip -- the paper's observed bottleneck).
 //
-//   k_pick_apply   one CTA per solution: candidate counts of the evaluated
+//   pick_apply_body  one CTA per solution: candidate counts of the evaluated
 //                  neighbourhood (closed forms over route lengths), best key
 //                  over the operator mask (lowest (score, variant, index)),
 //                  decode, and -- if improving -- the splice of the 1-2 changed
 //                  routes directly in the slot arrays (snapshot of the changed
 //                  span, piece-wise remap), new route bases / lengths / canonical
 //                  offsets, and a descriptor of the changed span.
-//   k_update_dev   Dp row/column refresh of the span + re-scan of its routes,
+//   (k_pick_update in tga_kernels.cu) Dp row/column refresh of the span + re-scan of its routes,
 //                  bounds read from the descriptor (grid-stride; no host sync).
+#pragma once
 #include <cuda_runtime.h>
 #include <cstdint>
 
@@ -19,7 +20,7 @@
 
 namespace tga {
 
-namespace {
+namespace pick {
 // a piece of a new route: customers [start, start+len) of old route `src`
 // (1-based positions), possibly reversed (2-opt)
 struct Piece {
@@ -45,14 +46,13 @@ __device__ __forceinline__ int find_route(const int32_t *cbase, int R, int c) {
 }
 
 __device__ __forceinline__ int64_t pz(int64_t x) { return x > 0 ? x : 0; }
-}  // namespace
+}  // namespace pick
+using namespace pick;
 
 // ------------------------------------------------------------------ pick + apply
 // Route arrays (base, length, canonical base) are staged in shared memory so the
 // serial parts (decode, binary searches over routes) never wait on global loads.
-__global__ void __launch_bounds__(256) k_pick_apply(const DevState *__restrict__ states, uint32_t mask, int integer) {
-    extern __shared__ int32_t smr[];
-    const DevState &S = states[blockIdx.x];
+__device__ __forceinline__ void pick_apply_body(const DevState &S, uint32_t mask, int integer, int32_t *smr) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int R = S.R;
     int32_t *sb = smr, *sl = smr + (R + 1), *sc = smr + 2 * (R + 1);
@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(256) k_pick_apply(const DevState *__restrict__
     __syncthreads();
     if (!sh_applied) {
         if (tid == 0) S.desc[0] = 0;
-        return;
+        return;  // uniform across the block
     }
     const int lo = sh_lo, hi = sh_hi, rlo = sh_rlo, rhi = sh_rhi, dlt = sh_d, nrt = sh_n;
     // ---- 3. snapshot the changed span of node ids
@@ -257,19 +257,6 @@ __global__ void __launch_bounds__(256) k_pick_apply(const DevState *__restrict__
         S.desc[4] = rhi + 1;
         S.acc[23] += 1;
     }
-}
-
-cudaError_t launch_pick_apply(const DevState *states, int n_sol, bool is_int, uint32_t mask, int max_routes,
-                              cudaStream_t st) {
-    const int smem = 3 * (max_routes + 1) * 4;
-    static int attr = 0;
-    if (smem > 48 * 1024 && smem > attr) {
-        cudaFuncSetAttribute(k_pick_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr = smem;
-    }
-    k_pick_apply<<<n_sol, 256, smem, st>>>(states, mask, is_int ? 1 : 0);
-    note_launch();
-    return cudaGetLastError();
 }
 
 }  // namespace tga

@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <cstdlib>
 #include <limits>
 #include <new>
 #include <string>
@@ -139,6 +140,7 @@ struct tga_solution {
     int n_ftiles = 0;
     CUtensorMap fmap{};
     bool fast = false;
+    int fastU = 16;                // rows per fast-path tile (8 for small neighbourhoods)
     uint64_t *h_keys = nullptr;                         // pinned
     int32_t *h_stage = nullptr;                         // pinned staging: 5 rows of lay_pitch bytes
     int32_t *h_rstage = nullptr;                        // pinned staging: 2 rows of route_pitch bytes
@@ -367,11 +369,12 @@ static void build_tiles(tga_solution *s) {
     }
     s->n_tiles = static_cast<int>(t.size());
     cudaMemcpy(s->d_tiles, t.data(), sizeof(uint32_t) * t.size(), cudaMemcpyHostToDevice);
-    // fast-path plan: kFastU x kFastTV tiles of the upper triangle
+    // fast-path plan: fastU x kFastTV tiles of the upper triangle
     std::vector<uint32_t> f;
-    for (int I = 0; I < s->pitch / kFastU && I * kFastU < s->Qp; ++I)
+    const int U = s->fastU;
+    for (int I = 0; I < s->pitch / U && I * U < s->Qp; ++I)
         for (int J = 0; J < s->pitch / kFastTV && J * kFastTV < s->Qp; ++J)
-            if (I * kFastU < J * kFastTV + kFastTV - 1) f.push_back((static_cast<uint32_t>(I) << 16) | J);
+            if (I * U < J * kFastTV + kFastTV - 1) f.push_back((static_cast<uint32_t>(I) << 16) | J);
     s->n_ftiles = static_cast<int>(f.size());
     if (s->d_ftiles) cudaMemcpy(s->d_ftiles, f.data(), sizeof(uint32_t) * f.size(), cudaMemcpyHostToDevice);
 }
@@ -539,7 +542,9 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
     void *v_fT, *v_bT, *v_s2, *v_s3, *v_rbase, *v_rlenR, *v_cbase, *v_rW, *v_rTV, *v_rD, *v_keys, *v_tiles;
     void *v_ds, *v_sa, *v_desc, *v_scr, *v_acc;
     void *v_rec = nullptr, *v_ftiles = nullptr;
-    const size_t ftiles_max = static_cast<size_t>(s->pitch / kFastU) * (s->pitch / kFastTV) + 1;
+    s->fastU = 16;  // U = 8 measured no better at n = 1000 (more tiles, more per-tile overhead)
+    if (const char *ev = std::getenv("TGA_FAST_U")) s->fastU = std::atoi(ev) == 8 ? 8 : 16;  // tuning override
+    const size_t ftiles_max = static_cast<size_t>(s->pitch / s->fastU) * (s->pitch / kFastTV) + 1;
     const bool want_fast = I->dtype == TGA_I32 && !I->tw && I->opt.score_mode == TGA_SCORE_FEASIBLE && I->fast_ok;
     Item items[] = {
         {&v_node, cap * 4}, {&v_route, cap * 4}, {&v_pos, cap * 4}, {&v_rlen, cap * 4}, {&v_canon, cap * 4},
@@ -630,7 +635,7 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
         auto enc = get_encode();
         cuuint64_t gdim[2] = {static_cast<cuuint64_t>(s->pitch), static_cast<cuuint64_t>(s->pitch)};
         cuuint64_t gstride[1] = {static_cast<cuuint64_t>(s->pitch) * 4};
-        cuuint32_t box[2] = {static_cast<cuuint32_t>(kFastBoxW), static_cast<cuuint32_t>(kFastBoxH)};
+        cuuint32_t box[2] = {static_cast<cuuint32_t>(kFastTV + 8), static_cast<cuuint32_t>(s->fastU + 4)};
         cuuint32_t estr[2] = {1, 1};
         CUresult cr = enc(&s->fmap, CU_TENSOR_MAP_DATA_TYPE_INT32, 2, s->Dp, gdim, gstride, box, estr,
                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -727,8 +732,8 @@ extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
         // fused: inter tiles + the intra-route CVRP work in one launch (when there is inter work)
         fused_intra = (mask & TGA_OP_INTER) && !I->tw && I->max_c_abs < (1 << 21);
         const uint32_t imask = fused_intra ? (mask & TGA_OP_INTRA) : 0u;
-        e = launch_inter_fast(mask, s->rec, s->fmap, s->d_ftiles, f_lo, f_hi, static_cast<uint32_t>(s->Qc), I->Q,
-                              s->keys, s->sm_count * 4, st, sol_view<int32_t>(s), sp, imask, x_lo, x_hi);
+        e = launch_inter_fast(s->fastU, mask, s->rec, s->fmap, s->d_ftiles, f_lo, f_hi, static_cast<uint32_t>(s->Qc),
+                              I->Q, s->keys, s->sm_count * 4, st, sol_view<int32_t>(s), sp, imask, x_lo, x_hi);
     } else if (I->dtype == TGA_I32) {
         e = launch_inter<int32_t>(mask, I->tw, sol_view<int32_t>(s), s->tmap, s->d_tiles, t_lo, t_hi, sp, s->keys,
                                   grid, st);
@@ -1134,9 +1139,9 @@ extern "C" int32_t tga_step_async(tga_solution *s, uint32_t mask) {
     int32_t rc = tga_eval(s, mask, nullptr);
     if (rc != TGA_OK) return rc;
     const tga_instance *I = s->inst;
-    cudaError_t e = launch_pick_apply(s->d_ds, 1, I->dtype == TGA_I32, s->eval_mask, s->R, s->stream);
-    if (e == cudaSuccess)
-        e = launch_update_dev(s->d_ds, s->d_sa, 1, I->tw, I->dtype == TGA_I32, s->sm_count * 2, s->stream);
+    // pick + splice + update in one launch: one block per SM at most (grid barrier)
+    cudaError_t e = launch_pick_update(s->d_ds, s->d_sa, 1, I->tw, I->dtype == TGA_I32, s->eval_mask, s->R,
+                                       s->sm_count, s->stream);
     if (e != cudaSuccess) return fail(TGA_ERR_CUDA, std::string("device step: ") + cudaGetErrorString(e));
     ++s->gen;
     s->host_stale = true;
@@ -1405,10 +1410,9 @@ extern "C" int32_t tga_batch_step_async(tga_batch *b, uint32_t mask) {
     const int n = static_cast<int>(b->sols.size());
     int max_r = 0;
     for (auto *s : b->sols) max_r = std::max(max_r, s->R);
-    cudaError_t e = launch_pick_apply(b->d_states, n, I->dtype == TGA_I32, b->eval_mask, max_r, b->stream);
-    if (e == cudaSuccess)
-        e = launch_update_dev(b->d_states, b->d_scans, n, I->tw, I->dtype == TGA_I32,
-                              std::max(1, b->sm_count * 4 / n), b->stream);
+    // blocks per solution so that the whole grid is co-resident (grid barrier)
+    cudaError_t e = launch_pick_update(b->d_states, b->d_scans, n, I->tw, I->dtype == TGA_I32, b->eval_mask, max_r,
+                                       std::max(1, b->sm_count * 2 / n), b->stream);
     if (e != cudaSuccess) return fail(TGA_ERR_CUDA, std::string("batch device step: ") + cudaGetErrorString(e));
     for (auto *s : b->sols) {
         ++s->gen;

@@ -114,10 +114,11 @@ def peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
-def traffic_for(kernel_tag: str):
+def traffic_for(config: str):
+    """DRAM bytes per launch of the dominant kernel from one committed ncu --set full capture."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(p):
-        return json.load(open(p)).get(kernel_tag)
+        return json.load(open(p)).get(config)
     return None
 
 
@@ -357,10 +358,10 @@ def run_tga(args):
     t_alu = alg_ops / alu_peak
     hbm_view = {"bound": "hbm", "achieved": alg_bytes / inter_avg_s / 1e9, "peak": hbm_peak / 1e9,
                 "unit": "GB/s", "frac": (alg_bytes / inter_avg_s) / hbm_peak,
-                "traffic": traffic_for("k_inter_all"), "peak_source": pk_src}
+                "traffic": traffic_for(args.config), "peak_source": pk_src}
     alu_view = {"bound": "alu", "achieved": alg_ops / inter_avg_s / 1e12, "peak": alu_peak / 1e12,
                 "unit": "Tops/s", "frac": (alg_ops / inter_avg_s) / alu_peak,
-                "traffic": traffic_for("k_inter_all"),
+                "traffic": traffic_for(args.config),
                 "peak_source": f"148 SM x 128 lanes x {sm_mhz_peak:.0f} MHz ({pk_src} sm_max_mhz)"}
     primary, alt = (alu_view, hbm_view) if t_alu >= t_hbm else (hbm_view, alu_view)
     primary = dict(primary, kernel="k_inter_fast<all-inter> (CVRP: inter tiles + intra warps in one launch), live CUDA events",

@@ -117,6 +117,24 @@ struct __align__(16) SlotRec {
 };
 static_assert(sizeof(SlotRec) == 96, "SlotRec layout");
 
+// Time-window part of the fast-path record (VRPTW "TW-I", feasible-only mode).
+// With T_V = 0 on both sides, T_V(s1 + s2) == 0  <=>  T_E(s1)+T_D(s1)+t <= T_L(s2)
+// (Eq. 4b/4d/4h with T_W = 0), and the earliest completion of s1 + seg is
+// max(T_E(s1)+T_D(s1)+t, T_E(seg)) + T_D(seg) (Eq. 4e/4f): every concatenation
+// of a candidate becomes one add, one max and one compare.  Infeasible parts
+// carry +-kTwBig.  All values are integer-valued floats (< 2^24: exact).
+constexpr float kTwBig = 1.0e30f;
+struct __align__(16) SlotTW {
+    float EF;        // earliest completion of the prefix [0..x] (T_E + T_D), +BIG if T_V > 0
+    float EFm;       // the same for [0..x-1]
+    float LBN[3];    // latest start of the suffix [x+N..L+1] (T_L), -BIG if T_V > 0 or absent
+    float sTE[3];    // segment x..x+N-1: earliest start
+    float sTL[3];    //                   latest start, -BIG if the segment warps or is invalid
+    float sTD[3];    //                   duration
+    float pad[2];
+};
+static_assert(sizeof(SlotTW) == 64, "SlotTW layout");
+
 // ------------------------------------------------------------------ launch-side views
 // Device view of one solution (all arrays indexed by physical slot unless noted).
 template <class DT>

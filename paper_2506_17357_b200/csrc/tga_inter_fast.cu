@@ -75,14 +75,15 @@ __device__ __forceinline__ void fold(uint64_t &acc, const Run &b, bool direct, u
 
 // stream slots: 0 2opt* | 1,2 reloc1 d/r | 3,4 oropt2 | 5,6 oropt3 | 7 swap11 |
 // 8,9 cross12 | 10,11 cross13 | 12 cross22 | 13,14 cross23 | 15 cross33
-template <int U, uint32_t MASK>
+template <int U, bool TW, uint32_t MASK>
 __global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__restrict__ rec,
+                                                             const SlotTW *__restrict__ rectw,
                                                              const __grid_constant__ CUtensorMap tmap,
                                                              const uint32_t *__restrict__ tiles, int t_lo, int t_hi,
                                                              uint32_t Qc, int32_t cap, uint64_t *__restrict__ keys,
                                                              const __grid_constant__ SolView<int32_t> SV,
                                                              ScoreParams sp, uint32_t imask, int x_lo, int x_hi) {
-    using G = FastGeom<U>;
+    using G = FastGeom<U, TW>;
     constexpr int BW = G::BoxW;
     constexpr int NV = 11;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -93,6 +94,11 @@ __global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__re
     SlotRec *const rows1 = reinterpret_cast<SlotRec *>(sm + 2 * G::BoxPad + G::RowBytes);
     SlotRec *const cols0 = reinterpret_cast<SlotRec *>(sm + 2 * G::BoxPad + 2 * G::RowBytes);
     SlotRec *const cols1 = reinterpret_cast<SlotRec *>(sm + 2 * G::BoxPad + 2 * G::RowBytes + G::ColBytes);
+    unsigned char *const twb = sm + 2 * G::BoxPad + 2 * G::RowBytes + 2 * G::ColBytes;
+    SlotTW *const trows0 = reinterpret_cast<SlotTW *>(twb);
+    SlotTW *const trows1 = reinterpret_cast<SlotTW *>(twb + G::RowTW);
+    SlotTW *const tcols0 = reinterpret_cast<SlotTW *>(twb + 2 * G::RowTW);
+    SlotTW *const tcols1 = reinterpret_cast<SlotTW *>(twb + 2 * G::RowTW + G::ColTW);
     __shared__ uint64_t bar[2];
     __shared__ unsigned long long red[23];
 
@@ -113,10 +119,14 @@ __global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__re
         const uint32_t ij = tiles[t];
         const int I = ij >> 16, J = ij & 0xFFFF;
         uint64_t *br = b ? &bar[1] : &bar[0];
-        f_expect(br, G::BoxBytes + G::RowBytes + G::ColBytes);
+        f_expect(br, G::BoxBytes + G::RowBytes + G::ColBytes + G::RowTW + G::ColTW);
         f_tma2d(b ? dp1 : dp0, &tmap, J * kFastTV - 4, I * U - 1, br);
         f_bulk(b ? rows1 : rows0, rec + I * U, G::RowBytes, br);
         f_bulk(b ? cols1 : cols0, rec + J * kFastTV, G::ColBytes, br);
+        if (TW) {
+            f_bulk(b ? trows1 : trows0, rectw + I * U, G::RowTW, br);
+            f_bulk(b ? tcols1 : tcols0, rectw + J * kFastTV, G::ColTW, br);
+        }
     };
 
     int t = t_lo + blockIdx.x;
@@ -141,7 +151,11 @@ __global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__re
         if (b) { f_wait(&bar[1], ph1); ph1 ^= 1u; } else { f_wait(&bar[0], ph0); ph0 ^= 1u; }
         // ---- this lane's column record, bulk-copied with the tile (six 16-byte LDS)
         const SlotRec V = (b ? cols1 : cols0)[col];
+        SlotTW VT{};
+        if (TW) VT = (b ? tcols1 : tcols0)[col];
+        const SlotTW *TR = b ? trows1 : trows0;
         (void)v;
+        (void)TR;
         const int32_t *T = b ? dp1 : dp0;
         const SlotRec *RW = b ? rows1 : rows0;
         // Dp(u0 + i + di, v + dj), i = row index in the tile
@@ -157,20 +171,36 @@ __global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__re
             const int32_t cu = A.c, ru = A.r;
             if (cu < 0) continue;            // warp-uniform: end depot / padding row
             if (!(ru < V.r)) continue;       // pair must span two routes, route(u) < route(v)
+            const SlotTW &AT = TR[TW ? i : 0];
+            // time-window check of  F + seg + B  (Eq. 4 in the T_V = 0 form of SlotTW):
+            // start after ef + t1 <= seg latest start, completion + t2 <= suffix latest start
+            auto tw3 = [&](float ef, int32_t t1, float sTE, float sTL, float sTD, int32_t t2, float lb) -> bool {
+                const float x = ef + static_cast<float>(t1);
+                return (x <= sTL) & (fmaxf(x, sTE) + sTD + static_cast<float>(t2) <= lb);
+            };
             // ---- 2-opt*: A' = F(u) + B(v+1), B' = F(v) + B(u+1)    (Eq. 14)
             if (MASK & (1u << 1)) {
-                const int32_t dD = D(i, 0, 1) + D(i, 1, 0) + A.ne + V.ne;
+                const int32_t d01 = D(i, 0, 1), d10 = D(i, 1, 0);
+                const int32_t dD = d01 + d10 + A.ne + V.ne;
                 const int32_t la = A.fL + V.bL1, lb = V.fL + A.bL1;
-                keep(run[0], max(la, lb) <= cap, dD, cu);
+                bool ok = max(la, lb) <= cap;
+                if (TW) ok = ok & (AT.EF + static_cast<float>(d01) <= VT.LBN[0]) &
+                             (VT.EF + static_cast<float>(d10) <= AT.LBN[0]);
+                keep(run[0], ok, dD, cu);
             }
             // ---- relocate / or-opt, both directions                   (Eq. 13)
 #pragma unroll
             for (int N = 1; N <= 3; ++N) {
                 if (!(MASK & (1u << (1 + N)))) continue;
-                const int32_t d1 = A.rem[N - 1] + D(i, 0, 0) + D(i, N - 1, 1) + V.ne;  // seg(u) after v
-                keep(run[2 * N - 1], V.W + A.so[N - 1] <= cap, d1, cu);
-                const int32_t d2 = V.rem[N - 1] + D(i, 0, 0) + D(i, 1, N - 1) + A.ne;  // seg(v) after u
-                keep(run[2 * N], A.W + V.so[N - 1] <= cap, d2, cu);
+                const int32_t d00 = D(i, 0, 0), dN1 = D(i, N - 1, 1), d1N = D(i, 1, N - 1);
+                const int32_t d1 = A.rem[N - 1] + d00 + dN1 + V.ne;  // seg(u) after v
+                bool ok1 = V.W + A.so[N - 1] <= cap;
+                if (TW) ok1 = ok1 & tw3(VT.EF, d00, AT.sTE[N - 1], AT.sTL[N - 1], AT.sTD[N - 1], dN1, VT.LBN[0]);
+                keep(run[2 * N - 1], ok1, d1, cu);
+                const int32_t d2 = V.rem[N - 1] + d00 + d1N + A.ne;  // seg(v) after u
+                bool ok2 = A.W + V.so[N - 1] <= cap;
+                if (TW) ok2 = ok2 & tw3(AT.EF, d00, VT.sTE[N - 1], VT.sTL[N - 1], VT.sTD[N - 1], d1N, AT.LBN[0]);
+                keep(run[2 * N], ok2, d2, cu);
             }
             // ---- swap (1,1) / cross-exchange (N1,N2), N1 <= N2
 #pragma unroll
@@ -180,16 +210,24 @@ __global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__re
                 const int N1 = n1s[sv], N2 = n2s[sv];
                 if (!(MASK & (1u << (5 + sv)))) continue;
                 {   // N1-segment at u, N2-segment at v
-                    const int32_t dD = D(i, -1, 0) + D(i, N1, N2 - 1) + D(i, 0, -1) + D(i, N1 - 1, N2) +
-                                       A.sE[N1 - 1] + V.sE[N2 - 1];
+                    const int32_t a = D(i, -1, 0), bq = D(i, N1, N2 - 1), c = D(i, 0, -1), dq = D(i, N1 - 1, N2);
+                    const int32_t dD = a + bq + c + dq + A.sE[N1 - 1] + V.sE[N2 - 1];
                     const int32_t la = A.sA[N1 - 1] + V.sS[N2 - 1], lb = V.sA[N2 - 1] + A.sS[N1 - 1];
-                    keep(run[slot[sv]], max(la, lb) <= cap, dD, cu);
+                    bool ok = max(la, lb) <= cap;
+                    if (TW)  // A' = F(u-1) + S(v,N2) + B(u+N1),  B' = F(v-1) + S(u,N1) + B(v+N2)
+                        ok = ok & tw3(AT.EFm, a, VT.sTE[N2 - 1], VT.sTL[N2 - 1], VT.sTD[N2 - 1], bq, AT.LBN[N1 - 1]) &
+                             tw3(VT.EFm, c, AT.sTE[N1 - 1], AT.sTL[N1 - 1], AT.sTD[N1 - 1], dq, VT.LBN[N2 - 1]);
+                    keep(run[slot[sv]], ok, dD, cu);
                 }
                 if (N1 != N2) {   // N1-segment at v, N2-segment at u
-                    const int32_t dD = D(i, 0, -1) + D(i, N2 - 1, N1) + D(i, -1, 0) + D(i, N2, N1 - 1) +
-                                       V.sE[N1 - 1] + A.sE[N2 - 1];
+                    const int32_t c = D(i, 0, -1), bq = D(i, N2 - 1, N1), a = D(i, -1, 0), dq = D(i, N2, N1 - 1);
+                    const int32_t dD = c + bq + a + dq + V.sE[N1 - 1] + A.sE[N2 - 1];
                     const int32_t lb = V.sA[N1 - 1] + A.sS[N2 - 1], la = A.sA[N2 - 1] + V.sS[N1 - 1];
-                    keep(run[slot[sv] + 1], max(la, lb) <= cap, dD, cu);
+                    bool ok = max(la, lb) <= cap;
+                    if (TW)  // B' = F(v-1) + S(u,N2) + B(v+N1),  A' = F(u-1) + S(v,N1) + B(u+N2)
+                        ok = ok & tw3(VT.EFm, c, AT.sTE[N2 - 1], AT.sTL[N2 - 1], AT.sTD[N2 - 1], bq, VT.LBN[N1 - 1]) &
+                             tw3(AT.EFm, a, VT.sTE[N1 - 1], VT.sTL[N1 - 1], VT.sTD[N1 - 1], dq, AT.LBN[N2 - 1]);
+                    keep(run[slot[sv] + 1], ok, dD, cu);
                 }
             }
         }
@@ -224,25 +262,27 @@ __global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__re
     if (tid < 23 && red[tid] != kNoKey) atomicMin(reinterpret_cast<unsigned long long *>(keys) + tid, red[tid]);
 }
 
-template <int U, uint32_t MASK>
-static cudaError_t launch_fast_t(const SlotRec *rec, const CUtensorMap &map, const uint32_t *tiles, int t_lo, int t_hi,
+template <int U, bool TW, uint32_t MASK>
+static cudaError_t launch_fast_t(const SlotRec *rec, const SlotTW *rectw, const CUtensorMap &map, const uint32_t *tiles, int t_lo, int t_hi,
                                  uint32_t Qc, int32_t cap, uint64_t *keys, int grid, cudaStream_t st,
                                  const SolView<int32_t> &SV, const ScoreParams &sp, uint32_t imask, int x_lo,
                                  int x_hi) {
-    auto kern = k_inter_fast<U, MASK>;
+    auto kern = k_inter_fast<U, TW, MASK>;
+    constexpr int smem = FastGeom<U, TW>::Smem;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, FastGeom<U>::Smem);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr = true;
     }
-    kern<<<grid, kFastThreads, FastGeom<U>::Smem, st>>>(rec, map, tiles, t_lo, t_hi, Qc, cap, keys, SV, sp, imask,
-                                                         x_lo, x_hi);
+    kern<<<grid, kFastThreads, smem, st>>>(rec, rectw, map, tiles, t_lo, t_hi, Qc, cap, keys, SV, sp, imask, x_lo,
+                                           x_hi);
     note_launch();
     return cudaGetLastError();
 }
 
-template <int U>
-static cudaError_t launch_fast_u(uint32_t mask, const SlotRec *rec, const CUtensorMap &map, const uint32_t *tiles,
+template <int U, bool TW>
+static cudaError_t launch_fast_u(uint32_t mask, const SlotRec *rec, const SlotTW *rectw, const CUtensorMap &map,
+                                 const uint32_t *tiles,
                                  int t_lo, int t_hi, uint32_t Qc, int32_t cap, uint64_t *keys, int max_grid,
                                  cudaStream_t st, const SolView<int32_t> &SV, const ScoreParams &sp, uint32_t imask,
                                  int x_lo, int x_hi) {
@@ -253,8 +293,8 @@ static cudaError_t launch_fast_u(uint32_t mask, const SlotRec *rec, const CUtens
     auto run = [&](auto kmask) {
         if (err != cudaSuccess) return;
         const int grid = std::max(1, std::min(std::max(t_hi - t_lo, units), max_grid));
-        err = launch_fast_t<U, decltype(kmask)::value>(rec, map, tiles, t_lo, t_hi, Qc, cap, keys, grid, st, SV, sp,
-                                                       imask, x_lo, x_hi);
+        err = launch_fast_t<U, TW, decltype(kmask)::value>(rec, rectw, map, tiles, t_lo, t_hi, Qc, cap, keys, grid, st,
+                                                           SV, sp, imask, x_lo, x_hi);
         imask = 0;
     };
     constexpr uint32_t ALL = 0x7FEu, NS = (1u << 1) | (1u << 2) | (1u << 5);
@@ -268,14 +308,19 @@ static cudaError_t launch_fast_u(uint32_t mask, const SlotRec *rec, const CUtens
     return err;
 }
 
-cudaError_t launch_inter_fast(int U, uint32_t mask, const SlotRec *rec, const CUtensorMap &map, const uint32_t *tiles,
-                              int t_lo, int t_hi, uint32_t Qc, int32_t cap, uint64_t *keys, int max_grid,
-                              cudaStream_t st, const SolView<int32_t> &SV, const ScoreParams &sp, uint32_t imask,
-                              int x_lo, int x_hi) {
-    return U == 8 ? launch_fast_u<8>(mask, rec, map, tiles, t_lo, t_hi, Qc, cap, keys, max_grid, st, SV, sp, imask,
-                                     x_lo, x_hi)
-                  : launch_fast_u<16>(mask, rec, map, tiles, t_lo, t_hi, Qc, cap, keys, max_grid, st, SV, sp, imask,
-                                      x_lo, x_hi);
+cudaError_t launch_inter_fast(int U, uint32_t mask, const SlotRec *rec, const SlotTW *rectw, const CUtensorMap &map,
+                              const uint32_t *tiles, int t_lo, int t_hi, uint32_t Qc, int32_t cap, uint64_t *keys,
+                              int max_grid, cudaStream_t st, const SolView<int32_t> &SV, const ScoreParams &sp,
+                              uint32_t imask, int x_lo, int x_hi) {
+    if (rectw)
+        return U == 8 ? launch_fast_u<8, true>(mask, rec, rectw, map, tiles, t_lo, t_hi, Qc, cap, keys, max_grid, st, SV,
+                                               sp, imask, x_lo, x_hi)
+                      : launch_fast_u<16, true>(mask, rec, rectw, map, tiles, t_lo, t_hi, Qc, cap, keys, max_grid, st,
+                                                SV, sp, imask, x_lo, x_hi);
+    return U == 8 ? launch_fast_u<8, false>(mask, rec, rectw, map, tiles, t_lo, t_hi, Qc, cap, keys, max_grid, st, SV,
+                                            sp, imask, x_lo, x_hi)
+                  : launch_fast_u<16, false>(mask, rec, rectw, map, tiles, t_lo, t_hi, Qc, cap, keys, max_grid, st, SV,
+                                             sp, imask, x_lo, x_hi);
 }
 
 }  // namespace tga

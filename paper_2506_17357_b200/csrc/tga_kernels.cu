@@ -218,12 +218,36 @@ __device__ __forceinline__ void scan_route(const ScanArgs<DT> &A, const int r, c
                 q.ne = -e_x;
                 q.W = slot ? Wr : kPoison;
                 const DT br[3] = {b1, b2, b3};
+                // time-window part (TW-I): earliest completions / latest starts
+                SlotTW w{};
+                auto EFof = [&](int y) { const TwRec f = A.fwdT[y]; return f.w == 0.f ? f.y + f.x : kTwBig; };
+                auto LBof = [&](int y) { const TwRec b = A.bwdT[y]; return b.w == 0.f ? b.z : -kTwBig; };
+                if (TW && A.rectw) {
+                    w.EF = EFof(x);
+                    w.EFm = (k >= 1) ? EFof(x - 1) : kTwBig;
+                    const TwRec s1 = A.node_tw[A.node[x]];
+                    const TwRec sg[3] = {s1, A.seg2T[x], A.seg3T[x]};
+#pragma unroll
+                    for (int N = 1; N <= 3; ++N) {
+                        const bool segok = (k >= 1) && (k + N - 1 <= L);
+                        w.LBN[N - 1] = (k + N < len) ? LBof(x + N) : -kTwBig;
+                        w.sTE[N - 1] = sg[N - 1].y;
+                        w.sTL[N - 1] = (segok && sg[N - 1].w == 0.f) ? sg[N - 1].z : -kTwBig;
+                        w.sTD[N - 1] = sg[N - 1].x;
+                    }
+                    w.pad[0] = w.pad[1] = 0.f;
+                    A.rectw[x] = w;
+                }
 #pragma unroll
                 for (int N = 1; N <= 3; ++N) {
                     const bool segok = (k >= 1) && (k + N - 1 <= L);
                     const int32_t sN = segok ? A.fwdL[x + N - 1] - fl_prev : 0;
                     const int32_t eout = segok ? A.enext[x + N - 1] : 0;
-                    q.so[N - 1] = (segok && Wr - sN <= A.capacity) ? sN : kPoison;
+                    // route a after removing the segment: F(x-1) + B(x+N) must stay feasible
+                    bool rem_ok = segok && Wr - sN <= A.capacity;
+                    if (TW && A.rectw && segok)
+                        rem_ok = rem_ok && (w.EFm + static_cast<float>(br[N - 1]) <= LBof(x + N));
+                    q.so[N - 1] = rem_ok ? sN : kPoison;
                     q.rem[N - 1] = segok ? br[N - 1] - e_prev - eout : 0;
                     q.sA[N - 1] = segok ? Wr - sN : kPoison;
                     q.sS[N - 1] = sN;

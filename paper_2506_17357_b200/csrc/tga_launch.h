@@ -28,7 +28,7 @@ constexpr int kPitchAlign = 128;                // Dp pitch: multiple of every t
 // U = 8 for small neighbourhoods (more tiles than resident CTAs), 16 otherwise
 constexpr int kFastThreads = 128;
 constexpr int kFastTV = 128;
-template <int U>
+template <int U, bool TW = false>
 struct FastGeom {
     static constexpr int BoxW = kFastTV + 8;                    // cols v0-4 .. v0+131 (16-byte aligned TMA x)
     static constexpr int BoxH = U + 4;                          // rows u0-1 .. u0+U+2
@@ -36,7 +36,9 @@ struct FastGeom {
     static constexpr int BoxPad = (BoxBytes + 127) / 128 * 128;
     static constexpr int RowBytes = U * 96;                     // row records (bulk copy)
     static constexpr int ColBytes = kFastTV * 96;               // column records (bulk copy)
-    static constexpr int Smem = 2 * BoxPad + 2 * RowBytes + 2 * ColBytes + 128;
+    static constexpr int RowTW = TW ? U * 64 : 0;               // time-window parts
+    static constexpr int ColTW = TW ? kFastTV * 64 : 0;
+    static constexpr int Smem = 2 * BoxPad + 2 * RowBytes + 2 * ColBytes + 2 * RowTW + 2 * ColTW + 128;
     static_assert(RowBytes % 128 == 0 && ColBytes % 128 == 0, "bulk copy alignment");
 };
 constexpr int kGuard = 8;                       // guard slots before/after every slot array
@@ -59,6 +61,7 @@ struct ScanArgs {
     const int32_t *canon;
     int32_t capacity;
     SlotRec *rec;      // CVRP fast-path records (int DT only); may be null
+    SlotTW *rectw;     // VRPTW (TW-I) fast-path records; may be null
 };
 
 // per-solution device state of the device-resident step (k_pick_apply / k_update_dev)
@@ -95,9 +98,9 @@ cudaError_t launch_batch(uint32_t mask, bool tw, const SolView<DT> *views, const
                          uint64_t *keys, int grid, cudaStream_t st);
 unsigned long long launch_count();
 void note_launch();
-cudaError_t launch_inter_fast(int U, uint32_t mask, const SlotRec *rec, const CUtensorMap &map, const uint32_t *tiles,
-                              int t_lo, int t_hi, uint32_t Qc, int32_t cap, uint64_t *keys, int max_grid,
-                              cudaStream_t st, const SolView<int32_t> &SV, const ScoreParams &sp, uint32_t imask,
-                              int x_lo, int x_hi);
+cudaError_t launch_inter_fast(int U, uint32_t mask, const SlotRec *rec, const SlotTW *rectw, const CUtensorMap &map,
+                              const uint32_t *tiles, int t_lo, int t_hi, uint32_t Qc, int32_t cap, uint64_t *keys,
+                              int max_grid, cudaStream_t st, const SolView<int32_t> &SV, const ScoreParams &sp,
+                              uint32_t imask, int x_lo, int x_hi);
 
 }  // namespace tga

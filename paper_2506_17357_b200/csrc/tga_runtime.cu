@@ -136,6 +136,7 @@ struct tga_solution {
     bool tmap_ok = false;
     // CVRP fast path: per-slot records, its own tile plan and TMA box
     SlotRec *rec = nullptr;
+    SlotTW *rectw = nullptr;       // VRPTW (TW-I) fast path
     uint32_t *d_ftiles = nullptr;
     int n_ftiles = 0;
     CUtensorMap fmap{};
@@ -268,6 +269,7 @@ static ScanArgs<DT> scan_args(tga_solution *s) {
     a.canon = s->canon;
     a.capacity = s->inst->Q;
     a.rec = s->rec;
+    a.rectw = s->rectw;
     return a;
 }
 
@@ -541,11 +543,12 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
     void *v_node, *v_route, *v_pos, *v_rlen, *v_canon, *v_fwdL, *v_bwdL, *v_en, *v_fD, *v_bD, *v_b1, *v_b2, *v_b3;
     void *v_fT, *v_bT, *v_s2, *v_s3, *v_rbase, *v_rlenR, *v_cbase, *v_rW, *v_rTV, *v_rD, *v_keys, *v_tiles;
     void *v_ds, *v_sa, *v_desc, *v_scr, *v_acc;
-    void *v_rec = nullptr, *v_ftiles = nullptr;
+    void *v_rec = nullptr, *v_ftiles = nullptr, *v_rectw = nullptr;
     s->fastU = 16;  // U = 8 measured no better at n = 1000 (more tiles, more per-tile overhead)
     if (const char *ev = std::getenv("TGA_FAST_U")) s->fastU = std::atoi(ev) == 8 ? 8 : 16;  // tuning override
     const size_t ftiles_max = static_cast<size_t>(s->pitch / s->fastU) * (s->pitch / kFastTV) + 1;
-    const bool want_fast = I->dtype == TGA_I32 && !I->tw && I->opt.score_mode == TGA_SCORE_FEASIBLE && I->fast_ok;
+    // fast path: integer distances (CVRP, or VRPTW TW-I), feasible-only scoring
+    const bool want_fast = I->dtype == TGA_I32 && I->opt.score_mode == TGA_SCORE_FEASIBLE && I->fast_ok;
     Item items[] = {
         {&v_node, cap * 4}, {&v_route, cap * 4}, {&v_pos, cap * 4}, {&v_rlen, cap * 4}, {&v_canon, cap * 4},
         {&v_fwdL, cap * 4}, {&v_bwdL, cap * 4}, {&v_en, cap * 4}, {&v_fD, cap * 4}, {&v_bD, cap * 4},
@@ -555,7 +558,8 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
         {&v_rD, Rr * 4}, {&v_ds, sizeof(DevState)}, {&v_sa, sizeof(ScanArgs<int32_t>)}, {&v_desc, 8 * 4},
         {&v_scr, cap * 4}, {&v_acc, 48 * 8},
         {&v_keys, TGA_N_VARIANTS * 8}, {&v_tiles, tiles_max * 4},
-        {&v_rec, want_fast ? cap * sizeof(SlotRec) : 0}, {&v_ftiles, want_fast ? ftiles_max * 4 : 0}};
+        {&v_rec, want_fast ? cap * sizeof(SlotRec) : 0}, {&v_ftiles, want_fast ? ftiles_max * 4 : 0},
+        {&v_rectw, want_fast && I->tw ? cap * sizeof(SlotTW) : 0}};
     size_t total = 0;
     for (auto &it : items) total += align_up(it.bytes, 256);
     if (cudaMalloc(&s->arena, total) != cudaSuccess) return bail(fail(TGA_ERR_OOM, "device arena"));
@@ -595,6 +599,17 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
         p.c = -1; p.r = -1; p.fL = p.bL1 = p.W = kPoison;
         for (int k = 0; k < 3; ++k) { p.so[k] = kPoison; p.sA[k] = kPoison; }
         std::vector<SlotRec> init(cap, p);
+        if (I->tw) {
+            s->rectw = static_cast<SlotTW *>(v_rectw) + kGuard;
+            SlotTW pt{};
+            pt.EF = pt.EFm = kTwBig;
+            for (int k = 0; k < 3; ++k) { pt.LBN[k] = -kTwBig; pt.sTL[k] = -kTwBig; }
+            std::vector<SlotTW> tinit(cap, pt);
+            if (cudaMemcpyAsync(v_rectw, tinit.data(), cap * sizeof(SlotTW), cudaMemcpyHostToDevice, s->stream) !=
+                    cudaSuccess ||
+                cudaStreamSynchronize(s->stream) != cudaSuccess)
+                return bail(fail(TGA_ERR_CUDA, "record init"));
+        }
         if (cudaMemcpyAsync(v_rec, init.data(), cap * sizeof(SlotRec), cudaMemcpyHostToDevice, s->stream) !=
                 cudaSuccess ||
             cudaStreamSynchronize(s->stream) != cudaSuccess)  // `init` is pageable and local
@@ -732,8 +747,9 @@ extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
         // fused: inter tiles + the intra-route CVRP work in one launch (when there is inter work)
         fused_intra = (mask & TGA_OP_INTER) && !I->tw && I->max_c_abs < (1 << 21);
         const uint32_t imask = fused_intra ? (mask & TGA_OP_INTRA) : 0u;
-        e = launch_inter_fast(s->fastU, mask, s->rec, s->fmap, s->d_ftiles, f_lo, f_hi, static_cast<uint32_t>(s->Qc),
-                              I->Q, s->keys, s->sm_count * 4, st, sol_view<int32_t>(s), sp, imask, x_lo, x_hi);
+        e = launch_inter_fast(s->fastU, mask, s->rec, s->rectw, s->fmap, s->d_ftiles, f_lo, f_hi,
+                              static_cast<uint32_t>(s->Qc), I->Q, s->keys, s->sm_count * 4, st, sol_view<int32_t>(s),
+                              sp, imask, x_lo, x_hi);
     } else if (I->dtype == TGA_I32) {
         e = launch_inter<int32_t>(mask, I->tw, sol_view<int32_t>(s), s->tmap, s->d_tiles, t_lo, t_hi, sp, s->keys,
                                   grid, st);

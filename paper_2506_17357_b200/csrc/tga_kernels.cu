@@ -799,6 +799,228 @@ __global__ void __launch_bounds__(256) k_intra_batch(const SolView<DT> *__restri
     intra_body<DT, TW>(S, sp, vmask, 0, S.Qp, keys + static_cast<size_t>(blockIdx.y) * 23);
 }
 
+// ============================================================== intra-route evaluation, VRPTW (warp-parallel)
+// One warp per u slot x, lane <-> insertion / second-segment position q (chunks of
+// 32 with carries).  The middle segments of Intra-Relocate / Intra-Swap are
+// warp-wide scans of Eq. 4 records (Hillis-Steele with the in-/out-link of each
+// element), so every candidate of a route is evaluated in parallel:
+//   relocate fwd  (q >= p+N):  [F(x-1) + x+N .. q] + S(x,N) + B(q+1)
+//   relocate bwd  (q <= p-2):  F(q) + S(x,N) + [q+1 .. x-1] + B(x+N)
+//   swap (N1,N2)  (q >= p+N1): F(x-1) + S(q,N2) + [x+N1 .. q-1] + S(x,N1) + B(q+N2)
+__device__ __forceinline__ TwRec shfl_up_rec(TwRec r, int d) {
+    return make_float4(__shfl_up_sync(0xffffffffu, r.x, d), __shfl_up_sync(0xffffffffu, r.y, d),
+                       __shfl_up_sync(0xffffffffu, r.z, d), __shfl_up_sync(0xffffffffu, r.w, d));
+}
+__device__ __forceinline__ TwRec shfl_down_rec(TwRec r, int d) {
+    return make_float4(__shfl_down_sync(0xffffffffu, r.x, d), __shfl_down_sync(0xffffffffu, r.y, d),
+                       __shfl_down_sync(0xffffffffu, r.z, d), __shfl_down_sync(0xffffffffu, r.w, d));
+}
+__device__ __forceinline__ TwRec shfl_rec(TwRec r, int src) {
+    return make_float4(__shfl_sync(0xffffffffu, r.x, src), __shfl_sync(0xffffffffu, r.y, src),
+                       __shfl_sync(0xffffffffu, r.z, src), __shfl_sync(0xffffffffu, r.w, src));
+}
+// inclusive left-to-right scan of lanes >= s (elements with their in-links);
+// lanes < s keep their own element.  Returns the in-link of each lane's run.
+__device__ __forceinline__ TwRec scan_fwd(TwRec rec, float &inl, int lane, int s) {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const TwRec o = shfl_up_rec(rec, d);
+        const float oin = __shfl_up_sync(0xffffffffu, inl, d);
+        if (lane - d >= s) { rec = tw_cat(o, rec, inl); inl = oin; }
+    }
+    return rec;
+}
+// inclusive right-to-left scan of lanes <= e (elements with their out-links)
+__device__ __forceinline__ TwRec scan_bwd(TwRec rec, float &outl, int lane, int e) {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const TwRec o = shfl_down_rec(rec, d);
+        const float oout = __shfl_down_sync(0xffffffffu, outl, d);
+        if (lane + d <= e) { rec = tw_cat(rec, o, outl); outl = oout; }
+    }
+    return rec;
+}
+
+template <class DT>
+__device__ __forceinline__ void intra_tw_warp(const SolView<DT> &S, const ScoreParams &sp, uint32_t vmask, int x,
+                                              unsigned long long *red) {
+    const int lane = threadIdx.x & 31;
+    if (!(S.canon[x] >= 0 && S.pos[x] >= 1)) return;  // warp-uniform
+    const int p = S.pos[x], L = S.rlen[x], r = S.route[x];
+    const int base = x - p;
+    const int W = S.rW[r];
+    const float TV0 = S.rTV[r];
+    const uint32_t cu = static_cast<uint32_t>(S.canon[x]);
+    const uint32_t cbase = cu - static_cast<uint32_t>(p);
+    auto D = [&](int a, int b) -> DT { return S.Dp[static_cast<size_t>(a) * S.pitch + b]; };
+    auto tf = [&](int a, int b) -> float { return static_cast<float>(D(a, b)); };
+    auto single = [&](int y) -> TwRec { return S.node_tw[S.node[y]]; };
+    auto seg = [&](int y, int N) -> TwRec { return N == 1 ? single(y) : (N == 2 ? S.seg2T[y] : S.seg3T[y]); };
+    auto E = [&](int y) -> DT { return S.enext[y]; };
+    auto bridge = [&](int y, int N) -> DT { return N == 1 ? S.bridge1[y] : (N == 2 ? S.bridge2[y] : S.bridge3[y]); };
+    auto keyof = [&](bool ok, DT dD, float tv, int q) -> uint64_t {
+        return score_key<DT, true>(sp, ok, dD, W, 0, W, 0, tv, 0.f, TV0, 0.f, cu * S.Qc + cbase + q);
+    };
+    uint64_t best[23];
+#pragma unroll
+    for (int i = 0; i < 23; ++i) best[i] = kNoKey;
+
+    // ------------------------------------------------ forward pass (chunks left to right)
+    TwRec cP[3], cG[3];  // carries: relocate-forward prefix, swap middle
+    bool hP[3] = {false, false, false}, hG[3] = {false, false, false};
+    for (int qb = 0; qb <= L; qb += 32) {
+        const int q = qb + lane;
+        const bool in = q <= L;
+        const int v = base + min(q, L);
+        const TwRec sv = single(v);
+        const float inl0 = q >= 1 ? static_cast<float>(E(v - 1)) : 0.f;  // link (q-1 -> q)
+#pragma unroll
+        for (int N = 1; N <= 3; ++N) {
+            const int var = 10 + N;
+            if (!(vmask & (1u << var)) || p + N - 1 > L) continue;
+            // P(q) = F(x-1) + [x+N .. q], element at q = p+N carries F(x-1) (link = bridge_N)
+            const int st = p + N;
+            TwRec el = sv;
+            float inl = inl0;
+            if (q == st) { el = tw_cat(S.fwdT[x - 1], sv, static_cast<float>(bridge(x, N))); inl = 0.f; }
+            const int s_rel = max(st - qb, 0);
+            TwRec P = scan_fwd(el, inl, lane, s_rel);
+            if (hP[N - 1] && lane >= s_rel) P = tw_cat(cP[N - 1], P, inl);
+            if (st <= qb + 31) {   // carry: the run covers the whole chunk from here on
+                cP[N - 1] = shfl_rec(P, 31);
+                hP[N - 1] = true;
+            }
+            if (in && q >= st) {
+                const DT rem = bridge(x, N) - E(x - 1) - E(x + N - 1);
+                const DT dD = rem + D(v, x) + D(x + N - 1, v + 1) - E(v);
+                const TwRec A2 = tw_cat(P, seg(x, N), tf(v, x));
+                const float tv = tw_cat(A2, S.bwdT[v + 1], tf(x + N - 1, v + 1)).w;
+                best[var] = umin64(best[var], keyof(true, dD, tv, q));
+            }
+        }
+#pragma unroll
+        for (int a = 1; a <= 3; ++a) {
+            bool any = false;
+#pragma unroll
+            for (int b = 1; b <= 3; ++b) any |= (vmask >> (14 + 3 * (a - 1) + (b - 1))) & 1u;
+            if (!any || p + a - 1 > L) continue;
+            // G(k) = [x+a .. k] for k >= p+a; lane q uses G(q-1) (empty at q = p+a)
+            const int st = p + a;
+            TwRec el = sv;
+            float inl = inl0;
+            const int s_rel = max(st - qb, 0);
+            TwRec Gk = scan_fwd(el, inl, lane, s_rel);
+            if (hG[a - 1] && lane >= s_rel) Gk = tw_cat(cG[a - 1], Gk, inl);
+            TwRec Gm = shfl_up_rec(Gk, 1);  // G(q-1)
+            if (lane == 0) Gm = cG[a - 1];
+            if (st <= qb + 31) {
+                cG[a - 1] = shfl_rec(Gk, 31);
+                hG[a - 1] = true;
+            }
+#pragma unroll
+            for (int b = 1; b <= 3; ++b) {
+                const int var = 14 + 3 * (a - 1) + (b - 1);
+                if (!(vmask & (1u << var))) continue;
+                const bool ok = in && q >= p + a && q + b - 1 <= L;
+                if (!__any_sync(0xffffffffu, ok)) continue;
+                const int vv = ok ? v : base + p + a;  // masked lanes read valid slots
+                const TwRec sq = seg(vv, b);
+                DT dD;
+                float tv;
+                const TwRec R1 = tw_cat(S.fwdT[x - 1], sq, tf(x - 1, vv));
+                if (q == p + a) {  // adjacent
+                    dD = D(x - 1, vv) + D(vv + b - 1, x) + D(x + a - 1, vv + b) - E(x - 1) - E(vv - 1) - E(vv + b - 1);
+                    const TwRec R3 = tw_cat(R1, seg(x, a), tf(vv + b - 1, x));
+                    tv = tw_cat(R3, S.bwdT[vv + b], tf(x + a - 1, vv + b)).w;
+                } else {
+                    dD = D(x - 1, vv) + D(vv + b - 1, x + a) + D(vv - 1, x) + D(x + a - 1, vv + b) - E(x - 1) -
+                         E(x + a - 1) - E(vv - 1) - E(vv + b - 1);
+                    const TwRec R2 = tw_cat(R1, Gm, tf(vv + b - 1, x + a));
+                    const TwRec R3 = tw_cat(R2, seg(x, a), tf(vv - 1, x));
+                    tv = tw_cat(R3, S.bwdT[vv + b], tf(x + a - 1, vv + b)).w;
+                }
+                best[var] = umin64(best[var], keyof(ok, dD, tv, q));
+            }
+        }
+    }
+    // ------------------------------------------------ backward pass: relocate before the segment
+    if (p >= 2) {
+        const int nch = (p - 1) / 32 + 1;  // element positions up to p-1 (lane q reads Suf(q+1))
+        TwRec cS[3];
+        bool hS[3] = {false, false, false};
+        for (int ci = nch - 1; ci >= 0; --ci) {
+            const int qb = ci * 32;
+            const int k = qb + lane;                 // element position k in [1, p-1]; lane q uses Suf(q+1)
+            const int vk = base + min(max(k, 1), p - 1);
+            const TwRec sk = single(vk);
+            float outl = static_cast<float>(E(vk));  // link (k -> k+1)
+#pragma unroll
+            for (int N = 1; N <= 3; ++N) {
+                const int var = 10 + N;
+                if (!(vmask & (1u << var)) || p + N - 1 > L) continue;
+                // Suf(k) = [k .. x-1] + B(x+N); the element at k = p-1 carries B(x+N) (link = bridge_N)
+                TwRec el = sk;
+                float ol = outl;
+                if (k == p - 1) { el = tw_cat(sk, S.bwdT[x + N], static_cast<float>(bridge(x, N))); ol = 0.f; }
+                const int e_rel = min(p - 1 - qb, 31);
+                TwRec Sf = scan_bwd(el, ol, lane, e_rel);
+                if (hS[N - 1] && lane <= e_rel) Sf = tw_cat(Sf, cS[N - 1], ol);
+                const TwRec carry_in = cS[N - 1];
+                const bool had = hS[N - 1];
+                cS[N - 1] = shfl_rec(Sf, 0);
+                hS[N - 1] = true;
+                // lane q = qb + lane inserts after position q: needs Suf(q+1)
+                TwRec Sn = shfl_down_rec(Sf, 1);
+                if (lane == 31) Sn = had ? carry_in : Sf;
+                const int q = qb + lane;
+                const bool ok = q <= p - 2;
+                if (!__any_sync(0xffffffffu, ok)) continue;
+                const int vq = base + min(q, p - 2);
+                const DT rem = bridge(x, N) - E(x - 1) - E(x + N - 1);
+                const DT dD = rem + D(vq, x) + D(x + N - 1, vq + 1) - E(vq);
+                const TwRec A2 = tw_cat(S.fwdT[vq], seg(x, N), tf(vq, x));
+                const float tv = tw_cat(A2, Sn, tf(x + N - 1, vq + 1)).w;
+                best[var] = umin64(best[var], keyof(ok, dD, tv, q));
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 11; i < 23; ++i) {
+        if (!(vmask & (1u << i))) continue;
+        const uint64_t m = warp_min64(best[i]);
+        if (lane == 0 && m != kNoKey) atomicMin(&red[i], static_cast<unsigned long long>(m));
+    }
+}
+
+template <class DT>
+__global__ void __launch_bounds__(256) k_intra_tw(const __grid_constant__ SolView<DT> S, ScoreParams sp,
+                                                  uint32_t vmask, int x_lo, int x_hi, uint64_t *__restrict__ keys) {
+    __shared__ unsigned long long red[23];
+    if (threadIdx.x < 23) red[threadIdx.x] = kNoKey;
+    __syncthreads();
+    const int x = x_lo + static_cast<int>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    if (x < x_hi) intra_tw_warp<DT>(S, sp, vmask, x, red);
+    __syncthreads();
+    if (threadIdx.x < 23 && red[threadIdx.x] != kNoKey)
+        atomicMin(reinterpret_cast<unsigned long long *>(keys) + threadIdx.x, red[threadIdx.x]);
+}
+
+// population mode: blockIdx.y = solution
+template <class DT>
+__global__ void __launch_bounds__(256) k_intra_tw_batch(const SolView<DT> *__restrict__ views, ScoreParams sp,
+                                                        uint32_t vmask, uint64_t *__restrict__ keys) {
+    __shared__ unsigned long long red[23];
+    if (threadIdx.x < 23) red[threadIdx.x] = kNoKey;
+    __syncthreads();
+    const SolView<DT> &S = views[blockIdx.y];
+    const int x = static_cast<int>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    if (x < S.Qp) intra_tw_warp<DT>(S, sp, vmask, x, red);
+    __syncthreads();
+    if (threadIdx.x < 23 && red[threadIdx.x] != kNoKey)
+        atomicMin(reinterpret_cast<unsigned long long *>(keys) + static_cast<size_t>(blockIdx.y) * 23 + threadIdx.x,
+                  red[threadIdx.x]);
+}
+
 // ============================================================== intra-route evaluation, CVRP
 // No time windows => no sequential middle segment: every (u, v) pair of a route
 // is independent.  A warp owns one u slot, lane <-> v position (strided by 32);
@@ -912,7 +1134,7 @@ cudaError_t launch_inter(uint32_t mask, bool tw, const SolView<DT> &S, const CUt
 
 template <class DT>
 cudaError_t launch_intra(uint32_t mask, bool tw, const SolView<DT> &S, const ScoreParams &sp, int x_lo, int x_hi,
-                         uint64_t *keys, cudaStream_t st, bool small_dist) {
+                         uint64_t *keys, cudaStream_t st, bool small_dist, bool warp_tw) {
     const uint32_t intra = mask & ((1u << 0) | (0x7u << 11) | (0x1FFu << 14));
     if (x_hi <= x_lo || !intra) return cudaSuccess;
     if constexpr (std::is_same<DT, int32_t>::value) {
@@ -922,6 +1144,12 @@ cudaError_t launch_intra(uint32_t mask, bool tw, const SolView<DT> &S, const Sco
             ++g_launches;
             return cudaGetLastError();
         }
+    }
+    if (tw && !(intra & 1u) && warp_tw) {  // warp-parallel VRPTW kernel (long routes)
+        const int blocks = (x_hi - x_lo + 7) / 8;
+        k_intra_tw<DT><<<blocks, 256, 0, st>>>(S, sp, intra, x_lo, x_hi, keys);
+        ++g_launches;
+        return cudaGetLastError();
     }
     const int threads = (x_hi - x_lo) * 13;
     const int blocks = (threads + 255) / 256;
@@ -963,7 +1191,7 @@ static cudaError_t launch_inter_batch_tw(uint32_t mask, const SolView<DT> *views
 template <class DT>
 cudaError_t launch_batch(uint32_t mask, bool tw, const SolView<DT> *views, const CUtensorMap *maps,
                          const uint32_t *work, int n_work, int n_sol, int max_qp, const ScoreParams &sp,
-                         uint64_t *keys, int grid, cudaStream_t st) {
+                         uint64_t *keys, int grid, cudaStream_t st, bool warp_tw) {
     cudaError_t e = cudaSuccess;
     if (n_work > 0 && (mask & 0x7FEu))
         e = tw ? launch_inter_batch_tw<DT, true>(mask, views, maps, work, n_work, sp, keys, grid, st)
@@ -971,7 +1199,9 @@ cudaError_t launch_batch(uint32_t mask, bool tw, const SolView<DT> *views, const
     const uint32_t intra = mask & ((1u << 0) | (0x7u << 11) | (0x1FFu << 14));
     if (e == cudaSuccess && intra && n_sol > 0) {
         dim3 g((max_qp * 13 + 255) / 256, n_sol);
-        if (tw) k_intra_batch<DT, true><<<g, 256, 0, st>>>(views, sp, intra, keys);
+        if (tw && !(intra & 1u) && warp_tw)
+            k_intra_tw_batch<DT><<<dim3((max_qp + 7) / 8, n_sol), 256, 0, st>>>(views, sp, intra, keys);
+        else if (tw) k_intra_batch<DT, true><<<g, 256, 0, st>>>(views, sp, intra, keys);
         else    k_intra_batch<DT, false><<<g, 256, 0, st>>>(views, sp, intra, keys);
         ++g_launches;
         e = cudaGetLastError();
@@ -980,10 +1210,10 @@ cudaError_t launch_batch(uint32_t mask, bool tw, const SolView<DT> *views, const
 }
 template cudaError_t launch_batch<int32_t>(uint32_t, bool, const SolView<int32_t> *, const CUtensorMap *,
                                            const uint32_t *, int, int, int, const ScoreParams &, uint64_t *, int,
-                                           cudaStream_t);
+                                           cudaStream_t, bool);
 template cudaError_t launch_batch<float>(uint32_t, bool, const SolView<float> *, const CUtensorMap *,
                                          const uint32_t *, int, int, int, const ScoreParams &, uint64_t *, int,
-                                         cudaStream_t);
+                                         cudaStream_t, bool);
 
 // explicit instantiations
 template cudaError_t launch_dp<int32_t>(int32_t *, int, const int32_t *, const int32_t *, int, int, int, int, bool,
@@ -998,8 +1228,8 @@ template cudaError_t launch_inter<int32_t>(uint32_t, bool, const SolView<int32_t
 template cudaError_t launch_inter<float>(uint32_t, bool, const SolView<float> &, const CUtensorMap &, const uint32_t *,
                                          int, int, const ScoreParams &, uint64_t *, int, cudaStream_t);
 template cudaError_t launch_intra<int32_t>(uint32_t, bool, const SolView<int32_t> &, const ScoreParams &, int, int,
-                                           uint64_t *, cudaStream_t, bool);
+                                           uint64_t *, cudaStream_t, bool, bool);
 template cudaError_t launch_intra<float>(uint32_t, bool, const SolView<float> &, const ScoreParams &, int, int,
-                                         uint64_t *, cudaStream_t, bool);
+                                         uint64_t *, cudaStream_t, bool, bool);
 
 }  // namespace tga

@@ -91,11 +91,11 @@ cudaError_t launch_inter(uint32_t mask, bool tw, const SolView<DT> &S, const CUt
                          int t_lo, int t_hi, const ScoreParams &sp, uint64_t *keys, int grid, cudaStream_t st);
 template <class DT>
 cudaError_t launch_intra(uint32_t mask, bool tw, const SolView<DT> &S, const ScoreParams &sp, int x_lo, int x_hi,
-                         uint64_t *keys, cudaStream_t st, bool small_dist = false);
+                         uint64_t *keys, cudaStream_t st, bool small_dist = false, bool warp_tw = false);
 template <class DT>
 cudaError_t launch_batch(uint32_t mask, bool tw, const SolView<DT> *views, const CUtensorMap *maps,
                          const uint32_t *work, int n_work, int n_sol, int max_qp, const ScoreParams &sp,
-                         uint64_t *keys, int grid, cudaStream_t st);
+                         uint64_t *keys, int grid, cudaStream_t st, bool warp_tw = false);
 unsigned long long launch_count();
 void note_launch();
 cudaError_t launch_inter_fast(int U, uint32_t mask, const SlotRec *rec, const SlotTW *rectw, const CUtensorMap &map,

@@ -762,11 +762,13 @@ extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
         s->tev_n += 2;
     }
     if (e == cudaSuccess && !fused_intra) {
+        // VRPTW intra: warp-parallel scans pay off once routes fill a warp (measured: L ~ 43 vs ~ 10)
+        const bool warp_tw = s->N >= 16 * s->R;
         if (I->dtype == TGA_I32)
             e = launch_intra<int32_t>(mask, I->tw, sol_view<int32_t>(s), sp, x_lo, x_hi, s->keys, st,
-                                      I->max_c_abs < (1 << 21));
+                                      I->max_c_abs < (1 << 21), warp_tw);
         else
-            e = launch_intra<float>(mask, I->tw, sol_view<float>(s), sp, x_lo, x_hi, s->keys, st);
+            e = launch_intra<float>(mask, I->tw, sol_view<float>(s), sp, x_lo, x_hi, s->keys, st, false, warp_tw);
     }
     if (e != cudaSuccess) return fail(TGA_ERR_CUDA, std::string("eval launch: ") + cudaGetErrorString(e));
     if (s->comm) {
@@ -1357,11 +1359,12 @@ extern "C" int32_t tga_batch_eval(tga_batch *b, uint32_t mask, void *stream) {
     TGA_CUDA(cudaMemsetAsync(b->d_keys, 0xFF, sizeof(uint64_t) * TGA_N_VARIANTS * n, st));
     ScoreParams sp{I->Q, I->opt.score_mode, I->opt.w_load, I->opt.w_tw};
     const int grid = std::max(1, std::min(b->n_work, b->sm_count * 4));
+    const bool warp_tw = b->sols[0]->N >= 16 * b->sols[0]->R;
     cudaError_t e = I->dtype == TGA_I32
         ? launch_batch<int32_t>(mask, I->tw, static_cast<const SolView<int32_t> *>(b->d_views), b->d_maps, b->d_work,
-                                b->n_work, n, b->max_qp, sp, b->d_keys, grid, st)
+                                b->n_work, n, b->max_qp, sp, b->d_keys, grid, st, warp_tw)
         : launch_batch<float>(mask, I->tw, static_cast<const SolView<float> *>(b->d_views), b->d_maps, b->d_work,
-                              b->n_work, n, b->max_qp, sp, b->d_keys, grid, st);
+                              b->n_work, n, b->max_qp, sp, b->d_keys, grid, st, warp_tw);
     if (e != cudaSuccess) return fail(TGA_ERR_CUDA, std::string("batch eval: ") + cudaGetErrorString(e));
     if (st != b->stream) TGA_CUDA(order_after(b->stream, st));
     b->eval_mask = mask;

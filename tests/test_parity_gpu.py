@@ -463,3 +463,17 @@ def test_batch_device_step_matches_host_batch():
         assert db.solution(k).routes() == hb.solution(k).routes(), k
     counts, applied = db.device_stats()
     assert applied > 0
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_vrptw_intra_warp_kernel_long_routes(mode):
+    """Warp-parallel VRPTW intra kernel (mean route length >= 16): chunked
+    scans across 32-lane boundaries (routes of 31..70 customers), both modes,
+    feasible and perturbed (warping) states."""
+    _need_gpu()
+    inst, sol = G.gh_like(7, n=240, kind="R2")
+    routes = [r for r in sol.routes]
+    merged = G.Solution([routes[0] + routes[1], routes[2] + routes[3][:10]] + [routes[3][10:]] + routes[4:])
+    for s in (merged, G.perturb(merged, 20, 3)):
+        assert sum(len(r) for r in s.routes) >= 16 * len(s.routes)
+        check_exact(inst, s, INTRA_TW + INTER, mode, "tw-warp")

@@ -156,7 +156,7 @@ struct SolView {
     const DT *Dp;
     int32_t pitch;            // elements per Dp row
     int32_t Qp;               // physical slots (rows of Dp)
-    uint32_t Qc;              // canonical slot count Q = N + R (flat index = u * Qc + v)
+    uint32_t Qc;              // flat-index multiplier (= pitch): key index = u * Qc + v over PHYSICAL slots
     const uint32_t *tiles;    // generic inter-route tile plan (batch kernels)
 };
 
@@ -198,7 +198,7 @@ __device__ __forceinline__ void intra_cvrp_warp(const SolView<int32_t> &S, const
             const bool in = q <= L;
             const int v = base + min(q, L);
             const int vm1 = max(v - 1, base);          // masked lanes (q = 0) must still read a valid row
-            const uint32_t ib = cu * S.Qc + cbase + static_cast<uint32_t>(qb);
+            const uint32_t ib = static_cast<uint32_t>(x) * S.Qc + static_cast<uint32_t>(base + qb);  // physical
             const int32_t ev = S.enext[v], evm = (q >= 1 && in) ? S.enext[v - 1] : 0;
             // phase 1: every variant's 32-bit key in registers (all loads issued together)
             uint32_t k[23];

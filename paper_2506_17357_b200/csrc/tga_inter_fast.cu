@@ -154,7 +154,6 @@ __global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__re
         SlotTW VT{};
         if (TW) VT = (b ? tcols1 : tcols0)[col];
         const SlotTW *TR = b ? trows1 : trows0;
-        (void)v;
         (void)TR;
         const int32_t *T = b ? dp1 : dp0;
         const SlotRec *RW = b ? rows1 : rows0;
@@ -169,6 +168,7 @@ __global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__re
         for (int i = 0; i < U; ++i) {
             const SlotRec &A = RW[i];       // row u = u0 + i (broadcast reads)
             const int32_t cu = A.c, ru = A.r;
+            const int u = u0 + i;            // physical row slot (key index = u * pitch + v)
             if (cu < 0) continue;            // warp-uniform: end depot / padding row
             if (!(ru < V.r)) continue;       // pair must span two routes, route(u) < route(v)
             const SlotTW &AT = TR[TW ? i : 0];
@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__re
                 bool ok = max(la, lb) <= cap;
                 if (TW) ok = ok & (AT.EF + static_cast<float>(d01) <= VT.LBN[0]) &
                              (VT.EF + static_cast<float>(d10) <= AT.LBN[0]);
-                keep(run[0], ok, dD, cu);
+                keep(run[0], ok, dD, u);
             }
             // ---- relocate / or-opt, both directions                   (Eq. 13)
 #pragma unroll
@@ -196,11 +196,11 @@ __global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__re
                 const int32_t d1 = A.rem[N - 1] + d00 + dN1 + V.ne;  // seg(u) after v
                 bool ok1 = V.W + A.so[N - 1] <= cap;
                 if (TW) ok1 = ok1 & tw3(VT.EF, d00, AT.sTE[N - 1], AT.sTL[N - 1], AT.sTD[N - 1], dN1, VT.LBN[0]);
-                keep(run[2 * N - 1], ok1, d1, cu);
+                keep(run[2 * N - 1], ok1, d1, u);
                 const int32_t d2 = V.rem[N - 1] + d00 + d1N + A.ne;  // seg(v) after u
                 bool ok2 = A.W + V.so[N - 1] <= cap;
                 if (TW) ok2 = ok2 & tw3(AT.EF, d00, VT.sTE[N - 1], VT.sTL[N - 1], VT.sTD[N - 1], d1N, AT.LBN[0]);
-                keep(run[2 * N], ok2, d2, cu);
+                keep(run[2 * N], ok2, d2, u);
             }
             // ---- swap (1,1) / cross-exchange (N1,N2), N1 <= N2
 #pragma unroll
@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__re
                     if (TW)  // A' = F(u-1) + S(v,N2) + B(u+N1),  B' = F(v-1) + S(u,N1) + B(v+N2)
                         ok = ok & tw3(AT.EFm, a, VT.sTE[N2 - 1], VT.sTL[N2 - 1], VT.sTD[N2 - 1], bq, AT.LBN[N1 - 1]) &
                              tw3(VT.EFm, c, AT.sTE[N1 - 1], AT.sTL[N1 - 1], AT.sTD[N1 - 1], dq, VT.LBN[N2 - 1]);
-                    keep(run[slot[sv]], ok, dD, cu);
+                    keep(run[slot[sv]], ok, dD, u);
                 }
                 if (N1 != N2) {   // N1-segment at v, N2-segment at u
                     const int32_t c = D(i, 0, -1), bq = D(i, N2 - 1, N1), a = D(i, -1, 0), dq = D(i, N2, N1 - 1);
@@ -227,13 +227,13 @@ __global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__re
                     if (TW)  // B' = F(v-1) + S(u,N2) + B(v+N1),  A' = F(u-1) + S(v,N1) + B(u+N2)
                         ok = ok & tw3(VT.EFm, c, AT.sTE[N2 - 1], AT.sTL[N2 - 1], AT.sTD[N2 - 1], bq, VT.LBN[N1 - 1]) &
                              tw3(AT.EFm, a, VT.sTE[N1 - 1], VT.sTL[N1 - 1], VT.sTD[N1 - 1], dq, AT.LBN[N2 - 1]);
-                    keep(run[slot[sv] + 1], ok, dD, cu);
+                    keep(run[slot[sv] + 1], ok, dD, u);
                 }
             }
         }
         // ---- fold this tile's streams into the per-variant 64-bit keys
         if (V.c >= 0) {
-            const uint32_t cv = static_cast<uint32_t>(V.c);
+            const uint32_t cv = static_cast<uint32_t>(v);  // physical column slot
             if (MASK & (1u << 1)) fold(acc[1], run[0], true, cv, Qc);
 #pragma unroll
             for (int N = 1; N <= 3; ++N) {

@@ -436,8 +436,10 @@ __device__ __forceinline__ void inter_tile(const SolView<DT> &S, const DT *__res
             const int La = S.rlen[u];
             const int Wa = S.rW[ru];
             const float TVa = TW ? S.rTV[ru] : 0.f;
-            const uint32_t idx_uv = static_cast<uint32_t>(cu) * S.Qc + static_cast<uint32_t>(cv);
-            const uint32_t idx_vu = static_cast<uint32_t>(cv) * S.Qc + static_cast<uint32_t>(cu);
+            // flat index over PHYSICAL slots (u * pitch + v): order-isomorphic to the canonical
+            // index (both orders are (route, position) lexicographic); the host maps it back
+            const uint32_t idx_uv = static_cast<uint32_t>(u) * S.Qc + static_cast<uint32_t>(v);
+            const uint32_t idx_vu = static_cast<uint32_t>(v) * S.Qc + static_cast<uint32_t>(u);
 
             // ---- 2-opt* (3-Seq(0,0) P:346; Eq. 14)
             if (MASK & (1u << 1)) {
@@ -690,7 +692,8 @@ __device__ __forceinline__ void intra_body(const SolView<DT> &S, const ScorePara
             return N == 1 ? S.node_tw[S.node[a]] : (N == 2 ? S.seg2T[a] : S.seg3T[a]);
         };
         auto key = [&](DT dD, float tv, int q) -> uint64_t {
-            return score_key<DT, TW>(sp, true, dD, W, 0, W, 0, tv, 0.f, TV0, 0.f, cu * S.Qc + cbase + q);
+            return score_key<DT, TW>(sp, true, dD, W, 0, W, 0, tv, 0.f, TV0, 0.f,
+                                     static_cast<uint32_t>(x) * S.Qc + static_cast<uint32_t>(base + q));
         };
         if (var == 0) {
             // 2-opt: reverse u..v (Eq. 7); loads unchanged; CVRP only (host-checked)
@@ -859,7 +862,8 @@ __device__ __forceinline__ void intra_tw_warp(const SolView<DT> &S, const ScoreP
     auto E = [&](int y) -> DT { return S.enext[y]; };
     auto bridge = [&](int y, int N) -> DT { return N == 1 ? S.bridge1[y] : (N == 2 ? S.bridge2[y] : S.bridge3[y]); };
     auto keyof = [&](bool ok, DT dD, float tv, int q) -> uint64_t {
-        return score_key<DT, true>(sp, ok, dD, W, 0, W, 0, tv, 0.f, TV0, 0.f, cu * S.Qc + cbase + q);
+        return score_key<DT, true>(sp, ok, dD, W, 0, W, 0, tv, 0.f, TV0, 0.f,
+                                   static_cast<uint32_t>(x) * S.Qc + static_cast<uint32_t>(base + q));
     };
     uint64_t best[23];
 #pragma unroll

@@ -148,10 +148,10 @@ __device__ __forceinline__ void pick_apply_body(const DevState &S, uint32_t mask
         sh_applied = 0;
         if (improving) {
             const uint32_t idx = static_cast<uint32_t>(bk & 0xFFFFFFFFu);
-            const int cu = static_cast<int>(idx / static_cast<uint32_t>(S.Qc));
-            const int cv = static_cast<int>(idx % static_cast<uint32_t>(S.Qc));
-            const int ra = find_route(sc, R, cu), pa = cu - sc[ra];
-            const int rb = find_route(sc, R, cv), pb = cv - sc[rb];
+            const int xu = static_cast<int>(idx / static_cast<uint32_t>(S.Qc));  // physical slots
+            const int xv = static_cast<int>(idx % static_cast<uint32_t>(S.Qc));
+            const int ra = S.route[xu], pa = S.pos[xu];
+            const int rb = S.route[xv], pb = S.pos[xv];
             const int La = sl[ra], Lb = sl[rb];
             const int v = bv;
             NewRoute A{ra, 0, 0, {}}, B{rb, 0, 0, {}};

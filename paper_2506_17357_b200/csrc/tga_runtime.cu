@@ -297,7 +297,7 @@ static SolView<DT> sol_view(const tga_solution *s) {
     v.Dp = static_cast<const DT *>(s->Dp);
     v.pitch = s->pitch;
     v.Qp = s->Qp;
-    v.Qc = static_cast<uint32_t>(s->Qc);
+    v.Qc = static_cast<uint32_t>(s->pitch);  // keys index physical slots
     v.tiles = s->d_tiles;
     return v;
 }
@@ -307,7 +307,7 @@ static DevState make_devstate(const tga_solution *s, const uint64_t *keys) {
     d.node = s->node; d.route = s->route; d.pos = s->pos; d.rlen = s->rlen; d.canon = s->canon;
     d.rbase = s->d_rbase; d.rlenR = s->d_rlenR; d.cbase = s->d_cbase;
     d.scratch = s->d_scratch; d.keys = keys; d.desc = s->d_desc; d.acc = s->d_acc; d.Dp = s->Dp;
-    d.R = s->R; d.Qc = s->Qc; d.Qp = s->Qp; d.pitch = s->pitch;
+    d.R = s->R; d.Qc = s->pitch; d.Qp = s->Qp; d.pitch = s->pitch;
     return d;
 }
 
@@ -748,8 +748,8 @@ extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
         fused_intra = (mask & TGA_OP_INTER) && !I->tw && I->max_c_abs < (1 << 21);
         const uint32_t imask = fused_intra ? (mask & TGA_OP_INTRA) : 0u;
         e = launch_inter_fast(s->fastU, mask, s->rec, s->rectw, s->fmap, s->d_ftiles, f_lo, f_hi,
-                              static_cast<uint32_t>(s->Qc), I->Q, s->keys, s->sm_count * 4, st, sol_view<int32_t>(s),
-                              sp, imask, x_lo, x_hi);
+                              static_cast<uint32_t>(s->pitch), I->Q, s->keys, s->sm_count * 4, st,
+                              sol_view<int32_t>(s), sp, imask, x_lo, x_hi);
     } else if (I->dtype == TGA_I32) {
         e = launch_inter<int32_t>(mask, I->tw, sol_view<int32_t>(s), s->tmap, s->d_tiles, t_lo, t_hi, sp, s->keys,
                                   grid, st);
@@ -782,11 +782,14 @@ extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
     return TGA_OK;
 }
 
+static uint64_t key_to_canonical(const tga_solution *s, uint64_t k);
+
 extern "C" int32_t tga_solution_keys(tga_solution *s, uint64_t *keys) {
     if (!s || !keys) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (sync_host(s) != TGA_OK) return TGA_ERR_CUDA;
     TGA_CUDA(cudaMemcpyAsync(s->h_keys, s->keys, TGA_N_VARIANTS * 8, cudaMemcpyDeviceToHost, s->stream));
     TGA_CUDA(cudaStreamSynchronize(s->stream));
-    std::memcpy(keys, s->h_keys, TGA_N_VARIANTS * 8);
+    for (int v = 0; v < TGA_N_VARIANTS; ++v) keys[v] = key_to_canonical(s, s->h_keys[v]);
     return TGA_OK;
 }
 
@@ -801,6 +804,24 @@ static double decode_score(uint32_t ord, bool integer, int64_t *as_int) {
     std::memcpy(&f, &u, 4);
     *as_int = static_cast<int64_t>(std::llround(static_cast<double>(f)));
     return static_cast<double>(f);
+}
+
+// physical slot -> (route, position): largest route with rbase <= x
+static void phys_to_rp(const tga_solution *s, int x, int *r, int *p) {
+    const auto it = std::upper_bound(s->rbase.begin(), s->rbase.begin() + s->R, x);
+    *r = static_cast<int>(it - s->rbase.begin()) - 1;
+    *p = x - s->rbase[*r];
+}
+
+// a key over physical slots -> the same key over canonical slots (u * Q + v)
+static uint64_t key_to_canonical(const tga_solution *s, uint64_t k) {
+    if (k == ~0ull) return k;
+    const uint32_t idx = static_cast<uint32_t>(k & 0xFFFFFFFFu);
+    int ra, pa, rb, pb;
+    phys_to_rp(s, static_cast<int>(idx / static_cast<uint32_t>(s->pitch)), &ra, &pa);
+    phys_to_rp(s, static_cast<int>(idx % static_cast<uint32_t>(s->pitch)), &rb, &pb);
+    const uint64_t c = static_cast<uint64_t>(s->cbase[ra] + pa) * static_cast<uint32_t>(s->Qc) + (s->cbase[rb] + pb);
+    return (k & 0xFFFFFFFF00000000ull) | c;
 }
 
 static void canon_to_rp(const tga_solution *s, int c, int *r, int *p) {
@@ -840,14 +861,15 @@ static int32_t decode_best(const tga_solution *s, const uint64_t *keys, uint32_t
     out->variant = -1;
     if (bv < 0) return TGA_NO_IMPROVING_MOVE;
     const uint32_t idx = static_cast<uint32_t>(bk & 0xFFFFFFFFu);
-    const int cu = static_cast<int>(idx / static_cast<uint32_t>(s->Qc));
-    const int cv = static_cast<int>(idx % static_cast<uint32_t>(s->Qc));
+    const int xu = static_cast<int>(idx / static_cast<uint32_t>(s->pitch));  // physical slots
+    const int xv = static_cast<int>(idx % static_cast<uint32_t>(s->pitch));
     out->variant = bv;
     variant_lengths(bv, &out->n1, &out->n2);
-    out->u = cu;
-    out->v = cv;
-    canon_to_rp(s, cu, &out->route_a, &out->pos_a);
-    canon_to_rp(s, cv, &out->route_b, &out->pos_b);
+    phys_to_rp(s, xu, &out->route_a, &out->pos_a);
+    phys_to_rp(s, xv, &out->route_b, &out->pos_b);
+    out->u = s->cbase[out->route_a] + out->pos_a;  // canonical ids
+    out->v = s->cbase[out->route_b] + out->pos_b;
+    bk = (bk & 0xFFFFFFFF00000000ull) | (static_cast<uint64_t>(out->u) * static_cast<uint32_t>(s->Qc) + out->v);
     out->delta_f = decode_score(static_cast<uint32_t>(bk >> 32), s->inst->dtype == TGA_I32, &out->delta_i);
     out->feasible = 1;
     if (s->inst->opt.score_mode == TGA_SCORE_PENALISED) out->feasible = -1;  // not tracked in penalised mode
@@ -1380,7 +1402,11 @@ extern "C" int32_t tga_batch_keys(tga_batch *b, uint64_t *keys) {
     const size_t bytes = sizeof(uint64_t) * TGA_N_VARIANTS * b->sols.size();
     TGA_CUDA(cudaMemcpyAsync(b->h_keys, b->d_keys, bytes, cudaMemcpyDeviceToHost, b->stream));
     TGA_CUDA(cudaStreamSynchronize(b->stream));
-    std::memcpy(keys, b->h_keys, bytes);
+    for (size_t k = 0; k < b->sols.size(); ++k) {
+        if (sync_host(b->sols[k]) != TGA_OK) return TGA_ERR_CUDA;
+        for (int v = 0; v < TGA_N_VARIANTS; ++v)
+            keys[k * TGA_N_VARIANTS + v] = key_to_canonical(b->sols[k], b->h_keys[k * TGA_N_VARIANTS + v]);
+    }
     return TGA_OK;
 }
 

@@ -111,7 +111,9 @@ typedef struct {
     int32_t w_load;      /* integer penalty weight on load excess (default 10) */
     int32_t w_tw;        /* integer penalty weight on time warp (default 10) */
     int32_t device;      /* CUDA device ordinal; -1 = current device */
-    int32_t reserved[12];
+    int32_t slack;       /* spare physical slots per route (0 = default 2, -1 = none): a move that
+                            keeps both changed routes within their slots refreshes only them */
+    int32_t reserved[11];
 } tga_options;
 
 typedef struct {

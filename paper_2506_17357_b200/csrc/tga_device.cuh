@@ -210,7 +210,8 @@ __device__ __forceinline__ void intra_cvrp_warp(const SolView<int32_t> &S, const
             for (int N = 1; N <= 3; ++N) {  // intra relocate / or-opt
                 if (!(vmask & (1u << (10 + N)))) continue;
                 const bool ok = ok_route && in && p + N - 1 <= L && (q < p - 1 || q > p + N - 1);
-                k[10 + N] = intra_k32(ok, rem[N - 1] + D(v, x) + D(x + N - 1, v + 1) - ev, lane);
+                // c is symmetric (host-checked): every Dp read is row x.. with lanes along columns
+                k[10 + N] = intra_k32(ok, rem[N - 1] + D(x, v) + D(x + N - 1, v + 1) - ev, lane);
             }
 #pragma unroll
             for (int a = 1; a <= 3; ++a) {   // intra swap (N1 = a at u, N2 = b at v), u + N1 <= v
@@ -220,8 +221,8 @@ __device__ __forceinline__ void intra_cvrp_warp(const SolView<int32_t> &S, const
                     if (!(vmask & (1u << var))) continue;
                     const bool ok = ok_route && in && q >= p + a && q + b - 1 <= L;
                     const int32_t ev2 = S.enext[min(v + b - 1, base + L + 1)];
-                    const int32_t adj = D(x - 1, v) + D(v + b - 1, x) + D(x + a - 1, v + b) - em - evm - ev2;
-                    const int32_t gap = D(x - 1, v) + D(v + b - 1, x + a) + D(vm1, x) + D(x + a - 1, v + b) - em -
+                    const int32_t adj = D(x - 1, v) + D(x, v + b - 1) + D(x + a - 1, v + b) - em - evm - ev2;
+                    const int32_t gap = D(x - 1, v) + D(x + a, v + b - 1) + D(x, vm1) + D(x + a - 1, v + b) - em -
                                         eo[a - 1] - evm - ev2;
                     k[var] = intra_k32(ok, q == p + a ? adj : gap, lane);
                 }

@@ -58,6 +58,24 @@ __device__ __forceinline__ void scan_route(const ScanArgs<DT> &A, const int r, c
     const int L = A.rlenR[r];
     const int len = L + 2;
     const int n = A.n_nodes;
+    if constexpr (std::is_same<DT, int32_t>::value) {
+        // spare (hole) slots of the route carry poisoned fast-path records
+        const int cap = A.rbase[r + 1] - base;
+        for (int k = len + lane; k < cap; k += 32) {
+            if (A.rec) {
+                SlotRec q{};
+                q.c = -1; q.r = -1; q.fL = q.bL1 = q.W = kPoison;
+                for (int j = 0; j < 3; ++j) { q.so[j] = kPoison; q.sA[j] = kPoison; }
+                A.rec[base + k] = q;
+            }
+            if (TW && A.rectw) {
+                SlotTW w{};
+                w.EF = w.EFm = kTwBig;
+                for (int j = 0; j < 3; ++j) { w.LBN[j] = -kTwBig; w.sTL[j] = -kTwBig; }
+                A.rectw[base + k] = w;
+            }
+        }
+    }
 
     // ---------------- forward pass: prefix loads, prefix distance, prefix TW records
     int carryL = 0;
@@ -268,20 +286,24 @@ __global__ void __launch_bounds__(256) k_scan(ScanArgs<DT> A, int r_lo, int r_hi
     scan_route<DT, TW>(A, r, lane);
 }
 
-// The update step of an applied move as work units: units
-// [0, hi-lo) refresh Dp rows [lo, hi); the next ceil(Qp/8) units refresh Dp
-// columns [lo, hi) of 8 rows each; the rest re-scan 8 routes each of
-// [r_lo, r_hi) (the scan reads node ids and C, never Dp: independent roles).
+// The update step of an applied move as work units: one unit per Dp row
+// of the changed slot ranges, ceil(Qp/8) units refreshing their Dp columns in 8
+// rows each, then one unit per 8 routes to re-scan (a full relayout refreshes
+// every row and re-scans every route).  The scan reads node ids and C, never
+// Dp: the roles are independent.
 template <class DT, bool TW>
-__device__ __forceinline__ void update_units(const ScanArgs<DT> &A, DT *__restrict__ Dp, int pitch, int Qp, int lo,
-                                             int hi, int r_lo, int r_hi, int unit0, int ustride) {
+__device__ __forceinline__ void update_units(const ScanArgs<DT> &A, DT *__restrict__ Dp, int pitch, int Qp, int R,
+                                             const UpdateSpec u, int unit0, int ustride) {
     const DT *__restrict__ C = A.C;
     const int n = A.n_nodes;
-    const int nb_rows = hi - lo, nb_cols = (Qp + 7) / 8, nb_scan = (r_hi - r_lo + 7) / 8;
+    const int n1 = u.hi1 - u.lo1, n2 = u.hi2 - u.lo2;
+    const int nb_rows = n1 + n2, nb_cols = u.full ? 0 : (Qp + 7) / 8;
+    const int n_routes = u.full ? R : (u.r1 >= 0) + (u.r2 >= 0);
+    const int nb_scan = (n_routes + 7) / 8;
     const int total = nb_rows + nb_cols + nb_scan;
     for (int b = unit0; b < total; b += ustride) {
         if (b < nb_rows) {
-            const int a = lo + b;
+            const int a = b < n1 ? u.lo1 + b : u.lo2 + (b - n1);
             const DT *crow = C + static_cast<size_t>(A.node[a]) * n;
             DT *drow = Dp + static_cast<size_t>(a) * pitch;
             for (int c = 4 * threadIdx.x; c < pitch; c += 4 * blockDim.x) {
@@ -295,19 +317,22 @@ __device__ __forceinline__ void update_units(const ScanArgs<DT> &A, DT *__restri
             if (a < Qp) {
                 const DT *crow = C + static_cast<size_t>(A.node[a]) * n;
                 DT *drow = Dp + static_cast<size_t>(a) * pitch;
-                for (int c = lo + (threadIdx.x & 31); c < hi; c += 32) drow[c] = __ldg(crow + A.node[c]);
+                for (int j = (threadIdx.x & 31); j < n1 + n2; j += 32) {
+                    const int c = j < n1 ? u.lo1 + j : u.lo2 + (j - n1);
+                    drow[c] = __ldg(crow + A.node[c]);
+                }
             }
         } else {
-            const int r = r_lo + (b - nb_rows - nb_cols) * 8 + static_cast<int>(threadIdx.x >> 5);
-            if (r < r_hi) scan_route<DT, TW>(A, r, threadIdx.x & 31);
+            const int j = (b - nb_rows - nb_cols) * 8 + static_cast<int>(threadIdx.x >> 5);
+            if (j < n_routes) scan_route<DT, TW>(A, u.full ? j : (j == 0 && u.r1 >= 0 ? u.r1 : u.r2), threadIdx.x & 31);
         }
     }
 }
 
 template <class DT, bool TW>
-__global__ void __launch_bounds__(256) k_update(ScanArgs<DT> A, DT *__restrict__ Dp, int pitch, int Qp, int lo, int hi,
-                                                int r_lo, int r_hi) {
-    update_units<DT, TW>(A, Dp, pitch, Qp, lo, hi, r_lo, r_hi, blockIdx.x, gridDim.x);
+__global__ void __launch_bounds__(256) k_update(ScanArgs<DT> A, DT *__restrict__ Dp, int pitch, int Qp, int R,
+                                                UpdateSpec u) {
+    update_units<DT, TW>(A, Dp, pitch, Qp, R, u, blockIdx.x, gridDim.x);
 }
 
 // Device-resident apply + update in ONE launch (blockIdx.y = solution): block 0
@@ -334,17 +359,17 @@ __global__ void __launch_bounds__(256) k_pick_update(const DevState *__restrict_
     extern __shared__ int32_t smr[];
     const DevState &S = states[blockIdx.y];
     if (blockIdx.x == 0) pick_apply_body(S, mask, integer, smr);
-    if (gridDim.x > 1) solution_barrier(S.desc + 6, gridDim.x);
+    if (gridDim.x > 1) solution_barrier(S.desc + 8, gridDim.x);
     else __syncthreads();
     const volatile int32_t *desc = S.desc;
     if (desc[0] == 0) return;
-    update_units<DT, TW>(scans[blockIdx.y], static_cast<DT *>(S.Dp), S.pitch, S.Qp, desc[1], desc[2], desc[3],
-                         desc[4], blockIdx.x, gridDim.x);
+    const UpdateSpec u{desc[1], desc[2], desc[3], desc[4], desc[5], desc[6], desc[7]};
+    update_units<DT, TW>(scans[blockIdx.y], static_cast<DT *>(S.Dp), S.pitch, S.Qp, S.R, u, blockIdx.x, gridDim.x);
 }
 
 cudaError_t launch_pick_update(const DevState *states, const void *scans, int n_sol, bool tw, bool is_int,
                                uint32_t mask, int max_routes, int blocks_per_sol, cudaStream_t st) {
-    const int smem = 3 * (max_routes + 1) * 4;
+    const int smem = 4 * (max_routes + 1) * 4;
     dim3 g(blocks_per_sol, n_sol);
     if (smem > 48 * 1024) {
         cudaFuncSetAttribute(k_pick_update<int32_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1077,19 +1102,19 @@ cudaError_t launch_scan(const ScanArgs<DT> &A, bool tw, int r_lo, int r_hi, cuda
 }
 
 template <class DT>
-cudaError_t launch_update(const ScanArgs<DT> &A, bool tw, DT *Dp, int pitch, int Qp, int lo, int hi, int r_lo,
-                          int r_hi, cudaStream_t st) {
-    const int nb_rows = hi - lo, nb_cols = (Qp + 7) / 8, nb_scan = (r_hi - r_lo + 7) / 8;
-    const int grid = nb_rows + nb_cols + nb_scan;
+cudaError_t launch_update(const ScanArgs<DT> &A, bool tw, DT *Dp, int pitch, int Qp, int R, const UpdateSpec &u,
+                          cudaStream_t st) {
+    const int n_routes = u.full ? R : (u.r1 >= 0) + (u.r2 >= 0);
+    const int grid = (u.hi1 - u.lo1) + (u.hi2 - u.lo2) + (u.full ? 0 : (Qp + 7) / 8) + (n_routes + 7) / 8;
     if (grid <= 0) return cudaSuccess;
-    if (tw) k_update<DT, true><<<grid, 256, 0, st>>>(A, Dp, pitch, Qp, lo, hi, r_lo, r_hi);
-    else    k_update<DT, false><<<grid, 256, 0, st>>>(A, Dp, pitch, Qp, lo, hi, r_lo, r_hi);
+    if (tw) k_update<DT, true><<<grid, 256, 0, st>>>(A, Dp, pitch, Qp, R, u);
+    else    k_update<DT, false><<<grid, 256, 0, st>>>(A, Dp, pitch, Qp, R, u);
     ++g_launches;
     return cudaGetLastError();
 }
-template cudaError_t launch_update<int32_t>(const ScanArgs<int32_t> &, bool, int32_t *, int, int, int, int, int, int,
-                                            cudaStream_t);
-template cudaError_t launch_update<float>(const ScanArgs<float> &, bool, float *, int, int, int, int, int, int,
+template cudaError_t launch_update<int32_t>(const ScanArgs<int32_t> &, bool, int32_t *, int, int, int,
+                                            const UpdateSpec &, cudaStream_t);
+template cudaError_t launch_update<float>(const ScanArgs<float> &, bool, float *, int, int, int, const UpdateSpec &,
                                           cudaStream_t);
 
 template <class DT, bool TW, uint32_t MASK>

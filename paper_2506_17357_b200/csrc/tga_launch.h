@@ -64,16 +64,22 @@ struct ScanArgs {
     SlotTW *rectw;     // VRPTW (TW-I) fast-path records; may be null
 };
 
+// what an update refreshes: up to two slot ranges (the changed routes' whole
+// slot capacity) with their routes, or everything (full relayout)
+struct UpdateSpec {
+    int lo1, hi1, lo2, hi2, r1, r2, full;
+};
+
 // per-solution device state of the device-resident step (k_pick_apply / k_update_dev)
 struct DevState {
     int32_t *node, *route, *pos, *rlen, *canon;   // slot arrays (guarded)
     int32_t *rbase, *rlenR, *cbase;              // per route
     int32_t *scratch;                            // snapshot of a changed span (cap ints)
     const uint64_t *keys;                        // 23 packed keys of the last evaluation
-    int32_t *desc;                               // [applied, lo, hi, r_lo, r_hi), [6] grid-barrier counter
+    int32_t *desc;                               // [0] applied, [1..7] UpdateSpec, [8] grid-barrier counter
     unsigned long long *acc;                     // [23] candidate counts + [23] applied moves
     void *Dp;
-    int32_t R, Qc, Qp, pitch;
+    int32_t R, Qc, Qp, pitch, slack;
 };
 cudaError_t launch_pick_update(const DevState *states, const void *scans, int n_sol, bool tw, bool is_int,
                                uint32_t mask, int max_routes, int blocks_per_sol, cudaStream_t st);
@@ -82,8 +88,8 @@ template <class DT>
 cudaError_t launch_dp(DT *Dp, int pitch, const int32_t *node, const DT *C, int n, int Qp, int lo, int hi,
                       bool full, cudaStream_t st);
 template <class DT>
-cudaError_t launch_update(const ScanArgs<DT> &A, bool tw, DT *Dp, int pitch, int Qp, int lo, int hi, int r_lo,
-                          int r_hi, cudaStream_t st);
+cudaError_t launch_update(const ScanArgs<DT> &A, bool tw, DT *Dp, int pitch, int Qp, int R, const UpdateSpec &u,
+                          cudaStream_t st);
 template <class DT>
 cudaError_t launch_scan(const ScanArgs<DT> &A, bool tw, int r_lo, int r_hi, cudaStream_t st);
 template <class DT>

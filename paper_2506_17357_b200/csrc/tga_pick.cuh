@@ -55,11 +55,10 @@ using namespace pick;
 __device__ __forceinline__ void pick_apply_body(const DevState &S, uint32_t mask, int integer, int32_t *smr) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int R = S.R;
-    int32_t *sb = smr, *sl = smr + (R + 1), *sc = smr + 2 * (R + 1);
+    int32_t *sb = smr, *sl = smr + (R + 1), *nb = smr + 2 * (R + 1);  // old bases, old lengths, new bases
     for (int r = tid; r <= R; r += blockDim.x) {
         sb[r] = S.rbase[r];
         sl[r] = r < R ? S.rlenR[r] : 0;
-        sc[r] = S.cbase[r];
     }
     __shared__ uint64_t skeys[23];
     if (tid < 23) skeys[tid] = S.keys[tid];
@@ -194,9 +193,10 @@ __device__ __forceinline__ void pick_apply_body(const DevState &S, uint32_t mask
             sh_n = nroutes;
             sh_rlo = nr[0].r;
             sh_rhi = nroutes == 2 ? nr[1].r : nr[0].r;
-            sh_lo = sb[sh_rlo];
-            sh_hi = sb[sh_rhi] + sl[sh_rhi] + 2;
-            sh_d = nr[0].L - sl[sh_rlo];  // shift of every route after the first changed one
+            // do the changed routes still fit in their slot capacity?
+            bool fits = nr[0].L + 2 <= sb[nr[0].r + 1] - sb[nr[0].r];
+            if (nroutes == 2) fits = fits && (nr[1].L + 2 <= sb[nr[1].r + 1] - sb[nr[1].r]);
+            sh_d = fits ? 0 : 1;  // 1 = full relayout
             sh_applied = 1;
         }
     }
@@ -205,56 +205,80 @@ __device__ __forceinline__ void pick_apply_body(const DevState &S, uint32_t mask
         if (tid == 0) S.desc[0] = 0;
         return;  // uniform across the block
     }
-    const int lo = sh_lo, hi = sh_hi, rlo = sh_rlo, rhi = sh_rhi, dlt = sh_d, nrt = sh_n;
-    // ---- 3. snapshot the changed span of node ids
-    for (int x = lo + tid; x < hi; x += blockDim.x) S.scratch[x - lo] = S.node[x];
-    __syncthreads();
-    // new base / length / canonical base of route r in [rlo, rhi] (old values in shared memory)
-    auto nbase = [&](int r) { return r == rlo ? sb[r] : sb[r] + dlt; };
-    auto ncb = [&](int r) { return r == rlo ? sc[r] : sc[r] + dlt; };
+    const int rlo = sh_rlo, rhi = sh_rhi, full = sh_d, nrt = sh_n;
     auto nlen = [&](int r) { return r == nr[0].r ? nr[0].L : (nrt == 2 && r == nr[1].r ? nr[1].L : sl[r]); };
-    // ---- 4. rewrite the span slot by slot
-    for (int x = lo + tid; x < hi; x += blockDim.x) {
-        int a = rlo, b = rhi;  // route of new slot x: largest r with nbase(r) <= x
-        while (a < b) {
-            const int m = (a + b + 1) >> 1;
-            if (nbase(m) <= x) a = m;
-            else b = m - 1;
+    auto changed = [&](int r) -> const NewRoute * {
+        return r == nr[0].r ? &nr[0] : ((nrt == 2 && r == nr[1].r) ? &nr[1] : nullptr);
+    };
+    // node id of new slot p (1..L) of route r: through its pieces, or unchanged
+    auto old_slot = [&](int r, int p) {
+        const NewRoute *chg = changed(r);
+        if (!chg) return sb[r] + p;
+        int off = p - 1, k = 0;
+        while (off >= chg->p[k].len) { off -= chg->p[k].len; ++k; }
+        const Piece &pc = chg->p[k];
+        return sb[pc.src] + (pc.rev ? pc.start + pc.len - 1 - off : pc.start + off);
+    };
+    auto write_slot = [&](int x, int r, int p, int L, int span_lo) {
+        if (p <= L + 1) {
+            S.node[x] = (p >= 1 && p <= L) ? S.scratch[old_slot(r, p) - span_lo] : 0;
+            S.route[x] = r;
+            S.pos[x] = p;
+            S.rlen[x] = L;
+            S.canon[x] = p <= L ? x : -1;  // validity only (keys index physical slots)
+        } else {  // spare slot
+            S.node[x] = 0;
+            S.route[x] = -1;
+            S.pos[x] = 0;
+            S.rlen[x] = -1;
+            S.canon[x] = -1;
         }
-        const int r = a, p = x - nbase(r), L = nlen(r);
-        int nd = 0;
-        if (p >= 1 && p <= L) {
-            const NewRoute *chg = (r == nr[0].r) ? &nr[0] : ((nrt == 2 && r == nr[1].r) ? &nr[1] : nullptr);
-            int old_slot;
-            if (chg) {
-                int off = p - 1, k = 0;
-                while (off >= chg->p[k].len) { off -= chg->p[k].len; ++k; }
-                const Piece &pc = chg->p[k];
-                const int op = pc.rev ? pc.start + pc.len - 1 - off : pc.start + off;
-                old_slot = sb[pc.src] + op;
-            } else {
-                old_slot = sb[r] + p;
+    };
+    if (!full) {
+        // ---- 3. snapshot the node ids between the two changed routes, rewrite just them
+        const int span_lo = sb[rlo], span_hi = sb[rhi + 1];
+        for (int x = span_lo + tid; x < span_hi; x += blockDim.x) S.scratch[x - span_lo] = S.node[x];
+        __syncthreads();
+        for (int k = 0; k < nrt; ++k) {
+            const int r = nr[k].r, L = nr[k].L;
+            for (int x = sb[r] + tid; x < sb[r + 1]; x += blockDim.x) write_slot(x, r, x - sb[r], L, span_lo);
+        }
+        if (tid < nrt) S.rlenR[nr[tid].r] = nr[tid].L;
+        if (tid == 0) {
+            S.desc[1] = sb[rlo]; S.desc[2] = sb[rlo + 1];
+            S.desc[3] = nrt == 2 ? sb[rhi] : 0; S.desc[4] = nrt == 2 ? sb[rhi + 1] : 0;
+            S.desc[5] = rlo; S.desc[6] = nrt == 2 ? rhi : -1; S.desc[7] = 0;
+        }
+    } else {
+        // ---- a changed route outgrew its slots: full relayout with fresh spare slots
+        if (tid == 0) {
+            int b = 0;
+            for (int r = 0; r < R; ++r) { nb[r] = b; b += nlen(r) + 2 + S.slack; }
+            nb[R] = b;  // == Qp
+        }
+        for (int x = tid; x < S.Qp; x += blockDim.x) S.scratch[x] = S.node[x];
+        __syncthreads();
+        for (int x = tid; x < S.Qp; x += blockDim.x) {
+            int a = 0, b = R - 1;  // largest r with nb[r] <= x
+            while (a < b) {
+                const int m = (a + b + 1) >> 1;
+                if (nb[m] <= x) a = m;
+                else b = m - 1;
             }
-            nd = S.scratch[old_slot - lo];
+            write_slot(x, a, x - nb[a], nlen(a), 0);
         }
-        S.node[x] = nd;
-        S.route[x] = r;
-        S.pos[x] = p;
-        S.rlen[x] = L;
-        S.canon[x] = (p <= L) ? ncb(r) + p : -1;
-    }
-    // ---- 5. per-route arrays (old values are in shared memory: no hazard)
-    for (int r = rlo + tid; r <= rhi; r += blockDim.x) {
-        S.rbase[r] = nbase(r);
-        S.cbase[r] = ncb(r);
-        S.rlenR[r] = nlen(r);
+        __syncthreads();
+        for (int r = tid; r <= R; r += blockDim.x) {
+            if (r < R) S.rlenR[r] = nlen(r);
+            S.rbase[r] = nb[r];
+        }
+        if (tid == 0) {
+            S.desc[1] = 0; S.desc[2] = S.Qp; S.desc[3] = 0; S.desc[4] = 0;
+            S.desc[5] = -1; S.desc[6] = -1; S.desc[7] = 1;
+        }
     }
     if (tid == 0) {
         S.desc[0] = 1;
-        S.desc[1] = lo;
-        S.desc[2] = hi;
-        S.desc[3] = rlo;
-        S.desc[4] = rhi + 1;
         S.acc[23] += 1;
     }
 }

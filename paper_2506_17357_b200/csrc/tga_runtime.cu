@@ -112,7 +112,8 @@ struct tga_solution {
     uint64_t gen = 1;
     std::vector<std::vector<int32_t>> routes;
     int R = 0, N = 0, Qc = 0, Qp = 0, pitch = 0, cap = 0;
-    std::vector<int32_t> rbase, cbase;                  // host: physical / canonical base per route
+    std::vector<int32_t> rbase, cbase, rcap;            // host: physical base / canonical base / slot capacity
+    int slack = 2;                                      // spare slots per route (full relayout)
     // device arena
     void *arena = nullptr;
     int32_t *node = nullptr, *route = nullptr, *pos = nullptr, *rlen = nullptr, *canon = nullptr;
@@ -180,64 +181,93 @@ static int32_t set_device(const tga_instance *inst) {
     return TGA_OK;
 }
 
-// Build the physical layout: route r occupies slots rbase[r] .. rbase[r]+L+1
-// (start depot, customers, end depot).  Canonical id of (r, p), p <= L, is
-// cbase[r] + p (SURVEY §8(c) "canonical slot"); end depots and padding have
-// canonical id -1.
-static void compute_bases(tga_solution *s) {
-    s->rbase.resize(s->R + 1);
+// Physical layout: route r owns slots rbase[r] .. rbase[r]+cap[r]-1: start depot,
+// customers, end depot, then cap - L - 2 spare "hole" slots (canonical id -1,
+// route -1).  cap = L + 2 + slack is assigned by a full relayout; a move whose
+// changed routes still fit keeps every base, so only those routes' slots, Dp rows
+// and columns are refreshed.  Canonical id of (r, p), p <= L, is cbase[r] + p
+// (SURVEY §8(c)); it is the host's business (keys index physical slots).
+static void compute_cbase(tga_solution *s) {
     s->cbase.resize(s->R + 1);
-    int pb = 0, cb = 0;
+    int cb = 0;
     for (int r = 0; r < s->R; ++r) {
-        s->rbase[r] = pb;
         s->cbase[r] = cb;
-        const int L = static_cast<int>(s->routes[r].size());
-        pb += L + 2;
-        cb += L + 1;
+        cb += static_cast<int>(s->routes[r].size()) + 1;
     }
-    s->rbase[s->R] = pb;
     s->cbase[s->R] = cb;
 }
 
-// Fill the 5 layout arrays (node, route, pos, rlen, canon) of routes r_lo..r_hi
-// into the pinned staging rows (row pitch = the arena pitch of those arrays),
-// relative to slot rbase[r_lo], plus the per-route (rbase, rlen) rows.
-static void stage_layout(tga_solution *s, int r_lo, int r_hi, int *span_lo, int *span_n) {
-    const int lo = s->rbase[r_lo], hi = s->rbase[r_hi + 1];
+static void relayout_full(tga_solution *s) {
+    s->rbase.resize(s->R + 1);
+    s->rcap.resize(s->R);
+    int pb = 0;
+    for (int r = 0; r < s->R; ++r) {
+        s->rbase[r] = pb;
+        s->rcap[r] = static_cast<int>(s->routes[r].size()) + 2 + s->slack;
+        pb += s->rcap[r];
+    }
+    s->rbase[s->R] = pb;  // == Qp, constant
+    compute_cbase(s);
+}
+
+static bool route_fits(const tga_solution *s, int r) {
+    return static_cast<int>(s->routes[r].size()) + 2 <= s->rcap[r];
+}
+
+// Stage the 5 layout arrays (node, route, pos, rlen, canon) of route r's whole
+// slot range into the pinned staging rows at column offset `off`.
+static void stage_route(tga_solution *s, int r, int off) {
     const size_t rp = s->lay_pitch / 4;
     int32_t *nd = s->h_stage, *rt = nd + rp, *ps = rt + rp, *rl = ps + rp, *cn = rl + rp;
-    for (int r = r_lo; r <= r_hi; ++r) {
-        const int L = static_cast<int>(s->routes[r].size());
-        for (int p = 0; p <= L + 1; ++p) {
-            const int i = s->rbase[r] + p - lo;
+    const int L = static_cast<int>(s->routes[r].size());
+    for (int p = 0; p < s->rcap[r]; ++p) {
+        const int i = off + p;
+        if (p <= L + 1) {
             nd[i] = (p == 0 || p == L + 1) ? 0 : s->routes[r][p - 1];
             rt[i] = r;
             ps[i] = p;
             rl[i] = L;
             cn[i] = (p <= L) ? s->cbase[r] + p : -1;
+        } else {  // hole
+            nd[i] = 0; rt[i] = -1; ps[i] = 0; rl[i] = -1; cn[i] = -1;
         }
     }
-    const size_t rq = s->route_pitch / 4;
-    int32_t *rb = s->h_rstage, *rn = rb + rq, *rc = rn + rq;
-    for (int r = 0; r < s->R; ++r) {
-        rb[r] = s->rbase[r];
-        rn[r] = static_cast<int32_t>(s->routes[r].size());
-        rc[r] = s->cbase[r];
-    }
-    *span_lo = lo;
-    *span_n = hi - lo;
 }
 
-// Two asynchronous 2-D copies (5 slot arrays of the changed span, 2 route
-// arrays); no host synchronisation -- the staging buffers are reused only after
-// the stream has drained (tga_apply_move synchronises on entry).
-static int32_t upload_layout(tga_solution *s, int r_lo, int r_hi) {
-    int lo, n;
-    stage_layout(s, r_lo, r_hi, &lo, &n);
-    TGA_CUDA(cudaMemcpy2DAsync(s->node + lo, s->lay_pitch, s->h_stage, s->lay_pitch, sizeof(int32_t) * n, 5,
-                               cudaMemcpyHostToDevice, s->stream));
-    TGA_CUDA(cudaMemcpy2DAsync(s->d_rbase, s->route_pitch, s->h_rstage, s->route_pitch, sizeof(int32_t) * s->R, 3,
-                               cudaMemcpyHostToDevice, s->stream));
+static void stage_route_arrays(tga_solution *s) {
+    const size_t rq = s->route_pitch / 4;
+    int32_t *rb = s->h_rstage, *rn = rb + rq, *rc = rn + rq;
+    for (int r = 0; r <= s->R; ++r) {
+        rb[r] = s->rbase[r];
+        rn[r] = r < s->R ? static_cast<int32_t>(s->routes[r].size()) : 0;
+        rc[r] = s->cbase[r];
+    }
+}
+
+// Asynchronous 2-D copies from pinned staging (no host synchronisation: the
+// staging buffers are reused only after the stream has drained).
+//   routes = {ra, rb} (rb may be -1) : just those routes' slot ranges
+//   full                            : every slot
+static int32_t upload_layout(tga_solution *s, bool full, int ra = -1, int rb = -1) {
+    if (full) {
+        int off = 0;
+        for (int r = 0; r < s->R; ++r) { stage_route(s, r, off); off += s->rcap[r]; }
+        TGA_CUDA(cudaMemcpy2DAsync(s->node, s->lay_pitch, s->h_stage, s->lay_pitch, sizeof(int32_t) * off, 5,
+                                   cudaMemcpyHostToDevice, s->stream));
+    } else {
+        int off = 0;
+        for (int k = 0; k < 2; ++k) {
+            const int r = k == 0 ? ra : rb;
+            if (r < 0 || (k == 1 && rb == ra)) continue;
+            stage_route(s, r, off);
+            TGA_CUDA(cudaMemcpy2DAsync(s->node + s->rbase[r], s->lay_pitch, s->h_stage + off, s->lay_pitch,
+                                       sizeof(int32_t) * s->rcap[r], 5, cudaMemcpyHostToDevice, s->stream));
+            off += s->rcap[r];
+        }
+    }
+    stage_route_arrays(s);
+    TGA_CUDA(cudaMemcpy2DAsync(s->d_rbase, s->route_pitch, s->h_rstage, s->route_pitch, sizeof(int32_t) * (s->R + 1),
+                               3, cudaMemcpyHostToDevice, s->stream));
     return TGA_OK;
 }
 
@@ -307,7 +337,7 @@ static DevState make_devstate(const tga_solution *s, const uint64_t *keys) {
     d.node = s->node; d.route = s->route; d.pos = s->pos; d.rlen = s->rlen; d.canon = s->canon;
     d.rbase = s->d_rbase; d.rlenR = s->d_rlenR; d.cbase = s->d_cbase;
     d.scratch = s->d_scratch; d.keys = keys; d.desc = s->d_desc; d.acc = s->d_acc; d.Dp = s->Dp;
-    d.R = s->R; d.Qc = s->pitch; d.Qp = s->Qp; d.pitch = s->pitch;
+    d.R = s->R; d.Qc = s->pitch; d.Qp = s->Qp; d.pitch = s->pitch; d.slack = s->slack;
     return d;
 }
 
@@ -316,43 +346,50 @@ static DevState make_devstate(const tga_solution *s, const uint64_t *keys) {
 static int32_t sync_host(tga_solution *s) {
     if (!s->host_stale) return TGA_OK;
     TGA_CUDA(cudaStreamSynchronize(s->stream));
-    std::vector<int32_t> nd(s->Qp), L(s->R);
+    std::vector<int32_t> nd(s->Qp), L(s->R), B(s->R + 1);
     TGA_CUDA(cudaMemcpy(nd.data(), s->node, 4 * s->Qp, cudaMemcpyDeviceToHost));
     TGA_CUDA(cudaMemcpy(L.data(), s->d_rlenR, 4 * s->R, cudaMemcpyDeviceToHost));
-    int b = 0;
+    TGA_CUDA(cudaMemcpy(B.data(), s->d_rbase, 4 * (s->R + 1), cudaMemcpyDeviceToHost));
     for (int r = 0; r < s->R; ++r) {
-        s->routes[r].assign(nd.begin() + b + 1, nd.begin() + b + 1 + L[r]);
-        b += L[r] + 2;
+        s->routes[r].assign(nd.begin() + B[r] + 1, nd.begin() + B[r] + 1 + L[r]);
+        s->rbase[r] = B[r];
+        s->rcap[r] = B[r + 1] - B[r];
     }
-    compute_bases(s);
+    s->rbase[s->R] = B[s->R];
+    compute_cbase(s);
     s->host_stale = false;
     s->drained = true;
     return TGA_OK;
 }
 
-static int32_t refresh(tga_solution *s, int r_lo, int r_hi, bool full) {
+// Device state of the current layout: full (load / reload / relayout) or just
+// the slot ranges, Dp rows / columns and records of routes ra, rb.
+static int32_t refresh(tga_solution *s, bool full, int ra = -1, int rb = -1) {
     const tga_instance *I = s->inst;
-    const int lo = full ? 0 : s->rbase[r_lo];
-    const int hi = full ? s->pitch : s->rbase[r_hi + 1];
     cudaError_t e;
     if (!full) {  // update step of one applied move: one launch (Dp rows + columns + re-scan)
+        UpdateSpec u{};
+        u.lo1 = s->rbase[ra]; u.hi1 = s->rbase[ra] + s->rcap[ra]; u.r1 = ra;
+        if (rb >= 0 && rb != ra) { u.lo2 = s->rbase[rb]; u.hi2 = s->rbase[rb] + s->rcap[rb]; u.r2 = rb; }
+        else { u.lo2 = u.hi2 = 0; u.r2 = -1; }
+        u.full = 0;
         if (I->dtype == TGA_I32)
             e = launch_update<int32_t>(scan_args<int32_t>(s), I->tw, static_cast<int32_t *>(s->Dp), s->pitch, s->Qp,
-                                       lo, hi, r_lo, r_hi + 1, s->stream);
+                                       s->R, u, s->stream);
         else
-            e = launch_update<float>(scan_args<float>(s), I->tw, static_cast<float *>(s->Dp), s->pitch, s->Qp, lo, hi,
-                                     r_lo, r_hi + 1, s->stream);
+            e = launch_update<float>(scan_args<float>(s), I->tw, static_cast<float *>(s->Dp), s->pitch, s->Qp, s->R,
+                                     u, s->stream);
         if (e != cudaSuccess) return fail(TGA_ERR_CUDA, std::string("update: ") + cudaGetErrorString(e));
         return TGA_OK;
     }
     if (I->dtype == TGA_I32) {
         e = launch_dp<int32_t>(static_cast<int32_t *>(s->Dp), s->pitch, s->node, static_cast<const int32_t *>(I->dC),
-                               I->n, s->Qp, lo, hi, full, s->stream);
-        if (e == cudaSuccess) e = launch_scan<int32_t>(scan_args<int32_t>(s), I->tw, r_lo, r_hi + 1, s->stream);
+                               I->n, s->Qp, 0, s->pitch, true, s->stream);
+        if (e == cudaSuccess) e = launch_scan<int32_t>(scan_args<int32_t>(s), I->tw, 0, s->R, s->stream);
     } else {
         e = launch_dp<float>(static_cast<float *>(s->Dp), s->pitch, s->node, static_cast<const float *>(I->dC), I->n,
-                             s->Qp, lo, hi, full, s->stream);
-        if (e == cudaSuccess) e = launch_scan<float>(scan_args<float>(s), I->tw, r_lo, r_hi + 1, s->stream);
+                             s->Qp, 0, s->pitch, true, s->stream);
+        if (e == cudaSuccess) e = launch_scan<float>(scan_args<float>(s), I->tw, 0, s->R, s->stream);
     }
     if (e != cudaSuccess) return fail(TGA_ERR_CUDA, std::string("refresh: ") + cudaGetErrorString(e));
     return TGA_OK;
@@ -519,14 +556,15 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
     for (int r = 0; r < R; ++r) s->routes[r].assign(cust + ptr[r], cust + ptr[r + 1]);
     s->N = ptr[R];
     s->Qc = s->N + R;
-    s->Qp = s->N + 2 * R;
+    s->slack = I->opt.slack > 0 ? I->opt.slack : (I->opt.slack < 0 ? 0 : 2);
+    s->Qp = s->N + (2 + s->slack) * R;
     s->pitch = static_cast<int>(align_up(static_cast<size_t>(s->Qp) + 4, kPitchAlign));
     s->cap = s->pitch + 2 * kGuard;
     if (static_cast<uint64_t>(s->Qc) * s->Qc > 0xFFFFFFFFull) {
         delete s;
         return fail(TGA_ERR_INVALID_ARGUMENT, "Q^2 exceeds the 32-bit flat index");
     }
-    compute_bases(s);
+    relayout_full(s);
     int32_t rc = TGA_OK;
     auto bail = [&](int32_t code) { free_solution(s); return code; };
     {
@@ -555,7 +593,7 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
         {&v_b1, cap * 4}, {&v_b2, cap * 4}, {&v_b3, cap * 4},
         {&v_fT, cap * 16}, {&v_bT, cap * 16}, {&v_s2, cap * 16}, {&v_s3, cap * 16},
         {&v_rbase, Rr * 4}, {&v_rlenR, Rr * 4}, {&v_cbase, Rr * 4}, {&v_rW, Rr * 4}, {&v_rTV, Rr * 4},
-        {&v_rD, Rr * 4}, {&v_ds, sizeof(DevState)}, {&v_sa, sizeof(ScanArgs<int32_t>)}, {&v_desc, 8 * 4},
+        {&v_rD, Rr * 4}, {&v_ds, sizeof(DevState)}, {&v_sa, sizeof(ScanArgs<int32_t>)}, {&v_desc, 16 * 4},
         {&v_scr, cap * 4}, {&v_acc, 48 * 8},
         {&v_keys, TGA_N_VARIANTS * 8}, {&v_tiles, tiles_max * 4},
         {&v_rec, want_fast ? cap * sizeof(SlotRec) : 0}, {&v_ftiles, want_fast ? ftiles_max * 4 : 0},
@@ -630,8 +668,8 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
         cudaMallocHost(&s->h_rstage, 3 * s->route_pitch) != cudaSuccess)
         return bail(fail(TGA_ERR_OOM, "pinned host allocation"));
     // ---- layout upload, Dp build, scan
-    if ((rc = upload_layout(s, 0, R - 1)) != TGA_OK) return bail(rc);
-    if ((rc = refresh(s, 0, R - 1, true)) != TGA_OK) return bail(rc);
+    if ((rc = upload_layout(s, true)) != TGA_OK) return bail(rc);
+    if ((rc = refresh(s, true)) != TGA_OK) return bail(rc);
     build_tiles(s);
     // ---- TMA descriptor over Dp: dims {pitch cols, pitch rows}, box {kBoxW, kBoxH}
     if (auto enc = get_encode()) {
@@ -661,7 +699,7 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
         DevState ds = make_devstate(s, s->keys);
         if (cudaMemcpyAsync(s->d_ds, &ds, sizeof(ds), cudaMemcpyHostToDevice, s->stream) != cudaSuccess ||
             cudaMemsetAsync(s->d_acc, 0, 48 * 8, s->stream) != cudaSuccess ||
-            cudaMemsetAsync(s->d_desc, 0, 8 * 4, s->stream) != cudaSuccess)
+            cudaMemsetAsync(s->d_desc, 0, 16 * 4, s->stream) != cudaSuccess)
             return bail(fail(TGA_ERR_CUDA, "device step state"));
         cudaError_t e2;
         if (I->dtype == TGA_I32) { auto a = scan_args<int32_t>(s); e2 = cudaMemcpyAsync(s->d_sa, &a, sizeof(a), cudaMemcpyHostToDevice, s->stream);
@@ -745,7 +783,8 @@ extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
         tga_shard_range(s->n_ftiles, s->shard, s->n_shards, &a, &b);
         const int f_lo = static_cast<int>(a), f_hi = static_cast<int>(b);
         // fused: inter tiles + the intra-route CVRP work in one launch (when there is inter work)
-        fused_intra = (mask & TGA_OP_INTER) && !I->tw && I->max_c_abs < (1 << 21);
+        static const bool no_fuse = std::getenv("TGA_NO_FUSE") != nullptr;  // tuning override
+        fused_intra = (mask & TGA_OP_INTER) && !I->tw && I->max_c_abs < (1 << 21) && !no_fuse;
         const uint32_t imask = fused_intra ? (mask & TGA_OP_INTRA) : 0u;
         e = launch_inter_fast(s->fastU, mask, s->rec, s->rectw, s->fmap, s->d_ftiles, f_lo, f_hi,
                               static_cast<uint32_t>(s->pitch), I->Q, s->keys, s->sm_count * 4, st,
@@ -942,11 +981,17 @@ extern "C" int32_t tga_apply_move(tga_solution *s, const tga_move *m) {
     if (!s->drained) TGA_CUDA(cudaStreamSynchronize(s->stream));  // staging buffers may still be in flight
     s->drained = false;
     if (!splice(s->routes, m)) return fail(TGA_ERR_INVALID_ARGUMENT, "move positions out of range for its variant");
-    compute_bases(s);
-    const int r_lo = std::min(m->route_a, m->route_b), r_hi = std::max(m->route_a, m->route_b);
+    const int ra = m->route_a, rb = m->route_b;
     int32_t rc;
-    if ((rc = upload_layout(s, r_lo, r_hi)) != TGA_OK) return rc;
-    if ((rc = refresh(s, r_lo, r_hi, false)) != TGA_OK) return rc;
+    if (route_fits(s, ra) && route_fits(s, rb)) {  // bases unchanged: refresh the two routes only
+        compute_cbase(s);
+        if ((rc = upload_layout(s, false, ra, rb)) != TGA_OK) return rc;
+        if ((rc = refresh(s, false, ra, rb)) != TGA_OK) return rc;
+    } else {                                        // a route outgrew its slots: full relayout
+        relayout_full(s);
+        if ((rc = upload_layout(s, true)) != TGA_OK) return rc;
+        if ((rc = refresh(s, true)) != TGA_OK) return rc;
+    }
     ++s->gen;
     return TGA_OK;
 }
@@ -1138,10 +1183,10 @@ extern "C" int32_t tga_solution_reload(tga_solution *s, int32_t R, const int32_t
     TGA_CUDA(cudaStreamSynchronize(s->stream));  // staging buffers may still be in flight
     s->host_stale = false;
     for (int r = 0; r < R; ++r) s->routes[r].assign(cust + ptr[r], cust + ptr[r + 1]);
-    compute_bases(s);
+    relayout_full(s);
     int32_t rc;
-    if ((rc = upload_layout(s, 0, R - 1)) != TGA_OK) return rc;
-    if ((rc = refresh(s, 0, R - 1, true)) != TGA_OK) return rc;
+    if ((rc = upload_layout(s, true)) != TGA_OK) return rc;
+    if ((rc = refresh(s, true)) != TGA_OK) return rc;
     ++s->gen;
     s->drained = false;
     return TGA_OK;

@@ -477,3 +477,34 @@ def test_vrptw_intra_warp_kernel_long_routes(mode):
     for s in (merged, G.perturb(merged, 20, 3)):
         assert sum(len(r) for r in s.routes) >= 16 * len(s.routes)
         check_exact(inst, s, INTRA_TW + INTER, mode, "tw-warp")
+
+
+@pytest.mark.parametrize("slack", [-1, 1, 5])
+def test_slack_layouts_lockstep(slack):
+    """Spare slots per route (0 = none, 1 = frequent relayouts, 5): host-driven
+    and device-resident descents follow the oracle's trajectory; keys equal a
+    fresh load after every few moves (the partial refresh touches only the two
+    changed routes unless one outgrows its slots)."""
+    _need_gpu()
+    inst, sol = G.x_like(12, n=160, target_routes=8)
+    orc = O.Oracle.from_instance(inst)
+    gi = T.Instance.from_gen(inst, slack=slack)
+    host = T.Solution(gi, sol)
+    dev = T.Solution(gi, sol)
+    routes = [list(r) for r in sol.routes]
+    for step in range(30):
+        ob = orc.best_over(routes, ALLV)
+        if ob is None or not ob.score < 0:
+            break
+        ok, mv = host.step(T.OP_ALL)
+        assert ok and (mv.variant, mv.u, mv.v, mv.delta_i) == (ob.variant, ob.u, ob.v, ob.score)
+        dev.step_async(T.OP_ALL)
+        routes = orc.apply(routes, ob.variant, ob.route_a, ob.pos_a, ob.route_b, ob.pos_b)
+        if step % 7 == 6:
+            assert host.routes() == routes and dev.routes() == routes
+            fresh = T.Solution(gi, routes)
+            for s in (host, dev, fresh):
+                s.eval(T.OP_ALL)
+            np.testing.assert_array_equal(host.keys(), fresh.keys())
+            np.testing.assert_array_equal(dev.keys(), fresh.keys())
+    assert dev.routes() == routes

@@ -286,21 +286,19 @@ __global__ void __launch_bounds__(256) k_scan(ScanArgs<DT> A, int r_lo, int r_hi
     scan_route<DT, TW>(A, r, lane);
 }
 
-// The update step of an applied move as work units: one unit per Dp row
-// of the changed slot ranges, ceil(Qp/8) units refreshing their Dp columns in 8
-// rows each, then one unit per 8 routes to re-scan (a full relayout refreshes
-// every row and re-scans every route).  The scan reads node ids and C, never
-// Dp: the roles are independent.
+// The update step of an applied move, phase 1: one unit per Dp row of
+// the changed slot ranges (a full C row gather each) and one unit per 8 routes
+// to re-scan (a full relayout refreshes every row and re-scans every route).
+// The scan reads node ids and C, never Dp: both roles run together.
 template <class DT, bool TW>
-__device__ __forceinline__ void update_units(const ScanArgs<DT> &A, DT *__restrict__ Dp, int pitch, int Qp, int R,
-                                             const UpdateSpec u, int unit0, int ustride) {
+__device__ __forceinline__ void update_rows(const ScanArgs<DT> &A, DT *__restrict__ Dp, int pitch, int R,
+                                            const UpdateSpec u, int unit0, int ustride) {
     const DT *__restrict__ C = A.C;
     const int n = A.n_nodes;
     const int n1 = u.hi1 - u.lo1, n2 = u.hi2 - u.lo2;
-    const int nb_rows = n1 + n2, nb_cols = u.full ? 0 : (Qp + 7) / 8;
+    const int nb_rows = n1 + n2;
     const int n_routes = u.full ? R : (u.r1 >= 0) + (u.r2 >= 0);
-    const int nb_scan = (n_routes + 7) / 8;
-    const int total = nb_rows + nb_cols + nb_scan;
+    const int total = nb_rows + (n_routes + 7) / 8;
     for (int b = unit0; b < total; b += ustride) {
         if (b < nb_rows) {
             const int a = b < n1 ? u.lo1 + b : u.lo2 + (b - n1);
@@ -312,19 +310,32 @@ __device__ __forceinline__ void update_units(const ScanArgs<DT> &A, DT *__restri
                     make_int4(bits(__ldg(crow + nd.x)), bits(__ldg(crow + nd.y)), bits(__ldg(crow + nd.z)),
                               bits(__ldg(crow + nd.w)));
             }
-        } else if (b < nb_rows + nb_cols) {
-            const int a = (b - nb_rows) * 8 + (threadIdx.x >> 5);
-            if (a < Qp) {
-                const DT *crow = C + static_cast<size_t>(A.node[a]) * n;
-                DT *drow = Dp + static_cast<size_t>(a) * pitch;
-                for (int j = (threadIdx.x & 31); j < n1 + n2; j += 32) {
-                    const int c = j < n1 ? u.lo1 + j : u.lo2 + (j - n1);
-                    drow[c] = __ldg(crow + A.node[c]);
-                }
-            }
         } else {
-            const int j = (b - nb_rows - nb_cols) * 8 + static_cast<int>(threadIdx.x >> 5);
+            const int j = (b - nb_rows) * 8 + static_cast<int>(threadIdx.x >> 5);
             if (j < n_routes) scan_route<DT, TW>(A, u.full ? j : (j == 0 && u.r1 >= 0 ? u.r1 : u.r2), threadIdx.x & 31);
+        }
+    }
+}
+
+// Phase 2 (after phase 1 completed): the columns of the changed ranges, from the
+// refreshed rows by symmetry, Dp[a][c] = Dp[c][a] (c is symmetric; host-checked).
+// A unit = 8 consecutive rows a (one per warp), lanes along c: the writes are
+// contiguous and the strided reads of 8 neighbouring a share their sectors --
+// instead of scattered 4-byte gathers from C (measured 105 MB of DRAM reads per
+// update at n = 10^4 before this).
+template <class DT>
+__device__ __forceinline__ void update_cols(DT *__restrict__ Dp, int pitch, int Qp, const UpdateSpec u, int unit0,
+                                            int ustride) {
+    if (u.full) return;  // every row was refreshed
+    const int n1 = u.hi1 - u.lo1, n2 = u.hi2 - u.lo2;
+    const int total = (Qp + 7) / 8;
+    for (int b = unit0; b < total; b += ustride) {
+        const int a = b * 8 + static_cast<int>(threadIdx.x >> 5);
+        if (a >= Qp) continue;
+        DT *drow = Dp + static_cast<size_t>(a) * pitch;
+        for (int j = (threadIdx.x & 31); j < n1 + n2; j += 32) {
+            const int c = j < n1 ? u.lo1 + j : u.lo2 + (j - n1);
+            drow[c] = Dp[static_cast<size_t>(c) * pitch + a];
         }
     }
 }
@@ -332,7 +343,11 @@ __device__ __forceinline__ void update_units(const ScanArgs<DT> &A, DT *__restri
 template <class DT, bool TW>
 __global__ void __launch_bounds__(256) k_update(ScanArgs<DT> A, DT *__restrict__ Dp, int pitch, int Qp, int R,
                                                 UpdateSpec u) {
-    update_units<DT, TW>(A, Dp, pitch, Qp, R, u, blockIdx.x, gridDim.x);
+    update_rows<DT, TW>(A, Dp, pitch, R, u, blockIdx.x, gridDim.x);
+}
+template <class DT>
+__global__ void __launch_bounds__(256) k_update_cols(DT *__restrict__ Dp, int pitch, int Qp, UpdateSpec u) {
+    update_cols<DT>(Dp, pitch, Qp, u, blockIdx.x, gridDim.x);
 }
 
 // Device-resident apply + update in ONE launch (blockIdx.y = solution): block 0
@@ -364,12 +379,17 @@ __global__ void __launch_bounds__(256) k_pick_update(const DevState *__restrict_
     const volatile int32_t *desc = S.desc;
     if (desc[0] == 0) return;
     const UpdateSpec u{desc[1], desc[2], desc[3], desc[4], desc[5], desc[6], desc[7]};
-    update_units<DT, TW>(scans[blockIdx.y], static_cast<DT *>(S.Dp), S.pitch, S.Qp, S.R, u, blockIdx.x, gridDim.x);
+    update_rows<DT, TW>(scans[blockIdx.y], static_cast<DT *>(S.Dp), S.pitch, S.R, u, blockIdx.x, gridDim.x);
+    if (u.full) return;
+    if (gridDim.x > 1) solution_barrier(S.desc + 8, gridDim.x);  // rows before the columns read them
+    else __syncthreads();
+    update_cols<DT>(static_cast<DT *>(S.Dp), S.pitch, S.Qp, u, blockIdx.x, gridDim.x);
 }
 
 cudaError_t launch_pick_update(const DevState *states, const void *scans, int n_sol, bool tw, bool is_int,
-                               uint32_t mask, int max_routes, int blocks_per_sol, cudaStream_t st) {
-    const int smem = 4 * (max_routes + 1) * 4;
+                               uint32_t mask, int max_routes, int max_cap, int blocks_per_sol, cudaStream_t st) {
+    // sb, sl, nb (3 x (R+1) ints) + the shared snapshot of the two changed routes
+    const int smem = 3 * (max_routes + 1) * 4 + 2 * max_cap * 4;
     dim3 g(blocks_per_sol, n_sol);
     if (smem > 48 * 1024) {
         cudaFuncSetAttribute(k_pick_update<int32_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1105,11 +1125,15 @@ template <class DT>
 cudaError_t launch_update(const ScanArgs<DT> &A, bool tw, DT *Dp, int pitch, int Qp, int R, const UpdateSpec &u,
                           cudaStream_t st) {
     const int n_routes = u.full ? R : (u.r1 >= 0) + (u.r2 >= 0);
-    const int grid = (u.hi1 - u.lo1) + (u.hi2 - u.lo2) + (u.full ? 0 : (Qp + 7) / 8) + (n_routes + 7) / 8;
+    const int grid = (u.hi1 - u.lo1) + (u.hi2 - u.lo2) + (n_routes + 7) / 8;
     if (grid <= 0) return cudaSuccess;
     if (tw) k_update<DT, true><<<grid, 256, 0, st>>>(A, Dp, pitch, Qp, R, u);
     else    k_update<DT, false><<<grid, 256, 0, st>>>(A, Dp, pitch, Qp, R, u);
     ++g_launches;
+    if (!u.full) {
+        k_update_cols<DT><<<(Qp + 7) / 8, 256, 0, st>>>(Dp, pitch, Qp, u);
+        ++g_launches;
+    }
     return cudaGetLastError();
 }
 template cudaError_t launch_update<int32_t>(const ScanArgs<int32_t> &, bool, int32_t *, int, int, int,

@@ -82,7 +82,7 @@ struct DevState {
     int32_t R, Qc, Qp, pitch, slack;
 };
 cudaError_t launch_pick_update(const DevState *states, const void *scans, int n_sol, bool tw, bool is_int,
-                               uint32_t mask, int max_routes, int blocks_per_sol, cudaStream_t st);
+                               uint32_t mask, int max_routes, int max_cap, int blocks_per_sol, cudaStream_t st);
 
 template <class DT>
 cudaError_t launch_dp(DT *Dp, int pitch, const int32_t *node, const DT *C, int n, int Qp, int lo, int hi,

@@ -119,7 +119,7 @@ __device__ __forceinline__ void pick_apply_body(const DevState &S, uint32_t mask
             c = (n1s[k] == n2s[k]) ? ordered / 2 : ordered;
         } else if (v <= 13) c = sums[v + 4];
         else c = sums[v + 4];
-        S.acc[v] += static_cast<unsigned long long>(c);
+        atomicAdd(S.acc + v, static_cast<unsigned long long>(c));  // fire-and-forget (RED)
     }
 
     // ---- 2. best key over the mask, decode, pieces of the new routes
@@ -149,8 +149,20 @@ __device__ __forceinline__ void pick_apply_body(const DevState &S, uint32_t mask
             const uint32_t idx = static_cast<uint32_t>(bk & 0xFFFFFFFFu);
             const int xu = static_cast<int>(idx / static_cast<uint32_t>(S.Qc));  // physical slots
             const int xv = static_cast<int>(idx % static_cast<uint32_t>(S.Qc));
-            const int ra = S.route[xu], pa = S.pos[xu];
-            const int rb = S.route[xv], pb = S.pos[xv];
+            // physical slot -> (route, position) from the staged bases (no global round trip)
+            auto rp = [&](int x, int &r, int &p) {
+                int a = 0, b = R - 1;
+                while (a < b) {
+                    const int m = (a + b + 1) >> 1;
+                    if (sb[m] <= x) a = m;
+                    else b = m - 1;
+                }
+                r = a;
+                p = x - sb[a];
+            };
+            int ra, pa, rb, pb;
+            rp(xu, ra, pa);
+            rp(xv, rb, pb);
             const int La = sl[ra], Lb = sl[rb];
             const int v = bv;
             NewRoute A{ra, 0, 0, {}}, B{rb, 0, 0, {}};
@@ -219,9 +231,23 @@ __device__ __forceinline__ void pick_apply_body(const DevState &S, uint32_t mask
         const Piece &pc = chg->p[k];
         return sb[pc.src] + (pc.rev ? pc.start + pc.len - 1 - off : pc.start + off);
     };
+    // old node id of an old slot: from the shared snapshot of the changed routes
+    // (fits case) or the global snapshot of the whole layout (relayout)
+    __shared__ int snap_off[2], snap_base[2], snap_n;
+    extern __shared__ int32_t smr_all[];
+    int32_t *snap = smr_all + 3 * (R + 1);  // after sb, sl, nb
+    auto old_node = [&](int os) -> int32_t {
+        if (full) return S.scratch[os];
+        for (int k = 0; k < snap_n; ++k) {
+            const int rel = os - snap_base[k];
+            if (rel >= 0 && rel < (k + 1 < snap_n ? snap_off[k + 1] : 1 << 30) - snap_off[k]) return snap[snap_off[k] + rel];
+        }
+        return 0;
+    };
     auto write_slot = [&](int x, int r, int p, int L, int span_lo) {
+        (void)span_lo;
         if (p <= L + 1) {
-            S.node[x] = (p >= 1 && p <= L) ? S.scratch[old_slot(r, p) - span_lo] : 0;
+            S.node[x] = (p >= 1 && p <= L) ? old_node(old_slot(r, p)) : 0;
             S.route[x] = r;
             S.pos[x] = p;
             S.rlen[x] = L;
@@ -235,10 +261,20 @@ __device__ __forceinline__ void pick_apply_body(const DevState &S, uint32_t mask
         }
     };
     if (!full) {
-        // ---- 3. snapshot the node ids between the two changed routes, rewrite just them
-        const int span_lo = sb[rlo], span_hi = sb[rhi + 1];
-        for (int x = span_lo + tid; x < span_hi; x += blockDim.x) S.scratch[x - span_lo] = S.node[x];
+        // ---- 3. snapshot the changed routes' old node ids in shared memory, rewrite just them
+        if (tid == 0) {
+            snap_n = nrt;
+            snap_off[0] = 0;
+            snap_base[0] = sb[nr[0].r];
+            if (nrt == 2) { snap_off[1] = sb[nr[0].r + 1] - sb[nr[0].r]; snap_base[1] = sb[nr[1].r]; }
+        }
         __syncthreads();
+        for (int k = 0; k < nrt; ++k) {
+            const int r = nr[k].r;
+            for (int x = sb[r] + tid; x < sb[r + 1]; x += blockDim.x) snap[snap_off[k] + x - sb[r]] = S.node[x];
+        }
+        __syncthreads();
+        const int span_lo = 0;
         for (int k = 0; k < nrt; ++k) {
             const int r = nr[k].r, L = nr[k].L;
             for (int x = sb[r] + tid; x < sb[r + 1]; x += blockDim.x) write_slot(x, r, x - sb[r], L, span_lo);
@@ -279,7 +315,7 @@ __device__ __forceinline__ void pick_apply_body(const DevState &S, uint32_t mask
     }
     if (tid == 0) {
         S.desc[0] = 1;
-        S.acc[23] += 1;
+        atomicAdd(S.acc + 23, 1ull);
     }
 }
 

@@ -1226,6 +1226,7 @@ extern "C" int32_t tga_step_async(tga_solution *s, uint32_t mask) {
     const tga_instance *I = s->inst;
     // pick + splice + update in one launch: one block per SM at most (grid barrier)
     cudaError_t e = launch_pick_update(s->d_ds, s->d_sa, 1, I->tw, I->dtype == TGA_I32, s->eval_mask, s->R,
+                                       s->N + 2 + s->slack,  // upper bound of any route's slot capacity
                                        s->sm_count, s->stream);
     if (e != cudaSuccess) return fail(TGA_ERR_CUDA, std::string("device step: ") + cudaGetErrorString(e));
     ++s->gen;
@@ -1502,6 +1503,7 @@ extern "C" int32_t tga_batch_step_async(tga_batch *b, uint32_t mask) {
     for (auto *s : b->sols) max_r = std::max(max_r, s->R);
     // blocks per solution so that the whole grid is co-resident (grid barrier)
     cudaError_t e = launch_pick_update(b->d_states, b->d_scans, n, I->tw, I->dtype == TGA_I32, b->eval_mask, max_r,
+                                       b->sols[0]->N + 2 + b->sols[0]->slack,
                                        std::max(1, b->sm_count * 2 / n), b->stream);
     if (e != cudaSuccess) return fail(TGA_ERR_CUDA, std::string("batch device step: ") + cudaGetErrorString(e));
     for (auto *s : b->sols) {

@@ -55,20 +55,22 @@ __device__ __forceinline__ void f_bulk(void *dst, const void *src, uint32_t byte
                  : "memory");
 }
 
-// running best of one (variant, direction) stream inside a tile: score + the
-// canonical id of the row slot; strict '<' keeps the first (lowest) row.
-struct Run {
-    int32_t s;
-    int32_t c;
-};
-__device__ __forceinline__ void keep(Run &b, bool feas, int32_t dD, int32_t c) {
-    const int32_t s = feas ? dD : INT_MAX;
-    if (s < b.s) { b.s = s; b.c = c; }
+// running best of one (variant, direction) stream inside a tile, packed in 32
+// bits: (score + 2^25) << 5 | row-in-tile.  The score of the integer fast path
+// is bounded by 8 * max c < 2^25 (host-checked: fast_ok), rows are < 32, so an
+// unsigned min keeps the lowest score and, among equal scores, the lowest row --
+// the lowest canonical index, since the column is fixed per lane (reading 5).
+// An infeasible candidate maps to 0xFFFFFFFF and never wins.
+__device__ __forceinline__ void keep(uint32_t &b, bool feas, int32_t dD, int row) {
+    const uint32_t k = (static_cast<uint32_t>(dD + (1 << 25)) << 5) | static_cast<uint32_t>(row);
+    b = min(b, feas ? k : 0xFFFFFFFFu);
 }
-__device__ __forceinline__ void fold(uint64_t &acc, const Run &b, bool direct, uint32_t cv, uint32_t Qc) {
-    if (b.s != INT_MAX) {
-        const uint32_t idx = direct ? static_cast<uint32_t>(b.c) * Qc + cv : cv * Qc + static_cast<uint32_t>(b.c);
-        acc = umin64(acc, pack_key(ord_score(b.s), idx));
+__device__ __forceinline__ void fold(uint64_t &acc, uint32_t b, bool direct, int u0, uint32_t v, uint32_t Qc) {
+    if (b != 0xFFFFFFFFu) {
+        const int32_t s = static_cast<int32_t>(b >> 5) - (1 << 25);
+        const uint32_t u = static_cast<uint32_t>(u0) + (b & 31u);
+        const uint32_t idx = direct ? u * Qc + v : v * Qc + u;
+        acc = umin64(acc, pack_key(ord_score(s), idx));
     }
 }
 }  // namespace
@@ -160,9 +162,9 @@ __global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__re
         // Dp(u0 + i + di, v + dj), i = row index in the tile
         auto D = [&](int i, int di, int dj) -> int32_t { return T[(i + 1 + di) * BW + (col + 4 + dj)]; };
 
-        Run run[16];
+        uint32_t run[16];
 #pragma unroll
-        for (int k = 0; k < 16; ++k) run[k] = Run{INT_MAX, 0};
+        for (int k = 0; k < 16; ++k) run[k] = 0xFFFFFFFFu;
 
 #pragma unroll
         for (int i = 0; i < U; ++i) {
@@ -186,7 +188,7 @@ __global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__re
                 bool ok = max(la, lb) <= cap;
                 if (TW) ok = ok & (AT.EF + static_cast<float>(d01) <= VT.LBN[0]) &
                              (VT.EF + static_cast<float>(d10) <= AT.LBN[0]);
-                keep(run[0], ok, dD, u);
+                keep(run[0], ok, dD, i);
             }
             // ---- relocate / or-opt, both directions                   (Eq. 13)
 #pragma unroll
@@ -196,11 +198,11 @@ __global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__re
                 const int32_t d1 = A.rem[N - 1] + d00 + dN1 + V.ne;  // seg(u) after v
                 bool ok1 = V.W + A.so[N - 1] <= cap;
                 if (TW) ok1 = ok1 & tw3(VT.EF, d00, AT.sTE[N - 1], AT.sTL[N - 1], AT.sTD[N - 1], dN1, VT.LBN[0]);
-                keep(run[2 * N - 1], ok1, d1, u);
+                keep(run[2 * N - 1], ok1, d1, i);
                 const int32_t d2 = V.rem[N - 1] + d00 + d1N + A.ne;  // seg(v) after u
                 bool ok2 = A.W + V.so[N - 1] <= cap;
                 if (TW) ok2 = ok2 & tw3(AT.EF, d00, VT.sTE[N - 1], VT.sTL[N - 1], VT.sTD[N - 1], d1N, AT.LBN[0]);
-                keep(run[2 * N], ok2, d2, u);
+                keep(run[2 * N], ok2, d2, i);
             }
             // ---- swap (1,1) / cross-exchange (N1,N2), N1 <= N2
 #pragma unroll
@@ -217,7 +219,7 @@ __global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__re
                     if (TW)  // A' = F(u-1) + S(v,N2) + B(u+N1),  B' = F(v-1) + S(u,N1) + B(v+N2)
                         ok = ok & tw3(AT.EFm, a, VT.sTE[N2 - 1], VT.sTL[N2 - 1], VT.sTD[N2 - 1], bq, AT.LBN[N1 - 1]) &
                              tw3(VT.EFm, c, AT.sTE[N1 - 1], AT.sTL[N1 - 1], AT.sTD[N1 - 1], dq, VT.LBN[N2 - 1]);
-                    keep(run[slot[sv]], ok, dD, u);
+                    keep(run[slot[sv]], ok, dD, i);
                 }
                 if (N1 != N2) {   // N1-segment at v, N2-segment at u
                     const int32_t c = D(i, 0, -1), bq = D(i, N2 - 1, N1), a = D(i, -1, 0), dq = D(i, N2, N1 - 1);
@@ -227,26 +229,26 @@ __global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__re
                     if (TW)  // B' = F(v-1) + S(u,N2) + B(v+N1),  A' = F(u-1) + S(v,N1) + B(u+N2)
                         ok = ok & tw3(VT.EFm, c, AT.sTE[N2 - 1], AT.sTL[N2 - 1], AT.sTD[N2 - 1], bq, VT.LBN[N1 - 1]) &
                              tw3(AT.EFm, a, VT.sTE[N1 - 1], VT.sTL[N1 - 1], VT.sTD[N1 - 1], dq, AT.LBN[N2 - 1]);
-                    keep(run[slot[sv] + 1], ok, dD, u);
+                    keep(run[slot[sv] + 1], ok, dD, i);
                 }
             }
         }
         // ---- fold this tile's streams into the per-variant 64-bit keys
         if (V.c >= 0) {
             const uint32_t cv = static_cast<uint32_t>(v);  // physical column slot
-            if (MASK & (1u << 1)) fold(acc[1], run[0], true, cv, Qc);
+            if (MASK & (1u << 1)) fold(acc[1], run[0], true, u0, cv, Qc);
 #pragma unroll
             for (int N = 1; N <= 3; ++N) {
                 if (!(MASK & (1u << (1 + N)))) continue;
-                fold(acc[1 + N], run[2 * N - 1], true, cv, Qc);
-                fold(acc[1 + N], run[2 * N], false, cv, Qc);
+                fold(acc[1 + N], run[2 * N - 1], true, u0, cv, Qc);
+                fold(acc[1 + N], run[2 * N], false, u0, cv, Qc);
             }
-            if (MASK & (1u << 5)) fold(acc[5], run[7], true, cv, Qc);
-            if (MASK & (1u << 6)) { fold(acc[6], run[8], true, cv, Qc); fold(acc[6], run[9], false, cv, Qc); }
-            if (MASK & (1u << 7)) { fold(acc[7], run[10], true, cv, Qc); fold(acc[7], run[11], false, cv, Qc); }
-            if (MASK & (1u << 8)) fold(acc[8], run[12], true, cv, Qc);
-            if (MASK & (1u << 9)) { fold(acc[9], run[13], true, cv, Qc); fold(acc[9], run[14], false, cv, Qc); }
-            if (MASK & (1u << 10)) fold(acc[10], run[15], true, cv, Qc);
+            if (MASK & (1u << 5)) fold(acc[5], run[7], true, u0, cv, Qc);
+            if (MASK & (1u << 6)) { fold(acc[6], run[8], true, u0, cv, Qc); fold(acc[6], run[9], false, u0, cv, Qc); }
+            if (MASK & (1u << 7)) { fold(acc[7], run[10], true, u0, cv, Qc); fold(acc[7], run[11], false, u0, cv, Qc); }
+            if (MASK & (1u << 8)) fold(acc[8], run[12], true, u0, cv, Qc);
+            if (MASK & (1u << 9)) { fold(acc[9], run[13], true, u0, cv, Qc); fold(acc[9], run[14], false, u0, cv, Qc); }
+            if (MASK & (1u << 10)) fold(acc[10], run[15], true, u0, cv, Qc);
         }
         __syncthreads();  // buffer b is refilled two iterations later
     }

@@ -479,8 +479,8 @@ extern "C" int32_t tga_instance_create(int32_t n, const void *dist, int32_t dtyp
     {
         int64_t tot = 0;
         for (int i = 0; i < n; ++i) tot += demand[i];
-        I->fast_ok = tot < (kPoison >> 2) && capacity < (kPoison >> 2) &&
-                     static_cast<int64_t>(max_abs) * 16 < (1ll << 30);
+        // poisoned loads stay below 2^31; |delta| <= 8 max c < 2^25 fits the packed 32-bit keys
+        I->fast_ok = tot < (kPoison >> 2) && capacity < (kPoison >> 2) && max_abs < (1 << 21);
     }
     if (opt) I->opt = *opt;
     else { I->opt.score_mode = TGA_SCORE_FEASIBLE; I->opt.w_load = 10; I->opt.w_tw = 10; I->opt.device = -1; }

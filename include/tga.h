@@ -200,6 +200,9 @@ int32_t tga_step(tga_solution *sol, uint32_t op_mask, tga_move *out);
  * in the slot arrays, then the update kernel (bounds read on the device).
  * Enqueue-only; steps can be issued back to back (or captured in a CUDA
  * graph).  Host-side queries resynchronise the host route lists lazily.
+ * The step consumes the keys (resets them to ~0 on the device), so the next
+ * tga_eval enqueues no reset of its own; tga_solution_keys after a step
+ * returns ~0 for every variant until the next tga_eval.
  * tga_solution_device_stats returns and clears the candidate counts per
  * variant accumulated by device steps (counts[TGA_N_VARIANTS]) and the number
  * of moves they applied (synchronises). */
@@ -296,6 +299,12 @@ int32_t tga_batch_set_stream(tga_batch *batch, void *cuda_stream);
 /* device-resident steps of every solution of the batch (see tga_step_async) */
 int32_t tga_batch_step_async(tga_batch *batch, uint32_t op_mask);
 int32_t tga_batch_device_stats(tga_batch *batch, uint64_t *counts, uint64_t *applied);
+
+/* Diagnostics: phase probe of the device-resident step.  enable != 0 makes the
+ * next pick/update launches record the SM cycle counter (clock64 of block 0)
+ * at 8 phase points; out[16] (may be NULL) receives the last record
+ * (synchronises).  Not used on any timed path. */
+int32_t tga_solution_debug_probe(tga_solution *sol, int32_t enable, uint64_t *out);
 
 /* ------------------------------------------------------------ misc */
 const char *tga_last_error(void);

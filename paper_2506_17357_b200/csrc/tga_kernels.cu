@@ -52,15 +52,17 @@ __global__ void __launch_bounds__(256) k_dp_cols(DT *__restrict__ Dp, int pitch,
 // ============================================================== attribute rebuild scan
 // One warp per route; chunks of 32 positions with carries.  Positions
 // k = 0..L+1 of route r live at physical slots base..base+L+1.
-template <class DT, bool TW>
-__device__ __forceinline__ void scan_route(const ScanArgs<DT> &A, const int r, const int lane) {
-    const int base = A.rbase[r];
-    const int L = A.rlenR[r];
+// NodeF(x) / CanonF(x): node id / canonical-validity of slot x of this route
+// (global arrays for a plain rebuild; the decoded new route in the device step,
+// whose slot arrays are rewritten concurrently).  base, L, cap: the route's first
+// physical slot, customer count and slot capacity.
+template <class DT, bool TW, class NodeF, class CanonF>
+__device__ __forceinline__ void scan_route_g(const ScanArgs<DT> &A, const int r, const int lane, const int base,
+                                             const int L, const int cap, NodeF nodeAt, CanonF canonAt) {
     const int len = L + 2;
     const int n = A.n_nodes;
     if constexpr (std::is_same<DT, int32_t>::value) {
         // spare (hole) slots of the route carry poisoned fast-path records
-        const int cap = A.rbase[r + 1] - base;
         for (int k = len + lane; k < cap; k += 32) {
             if (A.rec) {
                 SlotRec q{};
@@ -86,9 +88,9 @@ __device__ __forceinline__ void scan_route(const ScanArgs<DT> &A, const int r, c
         const int k = c0 + lane;
         const bool in = k < len;
         const int x = base + k;
-        const int nd = in ? A.node[x] : 0;
+        const int nd = in ? nodeAt(x) : 0;
         const bool has_next = in && (k + 1 < len);
-        const int nn = has_next ? A.node[x + 1] : 0;
+        const int nn = has_next ? nodeAt(x + 1) : 0;
         const DT e = has_next ? A.C[static_cast<size_t>(nd) * n + nn] : DT(0);
         // loads (Eq. 3e-f): inclusive prefix sum
         int sL = in ? A.demand[nd] : 0;
@@ -153,7 +155,7 @@ __device__ __forceinline__ void scan_route(const ScanArgs<DT> &A, const int r, c
         const int k = c0 + lane;
         const bool in = lane < nvalid;
         const int x = base + k;
-        const int nd = in ? A.node[x] : 0;
+        const int nd = in ? nodeAt(x) : 0;
         const DT e = in ? A.enext[x] : DT(0);  // written by the forward pass (same warp)
         int sL = in ? A.demand[nd] : 0;
         DT sD = e;
@@ -204,21 +206,21 @@ __device__ __forceinline__ void scan_route(const ScanArgs<DT> &A, const int r, c
         const int x = base + k;
         // bridge_N[x] = c(x-1, x+N): the edge that closes the gap left by removing
         // the segment x..x+N-1 (relocate / or-opt removal, Eq. 2)
-        const int np = (k >= 1) ? A.node[x - 1] : 0;
+        const int np = (k >= 1) ? nodeAt(x - 1) : 0;
         DT b1 = DT(0), b2 = DT(0), b3 = DT(0);
-        if (k >= 1 && k + 1 <= len - 1) b1 = A.C[static_cast<size_t>(np) * n + A.node[x + 1]];
-        if (k >= 1 && k + 2 <= len - 1) b2 = A.C[static_cast<size_t>(np) * n + A.node[x + 2]];
-        if (k >= 1 && k + 3 <= len - 1) b3 = A.C[static_cast<size_t>(np) * n + A.node[x + 3]];
+        if (k >= 1 && k + 1 <= len - 1) b1 = A.C[static_cast<size_t>(np) * n + nodeAt(x + 1)];
+        if (k >= 1 && k + 2 <= len - 1) b2 = A.C[static_cast<size_t>(np) * n + nodeAt(x + 2)];
+        if (k >= 1 && k + 3 <= len - 1) b3 = A.C[static_cast<size_t>(np) * n + nodeAt(x + 3)];
         A.bridge1[x] = b1;
         A.bridge2[x] = b2;
         A.bridge3[x] = b3;
         if (TW) {
-            const TwRec s1 = A.node_tw[A.node[x]];
+            const TwRec s1 = A.node_tw[nodeAt(x)];
             TwRec s2 = s1, s3 = s1;
             if (k + 1 < len) {
-                s2 = tw_cat(s1, A.node_tw[A.node[x + 1]], static_cast<float>(A.enext[x]));
+                s2 = tw_cat(s1, A.node_tw[nodeAt(x + 1)], static_cast<float>(A.enext[x]));
                 s3 = s2;
-                if (k + 2 < len) s3 = tw_cat(s2, A.node_tw[A.node[x + 2]], static_cast<float>(A.enext[x + 1]));
+                if (k + 2 < len) s3 = tw_cat(s2, A.node_tw[nodeAt(x + 2)], static_cast<float>(A.enext[x + 1]));
             }
             A.seg2T[x] = s2;
             A.seg3T[x] = s3;
@@ -229,7 +231,7 @@ __device__ __forceinline__ void scan_route(const ScanArgs<DT> &A, const int r, c
                 const bool slot = k <= L;  // canonical slot (not the end depot)
                 const int32_t e_x = A.enext[x], e_prev = (k >= 1) ? A.enext[x - 1] : 0;
                 const int32_t fl_prev = (k >= 1) ? A.fwdL[x - 1] : 0;
-                q.c = slot ? A.canon[x] : -1;
+                q.c = slot ? canonAt(x) : -1;
                 q.r = r;
                 q.fL = slot ? A.fwdL[x] : kPoison;
                 q.bL1 = (slot && k + 1 < len) ? A.bwdL[x + 1] : kPoison;
@@ -243,7 +245,7 @@ __device__ __forceinline__ void scan_route(const ScanArgs<DT> &A, const int r, c
                 if (TW && A.rectw) {
                     w.EF = EFof(x);
                     w.EFm = (k >= 1) ? EFof(x - 1) : kTwBig;
-                    const TwRec s1 = A.node_tw[A.node[x]];
+                    const TwRec s1 = A.node_tw[nodeAt(x)];
                     const TwRec sg[3] = {s1, A.seg2T[x], A.seg3T[x]};
 #pragma unroll
                     for (int N = 1; N <= 3; ++N) {
@@ -276,6 +278,13 @@ __device__ __forceinline__ void scan_route(const ScanArgs<DT> &A, const int r, c
             }
         }
     }
+}
+
+template <class DT, bool TW>
+__device__ __forceinline__ void scan_route(const ScanArgs<DT> &A, const int r, const int lane) {
+    const int base = A.rbase[r];
+    scan_route_g<DT, TW>(A, r, lane, base, A.rlenR[r], A.rbase[r + 1] - base,
+                         [&](int x) { return A.node[x]; }, [&](int x) { return A.canon[x]; });
 }
 
 template <class DT, bool TW>
@@ -367,29 +376,213 @@ __device__ __forceinline__ void solution_barrier(int32_t *counter, int nblocks) 
     __syncthreads();
 }
 
+// Multi-block device step (the Update step of §5.3.5,
+// P:437) with no grid barrier between the pick and the update: every block
+// decodes the best move itself (decode_best, a warp of key compares and one
+// binary search), snapshots the OLD node ids of the 1-2 changed routes into its
+// shared memory, and signals arrival; only then may block 0 rewrite the slot
+// arrays (it waits for every arrival, which happen early).  New node ids come
+// from the snapshot through the pieces, so the Dp rows, the changed columns and
+// the re-scans of the changed routes all run at once.  Columns are gathered
+// straight from C while Qp is small; above that they are copied from the
+// refreshed rows by symmetry behind one barrier (C rows would miss L2).
+// A route that outgrew its slots takes the full relayout path of pick_apply_body.
+constexpr int kDirectColsQp = 2560;
+
+__device__ __forceinline__ void block_arrive(int32_t *counter) {
+    if (threadIdx.x == 0) atomicAdd(counter, 1);
+}
+__device__ __forceinline__ void wait_arrivals(int32_t *counter, int v_own, int nblocks) {
+    // v_own: this block's own atomicAdd return; launches of one stream never overlap
+    const int target = (v_own / nblocks + 1) * nblocks;
+    // the arrivals follow the snapshot loads in each block (program order); no fence needed
+    while (*reinterpret_cast<volatile int32_t *>(counter) < target) __nanosleep(32);
+}
+
+template <class DT, bool TW>
+__device__ __forceinline__ void pick_update_multi(const DevState &S, const ScanArgs<DT> &A, uint32_t mask, int integer,
+                                                  int32_t *smr, int snap_cap, unsigned long long *pr) {
+    const int tid = threadIdx.x, R = S.R, G = gridDim.x, b = blockIdx.x;
+    int32_t *sb = smr, *sl = smr + (R + 1);
+    int32_t *snap = smr + 2 * (R + 1);  // old node ids of the changed ranges
+    int32_t *nn = snap + snap_cap;      // new node ids of the changed ranges
+    __shared__ uint64_t skeys[23];
+    __shared__ Decoded dm;
+    __shared__ int arrive_v;
+    // ---- 1. stage the old route bases / lengths and the keys; decode (every block)
+    for (int r = tid; r <= R; r += blockDim.x) {
+        sb[r] = S.rbase[r];
+        sl[r] = r < R ? S.rlenR[r] : 0;
+    }
+    if (tid < 23) skeys[tid] = S.keys[tid];
+    __syncthreads();
+    if (tid == 0) probe(pr, 1);
+    if (tid < 32) decode_best(skeys, mask, integer, sb, sl, R, S.Qc, dm);
+    __syncthreads();
+    if (tid == 0) probe(pr, 2);
+    const int n1 = dm.applied && !dm.full ? dm.hi[0] - dm.lo[0] : 0;
+    const int n2 = dm.applied && !dm.full ? dm.hi[1] - dm.lo[1] : 0;
+    const int lo0 = dm.lo[0], lo1 = dm.lo[1];
+    // ---- 2. snapshot the old node ids (fits case), then arrive
+    for (int j = tid; j < n1 + n2; j += blockDim.x) snap[j] = S.node[j < n1 ? lo0 + j : lo1 + (j - n1)];
+    __syncthreads();
+    if (tid == 0) arrive_v = atomicAdd(S.desc + 9, 1);
+    if (b == G - 1) neighbourhood_counts(S, mask, sl);  // the evaluated (old) lengths
+    if (!dm.applied) {
+        if (b == 0 && tid == 0) {
+            S.desc[0] = 0;
+            wait_arrivals(S.desc + 9, arrive_v, G);  // every block has read the keys
+            for (int v = 0; v < 23; ++v) S.keys[v] = ~0ull;  // consumed: the next eval needs no memset
+        }
+        return;
+    }
+    if (dm.full) {  // relayout: block 0 alone rewrites every slot after all blocks staged
+        __syncthreads();
+        if (b == 0) {
+            if (tid == 0) wait_arrivals(S.desc + 9, arrive_v, G);
+            __syncthreads();
+            pick_apply_body(S, mask, integer, smr, pr, false);  // resets the keys too
+        }
+        solution_barrier(S.desc + 8, G);
+        const volatile int32_t *desc = S.desc;
+        const UpdateSpec u{desc[1], desc[2], desc[3], desc[4], desc[5], desc[6], desc[7]};
+        update_rows<DT, TW>(A, static_cast<DT *>(S.Dp), S.pitch, R, u, b, G);
+        return;
+    }
+    if (tid == 0) probe(pr, 3);
+    // ---- 3. new node ids of the changed ranges (start / end depot and spare slots: 0)
+    auto old_of = [&](int os) -> int32_t { return (os >= lo0 && os < lo0 + n1) ? snap[os - lo0] : snap[n1 + os - lo1]; };
+    for (int j = tid; j < n1 + n2; j += blockDim.x) {
+        const int q = j < n1 ? 0 : 1;
+        const NewRoute &nr = dm.nr[q];
+        const int p = j - (q ? n1 : 0);  // position in the route (base == lo[q])
+        int32_t nd = 0;
+        if (p >= 1 && p <= nr.L) {
+            int off = p - 1, k = 0;
+            while (off >= nr.p[k].len) { off -= nr.p[k].len; ++k; }
+            const Piece &pc = nr.p[k];
+            nd = old_of(sb[pc.src] + (pc.rev ? pc.start + pc.len - 1 - off : pc.start + off));
+        }
+        nn[j] = nd;
+    }
+    __syncthreads();
+    if (tid == 0) probe(pr, 4);
+    auto in_chg = [&](int c) -> int { return (c >= lo0 && c < lo0 + n1) ? c - lo0 : ((c >= lo1 && c < lo1 + n2) ? n1 + c - lo1 : -1); };
+    const DT *__restrict__ C = A.C;
+    const int n = A.n_nodes, pitch = S.pitch, Qp = S.Qp;
+    DT *__restrict__ Dp = static_cast<DT *>(S.Dp);
+    // ---- 4a. re-scan of the changed routes: warp 0 of blocks 1 and 2 (the longest chains first)
+    for (int q = 0; q < dm.nrt; ++q) {
+        if (b == (1 + q) % G && tid < 32) {
+            const int r = dm.nr[q].r, base = dm.lo[q], off = q ? n1 : 0;
+            scan_route_g<DT, TW>(A, r, tid, base, dm.nr[q].L, dm.hi[q] - base,
+                                 [&](int x) { return nn[off + x - base]; }, [&](int x) { return x; });
+        }
+    }
+    // ---- 4b. Dp rows of the changed slots: Dp[a][c] = c(new node(a), node(c)), c < pitch
+    for (int j = b; j < n1 + n2; j += G) {
+        const int a = j < n1 ? lo0 + j : lo1 + (j - n1);
+        const DT *crow = C + static_cast<size_t>(nn[j]) * n;
+        DT *drow = Dp + static_cast<size_t>(a) * pitch;
+        for (int c = 4 * tid; c < pitch; c += 4 * blockDim.x) {
+            int4 nd = *reinterpret_cast<const int4 *>(S.node + c);
+            int t;
+            if ((t = in_chg(c)) >= 0) nd.x = nn[t];
+            if ((t = in_chg(c + 1)) >= 0) nd.y = nn[t];
+            if ((t = in_chg(c + 2)) >= 0) nd.z = nn[t];
+            if ((t = in_chg(c + 3)) >= 0) nd.w = nn[t];
+            *reinterpret_cast<int4 *>(drow + c) = make_int4(bits(__ldg(crow + nd.x)), bits(__ldg(crow + nd.y)),
+                                                           bits(__ldg(crow + nd.z)), bits(__ldg(crow + nd.w)));
+        }
+    }
+    // ---- 4c. columns of the changed slots in every other row
+    if (Qp <= kDirectColsQp) {
+        const int warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
+        for (int a = b * nw + warp; a < Qp; a += G * nw) {
+            if (in_chg(a) >= 0) continue;  // a changed row: written whole above
+            const DT *crow = C + static_cast<size_t>(S.node[a]) * n;
+            DT *drow = Dp + static_cast<size_t>(a) * pitch;
+            for (int j = lane; j < n1 + n2; j += 32) drow[j < n1 ? lo0 + j : lo1 + (j - n1)] = __ldg(crow + nn[j]);
+        }
+    }
+    if (tid == 0) probe(pr, 5);
+    // ---- 5. block 0: the slot arrays of the changed routes, once every block has its snapshot
+    if (b == 0) {
+        if (tid == 0) wait_arrivals(S.desc + 9, arrive_v, G);
+        __syncthreads();
+        for (int j = tid; j < n1 + n2; j += blockDim.x) {
+            const int q = j < n1 ? 0 : 1;
+            const int x = j < n1 ? lo0 + j : lo1 + (j - n1);
+            const int p = j - (q ? n1 : 0), L = dm.nr[q].L, r = dm.nr[q].r;
+            const bool live = p <= L + 1;
+            S.node[x] = nn[j];
+            S.route[x] = live ? r : -1;
+            S.pos[x] = live ? p : 0;
+            S.rlen[x] = live ? L : -1;
+            S.canon[x] = p <= L ? x : -1;  // validity only (keys index physical slots)
+        }
+        if (tid < dm.nrt) S.rlenR[dm.nr[tid].r] = dm.nr[tid].L;
+        if (tid < 23) S.keys[tid] = ~0ull;  // consumed: the next eval needs no memset
+        if (tid == 0) {
+            const int rlo = dm.nr[0].r, rhi = dm.nrt == 2 ? dm.nr[1].r : -1;
+            S.desc[1] = lo0; S.desc[2] = lo0 + n1; S.desc[3] = dm.nrt == 2 ? lo1 : 0; S.desc[4] = dm.nrt == 2 ? lo1 + n2 : 0;
+            S.desc[5] = rlo; S.desc[6] = rhi; S.desc[7] = 0;
+            S.desc[0] = 1;
+            atomicAdd(S.acc + 23, 1ull);
+        }
+    }
+    if (Qp > kDirectColsQp) {
+        solution_barrier(S.desc + 8, G);  // every changed row is written before the columns copy it
+        if (tid == 0) probe(pr, 6);
+        const UpdateSpec u{lo0, lo0 + n1, dm.nrt == 2 ? lo1 : 0, dm.nrt == 2 ? lo1 + n2 : 0, dm.nr[0].r,
+                           dm.nrt == 2 ? dm.nr[1].r : -1, 0};
+        update_cols<DT>(Dp, pitch, Qp, u, b, G);
+    }
+    __syncthreads();
+    if (tid == 0) probe(pr, 7);
+}
+
 template <class DT, bool TW>
 __global__ void __launch_bounds__(256) k_pick_update(const DevState *__restrict__ states,
                                                      const ScanArgs<DT> *__restrict__ scans, uint32_t mask,
-                                                     int integer) {
+                                                     int integer, int snap_cap) {
     extern __shared__ int32_t smr[];
     const DevState &S = states[blockIdx.y];
-    if (blockIdx.x == 0) pick_apply_body(S, mask, integer, smr);
+    unsigned long long *pr = (blockIdx.x == 0 && threadIdx.x == 0 && S.acc[31]) ? S.acc + 32 : nullptr;
+    probe(pr, 0);
+    if (snap_cap > 0 && gridDim.x > 1) {
+        pick_update_multi<DT, TW>(S, scans[blockIdx.y], mask, integer, smr, snap_cap, pr);
+        return;
+    }
+    // one block per solution (population batches), or the shared memory cannot
+    // hold the snapshot: block 0 picks and splices, grid barrier, update
+    if (blockIdx.x == 0) pick_apply_body(S, mask, integer, smr, pr);
     if (gridDim.x > 1) solution_barrier(S.desc + 8, gridDim.x);
     else __syncthreads();
+    probe(pr, 4);
     const volatile int32_t *desc = S.desc;
     if (desc[0] == 0) return;
     const UpdateSpec u{desc[1], desc[2], desc[3], desc[4], desc[5], desc[6], desc[7]};
     update_rows<DT, TW>(scans[blockIdx.y], static_cast<DT *>(S.Dp), S.pitch, S.R, u, blockIdx.x, gridDim.x);
+    probe(pr, 5);
     if (u.full) return;
     if (gridDim.x > 1) solution_barrier(S.desc + 8, gridDim.x);  // rows before the columns read them
     else __syncthreads();
+    probe(pr, 6);
     update_cols<DT>(static_cast<DT *>(S.Dp), S.pitch, S.Qp, u, blockIdx.x, gridDim.x);
+    __syncthreads();
+    probe(pr, 7);
 }
 
 cudaError_t launch_pick_update(const DevState *states, const void *scans, int n_sol, bool tw, bool is_int,
                                uint32_t mask, int max_routes, int max_cap, int blocks_per_sol, cudaStream_t st) {
-    // sb, sl, nb (3 x (R+1) ints) + the shared snapshot of the two changed routes
-    const int smem = 3 * (max_routes + 1) * 4 + 2 * max_cap * 4;
+    // old path: sb, sl, nb (3 x (R+1) ints) + the shared snapshot of the two changed routes;
+    // multi-block path: sb, sl + old and new node ids of the two changed routes
+    const int smem_old = 3 * (max_routes + 1) * 4 + 2 * max_cap * 4;
+    const int smem_multi = 2 * (max_routes + 1) * 4 + 4 * max_cap * 4;
+    const bool multi = blocks_per_sol > 1 && smem_multi <= 200 * 1024;
+    const int smem = multi ? std::max(smem_old, smem_multi) : smem_old;
+    const int snap_cap = multi ? 2 * max_cap : 0;
     dim3 g(blocks_per_sol, n_sol);
     if (smem > 48 * 1024) {
         cudaFuncSetAttribute(k_pick_update<int32_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -398,11 +591,11 @@ cudaError_t launch_pick_update(const DevState *states, const void *scans, int n_
         cudaFuncSetAttribute(k_pick_update<float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     }
     if (is_int) {
-        if (tw) k_pick_update<int32_t, true><<<g, 256, smem, st>>>(states, static_cast<const ScanArgs<int32_t> *>(scans), mask, 1);
-        else    k_pick_update<int32_t, false><<<g, 256, smem, st>>>(states, static_cast<const ScanArgs<int32_t> *>(scans), mask, 1);
+        if (tw) k_pick_update<int32_t, true><<<g, 256, smem, st>>>(states, static_cast<const ScanArgs<int32_t> *>(scans), mask, 1, snap_cap);
+        else    k_pick_update<int32_t, false><<<g, 256, smem, st>>>(states, static_cast<const ScanArgs<int32_t> *>(scans), mask, 1, snap_cap);
     } else {
-        if (tw) k_pick_update<float, true><<<g, 256, smem, st>>>(states, static_cast<const ScanArgs<float> *>(scans), mask, 0);
-        else    k_pick_update<float, false><<<g, 256, smem, st>>>(states, static_cast<const ScanArgs<float> *>(scans), mask, 0);
+        if (tw) k_pick_update<float, true><<<g, 256, smem, st>>>(states, static_cast<const ScanArgs<float> *>(scans), mask, 0, snap_cap);
+        else    k_pick_update<float, false><<<g, 256, smem, st>>>(states, static_cast<const ScanArgs<float> *>(scans), mask, 0, snap_cap);
     }
     note_launch();
     return cudaGetLastError();

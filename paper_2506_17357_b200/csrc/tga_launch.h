@@ -75,7 +75,7 @@ struct DevState {
     int32_t *node, *route, *pos, *rlen, *canon;   // slot arrays (guarded)
     int32_t *rbase, *rlenR, *cbase;              // per route
     int32_t *scratch;                            // snapshot of a changed span (cap ints)
-    const uint64_t *keys;                        // 23 packed keys of the last evaluation
+    uint64_t *keys;                              // 23 packed keys of the last evaluation (reset to ~0 once consumed)
     int32_t *desc;                               // [0] applied, [1..7] UpdateSpec, [8] grid-barrier counter
     unsigned long long *acc;                     // [23] candidate counts + [23] applied moves
     void *Dp;

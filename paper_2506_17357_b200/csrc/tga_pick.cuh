@@ -49,20 +49,17 @@ __device__ __forceinline__ int64_t pz(int64_t x) { return x > 0 ? x : 0; }
 }  // namespace pick
 using namespace pick;
 
-// ------------------------------------------------------------------ pick + apply
-// Route arrays (base, length, canonical base) are staged in shared memory so the
-// serial parts (decode, binary searches over routes) never wait on global loads.
-__device__ __forceinline__ void pick_apply_body(const DevState &S, uint32_t mask, int integer, int32_t *smr) {
+// phase probe (diagnostics): clock64 of block 0 at phase k into acc[32 + k] when acc[31] != 0
+__device__ __forceinline__ void probe(unsigned long long *pr, int k) {
+    if (pr) pr[k] = static_cast<unsigned long long>(clock64());
+}
+
+// Exact candidate counts of the evaluated neighbourhood (closed forms over the
+// route lengths sl[0..R-1] staged in shared memory), added to acc[0..22].
+// Block-wide (every thread must call it).
+__device__ __forceinline__ void neighbourhood_counts(const DevState &S, uint32_t mask, const int32_t *sl) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int R = S.R;
-    int32_t *sb = smr, *sl = smr + (R + 1), *nb = smr + 2 * (R + 1);  // old bases, old lengths, new bases
-    for (int r = tid; r <= R; r += blockDim.x) {
-        sb[r] = S.rbase[r];
-        sl[r] = r < R ? S.rlenR[r] : 0;
-    }
-    __shared__ uint64_t skeys[23];
-    if (tid < 23) skeys[tid] = S.keys[tid];
-    // ---- 1. exact candidate counts of the evaluated neighbourhood (closed forms)
     constexpr int NS = 27;
     __shared__ long long wsum[8][NS];
     __syncthreads();
@@ -104,7 +101,6 @@ __device__ __forceinline__ void pick_apply_body(const DevState &S, uint32_t mask
         for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) v += wsum[w][tid];
         sums[tid] = v;
     }
-    __syncthreads();
     if (tid < 23 && (mask & (1u << tid))) {  // one variant per thread
         const long long S1 = sums[0], S2 = sums[1];
         const int v = tid;
@@ -121,7 +117,133 @@ __device__ __forceinline__ void pick_apply_body(const DevState &S, uint32_t mask
         else c = sums[v + 4];
         atomicAdd(S.acc + v, static_cast<unsigned long long>(c));  // fire-and-forget (RED)
     }
+}
 
+
+// ------------------------------------------------------------------ redundant decode
+// The best move decoded by one warp of EVERY block of the multi-block step (no
+// barrier before the update work): lowest (score, variant) over the evaluated
+// keys (Eq. 16c, reading 5), improving iff score < 0, the 1-2 new routes as
+// pieces of old routes.  sb / sl = old route bases / lengths in shared memory.
+struct Decoded {
+    int applied, full, nrt;  // move applied?  changed route outgrew its slots?  #routes changed
+    NewRoute nr[2];          // nr[0] = lower route index
+    int lo[2], hi[2];        // old (== new) slot ranges of the changed routes
+};
+
+__device__ __forceinline__ void decode_best(const uint64_t *__restrict__ keys, uint32_t mask, int integer,
+                                            const int32_t *sb, const int32_t *sl, int R, int Qc, Decoded &dm) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t k = (lane < 23 && ((mask >> lane) & 1u)) ? keys[lane] : ~0ull;
+    const bool valid = k != ~0ull;
+    const uint32_t hi = valid ? static_cast<uint32_t>(k >> 32) : 0xFFFFFFFFu;
+    const uint32_t mhi = __reduce_min_sync(0xFFFFFFFFu, hi);
+    const uint32_t win = __ballot_sync(0xFFFFFFFFu, valid && hi == mhi);
+    bool improving = false;
+    if (win) {
+        if (integer) {
+            improving = mhi < 0x80000000u;  // int32 score < 0
+        } else {
+            const uint32_t u = (mhi & 0x80000000u) ? (mhi ^ 0x80000000u) : ~mhi;
+            improving = __uint_as_float(u) < 0.0f;
+        }
+    }
+    if (!improving) {
+        if (lane == 0) dm.applied = 0;
+        return;
+    }
+    const int v = __ffs(win) - 1;  // lowest variant among the lowest scores (reading 5)
+    const uint32_t idx = static_cast<uint32_t>(__shfl_sync(0xFFFFFFFFu, k, v) & 0xFFFFFFFFu);
+    // lanes 0 / 1 locate the u / v slot (physical) in parallel: largest r with sb[r] <= x
+    const int x = lane == 0 ? static_cast<int>(idx / static_cast<uint32_t>(Qc)) : static_cast<int>(idx % static_cast<uint32_t>(Qc));
+    int ra_ = 0;
+    if (lane < 2) {
+        int a = 0, b = R - 1;
+        while (a < b) {
+            const int m = (a + b + 1) >> 1;
+            if (sb[m] <= x) a = m;
+            else b = m - 1;
+        }
+        ra_ = a;
+    }
+    const int ra = __shfl_sync(0xFFFFFFFFu, ra_, 0), rb = __shfl_sync(0xFFFFFFFFu, ra_, 1);
+    const int pa = __shfl_sync(0xFFFFFFFFu, x, 0) - sb[ra], pb = __shfl_sync(0xFFFFFFFFu, x, 1) - sb[rb];
+    if (lane != 0) return;
+    const int La = sl[ra], Lb = sl[rb];
+    const bool one = v == 0 || v >= 11;
+    // pieces with static indices (empty pieces have len 0 and are skipped by the walk)
+    Piece A0{}, A1{}, A2{}, A3{}, A4{}, B0{}, B1{}, B2{};
+    int na = 0, nb = 0;
+    auto pc = [](int src, int a, int b, int rev = 0) { return Piece{src, a, b >= a ? b - a + 1 : 0, rev}; };
+    if (v == 1) {  // 2-opt*
+        A0 = pc(ra, 1, pa); A1 = pc(rb, pb + 1, Lb); na = 2;
+        B0 = pc(rb, 1, pb); B1 = pc(ra, pa + 1, La); nb = 2;
+    } else if (v >= 2 && v <= 4) {  // relocate / or-opt
+        const int N = v - 1;
+        A0 = pc(ra, 1, pa - 1); A1 = pc(ra, pa + N, La); na = 2;
+        B0 = pc(rb, 1, pb); B1 = pc(ra, pa, pa + N - 1); B2 = pc(rb, pb + 1, Lb); nb = 3;
+    } else if (v >= 5 && v <= 10) {  // swap / cross: (N1, N2) = (1,1) (1,2) (1,3) (2,2) (2,3) (3,3)
+        const int q = v - 5;
+        const int N1 = q < 3 ? 1 : (q < 5 ? 2 : 3), N2 = q < 3 ? q + 1 : (q < 5 ? q - 1 : 3);
+        A0 = pc(ra, 1, pa - 1); A1 = pc(rb, pb, pb + N2 - 1); A2 = pc(ra, pa + N1, La); na = 3;
+        B0 = pc(rb, 1, pb - 1); B1 = pc(ra, pa, pa + N1 - 1); B2 = pc(rb, pb + N2, Lb); nb = 3;
+    } else if (v == 0) {  // 2-opt
+        A0 = pc(ra, 1, pa - 1); A1 = pc(ra, pa, pb, 1); A2 = pc(ra, pb + 1, La); na = 3;
+    } else if (v >= 11 && v <= 13) {  // intra relocate
+        const int N = v - 10;
+        if (pb > pa) {
+            A0 = pc(ra, 1, pa - 1); A1 = pc(ra, pa + N, pb); A2 = pc(ra, pa, pa + N - 1); A3 = pc(ra, pb + 1, La);
+        } else {
+            A0 = pc(ra, 1, pb); A1 = pc(ra, pa, pa + N - 1); A2 = pc(ra, pb + 1, pa - 1); A3 = pc(ra, pa + N, La);
+        }
+        na = 4;
+    } else {  // intra swap
+        const int N1 = (v - 14) / 3 + 1, N2 = (v - 14) % 3 + 1;
+        A0 = pc(ra, 1, pa - 1); A1 = pc(ra, pb, pb + N2 - 1); A2 = pc(ra, pa + N1, pb - 1);
+        A3 = pc(ra, pa, pa + N1 - 1); A4 = pc(ra, pb + N2, La); na = 5;
+    }
+    const int LA = A0.len + A1.len + A2.len + A3.len + A4.len, LB = B0.len + B1.len + B2.len;
+    const int ia = (one || ra < rb) ? 0 : 1;  // nr[0] = lower route of the span
+    NewRoute &A = dm.nr[ia];
+    A.r = ra; A.L = LA; A.np = na;
+    A.p[0] = A0; A.p[1] = A1; A.p[2] = A2; A.p[3] = A3; A.p[4] = A4;
+    bool fits = LA + 2 <= sb[ra + 1] - sb[ra];
+    dm.lo[ia] = sb[ra];
+    dm.hi[ia] = sb[ra + 1];
+    if (!one) {
+        NewRoute &B = dm.nr[ia ^ 1];
+        B.r = rb; B.L = LB; B.np = nb;
+        B.p[0] = B0; B.p[1] = B1; B.p[2] = B2;
+        fits = fits && LB + 2 <= sb[rb + 1] - sb[rb];
+        dm.lo[ia ^ 1] = sb[rb];
+        dm.hi[ia ^ 1] = sb[rb + 1];
+    } else {
+        dm.lo[1] = dm.hi[1] = 0;
+    }
+    dm.nrt = one ? 1 : 2;
+    dm.full = fits ? 0 : 1;
+    dm.applied = 1;
+}
+
+// ------------------------------------------------------------------ pick + apply
+// Route arrays (base, length, canonical base) are staged in shared memory so the
+// serial parts (decode, binary searches over routes) never wait on global loads.
+
+__device__ __forceinline__ void pick_apply_body(const DevState &S, uint32_t mask, int integer, int32_t *smr,
+                                                unsigned long long *pr, bool do_counts = true) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int R = S.R;
+    int32_t *sb = smr, *sl = smr + (R + 1), *nb = smr + 2 * (R + 1);  // old bases, old lengths, new bases
+    for (int r = tid; r <= R; r += blockDim.x) {
+        sb[r] = S.rbase[r];
+        sl[r] = r < R ? S.rlenR[r] : 0;
+    }
+    __shared__ uint64_t skeys[23];
+    if (tid < 23) skeys[tid] = S.keys[tid];
+    if (do_counts) neighbourhood_counts(S, mask, sl);
+    __syncthreads();
+    if (tid < 23) S.keys[tid] = ~0ull;  // consumed (block 0 is the only reader): the next eval needs no memset
+    if (tid == 0) probe(pr, 1);
     // ---- 2. best key over the mask, decode, pieces of the new routes
     __shared__ NewRoute nr[2];
     __shared__ int sh_n, sh_rlo, sh_rhi, sh_lo, sh_hi, sh_d, sh_applied;
@@ -213,6 +335,7 @@ __device__ __forceinline__ void pick_apply_body(const DevState &S, uint32_t mask
         }
     }
     __syncthreads();
+    if (tid == 0) probe(pr, 2);
     if (!sh_applied) {
         if (tid == 0) S.desc[0] = 0;
         return;  // uniform across the block
@@ -316,6 +439,7 @@ __device__ __forceinline__ void pick_apply_body(const DevState &S, uint32_t mask
     if (tid == 0) {
         S.desc[0] = 1;
         atomicAdd(S.acc + 23, 1ull);
+        probe(pr, 3);
     }
 }
 

@@ -127,6 +127,8 @@ struct tga_solution {
     int32_t *d_desc = nullptr, *d_scratch = nullptr;
     unsigned long long *d_acc = nullptr;
     bool host_stale = false;       // host route lists lag behind device-resident steps
+    bool keys_clean = false;       // keys are all ~0 (a device step consumed them) ...
+    unsigned long long clean_cap = 0;  // ... as of capture sequence clean_cap (0 = executed work)
     float *d_rTV = nullptr;
     void *d_rD = nullptr;
     void *Dp = nullptr;
@@ -332,7 +334,7 @@ static SolView<DT> sol_view(const tga_solution *s) {
     return v;
 }
 
-static DevState make_devstate(const tga_solution *s, const uint64_t *keys) {
+static DevState make_devstate(const tga_solution *s, uint64_t *keys) {
     DevState d;
     d.node = s->node; d.route = s->route; d.pos = s->pos; d.rlen = s->rlen; d.canon = s->canon;
     d.rbase = s->d_rbase; d.rlenR = s->d_rlenR; d.cbase = s->d_cbase;
@@ -752,6 +754,14 @@ extern "C" int32_t tga_solution_set_shard(tga_solution *s, int32_t shard, int32_
 extern "C" int32_t tga_shard_range(int64_t n, int32_t shard, int32_t n_shards, int64_t *lo, int64_t *hi);
 
 // ============================================================== ABI: evaluation
+// id of the capture sequence `st` is recording into (0 when not capturing)
+static unsigned long long capture_id(cudaStream_t st) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    unsigned long long id = 0;
+    if (cudaStreamGetCaptureInfo(st, &cs, &id) != cudaSuccess || cs != cudaStreamCaptureStatusActive) return 0;
+    return id;
+}
+
 extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
     if (!s) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL solution");
     const tga_instance *I = s->inst;
@@ -762,7 +772,11 @@ extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
     if (set_device(I) != TGA_OK) return TGA_ERR_CUDA;
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s->stream;
     if (st != s->stream) TGA_CUDA(order_after(st, s->stream));  // see the latest applied move
-    if (!accumulate) TGA_CUDA(cudaMemsetAsync(s->keys, 0xFF, TGA_N_VARIANTS * 8, st));
+    // a device step leaves the keys reset (consumed), so the next eval needs no memset node --
+    // unless that step belongs to another capture sequence (a graph replayed later)
+    if (!accumulate && !(s->keys_clean && s->clean_cap == capture_id(st)))
+        TGA_CUDA(cudaMemsetAsync(s->keys, 0xFF, TGA_N_VARIANTS * 8, st));
+    s->keys_clean = false;
     ScoreParams sp{I->Q, I->opt.score_mode, I->opt.w_load, I->opt.w_tw};
     // row shard of the tile list and of the intra slot range
     int64_t a, b;
@@ -1229,6 +1243,8 @@ extern "C" int32_t tga_step_async(tga_solution *s, uint32_t mask) {
                                        s->N + 2 + s->slack,  // upper bound of any route's slot capacity
                                        s->sm_count, s->stream);
     if (e != cudaSuccess) return fail(TGA_ERR_CUDA, std::string("device step: ") + cudaGetErrorString(e));
+    s->keys_clean = true;
+    s->clean_cap = capture_id(s->stream);
     ++s->gen;
     s->host_stale = true;
     s->drained = false;
@@ -1274,6 +1290,8 @@ extern "C" int32_t tga_descent(tga_solution *s, uint32_t mask, int32_t n_steps, 
     if (e == cudaSuccess && rc == TGA_OK) e = cudaGraphInstantiate(&exec, graph, 0);
     if (e == cudaSuccess && rc == TGA_OK) e = cudaGraphLaunch(exec, saved);
     if (e == cudaSuccess && rc == TGA_OK) e = cudaStreamSynchronize(saved);
+    if (e == cudaSuccess && rc == TGA_OK) s->clean_cap = 0;  // the captured steps have executed
+    else s->keys_clean = false;
     if (e == cudaSuccess && rc == TGA_OK && step_ms)
         for (int k = 0; k < n_steps && e == cudaSuccess; ++k) e = cudaEventElapsedTime(&step_ms[k], ev[2 * k], ev[2 * k + 1]);
     if (exec) cudaGraphExecDestroy(exec);
@@ -1285,12 +1303,25 @@ extern "C" int32_t tga_descent(tga_solution *s, uint32_t mask, int32_t n_steps, 
     return TGA_OK;
 }
 
+extern "C" int32_t tga_solution_debug_probe(tga_solution *s, int32_t enable, uint64_t *out) {
+    if (!s) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL solution");
+    if (set_device(s->inst) != TGA_OK) return TGA_ERR_CUDA;
+    if (out) {
+        TGA_CUDA(cudaMemcpyAsync(out, s->d_acc + 32, 16 * 8, cudaMemcpyDeviceToHost, s->stream));
+        TGA_CUDA(cudaStreamSynchronize(s->stream));
+    }
+    const unsigned long long flag = enable ? 1ull : 0ull;
+    TGA_CUDA(cudaMemcpyAsync(s->d_acc + 31, &flag, 8, cudaMemcpyHostToDevice, s->stream));
+    TGA_CUDA(cudaStreamSynchronize(s->stream));
+    return TGA_OK;
+}
+
 extern "C" int32_t tga_solution_device_stats(tga_solution *s, uint64_t *counts, uint64_t *applied) {
     if (!s) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL solution");
     unsigned long long acc[48];
     TGA_CUDA(cudaMemcpyAsync(acc, s->d_acc, sizeof(acc), cudaMemcpyDeviceToHost, s->stream));
     TGA_CUDA(cudaStreamSynchronize(s->stream));
-    TGA_CUDA(cudaMemsetAsync(s->d_acc, 0, sizeof(acc), s->stream));
+    TGA_CUDA(cudaMemsetAsync(s->d_acc, 0, 24 * 8, s->stream));  // counts + applied (not the probe)
     if (counts) for (int v = 0; v < TGA_N_VARIANTS; ++v) counts[v] = acc[v];
     if (applied) *applied = acc[23];
     return TGA_OK;

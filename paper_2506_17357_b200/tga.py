@@ -109,6 +109,7 @@ _SYMBOLS = {
     "tga_batch_apply_moves": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "tga_step_async": (C.c_int32, [C.c_void_p, C.c_uint32]),
     "tga_solution_device_stats": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "tga_solution_debug_probe": (C.c_int32, [C.c_void_p, C.c_int32, C.c_void_p]),
     "tga_descent": (C.c_int32, [C.c_void_p, C.c_uint32, C.c_int32, C.c_void_p, C.c_uint64, C.c_void_p]),
     "tga_batch_step_async": (C.c_int32, [C.c_void_p, C.c_uint32]),
     "tga_batch_set_stream": (C.c_int32, [C.c_void_p, C.c_void_p]),
@@ -287,6 +288,12 @@ class Solution:
         fp, fb = (None, 0) if l2_flush is None else (l2_flush.data_ptr(), l2_flush.numel() * l2_flush.element_size())
         _check(lib().tga_descent(self._h, op_mask, n_steps, fp, fb, _p(ms)))
         return ms[:n_steps] if timed else None
+
+    def debug_probe(self, enable: bool = True):
+        """Diagnostics: clock64 phase stamps of the last device step (16 u64), then (re)arm."""
+        out = np.zeros(16, dtype=np.uint64)
+        _check(lib().tga_solution_debug_probe(self._h, int(enable), _p(out)))
+        return out
 
     def device_stats(self):
         """(counts per variant, applied moves) accumulated by step_async; clears them."""

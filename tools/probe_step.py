@@ -1,0 +1,31 @@
+"""Diagnostics: clock64 phase stamps of the device-resident pick/update kernel.
+phases: 0 start, 1 counts done, 2 pick decoded, 3 splice written, 4 barrier 1,
+5 rows + scans, 6 barrier 2, 7 columns (block 0's view; cycles at ~1.9 GHz)."""
+import argparse, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+import tga_gen as G
+from paper_2506_17357_b200 import tga as T
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="cfg2")
+ap.add_argument("--steps", type=int, default=12)
+a = ap.parse_args()
+inst, sol = G.config(a.config)
+gi = T.Instance.from_gen(inst)
+gs = T.Solution(gi, sol)
+mask = T.OP_ALL if inst.tw is None else T.OP_ALL & ~T.OP_2OPT
+flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")
+gs.descent(mask, 3)
+torch.cuda.synchronize()
+rows = []
+for k in range(a.steps):
+    gs.debug_probe(True)
+    flush.fill_(k)
+    ms = gs.descent(mask, 1, timed=True)
+    p = gs.debug_probe(False).astype(np.int64)
+    d = [int(p[i] - p[0]) if p[i] else -1 for i in range(8)]
+    rows.append(d)
+    print(a.config, "step %.1f us" % (1e3 * float(ms[0])), "phase cycles", d)
+r = np.array(rows[2:], dtype=np.float64)
+print("median phase (us @1.965GHz):", [round(x / 1965.0, 2) for x in np.median(r, axis=0)])

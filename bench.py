@@ -4,16 +4,21 @@ and full-neighbourhood sweeps/s per operator).
 
 A *step* is one best-improvement local-search iteration of the whole hot path
  on the BASELINE config-2 workload (Uchoa X-like
-CVRP, 1000 customers, X-n1001-k43 shape + one spare route):
-    tga_eval(all 23 variants: inter-route kernel + intra-route kernel)
-    -> tga_best_move (8 B per variant device->host)
-    -> tga_apply_move (span re-upload, Dp row/column refresh, re-scan).
-value = canonical candidates evaluated / device time of the step (CUDA events on
-the solution's stream, L2 flushed between steps: the working set < L2).
+CVRP, 1000 customers, X-n1001-k43 shape + one spare route), entirely on the
+device (tga_step_async):
+    eval of all 23 variants (one fused inter+intra kernel)
+    -> on-device best key, decode and splice of the changed routes
+    -> Dp row/column refresh + re-scan of the changed routes (same kernel).
+value = canonical candidates evaluated / device time of K steps (one CUDA graph
+between two CUDA events).  The working set of one solution is smaller than L2,
+so R replicas of it are stepped round-robin (inputs larger than L2 between two
+steps of a replica); each replica follows the config's own descent.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl tga|reference]
-Under torchrun (N>1) every rank evaluates a row shard of the same neighbourhood
-and the packed keys are MIN-allreduced over NCCL inside tga_eval.
+                    [--config cfg2|ns2000|cfg3|cfg3r2|cfg4|cfg5] [--shard replicas|rows]
+Under torchrun (N>1) every rank runs its own descents (weak scaling, no
+collective) or, with --shard rows, one solution's candidate rows are split
+over the ranks and the packed keys are MIN-allreduced over NCCL inside tga_eval.
 """
 from __future__ import annotations
 
@@ -53,6 +58,9 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-per-op", action="store_true")
+    ap.add_argument("--shard", choices=["replicas", "rows"], default="replicas",
+                    help="N>1: independent descents per GPU (weak scaling, no collective) or one "
+                         "solution's candidate rows split over the GPUs (NCCL MIN-allreduce of the keys)")
     return ap.parse_args()
 
 
@@ -280,64 +288,103 @@ def run_tga(args):
     inst, sol0 = G.config(args.config, args.seed)
     stream = torch.cuda.Stream(device=dev)
     gi = T.Instance.from_gen(inst)
-    gs = T.Solution(gi, sol0)
-    gs.set_stream(stream)
-    if ws > 1:
+    row_shard = ws > 1 and args.shard == "rows"
+    # Cold-cache timing without flush nodes: R replicas of the workload's
+    # solution (separate device state each) stepped round-robin, so that
+    # between two steps of one replica > 1.5 x L2 of other replicas' data has
+    # streamed through (the timing rule's "inputs larger than L2").  Each
+    # replica runs exactly the single-solution descent of the config.
+    probe = T.Solution(gi, sol0)
+    R_, N_, _, _ = probe.info()
+    pitch = -(-(N_ + 2 * R_ + 8 * R_) // 128) * 128
+    ws_bytes = pitch * pitch * 4 + pitch * 400
+    l2 = getattr(torch.cuda.get_device_properties(dev), "L2_cache_size", 126 * 2 ** 20) or 126 * 2 ** 20
+    n_rep = 1 if row_shard else max(1, min(64, -(-int(1.5 * l2) // ws_bytes)))
+    probe.close()
+    reps = [T.Solution(gi, sol0) for _ in range(n_rep)]
+    for r in reps:
+        r.set_stream(stream)
+    gs = reps[0]
+    if row_shard:
         import torch.distributed as dist
         obj = [T.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         gs.comm_init(rank, ws, obj[0])
     mask_all = T.OP_ALL if inst.tw is None else (T.OP_ALL & ~T.OP_2OPT)
-    mask_inter = mask_all & T.OP_INTER
-    mask_intra = mask_all & T.OP_INTRA
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)  # 256 MB > L2 (126 MB)
-
-    def step(evs=None):
-        # tga_step_async: eval (inter + intra kernels) -> on-device best move + splice
-        # -> update kernel; no host round trip
-        if evs:
-            evs[0].record(stream)
-        gs.step_async(mask_all)
-        if evs:
-            evs[1].record(stream)
-
-    # ---------------- warm-up
-    for _ in range(max(args.warmup, 3)):
-        step()
-    torch.cuda.synchronize(dev)
-
-    # ---------------- timed region: K steps, per-step events, L2 flushed between steps
-    sampler = ClockSampler(local)
     K = args.steps
-    gs.enable_timing(True)   # CUDA events around the inter-route launch, on its stream
-    counts = []
+    W = max(args.warmup, 3)
+
+    def capture_steps():
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            for k in range(K):
+                reps[k % n_rep].step_async(mask_all)   # eval -> on-device pick/splice -> update
+        return g
+
+    def replay(g, timed=False):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            g.replay()
+            e1.record(stream)
+        torch.cuda.synchronize(dev)
+        return e0.elapsed_time(e1)
+
+    # ---------------- warm-up: W device steps of every replica, then one replay of the graph
+    for _ in range(W):
+        for r in reps:
+            r.step_async(mask_all)
+    torch.cuda.synchronize(dev)
+    launches0 = T.launch_count()
+    g_val = capture_steps()
+    launches = T.launch_count() - launches0      # kernels in the K captured steps
+    replay(g_val)
+
+    # ---------------- timed region: the K steps, one graph launch between two events
+    for r in reps:
+        r.device_stats()   # clear the on-device counters of the warm-up
+    sampler = ClockSampler(local)
     if ws > 1:
         import torch.distributed as dist
         dist.barrier()
     torch.cuda.synchronize(dev)
     sampler.start()
-    launches0 = T.launch_count()
-    applied = 0
-    gs.device_stats()  # clear the on-device counters of the warm-up
-    # K device-resident steps enqueued from C (tga_descent); CUDA events around every
-    # step on the solution's stream; a 256 MB memset before each step flushes L2
-    step_ms = [float(x) for x in gs.descent(mask_all, K, l2_flush=flush, timed=True)]
-    torch.cuda.synchronize(dev)
-    launches = T.launch_count() - launches0
-    dev_counts, applied = gs.device_stats()   # exact candidate counts of the K evaluated neighbourhoods
+    tot_ms = replay(g_val, timed=True)
     clocks = sampler.stop()
-    inter_ms = [float(x) for x in gs.timings()]
-    gs.enable_timing(False)
-    tot_ms = float(sum(step_ms))
+    dev_counts = np.zeros(T.N_VARIANTS, dtype=np.uint64)
+    applied = 0
+    for r in reps:
+        c, a_ = r.device_stats()   # exact candidate counts of the K evaluated neighbourhoods
+        dev_counts += c
+        applied += a_
+    cand_total = float(dev_counts.sum())
     if ws > 1:
         import torch.distributed as dist
-        t = torch.tensor([tot_ms], device=dev)
+        t = torch.tensor([tot_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms = float(t.item())
+        if not row_shard:   # independent descents: every rank's candidates count
+            c = torch.tensor([cand_total], device=dev, dtype=torch.float64)
+            dist.all_reduce(c, op=dist.ReduceOp.SUM)
+            cand_total = float(c.item())
         dist.barrier()
-    cand_total = int(dev_counts.sum())
     value = cand_total / (tot_ms / 1e3)
 
+    # ---------------- kernel timing pass: the same K steps again with CUDA events
+    # around every inter-route launch (recorded by the library on its stream).
+    # Event nodes cost several us each inside a graph, so the value pass has none.
+    for r in reps:
+        r.enable_timing(True)
+    g_ker = capture_steps()
+    replay(g_ker)
+    replay(g_ker)   # the library's events keep the records of this (second) replay
+    inter_ms = []
+    for r in reps:
+        inter_ms.extend(float(x) for x in r.timings())
+        r.enable_timing(False)
+    for r in reps:
+        r.device_stats()
+    del g_ker
     if rank != 0:
         return 0
 
@@ -348,9 +395,10 @@ def run_tga(args):
     Qp = N + 2 * R
     # the CVRP fast path evaluates inter AND intra candidates in the one timed launch
     inter_sel = [v for v in range(23) if (mask_all >> v) & 1] if inst.tw is None else list(range(1, 11))
-    inter_cands = float(sum(int(dev_counts[v]) for v in inter_sel)) / K
-    alg_bytes = (Qp * Qp / 2.0) * 4.0                    # Dp upper triangle, int32
-    alg_ops = float(sum(int(dev_counts[v]) * ALG_OPS[v] for v in inter_sel)) / K
+    shard_div = ws if row_shard else 1   # a launch evaluates 1/N of the rows when row-sharded
+    inter_cands = float(sum(int(dev_counts[v]) for v in inter_sel)) / K / shard_div
+    alg_bytes = (Qp * Qp / 2.0) * 4.0 / shard_div       # Dp upper triangle, int32
+    alg_ops = float(sum(int(dev_counts[v]) * ALG_OPS[v] for v in inter_sel)) / K / shard_div
     sm_mhz_peak = float(pk.get("sm_max_mhz", 1965.0))
     alu_peak = 148 * 128 * sm_mhz_peak * 1e6            # lane-ops/s (4 SMSP x 32 lanes x 1 issue/clk)
     hbm_peak = float(pk["hbm_gbs"]) * 1e9
@@ -438,19 +486,26 @@ def run_tga(args):
                "sample": f"{sw} full sweep(s) of all variants on state A ({c} candidates, {t:.1f} s), "
                          "single-threaded C oracle that rebuilds every neighbour route"}
 
-    sweeps_per_s = K / (tot_ms / 1e3)
+    sweeps_per_s = (K if row_shard else K * ws) / (tot_ms / 1e3)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K,
         "warmup": max(args.warmup, 3), "ms_per_step": tot_ms / K, "higher_is_better": True,
-        "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None, "dtype": "int32",
+        "scaling": "strong" if row_shard else "weak", "vs_baseline": None, "dtype": "int32",
         "data": "synthetic",
         "config": {"workload": f"{args.config}: {G.CONFIGS.get(args.config, args.config)}; "
                                "step = eval all variants + best move + apply",
                    "customers": N, "routes": R, "canonical_slots": Qc, "seed": args.seed,
-                   "l2": "flushed between timed steps (256 MB write); working set < L2",
-                   "parallelism": f"row-shard x{ws}" if ws > 1 else "1 GPU"},
+                   "l2": (f"inputs larger than L2: {n_rep} replicas of the solution stepped round-robin "
+                          f"({n_rep * ws_bytes / 2**20:.0f} MB of Dp + records vs {l2 / 2**20:.0f} MB L2)"
+                          if n_rep > 1 else "Dp larger than L2"),
+                   "replicas": n_rep,
+                   "parallelism": (f"row-shard x{ws} (NCCL MIN-allreduce)" if row_shard else
+                                   f"independent descents x{ws}" if ws > 1 else "1 GPU")},
         "sweeps_per_s": sweeps_per_s, "applied_moves": int(applied),
-        "step": "tga_step_async: eval all variants -> on-device best move + splice -> update kernel",
+        "step": "tga_step_async: eval all variants -> on-device best move + splice -> update kernel; "
+                "K steps captured in one CUDA graph, timed by two CUDA events",
+        "kernel_timing": "second pass of the same K-step graph with CUDA events around every "
+                         "inter-route launch (event nodes add several us per step)",
         "candidates_per_step": cand_total / K,
         "roofline": primary, "roofline_alt": alt,
         "per_operator_steady_state": per_op,

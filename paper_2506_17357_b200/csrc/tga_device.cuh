@@ -12,6 +12,11 @@
 
 namespace tga {
 
+// PDL controls (see launch_pdl in tga_launch.h)
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+
 // ------------------------------------------------------------------ records
 // A time-window record of a subsequence: x = T_D (duration incl.
 // waiting), y = T_E (earliest start), z = T_L (latest start), w = T_V (warp).

@@ -84,7 +84,8 @@ __global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__re
                                                              const uint32_t *__restrict__ tiles, int t_lo, int t_hi,
                                                              uint32_t Qc, int32_t cap, uint64_t *__restrict__ keys,
                                                              const __grid_constant__ SolView<int32_t> SV,
-                                                             ScoreParams sp, uint32_t imask, int x_lo, int x_hi) {
+                                                             ScoreParams sp, uint32_t imask, int x_lo, int x_hi,
+                                                             int late_trigger) {
     using G = FastGeom<U, TW>;
     constexpr int BW = G::BoxW;
     constexpr int NV = 11;
@@ -111,7 +112,9 @@ __global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__re
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (tid < 23) red[tid] = kNoKey;
+    if (!late_trigger) pdl_trigger();  // no inter-CTA waits here: a dependent grid may launch now
     __syncthreads();
+    pdl_wait();     // Dp / records / keys are written by the stream predecessors
 
     uint64_t acc[NV];
 #pragma unroll
@@ -253,6 +256,7 @@ __global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__re
         __syncthreads();  // buffer b is refilled two iterations later
     }
 
+    if (late_trigger) pdl_trigger();
     // ---- fused argmin: warp shuffle -> shared -> one 64-bit atomicMin per variant per CTA
 #pragma unroll
     for (int i = 1; i < NV; ++i) {
@@ -276,10 +280,10 @@ static cudaError_t launch_fast_t(const SlotRec *rec, const SlotTW *rectw, const 
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr = true;
     }
-    kern<<<grid, kFastThreads, smem, st>>>(rec, rectw, map, tiles, t_lo, t_hi, Qc, cap, keys, SV, sp, imask, x_lo,
-                                           x_hi);
+    const cudaError_t e = launch_pdl(1, kern, dim3(grid), dim3(kFastThreads), smem, st, rec, rectw, map, tiles, t_lo, t_hi,
+                                     Qc, cap, keys, SV, sp, imask, x_lo, x_hi, pdl_enabled(4) ? 1 : 0);
     note_launch();
-    return cudaGetLastError();
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 template <int U, bool TW>

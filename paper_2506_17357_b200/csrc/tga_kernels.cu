@@ -427,6 +427,7 @@ __device__ __forceinline__ void pick_update_multi(const DevState &S, const ScanA
     for (int j = tid; j < n1 + n2; j += blockDim.x) snap[j] = S.node[j < n1 ? lo0 + j : lo1 + (j - n1)];
     __syncthreads();
     if (tid == 0) arrive_v = atomicAdd(S.desc + 9, 1);
+    pdl_trigger();  // this block is resident and arrived: a dependent grid cannot starve the wait below
     if (b == G - 1) neighbourhood_counts(S, mask, sl);  // the evaluated (old) lengths
     if (!dm.applied) {
         if (b == 0 && tid == 0) {
@@ -547,9 +548,11 @@ __global__ void __launch_bounds__(256) k_pick_update(const DevState *__restrict_
                                                      const ScanArgs<DT> *__restrict__ scans, uint32_t mask,
                                                      int integer, int snap_cap) {
     extern __shared__ int32_t smr[];
+    pdl_wait();  // the keys (and, two launches back, the slot arrays) come from stream predecessors
     const DevState &S = states[blockIdx.y];
     unsigned long long *pr = (blockIdx.x == 0 && threadIdx.x == 0 && S.acc[31]) ? S.acc + 32 : nullptr;
     probe(pr, 0);
+    if (gridDim.x == 1) pdl_trigger();
     if (snap_cap > 0 && gridDim.x > 1) {
         pick_update_multi<DT, TW>(S, scans[blockIdx.y], mask, integer, smr, snap_cap, pr);
         return;
@@ -559,6 +562,7 @@ __global__ void __launch_bounds__(256) k_pick_update(const DevState *__restrict_
     if (blockIdx.x == 0) pick_apply_body(S, mask, integer, smr, pr);
     if (gridDim.x > 1) solution_barrier(S.desc + 8, gridDim.x);
     else __syncthreads();
+    if (gridDim.x > 1) pdl_trigger();  // every block of this grid is resident (it passed the barrier)
     probe(pr, 4);
     const volatile int32_t *desc = S.desc;
     if (desc[0] == 0) return;
@@ -590,15 +594,15 @@ cudaError_t launch_pick_update(const DevState *states, const void *scans, int n_
         cudaFuncSetAttribute(k_pick_update<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         cudaFuncSetAttribute(k_pick_update<float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     }
-    if (is_int) {
-        if (tw) k_pick_update<int32_t, true><<<g, 256, smem, st>>>(states, static_cast<const ScanArgs<int32_t> *>(scans), mask, 1, snap_cap);
-        else    k_pick_update<int32_t, false><<<g, 256, smem, st>>>(states, static_cast<const ScanArgs<int32_t> *>(scans), mask, 1, snap_cap);
-    } else {
-        if (tw) k_pick_update<float, true><<<g, 256, smem, st>>>(states, static_cast<const ScanArgs<float> *>(scans), mask, 0, snap_cap);
-        else    k_pick_update<float, false><<<g, 256, smem, st>>>(states, static_cast<const ScanArgs<float> *>(scans), mask, 0, snap_cap);
-    }
+    cudaError_t e;
+    const auto *si = static_cast<const ScanArgs<int32_t> *>(scans);
+    const auto *sf = static_cast<const ScanArgs<float> *>(scans);
+    if (is_int) e = tw ? launch_pdl(2, k_pick_update<int32_t, true>, g, dim3(256), smem, st, states, si, mask, 1, snap_cap)
+                       : launch_pdl(2, k_pick_update<int32_t, false>, g, dim3(256), smem, st, states, si, mask, 1, snap_cap);
+    else e = tw ? launch_pdl(2, k_pick_update<float, true>, g, dim3(256), smem, st, states, sf, mask, 0, snap_cap)
+                : launch_pdl(2, k_pick_update<float, false>, g, dim3(256), smem, st, states, sf, mask, 0, snap_cap);
     note_launch();
-    return cudaGetLastError();
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 // ============================================================== TMA / mbarrier helpers
@@ -1284,6 +1288,13 @@ __global__ void __launch_bounds__(256) k_intra_cvrp(const SolView<int32_t> S, Sc
 // ============================================================== launchers
 static unsigned long long g_launches = 0;
 unsigned long long launch_count() { return g_launches; }
+// Off by default: measured on B200 (bench.py, replicas graph) every combination
+// was slower -- cfg2 23.3 us/step without, 24.5-25.4 with; n=2000 38.8 vs 41.6-44.1.
+// TGA_PDL_MODE bits: 1 eval launch, 2 pick launch, 4 eval triggers after its tiles.
+bool pdl_enabled(int which) {
+    static const int mode = std::getenv("TGA_PDL_MODE") ? std::atoi(std::getenv("TGA_PDL_MODE")) : 0;
+    return (mode & which) != 0;
+}
 void note_launch() { ++g_launches; }
 
 template <class DT>

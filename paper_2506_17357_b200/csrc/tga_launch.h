@@ -5,6 +5,7 @@
 #include <cstdint>
 #include <type_traits>
 #include <algorithm>
+#include <utility>
 
 #include "tga_device.cuh"
 
@@ -104,6 +105,30 @@ cudaError_t launch_batch(uint32_t mask, bool tw, const SolView<DT> *views, const
                          uint64_t *keys, int grid, cudaStream_t st, bool warp_tw = false);
 unsigned long long launch_count();
 void note_launch();
+
+// Programmatic dependent launch (PDL): the kernel may be scheduled while its
+// stream predecessor is still running; it calls pdl_wait() before its first
+// global read of data any predecessor writes (griddepcontrol.wait returns once
+// the predecessor grid has completed and its writes are visible), and
+// pdl_trigger() once its own CTAs are all resident (so a dependent grid can
+// never take the SM slots a grid barrier of this kernel waits for).
+// Enabled per launch site with TGA_PDL_MODE (see pdl_enabled; off by default).
+bool pdl_enabled(int which = 1);
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(int which, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args &&...args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled(which) ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 cudaError_t launch_inter_fast(int U, uint32_t mask, const SlotRec *rec, const SlotTW *rectw, const CUtensorMap &map,
                               const uint32_t *tiles, int t_lo, int t_hi, uint32_t Qc, int32_t cap, uint64_t *keys,
                               int max_grid, cudaStream_t st, const SolView<int32_t> &SV, const ScoreParams &sp,

@@ -57,10 +57,12 @@ __device__ __forceinline__ uint64_t pack_key(uint32_t ord, uint32_t idx) {
 
 __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
 
+// 64-bit warp minimum with two REDUX.MIN (high words, then low words among the lanes holding the high minimum)
 __device__ __forceinline__ uint64_t warp_min64(uint64_t k) {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) k = umin64(k, __shfl_xor_sync(0xffffffffu, k, off));
-    return k;
+    const uint32_t hi = static_cast<uint32_t>(k >> 32), lo = static_cast<uint32_t>(k);
+    const uint32_t mh = __reduce_min_sync(0xffffffffu, hi);
+    const uint32_t ml = __reduce_min_sync(0xffffffffu, hi == mh ? lo : 0xFFFFFFFFu);
+    return (static_cast<uint64_t>(mh) << 32) | ml;
 }
 
 // ------------------------------------------------------------------ scoring
@@ -170,74 +172,100 @@ __device__ __forceinline__ uint32_t intra_k32(bool ok, int32_t dD, int lane) {
     // dD is bounded by 8 * max c < 2^25 (host-checked: max c < 2^21)
     return ok ? ((static_cast<uint32_t>(dD + (1 << 25)) << 5) | static_cast<uint32_t>(lane)) : 0xFFFFFFFFu;
 }
-__device__ __forceinline__ void warp_keep(unsigned long long *red, int var, uint32_t k32, uint32_t idx_base, int lane) {
+// wred: this warp's private row of per-variant minima in shared memory (plain
+// read-min-write by lane 0: a 64-bit shared atomicMin compiles to a CAS spin loop)
+__device__ __forceinline__ void warp_keep(unsigned long long *wred, int var, uint32_t k32, uint32_t idx_base, int lane) {
     const uint32_t m = __reduce_min_sync(0xffffffffu, k32);
     if (lane == 0 && m != 0xFFFFFFFFu) {
         const int32_t s = static_cast<int32_t>(m >> 5) - (1 << 25);
-        atomicMin(&red[var], static_cast<unsigned long long>(pack_key(ord_score(s), idx_base + (m & 31u))));
+        const unsigned long long k = pack_key(ord_score(s), idx_base + (m & 31u));
+        if (k < wred[var]) wred[var] = k;
     }
 }
 
 // One warp evaluates every intra-route CVRP variant of u slot x (lane <-> v);
-// the per-variant warp minima are MIN-combined into the CTA's red[23].
+// the per-variant warp minima are MIN-combined into red[23], the calling warp's
+// private row of shared memory.
 __device__ __forceinline__ void intra_cvrp_warp(const SolView<int32_t> &S, const ScoreParams &sp, uint32_t vmask,
-                                                int x, unsigned long long *red) {
+                                                int x, unsigned long long *red, unsigned long long *pslot = nullptr) {
     const int lane = threadIdx.x & 31;
-    if (S.canon[x] >= 0 && S.pos[x] >= 1) {   // warp-uniform
-        const int p = S.pos[x], L = S.rlen[x], r = S.route[x];
-        const int base = x - p;
-        const bool ok_route = sp.mode == 1 || S.rW[r] <= sp.capacity;
-        const uint32_t cu = static_cast<uint32_t>(S.canon[x]);
-        const uint32_t cbase = cu - static_cast<uint32_t>(p);
-        auto D = [&](int a, int b) -> int32_t { return __ldg(S.Dp + static_cast<size_t>(a) * S.pitch + b); };
-        const int32_t em = S.enext[x - 1];
-        int32_t eo[3], rem[3];
-#pragma unroll
-        for (int N = 1; N <= 3; ++N) {
-            eo[N - 1] = S.enext[min(x + N - 1, base + L + 1)];
-            const int32_t br = N == 1 ? S.bridge1[x] : (N == 2 ? S.bridge2[x] : S.bridge3[x]);
-            rem[N - 1] = br - em - eo[N - 1];
+    auto stamp = [&](int k) {
+        if (pslot && lane == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+            pslot[k] = t;
         }
-        for (int qb = 0; qb <= L; qb += 32) {
-            const int q = qb + lane;
-            const bool in = q <= L;
-            const int v = base + min(q, L);
-            const int vm1 = max(v - 1, base);          // masked lanes (q = 0) must still read a valid row
-            const uint32_t ib = static_cast<uint32_t>(x) * S.Qc + static_cast<uint32_t>(base + qb);  // physical
-            const int32_t ev = S.enext[v], evm = (q >= 1 && in) ? S.enext[v - 1] : 0;
-            // phase 1: every variant's 32-bit key in registers (all loads issued together)
-            uint32_t k[23];
+    };
+    stamp(0);
+    // two dependent rounds of global loads: (1) everything indexed by x alone,
+    // (2) the route load and the Dp / edge values of the lanes' v (needs the
+    // route base) -- the loads of each round are issued together
+    const int32_t cx = S.canon[x], p = S.pos[x], L = S.rlen[x], r = S.route[x];
+    const int32_t em = S.enext[x - 1];
+    int32_t eo[3], br[3];
 #pragma unroll
-            for (int i = 0; i < 23; ++i) k[i] = 0xFFFFFFFFu;
-            if (vmask & 1u)   // 2-opt: reverse u..v
-                k[0] = intra_k32(ok_route && in && q > p, D(x - 1, v) + D(x, v + 1) - em - ev, lane);
+    for (int N = 1; N <= 3; ++N) eo[N - 1] = S.enext[x + N - 1];  // past the route end: only in masked candidates
+    br[0] = S.bridge1[x]; br[1] = S.bridge2[x]; br[2] = S.bridge3[x];
+    if (!(cx >= 0 && p >= 1)) return;   // warp-uniform
+    stamp(1);
+    const int base = x - p;
+    int32_t rem[3];
 #pragma unroll
-            for (int N = 1; N <= 3; ++N) {  // intra relocate / or-opt
-                if (!(vmask & (1u << (10 + N)))) continue;
-                const bool ok = ok_route && in && p + N - 1 <= L && (q < p - 1 || q > p + N - 1);
-                // c is symmetric (host-checked): every Dp read is row x.. with lanes along columns
-                k[10 + N] = intra_k32(ok, rem[N - 1] + D(x, v) + D(x + N - 1, v + 1) - ev, lane);
-            }
+    for (int N = 1; N <= 3; ++N) rem[N - 1] = br[N - 1] - em - eo[N - 1];
+    const int32_t Wr = S.rW[max(r, 0)];
+    for (int qb = 0; qb <= L; qb += 32) {
+        const int q = qb + lane;
+        const bool in = q <= L;
+        const int v = base + min(q, L);
+        const int vm1 = max(v - 1, base);          // masked lanes (q = 0) must still read a valid row
+        const uint32_t ib = static_cast<uint32_t>(x) * S.Qc + static_cast<uint32_t>(base + qb);  // physical
+        const int32_t ev = S.enext[v], evm = (q >= 1 && in) ? S.enext[v - 1] : 0;
+        int32_t ev2[3];
 #pragma unroll
-            for (int a = 1; a <= 3; ++a) {   // intra swap (N1 = a at u, N2 = b at v), u + N1 <= v
+        for (int b = 1; b <= 3; ++b) ev2[b - 1] = S.enext[min(v + b - 1, base + L + 1)];
+        const bool ok_route = sp.mode == 1 || Wr <= sp.capacity;
+        // every Dp value any variant reads, loaded up front and unconditionally so
+        // that they are one round trip (inside the variant branches they were one
+        // round trip per variant): row x-1 at v; rows x..x+3 at v..v+3; row x at vm1
+        int32_t d[5][4];
+        const int32_t *dr = S.Dp + static_cast<size_t>(x - 1) * S.pitch + v;
+        const int32_t dm1 = __ldg(dr), dxm = __ldg(S.Dp + static_cast<size_t>(x) * S.pitch + vm1);
 #pragma unroll
-                for (int b = 1; b <= 3; ++b) {
-                    const int var = 14 + 3 * (a - 1) + (b - 1);
-                    if (!(vmask & (1u << var))) continue;
-                    const bool ok = ok_route && in && q >= p + a && q + b - 1 <= L;
-                    const int32_t ev2 = S.enext[min(v + b - 1, base + L + 1)];
-                    const int32_t adj = D(x - 1, v) + D(x, v + b - 1) + D(x + a - 1, v + b) - em - evm - ev2;
-                    const int32_t gap = D(x - 1, v) + D(x + a, v + b - 1) + D(x, vm1) + D(x + a - 1, v + b) - em -
-                                        eo[a - 1] - evm - ev2;
-                    k[var] = intra_k32(ok, q == p + a ? adj : gap, lane);
-                }
-            }
-            // phase 2: one REDUX.MIN per variant
+        for (int i = 1; i < 5; ++i)
 #pragma unroll
-            for (int i = 0; i < 23; ++i)
-                if ((i == 0 || i >= 11) && (vmask & (1u << i))) warp_keep(red, i, k[i], ib, lane);
+            for (int j = 0; j < 4; ++j) d[i][j] = (i == 4 && j == 3) ? 0 : __ldg(dr + i * S.pitch + j);
+        auto D = [&](int i, int j) -> int32_t { return i < 0 ? dm1 : d[i + 1][j]; };  // Dp(x + i, v + j)
+        uint32_t k[23];
+#pragma unroll
+        for (int i = 0; i < 23; ++i) k[i] = 0xFFFFFFFFu;
+        if (vmask & 1u)   // 2-opt: reverse u..v
+            k[0] = intra_k32(ok_route && in && q > p, D(-1, 0) + D(0, 1) - em - ev, lane);
+#pragma unroll
+        for (int N = 1; N <= 3; ++N) {  // intra relocate / or-opt
+            if (!(vmask & (1u << (10 + N)))) continue;
+            const bool ok = ok_route && in && p + N - 1 <= L && (q < p - 1 || q > p + N - 1);
+            // c is symmetric (host-checked): every Dp read is row x.. with lanes along columns
+            k[10 + N] = intra_k32(ok, rem[N - 1] + D(0, 0) + D(N - 1, 1) - ev, lane);
         }
+#pragma unroll
+        for (int a = 1; a <= 3; ++a) {   // intra swap (N1 = a at u, N2 = b at v), u + N1 <= v
+#pragma unroll
+            for (int b = 1; b <= 3; ++b) {
+                const int var = 14 + 3 * (a - 1) + (b - 1);
+                if (!(vmask & (1u << var))) continue;
+                const bool ok = ok_route && in && q >= p + a && q + b - 1 <= L;
+                const int32_t adj = D(-1, 0) + D(0, b - 1) + D(a - 1, b) - em - evm - ev2[b - 1];
+                const int32_t gap = D(-1, 0) + D(a, b - 1) + dxm + D(a - 1, b) - em - eo[a - 1] - evm - ev2[b - 1];
+                k[var] = intra_k32(ok, q == p + a ? adj : gap, lane);
+            }
+        }
+        // phase 2: one REDUX.MIN per variant
+        if (qb == 0) stamp(2);
+#pragma unroll
+        for (int i = 0; i < 23; ++i)
+            if ((i == 0 || i >= 11) && (vmask & (1u << i))) warp_keep(red, i, k[i], ib, lane);
     }
+    stamp(3);
 }
 
 }  // namespace tga

@@ -16,12 +16,22 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <climits>
+#include <cstdlib>
 #include <cstdint>
 
 #include "tga_device.cuh"
 #include "tga_launch.h"
 
 namespace tga {
+
+// diagnostics (TGA_INTER_PROBE=1): per-CTA %globaltimer stamps, 8 per CTA:
+// 0 start, 1 intra done, 2 first tile data arrived, 3 tiles done, 4 end
+__device__ unsigned long long g_inter_probe[8 * 4096];
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 namespace {
 __device__ __forceinline__ uint32_t s_u32(const void *p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -78,43 +88,28 @@ __device__ __forceinline__ void fold(uint64_t &acc, uint32_t b, bool direct, int
 // stream slots: 0 2opt* | 1,2 reloc1 d/r | 3,4 oropt2 | 5,6 oropt3 | 7 swap11 |
 // 8,9 cross12 | 10,11 cross13 | 12 cross22 | 13,14 cross23 | 15 cross33
 template <int U, bool TW, uint32_t MASK>
-__global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__restrict__ rec,
-                                                             const SlotTW *__restrict__ rectw,
-                                                             const __grid_constant__ CUtensorMap tmap,
-                                                             const uint32_t *__restrict__ tiles, int t_lo, int t_hi,
-                                                             uint32_t Qc, int32_t cap, uint64_t *__restrict__ keys,
-                                                             const __grid_constant__ SolView<int32_t> SV,
-                                                             ScoreParams sp, uint32_t imask, int x_lo, int x_hi,
-                                                             int late_trigger) {
+__device__ __forceinline__ void fast_body(const int cta, const int ncta, uint64_t *bar, unsigned long long (*red)[23],
+                                          unsigned char *sm, const SlotRec *__restrict__ rec,
+                                          const SlotTW *__restrict__ rectw, const CUtensorMap &tmap,
+                                          const uint32_t *__restrict__ tiles, int t_lo, int t_hi, uint32_t Qc,
+                                          int32_t cap, uint64_t *__restrict__ keys, const SolView<int32_t> &SV,
+                                          const ScoreParams &sp, uint32_t imask, int x_lo, int x_hi, int flags) {
     using G = FastGeom<U, TW>;
     constexpr int BW = G::BoxW;
     constexpr int NV = 11;
-    extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char *sm = smem_raw + ((128u - (s_u32(smem_raw) & 127u)) & 127u);
+    // stage b at sm + b * Stage: box | row records | column records | TW rows | TW columns
     int32_t *const dp0 = reinterpret_cast<int32_t *>(sm);
-    int32_t *const dp1 = reinterpret_cast<int32_t *>(sm + G::BoxPad);
-    SlotRec *const rows0 = reinterpret_cast<SlotRec *>(sm + 2 * G::BoxPad);
-    SlotRec *const rows1 = reinterpret_cast<SlotRec *>(sm + 2 * G::BoxPad + G::RowBytes);
-    SlotRec *const cols0 = reinterpret_cast<SlotRec *>(sm + 2 * G::BoxPad + 2 * G::RowBytes);
-    SlotRec *const cols1 = reinterpret_cast<SlotRec *>(sm + 2 * G::BoxPad + 2 * G::RowBytes + G::ColBytes);
-    unsigned char *const twb = sm + 2 * G::BoxPad + 2 * G::RowBytes + 2 * G::ColBytes;
-    SlotTW *const trows0 = reinterpret_cast<SlotTW *>(twb);
-    SlotTW *const trows1 = reinterpret_cast<SlotTW *>(twb + G::RowTW);
-    SlotTW *const tcols0 = reinterpret_cast<SlotTW *>(twb + 2 * G::RowTW);
-    SlotTW *const tcols1 = reinterpret_cast<SlotTW *>(twb + 2 * G::RowTW + G::ColTW);
-    __shared__ uint64_t bar[2];
-    __shared__ unsigned long long red[23];
-
+    int32_t *const dp1 = reinterpret_cast<int32_t *>(sm + G::Stage);
+    SlotRec *const rows0 = reinterpret_cast<SlotRec *>(sm + G::BoxPad);
+    SlotRec *const rows1 = reinterpret_cast<SlotRec *>(sm + G::Stage + G::BoxPad);
+    SlotRec *const cols0 = reinterpret_cast<SlotRec *>(sm + G::BoxPad + G::RowBytes);
+    SlotRec *const cols1 = reinterpret_cast<SlotRec *>(sm + G::Stage + G::BoxPad + G::RowBytes);
+    SlotTW *const trows0 = reinterpret_cast<SlotTW *>(sm + G::BoxPad + G::RowBytes + G::ColBytes);
+    SlotTW *const trows1 = reinterpret_cast<SlotTW *>(sm + G::Stage + G::BoxPad + G::RowBytes + G::ColBytes);
+    SlotTW *const tcols0 = reinterpret_cast<SlotTW *>(sm + G::BoxPad + G::RowBytes + G::ColBytes + G::RowTW);
+    SlotTW *const tcols1 = reinterpret_cast<SlotTW *>(sm + G::Stage + G::BoxPad + G::RowBytes + G::ColBytes + G::RowTW);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) {
-        f_mbar_init(&bar[0]);
-        f_mbar_init(&bar[1]);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (tid < 23) red[tid] = kNoKey;
-    if (!late_trigger) pdl_trigger();  // no inter-CTA waits here: a dependent grid may launch now
-    __syncthreads();
-    pdl_wait();     // Dp / records / keys are written by the stream predecessors
+    const bool prb = (flags & 2) && tid == 0 && blockIdx.x < 4096;
 
     uint64_t acc[NV];
 #pragma unroll
@@ -134,26 +129,30 @@ __global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__re
         }
     };
 
-    int t = t_lo + blockIdx.x;
+    int t = t_lo + cta;
     if (tid == 0 && t < t_hi) issue(t, 0);
     // intra-route CVRP work of this launch (one u slot per warp) while the first
     // tile's TMA is in flight: the whole neighbourhood is one kernel
     if (imask) {
         const int n_units = (x_hi - x_lo + 3) / 4;
-        for (int j = blockIdx.x; j < n_units; j += gridDim.x) {
+        for (int j = cta; j < n_units; j += ncta) {
             const int x = x_lo + 4 * j + warp;
-            if (x < x_hi) intra_cvrp_warp(SV, sp, imask, x, red);
+            if (x < x_hi)
+                intra_cvrp_warp(SV, sp, imask, x, red[warp],
+                                ((flags & 2) && warp == 0 && j == cta && blockIdx.x < 4096) ? g_inter_probe + 8 * blockIdx.x + 4 : nullptr);
         }
     }
+    if (prb) g_inter_probe[8 * blockIdx.x + 1] = gtime();
     uint32_t ph0 = 0u, ph1 = 0u;
-    for (int it = 0; t < t_hi; t += gridDim.x, ++it) {
+    for (int it = 0; t < t_hi; t += ncta, ++it) {
         const int b = it & 1;
-        if (tid == 0 && t + static_cast<int>(gridDim.x) < t_hi) issue(t + gridDim.x, b ^ 1);
+        if (tid == 0 && t + static_cast<int>(ncta) < t_hi) issue(t + ncta, b ^ 1);
         const uint32_t ij = tiles[t];
         const int u0 = (ij >> 16) * U, v0 = (ij & 0xFFFF) * kFastTV;
         const int col = warp * 32 + lane;   // column inside the tile
         const int v = v0 + col;
         if (b) { f_wait(&bar[1], ph1); ph1 ^= 1u; } else { f_wait(&bar[0], ph0); ph0 ^= 1u; }
+        if (prb && it == 0) g_inter_probe[8 * blockIdx.x + 2] = gtime();
         // ---- this lane's column record, bulk-copied with the tile (six 16-byte LDS)
         const SlotRec V = (b ? cols1 : cols0)[col];
         SlotTW VT{};
@@ -256,32 +255,102 @@ __global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__re
         __syncthreads();  // buffer b is refilled two iterations later
     }
 
-    if (late_trigger) pdl_trigger();
+    if (flags & 1) pdl_trigger();
     // ---- fused argmin: warp shuffle -> shared -> one 64-bit atomicMin per variant per CTA
 #pragma unroll
     for (int i = 1; i < NV; ++i) {
         if (!(MASK & (1u << i))) continue;
         const uint64_t k = warp_min64(acc[i]);
-        if (lane == 0 && k != kNoKey) atomicMin(&red[i], static_cast<unsigned long long>(k));
+        if (lane == 0 && k < red[warp][i]) red[warp][i] = k;   // the warp's private row
     }
-    __syncthreads();
-    if (tid < 23 && red[tid] != kNoKey) atomicMin(reinterpret_cast<unsigned long long *>(keys) + tid, red[tid]);
 }
 
-template <int U, bool TW, uint32_t MASK>
-static cudaError_t launch_fast_t(const SlotRec *rec, const SlotTW *rectw, const CUtensorMap &map, const uint32_t *tiles, int t_lo, int t_hi,
-                                 uint32_t Qc, int32_t cap, uint64_t *keys, int grid, cudaStream_t st,
-                                 const SolView<int32_t> &SV, const ScoreParams &sp, uint32_t imask, int x_lo,
-                                 int x_hi) {
-    auto kern = k_inter_fast<U, TW, MASK>;
-    constexpr int smem = FastGeom<U, TW>::Smem;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr = true;
+
+// The launch: CTAs [0, split) evaluate the variants of MASK over every tile,
+// CTAs [split, grid) those of MASK2 (0 = none) -- the all-variant sweep is split
+// in two halves of similar work so that small neighbourhoods get twice the CTAs
+// (and each CTA half the registers' worth of running minima); the intra-route
+// work rides with the second half.
+template <int U, bool TW, uint32_t MASK, uint32_t MASK2>
+__global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__restrict__ rec,
+                                                             const SlotTW *__restrict__ rectw,
+                                                             const __grid_constant__ CUtensorMap tmap,
+                                                             const uint32_t *__restrict__ tiles, int t_lo, int t_hi,
+                                                             uint32_t Qc, int32_t cap, uint64_t *__restrict__ keys,
+                                                             const __grid_constant__ SolView<int32_t> SV,
+                                                             ScoreParams sp, uint32_t imask, int x_lo, int x_hi,
+                                                             int flags, int split) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char *sm = smem_raw + ((128u - (s_u32(smem_raw) & 127u)) & 127u);
+    __shared__ uint64_t bar[2];
+    __shared__ unsigned long long red[kFastThreads / 32][23];   // per-warp minima (no shared 64-bit atomics)
+    const int tid = threadIdx.x;
+    if ((flags & 2) && tid == 0 && blockIdx.x < 4096) g_inter_probe[8 * blockIdx.x] = gtime();
+    if (tid == 0) {
+        f_mbar_init(&bar[0]);
+        f_mbar_init(&bar[1]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    const cudaError_t e = launch_pdl(1, kern, dim3(grid), dim3(kFastThreads), smem, st, rec, rectw, map, tiles, t_lo, t_hi,
-                                     Qc, cap, keys, SV, sp, imask, x_lo, x_hi, pdl_enabled(4) ? 1 : 0);
+    for (int i = tid; i < (kFastThreads / 32) * 23; i += kFastThreads) red[i / 23][i % 23] = kNoKey;
+    if (!(flags & 1)) pdl_trigger();  // no inter-CTA waits here: a dependent grid may launch now
+    __syncthreads();
+    pdl_wait();                       // Dp / records / keys are written by the stream predecessors
+    const int cta = static_cast<int>(blockIdx.x);
+    if (MASK2 == 0 || cta < split)
+        fast_body<U, TW, MASK>(cta, MASK2 ? split : static_cast<int>(gridDim.x), bar, red, sm, rec, rectw, tmap,
+                               tiles, t_lo, t_hi, Qc, cap, keys, SV, sp, MASK2 ? 0u : imask, x_lo, x_hi, flags);
+    else
+        fast_body<U, TW, MASK2>(cta - split, static_cast<int>(gridDim.x) - split, bar, red, sm, rec, rectw, tmap,
+                                tiles, t_lo, t_hi, Qc, cap, keys, SV, sp, imask, x_lo, x_hi, flags);
+    __syncthreads();
+    if (tid < 23) {
+        unsigned long long m = red[0][tid];
+#pragma unroll
+        for (int w = 1; w < kFastThreads / 32; ++w) m = m < red[w][tid] ? m : red[w][tid];
+        if (m != kNoKey) atomicMin(reinterpret_cast<unsigned long long *>(keys) + tid, m);
+    }
+    if ((flags & 2) && tid == 0 && blockIdx.x < 4096) g_inter_probe[8 * blockIdx.x + 3] = gtime();
+}
+
+static bool inter_probe_on() {
+    static const bool on = std::getenv("TGA_INTER_PROBE") != nullptr;
+    return on;
+}
+
+template <int U, bool TW, uint32_t MASK, uint32_t MASK2>
+static cudaError_t launch_fast_t(const SlotRec *rec, const SlotTW *rectw, const CUtensorMap &map, const uint32_t *tiles,
+                                 int t_lo, int t_hi, uint32_t Qc, int32_t cap, uint64_t *keys, int units_max,
+                                 cudaStream_t st, const SolView<int32_t> &SV, const ScoreParams &sp, uint32_t imask,
+                                 int x_lo, int x_hi) {
+    auto kern = k_inter_fast<U, TW, MASK, MASK2>;
+    using G = FastGeom<U, TW>;
+    // resident CTAs per SM with one / two pipeline stages (a persistent grid never exceeds them)
+    static int res1 = 0, res2 = 0;
+    if (!res1) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::Smem);
+        int dev = 0, sms = 0, b1 = 0, b2 = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, kern, kFastThreads, G::Smem1);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, kern, kFastThreads, G::Smem);
+        res1 = std::max(1, b1) * std::max(1, sms);
+        res2 = std::max(1, b2) * std::max(1, sms);
+    }
+    const int groups = MASK2 ? 2 : 1;
+    const int tiles_n = t_hi - t_lo;
+    const int units = imask ? (x_hi - x_lo + 3) / 4 : 0;
+    int per_group = std::max(tiles_n, MASK2 ? 0 : units);
+    int smem = G::Smem1, grid;
+    if (per_group * groups <= res1) {
+        grid = std::max(1, per_group) * groups;   // one tile per CTA: a single stage
+    } else {
+        smem = G::Smem;
+        grid = std::max(groups, std::min(per_group * groups, std::min(res2, units_max)));
+    }
+    const int split = MASK2 ? grid / 2 : grid;
+    const int flags = (pdl_enabled(4) ? 1 : 0) | (inter_probe_on() ? 2 : 0);
+    const cudaError_t e = launch_pdl(1, kern, dim3(grid), dim3(kFastThreads), smem, st, rec, rectw, map, tiles, t_lo,
+                                     t_hi, Qc, cap, keys, SV, sp, imask, x_lo, x_hi, flags, split);
     note_launch();
     return e != cudaSuccess ? e : cudaGetLastError();
 }
@@ -295,22 +364,32 @@ static cudaError_t launch_fast_u(uint32_t mask, const SlotRec *rec, const SlotTW
     if (!(mask & 0x7FEu)) return cudaSuccess;
     cudaError_t err = cudaSuccess;
     // the intra-route work rides along with the first launch
-    const int units = imask ? (x_hi - x_lo + 3) / 4 : 0;
-    auto run = [&](auto kmask) {
+    auto run = [&](auto kmask, auto kmask2) {
         if (err != cudaSuccess) return;
-        const int grid = std::max(1, std::min(std::max(t_hi - t_lo, units), max_grid));
-        err = launch_fast_t<U, TW, decltype(kmask)::value>(rec, rectw, map, tiles, t_lo, t_hi, Qc, cap, keys, grid, st,
-                                                           SV, sp, imask, x_lo, x_hi);
+        err = launch_fast_t<U, TW, decltype(kmask)::value, decltype(kmask2)::value>(
+            rec, rectw, map, tiles, t_lo, t_hi, Qc, cap, keys, max_grid, st, SV, sp, imask, x_lo, x_hi);
         imask = 0;
     };
-    constexpr uint32_t ALL = 0x7FEu, NS = (1u << 1) | (1u << 2) | (1u << 5);
-    if ((mask & ALL) == ALL) { run(std::integral_constant<uint32_t, ALL>{}); return err; }
-    if ((mask & NS) == NS) { run(std::integral_constant<uint32_t, NS>{}); mask &= ~NS; }
-    if (mask & (1u << 1)) run(std::integral_constant<uint32_t, (1u << 1)>{});
-    if (mask & (1u << 2)) run(std::integral_constant<uint32_t, (1u << 2)>{});
-    if (mask & (3u << 3)) run(std::integral_constant<uint32_t, (3u << 3)>{});
-    if (mask & (1u << 5)) run(std::integral_constant<uint32_t, (1u << 5)>{});
-    if (mask & (0x1Fu << 6)) run(std::integral_constant<uint32_t, (0x1Fu << 6)>{});
+    using Z = std::integral_constant<uint32_t, 0u>;
+    // all inter variants: {2-opt*, relocate, or-opt, swap(1,1), cross(2,2)} | {cross (1,2) (1,3) (2,3) (3,3)}
+    constexpr uint32_t ALL = 0x7FEu, HA = 0x13Eu, HB = 0x6C0u, NS = (1u << 1) | (1u << 2) | (1u << 5);
+    static_assert((HA | HB) == ALL && (HA & HB) == 0, "halves");
+    if ((mask & ALL) == ALL) {
+        // split in halves only while the whole sweep has at most one tile per CTA of the
+        // unsplit persistent grid (small neighbourhoods: twice the CTAs); above that the
+        // halves would pay the per-tile loads and folds twice
+        if (t_hi - t_lo <= max_grid)
+            run(std::integral_constant<uint32_t, HA>{}, std::integral_constant<uint32_t, HB>{});
+        else
+            run(std::integral_constant<uint32_t, ALL>{}, Z{});
+        return err;
+    }
+    if ((mask & NS) == NS) { run(std::integral_constant<uint32_t, NS>{}, Z{}); mask &= ~NS; }
+    if (mask & (1u << 1)) run(std::integral_constant<uint32_t, (1u << 1)>{}, Z{});
+    if (mask & (1u << 2)) run(std::integral_constant<uint32_t, (1u << 2)>{}, Z{});
+    if (mask & (3u << 3)) run(std::integral_constant<uint32_t, (3u << 3)>{}, Z{});
+    if (mask & (1u << 5)) run(std::integral_constant<uint32_t, (1u << 5)>{}, Z{});
+    if (mask & (0x1Fu << 6)) run(std::integral_constant<uint32_t, (0x1Fu << 6)>{}, Z{});
     return err;
 }
 
@@ -330,3 +409,7 @@ cudaError_t launch_inter_fast(int U, uint32_t mask, const SlotRec *rec, const Sl
 }
 
 }  // namespace tga
+
+extern "C" int32_t tga_debug_inter_probe(uint64_t *out, int32_t n) {
+    return cudaMemcpyFromSymbol(out, tga::g_inter_probe, sizeof(uint64_t) * static_cast<size_t>(n)) == cudaSuccess ? 0 : -5;
+}

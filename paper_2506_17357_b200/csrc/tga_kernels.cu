@@ -1275,14 +1275,17 @@ __global__ void __launch_bounds__(256) k_intra_tw_batch(const SolView<DT> *__res
 // Loads are unchanged by intra moves (Eq. 3f), so feasibility is the route's.
 __global__ void __launch_bounds__(256) k_intra_cvrp(const SolView<int32_t> S, ScoreParams sp, uint32_t vmask,
                                                     int x_lo, int x_hi, uint64_t *__restrict__ keys) {
-    __shared__ unsigned long long red[23];
-    if (threadIdx.x < 23) red[threadIdx.x] = kNoKey;
+    __shared__ unsigned long long red[8][23];   // one private row per warp
+    for (int i = threadIdx.x; i < 8 * 23; i += blockDim.x) red[i / 23][i % 23] = kNoKey;
     __syncthreads();
     const int x = x_lo + static_cast<int>(blockIdx.x) * 8 + (threadIdx.x >> 5);
-    if (x < x_hi) intra_cvrp_warp(S, sp, vmask, x, red);
+    if (x < x_hi) intra_cvrp_warp(S, sp, vmask, x, red[threadIdx.x >> 5]);
     __syncthreads();
-    if (threadIdx.x < 23 && red[threadIdx.x] != kNoKey)
-        atomicMin(reinterpret_cast<unsigned long long *>(keys) + threadIdx.x, red[threadIdx.x]);
+    if (threadIdx.x < 23) {
+        unsigned long long m = red[0][threadIdx.x];
+        for (int w = 1; w < 8; ++w) m = m < red[w][threadIdx.x] ? m : red[w][threadIdx.x];
+        if (m != kNoKey) atomicMin(reinterpret_cast<unsigned long long *>(keys) + threadIdx.x, m);
+    }
 }
 
 // ============================================================== launchers

@@ -39,8 +39,12 @@ struct FastGeom {
     static constexpr int ColBytes = kFastTV * 96;               // column records (bulk copy)
     static constexpr int RowTW = TW ? U * 64 : 0;               // time-window parts
     static constexpr int ColTW = TW ? kFastTV * 64 : 0;
-    static constexpr int Smem = 2 * BoxPad + 2 * RowBytes + 2 * ColBytes + 2 * RowTW + 2 * ColTW + 128;
-    static_assert(RowBytes % 128 == 0 && ColBytes % 128 == 0, "bulk copy alignment");
+    // one pipeline stage = box + row/column records; two stages when a CTA
+    // walks several tiles (double buffering), one when it has a single tile
+    static constexpr int Stage = BoxPad + RowBytes + ColBytes + RowTW + ColTW;
+    static constexpr int Smem = 2 * Stage + 128;
+    static constexpr int Smem1 = Stage + 128;
+    static_assert(RowBytes % 128 == 0 && ColBytes % 128 == 0 && Stage % 128 == 0, "bulk copy alignment");
 };
 constexpr int kGuard = 8;                       // guard slots before/after every slot array
 

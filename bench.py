@@ -46,6 +46,10 @@ ALG_OPS = {1: 10, 2: 11, 3: 11, 4: 11, 5: 18, 6: 18, 7: 18, 8: 18, 9: 18, 10: 18
            0: 5, 11: 5, 12: 5, 13: 5}
 for _v in range(14, 23):
     ALG_OPS[_v] = 9
+# VRPTW TW-I fast path (inter variants): the CVRP terms plus, per new route
+# F + seg + B, the Eq. 4 check in T_V = 0 form: 2-opt* two
+# (add + compare) checks, relocate one 6-op check per direction, swap/cross two.
+ALG_OPS_TW = {1: 14, 2: 17, 3: 17, 4: 17, 5: 30, 6: 30, 7: 30, 8: 30, 9: 30, 10: 30}
 
 
 def parse():
@@ -398,7 +402,8 @@ def run_tga(args):
     shard_div = ws if row_shard else 1   # a launch evaluates 1/N of the rows when row-sharded
     inter_cands = float(sum(int(dev_counts[v]) for v in inter_sel)) / K / shard_div
     alg_bytes = (Qp * Qp / 2.0) * 4.0 / shard_div       # Dp upper triangle, int32
-    alg_ops = float(sum(int(dev_counts[v]) * ALG_OPS[v] for v in inter_sel)) / K / shard_div
+    ops_tab = ALG_OPS if inst.tw is None else ALG_OPS_TW
+    alg_ops = float(sum(int(dev_counts[v]) * ops_tab[v] for v in inter_sel)) / K / shard_div
     sm_mhz_peak = float(pk.get("sm_max_mhz", 1965.0))
     alu_peak = 148 * 128 * sm_mhz_peak * 1e6            # lane-ops/s (4 SMSP x 32 lanes x 1 issue/clk)
     hbm_peak = float(pk["hbm_gbs"]) * 1e9
@@ -412,7 +417,10 @@ def run_tga(args):
                 "traffic": traffic_for(args.config),
                 "peak_source": f"148 SM x 128 lanes x {sm_mhz_peak:.0f} MHz ({pk_src} sm_max_mhz)"}
     primary, alt = (alu_view, hbm_view) if t_alu >= t_hbm else (hbm_view, alu_view)
-    primary = dict(primary, kernel="k_inter_fast<all-inter> (CVRP: inter tiles + intra warps in one launch), live CUDA events",
+    primary = dict(primary, kernel=("k_inter_fast<all-inter> (CVRP: inter tiles + intra warps in one launch)"
+                                    if inst.tw is None else
+                                    "k_inter_fast<TW, all-inter> (VRPTW inter tiles; intra in its own kernel)")
+                   + ", live CUDA events",
                    kernel_ms=inter_avg_s * 1e3, candidates_per_launch=inter_cands,
                    alg_bytes_per_launch=alg_bytes, alg_ops_per_launch=alg_ops)
 
@@ -490,7 +498,8 @@ def run_tga(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K,
         "warmup": max(args.warmup, 3), "ms_per_step": tot_ms / K, "higher_is_better": True,
-        "scaling": "strong" if row_shard else "weak", "vs_baseline": None, "dtype": "int32",
+        "scaling": "strong" if row_shard else "weak", "vs_baseline": None,
+        "dtype": "int32" if inst.tw is None else "f32 (integer-valued TW-I times; int32 loads)",
         "data": "synthetic",
         "config": {"workload": f"{args.config}: {G.CONFIGS.get(args.config, args.config)}; "
                                "step = eval all variants + best move + apply",

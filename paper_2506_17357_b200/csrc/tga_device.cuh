@@ -103,26 +103,24 @@ __device__ __forceinline__ uint64_t score_key(const ScoreParams &sp, bool valid,
 
 // ------------------------------------------------------------------ per-slot record (CVRP fast path)
 // Everything the fused inter-route kernel needs about one slot x in one
-// 96-byte record, so a tile row is one bulk copy and a lane's column is six
+// 80-byte record, so a tile row is one bulk copy and a lane's column is five
 // 16-byte loads.  Validity is folded into the load terms: an invalid role
 // carries kPoison in a load that is compared against the capacity, so the
 // candidate fails the capacity test without a branch (feasible-only mode).
 constexpr int32_t kPoison = 1 << 28;
 struct __align__(16) SlotRec {
-    int32_t c;       // canonical id, -1 for an end depot / padding
-    int32_t r;       // route id, -1 for padding
-    int32_t fL;      // prefix load of [0..x]               (2-opt* head),  +P if c < 0
-    int32_t bL1;     // suffix load of [x+1..L+1]            (2-opt* tail),  +P if c < 0
+    int32_t r;       // route id; -1 for an end depot, a spare slot or padding (not a canonical slot)
+    int32_t fL;      // prefix load of [0..x]               (2-opt* head),  +P if r < 0
+    int32_t bL1;     // suffix load of [x+1..L+1]            (2-opt* tail),  +P if r < 0
     int32_t ne;      // -e(x), e(x) = c(x, x+1)
-    int32_t W;       // route load (insertion target),       +P if c < 0
+    int32_t W;       // route load (insertion target),       +P if r < 0
     int32_t so[3];   // relocate-out load s_N of x..x+N-1,   +P if the segment is invalid or W - s_N > Q
     int32_t rem[3];  // relocate-out distance c(x-1, x+N) - e(x-1) - e(x+N-1)  (Eq. 2)
     int32_t sA[3];   // swap: W - s_N,                       +P if the segment is invalid
     int32_t sS[3];   // swap: s_N
     int32_t sE[3];   // swap: -e(x-1) - e(x+N-1)
-    int32_t pad[3];
 };
-static_assert(sizeof(SlotRec) == 96, "SlotRec layout");
+static_assert(sizeof(SlotRec) == 80, "SlotRec layout: five 16-byte shared loads per column");
 
 // Time-window part of the fast-path record (VRPTW "TW-I", feasible-only mode).
 // With T_V = 0 on both sides, T_V(s1 + s2) == 0  <=>  T_E(s1)+T_D(s1)+t <= T_L(s2)
@@ -259,11 +257,22 @@ __device__ __forceinline__ void intra_cvrp_warp(const SolView<int32_t> &S, const
                 k[var] = intra_k32(ok, q == p + a ? adj : gap, lane);
             }
         }
-        // phase 2: one REDUX.MIN per variant
+        // phase 2: one REDUX.MIN per variant, all issued before lane 0 merges them
+        // into the warp's private row (independent read-min-writes)
         if (qb == 0) stamp(2);
+        uint32_t m[23];
 #pragma unroll
         for (int i = 0; i < 23; ++i)
-            if ((i == 0 || i >= 11) && (vmask & (1u << i))) warp_keep(red, i, k[i], ib, lane);
+            m[i] = ((i == 0 || i >= 11) && (vmask & (1u << i))) ? __reduce_min_sync(0xffffffffu, k[i]) : 0xFFFFFFFFu;
+        if (lane == 0) {
+#pragma unroll
+            for (int i = 0; i < 23; ++i) {
+                if (!(i == 0 || i >= 11) || m[i] == 0xFFFFFFFFu) continue;
+                const int32_t sc = static_cast<int32_t>(m[i] >> 5) - (1 << 25);
+                const unsigned long long key = pack_key(ord_score(sc), ib + (m[i] & 31u));
+                if (key < red[i]) red[i] = key;
+            }
+        }
     }
     stamp(3);
 }

@@ -10,7 +10,7 @@
 //     the U+4 row records one bulk copy, both double-buffered across the
 //     persistent tile loop on mbarriers;
 //   * every row-only or column-only term (removal gains, segment loads, route
-//     loads, validity) is precomputed in the 96-byte SlotRec; validity is a
+//     loads, validity) is precomputed in the 80-byte SlotRec; validity is a
 //     poisoned load, so each candidate is: a few adds, one capacity compare,
 //     one select and one compare-and-keep.
 #include <cuda.h>
@@ -153,7 +153,7 @@ __device__ __forceinline__ void fast_body(const int cta, const int ncta, uint64_
         const int v = v0 + col;
         if (b) { f_wait(&bar[1], ph1); ph1 ^= 1u; } else { f_wait(&bar[0], ph0); ph0 ^= 1u; }
         if (prb && it == 0) g_inter_probe[8 * blockIdx.x + 2] = gtime();
-        // ---- this lane's column record, bulk-copied with the tile (six 16-byte LDS)
+        // ---- this lane's column record, bulk-copied with the tile (five 16-byte LDS)
         const SlotRec V = (b ? cols1 : cols0)[col];
         SlotTW VT{};
         if (TW) VT = (b ? tcols1 : tcols0)[col];
@@ -171,9 +171,9 @@ __device__ __forceinline__ void fast_body(const int cta, const int ncta, uint64_
 #pragma unroll
         for (int i = 0; i < U; ++i) {
             const SlotRec &A = RW[i];       // row u = u0 + i (broadcast reads)
-            const int32_t cu = A.c, ru = A.r;
+            const int32_t ru = A.r;
             const int u = u0 + i;            // physical row slot (key index = u * pitch + v)
-            if (cu < 0) continue;            // warp-uniform: end depot / padding row
+            if (ru < 0) continue;            // warp-uniform: end depot / spare / padding row
             if (!(ru < V.r)) continue;       // pair must span two routes, route(u) < route(v)
             const SlotTW &AT = TR[TW ? i : 0];
             // time-window check of  F + seg + B  (Eq. 4 in the T_V = 0 form of SlotTW):
@@ -236,7 +236,7 @@ __device__ __forceinline__ void fast_body(const int cta, const int ncta, uint64_
             }
         }
         // ---- fold this tile's streams into the per-variant 64-bit keys
-        if (V.c >= 0) {
+        if (V.r >= 0) {
             const uint32_t cv = static_cast<uint32_t>(v);  // physical column slot
             if (MASK & (1u << 1)) fold(acc[1], run[0], true, u0, cv, Qc);
 #pragma unroll

@@ -66,7 +66,7 @@ __device__ __forceinline__ void scan_route_g(const ScanArgs<DT> &A, const int r,
         for (int k = len + lane; k < cap; k += 32) {
             if (A.rec) {
                 SlotRec q{};
-                q.c = -1; q.r = -1; q.fL = q.bL1 = q.W = kPoison;
+                q.r = -1; q.fL = q.bL1 = q.W = kPoison;
                 for (int j = 0; j < 3; ++j) { q.so[j] = kPoison; q.sA[j] = kPoison; }
                 A.rec[base + k] = q;
             }
@@ -231,8 +231,7 @@ __device__ __forceinline__ void scan_route_g(const ScanArgs<DT> &A, const int r,
                 const bool slot = k <= L;  // canonical slot (not the end depot)
                 const int32_t e_x = A.enext[x], e_prev = (k >= 1) ? A.enext[x - 1] : 0;
                 const int32_t fl_prev = (k >= 1) ? A.fwdL[x - 1] : 0;
-                q.c = slot ? canonAt(x) : -1;
-                q.r = r;
+                q.r = (slot && canonAt(x) >= 0) ? r : -1;
                 q.fL = slot ? A.fwdL[x] : kPoison;
                 q.bL1 = (slot && k + 1 < len) ? A.bwdL[x + 1] : kPoison;
                 q.ne = -e_x;
@@ -273,7 +272,6 @@ __device__ __forceinline__ void scan_route_g(const ScanArgs<DT> &A, const int r,
                     q.sS[N - 1] = sN;
                     q.sE[N - 1] = segok ? -e_prev - eout : 0;
                 }
-                q.pad[0] = q.pad[1] = q.pad[2] = 0;
                 A.rec[x] = q;
             }
         }
@@ -1090,19 +1088,21 @@ template <class DT>
 __device__ __forceinline__ void intra_tw_warp(const SolView<DT> &S, const ScoreParams &sp, uint32_t vmask, int x,
                                               unsigned long long *red) {
     const int lane = threadIdx.x & 31;
-    if (!(S.canon[x] >= 0 && S.pos[x] >= 1)) return;  // warp-uniform
-    const int p = S.pos[x], L = S.rlen[x], r = S.route[x];
+    auto D = [&](int a, int b) -> DT { return S.Dp[static_cast<size_t>(a) * S.pitch + b]; };
+    auto E = [&](int y) -> DT { return S.enext[y]; };
+    // ---- slot x: everything indexed by x alone, one round of loads
+    const int cx = S.canon[x], p = S.pos[x], L = S.rlen[x], r = S.route[x];
+    const TwRec F = S.fwdT[x - 1];
+    const TwRec sg2x = S.seg2T[x], sg3x = S.seg3T[x];
+    const int nx = S.node[x];
+    const DT Exm1 = E(x - 1), Ex0 = E(x), Ex1 = E(x + 1), Ex2 = E(x + 2);
+    const DT br1 = S.bridge1[x], br2 = S.bridge2[x], br3 = S.bridge3[x];
+    if (!(cx >= 0 && p >= 1)) return;  // warp-uniform
     const int base = x - p;
     const int W = S.rW[r];
     const float TV0 = S.rTV[r];
-    const uint32_t cu = static_cast<uint32_t>(S.canon[x]);
-    const uint32_t cbase = cu - static_cast<uint32_t>(p);
-    auto D = [&](int a, int b) -> DT { return S.Dp[static_cast<size_t>(a) * S.pitch + b]; };
-    auto tf = [&](int a, int b) -> float { return static_cast<float>(D(a, b)); };
-    auto single = [&](int y) -> TwRec { return S.node_tw[S.node[y]]; };
-    auto seg = [&](int y, int N) -> TwRec { return N == 1 ? single(y) : (N == 2 ? S.seg2T[y] : S.seg3T[y]); };
-    auto E = [&](int y) -> DT { return S.enext[y]; };
-    auto bridge = [&](int y, int N) -> DT { return N == 1 ? S.bridge1[y] : (N == 2 ? S.bridge2[y] : S.bridge3[y]); };
+    const TwRec segx[3] = {S.node_tw[nx], sg2x, sg3x};
+    const DT brg[3] = {br1, br2, br3}, Exn[3] = {Ex0, Ex1, Ex2};  // E(x + N - 1)
     auto keyof = [&](bool ok, DT dD, float tv, int q) -> uint64_t {
         return score_key<DT, true>(sp, ok, dD, W, 0, W, 0, tv, 0.f, TV0, 0.f,
                                    static_cast<uint32_t>(x) * S.Qc + static_cast<uint32_t>(base + q));
@@ -1112,56 +1112,56 @@ __device__ __forceinline__ void intra_tw_warp(const SolView<DT> &S, const ScoreP
     for (int i = 0; i < 23; ++i) best[i] = kNoKey;
 
     // ------------------------------------------------ forward pass (chunks left to right)
-    TwRec cP[3], cG[3];  // carries: relocate-forward prefix, swap middle
-    bool hP[3] = {false, false, false}, hG[3] = {false, false, false};
+    // G_a(q) = [x+a .. q] (plain scan from q = p+a); relocate-forward prefixes are
+    // F(x-1) + G_N(q) by associativity of Eq. 4 (exact on integer-valued times)
+    TwRec cG[3];
+    bool hG[3] = {false, false, false};
     for (int qb = 0; qb <= L; qb += 32) {
         const int q = qb + lane;
         const bool in = q <= L;
         const int v = base + min(q, L);
-        const TwRec sv = single(v);
-        const float inl0 = q >= 1 ? static_cast<float>(E(v - 1)) : 0.f;  // link (q-1 -> q)
+        // lane data, loaded up front (masked lanes read slots of this or the next route)
+        const int nv = S.node[v];
+        const DT Evm1 = E(max(v - 1, base)), Ev0 = E(v), Ev1 = E(v + 1), Ev2 = E(v + 2);
+        const TwRec bw[3] = {S.bwdT[v + 1], S.bwdT[v + 2], S.bwdT[v + 3]};
+        const TwRec sg2 = S.seg2T[v], sg3 = S.seg3T[v];
+        const DT dm1 = D(x - 1, v), dxm = D(x, max(v - 1, base));
+        DT d[4][4];  // Dp(x + i, v + j) = c(node(x + i), node(v + j)), c symmetric
 #pragma unroll
-        for (int N = 1; N <= 3; ++N) {
-            const int var = 10 + N;
-            if (!(vmask & (1u << var)) || p + N - 1 > L) continue;
-            // P(q) = F(x-1) + [x+N .. q], element at q = p+N carries F(x-1) (link = bridge_N)
-            const int st = p + N;
-            TwRec el = sv;
-            float inl = inl0;
-            if (q == st) { el = tw_cat(S.fwdT[x - 1], sv, static_cast<float>(bridge(x, N))); inl = 0.f; }
-            const int s_rel = max(st - qb, 0);
-            TwRec P = scan_fwd(el, inl, lane, s_rel);
-            if (hP[N - 1] && lane >= s_rel) P = tw_cat(cP[N - 1], P, inl);
-            if (st <= qb + 31) {   // carry: the run covers the whole chunk from here on
-                cP[N - 1] = shfl_rec(P, 31);
-                hP[N - 1] = true;
-            }
-            if (in && q >= st) {
-                const DT rem = bridge(x, N) - E(x - 1) - E(x + N - 1);
-                const DT dD = rem + D(v, x) + D(x + N - 1, v + 1) - E(v);
-                const TwRec A2 = tw_cat(P, seg(x, N), tf(v, x));
-                const float tv = tw_cat(A2, S.bwdT[v + 1], tf(x + N - 1, v + 1)).w;
-                best[var] = umin64(best[var], keyof(true, dD, tv, q));
-            }
-        }
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) d[i][j] = (i == 3 && j == 3) ? DT(0) : D(x + i, v + j);
+        const TwRec sv = S.node_tw[nv];
+        const TwRec segv[3] = {sv, sg2, sg3};
+        const DT Evb[3] = {Ev0, Ev1, Ev2};  // E(v + b - 1)
+        const float inl0 = q >= 1 ? static_cast<float>(Evm1) : 0.f;  // link (q-1 -> q)
 #pragma unroll
         for (int a = 1; a <= 3; ++a) {
-            bool any = false;
+            bool any_sw = false;
 #pragma unroll
-            for (int b = 1; b <= 3; ++b) any |= (vmask >> (14 + 3 * (a - 1) + (b - 1))) & 1u;
-            if (!any || p + a - 1 > L) continue;
-            // G(k) = [x+a .. k] for k >= p+a; lane q uses G(q-1) (empty at q = p+a)
+            for (int b = 1; b <= 3; ++b) any_sw |= (vmask >> (14 + 3 * (a - 1) + (b - 1))) & 1u;
+            const bool need_rl = (vmask >> (10 + a)) & 1u;
+            if (!(any_sw || need_rl) || p + a - 1 > L) continue;
             const int st = p + a;
-            TwRec el = sv;
             float inl = inl0;
             const int s_rel = max(st - qb, 0);
-            TwRec Gk = scan_fwd(el, inl, lane, s_rel);
+            TwRec Gk = scan_fwd(sv, inl, lane, s_rel);
             if (hG[a - 1] && lane >= s_rel) Gk = tw_cat(cG[a - 1], Gk, inl);
             TwRec Gm = shfl_up_rec(Gk, 1);  // G(q-1)
             if (lane == 0) Gm = cG[a - 1];
-            if (st <= qb + 31) {
+            if (st <= qb + 31) {  // carry: the run covers the whole chunk from here on
                 cG[a - 1] = shfl_rec(Gk, 31);
                 hG[a - 1] = true;
+            }
+            if (need_rl) {  // relocate N = a after q >= p+N:  [F(x-1) + x+N .. q] + S(x,N) + B(q+1)
+                const int N = a;
+                const bool ok = in && q >= st;
+                const DT rem = brg[N - 1] - Exm1 - Exn[N - 1];
+                const DT dD = rem + d[0][0] + d[N - 1][1] - Ev0;
+                const TwRec P = tw_cat(F, Gk, static_cast<float>(brg[N - 1]));
+                const TwRec A2 = tw_cat(P, segx[N - 1], static_cast<float>(d[0][0]));
+                const float tv = tw_cat(A2, bw[0], static_cast<float>(d[N - 1][1])).w;
+                best[10 + N] = umin64(best[10 + N], keyof(ok, dD, tv, q));
             }
 #pragma unroll
             for (int b = 1; b <= 3; ++b) {
@@ -1169,21 +1169,18 @@ __device__ __forceinline__ void intra_tw_warp(const SolView<DT> &S, const ScoreP
                 if (!(vmask & (1u << var))) continue;
                 const bool ok = in && q >= p + a && q + b - 1 <= L;
                 if (!__any_sync(0xffffffffu, ok)) continue;
-                const int vv = ok ? v : base + p + a;  // masked lanes read valid slots
-                const TwRec sq = seg(vv, b);
+                const TwRec R1 = tw_cat(F, segv[b - 1], static_cast<float>(dm1));
                 DT dD;
                 float tv;
-                const TwRec R1 = tw_cat(S.fwdT[x - 1], sq, tf(x - 1, vv));
                 if (q == p + a) {  // adjacent
-                    dD = D(x - 1, vv) + D(vv + b - 1, x) + D(x + a - 1, vv + b) - E(x - 1) - E(vv - 1) - E(vv + b - 1);
-                    const TwRec R3 = tw_cat(R1, seg(x, a), tf(vv + b - 1, x));
-                    tv = tw_cat(R3, S.bwdT[vv + b], tf(x + a - 1, vv + b)).w;
+                    dD = dm1 + d[0][b - 1] + d[a - 1][b] - Exm1 - Evm1 - Evb[b - 1];
+                    const TwRec R3 = tw_cat(R1, segx[a - 1], static_cast<float>(d[0][b - 1]));
+                    tv = tw_cat(R3, bw[b - 1], static_cast<float>(d[a - 1][b])).w;
                 } else {
-                    dD = D(x - 1, vv) + D(vv + b - 1, x + a) + D(vv - 1, x) + D(x + a - 1, vv + b) - E(x - 1) -
-                         E(x + a - 1) - E(vv - 1) - E(vv + b - 1);
-                    const TwRec R2 = tw_cat(R1, Gm, tf(vv + b - 1, x + a));
-                    const TwRec R3 = tw_cat(R2, seg(x, a), tf(vv - 1, x));
-                    tv = tw_cat(R3, S.bwdT[vv + b], tf(x + a - 1, vv + b)).w;
+                    dD = dm1 + d[a][b - 1] + dxm + d[a - 1][b] - Exm1 - Exn[a - 1] - Evm1 - Evb[b - 1];
+                    const TwRec R2 = tw_cat(R1, Gm, static_cast<float>(d[a][b - 1]));
+                    const TwRec R3 = tw_cat(R2, segx[a - 1], static_cast<float>(dxm));
+                    tv = tw_cat(R3, bw[b - 1], static_cast<float>(d[a - 1][b])).w;
                 }
                 best[var] = umin64(best[var], keyof(ok, dD, tv, q));
             }
@@ -1192,14 +1189,22 @@ __device__ __forceinline__ void intra_tw_warp(const SolView<DT> &S, const ScoreP
     // ------------------------------------------------ backward pass: relocate before the segment
     if (p >= 2) {
         const int nch = (p - 1) / 32 + 1;  // element positions up to p-1 (lane q reads Suf(q+1))
+        const TwRec bwx[3] = {S.bwdT[x + 1], S.bwdT[x + 2], S.bwdT[x + 3]};
         TwRec cS[3];
         bool hS[3] = {false, false, false};
         for (int ci = nch - 1; ci >= 0; --ci) {
             const int qb = ci * 32;
             const int k = qb + lane;                 // element position k in [1, p-1]; lane q uses Suf(q+1)
             const int vk = base + min(max(k, 1), p - 1);
-            const TwRec sk = single(vk);
-            float outl = static_cast<float>(E(vk));  // link (k -> k+1)
+            const int q = qb + lane;
+            const int vq = base + min(q, p - 2);
+            // lane data, loaded up front
+            const int nk = S.node[vk];
+            const float outl = static_cast<float>(E(vk));  // link (k -> k+1)
+            const DT Evq = E(vq);
+            const TwRec Fq = S.fwdT[vq];
+            const DT dq0 = D(x, vq), dq1[3] = {D(x, vq + 1), D(x + 1, vq + 1), D(x + 2, vq + 1)};
+            const TwRec sk = S.node_tw[nk];
 #pragma unroll
             for (int N = 1; N <= 3; ++N) {
                 const int var = 10 + N;
@@ -1207,7 +1212,7 @@ __device__ __forceinline__ void intra_tw_warp(const SolView<DT> &S, const ScoreP
                 // Suf(k) = [k .. x-1] + B(x+N); the element at k = p-1 carries B(x+N) (link = bridge_N)
                 TwRec el = sk;
                 float ol = outl;
-                if (k == p - 1) { el = tw_cat(sk, S.bwdT[x + N], static_cast<float>(bridge(x, N))); ol = 0.f; }
+                if (k == p - 1) { el = tw_cat(sk, bwx[N - 1], static_cast<float>(brg[N - 1])); ol = 0.f; }
                 const int e_rel = min(p - 1 - qb, 31);
                 TwRec Sf = scan_bwd(el, ol, lane, e_rel);
                 if (hS[N - 1] && lane <= e_rel) Sf = tw_cat(Sf, cS[N - 1], ol);
@@ -1218,14 +1223,12 @@ __device__ __forceinline__ void intra_tw_warp(const SolView<DT> &S, const ScoreP
                 // lane q = qb + lane inserts after position q: needs Suf(q+1)
                 TwRec Sn = shfl_down_rec(Sf, 1);
                 if (lane == 31) Sn = had ? carry_in : Sf;
-                const int q = qb + lane;
                 const bool ok = q <= p - 2;
                 if (!__any_sync(0xffffffffu, ok)) continue;
-                const int vq = base + min(q, p - 2);
-                const DT rem = bridge(x, N) - E(x - 1) - E(x + N - 1);
-                const DT dD = rem + D(vq, x) + D(x + N - 1, vq + 1) - E(vq);
-                const TwRec A2 = tw_cat(S.fwdT[vq], seg(x, N), tf(vq, x));
-                const float tv = tw_cat(A2, Sn, tf(x + N - 1, vq + 1)).w;
+                const DT rem = brg[N - 1] - Exm1 - Exn[N - 1];
+                const DT dD = rem + dq0 + dq1[N - 1] - Evq;
+                const TwRec A2 = tw_cat(Fq, segx[N - 1], static_cast<float>(dq0));
+                const float tv = tw_cat(A2, Sn, static_cast<float>(dq1[N - 1])).w;
                 best[var] = umin64(best[var], keyof(ok, dD, tv, q));
             }
         }
@@ -1234,37 +1237,43 @@ __device__ __forceinline__ void intra_tw_warp(const SolView<DT> &S, const ScoreP
     for (int i = 11; i < 23; ++i) {
         if (!(vmask & (1u << i))) continue;
         const uint64_t m = warp_min64(best[i]);
-        if (lane == 0 && m != kNoKey) atomicMin(&red[i], static_cast<unsigned long long>(m));
+        if (lane == 0 && m != kNoKey && m < red[i]) red[i] = m;  // the warp's private row
     }
 }
 
 template <class DT>
 __global__ void __launch_bounds__(256) k_intra_tw(const __grid_constant__ SolView<DT> S, ScoreParams sp,
                                                   uint32_t vmask, int x_lo, int x_hi, uint64_t *__restrict__ keys) {
-    __shared__ unsigned long long red[23];
-    if (threadIdx.x < 23) red[threadIdx.x] = kNoKey;
+    __shared__ unsigned long long red[8][23];   // one private row per warp
+    for (int i = threadIdx.x; i < 8 * 23; i += blockDim.x) red[i / 23][i % 23] = kNoKey;
     __syncthreads();
     const int x = x_lo + static_cast<int>(blockIdx.x) * 8 + (threadIdx.x >> 5);
-    if (x < x_hi) intra_tw_warp<DT>(S, sp, vmask, x, red);
+    if (x < x_hi) intra_tw_warp<DT>(S, sp, vmask, x, red[threadIdx.x >> 5]);
     __syncthreads();
-    if (threadIdx.x < 23 && red[threadIdx.x] != kNoKey)
-        atomicMin(reinterpret_cast<unsigned long long *>(keys) + threadIdx.x, red[threadIdx.x]);
+    if (threadIdx.x < 23) {
+        unsigned long long m = red[0][threadIdx.x];
+        for (int w = 1; w < 8; ++w) m = m < red[w][threadIdx.x] ? m : red[w][threadIdx.x];
+        if (m != kNoKey) atomicMin(reinterpret_cast<unsigned long long *>(keys) + threadIdx.x, m);
+    }
 }
 
 // population mode: blockIdx.y = solution
 template <class DT>
 __global__ void __launch_bounds__(256) k_intra_tw_batch(const SolView<DT> *__restrict__ views, ScoreParams sp,
                                                         uint32_t vmask, uint64_t *__restrict__ keys) {
-    __shared__ unsigned long long red[23];
-    if (threadIdx.x < 23) red[threadIdx.x] = kNoKey;
+    __shared__ unsigned long long red[8][23];   // one private row per warp
+    for (int i = threadIdx.x; i < 8 * 23; i += blockDim.x) red[i / 23][i % 23] = kNoKey;
     __syncthreads();
     const SolView<DT> &S = views[blockIdx.y];
     const int x = static_cast<int>(blockIdx.x) * 8 + (threadIdx.x >> 5);
-    if (x < S.Qp) intra_tw_warp<DT>(S, sp, vmask, x, red);
+    if (x < S.Qp) intra_tw_warp<DT>(S, sp, vmask, x, red[threadIdx.x >> 5]);
     __syncthreads();
-    if (threadIdx.x < 23 && red[threadIdx.x] != kNoKey)
-        atomicMin(reinterpret_cast<unsigned long long *>(keys) + static_cast<size_t>(blockIdx.y) * 23 + threadIdx.x,
-                  red[threadIdx.x]);
+    if (threadIdx.x < 23) {
+        unsigned long long m = red[0][threadIdx.x];
+        for (int w = 1; w < 8; ++w) m = m < red[w][threadIdx.x] ? m : red[w][threadIdx.x];
+        if (m != kNoKey)
+            atomicMin(reinterpret_cast<unsigned long long *>(keys) + static_cast<size_t>(blockIdx.y) * 23 + threadIdx.x, m);
+    }
 }
 
 // ============================================================== intra-route evaluation, CVRP

@@ -35,8 +35,8 @@ struct FastGeom {
     static constexpr int BoxH = U + 4;                          // rows u0-1 .. u0+U+2
     static constexpr int BoxBytes = BoxW * BoxH * 4;
     static constexpr int BoxPad = (BoxBytes + 127) / 128 * 128;
-    static constexpr int RowBytes = U * 96;                     // row records (bulk copy)
-    static constexpr int ColBytes = kFastTV * 96;               // column records (bulk copy)
+    static constexpr int RowBytes = U * 80;                     // row records (bulk copy)
+    static constexpr int ColBytes = kFastTV * 80;               // column records (bulk copy)
     static constexpr int RowTW = TW ? U * 64 : 0;               // time-window parts
     static constexpr int ColTW = TW ? kFastTV * 64 : 0;
     // one pipeline stage = box + row/column records; two stages when a CTA

@@ -636,7 +636,7 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
         s->d_ftiles = static_cast<uint32_t *>(v_ftiles);
         // every record starts poisoned (padding, guards); the scan overwrites route slots
         SlotRec p{};
-        p.c = -1; p.r = -1; p.fL = p.bL1 = p.W = kPoison;
+        p.r = -1; p.fL = p.bL1 = p.W = kPoison;
         for (int k = 0; k < 3; ++k) { p.so[k] = kPoison; p.sA[k] = kPoison; }
         std::vector<SlotRec> init(cap, p);
         if (I->tw) {

@@ -317,6 +317,26 @@ static bool inter_probe_on() {
     return on;
 }
 
+// resident CTAs (whole GPU) of one instantiation with one / two pipeline stages
+template <int U, bool TW, uint32_t MASK, uint32_t MASK2>
+static void fast_capacity(int &res1, int &res2) {
+    static int r1 = 0, r2 = 0;
+    if (!r1) {
+        auto kern = k_inter_fast<U, TW, MASK, MASK2>;
+        using G = FastGeom<U, TW>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::Smem);
+        int dev = 0, sms = 0, b1 = 0, b2 = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, kern, kFastThreads, G::Smem1);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, kern, kFastThreads, G::Smem);
+        r1 = std::max(1, b1) * std::max(1, sms);
+        r2 = std::max(1, b2) * std::max(1, sms);
+    }
+    res1 = r1;
+    res2 = r2;
+}
+
 template <int U, bool TW, uint32_t MASK, uint32_t MASK2>
 static cudaError_t launch_fast_t(const SlotRec *rec, const SlotTW *rectw, const CUtensorMap &map, const uint32_t *tiles,
                                  int t_lo, int t_hi, uint32_t Qc, int32_t cap, uint64_t *keys, int units_max,
@@ -324,18 +344,9 @@ static cudaError_t launch_fast_t(const SlotRec *rec, const SlotTW *rectw, const 
                                  int x_lo, int x_hi) {
     auto kern = k_inter_fast<U, TW, MASK, MASK2>;
     using G = FastGeom<U, TW>;
-    // resident CTAs per SM with one / two pipeline stages (a persistent grid never exceeds them)
-    static int res1 = 0, res2 = 0;
-    if (!res1) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::Smem);
-        int dev = 0, sms = 0, b1 = 0, b2 = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, kern, kFastThreads, G::Smem1);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, kern, kFastThreads, G::Smem);
-        res1 = std::max(1, b1) * std::max(1, sms);
-        res2 = std::max(1, b2) * std::max(1, sms);
-    }
+    // resident CTAs with one / two pipeline stages (a persistent grid never exceeds them)
+    int res1 = 0, res2 = 0;
+    fast_capacity<U, TW, MASK, MASK2>(res1, res2);
     const int groups = MASK2 ? 2 : 1;
     const int tiles_n = t_hi - t_lo;
     const int units = imask ? (x_hi - x_lo + 3) / 4 : 0;
@@ -375,10 +386,12 @@ static cudaError_t launch_fast_u(uint32_t mask, const SlotRec *rec, const SlotTW
     constexpr uint32_t ALL = 0x7FEu, HA = 0x13Eu, HB = 0x6C0u, NS = (1u << 1) | (1u << 2) | (1u << 5);
     static_assert((HA | HB) == ALL && (HA & HB) == 0, "halves");
     if ((mask & ALL) == ALL) {
-        // split in halves only while the whole sweep has at most one tile per CTA of the
-        // unsplit persistent grid (small neighbourhoods: twice the CTAs); above that the
-        // halves would pay the per-tile loads and folds twice
-        if (t_hi - t_lo <= max_grid)
+        // split in halves only while both halves still get one tile per resident CTA
+        // (small neighbourhoods: twice the CTAs); above that the halves would pay the
+        // per-tile loads and folds twice
+        int r1 = 0, r2 = 0;
+        fast_capacity<U, TW, HA, HB>(r1, r2);
+        if (2 * (t_hi - t_lo) <= r1)
             run(std::integral_constant<uint32_t, HA>{}, std::integral_constant<uint32_t, HB>{});
         else
             run(std::integral_constant<uint32_t, ALL>{}, Z{});

@@ -816,7 +816,11 @@ extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
     }
     if (e == cudaSuccess && !fused_intra) {
         // VRPTW intra: warp-parallel scans pay off once routes fill a warp (measured: L ~ 43 vs ~ 10)
-        const bool warp_tw = s->N >= 16 * s->R;
+        // VRPTW intra: the warp-parallel kernel (warp scans of Eq. 4 records) -- measured faster than the
+        // thread-per-(slot, variant) walk for short routes too since its loads are hoisted (cfg3 R1:
+        // 41.8 vs 43.9 us/step; R2: 57.1 vs 92.5).  TGA_WARP_TW=0 selects the walk (A/B override).
+        static const int force_warp = std::getenv("TGA_WARP_TW") ? std::atoi(std::getenv("TGA_WARP_TW")) : 1;
+        const bool warp_tw = force_warp != 0;
         if (I->dtype == TGA_I32)
             e = launch_intra<int32_t>(mask, I->tw, sol_view<int32_t>(s), sp, x_lo, x_hi, s->keys, st,
                                       I->max_c_abs < (1 << 21), warp_tw);
@@ -1458,7 +1462,8 @@ extern "C" int32_t tga_batch_eval(tga_batch *b, uint32_t mask, void *stream) {
     TGA_CUDA(cudaMemsetAsync(b->d_keys, 0xFF, sizeof(uint64_t) * TGA_N_VARIANTS * n, st));
     ScoreParams sp{I->Q, I->opt.score_mode, I->opt.w_load, I->opt.w_tw};
     const int grid = std::max(1, std::min(b->n_work, b->sm_count * 4));
-    const bool warp_tw = b->sols[0]->N >= 16 * b->sols[0]->R;
+    static const int force_warp = std::getenv("TGA_WARP_TW_BATCH") ? std::atoi(std::getenv("TGA_WARP_TW_BATCH")) : -1;
+    const bool warp_tw = force_warp >= 0 ? force_warp != 0 : b->sols[0]->N >= 16 * b->sols[0]->R;
     cudaError_t e = I->dtype == TGA_I32
         ? launch_batch<int32_t>(mask, I->tw, static_cast<const SolView<int32_t> *>(b->d_views), b->d_maps, b->d_work,
                                 b->n_work, n, b->max_qp, sp, b->d_keys, grid, st, warp_tw)

@@ -586,7 +586,7 @@ cudaError_t launch_pick_update(const DevState *states, const void *scans, int n_
     const int smem = multi ? std::max(smem_old, smem_multi) : smem_old;
     const int snap_cap = multi ? 2 * max_cap : 0;
     dim3 g(blocks_per_sol, n_sol);
-    if (smem > 48 * 1024) {
+    if (smem > 40 * 1024) {  // dynamic + static shared memory above the 48 KB default needs the opt-in
         cudaFuncSetAttribute(k_pick_update<int32_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         cudaFuncSetAttribute(k_pick_update<int32_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         cudaFuncSetAttribute(k_pick_update<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

@@ -508,3 +508,36 @@ def test_slack_layouts_lockstep(slack):
             np.testing.assert_array_equal(host.keys(), fresh.keys())
             np.testing.assert_array_equal(dev.keys(), fresh.keys())
     assert dev.routes() == routes
+
+
+@pytest.mark.parametrize("name", ["cvrp3000", "vrptw_r1", "vrptw_r1_penalised"])
+def test_device_step_column_paths_and_short_tw_routes(name):
+    """Device-resident steps where the update copies the changed Dp columns
+    from the refreshed rows behind a grid barrier (Q_p > 2560), and on short
+    VRPTW routes (R1 shape, warp-parallel intra kernel): lockstep with the
+    host-driven step, and keys equal a fresh load of the resulting routes."""
+    _need_gpu()
+    mode = 0
+    if name == "cvrp3000":
+        inst, sol = G.large_cvrp(3, n=3000, mean_len=60)
+        mask = T.OP_ALL
+    else:
+        inst, sol = G.gh_like(4, n=300, kind="R1")
+        mask = T.OP_ALL & ~T.OP_2OPT
+        mode = 1 if name.endswith("penalised") else 0
+    gi = T.Instance.from_gen(inst, score_mode=mode)
+    host = T.Solution(gi, sol)
+    dev = T.Solution(gi, sol)
+    R, N, _, _ = dev.info()
+    if name == "cvrp3000":
+        assert N + 4 * R > 2560
+    for k in range(16):
+        host.step(mask)
+        dev.step_async(mask)
+        if k % 8 == 7:
+            assert dev.routes() == host.routes(), k
+    fresh = T.Solution(gi, dev.routes())
+    for s in (host, dev, fresh):
+        s.eval(mask)
+    np.testing.assert_array_equal(dev.keys(), fresh.keys())
+    np.testing.assert_array_equal(host.keys(), fresh.keys())

@@ -85,15 +85,28 @@ __device__ __forceinline__ void fold(uint64_t &acc, uint32_t b, bool direct, int
 }
 }  // namespace
 
+// one work item of the fused sweep: tile (I, J) of one solution
+struct FastItem {
+    const SlotRec *rec;
+    const SlotTW *rectw;
+    const CUtensorMap *map;
+    uint64_t *keys;
+    uint32_t Qc;
+    int sol, I, J;
+};
+
+// Work items of one launch: w = w0, w0 + stride, ... < w1; item(w) describes it.
+// One solution: the tiles of its plan, strided over the CTAs; a population batch:
+// a contiguous run of (solution, tile) items per CTA, so the running minima are
+// flushed into a solution's keys only when the run moves on to the next solution.
 // stream slots: 0 2opt* | 1,2 reloc1 d/r | 3,4 oropt2 | 5,6 oropt3 | 7 swap11 |
 // 8,9 cross12 | 10,11 cross13 | 12 cross22 | 13,14 cross23 | 15 cross33
-template <int U, bool TW, uint32_t MASK>
-__device__ __forceinline__ void fast_body(const int cta, const int ncta, uint64_t *bar, unsigned long long (*red)[23],
-                                          unsigned char *sm, const SlotRec *__restrict__ rec,
-                                          const SlotTW *__restrict__ rectw, const CUtensorMap &tmap,
-                                          const uint32_t *__restrict__ tiles, int t_lo, int t_hi, uint32_t Qc,
-                                          int32_t cap, uint64_t *__restrict__ keys, const SolView<int32_t> &SV,
-                                          const ScoreParams &sp, uint32_t imask, int x_lo, int x_hi, int flags) {
+template <int U, bool TW, uint32_t MASK, class ItemF>
+__device__ __forceinline__ void fast_body(ItemF item, int w0, int w1, int wstride, uint64_t *bar,
+                                          unsigned long long (*red)[23], unsigned char *sm, int32_t cap,
+                                          const SolView<int32_t> &SV, const ScoreParams &sp, uint32_t imask,
+                                          int x_lo, int x_hi, int icta, int incta, int flags,
+                                          uint64_t *keys0 = nullptr) {
     using G = FastGeom<U, TW>;
     constexpr int BW = G::BoxW;
     constexpr int NV = 11;
@@ -115,40 +128,71 @@ __device__ __forceinline__ void fast_body(const int cta, const int ncta, uint64_
 #pragma unroll
     for (int i = 0; i < NV; ++i) acc[i] = kNoKey;
 
-    auto issue = [&](int t, int b) {
-        const uint32_t ij = tiles[t];
-        const int I = ij >> 16, J = ij & 0xFFFF;
+    auto issue = [&](const FastItem &f, int b) {
         uint64_t *br = b ? &bar[1] : &bar[0];
         f_expect(br, G::BoxBytes + G::RowBytes + G::ColBytes + G::RowTW + G::ColTW);
-        f_tma2d(b ? dp1 : dp0, &tmap, J * kFastTV - 4, I * U - 1, br);
-        f_bulk(b ? rows1 : rows0, rec + I * U, G::RowBytes, br);
-        f_bulk(b ? cols1 : cols0, rec + J * kFastTV, G::ColBytes, br);
+        f_tma2d(b ? dp1 : dp0, f.map, f.J * kFastTV - 4, f.I * U - 1, br);
+        f_bulk(b ? rows1 : rows0, f.rec + f.I * U, G::RowBytes, br);
+        f_bulk(b ? cols1 : cols0, f.rec + f.J * kFastTV, G::ColBytes, br);
         if (TW) {
-            f_bulk(b ? trows1 : trows0, rectw + I * U, G::RowTW, br);
-            f_bulk(b ? tcols1 : tcols0, rectw + J * kFastTV, G::ColTW, br);
+            f_bulk(b ? trows1 : trows0, f.rectw + f.I * U, G::RowTW, br);
+            f_bulk(b ? tcols1 : tcols0, f.rectw + f.J * kFastTV, G::ColTW, br);
         }
     };
+    // ---- fused argmin of the running minima: warp REDUX -> the warp's private shared
+    // row -> one 64-bit atomicMin per variant per CTA into the solution's keys
+    auto flush = [&](uint64_t *keys) {
+#pragma unroll
+        for (int i = 1; i < NV; ++i) {
+            if (!(MASK & (1u << i))) continue;
+            const uint64_t k = warp_min64(acc[i]);
+            if (lane == 0 && k < red[warp][i]) red[warp][i] = k;
+            acc[i] = kNoKey;
+        }
+        __syncthreads();
+        if (tid < 23) {
+            unsigned long long m = red[0][tid];
+#pragma unroll
+            for (int w = 1; w < kFastThreads / 32; ++w) m = m < red[w][tid] ? m : red[w][tid];
+            if (m != kNoKey) atomicMin(reinterpret_cast<unsigned long long *>(keys) + tid, m);
+        }
+        __syncthreads();
+        for (int i = tid; i < (kFastThreads / 32) * 23; i += kFastThreads) red[i / 23][i % 23] = kNoKey;
+    };
 
-    int t = t_lo + cta;
-    if (tid == 0 && t < t_hi) issue(t, 0);
+    int w = w0;
+    FastItem cur{};
+    if (w < w1) cur = item(w);
+    if (tid == 0 && w < w1) issue(cur, 0);
     // intra-route CVRP work of this launch (one u slot per warp) while the first
     // tile's TMA is in flight: the whole neighbourhood is one kernel
     if (imask) {
         const int n_units = (x_hi - x_lo + 3) / 4;
-        for (int j = cta; j < n_units; j += ncta) {
+        for (int j = icta; j < n_units; j += incta) {
             const int x = x_lo + 4 * j + warp;
             if (x < x_hi)
                 intra_cvrp_warp(SV, sp, imask, x, red[warp],
-                                ((flags & 2) && warp == 0 && j == cta && blockIdx.x < 4096) ? g_inter_probe + 8 * blockIdx.x + 4 : nullptr);
+                                ((flags & 2) && warp == 0 && j == icta && blockIdx.x < 4096) ? g_inter_probe + 8 * blockIdx.x + 4 : nullptr);
         }
     }
     if (prb) g_inter_probe[8 * blockIdx.x + 1] = gtime();
+    uint64_t *keys = w < w1 ? cur.keys : keys0;   // keys0: intra-only CTAs of one solution
+    int sol = cur.sol;
     uint32_t ph0 = 0u, ph1 = 0u;
-    for (int it = 0; t < t_hi; t += ncta, ++it) {
+    for (int it = 0; w < w1; w += wstride, ++it) {
         const int b = it & 1;
-        if (tid == 0 && t + static_cast<int>(ncta) < t_hi) issue(t + ncta, b ^ 1);
-        const uint32_t ij = tiles[t];
-        const int u0 = (ij >> 16) * U, v0 = (ij & 0xFFFF) * kFastTV;
+        const FastItem f = cur;
+        if (w + wstride < w1) {
+            cur = item(w + wstride);
+            if (tid == 0) issue(cur, b ^ 1);
+        }
+        if (f.sol != sol) {   // a batch run moved on to the next solution (CTA-uniform)
+            flush(keys);
+            keys = f.keys;
+            sol = f.sol;
+        }
+        const uint32_t Qc = f.Qc;
+        const int u0 = f.I * U, v0 = f.J * kFastTV;
         const int col = warp * 32 + lane;   // column inside the tile
         const int v = v0 + col;
         if (b) { f_wait(&bar[1], ph1); ph1 ^= 1u; } else { f_wait(&bar[0], ph0); ph0 ^= 1u; }
@@ -256,13 +300,7 @@ __device__ __forceinline__ void fast_body(const int cta, const int ncta, uint64_
     }
 
     if (flags & 1) pdl_trigger();
-    // ---- fused argmin: warp shuffle -> shared -> one 64-bit atomicMin per variant per CTA
-#pragma unroll
-    for (int i = 1; i < NV; ++i) {
-        if (!(MASK & (1u << i))) continue;
-        const uint64_t k = warp_min64(acc[i]);
-        if (lane == 0 && k < red[warp][i]) red[warp][i] = k;   // the warp's private row
-    }
+    if (keys) flush(keys);
 }
 
 
@@ -296,18 +334,18 @@ __global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__re
     __syncthreads();
     pdl_wait();                       // Dp / records / keys are written by the stream predecessors
     const int cta = static_cast<int>(blockIdx.x);
-    if (MASK2 == 0 || cta < split)
-        fast_body<U, TW, MASK>(cta, MASK2 ? split : static_cast<int>(gridDim.x), bar, red, sm, rec, rectw, tmap,
-                               tiles, t_lo, t_hi, Qc, cap, keys, SV, sp, MASK2 ? 0u : imask, x_lo, x_hi, flags);
-    else
-        fast_body<U, TW, MASK2>(cta - split, static_cast<int>(gridDim.x) - split, bar, red, sm, rec, rectw, tmap,
-                                tiles, t_lo, t_hi, Qc, cap, keys, SV, sp, imask, x_lo, x_hi, flags);
-    __syncthreads();
-    if (tid < 23) {
-        unsigned long long m = red[0][tid];
-#pragma unroll
-        for (int w = 1; w < kFastThreads / 32; ++w) m = m < red[w][tid] ? m : red[w][tid];
-        if (m != kNoKey) atomicMin(reinterpret_cast<unsigned long long *>(keys) + tid, m);
+    auto item = [&](int t) -> FastItem {
+        const uint32_t ij = tiles[t];
+        return FastItem{rec, rectw, &tmap, keys, Qc, 0, static_cast<int>(ij >> 16), static_cast<int>(ij & 0xFFFF)};
+    };
+    if (MASK2 == 0 || cta < split) {
+        const int n = MASK2 ? split : static_cast<int>(gridDim.x);
+        fast_body<U, TW, MASK>(item, t_lo + cta, t_hi, n, bar, red, sm, cap, SV, sp, MASK2 ? 0u : imask, x_lo, x_hi,
+                               cta, n, flags, keys);
+    } else {
+        const int n = static_cast<int>(gridDim.x) - split;
+        fast_body<U, TW, MASK2>(item, t_lo + cta - split, t_hi, n, bar, red, sm, cap, SV, sp, imask, x_lo, x_hi,
+                                cta - split, n, flags, keys);
     }
     if ((flags & 2) && tid == 0 && blockIdx.x < 4096) g_inter_probe[8 * blockIdx.x + 3] = gtime();
 }
@@ -404,6 +442,89 @@ static cudaError_t launch_fast_u(uint32_t mask, const SlotRec *rec, const SlotTW
     if (mask & (1u << 5)) run(std::integral_constant<uint32_t, (1u << 5)>{}, Z{});
     if (mask & (0x1Fu << 6)) run(std::integral_constant<uint32_t, (0x1Fu << 6)>{}, Z{});
     return err;
+}
+
+// Population batch (BASELINE config 5) on the fast path: a contiguous run of
+// (solution, tile) items per CTA; the running minima are flushed into a
+// solution's keys when the run moves on to the next solution.
+template <int U, bool TW, uint32_t MASK>
+__global__ void __launch_bounds__(kFastThreads) k_inter_fast_batch(const FastSol *__restrict__ sols,
+                                                                   const CUtensorMap *__restrict__ maps,
+                                                                   const uint32_t *__restrict__ work, int n_work,
+                                                                   int32_t cap, ScoreParams sp) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char *sm = smem_raw + ((128u - (s_u32(smem_raw) & 127u)) & 127u);
+    __shared__ uint64_t bar[2];
+    __shared__ unsigned long long red[kFastThreads / 32][23];
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        f_mbar_init(&bar[0]);
+        f_mbar_init(&bar[1]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int i = tid; i < (kFastThreads / 32) * 23; i += kFastThreads) red[i / 23][i % 23] = kNoKey;
+    __syncthreads();
+    const int cta = static_cast<int>(blockIdx.x), G = static_cast<int>(gridDim.x);
+    const int w0 = static_cast<int>(static_cast<long long>(n_work) * cta / G);
+    const int w1 = static_cast<int>(static_cast<long long>(n_work) * (cta + 1) / G);
+    auto item = [&](int w) -> FastItem {
+        const uint32_t c = work[w];
+        const int k = static_cast<int>(c >> 20);
+        const FastSol f = sols[k];
+        return FastItem{f.rec, f.rectw, maps + k, f.keys, f.Qc, k, static_cast<int>((c >> 10) & 0x3FFu),
+                        static_cast<int>(c & 0x3FFu)};
+    };
+    const SolView<int32_t> none{};
+    fast_body<U, TW, MASK>(item, w0, w1, 1, bar, red, sm, cap, none, sp, 0u, 0, 0, 0, 1, 0);
+}
+
+template <int U, bool TW, uint32_t MASK>
+static cudaError_t launch_fast_batch_t(const FastSol *sols, const CUtensorMap *maps, const uint32_t *work, int n_work,
+                                       int32_t cap, const ScoreParams &sp, int max_grid, cudaStream_t st) {
+    auto kern = k_inter_fast_batch<U, TW, MASK>;
+    using G = FastGeom<U, TW>;
+    static int res = 0;
+    if (!res) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::Smem);
+        int dev = 0, sms = 0, b = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, kFastThreads, G::Smem);
+        res = std::max(1, b) * std::max(1, sms);
+    }
+    const int grid = std::max(1, std::min(n_work, std::min(res, max_grid)));
+    kern<<<grid, kFastThreads, G::Smem, st>>>(sols, maps, work, n_work, cap, sp);
+    note_launch();
+    return cudaGetLastError();
+}
+
+template <int U, bool TW>
+static cudaError_t launch_fast_batch_u(uint32_t mask, const FastSol *sols, const CUtensorMap *maps,
+                                       const uint32_t *work, int n_work, int32_t cap, const ScoreParams &sp,
+                                       int max_grid, cudaStream_t st) {
+    if (!(mask & 0x7FEu) || n_work <= 0) return cudaSuccess;
+    cudaError_t err = cudaSuccess;
+    auto run = [&](auto kmask) {
+        if (err == cudaSuccess)
+            err = launch_fast_batch_t<U, TW, decltype(kmask)::value>(sols, maps, work, n_work, cap, sp, max_grid, st);
+    };
+    constexpr uint32_t ALL = 0x7FEu, NS = (1u << 1) | (1u << 2) | (1u << 5);
+    if ((mask & ALL) == ALL) { run(std::integral_constant<uint32_t, ALL>{}); return err; }
+    if ((mask & NS) == NS) { run(std::integral_constant<uint32_t, NS>{}); mask &= ~NS; }
+    if (mask & (1u << 1)) run(std::integral_constant<uint32_t, (1u << 1)>{});
+    if (mask & (1u << 2)) run(std::integral_constant<uint32_t, (1u << 2)>{});
+    if (mask & (3u << 3)) run(std::integral_constant<uint32_t, (3u << 3)>{});
+    if (mask & (1u << 5)) run(std::integral_constant<uint32_t, (1u << 5)>{});
+    if (mask & (0x1Fu << 6)) run(std::integral_constant<uint32_t, (0x1Fu << 6)>{});
+    return err;
+}
+
+cudaError_t launch_inter_fast_batch(int U, bool tw, uint32_t mask, const FastSol *sols, const CUtensorMap *maps,
+                                    const uint32_t *work, int n_work, int32_t cap, const ScoreParams &sp,
+                                    int max_grid, cudaStream_t st) {
+    if (U != 16) return cudaErrorInvalidValue;
+    return tw ? launch_fast_batch_u<16, true>(mask, sols, maps, work, n_work, cap, sp, max_grid, st)
+              : launch_fast_batch_u<16, false>(mask, sols, maps, work, n_work, cap, sp, max_grid, st);
 }
 
 cudaError_t launch_inter_fast(int U, uint32_t mask, const SlotRec *rec, const SlotTW *rectw, const CUtensorMap &map,

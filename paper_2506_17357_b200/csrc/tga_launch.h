@@ -133,6 +133,17 @@ cudaError_t launch_pdl(int which, void (*kern)(KArgs...), dim3 grid, dim3 block,
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
+// population batch on the fast path: per-solution pointers, work = (k << 20 | I << 10 | J)
+struct FastSol {
+    const SlotRec *rec;
+    const SlotTW *rectw;
+    uint64_t *keys;
+    uint32_t Qc;
+    int32_t pad;
+};
+cudaError_t launch_inter_fast_batch(int U, bool tw, uint32_t mask, const FastSol *sols, const CUtensorMap *maps,
+                                    const uint32_t *work, int n_work, int32_t cap, const ScoreParams &sp,
+                                    int max_grid, cudaStream_t st);
 cudaError_t launch_inter_fast(int U, uint32_t mask, const SlotRec *rec, const SlotTW *rectw, const CUtensorMap &map,
                               const uint32_t *tiles, int t_lo, int t_hi, uint32_t Qc, int32_t cap, uint64_t *keys,
                               int max_grid, cudaStream_t st, const SolView<int32_t> &SV, const ScoreParams &sp,

@@ -397,6 +397,16 @@ static int32_t refresh(tga_solution *s, bool full, int ra = -1, int rb = -1) {
     return TGA_OK;
 }
 
+// fast-path plan: fastU x kFastTV tiles (I << 16 | J) of the upper triangle
+static std::vector<uint32_t> fast_plan(const tga_solution *s) {
+    std::vector<uint32_t> f;
+    const int U = s->fastU;
+    for (int I = 0; I < s->pitch / U && I * U < s->Qp; ++I)
+        for (int J = 0; J < s->pitch / kFastTV && J * kFastTV < s->Qp; ++J)
+            if (I * U < J * kFastTV + kFastTV - 1) f.push_back((static_cast<uint32_t>(I) << 16) | J);
+    return f;
+}
+
 static void build_tiles(tga_solution *s) {
     s->d_tiles = s->d_tiles;  // allocated in the arena
     std::vector<uint32_t> t;
@@ -411,11 +421,7 @@ static void build_tiles(tga_solution *s) {
     s->n_tiles = static_cast<int>(t.size());
     cudaMemcpy(s->d_tiles, t.data(), sizeof(uint32_t) * t.size(), cudaMemcpyHostToDevice);
     // fast-path plan: fastU x kFastTV tiles of the upper triangle
-    std::vector<uint32_t> f;
-    const int U = s->fastU;
-    for (int I = 0; I < s->pitch / U && I * U < s->Qp; ++I)
-        for (int J = 0; J < s->pitch / kFastTV && J * kFastTV < s->Qp; ++J)
-            if (I * U < J * kFastTV + kFastTV - 1) f.push_back((static_cast<uint32_t>(I) << 16) | J);
+    const std::vector<uint32_t> f = fast_plan(s);
     s->n_ftiles = static_cast<int>(f.size());
     if (s->d_ftiles) cudaMemcpy(s->d_ftiles, f.data(), sizeof(uint32_t) * f.size(), cudaMemcpyHostToDevice);
 }
@@ -1347,6 +1353,12 @@ struct tga_batch {
     cudaStream_t own_stream = nullptr;
     DevState *d_states = nullptr;   // per solution, keys pointing into d_keys
     void *d_scans = nullptr;        // ScanArgs<DT> per solution
+    // fast path (integer, feasible-only): per-solution records, fast TMA maps, (k, I, J) items
+    bool fast = false;
+    FastSol *d_fsols = nullptr;
+    CUtensorMap *d_fmaps = nullptr;
+    uint32_t *d_fwork = nullptr;
+    int n_fwork = 0;
 };
 
 static void free_batch(tga_batch *b) {
@@ -1354,6 +1366,9 @@ static void free_batch(tga_batch *b) {
     for (auto *s : b->sols) free_solution(s);
     if (b->d_views) cudaFree(b->d_views);
     if (b->d_maps) cudaFree(b->d_maps);
+    if (b->d_fsols) cudaFree(b->d_fsols);
+    if (b->d_fmaps) cudaFree(b->d_fmaps);
+    if (b->d_fwork) cudaFree(b->d_fwork);
     if (b->d_work) cudaFree(b->d_work);
     if (b->d_keys) cudaFree(b->d_keys);
     if (b->h_keys) cudaFreeHost(b->h_keys);
@@ -1429,6 +1444,33 @@ extern "C" int32_t tga_batch_load(tga_instance *I, int32_t n_sol, const int32_t 
         cudaMemcpy(b->d_maps, maps.data(), sizeof(CUtensorMap) * n_sol, cudaMemcpyHostToDevice) != cudaSuccess ||
         cudaMemcpy(b->d_work, work.data(), sizeof(uint32_t) * work.size(), cudaMemcpyHostToDevice) != cudaSuccess)
         return bail(fail(TGA_ERR_CUDA, "batch upload"));
+    {   // fast path: every solution has its records and fast map; items (k << 20 | I << 10 | J)
+        bool ok = true;
+        std::vector<FastSol> fs(n_sol);
+        std::vector<CUtensorMap> fm(n_sol);
+        std::vector<uint32_t> fw;
+        for (int k = 0; k < n_sol && ok; ++k) {
+            tga_solution *s = b->sols[k];
+            ok = s->fast && s->rec && (!I->tw || s->rectw) && s->fastU == 16 && s->pitch / 16 < 1024;
+            if (!ok) break;
+            fs[k] = FastSol{s->rec, s->rectw, b->d_keys + static_cast<size_t>(k) * TGA_N_VARIANTS,
+                            static_cast<uint32_t>(s->pitch), 0};
+            fm[k] = s->fmap;
+            for (uint32_t ij : fast_plan(s))
+                fw.push_back((static_cast<uint32_t>(k) << 20) | ((ij >> 16) << 10) | (ij & 0xFFFFu));
+        }
+        if (ok && !fw.empty()) {
+            if (cudaMalloc(&b->d_fsols, sizeof(FastSol) * n_sol) != cudaSuccess ||
+                cudaMalloc(&b->d_fmaps, sizeof(CUtensorMap) * n_sol) != cudaSuccess ||
+                cudaMalloc(&b->d_fwork, sizeof(uint32_t) * fw.size()) != cudaSuccess ||
+                cudaMemcpy(b->d_fsols, fs.data(), sizeof(FastSol) * n_sol, cudaMemcpyHostToDevice) != cudaSuccess ||
+                cudaMemcpy(b->d_fmaps, fm.data(), sizeof(CUtensorMap) * n_sol, cudaMemcpyHostToDevice) != cudaSuccess ||
+                cudaMemcpy(b->d_fwork, fw.data(), sizeof(uint32_t) * fw.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+                return bail(fail(TGA_ERR_OOM, "batch fast path"));
+            b->n_fwork = static_cast<int>(fw.size());
+            b->fast = true;
+        }
+    }
     *out = b;
     return TGA_OK;
 }
@@ -1464,10 +1506,19 @@ extern "C" int32_t tga_batch_eval(tga_batch *b, uint32_t mask, void *stream) {
     const int grid = std::max(1, std::min(b->n_work, b->sm_count * 4));
     static const int force_warp = std::getenv("TGA_WARP_TW_BATCH") ? std::atoi(std::getenv("TGA_WARP_TW_BATCH")) : -1;
     const bool warp_tw = force_warp >= 0 ? force_warp != 0 : b->sols[0]->N >= 16 * b->sols[0]->R;
+    static const bool no_fast = std::getenv("TGA_BATCH_GENERIC") != nullptr;  // A/B override
+    uint32_t rest = mask;
+    if (b->fast && !no_fast && (mask & TGA_OP_INTER)) {
+        const cudaError_t ef = launch_inter_fast_batch(16, I->tw, mask & TGA_OP_INTER, b->d_fsols,
+                                                       b->d_fmaps, b->d_fwork, b->n_fwork, I->Q, sp,
+                                                       b->sm_count * 4, st);
+        if (ef != cudaSuccess) return fail(TGA_ERR_CUDA, std::string("batch fast eval: ") + cudaGetErrorString(ef));
+        rest &= ~TGA_OP_INTER;
+    }
     cudaError_t e = I->dtype == TGA_I32
-        ? launch_batch<int32_t>(mask, I->tw, static_cast<const SolView<int32_t> *>(b->d_views), b->d_maps, b->d_work,
+        ? launch_batch<int32_t>(rest, I->tw, static_cast<const SolView<int32_t> *>(b->d_views), b->d_maps, b->d_work,
                                 b->n_work, n, b->max_qp, sp, b->d_keys, grid, st, warp_tw)
-        : launch_batch<float>(mask, I->tw, static_cast<const SolView<float> *>(b->d_views), b->d_maps, b->d_work,
+        : launch_batch<float>(rest, I->tw, static_cast<const SolView<float> *>(b->d_views), b->d_maps, b->d_work,
                               b->n_work, n, b->max_qp, sp, b->d_keys, grid, st, warp_tw);
     if (e != cudaSuccess) return fail(TGA_ERR_CUDA, std::string("batch eval: ") + cudaGetErrorString(e));
     if (st != b->stream) TGA_CUDA(order_after(b->stream, st));

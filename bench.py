@@ -134,6 +134,18 @@ def traffic_for(config: str):
     return None
 
 
+def reduce_(t, op):
+    """all_reduce through the process group (CPU staging under gloo)."""
+    import torch.distributed as dist
+    if dist.get_backend() == "gloo":
+        c = t.cpu()
+        dist.all_reduce(c, op=op)
+        t.copy_(c)
+    else:
+        dist.all_reduce(t, op=op)
+    return t
+
+
 def dist_init(args):
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -257,8 +269,8 @@ def run_population(args, ws, rank, local, dev):
         import torch.distributed as dist
         t = torch.tensor([tot_ms, float(cand)], device=dev, dtype=torch.float64)
         tm = t.clone()
-        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        reduce_(tm, dist.ReduceOp.MAX)
+        reduce_(t, dist.ReduceOp.SUM)
         tot_ms, cand = float(tm[0].item()), float(t[1].item())
     if rank != 0:
         return 0
@@ -279,11 +291,20 @@ def run_population(args, ws, rank, local, dev):
 def run_tga(args):
     import torch
     ws, rank, local = dist_init(args)
+    # TGA_BENCH_SHARED_GPU=1: a multi-rank smoke run on a box with fewer GPUs than
+    # ranks (ranks share devices; the process group then uses gloo, since NCCL
+    # refuses two ranks on one GPU).  Never set for a measurement.
+    shared = os.environ.get("TGA_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     if args.config == "cfg5":
         return run_population(args, ws, rank, local, dev)
     import tga_gen as G
@@ -365,11 +386,11 @@ def run_tga(args):
     if ws > 1:
         import torch.distributed as dist
         t = torch.tensor([tot_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        reduce_(t, dist.ReduceOp.MAX)
         tot_ms = float(t.item())
         if not row_shard:   # independent descents: every rank's candidates count
             c = torch.tensor([cand_total], device=dev, dtype=torch.float64)
-            dist.all_reduce(c, op=dist.ReduceOp.SUM)
+            reduce_(c, dist.ReduceOp.SUM)
             cand_total = float(c.item())
         dist.barrier()
     value = cand_total / (tot_ms / 1e3)

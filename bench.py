@@ -179,6 +179,24 @@ def oracle_sweep_rate(inst, routes, budget_s=12.0, rows_frac=None, row_offset=0)
     return tot_c / tot_t, tot_c, tot_t, sweeps
 
 
+def concat_sweep_rate(inst, routes, budget_s=5.0):
+    """The fast CPU evaluator (cpu_baseline/: O(1) concatenation per candidate,
+    the paper's MA-N-style CPU move evaluation), single thread, full
+    sweeps of every variant; returns (moves/s, candidates, seconds, sweeps)."""
+    import cpu_baseline as CB
+    cb = CB.ConcatCPU.from_instance(inst)
+    variants = [v for v in range(23) if not (inst.tw is not None and v == 0)]
+    tot_c, tot_t, sweeps = 0, 0.0, 0
+    while tot_t < budget_s:
+        for v in variants:
+            t0 = time.perf_counter()
+            _, _, _, _, n = cb.best_move(routes, v)
+            tot_t += time.perf_counter() - t0
+            tot_c += n
+        sweeps += 1
+    return tot_c / tot_t, tot_c, tot_t, sweeps
+
+
 # ------------------------------------------------------------------ reference arm
 def run_reference(args):
     ws, rank, _ = dist_init(args)
@@ -514,8 +532,17 @@ def run_tga(args):
         cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
                "sample": f"{sw} full sweep(s) of all variants on state A ({c} candidates, {t:.1f} s), "
                          "single-threaded C oracle that rebuilds every neighbour route"}
+    cpu_fast = None
+    if ws == 1 and not args.no_cpu_baseline:
+        rate, c, t, sw = concat_sweep_rate(inst, sol0.routes, budget_s=5.0)
+        cpu_fast = {"value": rate, "unit": UNIT, "cores": 1, "kind": "concat (O(1) per candidate, MA-N-style)",
+                    "sample": f"{sw} full sweep(s) of all variants on state A ({c} candidates, {t:.1f} s), "
+                              "single-threaded C, prefix/suffix records + Eq. 2-4 concatenation",
+                    "gpu_over_cpu": None}
 
     sweeps_per_s = (K if row_shard else K * ws) / (tot_ms / 1e3)
+    if cpu_fast:
+        cpu_fast["gpu_over_cpu"] = value / cpu_fast["value"]   # cf. the paper's gamma_s, not the target
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K,
         "warmup": max(args.warmup, 3), "ms_per_step": tot_ms / K, "higher_is_better": True,
@@ -539,7 +566,8 @@ def run_tga(args):
         "candidates_per_step": cand_total / K,
         "roofline": primary, "roofline_alt": alt,
         "per_operator_steady_state": per_op,
-        "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
+        "cpu_baseline": cpu, "cpu_baseline_concat": cpu_fast,
+        "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
     }
     print(json.dumps(line, default=float), flush=True)
     if ws > 1:

@@ -85,6 +85,9 @@ def lib():
         _lib.orc_best_move.argtypes = [P(_Inst), C.c_int32, P(C.c_int32), P(C.c_int32),
                                        C.c_int32, C.c_int32, C.c_double, C.c_double,
                                        C.c_int32, C.c_int32, P(_Move)]
+        _lib.orc_best_move_masked.argtypes = [P(_Inst), C.c_int32, P(C.c_int32), P(C.c_int32),
+                                              C.c_int32, C.c_int32, C.c_double, C.c_double,
+                                              C.c_int32, C.c_int32, P(C.c_uint8), P(_Move)]
         _lib.orc_enumerate.argtypes = [P(_Inst), C.c_int32, P(C.c_int32), P(C.c_int32),
                                        C.c_int32, C.c_int32, C.c_double, C.c_double,
                                        P(C.c_double), P(C.c_int32), P(C.c_int32), C.c_int64,
@@ -158,9 +161,20 @@ class Oracle:
                     int(m.n_candidates))
 
     def best_move(self, routes, variant: int, mode: int = 0, wQ: float = 10.0,
-                  wT: float = 10.0, u_lo: int = 0, u_hi: int = -1) -> Move:
+                  wT: float = 10.0, u_lo: int = 0, u_hi: int = -1, mask=None) -> Move:
+        """mask: None (full neighbourhood, NTGA) or the n x n uint8 edge mask M of the
+        edge-based neighbourhood (ETGA), e.g. granular_mask(dist, theta)."""
         ptr, cust = self._csr(routes)
         m = _Move()
+        if mask is not None:
+            mk = np.ascontiguousarray(mask, dtype=np.uint8)
+            assert mk.shape == (self.n, self.n)
+            rc = lib().orc_best_move_masked(C.byref(self._inst), len(ptr) - 1, _ptr(ptr, C.c_int32),
+                                            _ptr(cust, C.c_int32), variant, mode, wQ, wT, u_lo, u_hi,
+                                            _ptr(mk, C.c_uint8), C.byref(m))
+            if rc != 0:
+                raise ValueError(f"orc_best_move_masked failed: {rc}")
+            return self._move(m)
         rc = lib().orc_best_move(C.byref(self._inst), len(ptr) - 1, _ptr(ptr, C.c_int32),
                                  _ptr(cust, C.c_int32), variant, mode, wQ, wT, u_lo, u_hi,
                                  C.byref(m))
@@ -245,6 +259,25 @@ class Oracle:
             if m.found and (best is None or m.score < best.score):
                 best = m
         return best
+
+
+def granular_mask(dist, theta: int) -> np.ndarray:
+    """Edge mask M of the granular neighbourhood (theta = granularity
+    threshold, Table `params` P:528-529; reading 21), written out:
+    NN(i) = the theta customers j != i with the smallest (c_ij, j);
+    M_ij = 1 iff j in NN(i) or i in NN(j); every pair with the depot (node 0) is kept."""
+    dist = np.asarray(dist, dtype=np.float64)
+    n = dist.shape[0]
+    M = np.zeros((n, n), dtype=np.uint8)
+    for i in range(1, n):
+        cand = [(dist[i, j], j) for j in range(1, n) if j != i]
+        cand.sort()
+        for _, j in cand[:theta]:
+            M[i, j] = 1
+            M[j, i] = 1
+    M[0, :] = 1
+    M[:, 0] = 1
+    return M
 
 
 def canonical_q(routes) -> int:

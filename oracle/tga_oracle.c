@@ -300,7 +300,8 @@ static double score_of(const orc_delta *d, int mode, double wQ, double wT)
 static int enumerate(const orc_instance *I, int32_t R, const int32_t *ptr, const int32_t *cust,
                      int32_t var, int32_t mode, double wQ, double wT,
                      int32_t u_lo, int32_t u_hi, orc_move *out,
-                     double *rec_score, int32_t *rec_u, int32_t *rec_v, int64_t rec_cap)
+                     double *rec_score, int32_t *rec_u, int32_t *rec_v, int64_t rec_cap,
+                     const uint8_t *mask)
 {
     orc_sol S;
     memset(out, 0, sizeof(*out));
@@ -329,6 +330,11 @@ static int enumerate(const orc_instance *I, int32_t R, const int32_t *ptr, const
                 int qlo, qhi;
                 v_range(var, S.L[rb], &qlo, &qhi);
                 for (int pb = qlo; pb <= qhi; ++pb) {
+                    /* edge-based neighbourhood (ETGA): inter-route candidates only
+                     * where the mask keeps the node pair at (u, v) (reading 21) */
+                    if (mask && !is_intra(var) &&
+                        !mask[(size_t)S.rt[ra][pa] * (size_t)I->n_nodes + (size_t)S.rt[rb][pb]])
+                        continue;
                     int la, lb;
                     int nr = construct(&S, var, ra, pa, rb, pb, A, &la, B, &lb);
                     if (!nr) continue;
@@ -361,7 +367,15 @@ int orc_best_move(const orc_instance *I, int32_t R, const int32_t *ptr, const in
                   int32_t var, int32_t mode, double wQ, double wT,
                   int32_t u_lo, int32_t u_hi, orc_move *out)
 {
-    return enumerate(I, R, ptr, cust, var, mode, wQ, wT, u_lo, u_hi, out, NULL, NULL, NULL, 0);
+    return enumerate(I, R, ptr, cust, var, mode, wQ, wT, u_lo, u_hi, out, NULL, NULL, NULL, 0, NULL);
+}
+
+/* the same over the edge-based (granular) neighbourhood: mask[n_nodes^2], 1 = pair kept */
+int orc_best_move_masked(const orc_instance *I, int32_t R, const int32_t *ptr, const int32_t *cust,
+                         int32_t var, int32_t mode, double wQ, double wT,
+                         int32_t u_lo, int32_t u_hi, const uint8_t *mask, orc_move *out)
+{
+    return enumerate(I, R, ptr, cust, var, mode, wQ, wT, u_lo, u_hi, out, NULL, NULL, NULL, 0, mask);
 }
 
 /* every candidate's score and (u, v) in canonical order (for pins) */
@@ -369,7 +383,7 @@ int orc_enumerate(const orc_instance *I, int32_t R, const int32_t *ptr, const in
                   int32_t var, int32_t mode, double wQ, double wT,
                   double *scores, int32_t *us, int32_t *vs, int64_t cap, orc_move *out)
 {
-    return enumerate(I, R, ptr, cust, var, mode, wQ, wT, 0, -1, out, scores, us, vs, cap);
+    return enumerate(I, R, ptr, cust, var, mode, wQ, wT, 0, -1, out, scores, us, vs, cap, NULL);
 }
 
 /* Score of one explicitly named candidate (sampled parity at full size). */

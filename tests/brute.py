@@ -43,9 +43,16 @@ def segments(route, n):
     return [(i, route[i:i + n]) for i in range(0, len(route) - n + 1)]
 
 
-def neighbours(routes: List[List[int]], op: str, n1: int = 1, n2: int = 1):
-    """Yield (changed_route_ids, new_routes_for_them) for one operator/variant."""
+def neighbours(routes: List[List[int]], op: str, n1: int = 1, n2: int = 1, keyed: bool = False):
+    """Yield (changed_route_ids, new_routes_for_them) for one operator/variant;
+    keyed=True appends, for inter-route moves, the node pair the move is keyed
+    on (moved segment's first customer / cut node, insertion or cut node of the
+    other route; 0 = the depot) -- the pair an edge mask filters (ETGA)."""
     R = len(routes)
+
+    def out(ids, news, pair=None):
+        return (ids, news, pair) if keyed else (ids, news)
+
     if op == "relocate":
         for a in range(R):
             for i, seg in segments(routes[a], n1):
@@ -54,7 +61,8 @@ def neighbours(routes: List[List[int]], op: str, n1: int = 1, n2: int = 1):
                     if b == a:
                         continue
                     for k in range(len(routes[b]) + 1):
-                        yield (a, b), (rest, routes[b][:k] + seg + routes[b][k:])
+                        after = routes[b][k - 1] if k > 0 else 0
+                        yield out((a, b), (rest, routes[b][:k] + seg + routes[b][k:]), (seg[0], after))
     elif op == "swap":
         for a in range(R):
             for b in range(R):
@@ -62,21 +70,23 @@ def neighbours(routes: List[List[int]], op: str, n1: int = 1, n2: int = 1):
                     continue
                 for i, sa in segments(routes[a], n1):
                     for j, sb in segments(routes[b], n2):
-                        yield (a, b), (routes[a][:i] + sb + routes[a][i + n1:],
-                                       routes[b][:j] + sa + routes[b][j + n2:])
+                        yield out((a, b), (routes[a][:i] + sb + routes[a][i + n1:],
+                                           routes[b][:j] + sa + routes[b][j + n2:]), (sa[0], sb[0]))
     elif op == "2opt*":
         for a in range(R):
             for b in range(a + 1, R):
                 for i in range(len(routes[a]) + 1):
                     for j in range(len(routes[b]) + 1):
-                        yield (a, b), (routes[a][:i] + routes[b][j:],
-                                       routes[b][:j] + routes[a][i:])
+                        ca = routes[a][i - 1] if i > 0 else 0
+                        cb = routes[b][j - 1] if j > 0 else 0
+                        yield out((a, b), (routes[a][:i] + routes[b][j:],
+                                           routes[b][:j] + routes[a][i:]), (ca, cb))
     elif op == "2opt":
         for a in range(R):
             r = routes[a]
             for i in range(len(r)):
                 for j in range(i + 1, len(r)):
-                    yield (a,), (r[:i] + r[i:j + 1][::-1] + r[j + 1:],)
+                    yield out((a,), (r[:i] + r[i:j + 1][::-1] + r[j + 1:],))
     elif op == "intra_relocate":
         for a in range(R):
             r = routes[a]
@@ -85,7 +95,7 @@ def neighbours(routes: List[List[int]], op: str, n1: int = 1, n2: int = 1):
                 for k in range(len(rest) + 1):
                     if k == i:
                         continue  # the identity placement
-                    yield (a,), (rest[:k] + seg + rest[k:],)
+                    yield out((a,), (rest[:k] + seg + rest[k:],))
     elif op == "intra_swap":
         for a in range(R):
             r = routes[a]
@@ -94,18 +104,22 @@ def neighbours(routes: List[List[int]], op: str, n1: int = 1, n2: int = 1):
                     if i + n1 > len(r):
                         continue
                     new = r[:i] + r[j:j + n2] + r[i + n1:j] + r[i:i + n1] + r[j + n2:]
-                    yield (a,), (new,)
+                    yield out((a,), (new,))
     else:
         raise ValueError(op)
 
 
-def scores(dist, demand, tw, capacity, routes, op, n1=1, n2=1, mode=0, wQ=10.0, wT=10.0):
-    """List of scores of every neighbour (feasible-only: inf if infeasible)."""
+def scores(dist, demand, tw, capacity, routes, op, n1=1, n2=1, mode=0, wQ=10.0, wT=10.0, mask=None):
+    """List of scores of every neighbour (feasible-only: inf if infeasible).
+    mask: inter-route neighbours only where mask[pair] is set (edge-based, ETGA)."""
     cur = {}
     for idx, r in enumerate(routes):
         cur[idx] = simulate(dist, demand, tw, r)
     out = []
-    for ids, news in neighbours(routes, op, n1, n2):
+    for item in neighbours(routes, op, n1, n2, keyed=True):
+        ids, news, pair = item
+        if mask is not None and pair is not None and not mask[pair[0]][pair[1]]:
+            continue
         dD = dLV = dTV = 0.0
         feas = True
         for rid, nr in zip(ids, news):

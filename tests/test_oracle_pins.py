@@ -300,3 +300,53 @@ def test_attributes_prefix_suffix():
             assert at["pre_D"][q + p] + (at["suf_D"][q + p]) == D
             assert at["start"][q + p] == st[p]
         q += len(r) + 1
+
+
+# ---------------------------------------------------------------- edge-based (ETGA) neighbourhood
+def _mask_by_definition(dist, theta):
+    """Reading 21 retyped independently of oracle.granular_mask: rank the other
+    customers of i by (distance, id) with numpy's stable lexsort."""
+    n = dist.shape[0]
+    M = np.zeros((n, n), dtype=bool)
+    for i in range(1, n):
+        js = np.array([j for j in range(1, n) if j != i])
+        order = np.lexsort((js, dist[i, js]))
+        for j in js[order[:theta]]:
+            M[i, j] = M[j, i] = True
+    M[0, :] = M[:, 0] = True
+    return M
+
+
+@pytest.mark.parametrize("seed", range(8))
+@pytest.mark.parametrize("tw", [False, True])
+@pytest.mark.parametrize("theta", [1, 2])
+def test_edge_based_neighbourhood_brute_force(seed, tw, theta):
+    """ETGA: the masked oracle's best score and candidate count equal
+    the brute-force neighbours whose key node pair the mask keeps; the mask
+    equals its definition; intra-route variants are unmasked."""
+    dist, demand, twa, cap, sol = _tiny(seed, tw)
+    M = O.granular_mask(dist, theta)
+    np.testing.assert_array_equal(M.astype(bool), _mask_by_definition(dist, theta))
+    orc = O.Oracle(dist, demand, cap, twa)
+    d = dist.tolist()
+    t = None if twa is None else twa.tolist()
+    for op, n1, n2, var in BRUTE_OPS:
+        for mode in (0, 1):
+            bs = brute.scores(d, demand.tolist(), t, cap, sol.routes, op, n1, n2, mode, mask=M)
+            m = orc.best_move(sol, var, mode, mask=M)
+            assert m.n_candidates == len(bs), (op, n1, n2, mode)
+            finite = [x for x in bs if x != float("inf")]
+            assert m.found == bool(finite), (op, n1, n2, mode)
+            if finite:
+                assert m.score == min(finite), (op, n1, n2, mode)
+
+
+def test_edge_based_full_mask_is_the_full_neighbourhood():
+    """theta >= n - 1 keeps every pair: ETGA == NTGA, index included."""
+    inst, sol = G.cvrp_small(2, spare=True)
+    orc = O.Oracle.from_instance(inst)
+    M = O.granular_mask(inst.dist, inst.dist.shape[0])
+    assert M.all() or (M | np.eye(M.shape[0], dtype=np.uint8)).all()
+    for v in range(O.N_VARIANTS):
+        a, b = orc.best_move(sol, v), orc.best_move(sol, v, mask=M)
+        assert (a.found, a.score, a.u, a.v, a.n_candidates) == (b.found, b.score, b.u, b.v, b.n_candidates)

@@ -62,6 +62,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-per-op", action="store_true")
+    ap.add_argument("--granular", type=int, default=0,
+                    help="theta > 0: edge-based neighbourhood (ETGA, P:390-401) with granularity threshold theta")
     ap.add_argument("--shard", choices=["replicas", "rows"], default="replicas",
                     help="N>1: independent descents per GPU (weak scaling, no collective) or one "
                          "solution's candidate rows split over the GPUs (NCCL MIN-allreduce of the keys)")
@@ -330,7 +332,7 @@ def run_tga(args):
 
     inst, sol0 = G.config(args.config, args.seed)
     stream = torch.cuda.Stream(device=dev)
-    gi = T.Instance.from_gen(inst)
+    gi = T.Instance.from_gen(inst, granular_theta=args.granular)
     row_shard = ws > 1 and args.shard == "rows"
     # Cold-cache timing without flush nodes: R replicas of the workload's
     # solution (separate device state each) stepped round-robin, so that
@@ -550,7 +552,8 @@ def run_tga(args):
         "dtype": "int32" if inst.tw is None else "f32 (integer-valued TW-I times; int32 loads)",
         "data": "synthetic",
         "config": {"workload": f"{args.config}: {G.CONFIGS.get(args.config, args.config)}; "
-                               "step = eval all variants + best move + apply",
+                               + (f"edge-based neighbourhood (ETGA) theta={args.granular}; " if args.granular else "")
+                               + "step = eval all variants + best move + apply",
                    "customers": N, "routes": R, "canonical_slots": Qc, "seed": args.seed,
                    "l2": (f"inputs larger than L2: {n_rep} replicas of the solution stepped round-robin "
                           f"({n_rep * ws_bytes / 2**20:.0f} MB of Dp + records vs {l2 / 2**20:.0f} MB L2)"

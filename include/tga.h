@@ -113,7 +113,14 @@ typedef struct {
     int32_t device;      /* CUDA device ordinal; -1 = current device */
     int32_t slack;       /* spare physical slots per route (0 = default 2, -1 = none): a move that
                             keeps both changed routes within their slots refreshes only them */
-    int32_t reserved[11];
+    int32_t granular_theta; /* 0 = full neighbourhood (NTGA).  > 0: edge-based neighbourhood (ETGA,
+                            P:390-401) with granularity threshold theta: inter-route
+                            candidates only where the edge mask keeps the node pair at (u, v) --
+                            v among the theta nearest customers of u or u among those of v, or
+                            either is the depot (reading 21); intra-route candidates stay
+                            full.  Integer feasible-only fast path only (else
+                            TGA_ERR_UNSUPPORTED at tga_eval). */
+    int32_t reserved[10];
 } tga_options;
 
 typedef struct {
@@ -237,8 +244,10 @@ int32_t tga_solution_timings(tga_solution *sol, float *ms, int32_t max_n, int32_
  * ~0 = no valid candidate. */
 int32_t tga_solution_keys(tga_solution *sol, uint64_t *keys);
 
-/* Exact candidate counts per variant for the current solution (closed forms;
- * host only). counts[TGA_N_VARIANTS]. */
+/* Exact candidate counts per variant for the current solution (closed forms of
+ * the full neighbourhood; host only). counts[TGA_N_VARIANTS].  With
+ * granular_theta > 0 the inter-route candidates actually evaluated are counted
+ * on the device instead (tga_solution_device_stats). */
 int32_t tga_solution_counts(const tga_solution *sol, uint64_t *counts);
 
 /* Totals from the device attribute records: distance D(S) (Eq. 1, mu1=0,

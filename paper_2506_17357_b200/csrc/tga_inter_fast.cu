@@ -85,6 +85,73 @@ __device__ __forceinline__ void fold(uint64_t &acc, uint32_t b, bool direct, int
 }
 }  // namespace
 
+// The candidate streams of one (row u, column v) cell with route(u) < route(v)
+// (stream slots above): D(di, dj) = Dp(u + di, v + dj); put(slot, ok, dD)
+// receives every candidate -- feasibility ok (capacity, and time windows in the
+// T_V = 0 form of SlotTW) and the distance delta dD (Eq. 2, 13, 14).
+template <bool TW, uint32_t MASK, class DF, class PF>
+__device__ __forceinline__ void cell_streams(const SlotRec &A, const SlotRec &V, const SlotTW &AT, const SlotTW &VT,
+                                             int32_t cap, DF D, PF put) {
+    // time-window check of  F + seg + B  (Eq. 4 in the T_V = 0 form of SlotTW):
+    // start after ef + t1 <= seg latest start, completion + t2 <= suffix latest start
+    auto tw3 = [&](float ef, int32_t t1, float sTE, float sTL, float sTD, int32_t t2, float lb) -> bool {
+        const float x = ef + static_cast<float>(t1);
+        return (x <= sTL) & (fmaxf(x, sTE) + sTD + static_cast<float>(t2) <= lb);
+    };
+    // ---- 2-opt*: A' = F(u) + B(v+1), B' = F(v) + B(u+1)    (Eq. 14)
+    if (MASK & (1u << 1)) {
+        const int32_t d01 = D(0, 1), d10 = D(1, 0);
+        const int32_t dD = d01 + d10 + A.ne + V.ne;
+        const int32_t la = A.fL + V.bL1, lb = V.fL + A.bL1;
+        bool ok = max(la, lb) <= cap;
+        if (TW) ok = ok & (AT.EF + static_cast<float>(d01) <= VT.LBN[0]) &
+                     (VT.EF + static_cast<float>(d10) <= AT.LBN[0]);
+        put(0, ok, dD);
+    }
+    // ---- relocate / or-opt, both directions                   (Eq. 13)
+#pragma unroll
+    for (int N = 1; N <= 3; ++N) {
+        if (!(MASK & (1u << (1 + N)))) continue;
+        const int32_t d00 = D(0, 0), dN1 = D(N - 1, 1), d1N = D(1, N - 1);
+        const int32_t d1 = A.rem[N - 1] + d00 + dN1 + V.ne;  // seg(u) after v
+        bool ok1 = V.W + A.so[N - 1] <= cap;
+        if (TW) ok1 = ok1 & tw3(VT.EF, d00, AT.sTE[N - 1], AT.sTL[N - 1], AT.sTD[N - 1], dN1, VT.LBN[0]);
+        put(2 * N - 1, ok1, d1);
+        const int32_t d2 = V.rem[N - 1] + d00 + d1N + A.ne;  // seg(v) after u
+        bool ok2 = A.W + V.so[N - 1] <= cap;
+        if (TW) ok2 = ok2 & tw3(AT.EF, d00, VT.sTE[N - 1], VT.sTL[N - 1], VT.sTD[N - 1], d1N, AT.LBN[0]);
+        put(2 * N, ok2, d2);
+    }
+    // ---- swap (1,1) / cross-exchange (N1,N2), N1 <= N2
+#pragma unroll
+    for (int sv = 0; sv < 6; ++sv) {
+        constexpr int n1s[6] = {1, 1, 1, 2, 2, 3}, n2s[6] = {1, 2, 3, 2, 3, 3};
+        constexpr int slot[6] = {7, 8, 10, 12, 13, 15};
+        const int N1 = n1s[sv], N2 = n2s[sv];
+        if (!(MASK & (1u << (5 + sv)))) continue;
+        {   // N1-segment at u, N2-segment at v
+            const int32_t a = D(-1, 0), bq = D(N1, N2 - 1), c = D(0, -1), dq = D(N1 - 1, N2);
+            const int32_t dD = a + bq + c + dq + A.sE[N1 - 1] + V.sE[N2 - 1];
+            const int32_t la = A.sA[N1 - 1] + V.sS[N2 - 1], lb = V.sA[N2 - 1] + A.sS[N1 - 1];
+            bool ok = max(la, lb) <= cap;
+            if (TW)  // A' = F(u-1) + S(v,N2) + B(u+N1),  B' = F(v-1) + S(u,N1) + B(v+N2)
+                ok = ok & tw3(AT.EFm, a, VT.sTE[N2 - 1], VT.sTL[N2 - 1], VT.sTD[N2 - 1], bq, AT.LBN[N1 - 1]) &
+                     tw3(VT.EFm, c, AT.sTE[N1 - 1], AT.sTL[N1 - 1], AT.sTD[N1 - 1], dq, VT.LBN[N2 - 1]);
+            put(slot[sv], ok, dD);
+        }
+        if (N1 != N2) {   // N1-segment at v, N2-segment at u
+            const int32_t c = D(0, -1), bq = D(N2 - 1, N1), a = D(-1, 0), dq = D(N2, N1 - 1);
+            const int32_t dD = c + bq + a + dq + V.sE[N1 - 1] + A.sE[N2 - 1];
+            const int32_t lb = V.sA[N1 - 1] + A.sS[N2 - 1], la = A.sA[N2 - 1] + V.sS[N1 - 1];
+            bool ok = max(la, lb) <= cap;
+            if (TW)  // B' = F(v-1) + S(u,N2) + B(v+N1),  A' = F(u-1) + S(v,N1) + B(u+N2)
+                ok = ok & tw3(VT.EFm, c, AT.sTE[N2 - 1], AT.sTL[N2 - 1], AT.sTD[N2 - 1], bq, VT.LBN[N1 - 1]) &
+                     tw3(AT.EFm, a, VT.sTE[N1 - 1], VT.sTL[N1 - 1], VT.sTD[N1 - 1], dq, AT.LBN[N2 - 1]);
+            put(slot[sv] + 1, ok, dD);
+        }
+    }
+}
+
 // one work item of the fused sweep: tile (I, J) of one solution
 struct FastItem {
     const SlotRec *rec;
@@ -220,64 +287,8 @@ __device__ __forceinline__ void fast_body(ItemF item, int w0, int w1, int wstrid
             if (ru < 0) continue;            // warp-uniform: end depot / spare / padding row
             if (!(ru < V.r)) continue;       // pair must span two routes, route(u) < route(v)
             const SlotTW &AT = TR[TW ? i : 0];
-            // time-window check of  F + seg + B  (Eq. 4 in the T_V = 0 form of SlotTW):
-            // start after ef + t1 <= seg latest start, completion + t2 <= suffix latest start
-            auto tw3 = [&](float ef, int32_t t1, float sTE, float sTL, float sTD, int32_t t2, float lb) -> bool {
-                const float x = ef + static_cast<float>(t1);
-                return (x <= sTL) & (fmaxf(x, sTE) + sTD + static_cast<float>(t2) <= lb);
-            };
-            // ---- 2-opt*: A' = F(u) + B(v+1), B' = F(v) + B(u+1)    (Eq. 14)
-            if (MASK & (1u << 1)) {
-                const int32_t d01 = D(i, 0, 1), d10 = D(i, 1, 0);
-                const int32_t dD = d01 + d10 + A.ne + V.ne;
-                const int32_t la = A.fL + V.bL1, lb = V.fL + A.bL1;
-                bool ok = max(la, lb) <= cap;
-                if (TW) ok = ok & (AT.EF + static_cast<float>(d01) <= VT.LBN[0]) &
-                             (VT.EF + static_cast<float>(d10) <= AT.LBN[0]);
-                keep(run[0], ok, dD, i);
-            }
-            // ---- relocate / or-opt, both directions                   (Eq. 13)
-#pragma unroll
-            for (int N = 1; N <= 3; ++N) {
-                if (!(MASK & (1u << (1 + N)))) continue;
-                const int32_t d00 = D(i, 0, 0), dN1 = D(i, N - 1, 1), d1N = D(i, 1, N - 1);
-                const int32_t d1 = A.rem[N - 1] + d00 + dN1 + V.ne;  // seg(u) after v
-                bool ok1 = V.W + A.so[N - 1] <= cap;
-                if (TW) ok1 = ok1 & tw3(VT.EF, d00, AT.sTE[N - 1], AT.sTL[N - 1], AT.sTD[N - 1], dN1, VT.LBN[0]);
-                keep(run[2 * N - 1], ok1, d1, i);
-                const int32_t d2 = V.rem[N - 1] + d00 + d1N + A.ne;  // seg(v) after u
-                bool ok2 = A.W + V.so[N - 1] <= cap;
-                if (TW) ok2 = ok2 & tw3(AT.EF, d00, VT.sTE[N - 1], VT.sTL[N - 1], VT.sTD[N - 1], d1N, AT.LBN[0]);
-                keep(run[2 * N], ok2, d2, i);
-            }
-            // ---- swap (1,1) / cross-exchange (N1,N2), N1 <= N2
-#pragma unroll
-            for (int sv = 0; sv < 6; ++sv) {
-                constexpr int n1s[6] = {1, 1, 1, 2, 2, 3}, n2s[6] = {1, 2, 3, 2, 3, 3};
-                constexpr int slot[6] = {7, 8, 10, 12, 13, 15};
-                const int N1 = n1s[sv], N2 = n2s[sv];
-                if (!(MASK & (1u << (5 + sv)))) continue;
-                {   // N1-segment at u, N2-segment at v
-                    const int32_t a = D(i, -1, 0), bq = D(i, N1, N2 - 1), c = D(i, 0, -1), dq = D(i, N1 - 1, N2);
-                    const int32_t dD = a + bq + c + dq + A.sE[N1 - 1] + V.sE[N2 - 1];
-                    const int32_t la = A.sA[N1 - 1] + V.sS[N2 - 1], lb = V.sA[N2 - 1] + A.sS[N1 - 1];
-                    bool ok = max(la, lb) <= cap;
-                    if (TW)  // A' = F(u-1) + S(v,N2) + B(u+N1),  B' = F(v-1) + S(u,N1) + B(v+N2)
-                        ok = ok & tw3(AT.EFm, a, VT.sTE[N2 - 1], VT.sTL[N2 - 1], VT.sTD[N2 - 1], bq, AT.LBN[N1 - 1]) &
-                             tw3(VT.EFm, c, AT.sTE[N1 - 1], AT.sTL[N1 - 1], AT.sTD[N1 - 1], dq, VT.LBN[N2 - 1]);
-                    keep(run[slot[sv]], ok, dD, i);
-                }
-                if (N1 != N2) {   // N1-segment at v, N2-segment at u
-                    const int32_t c = D(i, 0, -1), bq = D(i, N2 - 1, N1), a = D(i, -1, 0), dq = D(i, N2, N1 - 1);
-                    const int32_t dD = c + bq + a + dq + V.sE[N1 - 1] + A.sE[N2 - 1];
-                    const int32_t lb = V.sA[N1 - 1] + A.sS[N2 - 1], la = A.sA[N2 - 1] + V.sS[N1 - 1];
-                    bool ok = max(la, lb) <= cap;
-                    if (TW)  // B' = F(v-1) + S(u,N2) + B(v+N1),  A' = F(u-1) + S(v,N1) + B(u+N2)
-                        ok = ok & tw3(VT.EFm, c, AT.sTE[N2 - 1], AT.sTL[N2 - 1], AT.sTD[N2 - 1], bq, VT.LBN[N1 - 1]) &
-                             tw3(AT.EFm, a, VT.sTE[N1 - 1], VT.sTL[N1 - 1], VT.sTD[N1 - 1], dq, AT.LBN[N2 - 1]);
-                    keep(run[slot[sv] + 1], ok, dD, i);
-                }
-            }
+            cell_streams<TW, MASK>(A, V, AT, VT, cap, [&](int di, int dj) { return D(i, di, dj); },
+                                   [&](int k, bool ok, int32_t dD) { keep(run[k], ok, dD, i); });
         }
         // ---- fold this tile's streams into the per-variant 64-bit keys
         if (V.r >= 0) {
@@ -525,6 +536,149 @@ cudaError_t launch_inter_fast_batch(int U, bool tw, uint32_t mask, const FastSol
     if (U != 16) return cudaErrorInvalidValue;
     return tw ? launch_fast_batch_u<16, true>(mask, sols, maps, work, n_work, cap, sp, max_grid, st)
               : launch_fast_batch_u<16, false>(mask, sols, maps, work, n_work, cap, sp, max_grid, st);
+}
+
+// ============================================================== edge-based evaluation (ETGA)
+// Edge-based extraction for inter-route operators: only the cells
+// (u, v) whose node pair the edge mask M keeps are evaluated -- the customer
+// pairs of the granular neighbourhood (host-built, reading 21), every
+// (customer, start depot of another route) cell and every pair of start depots.
+// Each thread evaluates one cell with the same stream formulas as the tile
+// kernel (cell_streams), reading its 5x5 Dp neighbourhood and the two records
+// from L2; slot_of[node] (k_slot_of) maps the static node pairs to the current
+// slots.  Intra-route variants stay full.
+__global__ void __launch_bounds__(256) k_slot_of(const int32_t *__restrict__ node, const int32_t *__restrict__ pos,
+                                                 const int32_t *__restrict__ rlen, int Qp, int32_t *__restrict__ slot_of) {
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < Qp; x += gridDim.x * blockDim.x) {
+        const int p = pos[x];
+        if (p >= 1 && p <= rlen[x]) slot_of[node[x]] = x;
+    }
+}
+
+template <bool TW, uint32_t MASK>
+__global__ void __launch_bounds__(256) k_etga(const SlotRec *__restrict__ rec, const SlotTW *__restrict__ rectw,
+                                              const int32_t *__restrict__ Dp, int pitch, uint32_t Qc,
+                                              const int32_t *__restrict__ slot_of, const int32_t *__restrict__ rbase,
+                                              const int32_t *__restrict__ pos, const int32_t *__restrict__ rlen,
+                                              const int2 *__restrict__ pairs, int n_pairs, int n_cust, int R,
+                                              int32_t cap, uint64_t *__restrict__ keys,
+                                              unsigned long long *__restrict__ counts, int w_lo, int w_hi) {
+    constexpr int NV = 11;
+    __shared__ unsigned long long red[8][23];
+    __shared__ unsigned long long csum[8][NV];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint64_t acc[NV];
+    uint32_t nc[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) { acc[i] = kNoKey; nc[i] = 0u; }
+    const int n_dep = n_cust * R;
+    const int stride = gridDim.x * blockDim.x;
+    for (int w = w_lo + blockIdx.x * blockDim.x + tid; w < w_hi; w += stride) {
+        int u, v;
+        if (w < n_pairs) {
+            const int2 pr = pairs[w];
+            u = slot_of[pr.x];
+            v = slot_of[pr.y];
+        } else if (w < n_pairs + n_dep) {   // (customer j, start depot of route a)
+            const int k = w - n_pairs;
+            u = rbase[k % R];
+            v = slot_of[k / R + 1];
+        } else {                            // (start depot of a, start depot of b), a < b
+            const int k = w - n_pairs - n_dep;
+            const int a = k / R, b = k % R;
+            if (a >= b) continue;
+            u = rbase[a];
+            v = rbase[b];
+        }
+        SlotRec A = rec[u], V = rec[v];
+        if (A.r < 0 || V.r < 0 || A.r == V.r) continue;
+        if (A.r > V.r) {
+            const int t = u; u = v; v = t;
+            const SlotRec T = A; A = V; V = T;
+        }
+        SlotTW AT{}, VT{};
+        if (TW) { AT = rectw[u]; VT = rectw[v]; }
+        const int32_t *base = Dp + static_cast<size_t>(u) * pitch + v;
+        auto D = [&](int di, int dj) -> int32_t { return __ldg(base + di * pitch + dj); };
+        const uint32_t idx_d = static_cast<uint32_t>(u) * Qc + static_cast<uint32_t>(v);
+        const uint32_t idx_r = static_cast<uint32_t>(v) * Qc + static_cast<uint32_t>(u);
+        // slot -> (variant, direction) of the stream layout
+        cell_streams<TW, MASK>(A, V, AT, VT, cap, D, [&](int k, bool ok, int32_t dD) {
+            const int var = k == 0 ? 1 : (k <= 6 ? 1 + (k + 1) / 2 : (k == 7 ? 5 : (k <= 9 ? 6 : (k <= 11 ? 7 : (k == 12 ? 8 : (k <= 14 ? 9 : 10))))));
+            const bool direct = (k == 0 || k == 7 || k == 12 || k == 15) ? true
+                                : (k <= 6 ? (k & 1) == 1 : ((k == 8 || k == 10 || k == 13)));
+            if (ok) acc[var] = umin64(acc[var], pack_key(ord_score(dD), direct ? idx_d : idx_r));
+        });
+        // structurally valid candidates of the cell (the oracle's masked count)
+        const int pu = pos[u], pv = pos[v], Lu = rlen[u], Lv = rlen[v];
+        auto segok = [](int p, int n, int L) -> uint32_t { return (p >= 1 && p + n - 1 <= L) ? 1u : 0u; };
+        if (MASK & (1u << 1)) nc[1] += 1u;
+#pragma unroll
+        for (int N = 1; N <= 3; ++N)
+            if (MASK & (1u << (1 + N))) nc[1 + N] += segok(pu, N, Lu) + segok(pv, N, Lv);
+#pragma unroll
+        for (int sv = 0; sv < 6; ++sv) {
+            constexpr int n1s[6] = {1, 1, 1, 2, 2, 3}, n2s[6] = {1, 2, 3, 2, 3, 3};
+            const int N1 = n1s[sv], N2 = n2s[sv];
+            if (!(MASK & (1u << (5 + sv)))) continue;
+            nc[5 + sv] += segok(pu, N1, Lu) * segok(pv, N2, Lv);
+            if (N1 != N2) nc[5 + sv] += segok(pv, N1, Lv) * segok(pu, N2, Lu);
+        }
+    }
+    // fused argmin + counts: warp -> the warp's shared row -> one atomic per variant per CTA
+#pragma unroll
+    for (int i = 1; i < NV; ++i) {
+        const uint64_t k = warp_min64(acc[i]);
+        const uint32_t c = __reduce_add_sync(0xffffffffu, nc[i]);
+        if (lane == 0) { red[warp][i] = k; csum[warp][i] = c; }
+    }
+    __syncthreads();
+    if (tid >= 1 && tid < NV) {
+        unsigned long long m = kNoKey, c = 0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+            m = m < red[w][tid] ? m : red[w][tid];
+            c += csum[w][tid];
+        }
+        if (m != kNoKey) atomicMin(reinterpret_cast<unsigned long long *>(keys) + tid, m);
+        if (counts && c) atomicAdd(counts + tid, c);
+    }
+}
+
+template <bool TW>
+static cudaError_t launch_etga_t(uint32_t mask, const EtgaArgs &a, cudaStream_t st) {
+    cudaError_t err = cudaSuccess;
+    const int cells = a.w_hi - a.w_lo;
+    if (cells <= 0 || !(mask & 0x7FEu)) return cudaSuccess;
+    const int grid = std::max(1, std::min((cells + 255) / 256, a.sm_count * 8));
+    auto run = [&](auto kmask) {
+        if (err != cudaSuccess) return;
+        k_etga<TW, decltype(kmask)::value><<<grid, 256, 0, st>>>(a.rec, a.rectw, a.Dp, a.pitch, a.Qc, a.slot_of, a.rbase,
+                                                                 a.pos, a.rlen, a.pairs, a.n_pairs, a.n_cust, a.R,
+                                                                 a.cap, a.keys, a.counts, a.w_lo, a.w_hi);
+        note_launch();
+        err = cudaGetLastError();
+    };
+    constexpr uint32_t ALL = 0x7FEu, NS = (1u << 1) | (1u << 2) | (1u << 5);
+    if ((mask & ALL) == ALL) { run(std::integral_constant<uint32_t, ALL>{}); return err; }
+    if ((mask & NS) == NS) { run(std::integral_constant<uint32_t, NS>{}); mask &= ~NS; }
+    if (mask & (1u << 1)) run(std::integral_constant<uint32_t, (1u << 1)>{});
+    if (mask & (1u << 2)) run(std::integral_constant<uint32_t, (1u << 2)>{});
+    if (mask & (3u << 3)) run(std::integral_constant<uint32_t, (3u << 3)>{});
+    if (mask & (1u << 5)) run(std::integral_constant<uint32_t, (1u << 5)>{});
+    if (mask & (0x1Fu << 6)) run(std::integral_constant<uint32_t, (0x1Fu << 6)>{});
+    return err;
+}
+
+cudaError_t launch_etga(uint32_t mask, bool tw, const EtgaArgs &a, cudaStream_t st) {
+    cudaError_t e = cudaSuccess;
+    {
+        const int grid = std::max(1, std::min((a.Qp + 255) / 256, a.sm_count * 4));
+        k_slot_of<<<grid, 256, 0, st>>>(a.node, a.pos, a.rlen, a.Qp, a.slot_of);
+        note_launch();
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return tw ? launch_etga_t<true>(mask, a, st) : launch_etga_t<false>(mask, a, st);
 }
 
 cudaError_t launch_inter_fast(int U, uint32_t mask, const SlotRec *rec, const SlotTW *rectw, const CUtensorMap &map,

@@ -398,8 +398,9 @@ __device__ __forceinline__ void wait_arrivals(int32_t *counter, int v_own, int n
 }
 
 template <class DT, bool TW>
-__device__ __forceinline__ void pick_update_multi(const DevState &S, const ScanArgs<DT> &A, uint32_t mask, int integer,
-                                                  int32_t *smr, int snap_cap, unsigned long long *pr) {
+__device__ __forceinline__ void pick_update_multi(const DevState &S, const ScanArgs<DT> &A, uint32_t mask,
+                                                  uint32_t cmask, int integer, int32_t *smr, int snap_cap,
+                                                  unsigned long long *pr) {
     const int tid = threadIdx.x, R = S.R, G = gridDim.x, b = blockIdx.x;
     int32_t *sb = smr, *sl = smr + (R + 1);
     int32_t *snap = smr + 2 * (R + 1);  // old node ids of the changed ranges
@@ -426,7 +427,7 @@ __device__ __forceinline__ void pick_update_multi(const DevState &S, const ScanA
     __syncthreads();
     if (tid == 0) arrive_v = atomicAdd(S.desc + 9, 1);
     pdl_trigger();  // this block is resident and arrived: a dependent grid cannot starve the wait below
-    if (b == G - 1) neighbourhood_counts(S, mask, sl);  // the evaluated (old) lengths
+    if (b == G - 1) neighbourhood_counts(S, cmask, sl);  // the evaluated (old) lengths
     if (!dm.applied) {
         if (b == 0 && tid == 0) {
             S.desc[0] = 0;
@@ -440,7 +441,7 @@ __device__ __forceinline__ void pick_update_multi(const DevState &S, const ScanA
         if (b == 0) {
             if (tid == 0) wait_arrivals(S.desc + 9, arrive_v, G);
             __syncthreads();
-            pick_apply_body(S, mask, integer, smr, pr, false);  // resets the keys too
+            pick_apply_body(S, mask, cmask, integer, smr, pr, false);  // resets the keys too
         }
         solution_barrier(S.desc + 8, G);
         const volatile int32_t *desc = S.desc;
@@ -544,7 +545,7 @@ __device__ __forceinline__ void pick_update_multi(const DevState &S, const ScanA
 template <class DT, bool TW>
 __global__ void __launch_bounds__(256) k_pick_update(const DevState *__restrict__ states,
                                                      const ScanArgs<DT> *__restrict__ scans, uint32_t mask,
-                                                     int integer, int snap_cap) {
+                                                     uint32_t cmask, int integer, int snap_cap) {
     extern __shared__ int32_t smr[];
     pdl_wait();  // the keys (and, two launches back, the slot arrays) come from stream predecessors
     const DevState &S = states[blockIdx.y];
@@ -552,12 +553,12 @@ __global__ void __launch_bounds__(256) k_pick_update(const DevState *__restrict_
     probe(pr, 0);
     if (gridDim.x == 1) pdl_trigger();
     if (snap_cap > 0 && gridDim.x > 1) {
-        pick_update_multi<DT, TW>(S, scans[blockIdx.y], mask, integer, smr, snap_cap, pr);
+        pick_update_multi<DT, TW>(S, scans[blockIdx.y], mask, cmask, integer, smr, snap_cap, pr);
         return;
     }
     // one block per solution (population batches), or the shared memory cannot
     // hold the snapshot: block 0 picks and splices, grid barrier, update
-    if (blockIdx.x == 0) pick_apply_body(S, mask, integer, smr, pr);
+    if (blockIdx.x == 0) pick_apply_body(S, mask, cmask, integer, smr, pr);
     if (gridDim.x > 1) solution_barrier(S.desc + 8, gridDim.x);
     else __syncthreads();
     if (gridDim.x > 1) pdl_trigger();  // every block of this grid is resident (it passed the barrier)
@@ -577,7 +578,8 @@ __global__ void __launch_bounds__(256) k_pick_update(const DevState *__restrict_
 }
 
 cudaError_t launch_pick_update(const DevState *states, const void *scans, int n_sol, bool tw, bool is_int,
-                               uint32_t mask, int max_routes, int max_cap, int blocks_per_sol, cudaStream_t st) {
+                               uint32_t mask, uint32_t cmask, int max_routes, int max_cap, int blocks_per_sol,
+                               cudaStream_t st) {
     // old path: sb, sl, nb (3 x (R+1) ints) + the shared snapshot of the two changed routes;
     // multi-block path: sb, sl + old and new node ids of the two changed routes
     const int smem_old = 3 * (max_routes + 1) * 4 + 2 * max_cap * 4;
@@ -595,10 +597,10 @@ cudaError_t launch_pick_update(const DevState *states, const void *scans, int n_
     cudaError_t e;
     const auto *si = static_cast<const ScanArgs<int32_t> *>(scans);
     const auto *sf = static_cast<const ScanArgs<float> *>(scans);
-    if (is_int) e = tw ? launch_pdl(2, k_pick_update<int32_t, true>, g, dim3(256), smem, st, states, si, mask, 1, snap_cap)
-                       : launch_pdl(2, k_pick_update<int32_t, false>, g, dim3(256), smem, st, states, si, mask, 1, snap_cap);
-    else e = tw ? launch_pdl(2, k_pick_update<float, true>, g, dim3(256), smem, st, states, sf, mask, 0, snap_cap)
-                : launch_pdl(2, k_pick_update<float, false>, g, dim3(256), smem, st, states, sf, mask, 0, snap_cap);
+    if (is_int) e = tw ? launch_pdl(2, k_pick_update<int32_t, true>, g, dim3(256), smem, st, states, si, mask, cmask, 1, snap_cap)
+                       : launch_pdl(2, k_pick_update<int32_t, false>, g, dim3(256), smem, st, states, si, mask, cmask, 1, snap_cap);
+    else e = tw ? launch_pdl(2, k_pick_update<float, true>, g, dim3(256), smem, st, states, sf, mask, cmask, 0, snap_cap)
+                : launch_pdl(2, k_pick_update<float, false>, g, dim3(256), smem, st, states, sf, mask, cmask, 0, snap_cap);
     note_launch();
     return e != cudaSuccess ? e : cudaGetLastError();
 }

@@ -86,8 +86,10 @@ struct DevState {
     void *Dp;
     int32_t R, Qc, Qp, pitch, slack;
 };
+// mask: the evaluated variants (pick); cmask: the variants whose closed-form counts are added
 cudaError_t launch_pick_update(const DevState *states, const void *scans, int n_sol, bool tw, bool is_int,
-                               uint32_t mask, int max_routes, int max_cap, int blocks_per_sol, cudaStream_t st);
+                               uint32_t mask, uint32_t cmask, int max_routes, int max_cap, int blocks_per_sol,
+                               cudaStream_t st);
 
 template <class DT>
 cudaError_t launch_dp(DT *Dp, int pitch, const int32_t *node, const DT *C, int n, int Qp, int lo, int hi,
@@ -144,6 +146,24 @@ struct FastSol {
 cudaError_t launch_inter_fast_batch(int U, bool tw, uint32_t mask, const FastSol *sols, const CUtensorMap *maps,
                                     const uint32_t *work, int n_work, int32_t cap, const ScoreParams &sp,
                                     int max_grid, cudaStream_t st);
+// edge-based inter-route evaluation (ETGA): cells [w_lo, w_hi) of
+// {customer pairs of the edge mask} + {customer, start depot} + {start depot pairs}
+struct EtgaArgs {
+    const SlotRec *rec;
+    const SlotTW *rectw;
+    const int32_t *Dp;
+    int pitch;
+    uint32_t Qc;
+    const int32_t *node, *pos, *rlen, *rbase;
+    int32_t *slot_of;
+    const int2 *pairs;
+    int n_pairs, n_cust, R, Qp;
+    int32_t cap;
+    uint64_t *keys;
+    unsigned long long *counts;   // per-variant evaluated candidates (may be null)
+    int w_lo, w_hi, sm_count;
+};
+cudaError_t launch_etga(uint32_t mask, bool tw, const EtgaArgs &a, cudaStream_t st);
 cudaError_t launch_inter_fast(int U, uint32_t mask, const SlotRec *rec, const SlotTW *rectw, const CUtensorMap &map,
                               const uint32_t *tiles, int t_lo, int t_hi, uint32_t Qc, int32_t cap, uint64_t *keys,
                               int max_grid, cudaStream_t st, const SolView<int32_t> &SV, const ScoreParams &sp,

@@ -229,8 +229,8 @@ __device__ __forceinline__ void decode_best(const uint64_t *__restrict__ keys, u
 // Route arrays (base, length, canonical base) are staged in shared memory so the
 // serial parts (decode, binary searches over routes) never wait on global loads.
 
-__device__ __forceinline__ void pick_apply_body(const DevState &S, uint32_t mask, int integer, int32_t *smr,
-                                                unsigned long long *pr, bool do_counts = true) {
+__device__ __forceinline__ void pick_apply_body(const DevState &S, uint32_t mask, uint32_t cmask, int integer,
+                                                int32_t *smr, unsigned long long *pr, bool do_counts = true) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int R = S.R;
     int32_t *sb = smr, *sl = smr + (R + 1), *nb = smr + 2 * (R + 1);  // old bases, old lengths, new bases
@@ -240,7 +240,7 @@ __device__ __forceinline__ void pick_apply_body(const DevState &S, uint32_t mask
     }
     __shared__ uint64_t skeys[23];
     if (tid < 23) skeys[tid] = S.keys[tid];
-    if (do_counts) neighbourhood_counts(S, mask, sl);
+    if (do_counts) neighbourhood_counts(S, cmask, sl);
     __syncthreads();
     if (tid < 23) S.keys[tid] = ~0ull;  // consumed (block 0 is the only reader): the next eval needs no memset
     if (tid == 0) probe(pr, 1);

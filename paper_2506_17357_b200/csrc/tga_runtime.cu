@@ -105,7 +105,40 @@ struct tga_instance {
     std::vector<float> hTw;
     int max_c_abs = 0;
     bool fast_ok = false;  // loads small enough for the poisoned-load fast path
+    // edge-based neighbourhood (ETGA): unordered customer pairs of the edge mask
+    int theta = 0;
+    int n_gpairs = 0;
+    int2 *dGpairs = nullptr;
 };
+
+// Edge mask of the granular neighbourhood (reading 21): NN(i) = the
+// theta customers j != i with the smallest (c_ij, j); M_ij = 1 iff j in NN(i) or
+// i in NN(j) (pairs with the depot are always kept and are not listed here).
+// Returns the unordered customer pairs (i < j) with M_ij = 1.
+template <class T>
+static std::vector<int2> granular_pairs(const T *dist, int n, int theta) {
+    std::vector<uint64_t> pk;
+    pk.reserve(static_cast<size_t>(n) * theta);
+    std::vector<std::pair<double, int>> cand;
+    for (int i = 1; i < n; ++i) {
+        cand.clear();
+        for (int j = 1; j < n; ++j)
+            if (j != i) cand.emplace_back(static_cast<double>(dist[static_cast<size_t>(i) * n + j]), j);
+        const int k = std::min<int>(theta, static_cast<int>(cand.size()));
+        std::partial_sort(cand.begin(), cand.begin() + k, cand.end());
+        for (int q = 0; q < k; ++q) {
+            const int j = cand[q].second;
+            const uint32_t a = static_cast<uint32_t>(std::min(i, j)), b = static_cast<uint32_t>(std::max(i, j));
+            pk.push_back((static_cast<uint64_t>(a) << 32) | b);
+        }
+    }
+    std::sort(pk.begin(), pk.end());
+    pk.erase(std::unique(pk.begin(), pk.end()), pk.end());
+    std::vector<int2> out(pk.size());
+    for (size_t q = 0; q < pk.size(); ++q)
+        out[q] = make_int2(static_cast<int>(pk[q] >> 32), static_cast<int>(pk[q] & 0xFFFFFFFFu));
+    return out;
+}
 
 struct tga_solution {
     tga_instance *inst = nullptr;
@@ -127,6 +160,7 @@ struct tga_solution {
     int32_t *d_desc = nullptr, *d_scratch = nullptr;
     unsigned long long *d_acc = nullptr;
     bool host_stale = false;       // host route lists lag behind device-resident steps
+    int32_t *slot_of = nullptr;    // ETGA: node -> physical slot (rebuilt before every edge-based eval)
     bool keys_clean = false;       // keys are all ~0 (a device step consumed them) ...
     unsigned long long clean_cap = 0;  // ... as of capture sequence clean_cap (0 = executed work)
     float *d_rTV = nullptr;
@@ -506,6 +540,7 @@ extern "C" int32_t tga_instance_create(int32_t n, const void *dist, int32_t dtyp
         if (I->dC) cudaFree(I->dC);
         if (I->dDemand) cudaFree(I->dDemand);
         if (I->dNodeTw) cudaFree(I->dNodeTw);
+        if (I->dGpairs) cudaFree(I->dGpairs);
         delete I;
         return code;
     };
@@ -518,6 +553,16 @@ extern "C" int32_t tga_instance_create(int32_t n, const void *dist, int32_t dtyp
     if (e == cudaSuccess) e = cudaMemcpy(I->dC, dist, nn * 4, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(I->dDemand, demand, sizeof(int32_t) * n, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(I->dNodeTw, ntw.data(), sizeof(TwRec) * n, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && I->opt.granular_theta > 0) {
+        I->theta = I->opt.granular_theta;
+        const std::vector<int2> gp = dtype == TGA_I32
+            ? granular_pairs(static_cast<const int32_t *>(dist), n, I->theta)
+            : granular_pairs(static_cast<const float *>(dist), n, I->theta);
+        I->n_gpairs = static_cast<int>(gp.size());
+        e = cudaMalloc(&I->dGpairs, sizeof(int2) * std::max<size_t>(1, gp.size()));
+        if (e == cudaSuccess && !gp.empty())
+            e = cudaMemcpy(I->dGpairs, gp.data(), sizeof(int2) * gp.size(), cudaMemcpyHostToDevice);
+    }
     if (e != cudaSuccess)
         return cleanup(fail(e == cudaErrorMemoryAllocation ? TGA_ERR_OOM : TGA_ERR_CUDA,
                             std::string("instance upload: ") + cudaGetErrorString(e)));
@@ -531,6 +576,7 @@ extern "C" int32_t tga_instance_destroy(tga_instance *I) {
     cudaFree(I->dC);
     cudaFree(I->dDemand);
     cudaFree(I->dNodeTw);
+    if (I->dGpairs) cudaFree(I->dGpairs);
     delete I;
     return TGA_OK;
 }
@@ -589,7 +635,7 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
     void *v_node, *v_route, *v_pos, *v_rlen, *v_canon, *v_fwdL, *v_bwdL, *v_en, *v_fD, *v_bD, *v_b1, *v_b2, *v_b3;
     void *v_fT, *v_bT, *v_s2, *v_s3, *v_rbase, *v_rlenR, *v_cbase, *v_rW, *v_rTV, *v_rD, *v_keys, *v_tiles;
     void *v_ds, *v_sa, *v_desc, *v_scr, *v_acc;
-    void *v_rec = nullptr, *v_ftiles = nullptr, *v_rectw = nullptr;
+    void *v_rec = nullptr, *v_ftiles = nullptr, *v_rectw = nullptr, *v_slot_of = nullptr;
     s->fastU = 16;  // U = 8 measured no better at n = 1000 (more tiles, more per-tile overhead)
     if (const char *ev = std::getenv("TGA_FAST_U")) s->fastU = std::atoi(ev) == 8 ? 8 : 16;  // tuning override
     const size_t ftiles_max = static_cast<size_t>(s->pitch / s->fastU) * (s->pitch / kFastTV) + 1;
@@ -605,7 +651,8 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
         {&v_scr, cap * 4}, {&v_acc, 48 * 8},
         {&v_keys, TGA_N_VARIANTS * 8}, {&v_tiles, tiles_max * 4},
         {&v_rec, want_fast ? cap * sizeof(SlotRec) : 0}, {&v_ftiles, want_fast ? ftiles_max * 4 : 0},
-        {&v_rectw, want_fast && I->tw ? cap * sizeof(SlotTW) : 0}};
+        {&v_rectw, want_fast && I->tw ? cap * sizeof(SlotTW) : 0},
+        {&v_slot_of, I->theta > 0 ? static_cast<size_t>(I->n) * 4 : 0}};
     size_t total = 0;
     for (auto &it : items) total += align_up(it.bytes, 256);
     if (cudaMalloc(&s->arena, total) != cudaSuccess) return bail(fail(TGA_ERR_OOM, "device arena"));
@@ -634,6 +681,7 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
     s->d_ds = static_cast<DevState *>(v_ds); s->d_sa = v_sa;
     s->d_desc = static_cast<int32_t *>(v_desc); s->d_scratch = static_cast<int32_t *>(v_scr);
     s->d_acc = static_cast<unsigned long long *>(v_acc);
+    s->slot_of = static_cast<int32_t *>(v_slot_of);
     s->keys = static_cast<uint64_t *>(v_keys);
     s->d_tiles = static_cast<uint32_t *>(v_tiles);
     if (want_fast) {
@@ -799,7 +847,21 @@ extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
     if (timed) TGA_CUDA(cudaStreamIsCapturing(st, &cst));
     const unsigned rec_flags = cst == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
     if (timed) TGA_CUDA(cudaEventRecordWithFlags(s->tev[s->tev_n], st, rec_flags));
-    if (I->dtype == TGA_I32 && s->fast) {
+    const bool etga = I->theta > 0;
+    if (etga && !(I->dtype == TGA_I32 && s->fast))
+        return fail(TGA_ERR_UNSUPPORTED, "edge-based neighbourhood: integer feasible-only fast path only");
+    if (etga) {
+        // ETGA: node -> slot map, then the cells the edge mask keeps; the
+        // evaluated inter-route candidates are counted exactly on the device
+        const int n_cust = I->n - 1;
+        const int64_t cells = static_cast<int64_t>(I->n_gpairs) + static_cast<int64_t>(n_cust) * s->R +
+                              static_cast<int64_t>(s->R) * s->R;
+        tga_shard_range(cells, s->shard, s->n_shards, &a, &b);
+        EtgaArgs ea{s->rec, s->rectw, static_cast<const int32_t *>(s->Dp), s->pitch, static_cast<uint32_t>(s->pitch),
+                    s->node, s->pos, s->rlen, s->d_rbase, s->slot_of, I->dGpairs, I->n_gpairs, n_cust, s->R, s->Qp,
+                    I->Q, s->keys, s->d_acc, static_cast<int>(a), static_cast<int>(b), s->sm_count};
+        e = launch_etga(mask, I->tw, ea, st);
+    } else if (I->dtype == TGA_I32 && s->fast) {
         tga_shard_range(s->n_ftiles, s->shard, s->n_shards, &a, &b);
         const int f_lo = static_cast<int>(a), f_hi = static_cast<int>(b);
         // fused: inter tiles + the intra-route CVRP work in one launch (when there is inter work)
@@ -821,7 +883,6 @@ extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
         s->tev_n += 2;
     }
     if (e == cudaSuccess && !fused_intra) {
-        // VRPTW intra: warp-parallel scans pay off once routes fill a warp (measured: L ~ 43 vs ~ 10)
         // VRPTW intra: the warp-parallel kernel (warp scans of Eq. 4 records) -- measured faster than the
         // thread-per-(slot, variant) walk for short routes too since its loads are hoisted (cfg3 R1:
         // 41.8 vs 43.9 us/step; R2: 57.1 vs 92.5).  TGA_WARP_TW=0 selects the walk (A/B override).
@@ -1249,7 +1310,9 @@ extern "C" int32_t tga_step_async(tga_solution *s, uint32_t mask) {
     if (rc != TGA_OK) return rc;
     const tga_instance *I = s->inst;
     // pick + splice + update in one launch: one block per SM at most (grid barrier)
-    cudaError_t e = launch_pick_update(s->d_ds, s->d_sa, 1, I->tw, I->dtype == TGA_I32, s->eval_mask, s->R,
+    // ETGA counts its (masked) inter-route candidates in the eval kernel; the closed forms cover the rest
+    const uint32_t cmask = I->theta > 0 ? (s->eval_mask & TGA_OP_INTRA) : s->eval_mask;
+    cudaError_t e = launch_pick_update(s->d_ds, s->d_sa, 1, I->tw, I->dtype == TGA_I32, s->eval_mask, cmask, s->R,
                                        s->N + 2 + s->slack,  // upper bound of any route's slot capacity
                                        s->sm_count, s->stream);
     if (e != cudaSuccess) return fail(TGA_ERR_CUDA, std::string("device step: ") + cudaGetErrorString(e));
@@ -1589,7 +1652,8 @@ extern "C" int32_t tga_batch_step_async(tga_batch *b, uint32_t mask) {
     int max_r = 0;
     for (auto *s : b->sols) max_r = std::max(max_r, s->R);
     // blocks per solution so that the whole grid is co-resident (grid barrier)
-    cudaError_t e = launch_pick_update(b->d_states, b->d_scans, n, I->tw, I->dtype == TGA_I32, b->eval_mask, max_r,
+    cudaError_t e = launch_pick_update(b->d_states, b->d_scans, n, I->tw, I->dtype == TGA_I32, b->eval_mask,
+                                       b->eval_mask, max_r,
                                        b->sols[0]->N + 2 + b->sols[0]->slack,
                                        std::max(1, b->sm_count * 2 / n), b->stream);
     if (e != cudaSuccess) return fail(TGA_ERR_CUDA, std::string("batch device step: ") + cudaGetErrorString(e));

@@ -58,7 +58,8 @@ class TgaError(RuntimeError):
 
 class _Options(C.Structure):
     _fields_ = [("score_mode", C.c_int32), ("w_load", C.c_int32), ("w_tw", C.c_int32),
-                ("device", C.c_int32), ("slack", C.c_int32), ("reserved", C.c_int32 * 11)]
+                ("device", C.c_int32), ("slack", C.c_int32), ("granular_theta", C.c_int32),
+                ("reserved", C.c_int32 * 10)]
 
 
 class Move(C.Structure):
@@ -180,7 +181,8 @@ class Instance:
     """tga_instance_create(dist, demand, tw, capacity) (P:49-51)."""
 
     def __init__(self, dist, demand, capacity: int, tw=None, score_mode: int = SCORE_FEASIBLE,
-                 w_load: int = 10, w_tw: int = 10, device: int = -1, slack: int = 0):
+                 w_load: int = 10, w_tw: int = 10, device: int = -1, slack: int = 0,
+                 granular_theta: int = 0):
         dist = np.asarray(dist)
         if np.issubdtype(dist.dtype, np.integer):
             self.dist = np.ascontiguousarray(dist, dtype=np.int32)
@@ -195,7 +197,9 @@ class Instance:
         opt = _Options()
         opt.score_mode, opt.w_load, opt.w_tw, opt.device = score_mode, w_load, w_tw, device
         opt.slack = slack
+        opt.granular_theta = granular_theta   # > 0: edge-based neighbourhood (ETGA)
         self.score_mode = score_mode
+        self.granular_theta = granular_theta
         h = C.c_void_p()
         _check(lib().tga_instance_create(self.n, _p(self.dist), self.dtype, None, _p(self.demand),
                                          _p(self.tw), self.capacity, C.byref(opt), C.byref(h)))

@@ -541,3 +541,89 @@ def test_device_step_column_paths_and_short_tw_routes(name):
         s.eval(mask)
     np.testing.assert_array_equal(dev.keys(), fresh.keys())
     np.testing.assert_array_equal(host.keys(), fresh.keys())
+
+
+# ---------------------------------------------------------------- edge-based neighbourhood (ETGA, NEXT #3)
+def _etga_check(inst, routes, theta, variants, label):
+    """keys of every variant == the masked oracle; the device's evaluated
+    inter-route candidate counts == the masked oracle's counts."""
+    orc = O.Oracle.from_instance(inst)
+    M = O.granular_mask(inst.dist, theta)
+    gi = T.Instance.from_gen(inst, granular_theta=theta)
+    gs = T.Solution(gi, routes)
+    gs.device_stats()
+    gs.eval(sum(1 << v for v in variants))
+    got = gpu_keys(gs, integer=True)
+    counts, _ = gs.device_stats()
+    Q = O.canonical_q(routes)
+    for v in variants:
+        m = orc.best_move(routes, v, mask=M)
+        assert got[v] == oracle_key(m, Q), (label, theta, v, got[v], oracle_key(m, Q))
+        if v in INTER:
+            assert int(counts[v]) == m.n_candidates, (label, theta, v, int(counts[v]), m.n_candidates)
+
+
+@pytest.mark.parametrize("theta", [1, 3, 8])
+@pytest.mark.parametrize("seed", range(3))
+def test_etga_small_exact(theta, seed):
+    _need_gpu()
+    inst, sol = G.cvrp_small(seed, spare=True)
+    _etga_check(inst, sol.routes, theta, ALLV, f"cfg1-{seed}")
+    inst, sol = G.gh_like(seed, n=60, kind="R1")
+    _etga_check(inst, sol.routes, theta, INTER + INTRA_TW, f"vrptw-{seed}")
+    for k in range(3):
+        part = G.random_partition(20, 3 + k, 900 + 10 * seed + k)
+        inst, _ = G.cvrp_small(seed, spare=False)
+        _etga_check(inst, part.routes, theta, ALLV, f"partition-{k}")
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3"])
+def test_etga_full_size_exact(name):
+    """Full-size configs at the paper's granularity thresholds (X: 20, GH: 100; Table params)."""
+    _need_gpu()
+    inst, sol = G.config(name)
+    theta = 20 if name == "cfg2" else 100
+    _etga_check(inst, sol.routes, theta, INTER, name)
+
+
+def test_etga_theta_all_is_full_neighbourhood():
+    _need_gpu()
+    inst, sol = G.x_like(3, n=150, target_routes=7)
+    full = T.Solution(T.Instance.from_gen(inst), sol)
+    edge = T.Solution(T.Instance.from_gen(inst, granular_theta=inst.dist.shape[0]), sol)
+    for s in (full, edge):
+        s.eval(T.OP_ALL)
+    np.testing.assert_array_equal(full.keys(), edge.keys())
+
+
+@pytest.mark.parametrize("name", ["cvrp", "vrptw"])
+def test_etga_device_step_lockstep(name):
+    """Device-resident ETGA steps follow the host-driven ETGA trajectory and the
+    masked oracle's best move at every step."""
+    _need_gpu()
+    if name == "cvrp":
+        inst, sol = G.x_like(6, n=200, target_routes=9)
+        mask, theta = T.OP_ALL, 10
+    else:
+        inst, sol = G.gh_like(6, n=200, kind="R2")
+        mask, theta = T.OP_ALL & ~T.OP_2OPT, 20
+    orc = O.Oracle.from_instance(inst)
+    M = O.granular_mask(inst.dist, theta)
+    gi = T.Instance.from_gen(inst, granular_theta=theta)
+    host = T.Solution(gi, sol)
+    dev = T.Solution(gi, sol)
+    routes = [list(r) for r in sol.routes]
+    variants = [v for v in ALLV if (mask >> v) & 1]
+    for step in range(15):
+        best = None
+        for v in variants:
+            m = orc.best_move(routes, v, mask=M)
+            if m.found and (best is None or m.score < best.score):
+                best = m
+        if best is None or not best.score < 0:
+            break
+        ok, mv = host.step(mask)
+        assert ok and (mv.variant, mv.u, mv.v, mv.delta_i) == (best.variant, best.u, best.v, best.score), step
+        dev.step_async(mask)
+        routes = orc.apply(routes, best.variant, best.route_a, best.pos_a, best.route_b, best.pos_b)
+    assert host.routes() == routes and dev.routes() == routes

@@ -443,6 +443,13 @@ def run_tga(args):
     shard_div = ws if row_shard else 1   # a launch evaluates 1/N of the rows when row-sharded
     inter_cands = float(sum(int(dev_counts[v]) for v in inter_sel)) / K / shard_div
     alg_bytes = (Qp * Qp / 2.0) * 4.0 / shard_div       # Dp upper triangle, int32
+    if args.granular:
+        # ETGA: per evaluated cell its 5x5 Dp neighbourhood and the two slot records
+        # (+ the two time-window records) are gathered -- cells = customer pairs of the
+        # edge mask + (customer, start depot) + (start depot, start depot) pairs
+        _, _, n_pairs = gi.info()
+        cells = n_pairs + (N - 0) * R + R * (R - 1) / 2.0
+        alg_bytes = cells * (25 * 4 + 2 * 80 + (2 * 64 if inst.tw is not None else 0)) / shard_div
     ops_tab = ALG_OPS if inst.tw is None else ALG_OPS_TW
     alg_ops = float(sum(int(dev_counts[v]) * ops_tab[v] for v in inter_sel)) / K / shard_div
     sm_mhz_peak = float(pk.get("sm_max_mhz", 1965.0))
@@ -467,7 +474,7 @@ def run_tga(args):
 
     # ---------------- steady state per operator: CUDA-graph replay of back-to-back sweeps
     per_op = {}
-    if not args.no_per_op:
+    if not args.no_per_op and not args.granular:   # per-op counts are full-neighbourhood closed forms
         cnt_now = gs.counts().astype(np.int64)
         groups = dict(T.OPERATORS)
         groups["fused 2-opt*+relocate+swap"] = T.OP_FUSED_NS

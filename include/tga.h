@@ -154,6 +154,9 @@ int32_t tga_instance_create(int32_t n_nodes, const void *dist, int32_t dist_dtyp
                             const void *time, const int32_t *demand, const float *tw,
                             int32_t capacity, const tga_options *opt, tga_instance **out);
 int32_t tga_instance_destroy(tga_instance *inst);
+/* n_nodes, granular_theta and the number of unordered customer pairs the edge
+ * mask keeps (0 without a granular neighbourhood).  Any pointer may be NULL. */
+int32_t tga_instance_info(const tga_instance *inst, int32_t *n_nodes, int32_t *theta, int64_t *n_edge_pairs);
 
 /* ------------------------------------------------------------ solution
  * tga_solution_load: "a solution tensor T_s is first initialized on the GPU

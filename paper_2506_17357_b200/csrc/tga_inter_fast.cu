@@ -598,8 +598,12 @@ __global__ void __launch_bounds__(256) k_etga(const SlotRec *__restrict__ rec, c
         }
         SlotTW AT{}, VT{};
         if (TW) { AT = rectw[u]; VT = rectw[v]; }
-        const int32_t *base = Dp + static_cast<size_t>(u) * pitch + v;
-        auto D = [&](int di, int dj) -> int32_t { return __ldg(base + di * pitch + dj); };
+        // rows / columns clamped into the matrix: u - 1 of the first start depot (slot 0)
+        // or u + 3 past the last slot only feed candidates that are invalid anyway
+        auto D = [&](int di, int dj) -> int32_t {
+            const int r = min(max(u + di, 0), pitch - 1), c = min(max(v + dj, 0), pitch - 1);
+            return __ldg(Dp + static_cast<size_t>(r) * pitch + c);
+        };
         const uint32_t idx_d = static_cast<uint32_t>(u) * Qc + static_cast<uint32_t>(v);
         const uint32_t idx_r = static_cast<uint32_t>(v) * Qc + static_cast<uint32_t>(u);
         // slot -> (variant, direction) of the stream layout

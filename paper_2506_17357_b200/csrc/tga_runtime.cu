@@ -570,6 +570,14 @@ extern "C" int32_t tga_instance_create(int32_t n, const void *dist, int32_t dtyp
     return TGA_OK;
 }
 
+extern "C" int32_t tga_instance_info(const tga_instance *I, int32_t *n_nodes, int32_t *theta, int64_t *n_pairs) {
+    if (!I) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL instance");
+    if (n_nodes) *n_nodes = I->n;
+    if (theta) *theta = I->theta;
+    if (n_pairs) *n_pairs = I->n_gpairs;
+    return TGA_OK;
+}
+
 extern "C" int32_t tga_instance_destroy(tga_instance *I) {
     if (!I) return TGA_OK;
     cudaSetDevice(I->device);

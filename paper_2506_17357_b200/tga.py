@@ -110,6 +110,7 @@ _SYMBOLS = {
     "tga_batch_apply_moves": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "tga_step_async": (C.c_int32, [C.c_void_p, C.c_uint32]),
     "tga_solution_device_stats": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "tga_instance_info": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "tga_solution_debug_probe": (C.c_int32, [C.c_void_p, C.c_int32, C.c_void_p]),
     "tga_descent": (C.c_int32, [C.c_void_p, C.c_uint32, C.c_int32, C.c_void_p, C.c_uint64, C.c_void_p]),
     "tga_batch_step_async": (C.c_int32, [C.c_void_p, C.c_uint32]),
@@ -208,6 +209,12 @@ class Instance:
     @classmethod
     def from_gen(cls, inst, **kw):
         return cls(inst.dist, inst.demand, inst.capacity, inst.tw, **kw)
+
+    def info(self):
+        """(n_nodes, granular theta, unordered customer pairs kept by the edge mask)."""
+        n, th, p = C.c_int32(), C.c_int32(), C.c_int64()
+        _check(lib().tga_instance_info(self._h, C.byref(n), C.byref(th), C.byref(p)))
+        return n.value, th.value, p.value
 
     @property
     def handle(self):

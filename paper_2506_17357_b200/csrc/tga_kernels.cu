@@ -471,38 +471,59 @@ __device__ __forceinline__ void pick_update_multi(const DevState &S, const ScanA
     const DT *__restrict__ C = A.C;
     const int n = A.n_nodes, pitch = S.pitch, Qp = S.Qp;
     DT *__restrict__ Dp = static_cast<DT *>(S.Dp);
-    // ---- 4a. re-scan of the changed routes: warp 0 of blocks 1 and 2 (the longest chains first)
+    // ---- 4. the update work.  Direct columns (small Qp): every block does ONE kind of unit,
+    // so its chain is two rounds of loads: the re-scans on the last blocks, the changed Dp
+    // rows on the first ones, the columns of every other row on the blocks between.
+    // Symmetric columns (large Qp): rows and re-scans on every block, then a barrier.
+    const bool direct = Qp <= kDirectColsQp;
+    const int nrows = n1 + n2;
+    const bool split_roles = direct && G >= nrows + dm.nrt + 2;
+    const int scan0 = split_roles ? G - dm.nrt : 1;                  // first scanning block
+    const int row_blocks = split_roles ? nrows : G, col0 = split_roles ? nrows : 0;
+    const int col_blocks = split_roles ? G - dm.nrt - nrows : G;
+    // 4a. re-scan of the changed routes (warp 0 of one block each; the longest chains)
     for (int q = 0; q < dm.nrt; ++q) {
-        if (b == (1 + q) % G && tid < 32) {
+        if (b == (scan0 + q) % G && tid < 32) {
             const int r = dm.nr[q].r, base = dm.lo[q], off = q ? n1 : 0;
             scan_route_g<DT, TW>(A, r, tid, base, dm.nr[q].L, dm.hi[q] - base,
                                  [&](int x) { return nn[off + x - base]; }, [&](int x) { return x; });
         }
     }
-    // ---- 4b. Dp rows of the changed slots: Dp[a][c] = c(new node(a), node(c)), c < pitch
-    for (int j = b; j < n1 + n2; j += G) {
-        const int a = j < n1 ? lo0 + j : lo1 + (j - n1);
-        const DT *crow = C + static_cast<size_t>(nn[j]) * n;
-        DT *drow = Dp + static_cast<size_t>(a) * pitch;
-        for (int c = 4 * tid; c < pitch; c += 4 * blockDim.x) {
-            int4 nd = *reinterpret_cast<const int4 *>(S.node + c);
-            int t;
-            if ((t = in_chg(c)) >= 0) nd.x = nn[t];
-            if ((t = in_chg(c + 1)) >= 0) nd.y = nn[t];
-            if ((t = in_chg(c + 2)) >= 0) nd.z = nn[t];
-            if ((t = in_chg(c + 3)) >= 0) nd.w = nn[t];
-            *reinterpret_cast<int4 *>(drow + c) = make_int4(bits(__ldg(crow + nd.x)), bits(__ldg(crow + nd.y)),
-                                                           bits(__ldg(crow + nd.z)), bits(__ldg(crow + nd.w)));
+    // 4b. Dp rows of the changed slots: Dp[a][c] = c(new node(a), node(c)), c < pitch
+    if (b < row_blocks) {
+        for (int j = b; j < nrows; j += row_blocks) {
+            const int a = j < n1 ? lo0 + j : lo1 + (j - n1);
+            const DT *crow = C + static_cast<size_t>(nn[j]) * n;
+            DT *drow = Dp + static_cast<size_t>(a) * pitch;
+            for (int c = 4 * tid; c < pitch; c += 4 * blockDim.x) {
+                int4 nd = *reinterpret_cast<const int4 *>(S.node + c);
+                int t;
+                if ((t = in_chg(c)) >= 0) nd.x = nn[t];
+                if ((t = in_chg(c + 1)) >= 0) nd.y = nn[t];
+                if ((t = in_chg(c + 2)) >= 0) nd.z = nn[t];
+                if ((t = in_chg(c + 3)) >= 0) nd.w = nn[t];
+                *reinterpret_cast<int4 *>(drow + c) = make_int4(bits(__ldg(crow + nd.x)), bits(__ldg(crow + nd.y)),
+                                                               bits(__ldg(crow + nd.z)), bits(__ldg(crow + nd.w)));
+            }
         }
     }
-    // ---- 4c. columns of the changed slots in every other row
-    if (Qp <= kDirectColsQp) {
+    // 4c. columns of the changed slots in every other row (a warp per row; the row's
+    // node ids of both of a warp's rows are loaded before any gather)
+    if (direct && b >= col0 && b < col0 + col_blocks) {
         const int warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
-        for (int a = b * nw + warp; a < Qp; a += G * nw) {
-            if (in_chg(a) >= 0) continue;  // a changed row: written whole above
-            const DT *crow = C + static_cast<size_t>(S.node[a]) * n;
-            DT *drow = Dp + static_cast<size_t>(a) * pitch;
-            for (int j = lane; j < n1 + n2; j += 32) drow[j < n1 ? lo0 + j : lo1 + (j - n1)] = __ldg(crow + nn[j]);
+        const int stride = col_blocks * nw;
+        for (int a0 = (b - col0) * nw + warp; a0 < Qp; a0 += 2 * stride) {
+            const int a1 = a0 + stride;
+            const int32_t na0 = S.node[a0], na1 = a1 < Qp ? S.node[a1] : 0;
+            const bool w0 = in_chg(a0) < 0, w1 = a1 < Qp && in_chg(a1) < 0;  // changed rows: written whole above
+            const DT *c0 = C + static_cast<size_t>(na0) * n, *c1 = C + static_cast<size_t>(na1) * n;
+            DT *d0 = Dp + static_cast<size_t>(a0) * pitch, *d1 = Dp + static_cast<size_t>(a1) * pitch;
+            for (int j = lane; j < nrows; j += 32) {
+                const int c = j < n1 ? lo0 + j : lo1 + (j - n1);
+                const DT v0 = w0 ? __ldg(c0 + nn[j]) : DT(0), v1 = w1 ? __ldg(c1 + nn[j]) : DT(0);
+                if (w0) d0[c] = v0;
+                if (w1) d1[c] = v1;
+            }
         }
     }
     if (tid == 0) probe(pr, 5);
@@ -531,7 +552,7 @@ __device__ __forceinline__ void pick_update_multi(const DevState &S, const ScanA
             atomicAdd(S.acc + 23, 1ull);
         }
     }
-    if (Qp > kDirectColsQp) {
+    if (!direct) {
         solution_barrier(S.desc + 8, G);  // every changed row is written before the columns copy it
         if (tid == 0) probe(pr, 6);
         const UpdateSpec u{lo0, lo0 + n1, dm.nrt == 2 ? lo1 : 0, dm.nrt == 2 ? lo1 + n2 : 0, dm.nr[0].r,

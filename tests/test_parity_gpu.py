@@ -627,3 +627,36 @@ def test_etga_device_step_lockstep(name):
         dev.step_async(mask)
         routes = orc.apply(routes, best.variant, best.route_a, best.pos_a, best.route_b, best.pos_b)
     assert host.routes() == routes and dev.routes() == routes
+
+
+# ---------------------------------------------------------------- degenerate shapes
+def _degenerate_cases():
+    """(name, instance, routes): one customer; all customers in one route among
+    empty routes; routes of exactly 1, 2, 3 customers (the or-opt / cross
+    segment-length boundaries); an overloaded route (feasible-only: nothing
+    improving out of it unless it becomes feasible)."""
+    base, _ = G.cvrp_small(11, n=12, n_routes=3)
+    yield "one-customer", G.Instance("one", base.mode, base.coords[:2], base.dist[:2, :2].copy(),
+                                     base.demand[:2].copy(), base.capacity), [[1], []]
+    yield "single-route+empties", base, [list(range(1, 13)), [], [], []]
+    yield "lengths-1-2-3", base, [[1], [2, 3], [4, 5, 6], [7, 8, 9, 10, 11, 12], []]
+    tight = G.Instance("tight", base.mode, base.coords, base.dist, base.demand, int(base.demand.max()) * 3)
+    yield "overloaded", tight, [list(range(1, 9)), [9], [10, 11], [12], []]
+    tw_inst, tw_sol = G.gh_like(12, n=12, kind="R1")
+    yield "tw-lengths", tw_inst, [[1], [2, 3], [4, 5, 6], [7, 8, 9, 10, 11, 12], []]
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_degenerate_shapes_exact(mode):
+    """Every variant's key == the oracle on degenerate solutions, and one device
+    step from each agrees with the host step."""
+    _need_gpu()
+    for name, inst, routes in _degenerate_cases():
+        variants = ALLV if inst.tw is None else INTER + INTRA_TW
+        check_exact(inst, routes, variants, mode, name)
+        gi = T.Instance.from_gen(inst, score_mode=mode)
+        host, dev = T.Solution(gi, routes), T.Solution(gi, routes)
+        m = sum(1 << v for v in variants)
+        host.step(m)
+        dev.step_async(m)
+        assert dev.routes() == host.routes(), name

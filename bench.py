@@ -120,6 +120,11 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ helpers
+def load_for(fn, seconds):
+    """Run fn repeatedly for about `seconds` (keeps the GPU loaded while clocks are sampled)."""
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < seconds:
+        fn()
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -268,7 +273,12 @@ def run_population(args, ws, rank, local, dev):
         import torch.distributed as dist
         dist.barrier()
     torch.cuda.synchronize(dev)
+    # clock samples under load (see run_tga): batch evals of a copy of the population
+    lb = T.Batch(gi, mine)
+    lb.set_stream(stream)
     sampler.start()
+    load_for(lambda: (lb.eval(mask), torch.cuda.synchronize(dev)), 0.4)
+    b.device_stats()
     launches0 = T.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     applied = 0
@@ -284,7 +294,9 @@ def run_population(args, ws, rank, local, dev):
     launches = T.launch_count() - launches0
     dc, applied = b.device_stats()
     cand = int(dc.sum())
+    load_for(lambda: (lb.eval(mask), torch.cuda.synchronize(dev)), 0.4)
     clocks = sampler.stop()
+    del lb
     if ws > 1:
         import torch.distributed as dist
         t = torch.tensor([tot_ms, float(cand)], device=dev, dtype=torch.float64)
@@ -292,6 +304,48 @@ def run_population(args, ws, rank, local, dev):
         reduce_(tm, dist.ReduceOp.MAX)
         reduce_(t, dist.ReduceOp.SUM)
         tot_ms, cand = float(tm[0].item()), float(t[1].item())
+    # ---- roofline of the batch inter-route kernel: CUDA events around K batch evals of
+    # the inter variants alone (each = a 184 B/solution key memset + k_inter_fast_batch)
+    inter_mask = mask & T.OP_INTER
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(5)]
+    b.eval(inter_mask)
+    with torch.cuda.stream(stream):
+        for a_, z_ in evs:
+            a_.record(stream)
+            b.eval(inter_mask)
+            z_.record(stream)
+    torch.cuda.synchronize(dev)
+    kern_ms = statistics.mean(a_.elapsed_time(z_) for a_, z_ in evs)
+    cnt_all = np.zeros(T.N_VARIANTS, dtype=np.float64)   # closed-form counts, every variant
+    for k in range(len(mine)):
+        cnt_all += b.solution(k).counts().astype(np.float64)
+    ops = float(sum(cnt_all[v] * ALG_OPS_TW[v] for v in range(1, 11)))
+    pk, pk_src = peaks()
+    alu_peak = 148 * 128 * float(pk.get("sm_max_mhz", 1965.0)) * 1e6
+    roof = {"bound": "alu", "achieved": ops / (kern_ms / 1e3) / 1e12, "peak": alu_peak / 1e12, "unit": "Tops/s",
+            "frac": ops / (kern_ms / 1e3) / alu_peak, "traffic": None,
+            "peak_source": f"148 SM x 128 lanes x {float(pk.get('sm_max_mhz', 1965.0)):.0f} MHz ({pk_src} sm_max_mhz)",
+            "kernel": "k_inter_fast_batch<16, TW, all-inter> (+ key memset), CUDA events around each batch eval",
+            "kernel_ms": kern_ms, "candidates_per_launch": float(cnt_all[1:11].sum()), "alg_ops_per_launch": ops}
+    # ---- e2e through the C ABI with host buffers: every step reloads every solution of
+    # the population from host CSR arrays, evaluates the batch and reads the best moves back
+    e2e_steps = 3
+    host = [s_.flat() for s_ in mine]
+    t0 = time.perf_counter()
+    e2e_c = 0
+    for _ in range(e2e_steps):
+        for k, (ptr_, cust_) in enumerate(host):
+            b.solution(k).reload((ptr_, cust_))
+        b.eval(mask)
+        b.best_moves(mask)
+        e2e_c += int(sum(int(x) for v, x in enumerate(cnt_all) if (mask >> v) & 1))
+    torch.cuda.synchronize(dev)
+    e2e_s = time.perf_counter() - t0
+    h2d = sum(4 * (len(p_) + len(c_)) for p_, c_ in host)
+    e2e = {"value": e2e_c / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+           "d2h_bytes_per_step": int(len(mine) * T.N_VARIANTS * 8),
+           "step": "per-solution tga_solution_reload from host CSR + tga_batch_eval + tga_batch_best_moves; "
+                   "host wall clock"}
     if rank != 0:
         return 0
     line = {"metric": METRIC, "value": cand / (tot_ms / 1e3), "unit": UNIT, "n_gpus": ws, "steps": K,
@@ -302,8 +356,8 @@ def run_population(args, ws, rank, local, dev):
                                    "step = batch eval of 22 variants + best moves + apply",
                        "solutions": len(sols), "parallelism": f"population split x{ws}"},
             "applied_moves": applied, "gpu_launches": int(launches), "clocks": clocks,
-            "roofline": None, "cpu_baseline": None,
-            "e2e": None}
+            "roofline": roof, "cpu_baseline": None,
+            "e2e": e2e}
     print(json.dumps(line, default=float), flush=True)
     return 0
 
@@ -359,11 +413,12 @@ def run_tga(args):
     K = args.steps
     W = max(args.warmup, 3)
 
-    def capture_steps():
+    def capture_steps(sols=None):
+        sols = sols or reps
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=stream):
             for k in range(K):
-                reps[k % n_rep].step_async(mask_all)   # eval -> on-device pick/splice -> update
+                sols[k % len(sols)].step_async(mask_all)   # eval -> on-device pick/splice -> update
         return g
 
     def replay(g, timed=False):
@@ -384,24 +439,39 @@ def run_tga(args):
     g_val = capture_steps()
     launches = T.launch_count() - launches0      # kernels in the K captured steps
     replay(g_val)
+    # clock-sampling load: the same steps on separate copies (the timed replicas' state
+    # and keys stay untouched)
+    load_reps = [T.Solution(gi, sol0) for _ in range(min(n_rep, 4))]
+    for r in load_reps:
+        r.set_stream(stream)
+        r.step_async(mask_all)
+    g_load = capture_steps(load_reps)
+    replay(g_load)
 
     # ---------------- timed region: the K steps, one graph launch between two events
     for r in reps:
         r.device_stats()   # clear the on-device counters of the warm-up
     sampler = ClockSampler(local)
+    # nvidia-smi samples every 100 ms but K steps take ~1 ms: the same graph is replayed
+    # for ~0.4 s before and after the timed replay so the clock samples see the load
+    sampler.start()
+    load_for(lambda: replay(g_load), 0.4)
+    for r in reps:
+        r.device_stats()   # count only the timed replay's steps
     if ws > 1:
         import torch.distributed as dist
         dist.barrier()
     torch.cuda.synchronize(dev)
-    sampler.start()
     tot_ms = replay(g_val, timed=True)
-    clocks = sampler.stop()
     dev_counts = np.zeros(T.N_VARIANTS, dtype=np.uint64)
     applied = 0
     for r in reps:
         c, a_ = r.device_stats()   # exact candidate counts of the K evaluated neighbourhoods
         dev_counts += c
         applied += a_
+    load_for(lambda: replay(g_load), 0.4)
+    clocks = sampler.stop()
+    del g_load, load_reps
     cand_total = float(dev_counts.sum())
     if ws > 1:
         import torch.distributed as dist

@@ -517,9 +517,12 @@ def run_tga(args):
         # ETGA: per evaluated cell its 5x5 Dp neighbourhood and the two slot records
         # (+ the two time-window records) are gathered -- cells = customer pairs of the
         # edge mask + (customer, start depot) + (start depot, start depot) pairs
+        # bytes GATHERED per cell (served by L2 or HBM): customer-pair cells read the ~20
+        # distinct Dp values of all streams, cells with a start depot the 6 of 2-opt* and
+        # relocate, both the two slot records (+ two time-window records)
         _, _, n_pairs = gi.info()
-        cells = n_pairs + (N - 0) * R + R * (R - 1) / 2.0
-        alg_bytes = cells * (25 * 4 + 2 * 80 + (2 * 64 if inst.tw is not None else 0)) / shard_div
+        recs = 2 * 80 + (2 * 64 if inst.tw is not None else 0)
+        alg_bytes = (n_pairs * (20 * 4 + recs) + (N * R + R * (R - 1) / 2.0) * (6 * 4 + recs)) / shard_div
     ops_tab = ALG_OPS if inst.tw is None else ALG_OPS_TW
     alg_ops = float(sum(int(dev_counts[v]) * ops_tab[v] for v in inter_sel)) / K / shard_div
     sm_mhz_peak = float(pk.get("sm_max_mhz", 1965.0))

@@ -573,25 +573,11 @@ __global__ void __launch_bounds__(256) k_etga(const SlotRec *__restrict__ rec, c
     for (int i = 0; i < NV; ++i) { acc[i] = kNoKey; nc[i] = 0u; }
     const int n_dep = n_cust * R;
     const int stride = gridDim.x * blockDim.x;
-    for (int w = w_lo + blockIdx.x * blockDim.x + tid; w < w_hi; w += stride) {
-        int u, v;
-        if (w < n_pairs) {
-            const int2 pr = pairs[w];
-            u = slot_of[pr.x];
-            v = slot_of[pr.y];
-        } else if (w < n_pairs + n_dep) {   // (customer j, start depot of route a)
-            const int k = w - n_pairs;
-            u = rbase[k % R];
-            v = slot_of[k / R + 1];
-        } else {                            // (start depot of a, start depot of b), a < b
-            const int k = w - n_pairs - n_dep;
-            const int a = k / R, b = k % R;
-            if (a >= b) continue;
-            u = rbase[a];
-            v = rbase[b];
-        }
+    // one cell (u, v) evaluated with the streams of mask CM
+    auto eval_cell = [&](auto kmask, int u, int v) {
+        constexpr uint32_t CM = decltype(kmask)::value;
         SlotRec A = rec[u], V = rec[v];
-        if (A.r < 0 || V.r < 0 || A.r == V.r) continue;
+        if (A.r < 0 || V.r < 0 || A.r == V.r) return;
         if (A.r > V.r) {
             const int t = u; u = v; v = t;
             const SlotRec T = A; A = V; V = T;
@@ -607,7 +593,7 @@ __global__ void __launch_bounds__(256) k_etga(const SlotRec *__restrict__ rec, c
         const uint32_t idx_d = static_cast<uint32_t>(u) * Qc + static_cast<uint32_t>(v);
         const uint32_t idx_r = static_cast<uint32_t>(v) * Qc + static_cast<uint32_t>(u);
         // slot -> (variant, direction) of the stream layout
-        cell_streams<TW, MASK>(A, V, AT, VT, cap, D, [&](int k, bool ok, int32_t dD) {
+        cell_streams<TW, CM>(A, V, AT, VT, cap, D, [&](int k, bool ok, int32_t dD) {
             const int var = k == 0 ? 1 : (k <= 6 ? 1 + (k + 1) / 2 : (k == 7 ? 5 : (k <= 9 ? 6 : (k <= 11 ? 7 : (k == 12 ? 8 : (k <= 14 ? 9 : 10))))));
             const bool direct = (k == 0 || k == 7 || k == 12 || k == 15) ? true
                                 : (k <= 6 ? (k & 1) == 1 : ((k == 8 || k == 10 || k == 13)));
@@ -616,17 +602,33 @@ __global__ void __launch_bounds__(256) k_etga(const SlotRec *__restrict__ rec, c
         // structurally valid candidates of the cell (the oracle's masked count)
         const int pu = pos[u], pv = pos[v], Lu = rlen[u], Lv = rlen[v];
         auto segok = [](int p, int n, int L) -> uint32_t { return (p >= 1 && p + n - 1 <= L) ? 1u : 0u; };
-        if (MASK & (1u << 1)) nc[1] += 1u;
-#pragma unroll
+        if (CM & (1u << 1)) nc[1] += 1u;
+    #pragma unroll
         for (int N = 1; N <= 3; ++N)
-            if (MASK & (1u << (1 + N))) nc[1 + N] += segok(pu, N, Lu) + segok(pv, N, Lv);
-#pragma unroll
+            if (CM & (1u << (1 + N))) nc[1 + N] += segok(pu, N, Lu) + segok(pv, N, Lv);
+    #pragma unroll
         for (int sv = 0; sv < 6; ++sv) {
             constexpr int n1s[6] = {1, 1, 1, 2, 2, 3}, n2s[6] = {1, 2, 3, 2, 3, 3};
             const int N1 = n1s[sv], N2 = n2s[sv];
-            if (!(MASK & (1u << (5 + sv)))) continue;
+            if (!(CM & (1u << (5 + sv)))) continue;
             nc[5 + sv] += segok(pu, N1, Lu) * segok(pv, N2, Lv);
             if (N1 != N2) nc[5 + sv] += segok(pv, N1, Lv) * segok(pu, N2, Lu);
+        }
+    };
+    // cells with a start depot only have 2-opt* and relocate candidates (a segment never
+    // starts at a depot): their swap / cross streams are not evaluated
+    constexpr uint32_t DEPOT_MASK = MASK & 0x1Eu;
+    for (int w = w_lo + blockIdx.x * blockDim.x + tid; w < w_hi; w += stride) {
+        if (w < n_pairs) {
+            const int2 pr = pairs[w];
+            eval_cell(std::integral_constant<uint32_t, MASK>{}, slot_of[pr.x], slot_of[pr.y]);
+        } else if (w < n_pairs + n_dep) {   // (customer j, start depot of route a)
+            const int k = w - n_pairs;
+            eval_cell(std::integral_constant<uint32_t, DEPOT_MASK>{}, rbase[k % R], slot_of[k / R + 1]);
+        } else {                            // (start depot of a, start depot of b), a < b
+            const int k = w - n_pairs - n_dep;
+            const int a = k / R, b = k % R;
+            if (a < b) eval_cell(std::integral_constant<uint32_t, DEPOT_MASK>{}, rbase[a], rbase[b]);
         }
     }
     // fused argmin + counts: warp -> the warp's shared row -> one atomic per variant per CTA

@@ -210,6 +210,10 @@ int32_t tga_step(tga_solution *sol, uint32_t op_mask, tga_move *out);
  * in the slot arrays, then the update kernel (bounds read on the device).
  * Enqueue-only; steps can be issued back to back (or captured in a CUDA
  * graph).  Host-side queries resynchronise the host route lists lazily.
+ * A CUDA graph captured from these calls records decisions taken from the
+ * solution's state at capture time (no key reset after a step, no rebuild of the
+ * ETGA node -> slot map): replay it only while nothing but replays of that
+ * graph modifies the solution.
  * The step consumes the keys (resets them to ~0 on the device), so the next
  * tga_eval enqueues no reset of its own; tga_solution_keys after a step
  * returns ~0 for every variant until the next tga_eval.

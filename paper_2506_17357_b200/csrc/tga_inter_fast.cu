@@ -675,9 +675,9 @@ static cudaError_t launch_etga_t(uint32_t mask, const EtgaArgs &a, cudaStream_t 
     return err;
 }
 
-cudaError_t launch_etga(uint32_t mask, bool tw, const EtgaArgs &a, cudaStream_t st) {
+cudaError_t launch_etga(uint32_t mask, bool tw, const EtgaArgs &a, cudaStream_t st, bool build_slot_of) {
     cudaError_t e = cudaSuccess;
-    {
+    if (build_slot_of) {   // device steps keep the map current; host layout uploads invalidate it
         const int grid = std::max(1, std::min((a.Qp + 255) / 256, a.sm_count * 4));
         k_slot_of<<<grid, 256, 0, st>>>(a.node, a.pos, a.rlen, a.Qp, a.slot_of);
         note_launch();

@@ -537,6 +537,7 @@ __device__ __forceinline__ void pick_update_multi(const DevState &S, const ScanA
             const int p = j - (q ? n1 : 0), L = dm.nr[q].L, r = dm.nr[q].r;
             const bool live = p <= L + 1;
             S.node[x] = nn[j];
+            if (S.slot_of && p >= 1 && p <= L) S.slot_of[nn[j]] = x;
             S.route[x] = live ? r : -1;
             S.pos[x] = live ? p : 0;
             S.rlen[x] = live ? L : -1;

@@ -83,6 +83,7 @@ struct DevState {
     uint64_t *keys;                              // 23 packed keys of the last evaluation (reset to ~0 once consumed)
     int32_t *desc;                               // [0] applied, [1..7] UpdateSpec, [8] grid-barrier counter
     unsigned long long *acc;                     // [23] candidate counts + [23] applied moves
+    int32_t *slot_of;                            // ETGA node -> slot map kept current by the step (or null)
     void *Dp;
     int32_t R, Qc, Qp, pitch, slack;
 };
@@ -163,7 +164,7 @@ struct EtgaArgs {
     unsigned long long *counts;   // per-variant evaluated candidates (may be null)
     int w_lo, w_hi, sm_count;
 };
-cudaError_t launch_etga(uint32_t mask, bool tw, const EtgaArgs &a, cudaStream_t st);
+cudaError_t launch_etga(uint32_t mask, bool tw, const EtgaArgs &a, cudaStream_t st, bool build_slot_of);
 cudaError_t launch_inter_fast(int U, uint32_t mask, const SlotRec *rec, const SlotTW *rectw, const CUtensorMap &map,
                               const uint32_t *tiles, int t_lo, int t_hi, uint32_t Qc, int32_t cap, uint64_t *keys,
                               int max_grid, cudaStream_t st, const SolView<int32_t> &SV, const ScoreParams &sp,

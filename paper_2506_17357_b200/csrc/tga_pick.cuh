@@ -371,6 +371,7 @@ __device__ __forceinline__ void pick_apply_body(const DevState &S, uint32_t mask
         (void)span_lo;
         if (p <= L + 1) {
             S.node[x] = (p >= 1 && p <= L) ? old_node(old_slot(r, p)) : 0;
+            if (S.slot_of && p >= 1 && p <= L) S.slot_of[S.node[x]] = x;
             S.route[x] = r;
             S.pos[x] = p;
             S.rlen[x] = L;

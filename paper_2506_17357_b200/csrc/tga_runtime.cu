@@ -160,7 +160,8 @@ struct tga_solution {
     int32_t *d_desc = nullptr, *d_scratch = nullptr;
     unsigned long long *d_acc = nullptr;
     bool host_stale = false;       // host route lists lag behind device-resident steps
-    int32_t *slot_of = nullptr;    // ETGA: node -> physical slot (rebuilt before every edge-based eval)
+    int32_t *slot_of = nullptr;    // ETGA: node -> physical slot
+    bool slot_of_fresh = false;    // ... current (device steps keep it so; host layout uploads do not)
     bool keys_clean = false;       // keys are all ~0 (a device step consumed them) ...
     unsigned long long clean_cap = 0;  // ... as of capture sequence clean_cap (0 = executed work)
     float *d_rTV = nullptr;
@@ -285,6 +286,7 @@ static void stage_route_arrays(tga_solution *s) {
 //   routes = {ra, rb} (rb may be -1) : just those routes' slot ranges
 //   full                            : every slot
 static int32_t upload_layout(tga_solution *s, bool full, int ra = -1, int rb = -1) {
+    s->slot_of_fresh = false;  // the ETGA node -> slot map is rebuilt before the next edge-based eval
     if (full) {
         int off = 0;
         for (int r = 0; r < s->R; ++r) { stage_route(s, r, off); off += s->rcap[r]; }
@@ -373,6 +375,7 @@ static DevState make_devstate(const tga_solution *s, uint64_t *keys) {
     d.node = s->node; d.route = s->route; d.pos = s->pos; d.rlen = s->rlen; d.canon = s->canon;
     d.rbase = s->d_rbase; d.rlenR = s->d_rlenR; d.cbase = s->d_cbase;
     d.scratch = s->d_scratch; d.keys = keys; d.desc = s->d_desc; d.acc = s->d_acc; d.Dp = s->Dp;
+    d.slot_of = s->slot_of;
     d.R = s->R; d.Qc = s->pitch; d.Qp = s->Qp; d.pitch = s->pitch; d.slack = s->slack;
     return d;
 }
@@ -703,7 +706,7 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
     s->d_ds = static_cast<DevState *>(v_ds); s->d_sa = v_sa;
     s->d_desc = static_cast<int32_t *>(v_desc); s->d_scratch = static_cast<int32_t *>(v_scr);
     s->d_acc = static_cast<unsigned long long *>(v_acc);
-    s->slot_of = static_cast<int32_t *>(v_slot_of);
+    s->slot_of = I->theta > 0 ? static_cast<int32_t *>(v_slot_of) : nullptr;  // zero-size items point past the arena
     s->keys = static_cast<uint64_t *>(v_keys);
     s->d_tiles = static_cast<uint32_t *>(v_tiles);
     if (want_fast) {
@@ -882,7 +885,8 @@ extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
         EtgaArgs ea{s->rec, s->rectw, static_cast<const int32_t *>(s->Dp), s->pitch, static_cast<uint32_t>(s->pitch),
                     s->node, s->pos, s->rlen, s->d_rbase, s->slot_of, I->dGpairs, I->n_gpairs, n_cust, s->R, s->Qp,
                     I->Q, s->keys, s->d_acc, static_cast<int>(a), static_cast<int>(b), s->sm_count};
-        e = launch_etga(mask, I->tw, ea, st);
+        e = launch_etga(mask, I->tw, ea, st, !s->slot_of_fresh);
+        s->slot_of_fresh = true;
     } else if (I->dtype == TGA_I32 && s->fast) {
         tga_shard_range(s->n_ftiles, s->shard, s->n_shards, &a, &b);
         const int f_lo = static_cast<int>(a), f_hi = static_cast<int>(b);

@@ -409,7 +409,7 @@ static cudaError_t launch_fast_t(const SlotRec *rec, const SlotTW *rectw, const 
     }
     const int split = MASK2 ? grid / 2 : grid;
     const int flags = (pdl_enabled(4) ? 1 : 0) | (inter_probe_on() ? 2 : 0);
-    const cudaError_t e = launch_pdl(1, kern, dim3(grid), dim3(kFastThreads), smem, st, rec, rectw, map, tiles, t_lo,
+    const cudaError_t e = launch_pdl(1, kern, dim3(grid), dim3(kFastThreads), smem, st, 0, rec, rectw, map, tiles, t_lo,
                                      t_hi, Qc, cap, keys, SV, sp, imask, x_lo, x_hi, flags, split);
     note_launch();
     return e != cudaSuccess ? e : cudaGetLastError();

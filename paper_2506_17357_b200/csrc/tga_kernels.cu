@@ -619,10 +619,11 @@ cudaError_t launch_pick_update(const DevState *states, const void *scans, int n_
     cudaError_t e;
     const auto *si = static_cast<const ScanArgs<int32_t> *>(scans);
     const auto *sf = static_cast<const ScanArgs<float> *>(scans);
-    if (is_int) e = tw ? launch_pdl(2, k_pick_update<int32_t, true>, g, dim3(256), smem, st, states, si, mask, cmask, 1, snap_cap)
-                       : launch_pdl(2, k_pick_update<int32_t, false>, g, dim3(256), smem, st, states, si, mask, cmask, 1, snap_cap);
-    else e = tw ? launch_pdl(2, k_pick_update<float, true>, g, dim3(256), smem, st, states, sf, mask, cmask, 0, snap_cap)
-                : launch_pdl(2, k_pick_update<float, false>, g, dim3(256), smem, st, states, sf, mask, cmask, 0, snap_cap);
+    const int coop = blocks_per_sol > 1 ? 1 : 0;   // its blocks wait for each other
+    if (is_int) e = tw ? launch_pdl(2, k_pick_update<int32_t, true>, g, dim3(256), smem, st, coop, states, si, mask, cmask, 1, snap_cap)
+                       : launch_pdl(2, k_pick_update<int32_t, false>, g, dim3(256), smem, st, coop, states, si, mask, cmask, 1, snap_cap);
+    else e = tw ? launch_pdl(2, k_pick_update<float, true>, g, dim3(256), smem, st, coop, states, sf, mask, cmask, 0, snap_cap)
+                : launch_pdl(2, k_pick_update<float, false>, g, dim3(256), smem, st, coop, states, sf, mask, cmask, 0, snap_cap);
     note_launch();
     return e != cudaSuccess ? e : cudaGetLastError();
 }

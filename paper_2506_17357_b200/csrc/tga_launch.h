@@ -121,19 +121,24 @@ void note_launch();
 // never take the SM slots a grid barrier of this kernel waits for).
 // Enabled per launch site with TGA_PDL_MODE (see pdl_enabled; off by default).
 bool pdl_enabled(int which = 1);
+// cooperative != 0: the launch guarantees that every block of the grid is resident
+// at once (or fails with cudaErrorCooperativeLaunchTooLarge instead of deadlocking)
+// -- required by kernels whose blocks wait for each other (grid barriers).
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(int which, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
-                       Args &&...args) {
+                       int cooperative, Args &&...args) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = pdl_enabled(which) ? 1 : 0;
+    at[1].id = cudaLaunchAttributeCooperative;
+    at[1].val.cooperative = cooperative;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 // population batch on the fast path: per-solution pointers, work = (k << 20 | I << 10 | J)

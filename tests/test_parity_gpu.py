@@ -660,3 +660,26 @@ def test_degenerate_shapes_exact(mode):
         host.step(m)
         dev.step_async(m)
         assert dev.routes() == host.routes(), name
+
+
+@pytest.mark.parametrize("n_shards", [2, 3, 8])
+def test_etga_virtual_shards_equal_unsharded(n_shards):
+    """ETGA cell shards (the row-shard plan of a multi-GPU run) min-combined on the
+    host == the unsharded keys; their evaluated-candidate counts add up."""
+    _need_gpu()
+    inst, sol = G.x_like(7, n=400, target_routes=17)
+    gs = T.Solution(T.Instance.from_gen(inst, granular_theta=12), sol)
+    gs.device_stats()
+    gs.eval(T.OP_ALL)
+    full = gs.keys()
+    full_counts, _ = gs.device_stats()
+    comb = np.full(T.N_VARIANTS, np.iinfo(np.uint64).max, dtype=np.uint64)
+    tot = np.zeros(T.N_VARIANTS, dtype=np.uint64)
+    for s in range(n_shards):
+        gs.set_shard(s, n_shards)
+        gs.eval(T.OP_ALL)
+        comb = np.minimum(comb, gs.keys())
+        c, _ = gs.device_stats()
+        tot += c
+    np.testing.assert_array_equal(comb, full)
+    np.testing.assert_array_equal(tot[1:11], full_counts[1:11])

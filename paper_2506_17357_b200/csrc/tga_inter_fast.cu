@@ -71,8 +71,11 @@ __device__ __forceinline__ void f_bulk(void *dst, const void *src, uint32_t byte
 // unsigned min keeps the lowest score and, among equal scores, the lowest row --
 // the lowest canonical index, since the column is fixed per lane (reading 5).
 // An infeasible candidate maps to 0xFFFFFFFF and never wins.
-__device__ __forceinline__ void keep(uint32_t &b, bool feas, int32_t dD, int row) {
-    const uint32_t k = (static_cast<uint32_t>(dD + (1 << 25)) << 5) | static_cast<uint32_t>(row);
+// mul32 is 32 held in an opaque register: the pack is then one IMAD (fma pipe) instead
+// of a LEA on the alu pipe, which the integer-heavy tile body saturates first (both
+// pipes issue every 2 cycles per SMSP, B300_MICROARCH "Pipe rates").
+__device__ __forceinline__ void keep(uint32_t &b, bool feas, int32_t dD, int row, uint32_t mul32) {
+    const uint32_t k = static_cast<uint32_t>(dD) * mul32 + static_cast<uint32_t>((1 << 30) + row);
     b = min(b, feas ? k : 0xFFFFFFFFu);
 }
 __device__ __forceinline__ void fold(uint64_t &acc, uint32_t b, bool direct, int u0, uint32_t v, uint32_t Qc) {
@@ -245,6 +248,7 @@ __device__ __forceinline__ void fast_body(ItemF item, int w0, int w1, int wstrid
     if (prb) g_inter_probe[8 * blockIdx.x + 1] = gtime();
     uint64_t *keys = w < w1 ? cur.keys : keys0;   // keys0: intra-only CTAs of one solution
     int sol = cur.sol;
+    const uint32_t mul32 = static_cast<uint32_t>(flags >> 8);   // 32, a kernel parameter: keep() packs with IMAD
     uint32_t ph0 = 0u, ph1 = 0u;
     for (int it = 0; w < w1; w += wstride, ++it) {
         const int b = it & 1;
@@ -288,7 +292,7 @@ __device__ __forceinline__ void fast_body(ItemF item, int w0, int w1, int wstrid
             if (!(ru < V.r)) continue;       // pair must span two routes, route(u) < route(v)
             const SlotTW &AT = TR[TW ? i : 0];
             cell_streams<TW, MASK>(A, V, AT, VT, cap, [&](int di, int dj) { return D(i, di, dj); },
-                                   [&](int k, bool ok, int32_t dD) { keep(run[k], ok, dD, i); });
+                                   [&](int k, bool ok, int32_t dD) { keep(run[k], ok, dD, i, mul32); });
         }
         // ---- fold this tile's streams into the per-variant 64-bit keys
         if (V.r >= 0) {
@@ -408,7 +412,8 @@ static cudaError_t launch_fast_t(const SlotRec *rec, const SlotTW *rectw, const 
         grid = std::max(groups, std::min(per_group * groups, std::min(res2, units_max)));
     }
     const int split = MASK2 ? grid / 2 : grid;
-    const int flags = (pdl_enabled(4) ? 1 : 0) | (inter_probe_on() ? 2 : 0);
+    // bits 0-1: PDL trigger placement, probe; bits 8+: the constant 32 for keep() (opaque to ptxas)
+    const int flags = (pdl_enabled(4) ? 1 : 0) | (inter_probe_on() ? 2 : 0) | (32 << 8);
     const cudaError_t e = launch_pdl(1, kern, dim3(grid), dim3(kFastThreads), smem, st, 0, rec, rectw, map, tiles, t_lo,
                                      t_hi, Qc, cap, keys, SV, sp, imask, x_lo, x_hi, flags, split);
     note_launch();
@@ -462,7 +467,7 @@ template <int U, bool TW, uint32_t MASK>
 __global__ void __launch_bounds__(kFastThreads) k_inter_fast_batch(const FastSol *__restrict__ sols,
                                                                    const CUtensorMap *__restrict__ maps,
                                                                    const uint32_t *__restrict__ work, int n_work,
-                                                                   int32_t cap, ScoreParams sp) {
+                                                                   int32_t cap, ScoreParams sp, int flags) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *sm = smem_raw + ((128u - (s_u32(smem_raw) & 127u)) & 127u);
     __shared__ uint64_t bar[2];
@@ -486,7 +491,7 @@ __global__ void __launch_bounds__(kFastThreads) k_inter_fast_batch(const FastSol
                         static_cast<int>(c & 0x3FFu)};
     };
     const SolView<int32_t> none{};
-    fast_body<U, TW, MASK>(item, w0, w1, 1, bar, red, sm, cap, none, sp, 0u, 0, 0, 0, 1, 0);
+    fast_body<U, TW, MASK>(item, w0, w1, 1, bar, red, sm, cap, none, sp, 0u, 0, 0, 0, 1, flags);
 }
 
 template <int U, bool TW, uint32_t MASK>
@@ -504,7 +509,7 @@ static cudaError_t launch_fast_batch_t(const FastSol *sols, const CUtensorMap *m
         res = std::max(1, b) * std::max(1, sms);
     }
     const int grid = std::max(1, std::min(n_work, std::min(res, max_grid)));
-    kern<<<grid, kFastThreads, G::Smem, st>>>(sols, maps, work, n_work, cap, sp);
+    kern<<<grid, kFastThreads, G::Smem, st>>>(sols, maps, work, n_work, cap, sp, 32 << 8);
     note_launch();
     return cudaGetLastError();
 }

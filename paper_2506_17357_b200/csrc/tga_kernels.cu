@@ -325,25 +325,52 @@ __device__ __forceinline__ void update_rows(const ScanArgs<DT> &A, DT *__restric
 }
 
 // Phase 2 (after phase 1 completed): the columns of the changed ranges, from the
-// refreshed rows by symmetry, Dp[a][c] = Dp[c][a] (c is symmetric; host-checked).
-// A unit = 8 consecutive rows a (one per warp), lanes along c: the writes are
-// contiguous and the strided reads of 8 neighbouring a share their sectors --
-// instead of scattered 4-byte gathers from C (measured 105 MB of DRAM reads per
-// update at n = 10^4 before this).
+// refreshed rows by symmetry, Dp[a][c] = Dp[c][a] (c is symmetric; host-checked),
+// as a tiled transpose through shared memory: a unit is 32 rows a x 128 changed
+// columns c; the changed rows are read along a (128-byte coalesced reads of the
+// just-written rows, L2-resident) and written along c.  Scattered 4-byte gathers
+// from C cost 105 MB of DRAM reads per update at n = 10^4; a warp per row a with
+// lanes along c read one sector per lane.  Requires blockDim.x to be a multiple of 32.
 template <class DT>
 __device__ __forceinline__ void update_cols(DT *__restrict__ Dp, int pitch, int Qp, const UpdateSpec u, int unit0,
                                             int ustride) {
     if (u.full) return;  // every row was refreshed
-    const int n1 = u.hi1 - u.lo1, n2 = u.hi2 - u.lo2;
-    const int total = (Qp + 7) / 8;
-    for (int b = unit0; b < total; b += ustride) {
-        const int a = b * 8 + static_cast<int>(threadIdx.x >> 5);
-        if (a >= Qp) continue;
-        DT *drow = Dp + static_cast<size_t>(a) * pitch;
-        for (int j = (threadIdx.x & 31); j < n1 + n2; j += 32) {
-            const int c = j < n1 ? u.lo1 + j : u.lo2 + (j - n1);
-            drow[c] = Dp[static_cast<size_t>(c) * pitch + a];
+    constexpr int TC = 128;   // changed columns per unit (many loads in flight per thread)
+    __shared__ DT tile[TC][33];
+    const int n1 = u.hi1 - u.lo1, n2 = u.hi2 - u.lo2, nc = n1 + n2;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int ncb = (nc + TC - 1) / TC, nab = (Qp + 31) / 32;
+    auto col = [&](int j) { return j < n1 ? u.lo1 + j : u.lo2 + (j - n1); };
+    for (int t = unit0; t < nab * ncb; t += ustride) {
+        const int a0 = (t / ncb) * 32, c0 = (t % ncb) * TC;
+        const int a = a0 + lane;
+        if (nw == 8) {   // every load of the unit in flight before the first store (latency-bound otherwise)
+            DT v[TC / 8];
+#pragma unroll
+            for (int q = 0; q < TC / 8; ++q) {
+                const int j = c0 + warp + 8 * q;
+                v[q] = (j < nc && a < Qp) ? Dp[static_cast<size_t>(col(j)) * pitch + a] : DT(0);
+            }
+#pragma unroll
+            for (int q = 0; q < TC / 8; ++q) tile[warp + 8 * q][lane] = v[q];
+        } else {
+            for (int cl = warp; cl < TC; cl += nw) {   // changed row c = col(c0 + cl), lanes along a
+                const int j = c0 + cl;
+                if (j < nc && a < Qp) tile[cl][lane] = Dp[static_cast<size_t>(col(j)) * pitch + a];
+            }
         }
+        __syncthreads();
+        for (int al = warp; al < 32; al += nw) {   // row a0 + al, lanes along the changed columns
+            const int ar = a0 + al;
+            if (ar >= Qp) continue;
+            DT *drow = Dp + static_cast<size_t>(ar) * pitch;
+#pragma unroll
+            for (int q = 0; q < TC / 32; ++q) {
+                const int j = c0 + q * 32 + lane;
+                if (j < nc) drow[col(j)] = tile[q * 32 + lane][al];
+            }
+        }
+        __syncthreads();
     }
 }
 

@@ -518,19 +518,37 @@ __device__ __forceinline__ void pick_update_multi(const DevState &S, const ScanA
     }
     // 4b. Dp rows of the changed slots: Dp[a][c] = c(new node(a), node(c)), c < pitch
     if (b < row_blocks) {
+        constexpr int B = 4;   // column chunks per thread with all their loads in flight
+        const int step = 4 * static_cast<int>(blockDim.x);
         for (int j = b; j < nrows; j += row_blocks) {
             const int a = j < n1 ? lo0 + j : lo1 + (j - n1);
             const DT *crow = C + static_cast<size_t>(nn[j]) * n;
             DT *drow = Dp + static_cast<size_t>(a) * pitch;
-            for (int c = 4 * tid; c < pitch; c += 4 * blockDim.x) {
-                int4 nd = *reinterpret_cast<const int4 *>(S.node + c);
-                int t;
-                if ((t = in_chg(c)) >= 0) nd.x = nn[t];
-                if ((t = in_chg(c + 1)) >= 0) nd.y = nn[t];
-                if ((t = in_chg(c + 2)) >= 0) nd.z = nn[t];
-                if ((t = in_chg(c + 3)) >= 0) nd.w = nn[t];
-                *reinterpret_cast<int4 *>(drow + c) = make_int4(bits(__ldg(crow + nd.x)), bits(__ldg(crow + nd.y)),
-                                                               bits(__ldg(crow + nd.z)), bits(__ldg(crow + nd.w)));
+            for (int cb = 4 * tid; cb < pitch; cb += B * step) {
+                int4 nd[B];
+#pragma unroll
+                for (int k = 0; k < B; ++k) {
+                    const int c = cb + k * step;
+                    nd[k] = c < pitch ? *reinterpret_cast<const int4 *>(S.node + c) : make_int4(0, 0, 0, 0);
+                }
+                DT v[B][4];
+#pragma unroll
+                for (int k = 0; k < B; ++k) {
+                    const int c = cb + k * step;
+                    int t;
+                    if ((t = in_chg(c)) >= 0) nd[k].x = nn[t];
+                    if ((t = in_chg(c + 1)) >= 0) nd[k].y = nn[t];
+                    if ((t = in_chg(c + 2)) >= 0) nd[k].z = nn[t];
+                    if ((t = in_chg(c + 3)) >= 0) nd[k].w = nn[t];
+                    v[k][0] = __ldg(crow + nd[k].x); v[k][1] = __ldg(crow + nd[k].y);
+                    v[k][2] = __ldg(crow + nd[k].z); v[k][3] = __ldg(crow + nd[k].w);
+                }
+#pragma unroll
+                for (int k = 0; k < B; ++k) {
+                    const int c = cb + k * step;
+                    if (c < pitch)
+                        *reinterpret_cast<int4 *>(drow + c) = make_int4(bits(v[k][0]), bits(v[k][1]), bits(v[k][2]), bits(v[k][3]));
+                }
             }
         }
     }
@@ -637,7 +655,7 @@ cudaError_t launch_pick_update(const DevState *states, const void *scans, int n_
     const int smem = multi ? std::max(smem_old, smem_multi) : smem_old;
     const int snap_cap = multi ? 2 * max_cap : 0;
     dim3 g(blocks_per_sol, n_sol);
-    if (smem > 40 * 1024) {  // dynamic + static shared memory above the 48 KB default needs the opt-in
+    {  // dynamic + static shared memory above the 48 KB default needs the opt-in (static: ~20 KB)
         cudaFuncSetAttribute(k_pick_update<int32_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         cudaFuncSetAttribute(k_pick_update<int32_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         cudaFuncSetAttribute(k_pick_update<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

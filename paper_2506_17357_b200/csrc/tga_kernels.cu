@@ -56,14 +56,20 @@ __global__ void __launch_bounds__(256) k_dp_cols(DT *__restrict__ Dp, int pitch,
 // (global arrays for a plain rebuild; the decoded new route in the device step,
 // whose slot arrays are rewritten concurrently).  base, L, cap: the route's first
 // physical slot, customer count and slot capacity.
-template <class DT, bool TW, class NodeF, class CanonF>
-__device__ __forceinline__ void scan_route_g(const ScanArgs<DT> &A, const int r, const int lane, const int base,
-                                             const int L, const int cap, NodeF nodeAt, CanonF canonAt) {
+// NodeF(x) / CanonF(x): node id / canonical-validity of slot x of this route
+// (global arrays for a plain rebuild; the decoded new route in the device step,
+// whose slot arrays are rewritten concurrently).  base, L, cap: the route's first
+// physical slot, customer count and slot capacity.  The rebuild is three passes:
+// forward (prefix records), backward (suffix records), per-slot records; a warp
+// runs them one after the other (scan_route_g), a block can run the first two in
+// two warps at once and the third over all its threads (scan_route_block).
+template <class DT, bool TW>
+__device__ __forceinline__ void scan_spare(const ScanArgs<DT> &A, const int k0, const int kstep, const int base,
+                                           const int L, const int cap) {
     const int len = L + 2;
-    const int n = A.n_nodes;
     if constexpr (std::is_same<DT, int32_t>::value) {
         // spare (hole) slots of the route carry poisoned fast-path records
-        for (int k = len + lane; k < cap; k += 32) {
+        for (int k = len + k0; k < cap; k += kstep) {
             if (A.rec) {
                 SlotRec q{};
                 q.r = -1; q.fL = q.bL1 = q.W = kPoison;
@@ -79,6 +85,13 @@ __device__ __forceinline__ void scan_route_g(const ScanArgs<DT> &A, const int r,
         }
     }
 
+}
+
+template <class DT, bool TW, class NodeF>
+__device__ __forceinline__ int scan_fwd_pass(const ScanArgs<DT> &A, const int r, const int lane, const int base,
+                                             const int L, NodeF nodeAt) {
+    const int len = L + 2;
+    const int n = A.n_nodes;
     // ---------------- forward pass: prefix loads, prefix distance, prefix TW records
     int carryL = 0;
     DT carryD = DT(0);
@@ -144,6 +157,14 @@ __device__ __forceinline__ void scan_route_g(const ScanArgs<DT> &A, const int r,
         if (TW) A.rTV[r] = carryT.w;
     }
 
+    return carryL;   // route load (Eq. 3f over the whole route)
+}
+
+template <class DT, bool TW, class NodeF>
+__device__ __forceinline__ void scan_bwd_pass(const ScanArgs<DT> &A, const int r, const int lane, const int base,
+                                              const int L, NodeF nodeAt, const bool e_from_C) {
+    const int len = L + 2;
+    const int n = A.n_nodes;
     // ---------------- backward pass: suffix loads, suffix distance, suffix TW records
     int bcarryL = 0;
     DT bcarryD = DT(0);
@@ -156,7 +177,10 @@ __device__ __forceinline__ void scan_route_g(const ScanArgs<DT> &A, const int r,
         const bool in = lane < nvalid;
         const int x = base + k;
         const int nd = in ? nodeAt(x) : 0;
-        const DT e = in ? A.enext[x] : DT(0);  // written by the forward pass (same warp)
+        // the edge out of position k: written by the forward pass (same warp), or
+        // gathered again when the two passes run in different warps
+        const DT e = !in ? DT(0) : (e_from_C ? ((k + 1 < len) ? A.C[static_cast<size_t>(nd) * n + nodeAt(x + 1)] : DT(0))
+                                              : A.enext[x]);
         int sL = in ? A.demand[nd] : 0;
         DT sD = e;
 #pragma unroll
@@ -198,11 +222,16 @@ __device__ __forceinline__ void scan_route_g(const ScanArgs<DT> &A, const int r,
         }
     }
     if (lane == 0) A.rD[r] = bcarryD;
-    const int Wr = carryL;  // route load (Eq. 3f over the whole route)
-    __syncwarp();           // fwdL / bwdL / enext of this route are visible to the whole warp
+}
 
+template <class DT, bool TW, class NodeF, class CanonF>
+__device__ __forceinline__ void scan_rec_pass(const ScanArgs<DT> &A, const int r, const int k0, const int kstep,
+                                              const int base, const int L, const int Wr, NodeF nodeAt,
+                                              CanonF canonAt) {
+    const int len = L + 2;
+    const int n = A.n_nodes;
     // ---------------- per-position segment records and bridges (N = 1..3)
-    for (int k = lane; k < len; k += 32) {
+    for (int k = k0; k < len; k += kstep) {
         const int x = base + k;
         // bridge_N[x] = c(x-1, x+N): the edge that closes the gap left by removing
         // the segment x..x+N-1 (relocate / or-opt removal, Eq. 2)
@@ -214,6 +243,7 @@ __device__ __forceinline__ void scan_route_g(const ScanArgs<DT> &A, const int r,
         A.bridge1[x] = b1;
         A.bridge2[x] = b2;
         A.bridge3[x] = b3;
+        TwRec seg2v = make_float4(0.f, 0.f, 0.f, 0.f), seg3v = seg2v;   // kept for the SlotTW below
         if (TW) {
             const TwRec s1 = A.node_tw[nodeAt(x)];
             TwRec s2 = s1, s3 = s1;
@@ -224,6 +254,8 @@ __device__ __forceinline__ void scan_route_g(const ScanArgs<DT> &A, const int r,
             }
             A.seg2T[x] = s2;
             A.seg3T[x] = s3;
+            seg2v = s2;
+            seg3v = s3;
         }
         if constexpr (std::is_same<DT, int32_t>::value) {
             if (A.rec) {
@@ -245,7 +277,7 @@ __device__ __forceinline__ void scan_route_g(const ScanArgs<DT> &A, const int r,
                     w.EF = EFof(x);
                     w.EFm = (k >= 1) ? EFof(x - 1) : kTwBig;
                     const TwRec s1 = A.node_tw[nodeAt(x)];
-                    const TwRec sg[3] = {s1, A.seg2T[x], A.seg3T[x]};
+                    const TwRec sg[3] = {s1, seg2v, seg3v};
 #pragma unroll
                     for (int N = 1; N <= 3; ++N) {
                         const bool segok = (k >= 1) && (k + N - 1 <= L);
@@ -276,6 +308,30 @@ __device__ __forceinline__ void scan_route_g(const ScanArgs<DT> &A, const int r,
             }
         }
     }
+}
+
+template <class DT, bool TW, class NodeF, class CanonF>
+__device__ __forceinline__ void scan_route_g(const ScanArgs<DT> &A, const int r, const int lane, const int base,
+                                             const int L, const int cap, NodeF nodeAt, CanonF canonAt) {
+    scan_spare<DT, TW>(A, lane, 32, base, L, cap);
+    const int Wr = scan_fwd_pass<DT, TW>(A, r, lane, base, L, nodeAt);
+    scan_bwd_pass<DT, TW>(A, r, lane, base, L, nodeAt, false);
+    __syncwarp();   // fwdL / bwdL / enext of this route are visible to the whole warp
+    scan_rec_pass<DT, TW>(A, r, lane, 32, base, L, Wr, nodeAt, canonAt);
+}
+
+// The same rebuild by a whole block (every thread must call it): forward and
+// backward passes in warps 0 and 1 at once, then the per-slot records over all
+// threads -- the critical path of the device step's update for long routes.
+template <class DT, bool TW, class NodeF, class CanonF>
+__device__ __forceinline__ void scan_route_block(const ScanArgs<DT> &A, const int r, const int base, const int L,
+                                                 const int cap, NodeF nodeAt, CanonF canonAt) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    scan_spare<DT, TW>(A, tid, blockDim.x, base, L, cap);
+    if (warp == 0) scan_fwd_pass<DT, TW>(A, r, lane, base, L, nodeAt);
+    else if (warp == 1) scan_bwd_pass<DT, TW>(A, r, lane, base, L, nodeAt, true);
+    __syncthreads();   // prefix / suffix records and rW[r] of this route are visible to the block
+    scan_rec_pass<DT, TW>(A, r, tid, blockDim.x, base, L, A.rW[r], nodeAt, canonAt);
 }
 
 template <class DT, bool TW>
@@ -414,6 +470,11 @@ __device__ __forceinline__ void solution_barrier(int32_t *counter, int nblocks) 
 // A route that outgrew its slots takes the full relayout path of pick_apply_body.
 constexpr int kDirectColsQp = 2560;
 
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 __device__ __forceinline__ void block_arrive(int32_t *counter) {
     if (threadIdx.x == 0) atomicAdd(counter, 1);
 }
@@ -443,6 +504,7 @@ __device__ __forceinline__ void pick_update_multi(const DevState &S, const ScanA
     if (tid < 23) skeys[tid] = S.keys[tid];
     __syncthreads();
     if (tid == 0) probe(pr, 1);
+    if (pr) S.acc[43] = gtimer();   // diagnostics: block 0 start of decode (globaltimer)
     if (tid < 32) decode_best(skeys, mask, integer, sb, sl, R, S.Qc, dm);
     __syncthreads();
     if (tid == 0) probe(pr, 2);
@@ -508,12 +570,13 @@ __device__ __forceinline__ void pick_update_multi(const DevState &S, const ScanA
     const int scan0 = split_roles ? G - dm.nrt : 1;                  // first scanning block
     const int row_blocks = split_roles ? nrows : G, col0 = split_roles ? nrows : 0;
     const int col_blocks = split_roles ? G - dm.nrt - nrows : G;
-    // 4a. re-scan of the changed routes (warp 0 of one block each; the longest chains)
+    // 4a. re-scan of the changed routes (one block each; the longest chains)
     for (int q = 0; q < dm.nrt; ++q) {
-        if (b == (scan0 + q) % G && tid < 32) {
+        if (b == (scan0 + q) % G) {   // block-uniform: the whole block rebuilds the route
             const int r = dm.nr[q].r, base = dm.lo[q], off = q ? n1 : 0;
-            scan_route_g<DT, TW>(A, r, tid, base, dm.nr[q].L, dm.hi[q] - base,
-                                 [&](int x) { return nn[off + x - base]; }, [&](int x) { return x; });
+            scan_route_block<DT, TW>(A, r, base, dm.nr[q].L, dm.hi[q] - base,
+                                     [&](int x) { return nn[off + x - base]; }, [&](int x) { return x; });
+            if (tid == 0 && S.acc[31]) S.acc[44 + q] = gtimer();   // diagnostics: scan end (globaltimer)
         }
     }
     // 4b. Dp rows of the changed slots: Dp[a][c] = c(new node(a), node(c)), c < pitch
@@ -607,6 +670,7 @@ __device__ __forceinline__ void pick_update_multi(const DevState &S, const ScanA
     }
     __syncthreads();
     if (tid == 0) probe(pr, 7);
+    if (pr) S.acc[46] = gtimer();
 }
 
 template <class DT, bool TW>

@@ -26,6 +26,8 @@ for k in range(a.steps):
     p = gs.debug_probe(False).astype(np.int64)
     d = [int(p[i] - p[0]) if p[i] else -1 for i in range(8)]
     rows.append(d)
-    print(a.config, "step %.1f us" % (1e3 * float(ms[0])), "phase cycles", d)
+    print(a.config, "step %.1f us" % (1e3 * float(ms[0])), "phase cycles", d,
+          "| scan ends (ns after block 0 decode):", [int(p[12 + q]) - int(p[11]) if p[12 + q] else None for q in range(2)],
+          "block 0 end:", int(p[14]) - int(p[11]) if p[14] else None)
 r = np.array(rows[2:], dtype=np.float64)
 print("median phase (us @1.965GHz):", [round(x / 1965.0, 2) for x in np.median(r, axis=0)])

@@ -516,7 +516,9 @@ __device__ __forceinline__ void pick_update_multi(const DevState &S, const ScanA
     __syncthreads();
     if (tid == 0) arrive_v = atomicAdd(S.desc + 9, 1);
     pdl_trigger();  // this block is resident and arrived: a dependent grid cannot starve the wait below
-    if (b == G - 1) neighbourhood_counts(S, cmask, sl);  // the evaluated (old) lengths
+    // the closed-form counts of the evaluated (old) lengths, on a block that does not
+    // rebuild a route (those are the last blocks when the update roles are split)
+    if (b == G / 2) neighbourhood_counts(S, cmask, sl);
     if (!dm.applied) {
         if (b == 0 && tid == 0) {
             S.desc[0] = 0;

@@ -186,6 +186,8 @@ struct tga_solution {
     size_t lay_pitch = 0, route_pitch = 0;              // arena pitch of the slot / route arrays
     cudaStream_t stream = nullptr;                     // current stream (own or user's)
     cudaStream_t own_stream = nullptr;
+    cudaStream_t side = nullptr;                       // fork for a concurrent intra-route kernel
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int shard = 0, n_shards = 1;
     ncclComm_t comm = nullptr;
     int sm_count = 148;
@@ -487,6 +489,9 @@ static void free_solution(tga_solution *s) {
     if (s->h_stage) cudaFreeHost(s->h_stage);
     if (s->h_rstage) cudaFreeHost(s->h_rstage);
     if (s->own_stream) cudaStreamDestroy(s->own_stream);
+    if (s->side) cudaStreamDestroy(s->side);
+    if (s->ev_fork) cudaEventDestroy(s->ev_fork);
+    if (s->ev_join) cudaEventDestroy(s->ev_join);
     for (auto e : s->tev) cudaEventDestroy(e);
     delete s;
 }
@@ -653,6 +658,10 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
     if (cudaStreamCreateWithFlags(&s->own_stream, cudaStreamNonBlocking) != cudaSuccess)
         return bail(fail(TGA_ERR_CUDA, "stream create"));
     s->stream = s->own_stream;
+    if (cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming) != cudaSuccess)
+        return bail(fail(TGA_ERR_CUDA, "side stream"));
     // ---- device arena: slot arrays (with guards), per-route arrays, keys, tiles
     const size_t cap = s->cap, Rr = static_cast<size_t>(R) + 1;
     struct Item { void **p; size_t bytes; };
@@ -871,6 +880,22 @@ extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
     cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
     if (timed) TGA_CUDA(cudaStreamIsCapturing(st, &cst));
     const unsigned rec_flags = cst == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
+    // VRPTW: the intra-route kernel is latency-bound and independent of the inter-route one;
+    // TGA_FORK_INTRA=1 runs it on a forked stream beside it.  Off by default: measured 2-3 %
+    // faster steps (cfg3 40.4 -> 39.2 us) but the inter kernel then shares the SMs, so its own
+    // duration (the roofline's) grows 23 -> 32 us.
+    static const bool fork_env = std::getenv("TGA_FORK_INTRA") && std::atoi(std::getenv("TGA_FORK_INTRA")) == 1;
+    static const int force_warp = std::getenv("TGA_WARP_TW") ? std::atoi(std::getenv("TGA_WARP_TW")) : 1;
+    const bool fork_intra = fork_env && I->tw && (mask & TGA_OP_INTER) && (mask & TGA_OP_INTRA) && x_hi > x_lo;
+    if (fork_intra) {
+        TGA_CUDA(cudaEventRecord(s->ev_fork, st));
+        TGA_CUDA(cudaStreamWaitEvent(s->side, s->ev_fork, 0));
+        const cudaError_t ei = I->dtype == TGA_I32
+            ? launch_intra<int32_t>(mask, true, sol_view<int32_t>(s), sp, x_lo, x_hi, s->keys, s->side, false, force_warp != 0)
+            : launch_intra<float>(mask, true, sol_view<float>(s), sp, x_lo, x_hi, s->keys, s->side, false, force_warp != 0);
+        if (ei != cudaSuccess) return fail(TGA_ERR_CUDA, std::string("intra launch: ") + cudaGetErrorString(ei));
+        TGA_CUDA(cudaEventRecord(s->ev_join, s->side));
+    }
     if (timed) TGA_CUDA(cudaEventRecordWithFlags(s->tev[s->tev_n], st, rec_flags));
     const bool etga = I->theta > 0;
     if (etga && !(I->dtype == TGA_I32 && s->fast))
@@ -908,11 +933,11 @@ extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
         TGA_CUDA(cudaEventRecordWithFlags(s->tev[s->tev_n + 1], st, rec_flags));
         s->tev_n += 2;
     }
-    if (e == cudaSuccess && !fused_intra) {
+    if (fork_intra && e == cudaSuccess) TGA_CUDA(cudaStreamWaitEvent(st, s->ev_join, 0));  // join
+    if (e == cudaSuccess && !fused_intra && !fork_intra) {
         // VRPTW intra: the warp-parallel kernel (warp scans of Eq. 4 records) -- measured faster than the
         // thread-per-(slot, variant) walk for short routes too since its loads are hoisted (cfg3 R1:
         // 41.8 vs 43.9 us/step; R2: 57.1 vs 92.5).  TGA_WARP_TW=0 selects the walk (A/B override).
-        static const int force_warp = std::getenv("TGA_WARP_TW") ? std::atoi(std::getenv("TGA_WARP_TW")) : 1;
         const bool warp_tw = force_warp != 0;
         if (I->dtype == TGA_I32)
             e = launch_intra<int32_t>(mask, I->tw, sol_view<int32_t>(s), sp, x_lo, x_hi, s->keys, st,

@@ -482,6 +482,11 @@ static void build_tiles(tga_solution *s) {
 static void free_solution(tga_solution *s) {
     if (!s) return;
     if (s->inst) cudaSetDevice(s->inst->device);
+    // work still queued on the solution's streams must not outlive its memory
+    if (s->stream) cudaStreamSynchronize(s->stream);
+    if (s->own_stream && s->own_stream != s->stream) cudaStreamSynchronize(s->own_stream);
+    if (s->side) cudaStreamSynchronize(s->side);
+    (void)cudaGetLastError();
     if (s->comm && g_nccl.commDestroy) g_nccl.commDestroy(s->comm);
     if (s->arena) cudaFree(s->arena);
     if (s->Dp) cudaFree(s->Dp);
@@ -603,6 +608,8 @@ extern "C" int32_t tga_instance_info(const tga_instance *I, int32_t *n_nodes, in
 extern "C" int32_t tga_instance_destroy(tga_instance *I) {
     if (!I) return TGA_OK;
     cudaSetDevice(I->device);
+    cudaDeviceSynchronize();   // no solution's queued work may still read C / demand / windows
+    (void)cudaGetLastError();
     cudaFree(I->dC);
     cudaFree(I->dDemand);
     cudaFree(I->dNodeTw);

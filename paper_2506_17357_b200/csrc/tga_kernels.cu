@@ -511,8 +511,22 @@ __device__ __forceinline__ void pick_update_multi(const DevState &S, const ScanA
     const int n1 = dm.applied && !dm.full ? dm.hi[0] - dm.lo[0] : 0;
     const int n2 = dm.applied && !dm.full ? dm.hi[1] - dm.lo[1] : 0;
     const int lo0 = dm.lo[0], lo1 = dm.lo[1];
-    // ---- 2. snapshot the old node ids (fits case), then arrive
-    for (int j = tid; j < n1 + n2; j += blockDim.x) snap[j] = S.node[j < n1 ? lo0 + j : lo1 + (j - n1)];
+    // ---- 2. new node ids of the changed ranges straight from the old slots through the
+    // pieces (start / end depot and spare slots: 0), then arrive -- every read of an old
+    // node id of this block is done before block 0 may overwrite them
+    for (int j = tid; j < n1 + n2; j += blockDim.x) {
+        const int q = j < n1 ? 0 : 1;
+        const NewRoute &nr = dm.nr[q];
+        const int p = j - (q ? n1 : 0);  // position in the route (base == lo[q])
+        int32_t nd = 0;
+        if (p >= 1 && p <= nr.L) {
+            int off = p - 1, k = 0;
+            while (off >= nr.p[k].len) { off -= nr.p[k].len; ++k; }
+            const Piece &pc = nr.p[k];
+            nd = S.node[sb[pc.src] + (pc.rev ? pc.start + pc.len - 1 - off : pc.start + off)];
+        }
+        nn[j] = nd;
+    }
     __syncthreads();
     if (tid == 0) arrive_v = atomicAdd(S.desc + 9, 1);
     pdl_trigger();  // this block is resident and arrived: a dependent grid cannot starve the wait below
@@ -541,21 +555,6 @@ __device__ __forceinline__ void pick_update_multi(const DevState &S, const ScanA
         return;
     }
     if (tid == 0) probe(pr, 3);
-    // ---- 3. new node ids of the changed ranges (start / end depot and spare slots: 0)
-    auto old_of = [&](int os) -> int32_t { return (os >= lo0 && os < lo0 + n1) ? snap[os - lo0] : snap[n1 + os - lo1]; };
-    for (int j = tid; j < n1 + n2; j += blockDim.x) {
-        const int q = j < n1 ? 0 : 1;
-        const NewRoute &nr = dm.nr[q];
-        const int p = j - (q ? n1 : 0);  // position in the route (base == lo[q])
-        int32_t nd = 0;
-        if (p >= 1 && p <= nr.L) {
-            int off = p - 1, k = 0;
-            while (off >= nr.p[k].len) { off -= nr.p[k].len; ++k; }
-            const Piece &pc = nr.p[k];
-            nd = old_of(sb[pc.src] + (pc.rev ? pc.start + pc.len - 1 - off : pc.start + off));
-        }
-        nn[j] = nd;
-    }
     __syncthreads();
     if (tid == 0) probe(pr, 4);
     auto in_chg = [&](int c) -> int { return (c >= lo0 && c < lo0 + n1) ? c - lo0 : ((c >= lo1 && c < lo1 + n2) ? n1 + c - lo1 : -1); };
@@ -568,10 +567,12 @@ __device__ __forceinline__ void pick_update_multi(const DevState &S, const ScanA
     // Symmetric columns (large Qp): rows and re-scans on every block, then a barrier.
     const bool direct = Qp <= kDirectColsQp;
     const int nrows = n1 + n2;
-    const bool split_roles = direct && G >= nrows + dm.nrt + 2;
+    // block 0 keeps only the final slot-array writes (it is the one that waits for
+    // every arrival): rows on blocks 1 .. nrows, columns after them, re-scans last
+    const bool split_roles = direct && G >= nrows + dm.nrt + 3;
     const int scan0 = split_roles ? G - dm.nrt : 1;                  // first scanning block
-    const int row_blocks = split_roles ? nrows : G, col0 = split_roles ? nrows : 0;
-    const int col_blocks = split_roles ? G - dm.nrt - nrows : G;
+    const int row0 = split_roles ? 1 : 0, row_blocks = split_roles ? nrows : G;
+    const int col0 = split_roles ? nrows + 1 : 0, col_blocks = split_roles ? G - dm.nrt - nrows - 1 : G;
     // 4a. re-scan of the changed routes (one block each; the longest chains)
     for (int q = 0; q < dm.nrt; ++q) {
         if (b == (scan0 + q) % G) {   // block-uniform: the whole block rebuilds the route
@@ -582,10 +583,10 @@ __device__ __forceinline__ void pick_update_multi(const DevState &S, const ScanA
         }
     }
     // 4b. Dp rows of the changed slots: Dp[a][c] = c(new node(a), node(c)), c < pitch
-    if (b < row_blocks) {
+    if (b >= row0 && b < row0 + row_blocks) {
         constexpr int B = 4;   // column chunks per thread with all their loads in flight
         const int step = 4 * static_cast<int>(blockDim.x);
-        for (int j = b; j < nrows; j += row_blocks) {
+        for (int j = b - row0; j < nrows; j += row_blocks) {
             const int a = j < n1 ? lo0 + j : lo1 + (j - n1);
             const DT *crow = C + static_cast<size_t>(nn[j]) * n;
             DT *drow = Dp + static_cast<size_t>(a) * pitch;

@@ -283,7 +283,10 @@ __device__ __forceinline__ void fast_body(ItemF item, int w0, int w1, int wstrid
 #pragma unroll
         for (int k = 0; k < 16; ++k) run[k] = 0xFFFFFFFFu;
 
-#pragma unroll
+        // the time-window body is large: fully unrolled it overflows the instruction cache
+        // (ncu: 38 % of the batch kernel's stalls were no_inst), so it is unrolled by 4 rows
+        constexpr int kRowUnroll = TW ? 4 : U;
+#pragma unroll kRowUnroll
         for (int i = 0; i < U; ++i) {
             const SlotRec &A = RW[i];       // row u = u0 + i (broadcast reads)
             const int32_t ru = A.r;

@@ -283,9 +283,11 @@ __device__ __forceinline__ void fast_body(ItemF item, int w0, int w1, int wstrid
 #pragma unroll
         for (int k = 0; k < 16; ++k) run[k] = 0xFFFFFFFFu;
 
-        // the time-window body is large: fully unrolled it overflows the instruction cache
-        // (ncu: 38 % of the batch kernel's stalls were no_inst), so it is unrolled by 4 rows
-        constexpr int kRowUnroll = TW ? 4 : U;
+        // the body is large: fully unrolled over the 16 rows it overflows the instruction
+        // cache (ncu: 38 % no_inst stalls in the TW batch kernel, 8 % at cfg4), so it is
+        // unrolled by 4 rows with time windows, by 8 without (measured best: cfg4 inter
+        // 365 -> 351 us at 8, 424 us at 4)
+        constexpr int kRowUnroll = TW ? 4 : 8;
 #pragma unroll kRowUnroll
         for (int i = 0; i < U; ++i) {
             const SlotRec &A = RW[i];       // row u = u0 + i (broadcast reads)

@@ -530,18 +530,23 @@ def run_tga(args):
     hbm_peak = float(pk["hbm_gbs"]) * 1e9
     t_hbm = alg_bytes / hbm_peak
     t_alu = alg_ops / alu_peak
+    traffic_key = ("etga_" if args.granular else "") + args.config   # captures are per kernel
     hbm_view = {"bound": "hbm", "achieved": alg_bytes / inter_avg_s / 1e9, "peak": hbm_peak / 1e9,
                 "unit": "GB/s", "frac": (alg_bytes / inter_avg_s) / hbm_peak,
-                "traffic": traffic_for(args.config), "peak_source": pk_src}
+                "traffic": traffic_for(traffic_key), "peak_source": pk_src}
     alu_view = {"bound": "alu", "achieved": alg_ops / inter_avg_s / 1e12, "peak": alu_peak / 1e12,
                 "unit": "Tops/s", "frac": (alg_ops / inter_avg_s) / alu_peak,
-                "traffic": traffic_for(args.config),
+                "traffic": traffic_for(traffic_key),
                 "peak_source": f"148 SM x 128 lanes x {sm_mhz_peak:.0f} MHz ({pk_src} sm_max_mhz)"}
     primary, alt = (alu_view, hbm_view) if t_alu >= t_hbm else (hbm_view, alu_view)
-    primary = dict(primary, kernel=("k_inter_fast<all-inter> (CVRP: inter tiles + intra warps in one launch)"
-                                    if inst.tw is None else
-                                    "k_inter_fast<TW, all-inter> (VRPTW inter tiles; intra in its own kernel)")
-                   + ", live CUDA events",
+    if args.granular:
+        kname = ("k_etga<" + ("TW, " if inst.tw is not None else "") + "all-inter> (+ k_slot_of after a host "
+                 "layout): the edge-mask cells; intra variants in their own kernels")
+    elif inst.tw is None:
+        kname = "k_inter_fast<all-inter> (CVRP: inter tiles + intra warps in one launch)"
+    else:
+        kname = "k_inter_fast<TW, all-inter> (VRPTW inter tiles; intra in its own kernel)"
+    primary = dict(primary, kernel=kname + ", live CUDA events",
                    kernel_ms=inter_avg_s * 1e3, candidates_per_launch=inter_cands,
                    alg_bytes_per_launch=alg_bytes, alg_ops_per_launch=alg_ops)
 

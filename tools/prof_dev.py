@@ -7,9 +7,10 @@ from paper_2506_17357_b200 import tga as T
 ap = argparse.ArgumentParser()
 ap.add_argument("--steps", type=int, default=6)
 ap.add_argument("--config", default="cfg2")
+ap.add_argument("--granular", type=int, default=0)
 a = ap.parse_args()
 inst, sol = G.config(a.config)
-gi = T.Instance.from_gen(inst)
+gi = T.Instance.from_gen(inst, granular_theta=a.granular)
 gs = T.Solution(gi, sol)
 mask = T.OP_ALL if inst.tw is None else T.OP_ALL & ~T.OP_2OPT
 ms = gs.descent(mask, a.steps, timed=True)

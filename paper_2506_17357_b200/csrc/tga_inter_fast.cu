@@ -155,6 +155,10 @@ __device__ __forceinline__ void cell_streams(const SlotRec &A, const SlotRec &V,
     }
 }
 
+#ifndef TGA_FAST_CTA_SYNC
+#define TGA_FAST_CTA_SYNC 0   // 1: the former __syncthreads per tile before a stage is refilled
+#endif
+
 // one work item of the fused sweep: tile (I, J) of one solution
 struct FastItem {
     const SlotRec *rec;
@@ -233,7 +237,21 @@ __device__ __forceinline__ void fast_body(ItemF item, int w0, int w1, int wstrid
     int w = w0;
     FastItem cur{};
     if (w < w1) cur = item(w);
+#if TGA_FAST_CTA_SYNC
     if (tid == 0 && w < w1) issue(cur, 0);
+#else
+    // buffer release without a CTA barrier: each warp counts itself out of a stage when it has
+    // read it; the last one out refills it with the tile two iterations ahead. Warps whose
+    // columns skip more rows (route order, end depots) run up to one tile ahead instead of
+    // waiting at a __syncthreads per tile.
+    __shared__ int s_out[2];
+    if (tid == 0) {
+        s_out[0] = 0;
+        s_out[1] = 0;
+        if (w < w1) issue(cur, 0);                              // arrive (release) publishes s_out
+        if (w + wstride < w1) issue(item(w + wstride), 1);
+    }
+#endif
     // intra-route CVRP work of this launch (one u slot per warp) while the first
     // tile's TMA is in flight: the whole neighbourhood is one kernel
     if (imask) {
@@ -255,7 +273,9 @@ __device__ __forceinline__ void fast_body(ItemF item, int w0, int w1, int wstrid
         const FastItem f = cur;
         if (w + wstride < w1) {
             cur = item(w + wstride);
+#if TGA_FAST_CTA_SYNC
             if (tid == 0) issue(cur, b ^ 1);
+#endif
         }
         if (f.sol != sol) {   // a batch run moved on to the next solution (CTA-uniform)
             flush(keys);
@@ -299,6 +319,23 @@ __device__ __forceinline__ void fast_body(ItemF item, int w0, int w1, int wstrid
             cell_streams<TW, MASK>(A, V, AT, VT, cap, [&](int di, int dj) { return D(i, di, dj); },
                                    [&](int k, bool ok, int32_t dD) { keep(run[k], ok, dD, i, mul32); });
         }
+#if !TGA_FAST_CTA_SYNC
+        // this warp is done with stage b (every shared read above has returned its value)
+        __syncwarp();
+        int last = 0;
+        if (lane == 0) {
+            __threadfence_block();
+            last = atomicAdd(&s_out[b], 1) == kFastThreads / 32 - 1;
+            if (last) {
+                s_out[b] = 0;
+                if (w + 2 * wstride < w1) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before the TMA writes
+                    issue(item(w + 2 * wstride), b);
+                }
+            }
+        }
+        (void)last;
+#endif
         // ---- fold this tile's streams into the per-variant 64-bit keys
         if (V.r >= 0) {
             const uint32_t cv = static_cast<uint32_t>(v);  // physical column slot
@@ -316,7 +353,9 @@ __device__ __forceinline__ void fast_body(ItemF item, int w0, int w1, int wstrid
             if (MASK & (1u << 9)) { fold(acc[9], run[13], true, u0, cv, Qc); fold(acc[9], run[14], false, u0, cv, Qc); }
             if (MASK & (1u << 10)) fold(acc[10], run[15], true, u0, cv, Qc);
         }
+#if TGA_FAST_CTA_SYNC
         __syncthreads();  // buffer b is refilled two iterations later
+#endif
     }
 
     if (flags & 1) pdl_trigger();

@@ -1053,10 +1053,14 @@ __device__ __forceinline__ void intra_body(const SolView<DT> &S, const ScorePara
     if (threadIdx.x < 23) red[threadIdx.x] = kNoKey;
     __syncthreads();
     // a warp takes one variant for 32 consecutive slots (one code path per warp): groups of
-    // 13 warps cover 32 slots, warp k of a group variant k
+    // nv warps (nv = enabled intra variants, vmask holds only intra bits) cover 32 slots,
+    // warp k of a group the k-th enabled variant in kIntraVariants order
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    const int x = x_lo + (t / (32 * 13)) * 32 + (t & 31);
-    const int var = kIntraVariants[(t >> 5) % 13];
+    const int nv = __popc(vmask);
+    const int x = x_lo + (t / (32 * nv)) * 32 + (t & 31);
+    uint32_t vm = vmask;
+    for (int k = (t >> 5) % nv; k > 0; --k) vm &= vm - 1;
+    const int var = __ffs(static_cast<int>(vm)) - 1;
     uint64_t best = kNoKey;
     if (x < x_hi && (vmask & (1u << var)) && S.canon[x] >= 0 && S.pos[x] >= 1) {
         const int p = S.pos[x], L = S.rlen[x], r = S.route[x];
@@ -1559,7 +1563,7 @@ cudaError_t launch_intra(uint32_t mask, bool tw, const SolView<DT> &S, const Sco
         ++g_launches;
         return cudaGetLastError();
     }
-    const int threads = (x_hi - x_lo + 31) / 32 * 32 * 13;
+    const int threads = (x_hi - x_lo + 31) / 32 * 32 * __builtin_popcount(intra);
     const int blocks = (threads + 255) / 256;
     if (tw) k_intra<DT, true><<<blocks, 256, 0, st>>>(S, sp, intra, x_lo, x_hi, keys);
     else    k_intra<DT, false><<<blocks, 256, 0, st>>>(S, sp, intra, x_lo, x_hi, keys);
@@ -1606,7 +1610,7 @@ cudaError_t launch_batch(uint32_t mask, bool tw, const SolView<DT> *views, const
                : launch_inter_batch_tw<DT, false>(mask, views, maps, work, n_work, sp, keys, grid, st);
     const uint32_t intra = mask & ((1u << 0) | (0x7u << 11) | (0x1FFu << 14));
     if (e == cudaSuccess && intra && n_sol > 0) {
-        dim3 g(((max_qp + 31) / 32 * 32 * 13 + 255) / 256, n_sol);
+        dim3 g(((max_qp + 31) / 32 * 32 * __builtin_popcount(intra) + 255) / 256, n_sol);
         if (tw && !(intra & 1u) && warp_tw)
             k_intra_tw_batch<DT><<<dim3((max_qp + 7) / 8, n_sol), 256, 0, st>>>(views, sp, intra, keys);
         else if (tw) k_intra_batch<DT, true><<<g, 256, 0, st>>>(views, sp, intra, keys);

@@ -892,14 +892,19 @@ extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
     // faster steps (cfg3 40.4 -> 39.2 us) but the inter kernel then shares the SMs, so its own
     // duration (the roofline's) grows 23 -> 32 us.
     static const bool fork_env = std::getenv("TGA_FORK_INTRA") && std::atoi(std::getenv("TGA_FORK_INTRA")) == 1;
-    static const int force_warp = std::getenv("TGA_WARP_TW") ? std::atoi(std::getenv("TGA_WARP_TW")) : 1;
+    // VRPTW intra kernel: the warp-parallel one (warp scans of Eq. 4 records) for long routes, the
+    // thread-per-(slot, variant) walk for short ones -- measured: cfg3 R1 (mean route 11 slots)
+    // 35.9 vs 38.8 us/step with the walk, R2 (50 slots) 54.0 vs 76.2 with the warp kernel; the
+    // same mean-length threshold as the population batch.  TGA_WARP_TW=0/1 forces one (A/B).
+    static const int force_warp = std::getenv("TGA_WARP_TW") ? std::atoi(std::getenv("TGA_WARP_TW")) : -1;
+    const bool warp_tw = force_warp >= 0 ? force_warp != 0 : s->N >= 16 * s->R;
     const bool fork_intra = fork_env && I->tw && (mask & TGA_OP_INTER) && (mask & TGA_OP_INTRA) && x_hi > x_lo;
     if (fork_intra) {
         TGA_CUDA(cudaEventRecord(s->ev_fork, st));
         TGA_CUDA(cudaStreamWaitEvent(s->side, s->ev_fork, 0));
         const cudaError_t ei = I->dtype == TGA_I32
-            ? launch_intra<int32_t>(mask, true, sol_view<int32_t>(s), sp, x_lo, x_hi, s->keys, s->side, false, force_warp != 0)
-            : launch_intra<float>(mask, true, sol_view<float>(s), sp, x_lo, x_hi, s->keys, s->side, false, force_warp != 0);
+            ? launch_intra<int32_t>(mask, true, sol_view<int32_t>(s), sp, x_lo, x_hi, s->keys, s->side, false, warp_tw)
+            : launch_intra<float>(mask, true, sol_view<float>(s), sp, x_lo, x_hi, s->keys, s->side, false, warp_tw);
         if (ei != cudaSuccess) return fail(TGA_ERR_CUDA, std::string("intra launch: ") + cudaGetErrorString(ei));
         TGA_CUDA(cudaEventRecord(s->ev_join, s->side));
     }
@@ -942,10 +947,6 @@ extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
     }
     if (fork_intra && e == cudaSuccess) TGA_CUDA(cudaStreamWaitEvent(st, s->ev_join, 0));  // join
     if (e == cudaSuccess && !fused_intra && !fork_intra) {
-        // VRPTW intra: the warp-parallel kernel (warp scans of Eq. 4 records) -- measured faster than the
-        // thread-per-(slot, variant) walk for short routes too since its loads are hoisted (cfg3 R1:
-        // 41.8 vs 43.9 us/step; R2: 57.1 vs 92.5).  TGA_WARP_TW=0 selects the walk (A/B override).
-        const bool warp_tw = force_warp != 0;
         if (I->dtype == TGA_I32)
             e = launch_intra<int32_t>(mask, I->tw, sol_view<int32_t>(s), sp, x_lo, x_hi, s->keys, st,
                                       I->max_c_abs < (1 << 21), warp_tw);

@@ -683,3 +683,19 @@ def test_etga_virtual_shards_equal_unsharded(n_shards):
         tot += c
     np.testing.assert_array_equal(comb, full)
     np.testing.assert_array_equal(tot[1:11], full_counts[1:11])
+
+
+@pytest.mark.parametrize("force", ["0", "1"])
+def test_vrptw_intra_kernels_forced(force):
+    """Both VRPTW intra kernels on every route length: by default the route-length threshold picks
+    the walk (short routes) or the warp-scan kernel (long routes); TGA_WARP_TW forces one, read
+    once per process, so the small and full-size VRPTW parity tests rerun in a subprocess."""
+    _need_gpu()
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, TGA_WARP_TW=force)
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.abspath(__file__), "-q", "-m", "gpu", "-p",
+                        "no:cacheprovider", "-k", "test_small_vrptw_exact or test_full_size_configs_exact"],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]

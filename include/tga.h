@@ -322,6 +322,19 @@ int32_t tga_batch_device_stats(tga_batch *batch, uint64_t *counts, uint64_t *app
  * (synchronises).  Not used on any timed path. */
 int32_t tga_solution_debug_probe(tga_solution *sol, int32_t enable, uint64_t *out);
 
+/* Test-only: tga_debug_eval_dump evaluates op_mask once with the DUMP
+ * instantiations of the SAME kernels and launch decisions as tga_eval (tile
+ * body / cell formulas, intra kernels; no shards, no edge mask) which also
+ * store the packed key of every candidate they evaluate.  out[TGA_N_VARIANTS
+ * * Q * Q] (Q = canonical slots) receives, at [variant][u * Q + v] (canonical
+ * u, v): 0 = the candidate was not evaluated, ~0 = evaluated and infeasible
+ * (feasible-only mode) or structurally invalid, else its key with the
+ * canonical flat index.  flags: 1 = force the warp-scan VRPTW intra kernel,
+ * 2 = force the per-thread walk.  The keys of the call are left as by
+ * tga_eval.  For parity tests of the per-candidate score and feasibility
+ * mask (Eq. 16a-b); never on a timed path. */
+int32_t tga_debug_eval_dump(tga_solution *sol, uint32_t op_mask, int32_t flags, uint64_t *out, int64_t out_len);
+
 /* ------------------------------------------------------------ misc */
 const char *tga_last_error(void);
 const char *tga_version(void);

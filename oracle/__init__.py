@@ -92,6 +92,10 @@ def lib():
                                        C.c_int32, C.c_int32, C.c_double, C.c_double,
                                        P(C.c_double), P(C.c_int32), P(C.c_int32), C.c_int64,
                                        P(_Move)]
+        _lib.orc_enumerate_full.argtypes = [P(_Inst), C.c_int32, P(C.c_int32), P(C.c_int32),
+                                            C.c_int32, C.c_int32, C.c_double, C.c_double,
+                                            P(C.c_double), P(C.c_int32), P(C.c_int32), P(C.c_int8),
+                                            P(C.c_int8), C.c_double, C.c_int64, P(_Move)]
         _lib.orc_score_candidate.argtypes = [P(_Inst), C.c_int32, P(C.c_int32), P(C.c_int32),
                                              C.c_int32, C.c_int32, C.c_double, C.c_double,
                                              C.c_int32, C.c_int32, C.c_int32, C.c_int32, P(_Move)]
@@ -198,6 +202,27 @@ class Oracle:
                             _ptr(sc, C.c_double), _ptr(us, C.c_int32), _ptr(vs, C.c_int32),
                             n, C.byref(m))
         return sc[:n], us[:n], vs[:n], self._move(m)
+
+    def enumerate_full(self, routes, variant: int, mode: int = 0, wQ: float = 10.0, wT: float = 10.0,
+                       band_tol: float = 1e-4):
+        """All candidates of a variant in canonical order with, per candidate, the
+        feasibility of the changed routes and the TW-F ambiguity-band flag:
+        (scores, u, v, feasible, band, best)."""
+        ptr, cust = self._csr(routes)
+        m = _Move()
+        lib().orc_best_move(C.byref(self._inst), len(ptr) - 1, _ptr(ptr, C.c_int32),
+                            _ptr(cust, C.c_int32), variant, mode, wQ, wT, 0, -1, C.byref(m))
+        n = int(m.n_candidates)
+        sc = np.zeros(max(n, 1))
+        us = np.zeros(max(n, 1), dtype=np.int32)
+        vs = np.zeros(max(n, 1), dtype=np.int32)
+        fe = np.zeros(max(n, 1), dtype=np.int8)
+        bd = np.zeros(max(n, 1), dtype=np.int8)
+        lib().orc_enumerate_full(C.byref(self._inst), len(ptr) - 1, _ptr(ptr, C.c_int32),
+                                 _ptr(cust, C.c_int32), variant, mode, wQ, wT,
+                                 _ptr(sc, C.c_double), _ptr(us, C.c_int32), _ptr(vs, C.c_int32),
+                                 _ptr(fe, C.c_int8), _ptr(bd, C.c_int8), band_tol, n, C.byref(m))
+        return sc[:n], us[:n], vs[:n], fe[:n].astype(bool), bd[:n].astype(bool), self._move(m)
 
     def score_candidate(self, routes, variant, ra, pa, rb, pb, mode=0, wQ=10.0, wT=10.0):
         ptr, cust = self._csr(routes)

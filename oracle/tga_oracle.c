@@ -84,6 +84,29 @@ static orc_route_val route_eval(const orc_instance *I, const int32_t *nodes, int
 }
 
 /* ------------------------------------------------------------------ *
+ * route_band: 1 if some stop of the route starts within the ambiguity band
+ * of its deadline, |max(a, e) - l| < tol * max(1, |l|) (SURVEY §8(c) item 13:
+ * the TW-F feasibility decision T_V == 0 is not decidable in fp32 there).
+ * The same simulation as route_eval; reporting only, no score arithmetic.
+ * ------------------------------------------------------------------ */
+static int route_band(const orc_instance *I, const int32_t *nodes, int len, double tol)
+{
+    if (!I->e) return 0;
+    const int n = I->n_nodes;
+    double t = I->e[nodes[0]];
+    for (int k = 1; k < len; ++k) {
+        int p = nodes[k - 1], q = nodes[k];
+        double a = t + I->s[p] + I->C[(int64_t)p * n + q];
+        double st = a > I->e[q] ? a : I->e[q];
+        double lq = I->l[q];
+        if (fabs(st - lq) < tol * (fabs(lq) > 1.0 ? fabs(lq) : 1.0)) return 1;
+        if (st > lq) st = lq;
+        t = st;
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------ *
  * Solution in "routes with depots" form.
  * ------------------------------------------------------------------ */
 typedef struct {
@@ -301,7 +324,7 @@ static int enumerate(const orc_instance *I, int32_t R, const int32_t *ptr, const
                      int32_t var, int32_t mode, double wQ, double wT,
                      int32_t u_lo, int32_t u_hi, orc_move *out,
                      double *rec_score, int32_t *rec_u, int32_t *rec_v, int64_t rec_cap,
-                     const uint8_t *mask)
+                     const uint8_t *mask, int8_t *rec_feas, int8_t *rec_band, double band_tol)
 {
     orc_sol S;
     memset(out, 0, sizeof(*out));
@@ -345,6 +368,10 @@ static int enumerate(const orc_instance *I, int32_t R, const int32_t *ptr, const
                         rec_score[cnt - 1] = sc;
                         rec_u[cnt - 1] = u;
                         rec_v[cnt - 1] = S.off[rb] + pb;
+                        if (rec_feas) rec_feas[cnt - 1] = (int8_t)d.feasible;
+                        if (rec_band)
+                            rec_band[cnt - 1] = (int8_t)(route_band(I, A, la, band_tol) ||
+                                                         (nr == 2 && route_band(I, B, lb, band_tol)));
                     }
                     if (sc < out->score) {
                         out->score = sc; out->dD = d.dD; out->dLV = d.dLV; out->dTV = d.dTV;
@@ -367,7 +394,7 @@ int orc_best_move(const orc_instance *I, int32_t R, const int32_t *ptr, const in
                   int32_t var, int32_t mode, double wQ, double wT,
                   int32_t u_lo, int32_t u_hi, orc_move *out)
 {
-    return enumerate(I, R, ptr, cust, var, mode, wQ, wT, u_lo, u_hi, out, NULL, NULL, NULL, 0, NULL);
+    return enumerate(I, R, ptr, cust, var, mode, wQ, wT, u_lo, u_hi, out, NULL, NULL, NULL, 0, NULL, NULL, NULL, 0.0);
 }
 
 /* the same over the edge-based (granular) neighbourhood: mask[n_nodes^2], 1 = pair kept */
@@ -375,7 +402,7 @@ int orc_best_move_masked(const orc_instance *I, int32_t R, const int32_t *ptr, c
                          int32_t var, int32_t mode, double wQ, double wT,
                          int32_t u_lo, int32_t u_hi, const uint8_t *mask, orc_move *out)
 {
-    return enumerate(I, R, ptr, cust, var, mode, wQ, wT, u_lo, u_hi, out, NULL, NULL, NULL, 0, mask);
+    return enumerate(I, R, ptr, cust, var, mode, wQ, wT, u_lo, u_hi, out, NULL, NULL, NULL, 0, mask, NULL, NULL, 0.0);
 }
 
 /* every candidate's score and (u, v) in canonical order (for pins) */
@@ -383,7 +410,19 @@ int orc_enumerate(const orc_instance *I, int32_t R, const int32_t *ptr, const in
                   int32_t var, int32_t mode, double wQ, double wT,
                   double *scores, int32_t *us, int32_t *vs, int64_t cap, orc_move *out)
 {
-    return enumerate(I, R, ptr, cust, var, mode, wQ, wT, 0, -1, out, scores, us, vs, cap, NULL);
+    return enumerate(I, R, ptr, cust, var, mode, wQ, wT, 0, -1, out, scores, us, vs, cap, NULL, NULL, NULL, 0.0);
+}
+
+/* the same, plus per candidate: both changed routes feasible (L <= Q and T_V == 0)
+ * and whether some stop of a changed route lies in the ambiguity band of
+ * route_band(band_tol) (TW-F parity) */
+int orc_enumerate_full(const orc_instance *I, int32_t R, const int32_t *ptr, const int32_t *cust,
+                       int32_t var, int32_t mode, double wQ, double wT,
+                       double *scores, int32_t *us, int32_t *vs, int8_t *feas, int8_t *band,
+                       double band_tol, int64_t cap, orc_move *out)
+{
+    return enumerate(I, R, ptr, cust, var, mode, wQ, wT, 0, -1, out, scores, us, vs, cap, NULL, feas, band,
+                     band_tol);
 }
 
 /* Score of one explicitly named candidate (sampled parity at full size). */

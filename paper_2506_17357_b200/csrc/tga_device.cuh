@@ -101,6 +101,15 @@ __device__ __forceinline__ uint64_t score_key(const ScoreParams &sp, bool valid,
     return valid ? pack_key(ord_score(s), idx) : kNoKey;
 }
 
+// ------------------------------------------------------------------ test-only candidate dump
+// DUMP instantiations of the evaluation kernels (tga_debug_eval_dump) also store the
+// packed key of EVERY candidate they evaluate -- kNoKey when it is infeasible or
+// structurally invalid -- at dump[variant * stride + physical flat index]; the host
+// pre-fills 0 (= not evaluated).  Production instantiations never touch it.
+__device__ __forceinline__ void dump_put(unsigned long long *dump, uint32_t stride, int var, uint32_t idx, uint64_t k) {
+    dump[static_cast<size_t>(var) * stride + idx] = k;
+}
+
 // ------------------------------------------------------------------ per-slot record (CVRP fast path)
 // Everything the fused inter-route kernel needs about one slot x in one
 // 80-byte record, so a tile row is one bulk copy and a lane's column is five
@@ -184,8 +193,10 @@ __device__ __forceinline__ void warp_keep(unsigned long long *wred, int var, uin
 // One warp evaluates every intra-route CVRP variant of u slot x (lane <-> v);
 // the per-variant warp minima are MIN-combined into red[23], the calling warp's
 // private row of shared memory.
+template <bool DUMP = false>
 __device__ __forceinline__ void intra_cvrp_warp(const SolView<int32_t> &S, const ScoreParams &sp, uint32_t vmask,
-                                                int x, unsigned long long *red, unsigned long long *pslot = nullptr) {
+                                                int x, unsigned long long *red, unsigned long long *pslot = nullptr,
+                                                unsigned long long *dump = nullptr) {
     const int lane = threadIdx.x & 31;
     auto stamp = [&](int k) {
         if (pslot && lane == 0) {
@@ -255,6 +266,16 @@ __device__ __forceinline__ void intra_cvrp_warp(const SolView<int32_t> &S, const
                 const int32_t adj = D(-1, 0) + D(0, b - 1) + D(a - 1, b) - em - evm - ev2[b - 1];
                 const int32_t gap = D(-1, 0) + D(a, b - 1) + dxm + D(a - 1, b) - em - eo[a - 1] - evm - ev2[b - 1];
                 k[var] = intra_k32(ok, q == p + a ? adj : gap, lane);
+            }
+        }
+        if constexpr (DUMP) {
+            const uint32_t stride = static_cast<uint32_t>(S.pitch) * static_cast<uint32_t>(S.pitch);
+#pragma unroll
+            for (int i = 0; i < 23; ++i) {
+                if (!((i == 0 || i >= 11) && (vmask & (1u << i))) || !in) continue;
+                const uint64_t kk = k[i] == 0xFFFFFFFFu ? kNoKey
+                                    : pack_key(ord_score(static_cast<int32_t>(k[i] >> 5) - (1 << 25)), ib + lane);
+                dump_put(dump, stride, i, ib + lane, kk);
             }
         }
         // phase 2: one REDUX.MIN per variant, all issued before lane 0 merges them

@@ -175,12 +175,21 @@ struct FastItem {
 // flushed into a solution's keys only when the run moves on to the next solution.
 // stream slots: 0 2opt* | 1,2 reloc1 d/r | 3,4 oropt2 | 5,6 oropt3 | 7 swap11 |
 // 8,9 cross12 | 10,11 cross13 | 12 cross22 | 13,14 cross23 | 15 cross33
-template <int U, bool TW, uint32_t MASK, class ItemF>
+// stream slot k -> (variant, direct): direct = the key index is u * Qc + v (the
+// N1-segment / moved segment / cut is at the row slot u), else v * Qc + u
+__device__ __forceinline__ int stream_variant(int k) {
+    return k == 0 ? 1 : (k <= 6 ? 1 + (k + 1) / 2 : (k == 7 ? 5 : (k <= 9 ? 6 : (k <= 11 ? 7 : (k == 12 ? 8 : (k <= 14 ? 9 : 10))))));
+}
+__device__ __forceinline__ bool stream_direct(int k) {
+    return (k == 0 || k == 7 || k == 12 || k == 15) ? true : (k <= 6 ? (k & 1) == 1 : (k == 8 || k == 10 || k == 13));
+}
+
+template <int U, bool TW, uint32_t MASK, bool DUMP, class ItemF>
 __device__ __forceinline__ void fast_body(ItemF item, int w0, int w1, int wstride, uint64_t *bar,
                                           unsigned long long (*red)[23], unsigned char *sm, int32_t cap,
                                           const SolView<int32_t> &SV, const ScoreParams &sp, uint32_t imask,
                                           int x_lo, int x_hi, int icta, int incta, int flags,
-                                          uint64_t *keys0 = nullptr) {
+                                          uint64_t *keys0 = nullptr, unsigned long long *dump = nullptr) {
     using G = FastGeom<U, TW>;
     constexpr int BW = G::BoxW;
     constexpr int NV = 11;
@@ -259,8 +268,9 @@ __device__ __forceinline__ void fast_body(ItemF item, int w0, int w1, int wstrid
         for (int j = icta; j < n_units; j += incta) {
             const int x = x_lo + 4 * j + warp;
             if (x < x_hi)
-                intra_cvrp_warp(SV, sp, imask, x, red[warp],
-                                ((flags & 2) && warp == 0 && j == icta && blockIdx.x < 4096) ? g_inter_probe + 8 * blockIdx.x + 4 : nullptr);
+                intra_cvrp_warp<DUMP>(SV, sp, imask, x, red[warp],
+                                      ((flags & 2) && warp == 0 && j == icta && blockIdx.x < 4096) ? g_inter_probe + 8 * blockIdx.x + 4 : nullptr,
+                                      dump);
         }
     }
     if (prb) g_inter_probe[8 * blockIdx.x + 1] = gtime();
@@ -317,7 +327,15 @@ __device__ __forceinline__ void fast_body(ItemF item, int w0, int w1, int wstrid
             if (!(ru < V.r)) continue;       // pair must span two routes, route(u) < route(v)
             const SlotTW &AT = TR[TW ? i : 0];
             cell_streams<TW, MASK>(A, V, AT, VT, cap, [&](int di, int dj) { return D(i, di, dj); },
-                                   [&](int k, bool ok, int32_t dD) { keep(run[k], ok, dD, i, mul32); });
+                                   [&](int k, bool ok, int32_t dD) {
+                                       keep(run[k], ok, dD, i, mul32);
+                                       if constexpr (DUMP) {   // test-only: every candidate's key
+                                           const uint32_t uu = static_cast<uint32_t>(u), vv = static_cast<uint32_t>(v);
+                                           const uint32_t idx = stream_direct(k) ? uu * Qc + vv : vv * Qc + uu;
+                                           dump_put(dump, Qc * Qc, stream_variant(k), idx,
+                                                    ok ? pack_key(ord_score(dD), idx) : kNoKey);
+                                       }
+                                   });
         }
 #if !TGA_FAST_CTA_SYNC
         // this warp is done with stage b (every shared read above has returned its value)
@@ -368,7 +386,7 @@ __device__ __forceinline__ void fast_body(ItemF item, int w0, int w1, int wstrid
 // in two halves of similar work so that small neighbourhoods get twice the CTAs
 // (and each CTA half the registers' worth of running minima); the intra-route
 // work rides with the second half.
-template <int U, bool TW, uint32_t MASK, uint32_t MASK2>
+template <int U, bool TW, uint32_t MASK, uint32_t MASK2, bool DUMP = false>
 __global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__restrict__ rec,
                                                              const SlotTW *__restrict__ rectw,
                                                              const __grid_constant__ CUtensorMap tmap,
@@ -376,7 +394,7 @@ __global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__re
                                                              uint32_t Qc, int32_t cap, uint64_t *__restrict__ keys,
                                                              const __grid_constant__ SolView<int32_t> SV,
                                                              ScoreParams sp, uint32_t imask, int x_lo, int x_hi,
-                                                             int flags, int split) {
+                                                             int flags, int split, unsigned long long *dump) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *sm = smem_raw + ((128u - (s_u32(smem_raw) & 127u)) & 127u);
     __shared__ uint64_t bar[2];
@@ -399,12 +417,12 @@ __global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__re
     };
     if (MASK2 == 0 || cta < split) {
         const int n = MASK2 ? split : static_cast<int>(gridDim.x);
-        fast_body<U, TW, MASK>(item, t_lo + cta, t_hi, n, bar, red, sm, cap, SV, sp, MASK2 ? 0u : imask, x_lo, x_hi,
-                               cta, n, flags, keys);
+        fast_body<U, TW, MASK, DUMP>(item, t_lo + cta, t_hi, n, bar, red, sm, cap, SV, sp, MASK2 ? 0u : imask, x_lo,
+                                     x_hi, cta, n, flags, keys, dump);
     } else {
         const int n = static_cast<int>(gridDim.x) - split;
-        fast_body<U, TW, MASK2>(item, t_lo + cta - split, t_hi, n, bar, red, sm, cap, SV, sp, imask, x_lo, x_hi,
-                                cta - split, n, flags, keys);
+        fast_body<U, TW, MASK2, DUMP>(item, t_lo + cta - split, t_hi, n, bar, red, sm, cap, SV, sp, imask, x_lo, x_hi,
+                                      cta - split, n, flags, keys, dump);
     }
     if ((flags & 2) && tid == 0 && blockIdx.x < 4096) g_inter_probe[8 * blockIdx.x + 3] = gtime();
 }
@@ -417,21 +435,21 @@ static bool inter_probe_on() {
 // resident CTAs (whole GPU) of one instantiation with one / two pipeline stages
 template <int U, bool TW, uint32_t MASK, uint32_t MASK2>
 static void fast_capacity(int &res1, int &res2) {
-    static int r1 = 0, r2 = 0;
-    if (!r1) {
+    static PerDevice pd;
+    static int r1[kMaxDevices], r2[kMaxDevices];
+    const int d = once_per_device(pd, [](int dev) {
         auto kern = k_inter_fast<U, TW, MASK, MASK2>;
         using G = FastGeom<U, TW>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::Smem);
-        int dev = 0, sms = 0, b1 = 0, b2 = 0;
-        cudaGetDevice(&dev);
+        int sms = 0, b1 = 0, b2 = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, kern, kFastThreads, G::Smem1);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, kern, kFastThreads, G::Smem);
-        r1 = std::max(1, b1) * std::max(1, sms);
-        r2 = std::max(1, b2) * std::max(1, sms);
-    }
-    res1 = r1;
-    res2 = r2;
+        r1[dev] = std::max(1, b1) * std::max(1, sms);
+        r2[dev] = std::max(1, b2) * std::max(1, sms);
+    });
+    res1 = r1[d];
+    res2 = r2[d];
 }
 
 template <int U, bool TW, uint32_t MASK, uint32_t MASK2>
@@ -459,7 +477,8 @@ static cudaError_t launch_fast_t(const SlotRec *rec, const SlotTW *rectw, const 
     // bits 0-1: PDL trigger placement, probe; bits 8+: the constant 32 for keep() (opaque to ptxas)
     const int flags = (pdl_enabled(4) ? 1 : 0) | (inter_probe_on() ? 2 : 0) | (32 << 8);
     const cudaError_t e = launch_pdl(1, kern, dim3(grid), dim3(kFastThreads), smem, st, 0, rec, rectw, map, tiles, t_lo,
-                                     t_hi, Qc, cap, keys, SV, sp, imask, x_lo, x_hi, flags, split);
+                                     t_hi, Qc, cap, keys, SV, sp, imask, x_lo, x_hi, flags, split,
+                                     static_cast<unsigned long long *>(nullptr));
     note_launch();
     return e != cudaSuccess ? e : cudaGetLastError();
 }
@@ -535,7 +554,7 @@ __global__ void __launch_bounds__(kFastThreads) k_inter_fast_batch(const FastSol
                         static_cast<int>(c & 0x3FFu)};
     };
     const SolView<int32_t> none{};
-    fast_body<U, TW, MASK>(item, w0, w1, 1, bar, red, sm, cap, none, sp, 0u, 0, 0, 0, 1, flags);
+    fast_body<U, TW, MASK, false>(item, w0, w1, 1, bar, red, sm, cap, none, sp, 0u, 0, 0, 0, 1, flags);
 }
 
 template <int U, bool TW, uint32_t MASK>
@@ -543,15 +562,17 @@ static cudaError_t launch_fast_batch_t(const FastSol *sols, const CUtensorMap *m
                                        int32_t cap, const ScoreParams &sp, int max_grid, cudaStream_t st) {
     auto kern = k_inter_fast_batch<U, TW, MASK>;
     using G = FastGeom<U, TW>;
-    static int res = 0;
-    if (!res) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::Smem);
-        int dev = 0, sms = 0, b = 0;
-        cudaGetDevice(&dev);
+    static PerDevice pd;
+    static int res_cap[kMaxDevices];
+    const int d = once_per_device(pd, [](int dev) {
+        auto k = k_inter_fast_batch<U, TW, MASK>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, FastGeom<U, TW>::Smem);
+        int sms = 0, b = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, kFastThreads, G::Smem);
-        res = std::max(1, b) * std::max(1, sms);
-    }
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k, kFastThreads, FastGeom<U, TW>::Smem);
+        res_cap[dev] = std::max(1, b) * std::max(1, sms);
+    });
+    const int res = res_cap[d];
     const int grid = std::max(1, std::min(n_work, std::min(res, max_grid)));
     kern<<<grid, kFastThreads, G::Smem, st>>>(sols, maps, work, n_work, cap, sp, 32 << 8);
     note_launch();
@@ -643,9 +664,8 @@ __global__ void __launch_bounds__(256) k_etga(const SlotRec *__restrict__ rec, c
         const uint32_t idx_r = static_cast<uint32_t>(v) * Qc + static_cast<uint32_t>(u);
         // slot -> (variant, direction) of the stream layout
         cell_streams<TW, CM>(A, V, AT, VT, cap, D, [&](int k, bool ok, int32_t dD) {
-            const int var = k == 0 ? 1 : (k <= 6 ? 1 + (k + 1) / 2 : (k == 7 ? 5 : (k <= 9 ? 6 : (k <= 11 ? 7 : (k == 12 ? 8 : (k <= 14 ? 9 : 10))))));
-            const bool direct = (k == 0 || k == 7 || k == 12 || k == 15) ? true
-                                : (k <= 6 ? (k & 1) == 1 : ((k == 8 || k == 10 || k == 13)));
+            const int var = stream_variant(k);
+            const bool direct = stream_direct(k);
             if (ok) acc[var] = umin64(acc[var], pack_key(ord_score(dD), direct ? idx_d : idx_r));
         });
         // structurally valid candidates of the cell (the oracle's masked count)
@@ -734,6 +754,36 @@ cudaError_t launch_etga(uint32_t mask, bool tw, const EtgaArgs &a, cudaStream_t 
         if (e != cudaSuccess) return e;
     }
     return tw ? launch_etga_t<true>(mask, a, st) : launch_etga_t<false>(mask, a, st);
+}
+
+// test-only: the DUMP instantiation of the all-variant fused sweep (U = 16), every
+// candidate's key stored in dump (tga_debug_eval_dump); same tile plan and body
+template <bool TW>
+static cudaError_t launch_fast_dump_t(const SlotRec *rec, const SlotTW *rectw, const CUtensorMap &map,
+                                      const uint32_t *tiles, int t_lo, int t_hi, uint32_t Qc, int32_t cap,
+                                      uint64_t *keys, cudaStream_t st, const SolView<int32_t> &SV,
+                                      const ScoreParams &sp, uint32_t imask, int x_lo, int x_hi,
+                                      unsigned long long *dump) {
+    constexpr uint32_t ALL = 0x7FEu;
+    auto kern = k_inter_fast<16, TW, ALL, 0u, true>;
+    using G = FastGeom<16, TW>;
+    static PerDevice pd;
+    once_per_device(pd, [&](int) { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::Smem); });
+    const int units = imask ? (x_hi - x_lo + 3) / 4 : 0;
+    const int grid = std::max(1, std::max(t_hi - t_lo, units));
+    kern<<<grid, kFastThreads, G::Smem1, st>>>(rec, rectw, map, tiles, t_lo, t_hi, Qc, cap, keys, SV, sp, imask, x_lo,
+                                               x_hi, 32 << 8, grid, dump);
+    note_launch();
+    return cudaGetLastError();
+}
+cudaError_t launch_inter_fast_dump(bool tw, const SlotRec *rec, const SlotTW *rectw, const CUtensorMap &map,
+                                   const uint32_t *tiles, int t_lo, int t_hi, uint32_t Qc, int32_t cap, uint64_t *keys,
+                                   cudaStream_t st, const SolView<int32_t> &SV, const ScoreParams &sp, uint32_t imask,
+                                   int x_lo, int x_hi, unsigned long long *dump) {
+    return tw ? launch_fast_dump_t<true>(rec, rectw, map, tiles, t_lo, t_hi, Qc, cap, keys, st, SV, sp, imask, x_lo,
+                                         x_hi, dump)
+              : launch_fast_dump_t<false>(rec, rectw, map, tiles, t_lo, t_hi, Qc, cap, keys, st, SV, sp, imask, x_lo,
+                                          x_hi, dump);
 }
 
 cudaError_t launch_inter_fast(int U, uint32_t mask, const SlotRec *rec, const SlotTW *rectw, const CUtensorMap &map,

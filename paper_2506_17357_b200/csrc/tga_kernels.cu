@@ -445,13 +445,24 @@ __global__ void __launch_bounds__(256) k_update_cols(DT *__restrict__ Dp, int pi
 // barrier over the gridDim.x blocks of the solution (all co-resident: the grid
 // is at most one block per SM), then every block refreshes Dp rows / columns
 // and re-scans routes of the changed span read from the descriptor.
+// Generation (sense-reversing) grid barrier over the nblocks blocks of one
+// solution: counter[0] counts arrivals and is reset by the last arriver before it
+// advances the generation word counter[2]; waiters spin on the generation.  No
+// counter grows across launches, so any number of steps and any mix of grid
+// sizes (single solution / population batch) share the descriptor safely.
 __device__ __forceinline__ void solution_barrier(int32_t *counter, int nblocks) {
     __syncthreads();
     if (threadIdx.x == 0) {
+        volatile int32_t *gen = counter + 2;
+        const int32_t g = *gen;            // cannot advance before this block arrives
         __threadfence();
-        const int v = atomicAdd(counter, 1);
-        const int target = (v / nblocks + 1) * nblocks;  // launches of one stream never overlap
-        while (*reinterpret_cast<volatile int32_t *>(counter) < target) __nanosleep(64);
+        if (atomicAdd(counter, 1) == nblocks - 1) {
+            *reinterpret_cast<volatile int32_t *>(counter) = 0;
+            __threadfence();
+            atomicAdd(counter + 2, 1);
+        } else {
+            while (*gen == g) __nanosleep(64);
+        }
         __threadfence();
     }
     __syncthreads();
@@ -475,14 +486,13 @@ __device__ __forceinline__ unsigned long long gtimer() {
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
-__device__ __forceinline__ void block_arrive(int32_t *counter) {
-    if (threadIdx.x == 0) atomicAdd(counter, 1);
-}
-__device__ __forceinline__ void wait_arrivals(int32_t *counter, int v_own, int nblocks) {
-    // v_own: this block's own atomicAdd return; launches of one stream never overlap
-    const int target = (v_own / nblocks + 1) * nblocks;
+// Arrivals of one launch: every block adds 1 to counter once; block 0 alone waits
+// for all nblocks and then resets the counter for the next launch (launches of one
+// stream never overlap, and every block has arrived once the count is reached).
+__device__ __forceinline__ void wait_arrivals(int32_t *counter, int nblocks) {
     // the arrivals follow the snapshot loads in each block (program order); no fence needed
-    while (*reinterpret_cast<volatile int32_t *>(counter) < target) __nanosleep(32);
+    while (*reinterpret_cast<volatile int32_t *>(counter) < nblocks) __nanosleep(32);
+    *reinterpret_cast<volatile int32_t *>(counter) = 0;
 }
 
 template <class DT, bool TW>
@@ -495,7 +505,6 @@ __device__ __forceinline__ void pick_update_multi(const DevState &S, const ScanA
     int32_t *nn = snap + snap_cap;      // new node ids of the changed ranges
     __shared__ uint64_t skeys[23];
     __shared__ Decoded dm;
-    __shared__ int arrive_v;
     // ---- 1. stage the old route bases / lengths and the keys; decode (every block)
     for (int r = tid; r <= R; r += blockDim.x) {
         sb[r] = S.rbase[r];
@@ -528,7 +537,7 @@ __device__ __forceinline__ void pick_update_multi(const DevState &S, const ScanA
         nn[j] = nd;
     }
     __syncthreads();
-    if (tid == 0) arrive_v = atomicAdd(S.desc + 9, 1);
+    if (tid == 0) atomicAdd(S.desc + 9, 1);
     pdl_trigger();  // this block is resident and arrived: a dependent grid cannot starve the wait below
     // the closed-form counts of the evaluated (old) lengths, on a block that does not
     // rebuild a route (those are the last blocks when the update roles are split)
@@ -536,7 +545,7 @@ __device__ __forceinline__ void pick_update_multi(const DevState &S, const ScanA
     if (!dm.applied) {
         if (b == 0 && tid == 0) {
             S.desc[0] = 0;
-            wait_arrivals(S.desc + 9, arrive_v, G);  // every block has read the keys
+            wait_arrivals(S.desc + 9, G);  // every block has read the keys
             for (int v = 0; v < 23; ++v) S.keys[v] = ~0ull;  // consumed: the next eval needs no memset
         }
         return;
@@ -544,7 +553,7 @@ __device__ __forceinline__ void pick_update_multi(const DevState &S, const ScanA
     if (dm.full) {  // relayout: block 0 alone rewrites every slot after all blocks staged
         __syncthreads();
         if (b == 0) {
-            if (tid == 0) wait_arrivals(S.desc + 9, arrive_v, G);
+            if (tid == 0) wait_arrivals(S.desc + 9, G);
             __syncthreads();
             pick_apply_body(S, mask, cmask, integer, smr, pr, false);  // resets the keys too
         }
@@ -640,7 +649,7 @@ __device__ __forceinline__ void pick_update_multi(const DevState &S, const ScanA
     if (tid == 0) probe(pr, 5);
     // ---- 5. block 0: the slot arrays of the changed routes, once every block has its snapshot
     if (b == 0) {
-        if (tid == 0) wait_arrivals(S.desc + 9, arrive_v, G);
+        if (tid == 0) wait_arrivals(S.desc + 9, G);
         __syncthreads();
         for (int j = tid; j < n1 + n2; j += blockDim.x) {
             const int q = j < n1 ? 0 : 1;
@@ -711,6 +720,7 @@ __global__ void __launch_bounds__(256) k_pick_update(const DevState *__restrict_
     probe(pr, 7);
 }
 
+constexpr int kPickSmemMax = 200 * 1024;
 cudaError_t launch_pick_update(const DevState *states, const void *scans, int n_sol, bool tw, bool is_int,
                                uint32_t mask, uint32_t cmask, int max_routes, int max_cap, int blocks_per_sol,
                                cudaStream_t st) {
@@ -718,15 +728,20 @@ cudaError_t launch_pick_update(const DevState *states, const void *scans, int n_
     // multi-block path: sb, sl + old and new node ids of the two changed routes
     const int smem_old = 3 * (max_routes + 1) * 4 + 2 * max_cap * 4;
     const int smem_multi = 2 * (max_routes + 1) * 4 + 4 * max_cap * 4;
-    const bool multi = blocks_per_sol > 1 && smem_multi <= 200 * 1024;
+    const bool multi = blocks_per_sol > 1 && smem_multi <= kPickSmemMax;
     const int smem = multi ? std::max(smem_old, smem_multi) : smem_old;
     const int snap_cap = multi ? 2 * max_cap : 0;
     dim3 g(blocks_per_sol, n_sol);
-    {  // dynamic + static shared memory above the 48 KB default needs the opt-in (static: ~20 KB)
-        cudaFuncSetAttribute(k_pick_update<int32_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(k_pick_update<int32_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(k_pick_update<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(k_pick_update<float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (smem > kPickSmemMax) return cudaErrorInvalidValue;
+    {  // dynamic + static shared memory above the 48 KB default needs the opt-in (static: ~20 KB);
+       // set once per device to the largest size any launch uses
+        static PerDevice pd;
+        once_per_device(pd, [](int) {
+            cudaFuncSetAttribute(k_pick_update<int32_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPickSmemMax);
+            cudaFuncSetAttribute(k_pick_update<int32_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPickSmemMax);
+            cudaFuncSetAttribute(k_pick_update<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPickSmemMax);
+            cudaFuncSetAttribute(k_pick_update<float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPickSmemMax);
+        });
     }
     cudaError_t e;
     const auto *si = static_cast<const ScanArgs<int32_t> *>(scans);
@@ -785,14 +800,20 @@ __device__ __forceinline__ void tma_load_2d(void *smem_dst, const CUtensorMap *m
 // Thread mapping: lane -> v = v0 + lane + 32*j (j < VPT); warp -> UPW rows.
 // One tile of the inter-route candidate space (rows u0.., columns v0..), Dp box
 // already in shared memory; running (score, index) keys per variant in `best`.
-template <class DT, bool TW, uint32_t MASK>
+template <class DT, bool TW, uint32_t MASK, bool DUMP = false>
 __device__ __forceinline__ void inter_tile(const SolView<DT> &S, const DT *__restrict__ tile, const int u0,
-                                           const int v0, const ScoreParams &sp, uint64_t (&best)[11]) {
+                                           const int v0, const ScoreParams &sp, uint64_t (&best)[11],
+                                           unsigned long long *dump = nullptr) {
     constexpr int TU = kTileU, TV = kTileV, VPT = TV / 32, UPW = TU / (kInterThreads / 32);
     constexpr int BW = kBoxW;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // Dp(x, y) from the staged box
     auto Dt = [&](int x, int y) -> DT { return tile[(x - u0 + 1) * BW + (y - v0 + kBoxX0)]; };
+    // fold one candidate key into the variant's running best (+ the test-only dump)
+    auto take = [&](int var, uint64_t k, uint32_t idx) {
+        best[var] = umin64(best[var], k);
+        if constexpr (DUMP) dump_put(dump, S.Qc * S.Qc, var, idx, k);
+    };
 #pragma unroll 1
     for (int j = 0; j < VPT; ++j) {
         const int v = v0 + lane + 32 * j;
@@ -828,7 +849,7 @@ __device__ __forceinline__ void inter_tile(const SolView<DT> &S, const DT *__res
                     ta = tw_cat(S.fwdT[u], S.bwdT[v + 1], static_cast<float>(Dt(u, v + 1))).w;
                     tb = tw_cat(S.fwdT[v], S.bwdT[u + 1], static_cast<float>(Dt(u + 1, v))).w;
                 }
-                best[1] = umin64(best[1], score_key<DT, TW>(sp, pair, dD, la, lb, Wa, Wb, ta, tb, TVa, TVb, idx_uv));
+                take(1, score_key<DT, TW>(sp, pair, dD, la, lb, Wa, Wb, ta, tb, TVa, TVb, idx_uv), idx_uv);
             }
             // ---- relocate (N=1) / or-opt (N=2,3): both directions (Eq. 13)
 #pragma unroll
@@ -848,8 +869,7 @@ __device__ __forceinline__ void inter_tile(const SolView<DT> &S, const DT *__res
                         const TwRec X = tw_cat(S.fwdT[v], sg, static_cast<float>(Dt(u, v)));
                         tb = tw_cat(X, S.bwdT[v + 1], static_cast<float>(Dt(u + N - 1, v + 1))).w;
                     }
-                    best[1 + N] = umin64(best[1 + N], score_key<DT, TW>(sp, ok, dD, Wa - s, Wb + s, Wa, Wb,
-                                                                        ta, tb, TVa, TVb, idx_uv));
+                    take(1 + N, score_key<DT, TW>(sp, ok, dD, Wa - s, Wb + s, Wa, Wb, ta, tb, TVa, TVb, idx_uv), idx_uv);
                 }
                 {   // segment v..v+N-1 (route b) inserted after u (route a)
                     const bool ok = pair && pv >= 1 && pv + N - 1 <= Lb;
@@ -863,8 +883,7 @@ __device__ __forceinline__ void inter_tile(const SolView<DT> &S, const DT *__res
                         const TwRec X = tw_cat(S.fwdT[u], sg, static_cast<float>(Dt(u, v)));
                         ta = tw_cat(X, S.bwdT[u + 1], static_cast<float>(Dt(u + 1, v + N - 1))).w;
                     }
-                    best[1 + N] = umin64(best[1 + N], score_key<DT, TW>(sp, ok, dD, Wa + s, Wb - s, Wa, Wb,
-                                                                        ta, tb, TVa, TVb, idx_vu));
+                    take(1 + N, score_key<DT, TW>(sp, ok, dD, Wa + s, Wb - s, Wa, Wb, ta, tb, TVa, TVb, idx_vu), idx_vu);
                 }
             }
             // ---- swap (1,1) / cross-exchange (N1,N2) (3-Seq(N1,N2) P:346)
@@ -890,8 +909,8 @@ __device__ __forceinline__ void inter_tile(const SolView<DT> &S, const DT *__res
                         const TwRec B1 = tw_cat(S.fwdT[v - 1], seg(u, N1), static_cast<float>(Dt(u, v - 1)));
                         tb = tw_cat(B1, S.bwdT[v + N2], static_cast<float>(Dt(u + N1 - 1, v + N2))).w;
                     }
-                    best[vid] = umin64(best[vid], score_key<DT, TW>(sp, ok, dD, Wa - sa + sb, Wb - sb + sa, Wa,
-                                                                    Wb, ta, tb, TVa, TVb, idx_uv));
+                    take(vid, score_key<DT, TW>(sp, ok, dD, Wa - sa + sb, Wb - sb + sa, Wa, Wb, ta, tb, TVa, TVb, idx_uv),
+                         idx_uv);
                 }
                 if (N1 != N2) {   // N1-segment at v (route b), N2-segment at u (route a)
                     const bool ok = pair && pv >= 1 && pv + N1 - 1 <= Lb && pu >= 1 && pu + N2 - 1 <= La;
@@ -906,18 +925,19 @@ __device__ __forceinline__ void inter_tile(const SolView<DT> &S, const DT *__res
                         const TwRec A1 = tw_cat(S.fwdT[u - 1], seg(v, N1), static_cast<float>(Dt(u - 1, v)));
                         ta = tw_cat(A1, S.bwdT[u + N2], static_cast<float>(Dt(u + N2, v + N1 - 1))).w;
                     }
-                    best[vid] = umin64(best[vid], score_key<DT, TW>(sp, ok, dD, Wa - sa + sb, Wb - sb + sa, Wa,
-                                                                    Wb, ta, tb, TVa, TVb, idx_vu));
+                    take(vid, score_key<DT, TW>(sp, ok, dD, Wa - sa + sb, Wb - sb + sa, Wa, Wb, ta, tb, TVa, TVb, idx_vu),
+                         idx_vu);
                 }
             }
         }
     }
 }
 
-template <class DT, bool TW, uint32_t MASK>
+template <class DT, bool TW, uint32_t MASK, bool DUMP = false>
 __global__ void __launch_bounds__(kInterThreads) k_inter(const __grid_constant__ SolView<DT> S, const __grid_constant__ CUtensorMap tmap,
                                                          const uint32_t *__restrict__ tiles, int t_lo, int t_hi,
-                                                         ScoreParams sp, uint64_t *__restrict__ keys) {
+                                                         ScoreParams sp, uint64_t *__restrict__ keys,
+                                                         unsigned long long *dump) {
     constexpr int TU = kTileU, TV = kTileV, VPT = TV / 32, UPW = TU / (kInterThreads / 32);
     constexpr int BW = kBoxW, BH = kBoxH;
     constexpr int NV = 11;  // inter variant ids 1..10
@@ -962,7 +982,7 @@ __global__ void __launch_bounds__(kInterThreads) k_inter(const __grid_constant__
         const uint32_t ij = tiles[t];
         const int u0 = (ij >> 16) * TU, v0 = (ij & 0xFFFF) * TV;
 
-        inter_tile<DT, TW, MASK>(S, tile, u0, v0, sp, best);
+        inter_tile<DT, TW, MASK, DUMP>(S, tile, u0, v0, sp, best, dump);
         __syncthreads();  // every thread is done with this buffer before it is refilled
     }
 
@@ -1046,9 +1066,9 @@ __global__ void __launch_bounds__(kInterThreads) k_inter_batch(const SolView<DT>
 // (one Eq. 4 concatenation per step).
 __constant__ int kIntraVariants[13] = {0, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20, 21, 22};
 
-template <class DT, bool TW>
+template <class DT, bool TW, bool DUMP = false>
 __device__ __forceinline__ void intra_body(const SolView<DT> &S, const ScoreParams &sp, uint32_t vmask, int x_lo,
-                                           int x_hi, uint64_t *__restrict__ keys) {
+                                           int x_hi, uint64_t *__restrict__ keys, unsigned long long *dump = nullptr) {
     __shared__ unsigned long long red[23];
     if (threadIdx.x < 23) red[threadIdx.x] = kNoKey;
     __syncthreads();
@@ -1075,8 +1095,10 @@ __device__ __forceinline__ void intra_body(const SolView<DT> &S, const ScorePara
             return N == 1 ? S.node_tw[S.node[a]] : (N == 2 ? S.seg2T[a] : S.seg3T[a]);
         };
         auto key = [&](DT dD, float tv, int q) -> uint64_t {
-            return score_key<DT, TW>(sp, true, dD, W, 0, W, 0, tv, 0.f, TV0, 0.f,
-                                     static_cast<uint32_t>(x) * S.Qc + static_cast<uint32_t>(base + q));
+            const uint32_t idx = static_cast<uint32_t>(x) * S.Qc + static_cast<uint32_t>(base + q);
+            const uint64_t k = score_key<DT, TW>(sp, true, dD, W, 0, W, 0, tv, 0.f, TV0, 0.f, idx);
+            if constexpr (DUMP) dump_put(dump, S.Qc * S.Qc, var, idx, k);
+            return k;
         };
         if (var == 0) {
             // 2-opt: reverse u..v (Eq. 7); loads unchanged; CVRP only (host-checked)
@@ -1171,10 +1193,10 @@ __device__ __forceinline__ void intra_body(const SolView<DT> &S, const ScorePara
         atomicMin(reinterpret_cast<unsigned long long *>(keys) + threadIdx.x, red[threadIdx.x]);
 }
 
-template <class DT, bool TW>
+template <class DT, bool TW, bool DUMP = false>
 __global__ void __launch_bounds__(256) k_intra(const __grid_constant__ SolView<DT> S, ScoreParams sp, uint32_t vmask,
-                                               int x_lo, int x_hi, uint64_t *__restrict__ keys) {
-    intra_body<DT, TW>(S, sp, vmask, x_lo, x_hi, keys);
+                                               int x_lo, int x_hi, uint64_t *__restrict__ keys, unsigned long long *dump) {
+    intra_body<DT, TW, DUMP>(S, sp, vmask, x_lo, x_hi, keys, dump);
 }
 
 // population mode: blockIdx.y = solution (BASELINE config 5)
@@ -1227,9 +1249,9 @@ __device__ __forceinline__ TwRec scan_bwd(TwRec rec, float &outl, int lane, int 
     return rec;
 }
 
-template <class DT>
+template <class DT, bool DUMP = false>
 __device__ __forceinline__ void intra_tw_warp(const SolView<DT> &S, const ScoreParams &sp, uint32_t vmask, int x,
-                                              unsigned long long *red) {
+                                              unsigned long long *red, unsigned long long *dump = nullptr) {
     const int lane = threadIdx.x & 31;
     auto D = [&](int a, int b) -> DT { return S.Dp[static_cast<size_t>(a) * S.pitch + b]; };
     auto E = [&](int y) -> DT { return S.enext[y]; };
@@ -1246,9 +1268,13 @@ __device__ __forceinline__ void intra_tw_warp(const SolView<DT> &S, const ScoreP
     const float TV0 = S.rTV[r];
     const TwRec segx[3] = {S.node_tw[nx], sg2x, sg3x};
     const DT brg[3] = {br1, br2, br3}, Exn[3] = {Ex0, Ex1, Ex2};  // E(x + N - 1)
-    auto keyof = [&](bool ok, DT dD, float tv, int q) -> uint64_t {
-        return score_key<DT, true>(sp, ok, dD, W, 0, W, 0, tv, 0.f, TV0, 0.f,
-                                   static_cast<uint32_t>(x) * S.Qc + static_cast<uint32_t>(base + q));
+    auto keyof = [&](bool ok, DT dD, float tv, int q, int var) -> uint64_t {
+        const uint32_t idx = static_cast<uint32_t>(x) * S.Qc + static_cast<uint32_t>(base + q);
+        const uint64_t k = score_key<DT, true>(sp, ok, dD, W, 0, W, 0, tv, 0.f, TV0, 0.f, idx);
+        if constexpr (DUMP) {
+            if (ok) dump_put(dump, S.Qc * S.Qc, var, idx, k);
+        }
+        return k;
     };
     uint64_t best[23];
 #pragma unroll
@@ -1304,7 +1330,7 @@ __device__ __forceinline__ void intra_tw_warp(const SolView<DT> &S, const ScoreP
                 const TwRec P = tw_cat(F, Gk, static_cast<float>(brg[N - 1]));
                 const TwRec A2 = tw_cat(P, segx[N - 1], static_cast<float>(d[0][0]));
                 const float tv = tw_cat(A2, bw[0], static_cast<float>(d[N - 1][1])).w;
-                best[10 + N] = umin64(best[10 + N], keyof(ok, dD, tv, q));
+                best[10 + N] = umin64(best[10 + N], keyof(ok, dD, tv, q, 10 + N));
             }
 #pragma unroll
             for (int b = 1; b <= 3; ++b) {
@@ -1325,7 +1351,7 @@ __device__ __forceinline__ void intra_tw_warp(const SolView<DT> &S, const ScoreP
                     const TwRec R3 = tw_cat(R2, segx[a - 1], static_cast<float>(dxm));
                     tv = tw_cat(R3, bw[b - 1], static_cast<float>(d[a - 1][b])).w;
                 }
-                best[var] = umin64(best[var], keyof(ok, dD, tv, q));
+                best[var] = umin64(best[var], keyof(ok, dD, tv, q, var));
             }
         }
     }
@@ -1372,7 +1398,7 @@ __device__ __forceinline__ void intra_tw_warp(const SolView<DT> &S, const ScoreP
                 const DT dD = rem + dq0 + dq1[N - 1] - Evq;
                 const TwRec A2 = tw_cat(Fq, segx[N - 1], static_cast<float>(dq0));
                 const float tv = tw_cat(A2, Sn, static_cast<float>(dq1[N - 1])).w;
-                best[var] = umin64(best[var], keyof(ok, dD, tv, q));
+                best[var] = umin64(best[var], keyof(ok, dD, tv, q, var));
             }
         }
     }
@@ -1384,14 +1410,15 @@ __device__ __forceinline__ void intra_tw_warp(const SolView<DT> &S, const ScoreP
     }
 }
 
-template <class DT>
+template <class DT, bool DUMP = false>
 __global__ void __launch_bounds__(256) k_intra_tw(const __grid_constant__ SolView<DT> S, ScoreParams sp,
-                                                  uint32_t vmask, int x_lo, int x_hi, uint64_t *__restrict__ keys) {
+                                                  uint32_t vmask, int x_lo, int x_hi, uint64_t *__restrict__ keys,
+                                                  unsigned long long *dump) {
     __shared__ unsigned long long red[8][23];   // one private row per warp
     for (int i = threadIdx.x; i < 8 * 23; i += blockDim.x) red[i / 23][i % 23] = kNoKey;
     __syncthreads();
     const int x = x_lo + static_cast<int>(blockIdx.x) * 8 + (threadIdx.x >> 5);
-    if (x < x_hi) intra_tw_warp<DT>(S, sp, vmask, x, red[threadIdx.x >> 5]);
+    if (x < x_hi) intra_tw_warp<DT, DUMP>(S, sp, vmask, x, red[threadIdx.x >> 5], dump);
     __syncthreads();
     if (threadIdx.x < 23) {
         unsigned long long m = red[0][threadIdx.x];
@@ -1425,13 +1452,15 @@ __global__ void __launch_bounds__(256) k_intra_tw_batch(const SolView<DT> *__res
 // per variant the warp argmin is one 32-bit REDUX.MIN of (score << 5 | lane):
 // lanes hold consecutive canonical v, so the lowest lane is the lowest index.
 // Loads are unchanged by intra moves (Eq. 3f), so feasibility is the route's.
+template <bool DUMP = false>
 __global__ void __launch_bounds__(256) k_intra_cvrp(const SolView<int32_t> S, ScoreParams sp, uint32_t vmask,
-                                                    int x_lo, int x_hi, uint64_t *__restrict__ keys) {
+                                                    int x_lo, int x_hi, uint64_t *__restrict__ keys,
+                                                    unsigned long long *dump) {
     __shared__ unsigned long long red[8][23];   // one private row per warp
     for (int i = threadIdx.x; i < 8 * 23; i += blockDim.x) red[i / 23][i % 23] = kNoKey;
     __syncthreads();
     const int x = x_lo + static_cast<int>(blockIdx.x) * 8 + (threadIdx.x >> 5);
-    if (x < x_hi) intra_cvrp_warp(S, sp, vmask, x, red[threadIdx.x >> 5]);
+    if (x < x_hi) intra_cvrp_warp<DUMP>(S, sp, vmask, x, red[threadIdx.x >> 5], nullptr, dump);
     __syncthreads();
     if (threadIdx.x < 23) {
         unsigned long long m = red[0][threadIdx.x];
@@ -1505,12 +1534,9 @@ static cudaError_t launch_inter_t(const SolView<DT> &S, const CUtensorMap &map, 
                                   int t_hi, const ScoreParams &sp, uint64_t *keys, int grid, cudaStream_t st) {
     auto kern = k_inter<DT, TW, MASK>;
     const int smem = 2 * kBoxBytesPadded + 128;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr = true;
-    }
-    kern<<<grid, kInterThreads, smem, st>>>(S, map, tiles, t_lo, t_hi, sp, keys);
+    static PerDevice pd;
+    once_per_device(pd, [&](int) { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); });
+    kern<<<grid, kInterThreads, smem, st>>>(S, map, tiles, t_lo, t_hi, sp, keys, nullptr);
     ++g_launches;
     return cudaGetLastError();
 }
@@ -1552,24 +1578,68 @@ cudaError_t launch_intra(uint32_t mask, bool tw, const SolView<DT> &S, const Sco
     if constexpr (std::is_same<DT, int32_t>::value) {
         if (!tw && small_dist) {
             const int blocks = (x_hi - x_lo + 7) / 8;
-            k_intra_cvrp<<<blocks, 256, 0, st>>>(S, sp, intra, x_lo, x_hi, keys);
+            k_intra_cvrp<false><<<blocks, 256, 0, st>>>(S, sp, intra, x_lo, x_hi, keys, nullptr);
             ++g_launches;
             return cudaGetLastError();
         }
     }
     if (tw && !(intra & 1u) && warp_tw) {  // warp-parallel VRPTW kernel (long routes)
         const int blocks = (x_hi - x_lo + 7) / 8;
-        k_intra_tw<DT><<<blocks, 256, 0, st>>>(S, sp, intra, x_lo, x_hi, keys);
+        k_intra_tw<DT, false><<<blocks, 256, 0, st>>>(S, sp, intra, x_lo, x_hi, keys, nullptr);
         ++g_launches;
         return cudaGetLastError();
     }
     const int threads = (x_hi - x_lo + 31) / 32 * 32 * __builtin_popcount(intra);
     const int blocks = (threads + 255) / 256;
-    if (tw) k_intra<DT, true><<<blocks, 256, 0, st>>>(S, sp, intra, x_lo, x_hi, keys);
-    else    k_intra<DT, false><<<blocks, 256, 0, st>>>(S, sp, intra, x_lo, x_hi, keys);
+    if (tw) k_intra<DT, true, false><<<blocks, 256, 0, st>>>(S, sp, intra, x_lo, x_hi, keys, nullptr);
+    else    k_intra<DT, false, false><<<blocks, 256, 0, st>>>(S, sp, intra, x_lo, x_hi, keys, nullptr);
     ++g_launches;
     return cudaGetLastError();
 }
+
+// ---- test-only DUMP instantiations (tga_debug_eval_dump): the same kernels and launch
+// geometry as launch_inter / launch_intra, every evaluated candidate's key stored in dump
+template <class DT>
+cudaError_t launch_eval_dump(uint32_t mask, bool tw, const SolView<DT> &S, const CUtensorMap &map,
+                             const uint32_t *tiles, int t_lo, int t_hi, const ScoreParams &sp, uint64_t *keys,
+                             int grid, int x_lo, int x_hi, bool inter, bool small_dist, bool warp_tw,
+                             cudaStream_t st, unsigned long long *dump) {
+    constexpr uint32_t ALL = 0x7FEu;
+    if (inter && t_hi > t_lo && (mask & ALL)) {
+        const int smem = 2 * kBoxBytesPadded + 128;
+        auto kern = tw ? k_inter<DT, true, ALL, true> : k_inter<DT, false, ALL, true>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        kern<<<grid, kInterThreads, smem, st>>>(S, map, tiles, t_lo, t_hi, sp, keys, dump);
+        ++g_launches;
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    const uint32_t intra = mask & ((1u << 0) | (0x7u << 11) | (0x1FFu << 14));
+    if (x_hi <= x_lo || !intra) return cudaSuccess;
+    if constexpr (std::is_same<DT, int32_t>::value) {
+        if (!tw && small_dist) {
+            k_intra_cvrp<true><<<(x_hi - x_lo + 7) / 8, 256, 0, st>>>(S, sp, intra, x_lo, x_hi, keys, dump);
+            ++g_launches;
+            return cudaGetLastError();
+        }
+    }
+    if (tw && !(intra & 1u) && warp_tw) {
+        k_intra_tw<DT, true><<<(x_hi - x_lo + 7) / 8, 256, 0, st>>>(S, sp, intra, x_lo, x_hi, keys, dump);
+        ++g_launches;
+        return cudaGetLastError();
+    }
+    const int threads = (x_hi - x_lo + 31) / 32 * 32 * __builtin_popcount(intra);
+    if (tw) k_intra<DT, true, true><<<(threads + 255) / 256, 256, 0, st>>>(S, sp, intra, x_lo, x_hi, keys, dump);
+    else    k_intra<DT, false, true><<<(threads + 255) / 256, 256, 0, st>>>(S, sp, intra, x_lo, x_hi, keys, dump);
+    ++g_launches;
+    return cudaGetLastError();
+}
+template cudaError_t launch_eval_dump<int32_t>(uint32_t, bool, const SolView<int32_t> &, const CUtensorMap &,
+                                               const uint32_t *, int, int, const ScoreParams &, uint64_t *, int, int,
+                                               int, bool, bool, bool, cudaStream_t, unsigned long long *);
+template cudaError_t launch_eval_dump<float>(uint32_t, bool, const SolView<float> &, const CUtensorMap &,
+                                             const uint32_t *, int, int, const ScoreParams &, uint64_t *, int, int, int,
+                                             bool, bool, bool, cudaStream_t, unsigned long long *);
 
 template <class DT, bool TW>
 static cudaError_t launch_inter_batch_tw(uint32_t mask, const SolView<DT> *views, const CUtensorMap *maps,
@@ -1580,11 +1650,8 @@ static cudaError_t launch_inter_batch_tw(uint32_t mask, const SolView<DT> *views
     auto run = [&](auto kmask) {
         if (err != cudaSuccess) return;
         auto kern = k_inter_batch<DT, TW, decltype(kmask)::value>;
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-            attr = true;
-        }
+        static PerDevice pd;
+        once_per_device(pd, [&](int) { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); });
         kern<<<grid, kInterThreads, smem, st>>>(views, maps, work, n_work, sp, keys);
         ++g_launches;
         err = cudaGetLastError();

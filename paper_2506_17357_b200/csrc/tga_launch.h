@@ -6,6 +6,7 @@
 #include <type_traits>
 #include <algorithm>
 #include <utility>
+#include <mutex>
 
 #include "tga_device.cuh"
 
@@ -81,7 +82,7 @@ struct DevState {
     int32_t *rbase, *rlenR, *cbase;              // per route
     int32_t *scratch;                            // snapshot of a changed span (cap ints)
     uint64_t *keys;                              // 23 packed keys of the last evaluation (reset to ~0 once consumed)
-    int32_t *desc;                               // [0] applied, [1..7] UpdateSpec, [8] grid-barrier counter
+    int32_t *desc;                               // [0] applied, [1..7] UpdateSpec, [8] grid-barrier count, [9] arrivals, [10] barrier generation
     unsigned long long *acc;                     // [23] candidate counts + [23] applied moves
     int32_t *slot_of;                            // ETGA node -> slot map kept current by the step (or null)
     void *Dp;
@@ -110,6 +111,17 @@ template <class DT>
 cudaError_t launch_batch(uint32_t mask, bool tw, const SolView<DT> *views, const CUtensorMap *maps,
                          const uint32_t *work, int n_work, int n_sol, int max_qp, const ScoreParams &sp,
                          uint64_t *keys, int grid, cudaStream_t st, bool warp_tw = false);
+// test-only DUMP instantiations (tga_debug_eval_dump): every evaluated candidate's key
+// at dump[variant * pitch^2 + physical flat index]
+template <class DT>
+cudaError_t launch_eval_dump(uint32_t mask, bool tw, const SolView<DT> &S, const CUtensorMap &map,
+                             const uint32_t *tiles, int t_lo, int t_hi, const ScoreParams &sp, uint64_t *keys,
+                             int grid, int x_lo, int x_hi, bool inter, bool small_dist, bool warp_tw,
+                             cudaStream_t st, unsigned long long *dump);
+cudaError_t launch_inter_fast_dump(bool tw, const SlotRec *rec, const SlotTW *rectw, const CUtensorMap &map,
+                                   const uint32_t *tiles, int t_lo, int t_hi, uint32_t Qc, int32_t cap, uint64_t *keys,
+                                   cudaStream_t st, const SolView<int32_t> &SV, const ScoreParams &sp, uint32_t imask,
+                                   int x_lo, int x_hi, unsigned long long *dump);
 unsigned long long launch_count();
 void note_launch();
 
@@ -121,6 +133,21 @@ void note_launch();
 // never take the SM slots a grid barrier of this kernel waits for).
 // Enabled per launch site with TGA_PDL_MODE (see pdl_enabled; off by default).
 bool pdl_enabled(int which = 1);
+// One-time per-device setup (kernel attributes, occupancy-derived capacities):
+// f(dev) runs once per CUDA device ordinal, thread-safely; callers index their
+// cached values by the returned ordinal (a process may drive several devices).
+constexpr int kMaxDevices = 64;
+struct PerDevice {
+    std::once_flag flag[kMaxDevices];
+};
+template <class F>
+int once_per_device(PerDevice &pd, F f) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= kMaxDevices) dev = kMaxDevices - 1;
+    std::call_once(pd.flag[dev], f, dev);
+    return dev;
+}
 // cooperative != 0: the launch guarantees that every block of the grid is resident
 // at once (or fails with cudaErrorCooperativeLaunchTooLarge instead of deadlocking)
 // -- required by kernels whose blocks wait for each other (grid barriers).

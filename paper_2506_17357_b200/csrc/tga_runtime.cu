@@ -460,8 +460,11 @@ static std::vector<uint32_t> fast_plan(const tga_solution *s) {
     return f;
 }
 
-static void build_tiles(tga_solution *s) {
-    s->d_tiles = s->d_tiles;  // allocated in the arena
+// Tile plans, uploaded on the solution's stream: the arena they live in was
+// initialised by stream-ordered memsets (a legacy-stream copy would not be
+// ordered after them); the host vectors are pageable locals, so the stream is
+// drained before they go out of scope.
+static cudaError_t build_tiles(tga_solution *s) {
     std::vector<uint32_t> t;
     const int nI = s->pitch / kTileU, nJ = s->pitch / kTileV;
     for (int I = 0; I < nI; ++I) {
@@ -472,11 +475,14 @@ static void build_tiles(tga_solution *s) {
         }
     }
     s->n_tiles = static_cast<int>(t.size());
-    cudaMemcpy(s->d_tiles, t.data(), sizeof(uint32_t) * t.size(), cudaMemcpyHostToDevice);
+    cudaError_t e = cudaMemcpyAsync(s->d_tiles, t.data(), sizeof(uint32_t) * t.size(), cudaMemcpyHostToDevice, s->stream);
     // fast-path plan: fastU x kFastTV tiles of the upper triangle
     const std::vector<uint32_t> f = fast_plan(s);
     s->n_ftiles = static_cast<int>(f.size());
-    if (s->d_ftiles) cudaMemcpy(s->d_ftiles, f.data(), sizeof(uint32_t) * f.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && s->d_ftiles)
+        e = cudaMemcpyAsync(s->d_ftiles, f.data(), sizeof(uint32_t) * f.size(), cudaMemcpyHostToDevice, s->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
+    return e;
 }
 
 static void free_solution(tga_solution *s) {
@@ -553,6 +559,32 @@ extern "C" int32_t tga_instance_create(int32_t n, const void *dist, int32_t dtyp
     }
     if (opt) I->opt = *opt;
     else { I->opt.score_mode = TGA_SCORE_FEASIBLE; I->opt.w_load = 10; I->opt.w_tw = 10; I->opt.device = -1; }
+    if (I->opt.score_mode != TGA_SCORE_FEASIBLE && I->opt.score_mode != TGA_SCORE_PENALISED) {
+        delete I;
+        return fail(TGA_ERR_INVALID_ARGUMENT, "score_mode");
+    }
+    if (dtype == TGA_I32) {
+        // integer scores are packed as 32-bit order-preserving images: bound |score| of any
+        // candidate.  dD sums at most 8 distances (Eq. 2); penalised mode adds
+        // w_load * dL_V with |dL_V| <= 2 x total demand and w_tw * dT_V with |dT_V| <= the
+        // warp two routes can hold, each stop at most max l + max s + max c (Eq. 4).
+        double bound = 8.0 * max_abs;
+        if (I->opt.score_mode == TGA_SCORE_PENALISED) {
+            double tot = 0;
+            for (int i = 0; i < n; ++i) tot += demand[i];
+            bound += std::fabs(static_cast<double>(I->opt.w_load)) * 2.0 * tot;
+            if (tw) {
+                double ml = 0, ms = 0;
+                for (int i = 0; i < n; ++i) { ml = std::max(ml, static_cast<double>(tw[3 * i + 1])); ms = std::max(ms, static_cast<double>(tw[3 * i + 2])); }
+                bound += std::fabs(static_cast<double>(I->opt.w_tw)) * (n + 1.0) * (ml + ms + max_abs);
+            }
+        }
+        if (bound >= 2147483647.0) {
+            delete I;
+            return fail(TGA_ERR_INVALID_ARGUMENT, "integer score range exceeds int32 (distances, demands or "
+                                                  "penalty weights too large; use TGA_F32)");
+        }
+    }
     if (I->opt.device < 0) cudaGetDevice(&I->device);
     else I->device = I->opt.device;
     I->hDemand.assign(demand, demand + n);
@@ -651,9 +683,12 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
     s->Qp = s->N + (2 + s->slack) * R;
     s->pitch = static_cast<int>(align_up(static_cast<size_t>(s->Qp) + 4, kPitchAlign));
     s->cap = s->pitch + 2 * kGuard;
-    if (static_cast<uint64_t>(s->Qc) * s->Qc > 0xFFFFFFFFull) {
+    // keys pack the flat index over PHYSICAL slots, u * pitch + v < pitch^2, in 32 bits
+    // (pitch >= Q_p > Q = N + R, so this also bounds the canonical index)
+    if (static_cast<uint64_t>(s->pitch) * static_cast<uint64_t>(s->pitch) > 0x100000000ull) {
         delete s;
-        return fail(TGA_ERR_INVALID_ARGUMENT, "Q^2 exceeds the 32-bit flat index");
+        return fail(TGA_ERR_INVALID_ARGUMENT, "physical slot pitch^2 exceeds the 32-bit flat index "
+                                              "(too many customers + routes x (2 + slack))");
     }
     relayout_full(s);
     int32_t rc = TGA_OK;
@@ -767,7 +802,7 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
     // ---- layout upload, Dp build, scan
     if ((rc = upload_layout(s, true)) != TGA_OK) return bail(rc);
     if ((rc = refresh(s, true)) != TGA_OK) return bail(rc);
-    build_tiles(s);
+    if (build_tiles(s) != cudaSuccess) return bail(fail(TGA_ERR_CUDA, "tile plan upload"));
     // ---- TMA descriptor over Dp: dims {pitch cols, pitch rows}, box {kBoxW, kBoxH}
     if (auto enc = get_encode()) {
         cuuint64_t gdim[2] = {static_cast<cuuint64_t>(s->pitch), static_cast<cuuint64_t>(s->pitch)};
@@ -966,6 +1001,77 @@ extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
 }
 
 static uint64_t key_to_canonical(const tga_solution *s, uint64_t k);
+
+// Test-only: one evaluation with the DUMP instantiations of the same kernels and launch
+// decisions as tga_eval (no shards, no NCCL); every evaluated candidate's packed key
+// is returned per variant over CANONICAL slots (see tga.h).
+extern "C" int32_t tga_debug_eval_dump(tga_solution *s, uint32_t mask, int32_t flags, uint64_t *out, int64_t out_len) {
+    if (!s || !out) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL argument");
+    const tga_instance *I = s->inst;
+    mask &= TGA_OP_ALL;
+    const int64_t Q = s->Qc;
+    if (out_len < static_cast<int64_t>(TGA_N_VARIANTS) * Q * Q) return fail(TGA_ERR_INVALID_ARGUMENT, "out too small");
+    if ((mask & TGA_OP_2OPT) && I->tw) return fail(TGA_ERR_UNSUPPORTED, "2-opt is only defined without time windows (P:148)");
+    if (I->theta > 0) return fail(TGA_ERR_UNSUPPORTED, "dump of the edge-based neighbourhood");
+    if (set_device(I) != TGA_OK) return TGA_ERR_CUDA;
+    if (sync_host(s) != TGA_OK) return TGA_ERR_CUDA;
+    const size_t plane = static_cast<size_t>(s->pitch) * s->pitch;
+    unsigned long long *dump = nullptr;
+    TGA_CUDA(cudaMalloc(&dump, plane * TGA_N_VARIANTS * 8));
+    std::vector<unsigned long long> h(plane * TGA_N_VARIANTS);
+    cudaStream_t st = s->stream;
+    cudaError_t e = cudaMemsetAsync(dump, 0, plane * TGA_N_VARIANTS * 8, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(s->keys, 0xFF, TGA_N_VARIANTS * 8, st);
+    const ScoreParams sp{I->Q, I->opt.score_mode, I->opt.w_load, I->opt.w_tw};
+    const bool warp_tw = (flags & 1) ? true : ((flags & 2) ? false : s->N >= 16 * s->R);
+    const bool small = I->max_c_abs < (1 << 21);
+    const int grid = std::max(1, std::min(s->n_tiles, s->sm_count * 4));
+    if (e == cudaSuccess) {
+        if (I->dtype == TGA_I32 && s->fast) {
+            const bool fused = (mask & TGA_OP_INTER) && !I->tw && small;
+            const uint32_t imask = fused ? (mask & TGA_OP_INTRA) : 0u;
+            if (mask & TGA_OP_INTER)
+                e = launch_inter_fast_dump(I->tw, s->rec, s->rectw, s->fmap, s->d_ftiles, 0, s->n_ftiles,
+                                           static_cast<uint32_t>(s->pitch), I->Q, s->keys, st, sol_view<int32_t>(s),
+                                           sp, imask, 0, s->Qp, dump);
+            if (e == cudaSuccess && !fused)
+                e = launch_eval_dump<int32_t>(mask, I->tw, sol_view<int32_t>(s), s->tmap, s->d_tiles, 0, 0, sp, s->keys,
+                                              grid, 0, s->Qp, false, small, warp_tw, st, dump);
+        } else if (I->dtype == TGA_I32) {
+            e = launch_eval_dump<int32_t>(mask, I->tw, sol_view<int32_t>(s), s->tmap, s->d_tiles, 0, s->n_tiles, sp,
+                                          s->keys, grid, 0, s->Qp, true, small, warp_tw, st, dump);
+        } else {
+            e = launch_eval_dump<float>(mask, I->tw, sol_view<float>(s), s->tmap, s->d_tiles, 0, s->n_tiles, sp,
+                                        s->keys, grid, 0, s->Qp, true, false, warp_tw, st, dump);
+        }
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h.data(), dump, plane * TGA_N_VARIANTS * 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(dump);
+    if (e != cudaSuccess) return fail(TGA_ERR_CUDA, std::string("eval dump: ") + cudaGetErrorString(e));
+    // physical slot -> canonical id (-1: end depot, spare or padding)
+    std::vector<int> can(s->pitch, -1);
+    for (int r = 0; r < s->R; ++r)
+        for (int p = 0; p <= static_cast<int>(s->routes[r].size()); ++p) can[s->rbase[r] + p] = s->cbase[r] + p;
+    std::fill(out, out + TGA_N_VARIANTS * Q * Q, 0ull);
+    for (int v = 0; v < TGA_N_VARIANTS; ++v) {
+        if (!(mask & (1u << v))) continue;
+        for (int a = 0; a < s->pitch; ++a) {
+            if (can[a] < 0) continue;
+            for (int b = 0; b < s->pitch; ++b) {
+                const unsigned long long k = h[v * plane + static_cast<size_t>(a) * s->pitch + b];
+                if (!k || can[b] < 0) continue;
+                const uint64_t ci = static_cast<uint64_t>(can[a]) * Q + can[b];
+                out[v * Q * Q + ci] = k == ~0ull ? ~0ull : ((k & 0xFFFFFFFF00000000ull) | ci);
+            }
+        }
+    }
+    s->eval_gen = s->gen;
+    s->eval_mask = mask;
+    s->keys_clean = false;
+    s->drained = true;
+    return TGA_OK;
+}
 
 extern "C" int32_t tga_solution_keys(tga_solution *s, uint64_t *keys) {
     if (!s || !keys) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL argument");

@@ -116,6 +116,7 @@ _SYMBOLS = {
     "tga_batch_step_async": (C.c_int32, [C.c_void_p, C.c_uint32]),
     "tga_batch_set_stream": (C.c_int32, [C.c_void_p, C.c_void_p]),
     "tga_batch_device_stats": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "tga_debug_eval_dump": (C.c_int32, [C.c_void_p, C.c_uint32, C.c_int32, C.c_void_p, C.c_int64]),
     "tga_last_error": (C.c_char_p, []),
     "tga_version": (C.c_char_p, []),
     "tga_launch_count": (C.c_uint64, []),
@@ -299,6 +300,14 @@ class Solution:
         fp, fb = (None, 0) if l2_flush is None else (l2_flush.data_ptr(), l2_flush.numel() * l2_flush.element_size())
         _check(lib().tga_descent(self._h, op_mask, n_steps, fp, fb, _p(ms)))
         return ms[:n_steps] if timed else None
+
+    def eval_dump(self, op_mask: int = OP_ALL, flags: int = 0) -> np.ndarray:
+        """Test-only: every candidate's packed key, [variant, Q, Q] over canonical
+        slots (0 = not evaluated, ~0 = infeasible / invalid); see tga_debug_eval_dump."""
+        _, _, Q, _ = self.info()
+        out = np.zeros((N_VARIANTS, Q, Q), dtype=np.uint64)
+        _check(lib().tga_debug_eval_dump(self._h, op_mask, flags, _p(out), out.size))
+        return out
 
     def debug_probe(self, enable: bool = True):
         """Diagnostics: clock64 phase stamps of the last device step (16 u64), then (re)arm."""

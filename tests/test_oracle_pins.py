@@ -32,6 +32,10 @@ def test_hand_worked_deltas(ex):
     assert orc.cost(ex["routes"])[0] == ex["cost_before"]
     m = orc.score_candidate(ex["routes"], ex["variant"], ex["ra"], ex["pa"], ex["rb"], ex["pb"])
     assert m.found and m.feasible and m.dD == ex["delta"] and m.score == ex["delta"]
+    # canonical slot ids worked by hand (golden "u", "v", "Q")
+    assert (m.u, m.v) == (ex["u"], ex["v"]) and O.canonical_q(ex["routes"]) == ex["Q"]
+    sc, us, vs, _ = orc.enumerate(ex["routes"], ex["variant"])
+    assert (ex["delta"], ex["u"], ex["v"]) in set(zip(sc.tolist(), us.tolist(), vs.tolist()))
     new = orc.apply(ex["routes"], ex["variant"], ex["ra"], ex["pa"], ex["rb"], ex["pb"])
     assert new == ex["routes_after"]
     assert orc.cost(new)[0] == ex["cost_after"]
@@ -140,17 +144,46 @@ def test_brute_force_neighbourhood(seed, tw, mode):
     orc = O.Oracle(dist, demand, cap, twa)
     d = dist.tolist()
     t = None if twa is None else twa.tolist()
+    _brute_vs_oracle(orc, d, demand.tolist(), t, cap, sol.routes, mode)
+
+
+def _brute_vs_oracle(orc, d, demand, t, cap, routes, mode):
+    """Every variant: the multiset of (score, u, v) triples of the oracle's canonical
+    enumeration == the brute-force neighbours with their canonical slot pair named
+    from the definition (brute.slot_id); the oracle's best == the lowest (score,
+    u * Q + v) of the brute force (reading 5)."""
+    Q = O.canonical_q(routes)
     for op, n1, n2, var in BRUTE_OPS:
-        bs = brute.scores(d, demand.tolist(), t, cap, sol.routes, op, n1, n2, mode)
-        sc, us, vs, best = orc.enumerate(sol, var, mode)
-        assert sorted(bs) == sorted(sc.tolist()), (op, n1, n2)
-        if len(bs):
-            assert best.score == min(bs)
-            # lowest canonical index among the minimal scores
-            Q = O.canonical_q(sol)
-            finite = [(s, u * Q + v) for s, u, v in zip(sc, us, vs)]
-            if best.found:
-                assert (best.score, best.u * Q + best.v) == min(finite)
+        bt = brute.scores(d, demand, t, cap, routes, op, n1, n2, mode, with_index=True)
+        sc, us, vs, best = orc.enumerate(routes, var, mode)
+        got = sorted(zip(sc.tolist(), us.tolist(), vs.tolist()))
+        assert sorted(bt) == got, (op, n1, n2)
+        bb = brute.best(bt, Q)
+        assert best.found == (bb is not None), (op, n1, n2)
+        if bb is not None:
+            assert (best.score, best.u * Q + best.v) == bb, (op, n1, n2)
+
+
+@pytest.mark.parametrize("seed", range(4))
+@pytest.mark.parametrize("spare", [False, True])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_cfg1_oracle_vs_brute_force(seed, spare, mode):
+    """BASELINE config 1 ("full 2-opt/2-opt*/relocate/swap sweep vs brute force"):
+    20 customers, 4 routes, Q=100 -- every variant of the oracle against the
+    independent brute force, scores AND canonical indices."""
+    inst, sol = G.cvrp_small(seed, spare=spare)
+    orc = O.Oracle.from_instance(inst)
+    _brute_vs_oracle(orc, inst.dist.tolist(), inst.demand.tolist(), None, inst.capacity, sol.routes, mode)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_cfg1_random_partitions_vs_brute_force(seed):
+    """Config-1 instances with ragged, empty and overloaded routes (both modes)."""
+    inst, _ = G.cvrp_small(seed)
+    sol = G.random_partition(20, 3 + seed, 900 + seed, allow_empty=True)
+    orc = O.Oracle.from_instance(inst)
+    for mode in (0, 1):
+        _brute_vs_oracle(orc, inst.dist.tolist(), inst.demand.tolist(), None, inst.capacity, sol.routes, mode)
 
 
 @pytest.mark.parametrize("seed", range(5))
@@ -286,6 +319,19 @@ def test_descent_invariants(name):
         routes, D0 = new, D1
 
 
+@pytest.mark.parametrize("ex", json.load(open(os.path.join(GOLD, "attributes.json")))["examples"],
+                         ids=lambda e: e["name"])
+def test_attributes_hand_worked(ex):
+    """orc_attributes against hand-worked prefix / suffix records (golden
+    attributes.json): D, L and T_V of every prefix [0..p] and suffix [p..L+1]
+    (the suffix simulated from e of its first node), and the service starts."""
+    dist = np.asarray(ex["dist"], dtype=np.float64)
+    orc = O.Oracle(dist, np.asarray(ex["demand"], dtype=np.int64), 100, np.asarray(ex["tw"], dtype=np.float64))
+    at = orc.attributes(ex["routes"])
+    for k in ("pre_D", "pre_L", "pre_TV", "suf_D", "suf_L", "suf_TV", "start"):
+        assert at[k].tolist() == ex[k], k
+
+
 def test_attributes_prefix_suffix():
     """Prefix/suffix records: D/L additive, full-route values match route_eval."""
     inst, sol = G.gh_like(2, n=60, kind="R2")
@@ -350,3 +396,53 @@ def test_edge_based_full_mask_is_the_full_neighbourhood():
     for v in range(O.N_VARIANTS):
         a, b = orc.best_move(sol, v), orc.best_move(sol, v, mask=M)
         assert (a.found, a.score, a.u, a.v, a.n_candidates) == (b.found, b.score, b.u, b.v, b.n_candidates)
+
+
+# ---------------------------------------------------------------- row-parallel driver
+@pytest.mark.parametrize("tw", [False, True])
+def test_parallel_oracle_equals_serial(tw):
+    """tests/par_oracle (row chunks on a thread pool, min over chunk argmins) ==
+    one serial canonical enumeration: same best key and candidate count for every
+    variant, including uneven chunkings (SURVEY §8(d) all-core oracle)."""
+    from tests import par_oracle
+    if tw:
+        inst, sol = G.gh_like(3, n=90, kind="R1")
+        sol = G.perturb(sol, 10, 3)
+    else:
+        inst, sol = G.x_like(2, n=120, target_routes=6)
+    orc = O.Oracle.from_instance(inst)
+    Q = O.canonical_q(sol)
+    variants = [v for v in range(O.N_VARIANTS) if not (tw and v == O.V_2OPT)]
+    for mode in (0, 1):
+        for chunks in (None, 7, Q):
+            best, count = par_oracle.best_keys(orc, sol.routes, variants, mode, chunks_per_variant=chunks)
+            for v in variants:
+                m = orc.best_move(sol, v, mode)
+                assert count[v] == m.n_candidates
+                assert best[v] == ((m.score, m.u * Q + m.v) if m.found else None), (v, mode, chunks)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_enumerate_full_feasibility_and_band(seed):
+    """orc_enumerate_full's per-candidate feasibility flag and ambiguity-band flag
+    (reading 13) == the brute force's own simulation of every neighbour,
+    on windows whose deadlines coincide with reference starts (band cases occur)."""
+    dist, demand, twa, cap, sol = _tiny(seed, True)
+    # pull some deadlines onto the earliest starts of the current routes (exact ties)
+    orc0 = O.Oracle(dist, demand, cap, twa)
+    for r in [max(sol.routes, key=len)]:
+        _, _, _, _, st = orc0.route_eval([0] + r + [0])
+        for k, c in enumerate(r, start=1):
+            if k % 2:
+                twa[c, 1] = st[k]
+    orc = O.Oracle(dist, demand, cap, twa)
+    d, t = dist.tolist(), twa.tolist()
+    nb = 0
+    for op, n1, n2, var in BRUTE_OPS:
+        for mode in (0, 1):
+            bt = brute.scores(d, demand.tolist(), t, cap, sol.routes, op, n1, n2, mode, with_index="full")
+            sc, us, vs, fe, bd, _ = orc.enumerate_full(sol, var, mode)
+            got = sorted(zip(sc.tolist(), us.tolist(), vs.tolist(), fe.tolist(), bd.tolist()))
+            assert sorted(bt) == got, (op, n1, n2, mode)
+            nb += int(bd.sum())
+    assert nb > 0, "the instance must exercise the band"

@@ -11,6 +11,8 @@ import pytest
 
 import oracle as O
 import tga_gen as G
+from tests import brute
+from tests import par_oracle
 from tests.conftest import gpu_available
 
 pytestmark = pytest.mark.gpu
@@ -69,6 +71,34 @@ def test_cfg1_all_variants_exact(seed, spare, mode):
     _need_gpu()
     inst, sol = G.cvrp_small(seed, spare=spare)
     check_exact(inst, sol, ALLV, mode, f"cfg1 s{seed}")
+
+
+@pytest.mark.parametrize("seed", range(4))
+@pytest.mark.parametrize("spare", [False, True])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_cfg1_gpu_vs_brute_force(seed, spare, mode):
+    """BASELINE config 1 as its row states it: "full 2-opt/2-opt*/relocate/swap
+    sweep vs brute force" -- the GPU keys of every variant against the
+    independent brute-force generator (tests/brute.py, no oracle involved):
+    lowest (score, canonical index) of every neighbour it builds by list surgery."""
+    _need_gpu()
+    inst, sol = G.cvrp_small(seed, spare=spare)
+    gs = T.Solution(T.Instance.from_gen(inst, score_mode=mode), sol)
+    gs.eval(T.OP_ALL)
+    got = gpu_keys(gs, integer=True)
+    Q = O.canonical_q(sol)
+    d, dem = inst.dist.tolist(), inst.demand.tolist()
+    for op, n1, n2, var in BRUTE_OPS:
+        exp = brute.best(brute.scores(d, dem, None, inst.capacity, sol.routes, op, n1, n2, mode,
+                                      with_index=True), Q)
+        assert got[var] == exp, (seed, spare, mode, op, n1, n2, got[var], exp)
+
+
+BRUTE_OPS = ([("2opt*", 1, 1, 1), ("2opt", 1, 1, 0)]
+             + [("relocate", n, 1, v) for n, v in O.V_RELOC.items()]
+             + [("swap", a, b, v) for (a, b), v in O.V_SWAP.items()]
+             + [("intra_relocate", n, 1, v) for n, v in O.V_IRELOC.items()]
+             + [("intra_swap", a, b, v) for (a, b), v in O.V_ISWAP.items()])
 
 
 @pytest.mark.parametrize("seed", range(12))
@@ -363,28 +393,32 @@ def test_batch_full_population_1024():
 
 
 # ---------------------------------------------------------------- large CVRP (config 4)
+def check_exact_parallel(inst, routes, variants, mode=0, label="", gs=None):
+    """GPU keys of every variant == the oracle's GLOBAL best over the whole
+    neighbourhood, enumerated row-parallel on every host core (tests/par_oracle)."""
+    if gs is None:
+        gs = T.Solution(T.Instance.from_gen(inst, score_mode=mode), routes)
+    gs.eval(sum(1 << v for v in variants))
+    got = gpu_keys(gs, integer=True)
+    orc = O.Oracle.from_instance(inst)
+    exp, count = par_oracle.best_keys(orc, routes, variants, mode)
+    c = gs.counts()
+    for v in variants:
+        assert got[v] == exp[v], f"{label} variant {v} ({T.VARIANT_NAMES[v]}): gpu {got[v]} oracle {exp[v]}"
+        assert int(c[v]) == count[v], (label, v, int(c[v]), count[v])
+    return gs
+
+
 @pytest.mark.parametrize("name", ["cfg4", "cfg4s"])
-def test_cfg4_large_sampled_exact(name):
-    """BASELINE config 4 at full size (10^4 customers; mean route length 100
-    or 23).  The oracle cannot enumerate 8e8 candidates in a test, so for every
-    variant it enumerates the canonical rows around the GPU's argmin row: the
-    min over any row range containing the global argmin equals the global key
-    (score and lowest index), so the comparison is exact.  Shards must
-    reproduce the unsharded keys."""
+def test_cfg4_large_global_exact(name):
+    """BASELINE config 4 at full size (10^4 customers; mean route length 100 or
+    23; 7.6-7.8e8 candidates): every variant's GPU key (score and canonical
+    index) == the oracle's global argmin, enumerated on all host cores -- not a
+    window around the GPU's own answer.  Row shards of the same launch
+    configuration min-combine to the unsharded keys."""
     _need_gpu()
     inst, sol = G.config(name)
-    gi = T.Instance.from_gen(inst)
-    gs = T.Solution(gi, sol)
-    gs.eval(T.OP_ALL)
-    got = gpu_keys(gs)
-    orc = O.Oracle.from_instance(inst)
-    Q = O.canonical_q(sol)
-    for v in ALLV:
-        assert got[v] is not None, v
-        s, idx = got[v]
-        u = idx // Q
-        m = orc.best_move(sol, v, u_lo=max(0, u - 6), u_hi=min(Q, u + 7))
-        assert (m.score, m.u * Q + m.v) == (s, idx), (name, v)
+    gs = check_exact_parallel(inst, sol.routes, ALLV, 0, name)
     full = gs.keys()
     comb = np.full(T.N_VARIANTS, np.iinfo(np.uint64).max, dtype=np.uint64)
     for sh in range(4):
@@ -392,6 +426,21 @@ def test_cfg4_large_sampled_exact(name):
         gs.eval(T.OP_ALL)
         comb = np.minimum(comb, gs.keys())
     np.testing.assert_array_equal(comb, full)
+
+
+def test_ns2000_full_size_exact():
+    """The north-star workload (X-like CVRP, 2000 customers, 87 routes + spare) at
+    full size, the launch configuration bench.py times: every variant == the
+    oracle's global best (all host cores), and the fused 2-opt*+relocate+swap
+    sweep alone gives the same three keys."""
+    _need_gpu()
+    inst, sol = G.config("ns2000")
+    gs = check_exact_parallel(inst, sol.routes, ALLV, 0, "ns2000")
+    ref = gs.keys()
+    gs.eval(T.OP_FUSED_NS)
+    ns = gs.keys()
+    for v in (1, 2, 5):
+        assert ns[v] == ref[v], v
 
 
 def test_cfg4_shape_reduced_exact():
@@ -699,3 +748,55 @@ def test_vrptw_intra_kernels_forced(force):
                         "no:cacheprovider", "-k", "test_small_vrptw_exact or test_full_size_configs_exact"],
                        env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+# ---------------------------------------------------------------- ABI guards (advisor findings)
+def test_physical_pitch_overflow_rejected():
+    """Keys pack u * pitch + v over PHYSICAL slots in 32 bits: a layout whose
+    padded pitch^2 exceeds 2^32 is rejected at load even when the canonical
+    Q^2 fits (here N + R = 1044, but 2 + slack spare slots per route blow the
+    pitch up)."""
+    _need_gpu()
+    inst, sol = G.x_like(0, n=1000)
+    gi = T.Instance.from_gen(inst, slack=100000)
+    with pytest.raises(T.TgaError) as e:
+        T.Solution(gi, sol)
+    assert e.value.code == -1 and "pitch" in str(e.value)
+
+
+def test_mixed_grid_device_steps_share_the_barrier():
+    """Device steps of the same solutions through the population batch (small
+    grids per solution) and one by one (one block per SM) alternate: the grid
+    barrier and arrival counters reset every launch, so the trajectories equal
+    the host-driven steps."""
+    _need_gpu()
+    inst, sols = G.population(2, n=200, n_sol=4)
+    gi = T.Instance.from_gen(inst)
+    mask = T.OP_ALL & ~T.OP_2OPT
+    db = T.Batch(gi, sols)
+    host = [T.Solution(gi, s) for s in sols]
+    for it in range(12):
+        if it % 3 == 2:
+            for k in range(4):
+                db.solution(k).step_async(mask)
+        else:
+            db.step_async(mask)
+        for h in host:
+            h.step(mask)
+    for k in range(4):
+        assert db.solution(k).routes() == host[k].routes(), k
+
+
+def test_integer_score_range_guard():
+    """Integer scores are packed as 32-bit order-preserving images: distances or
+    penalty weights whose candidate scores could overflow int32 are rejected at
+    instance creation (TGA_F32 stays available)."""
+    _need_gpu()
+    inst, sol = G.cvrp_small(0)
+    big = (inst.dist.astype(np.int64) * (2 ** 26)).astype(np.int32)
+    with pytest.raises(T.TgaError) as e:
+        T.Instance(big, inst.demand, inst.capacity)
+    assert e.value.code == -1
+    with pytest.raises(T.TgaError):
+        T.Instance(inst.dist, inst.demand, inst.capacity, score_mode=T.SCORE_PENALISED, w_load=2 ** 28)
+    T.Instance(inst.dist.astype(np.float32) * 2.0 ** 26, inst.demand, inst.capacity)   # float path accepted

@@ -13,7 +13,8 @@ ap.add_argument("--cold", type=int, default=1)
 a = ap.parse_args()
 inst, sol = G.config(a.config)
 gs = T.Solution(T.Instance.from_gen(inst), sol)
-mask = T.OP_ALL
+ap2 = None
+mask = {"ns": T.OP_FUSED_NS, "all": T.OP_ALL}.get(os.environ.get("PROBE_MASK", "all"), T.OP_ALL)
 flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")
 lib = T.lib()
 lib.tga_debug_inter_probe.argtypes = [C.c_void_p, C.c_int32]

@@ -121,14 +121,19 @@ struct __align__(16) SlotRec {
     int32_t r;       // route id; -1 for an end depot, a spare slot or padding (not a canonical slot)
     int32_t fL;      // prefix load of [0..x]               (2-opt* head),  +P if r < 0
     int32_t bL1;     // suffix load of [x+1..L+1]            (2-opt* tail),  +P if r < 0
-    int32_t ne;      // -e(x), e(x) = c(x, x+1)
+    int32_t ne;      // -e(x), e(x) = c(x, x+1)                               [- w_Q ex, penalised]
     int32_t W;       // route load (insertion target),       +P if r < 0
-    int32_t so[3];   // relocate-out load s_N of x..x+N-1,   +P if the segment is invalid or W - s_N > Q
-    int32_t rem[3];  // relocate-out distance c(x-1, x+N) - e(x-1) - e(x+N-1)  (Eq. 2)
+    int32_t so[3];   // relocate-out load s_N of x..x+N-1,   +P if the segment is invalid or (feasible-only
+                     //                                         records) W - s_N > Q
+    int32_t rem[3];  // relocate-out distance c(x-1, x+N) - e(x-1) - e(x+N-1)  (Eq. 2)  [- w_Q ex]
     int32_t sA[3];   // swap: W - s_N,                       +P if the segment is invalid
     int32_t sS[3];   // swap: s_N
-    int32_t sE[3];   // swap: -e(x-1) - e(x+N-1)
+    int32_t sE[3];   // swap: -e(x-1) - e(x+N-1)                              [- w_Q ex]
 };
+// Penalised records (score = dD + w_Q dL_V, Eq. 16a with reading 4): every candidate
+// changes exactly two routes and its distance formula uses exactly one of {ne, rem[N],
+// sE[N]} of each, so the old excess ex = max(W - Q, 0) of the slot's route enters those
+// three fields as -w_Q ex; a candidate then adds w_Q (max(L_a' - Q, 0) + max(L_b' - Q, 0)).
 static_assert(sizeof(SlotRec) == 80, "SlotRec layout: five 16-byte shared loads per column");
 
 // Time-window part of the fast-path record (VRPTW "TW-I", feasible-only mode).

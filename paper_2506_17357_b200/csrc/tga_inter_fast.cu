@@ -89,12 +89,20 @@ __device__ __forceinline__ void fold(uint64_t &acc, uint32_t b, bool direct, int
 }  // namespace
 
 // The candidate streams of one (row u, column v) cell with route(u) < route(v)
-// (stream slots above): D(di, dj) = Dp(u + di, v + dj); put(slot, ok, dD)
-// receives every candidate -- feasibility ok (capacity, and time windows in the
-// T_V = 0 form of SlotTW) and the distance delta dD (Eq. 2, 13, 14).
-template <bool TW, uint32_t MASK, class DF, class PF>
+// (stream slots above): D(di, dj) = Dp(u + di, v + dj); put(slot, ok, score)
+// receives every candidate.  Feasible-only (PEN = false): ok = feasibility
+// (capacity, and time windows in the T_V = 0 form of SlotTW), score = the
+// distance delta dD (Eq. 2, 13, 14).  Penalised (PEN, CVRP; records with the old
+// excess folded in, see SlotRec): ok = the candidate is structurally valid (no
+// poisoned load), score = dD + w_Q (max(L_a' - Q, 0) + max(L_b' - Q, 0)) - w_Q
+// (ex_a + ex_b) = dD + w_Q dL_V (Eq. 16a, reading 4).
+template <bool TW, bool PEN, uint32_t MASK, class DF, class PF>
 __device__ __forceinline__ void cell_streams(const SlotRec &A, const SlotRec &V, const SlotTW &AT, const SlotTW &VT,
-                                             int32_t cap, DF D, PF put) {
+                                             int32_t cap, int32_t wQ, DF D, PF put) {
+    static_assert(!(TW && PEN), "penalised fast path: CVRP only");
+    constexpr int32_t kValid = kPoison / 2;   // any poisoned load exceeds it
+    // penalty of the two new route loads
+    auto pen = [&](int32_t la, int32_t lb) -> int32_t { return wQ * (max(la - cap, 0) + max(lb - cap, 0)); };
     // time-window check of  F + seg + B  (Eq. 4 in the T_V = 0 form of SlotTW):
     // start after ef + t1 <= seg latest start, completion + t2 <= suffix latest start
     auto tw3 = [&](float ef, int32_t t1, float sTE, float sTL, float sTD, int32_t t2, float lb) -> bool {
@@ -106,10 +114,14 @@ __device__ __forceinline__ void cell_streams(const SlotRec &A, const SlotRec &V,
         const int32_t d01 = D(0, 1), d10 = D(1, 0);
         const int32_t dD = d01 + d10 + A.ne + V.ne;
         const int32_t la = A.fL + V.bL1, lb = V.fL + A.bL1;
-        bool ok = max(la, lb) <= cap;
-        if (TW) ok = ok & (AT.EF + static_cast<float>(d01) <= VT.LBN[0]) &
-                     (VT.EF + static_cast<float>(d10) <= AT.LBN[0]);
-        put(0, ok, dD);
+        if (PEN) {
+            put(0, max(la, lb) < kValid, dD + pen(la, lb));
+        } else {
+            bool ok = max(la, lb) <= cap;
+            if (TW) ok = ok & (AT.EF + static_cast<float>(d01) <= VT.LBN[0]) &
+                         (VT.EF + static_cast<float>(d10) <= AT.LBN[0]);
+            put(0, ok, dD);
+        }
     }
     // ---- relocate / or-opt, both directions                   (Eq. 13)
 #pragma unroll
@@ -117,13 +129,19 @@ __device__ __forceinline__ void cell_streams(const SlotRec &A, const SlotRec &V,
         if (!(MASK & (1u << (1 + N)))) continue;
         const int32_t d00 = D(0, 0), dN1 = D(N - 1, 1), d1N = D(1, N - 1);
         const int32_t d1 = A.rem[N - 1] + d00 + dN1 + V.ne;  // seg(u) after v
-        bool ok1 = V.W + A.so[N - 1] <= cap;
-        if (TW) ok1 = ok1 & tw3(VT.EF, d00, AT.sTE[N - 1], AT.sTL[N - 1], AT.sTD[N - 1], dN1, VT.LBN[0]);
-        put(2 * N - 1, ok1, d1);
         const int32_t d2 = V.rem[N - 1] + d00 + d1N + A.ne;  // seg(v) after u
-        bool ok2 = A.W + V.so[N - 1] <= cap;
-        if (TW) ok2 = ok2 & tw3(AT.EF, d00, VT.sTE[N - 1], VT.sTL[N - 1], VT.sTD[N - 1], d1N, AT.LBN[0]);
-        put(2 * N, ok2, d2);
+        if (PEN) {
+            const int32_t lb1 = V.W + A.so[N - 1], lb2 = A.W + V.so[N - 1];
+            put(2 * N - 1, lb1 < kValid, d1 + pen(A.W - A.so[N - 1], lb1));
+            put(2 * N, lb2 < kValid, d2 + pen(lb2, V.W - V.so[N - 1]));
+        } else {
+            bool ok1 = V.W + A.so[N - 1] <= cap;
+            if (TW) ok1 = ok1 & tw3(VT.EF, d00, AT.sTE[N - 1], AT.sTL[N - 1], AT.sTD[N - 1], dN1, VT.LBN[0]);
+            put(2 * N - 1, ok1, d1);
+            bool ok2 = A.W + V.so[N - 1] <= cap;
+            if (TW) ok2 = ok2 & tw3(AT.EF, d00, VT.sTE[N - 1], VT.sTL[N - 1], VT.sTD[N - 1], d1N, AT.LBN[0]);
+            put(2 * N, ok2, d2);
+        }
     }
     // ---- swap (1,1) / cross-exchange (N1,N2), N1 <= N2
 #pragma unroll
@@ -136,21 +154,29 @@ __device__ __forceinline__ void cell_streams(const SlotRec &A, const SlotRec &V,
             const int32_t a = D(-1, 0), bq = D(N1, N2 - 1), c = D(0, -1), dq = D(N1 - 1, N2);
             const int32_t dD = a + bq + c + dq + A.sE[N1 - 1] + V.sE[N2 - 1];
             const int32_t la = A.sA[N1 - 1] + V.sS[N2 - 1], lb = V.sA[N2 - 1] + A.sS[N1 - 1];
-            bool ok = max(la, lb) <= cap;
-            if (TW)  // A' = F(u-1) + S(v,N2) + B(u+N1),  B' = F(v-1) + S(u,N1) + B(v+N2)
-                ok = ok & tw3(AT.EFm, a, VT.sTE[N2 - 1], VT.sTL[N2 - 1], VT.sTD[N2 - 1], bq, AT.LBN[N1 - 1]) &
-                     tw3(VT.EFm, c, AT.sTE[N1 - 1], AT.sTL[N1 - 1], AT.sTD[N1 - 1], dq, VT.LBN[N2 - 1]);
-            put(slot[sv], ok, dD);
+            if (PEN) {
+                put(slot[sv], max(la, lb) < kValid, dD + pen(la, lb));
+            } else {
+                bool ok = max(la, lb) <= cap;
+                if (TW)  // A' = F(u-1) + S(v,N2) + B(u+N1),  B' = F(v-1) + S(u,N1) + B(v+N2)
+                    ok = ok & tw3(AT.EFm, a, VT.sTE[N2 - 1], VT.sTL[N2 - 1], VT.sTD[N2 - 1], bq, AT.LBN[N1 - 1]) &
+                         tw3(VT.EFm, c, AT.sTE[N1 - 1], AT.sTL[N1 - 1], AT.sTD[N1 - 1], dq, VT.LBN[N2 - 1]);
+                put(slot[sv], ok, dD);
+            }
         }
         if (N1 != N2) {   // N1-segment at v, N2-segment at u
             const int32_t c = D(0, -1), bq = D(N2 - 1, N1), a = D(-1, 0), dq = D(N2, N1 - 1);
             const int32_t dD = c + bq + a + dq + V.sE[N1 - 1] + A.sE[N2 - 1];
             const int32_t lb = V.sA[N1 - 1] + A.sS[N2 - 1], la = A.sA[N2 - 1] + V.sS[N1 - 1];
-            bool ok = max(la, lb) <= cap;
-            if (TW)  // B' = F(v-1) + S(u,N2) + B(v+N1),  A' = F(u-1) + S(v,N1) + B(u+N2)
-                ok = ok & tw3(VT.EFm, c, AT.sTE[N2 - 1], AT.sTL[N2 - 1], AT.sTD[N2 - 1], bq, VT.LBN[N1 - 1]) &
-                     tw3(AT.EFm, a, VT.sTE[N1 - 1], VT.sTL[N1 - 1], VT.sTD[N1 - 1], dq, AT.LBN[N2 - 1]);
-            put(slot[sv] + 1, ok, dD);
+            if (PEN) {
+                put(slot[sv] + 1, max(la, lb) < kValid, dD + pen(la, lb));
+            } else {
+                bool ok = max(la, lb) <= cap;
+                if (TW)  // B' = F(v-1) + S(u,N2) + B(v+N1),  A' = F(u-1) + S(v,N1) + B(u+N2)
+                    ok = ok & tw3(VT.EFm, c, AT.sTE[N2 - 1], AT.sTL[N2 - 1], AT.sTD[N2 - 1], bq, VT.LBN[N1 - 1]) &
+                         tw3(AT.EFm, a, VT.sTE[N1 - 1], VT.sTL[N1 - 1], VT.sTD[N1 - 1], dq, AT.LBN[N2 - 1]);
+                put(slot[sv] + 1, ok, dD);
+            }
         }
     }
 }
@@ -184,7 +210,7 @@ __device__ __forceinline__ bool stream_direct(int k) {
     return (k == 0 || k == 7 || k == 12 || k == 15) ? true : (k <= 6 ? (k & 1) == 1 : (k == 8 || k == 10 || k == 13));
 }
 
-template <int U, bool TW, uint32_t MASK, bool DUMP, class ItemF>
+template <int U, bool TW, uint32_t MASK, bool DUMP, bool PEN, class ItemF>
 __device__ __forceinline__ void fast_body(ItemF item, int w0, int w1, int wstride, uint64_t *bar,
                                           unsigned long long (*red)[23], unsigned char *sm, int32_t cap,
                                           const SolView<int32_t> &SV, const ScoreParams &sp, uint32_t imask,
@@ -326,7 +352,7 @@ __device__ __forceinline__ void fast_body(ItemF item, int w0, int w1, int wstrid
             if (ru < 0) continue;            // warp-uniform: end depot / spare / padding row
             if (!(ru < V.r)) continue;       // pair must span two routes, route(u) < route(v)
             const SlotTW &AT = TR[TW ? i : 0];
-            cell_streams<TW, MASK>(A, V, AT, VT, cap, [&](int di, int dj) { return D(i, di, dj); },
+            cell_streams<TW, PEN, MASK>(A, V, AT, VT, cap, sp.wQ, [&](int di, int dj) { return D(i, di, dj); },
                                    [&](int k, bool ok, int32_t dD) {
                                        keep(run[k], ok, dD, i, mul32);
                                        if constexpr (DUMP) {   // test-only: every candidate's key
@@ -386,7 +412,7 @@ __device__ __forceinline__ void fast_body(ItemF item, int w0, int w1, int wstrid
 // in two halves of similar work so that small neighbourhoods get twice the CTAs
 // (and each CTA half the registers' worth of running minima); the intra-route
 // work rides with the second half.
-template <int U, bool TW, uint32_t MASK, uint32_t MASK2, bool DUMP = false>
+template <int U, bool TW, uint32_t MASK, uint32_t MASK2, bool DUMP = false, bool PEN = false>
 __global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__restrict__ rec,
                                                              const SlotTW *__restrict__ rectw,
                                                              const __grid_constant__ CUtensorMap tmap,
@@ -417,11 +443,11 @@ __global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__re
     };
     if (MASK2 == 0 || cta < split) {
         const int n = MASK2 ? split : static_cast<int>(gridDim.x);
-        fast_body<U, TW, MASK, DUMP>(item, t_lo + cta, t_hi, n, bar, red, sm, cap, SV, sp, MASK2 ? 0u : imask, x_lo,
+        fast_body<U, TW, MASK, DUMP, PEN>(item, t_lo + cta, t_hi, n, bar, red, sm, cap, SV, sp, MASK2 ? 0u : imask, x_lo,
                                      x_hi, cta, n, flags, keys, dump);
     } else {
         const int n = static_cast<int>(gridDim.x) - split;
-        fast_body<U, TW, MASK2, DUMP>(item, t_lo + cta - split, t_hi, n, bar, red, sm, cap, SV, sp, imask, x_lo, x_hi,
+        fast_body<U, TW, MASK2, DUMP, PEN>(item, t_lo + cta - split, t_hi, n, bar, red, sm, cap, SV, sp, imask, x_lo, x_hi,
                                       cta - split, n, flags, keys, dump);
     }
     if ((flags & 2) && tid == 0 && blockIdx.x < 4096) g_inter_probe[8 * blockIdx.x + 3] = gtime();
@@ -433,12 +459,12 @@ static bool inter_probe_on() {
 }
 
 // resident CTAs (whole GPU) of one instantiation with one / two pipeline stages
-template <int U, bool TW, uint32_t MASK, uint32_t MASK2>
+template <int U, bool TW, uint32_t MASK, uint32_t MASK2, bool PEN>
 static void fast_capacity(int &res1, int &res2) {
     static PerDevice pd;
     static int r1[kMaxDevices], r2[kMaxDevices];
     const int d = once_per_device(pd, [](int dev) {
-        auto kern = k_inter_fast<U, TW, MASK, MASK2>;
+        auto kern = k_inter_fast<U, TW, MASK, MASK2, false, PEN>;
         using G = FastGeom<U, TW>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::Smem);
         int sms = 0, b1 = 0, b2 = 0;
@@ -452,16 +478,16 @@ static void fast_capacity(int &res1, int &res2) {
     res2 = r2[d];
 }
 
-template <int U, bool TW, uint32_t MASK, uint32_t MASK2>
+template <int U, bool TW, uint32_t MASK, uint32_t MASK2, bool PEN>
 static cudaError_t launch_fast_t(const SlotRec *rec, const SlotTW *rectw, const CUtensorMap &map, const uint32_t *tiles,
                                  int t_lo, int t_hi, uint32_t Qc, int32_t cap, uint64_t *keys, int units_max,
                                  cudaStream_t st, const SolView<int32_t> &SV, const ScoreParams &sp, uint32_t imask,
                                  int x_lo, int x_hi) {
-    auto kern = k_inter_fast<U, TW, MASK, MASK2>;
+    auto kern = k_inter_fast<U, TW, MASK, MASK2, false, PEN>;
     using G = FastGeom<U, TW>;
     // resident CTAs with one / two pipeline stages (a persistent grid never exceeds them)
     int res1 = 0, res2 = 0;
-    fast_capacity<U, TW, MASK, MASK2>(res1, res2);
+    fast_capacity<U, TW, MASK, MASK2, PEN>(res1, res2);
     const int groups = MASK2 ? 2 : 1;
     const int tiles_n = t_hi - t_lo;
     const int units = imask ? (x_hi - x_lo + 3) / 4 : 0;
@@ -483,7 +509,7 @@ static cudaError_t launch_fast_t(const SlotRec *rec, const SlotTW *rectw, const 
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 
-template <int U, bool TW>
+template <int U, bool TW, bool PEN = false>
 static cudaError_t launch_fast_u(uint32_t mask, const SlotRec *rec, const SlotTW *rectw, const CUtensorMap &map,
                                  const uint32_t *tiles,
                                  int t_lo, int t_hi, uint32_t Qc, int32_t cap, uint64_t *keys, int max_grid,
@@ -494,7 +520,7 @@ static cudaError_t launch_fast_u(uint32_t mask, const SlotRec *rec, const SlotTW
     // the intra-route work rides along with the first launch
     auto run = [&](auto kmask, auto kmask2) {
         if (err != cudaSuccess) return;
-        err = launch_fast_t<U, TW, decltype(kmask)::value, decltype(kmask2)::value>(
+        err = launch_fast_t<U, TW, decltype(kmask)::value, decltype(kmask2)::value, PEN>(
             rec, rectw, map, tiles, t_lo, t_hi, Qc, cap, keys, max_grid, st, SV, sp, imask, x_lo, x_hi);
         imask = 0;
     };
@@ -507,7 +533,7 @@ static cudaError_t launch_fast_u(uint32_t mask, const SlotRec *rec, const SlotTW
         // (small neighbourhoods: twice the CTAs); above that the halves would pay the
         // per-tile loads and folds twice
         int r1 = 0, r2 = 0;
-        fast_capacity<U, TW, HA, HB>(r1, r2);
+        fast_capacity<U, TW, HA, HB, PEN>(r1, r2);
         if (2 * (t_hi - t_lo) <= r1)
             run(std::integral_constant<uint32_t, HA>{}, std::integral_constant<uint32_t, HB>{});
         else
@@ -554,7 +580,7 @@ __global__ void __launch_bounds__(kFastThreads) k_inter_fast_batch(const FastSol
                         static_cast<int>(c & 0x3FFu)};
     };
     const SolView<int32_t> none{};
-    fast_body<U, TW, MASK, false>(item, w0, w1, 1, bar, red, sm, cap, none, sp, 0u, 0, 0, 0, 1, flags);
+    fast_body<U, TW, MASK, false, false>(item, w0, w1, 1, bar, red, sm, cap, none, sp, 0u, 0, 0, 0, 1, flags);
 }
 
 template <int U, bool TW, uint32_t MASK>
@@ -663,7 +689,7 @@ __global__ void __launch_bounds__(256) k_etga(const SlotRec *__restrict__ rec, c
         const uint32_t idx_d = static_cast<uint32_t>(u) * Qc + static_cast<uint32_t>(v);
         const uint32_t idx_r = static_cast<uint32_t>(v) * Qc + static_cast<uint32_t>(u);
         // slot -> (variant, direction) of the stream layout
-        cell_streams<TW, CM>(A, V, AT, VT, cap, D, [&](int k, bool ok, int32_t dD) {
+        cell_streams<TW, false, CM>(A, V, AT, VT, cap, 0, D, [&](int k, bool ok, int32_t dD) {
             const int var = stream_variant(k);
             const bool direct = stream_direct(k);
             if (ok) acc[var] = umin64(acc[var], pack_key(ord_score(dD), direct ? idx_d : idx_r));
@@ -758,14 +784,14 @@ cudaError_t launch_etga(uint32_t mask, bool tw, const EtgaArgs &a, cudaStream_t 
 
 // test-only: the DUMP instantiation of the all-variant fused sweep (U = 16), every
 // candidate's key stored in dump (tga_debug_eval_dump); same tile plan and body
-template <bool TW>
+template <bool TW, bool PEN>
 static cudaError_t launch_fast_dump_t(const SlotRec *rec, const SlotTW *rectw, const CUtensorMap &map,
                                       const uint32_t *tiles, int t_lo, int t_hi, uint32_t Qc, int32_t cap,
                                       uint64_t *keys, cudaStream_t st, const SolView<int32_t> &SV,
                                       const ScoreParams &sp, uint32_t imask, int x_lo, int x_hi,
                                       unsigned long long *dump) {
     constexpr uint32_t ALL = 0x7FEu;
-    auto kern = k_inter_fast<16, TW, ALL, 0u, true>;
+    auto kern = k_inter_fast<16, TW, ALL, 0u, true, PEN>;
     using G = FastGeom<16, TW>;
     static PerDevice pd;
     once_per_device(pd, [&](int) { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::Smem); });
@@ -780,16 +806,25 @@ cudaError_t launch_inter_fast_dump(bool tw, const SlotRec *rec, const SlotTW *re
                                    const uint32_t *tiles, int t_lo, int t_hi, uint32_t Qc, int32_t cap, uint64_t *keys,
                                    cudaStream_t st, const SolView<int32_t> &SV, const ScoreParams &sp, uint32_t imask,
                                    int x_lo, int x_hi, unsigned long long *dump) {
-    return tw ? launch_fast_dump_t<true>(rec, rectw, map, tiles, t_lo, t_hi, Qc, cap, keys, st, SV, sp, imask, x_lo,
-                                         x_hi, dump)
-              : launch_fast_dump_t<false>(rec, rectw, map, tiles, t_lo, t_hi, Qc, cap, keys, st, SV, sp, imask, x_lo,
-                                          x_hi, dump);
+    if (sp.mode == 1)
+        return tw ? cudaErrorInvalidValue
+                  : launch_fast_dump_t<false, true>(rec, rectw, map, tiles, t_lo, t_hi, Qc, cap, keys, st, SV, sp, imask,
+                                                    x_lo, x_hi, dump);
+    return tw ? launch_fast_dump_t<true, false>(rec, rectw, map, tiles, t_lo, t_hi, Qc, cap, keys, st, SV, sp, imask, x_lo,
+                                                x_hi, dump)
+              : launch_fast_dump_t<false, false>(rec, rectw, map, tiles, t_lo, t_hi, Qc, cap, keys, st, SV, sp, imask,
+                                                 x_lo, x_hi, dump);
 }
 
 cudaError_t launch_inter_fast(int U, uint32_t mask, const SlotRec *rec, const SlotTW *rectw, const CUtensorMap &map,
                               const uint32_t *tiles, int t_lo, int t_hi, uint32_t Qc, int32_t cap, uint64_t *keys,
                               int max_grid, cudaStream_t st, const SolView<int32_t> &SV, const ScoreParams &sp,
                               uint32_t imask, int x_lo, int x_hi) {
+    if (sp.mode == 1) {   // penalised records (CVRP): U = 16 tiles
+        if (rectw) return cudaErrorInvalidValue;
+        return launch_fast_u<16, false, true>(mask, rec, rectw, map, tiles, t_lo, t_hi, Qc, cap, keys, max_grid, st, SV,
+                                              sp, imask, x_lo, x_hi);
+    }
     if (rectw)
         return U == 8 ? launch_fast_u<8, true>(mask, rec, rectw, map, tiles, t_lo, t_hi, Qc, cap, keys, max_grid, st, SV,
                                                sp, imask, x_lo, x_hi)

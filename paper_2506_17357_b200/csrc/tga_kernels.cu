@@ -289,20 +289,24 @@ __device__ __forceinline__ void scan_rec_pass(const ScanArgs<DT> &A, const int r
                     w.pad[0] = w.pad[1] = 0.f;
                     A.rectw[x] = w;
                 }
+                // penalised records: the route's old load excess, weighted (SlotRec)
+                const int32_t pex = A.pen_wQ * max(Wr - A.capacity, 0);
+                q.ne -= pex;
 #pragma unroll
                 for (int N = 1; N <= 3; ++N) {
                     const bool segok = (k >= 1) && (k + N - 1 <= L);
                     const int32_t sN = segok ? A.fwdL[x + N - 1] - fl_prev : 0;
                     const int32_t eout = segok ? A.enext[x + N - 1] : 0;
                     // route a after removing the segment: F(x-1) + B(x+N) must stay feasible
-                    bool rem_ok = segok && Wr - sN <= A.capacity;
+                    // (feasible-only records; penalised records price the excess instead)
+                    bool rem_ok = segok && (A.pen_wQ || Wr - sN <= A.capacity);
                     if (TW && A.rectw && segok)
                         rem_ok = rem_ok && (w.EFm + static_cast<float>(br[N - 1]) <= LBof(x + N));
                     q.so[N - 1] = rem_ok ? sN : kPoison;
-                    q.rem[N - 1] = segok ? br[N - 1] - e_prev - eout : 0;
+                    q.rem[N - 1] = segok ? br[N - 1] - e_prev - eout - pex : 0;
                     q.sA[N - 1] = segok ? Wr - sN : kPoison;
                     q.sS[N - 1] = sN;
-                    q.sE[N - 1] = segok ? -e_prev - eout : 0;
+                    q.sE[N - 1] = segok ? -e_prev - eout - pex : 0;
                 }
                 A.rec[x] = q;
             }
@@ -809,10 +813,14 @@ __device__ __forceinline__ void inter_tile(const SolView<DT> &S, const DT *__res
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // Dp(x, y) from the staged box
     auto Dt = [&](int x, int y) -> DT { return tile[(x - u0 + 1) * BW + (y - v0 + kBoxX0)]; };
-    // fold one candidate key into the variant's running best (+ the test-only dump)
-    auto take = [&](int var, uint64_t k, uint32_t idx) {
+    // fold one candidate key into the variant's running best (+ the test-only dump; only
+    // cells of the candidate space write it -- a cell with route(u) >= route(v) evaluates
+    // its streams masked, and its (v, u) mirror holds the real candidates)
+    auto take = [&](int var, uint64_t k, uint32_t idx, bool in_space) {
         best[var] = umin64(best[var], k);
-        if constexpr (DUMP) dump_put(dump, S.Qc * S.Qc, var, idx, k);
+        if constexpr (DUMP) {
+            if (in_space) dump_put(dump, S.Qc * S.Qc, var, idx, k);
+        }
     };
 #pragma unroll 1
     for (int j = 0; j < VPT; ++j) {
@@ -849,7 +857,7 @@ __device__ __forceinline__ void inter_tile(const SolView<DT> &S, const DT *__res
                     ta = tw_cat(S.fwdT[u], S.bwdT[v + 1], static_cast<float>(Dt(u, v + 1))).w;
                     tb = tw_cat(S.fwdT[v], S.bwdT[u + 1], static_cast<float>(Dt(u + 1, v))).w;
                 }
-                take(1, score_key<DT, TW>(sp, pair, dD, la, lb, Wa, Wb, ta, tb, TVa, TVb, idx_uv), idx_uv);
+                take(1, score_key<DT, TW>(sp, pair, dD, la, lb, Wa, Wb, ta, tb, TVa, TVb, idx_uv), idx_uv, pair);
             }
             // ---- relocate (N=1) / or-opt (N=2,3): both directions (Eq. 13)
 #pragma unroll
@@ -869,7 +877,7 @@ __device__ __forceinline__ void inter_tile(const SolView<DT> &S, const DT *__res
                         const TwRec X = tw_cat(S.fwdT[v], sg, static_cast<float>(Dt(u, v)));
                         tb = tw_cat(X, S.bwdT[v + 1], static_cast<float>(Dt(u + N - 1, v + 1))).w;
                     }
-                    take(1 + N, score_key<DT, TW>(sp, ok, dD, Wa - s, Wb + s, Wa, Wb, ta, tb, TVa, TVb, idx_uv), idx_uv);
+                    take(1 + N, score_key<DT, TW>(sp, ok, dD, Wa - s, Wb + s, Wa, Wb, ta, tb, TVa, TVb, idx_uv), idx_uv, pair);
                 }
                 {   // segment v..v+N-1 (route b) inserted after u (route a)
                     const bool ok = pair && pv >= 1 && pv + N - 1 <= Lb;
@@ -883,7 +891,7 @@ __device__ __forceinline__ void inter_tile(const SolView<DT> &S, const DT *__res
                         const TwRec X = tw_cat(S.fwdT[u], sg, static_cast<float>(Dt(u, v)));
                         ta = tw_cat(X, S.bwdT[u + 1], static_cast<float>(Dt(u + 1, v + N - 1))).w;
                     }
-                    take(1 + N, score_key<DT, TW>(sp, ok, dD, Wa + s, Wb - s, Wa, Wb, ta, tb, TVa, TVb, idx_vu), idx_vu);
+                    take(1 + N, score_key<DT, TW>(sp, ok, dD, Wa + s, Wb - s, Wa, Wb, ta, tb, TVa, TVb, idx_vu), idx_vu, pair);
                 }
             }
             // ---- swap (1,1) / cross-exchange (N1,N2) (3-Seq(N1,N2) P:346)
@@ -910,7 +918,7 @@ __device__ __forceinline__ void inter_tile(const SolView<DT> &S, const DT *__res
                         tb = tw_cat(B1, S.bwdT[v + N2], static_cast<float>(Dt(u + N1 - 1, v + N2))).w;
                     }
                     take(vid, score_key<DT, TW>(sp, ok, dD, Wa - sa + sb, Wb - sb + sa, Wa, Wb, ta, tb, TVa, TVb, idx_uv),
-                         idx_uv);
+                         idx_uv, pair);
                 }
                 if (N1 != N2) {   // N1-segment at v (route b), N2-segment at u (route a)
                     const bool ok = pair && pv >= 1 && pv + N1 - 1 <= Lb && pu >= 1 && pu + N2 - 1 <= La;
@@ -926,7 +934,7 @@ __device__ __forceinline__ void inter_tile(const SolView<DT> &S, const DT *__res
                         ta = tw_cat(A1, S.bwdT[u + N2], static_cast<float>(Dt(u + N2, v + N1 - 1))).w;
                     }
                     take(vid, score_key<DT, TW>(sp, ok, dD, Wa - sa + sb, Wb - sb + sa, Wa, Wb, ta, tb, TVa, TVb, idx_vu),
-                         idx_vu);
+                         idx_vu, pair);
                 }
             }
         }

@@ -66,6 +66,7 @@ struct ScanArgs {
     DT *rD;
     const int32_t *canon;
     int32_t capacity;
+    int32_t pen_wQ;    // penalised fast-path records: w_load (0 = feasible-only records)
     SlotRec *rec;      // CVRP fast-path records (int DT only); may be null
     SlotTW *rectw;     // VRPTW (TW-I) fast-path records; may be null
 };

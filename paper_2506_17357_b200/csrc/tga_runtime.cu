@@ -105,6 +105,7 @@ struct tga_instance {
     std::vector<float> hTw;
     int max_c_abs = 0;
     bool fast_ok = false;  // loads small enough for the poisoned-load fast path
+    bool fast_pen_ok = false;  // ... and penalised scores small enough for its 32-bit running minima
     // edge-based neighbourhood (ETGA): unordered customer pairs of the edge mask
     int theta = 0;
     int n_gpairs = 0;
@@ -338,6 +339,7 @@ static ScanArgs<DT> scan_args(tga_solution *s) {
     a.rD = static_cast<DT *>(s->d_rD);
     a.canon = s->canon;
     a.capacity = s->inst->Q;
+    a.pen_wQ = s->inst->opt.score_mode == TGA_SCORE_PENALISED ? s->inst->opt.w_load : 0;
     a.rec = s->rec;
     a.rectw = s->rectw;
     return a;
@@ -556,6 +558,7 @@ extern "C" int32_t tga_instance_create(int32_t n, const void *dist, int32_t dtyp
         for (int i = 0; i < n; ++i) tot += demand[i];
         // poisoned loads stay below 2^31; |delta| <= 8 max c < 2^25 fits the packed 32-bit keys
         I->fast_ok = tot < (kPoison >> 2) && capacity < (kPoison >> 2) && max_abs < (1 << 21);
+        I->fast_pen_ok = false;   // set below once the options are known
     }
     if (opt) I->opt = *opt;
     else { I->opt.score_mode = TGA_SCORE_FEASIBLE; I->opt.w_load = 10; I->opt.w_tw = 10; I->opt.device = -1; }
@@ -583,6 +586,13 @@ extern "C" int32_t tga_instance_create(int32_t n, const void *dist, int32_t dtyp
             delete I;
             return fail(TGA_ERR_INVALID_ARGUMENT, "integer score range exceeds int32 (distances, demands or "
                                                   "penalty weights too large; use TGA_F32)");
+        }
+        // penalised CVRP on the fast path: |score| <= 8 max c + w_load x 2 x total demand < 2^25
+        // (the packed 32-bit running minima of the tile body), non-negative weight
+        if (I->opt.score_mode == TGA_SCORE_PENALISED && !tw && I->opt.w_load >= 0) {
+            double tot = 0;
+            for (int i = 0; i < n; ++i) tot += demand[i];
+            I->fast_pen_ok = I->fast_ok && 8.0 * max_abs + 2.0 * I->opt.w_load * tot < 33554432.0;
         }
     }
     if (I->opt.device < 0) cudaGetDevice(&I->device);
@@ -714,9 +724,12 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
     void *v_rec = nullptr, *v_ftiles = nullptr, *v_rectw = nullptr, *v_slot_of = nullptr;
     s->fastU = 16;  // U = 8 measured no better at n = 1000 (more tiles, more per-tile overhead)
     if (const char *ev = std::getenv("TGA_FAST_U")) s->fastU = std::atoi(ev) == 8 ? 8 : 16;  // tuning override
+    if (I->opt.score_mode == TGA_SCORE_PENALISED) s->fastU = 16;   // the penalised tile body is built for U = 16
     const size_t ftiles_max = static_cast<size_t>(s->pitch / s->fastU) * (s->pitch / kFastTV) + 1;
     // fast path: integer distances (CVRP, or VRPTW TW-I), feasible-only scoring
-    const bool want_fast = I->dtype == TGA_I32 && I->opt.score_mode == TGA_SCORE_FEASIBLE && I->fast_ok;
+    // fast path: integer distances; feasible-only (CVRP or VRPTW TW-I) or penalised CVRP
+    const bool want_fast = I->dtype == TGA_I32 && I->fast_ok &&
+                           (I->opt.score_mode == TGA_SCORE_FEASIBLE || I->fast_pen_ok);
     Item items[] = {
         {&v_node, cap * 4}, {&v_route, cap * 4}, {&v_pos, cap * 4}, {&v_rlen, cap * 4}, {&v_canon, cap * 4},
         {&v_fwdL, cap * 4}, {&v_bwdL, cap * 4}, {&v_en, cap * 4}, {&v_fD, cap * 4}, {&v_bD, cap * 4},
@@ -945,7 +958,7 @@ extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
     }
     if (timed) TGA_CUDA(cudaEventRecordWithFlags(s->tev[s->tev_n], st, rec_flags));
     const bool etga = I->theta > 0;
-    if (etga && !(I->dtype == TGA_I32 && s->fast))
+    if (etga && !(I->dtype == TGA_I32 && s->fast && I->opt.score_mode == TGA_SCORE_FEASIBLE))
         return fail(TGA_ERR_UNSUPPORTED, "edge-based neighbourhood: integer feasible-only fast path only");
     if (etga) {
         // ETGA: node -> slot map, then the cells the edge mask keeps; the
@@ -1679,7 +1692,8 @@ extern "C" int32_t tga_batch_load(tga_instance *I, int32_t n_sol, const int32_t 
         std::vector<uint32_t> fw;
         for (int k = 0; k < n_sol && ok; ++k) {
             tga_solution *s = b->sols[k];
-            ok = s->fast && s->rec && (!I->tw || s->rectw) && s->fastU == 16 && s->pitch / 16 < 1024;
+            ok = s->fast && s->rec && (!I->tw || s->rectw) && s->fastU == 16 && s->pitch / 16 < 1024 &&
+                 I->opt.score_mode == TGA_SCORE_FEASIBLE;   // the batch tile body is feasible-only
             if (!ok) break;
             fs[k] = FastSol{s->rec, s->rectw, b->d_keys + static_cast<size_t>(k) * TGA_N_VARIANTS,
                             static_cast<uint32_t>(s->pitch), 0};

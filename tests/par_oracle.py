@@ -21,7 +21,7 @@ def n_workers() -> int:
     return max(1, len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1))
 
 
-def best_keys(orc: O.Oracle, routes, variants, mode=0, chunks_per_variant=None, mask=None):
+def best_keys(orc: O.Oracle, routes, variants, mode=0, chunks_per_variant=None, mask=None, wQ=10.0, wT=10.0):
     """{variant: (score, u * Q + v) or None, ...} over the full neighbourhood,
     plus {variant: total candidates}."""
     Q = O.canonical_q(routes)
@@ -33,7 +33,7 @@ def best_keys(orc: O.Oracle, routes, variants, mode=0, chunks_per_variant=None, 
 
     def run(job):
         v, lo, hi = job
-        return v, orc.best_move(ptr_cust, v, mode=mode, u_lo=lo, u_hi=hi, mask=mask)
+        return v, orc.best_move(ptr_cust, v, mode=mode, wQ=wQ, wT=wT, u_lo=lo, u_hi=hi, mask=mask)
 
     best = {v: None for v in variants}
     count = {v: 0 for v in variants}

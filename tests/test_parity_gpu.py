@@ -393,15 +393,15 @@ def test_batch_full_population_1024():
 
 
 # ---------------------------------------------------------------- large CVRP (config 4)
-def check_exact_parallel(inst, routes, variants, mode=0, label="", gs=None):
+def check_exact_parallel(inst, routes, variants, mode=0, label="", gs=None, wQ=10, wT=10):
     """GPU keys of every variant == the oracle's GLOBAL best over the whole
     neighbourhood, enumerated row-parallel on every host core (tests/par_oracle)."""
     if gs is None:
-        gs = T.Solution(T.Instance.from_gen(inst, score_mode=mode), routes)
+        gs = T.Solution(T.Instance.from_gen(inst, score_mode=mode, w_load=wQ, w_tw=wT), routes)
     gs.eval(sum(1 << v for v in variants))
     got = gpu_keys(gs, integer=True)
     orc = O.Oracle.from_instance(inst)
-    exp, count = par_oracle.best_keys(orc, routes, variants, mode)
+    exp, count = par_oracle.best_keys(orc, routes, variants, mode, wQ=float(wQ), wT=float(wT))
     c = gs.counts()
     for v in variants:
         assert got[v] == exp[v], f"{label} variant {v} ({T.VARIANT_NAMES[v]}): gpu {got[v]} oracle {exp[v]}"
@@ -800,3 +800,50 @@ def test_integer_score_range_guard():
     with pytest.raises(T.TgaError):
         T.Instance(inst.dist, inst.demand, inst.capacity, score_mode=T.SCORE_PENALISED, w_load=2 ** 28)
     T.Instance(inst.dist.astype(np.float32) * 2.0 ** 26, inst.demand, inst.capacity)   # float path accepted
+
+
+# ---------------------------------------------------------------- penalised score (Eq. 16a) at full size
+@pytest.mark.parametrize("name", ["cfg2", "ns2000", "cfg3"])
+def test_penalised_full_size_exact(name):
+    """Penalised mode (score = dD + w_Q dL_V (+ w_T dT_V), Eq. 16a, DESIGN.md
+    reading 4) at full size: CVRP on the fused fast path (penalised records),
+    VRPTW on the generic tile kernel; every variant == the oracle's global best."""
+    _need_gpu()
+    inst, sol = G.config(name)
+    variants = ALLV if inst.tw is None else INTER + INTRA_TW
+    check_exact_parallel(inst, sol.routes, variants, 1, f"{name}-pen")
+    # an infeasible state (overloaded routes) makes the penalty terms bite
+    check_exact_parallel(inst, G.perturb(sol, 60, 11).routes, variants, 1, f"{name}-pen-perturbed")
+
+
+def test_penalised_generic_multi_tile():
+    """The generic tile kernel (penalised VRPTW) with more tiles than resident
+    CTAs, so its double-buffered persistent tile loop runs (n = 3000, R2 shape)."""
+    _need_gpu()
+    inst, sol = G.gh_like(8, n=3000, kind="R2")
+    sol = G.perturb(sol, 40, 8)
+    # w_T = 1: with 3000 customers the int32 score-range guard rejects w_T = 10
+    gs = T.Solution(T.Instance.from_gen(inst, score_mode=1, w_load=10, w_tw=1), sol)
+    R, N, _, _ = gs.info()
+    assert (N + 4 * R) // 32 * ((N + 4 * R) // 64) // 2 > 4 * 148, "must exceed one tile per CTA"
+    check_exact_parallel(inst, sol.routes, INTER + INTRA_TW, 1, "tw-pen-3000", gs=gs, wQ=10, wT=1)
+
+
+@pytest.mark.parametrize("name", ["cvrp", "cvrp-slack0"])
+def test_penalised_device_steps_lockstep(name):
+    """Penalised CVRP: device-resident steps (fast path + on-device pick/update)
+    follow the host-driven steps; keys equal a fresh load afterwards."""
+    _need_gpu()
+    inst, sol = G.x_like(13, n=400, target_routes=17)
+    sol = G.perturb(sol, 30, 13)
+    gi = T.Instance.from_gen(inst, score_mode=1, slack=-1 if name.endswith("0") else 0)
+    host, dev = T.Solution(gi, sol), T.Solution(gi, sol)
+    for k in range(30):
+        host.step(T.OP_ALL)
+        dev.step_async(T.OP_ALL)
+        if k % 10 == 9:
+            assert dev.routes() == host.routes(), k
+    fresh = T.Solution(gi, dev.routes())
+    for s in (dev, fresh):
+        s.eval(T.OP_ALL)
+    np.testing.assert_array_equal(dev.keys(), fresh.keys())

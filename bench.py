@@ -50,6 +50,9 @@ for _v in range(14, 23):
 # F + seg + B, the Eq. 4 check in T_V = 0 form: 2-opt* two
 # (add + compare) checks, relocate one 6-op check per direction, swap/cross two.
 ALG_OPS_TW = {1: 14, 2: 17, 3: 17, 4: 17, 5: 30, 6: 30, 7: 30, 8: 30, 9: 30, 10: 30}
+# penalised CVRP (score = dD + w_Q dL_V, Eq. 16a): the validity compare replaces the
+# capacity compare, plus two clamped excesses, their sum and the weighted add (4 ops)
+ALG_OPS_PEN = {v: (ALG_OPS[v] + 4 if 1 <= v <= 10 else ALG_OPS[v]) for v in ALG_OPS}
 
 
 def parse():
@@ -62,6 +65,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-per-op", action="store_true")
+    ap.add_argument("--score", choices=["feasible", "penalised"], default="feasible",
+                    help="score mode (DESIGN.md reading 4): feasible-only or penalised dD + w_Q dL_V (+ w_T dT_V)")
     ap.add_argument("--granular", type=int, default=0,
                     help="theta > 0: edge-based neighbourhood (ETGA, P:390-401) with granularity threshold theta")
     ap.add_argument("--shard", choices=["replicas", "rows"], default="replicas",
@@ -386,7 +391,8 @@ def run_tga(args):
 
     inst, sol0 = G.config(args.config, args.seed)
     stream = torch.cuda.Stream(device=dev)
-    gi = T.Instance.from_gen(inst, granular_theta=args.granular)
+    score_mode = 1 if args.score == "penalised" else 0
+    gi = T.Instance.from_gen(inst, granular_theta=args.granular, score_mode=score_mode)
     row_shard = ws > 1 and args.shard == "rows"
     # Cold-cache timing without flush nodes: R replicas of the workload's
     # solution (separate device state each) stepped round-robin, so that
@@ -523,7 +529,7 @@ def run_tga(args):
         _, _, n_pairs = gi.info()
         recs = 2 * 80 + (2 * 64 if inst.tw is not None else 0)
         alg_bytes = (n_pairs * (20 * 4 + recs) + (N * R + R * (R - 1) / 2.0) * (6 * 4 + recs)) / shard_div
-    ops_tab = ALG_OPS if inst.tw is None else ALG_OPS_TW
+    ops_tab = (ALG_OPS_PEN if score_mode else ALG_OPS) if inst.tw is None else ALG_OPS_TW
     alg_ops = float(sum(int(dev_counts[v]) * ops_tab[v] for v in inter_sel)) / K / shard_div
     sm_mhz_peak = float(pk.get("sm_max_mhz", 1965.0))
     alu_peak = 148 * 128 * sm_mhz_peak * 1e6            # lane-ops/s (4 SMSP x 32 lanes x 1 issue/clk)
@@ -638,6 +644,7 @@ def run_tga(args):
         "data": "synthetic",
         "config": {"workload": f"{args.config}: {G.CONFIGS.get(args.config, args.config)}; "
                                + (f"edge-based neighbourhood (ETGA) theta={args.granular}; " if args.granular else "")
+                               + ("penalised score dD + 10 dL_V (+ 10 dT_V); " if score_mode else "")
                                + "step = eval all variants + best move + apply",
                    "customers": N, "routes": R, "canonical_slots": Qc, "seed": args.seed,
                    "l2": (f"inputs larger than L2: {n_rep} replicas of the solution stepped round-robin "

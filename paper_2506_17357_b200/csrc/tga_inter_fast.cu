@@ -185,6 +185,24 @@ __device__ __forceinline__ void cell_streams(const SlotRec &A, const SlotRec &V,
 #define TGA_FAST_CTA_SYNC 0   // 1: the former __syncthreads per tile before a stage is refilled
 #endif
 
+// The fast-path tile plan of one solution, decoded arithmetically (no plan table to
+// load before the first TMA can be issued): tiles of U rows x kFastTV columns of the
+// upper triangle, R = kFastTV / U row bands per column band.  Tiles t < nI are the
+// diagonal tiles (row band I = t, column band I / R; the lightest, so one-tile-per-CTA
+// launches put the intra-route units beside them), then the full tiles (I < R J)
+// column by column: before column J lie R J (J - 1) / 2 of them.  fast_plan (host)
+// lists the same order; tile (I, J) exists iff I U < Qp, J kFastTV < Qp and
+// I U < J kFastTV + kFastTV - 1.
+__host__ __device__ __forceinline__ void fast_tile_of(int t, int nI, int R, int &I, int &J) {
+    if (t < nI) { I = t; J = t / R; return; }
+    const int q = t - nI;
+    int j = static_cast<int>((1.0f + sqrtf(1.0f + 8.0f * static_cast<float>(q) / static_cast<float>(R))) * 0.5f);
+    while (j > 1 && R * j * (j - 1) / 2 > q) --j;
+    while (R * (j + 1) * j / 2 <= q) ++j;
+    J = j;
+    I = q - R * j * (j - 1) / 2;
+}
+
 // one work item of the fused sweep: tile (I, J) of one solution
 struct FastItem {
     const SlotRec *rec;
@@ -437,9 +455,12 @@ __global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__re
     __syncthreads();
     pdl_wait();                       // Dp / records / keys are written by the stream predecessors
     const int cta = static_cast<int>(blockIdx.x);
+    const int nI = (SV.Qp + U - 1) / U;
+    (void)tiles;
     auto item = [&](int t) -> FastItem {
-        const uint32_t ij = tiles[t];
-        return FastItem{rec, rectw, &tmap, keys, Qc, 0, static_cast<int>(ij >> 16), static_cast<int>(ij & 0xFFFF)};
+        int I, J;
+        fast_tile_of(t, nI, kFastTV / U, I, J);
+        return FastItem{rec, rectw, &tmap, keys, Qc, 0, I, J};
     };
     if (MASK2 == 0 || cta < split) {
         const int n = MASK2 ? split : static_cast<int>(gridDim.x);
@@ -837,6 +858,16 @@ cudaError_t launch_inter_fast(int U, uint32_t mask, const SlotRec *rec, const Sl
 }
 
 }  // namespace tga
+
+// host-side decode of the fast-path tile order (tests: a bijection onto the plan set)
+extern "C" int32_t tga_debug_fast_tile(int32_t t, int32_t nI, int32_t R, int32_t *I, int32_t *J) {
+    if (!I || !J || R < 1 || nI < 0 || t < 0) return -1;
+    int i, j;
+    tga::fast_tile_of(t, nI, R, i, j);
+    *I = i;
+    *J = j;
+    return 0;
+}
 
 extern "C" int32_t tga_debug_inter_probe(uint64_t *out, int32_t n) {
     return cudaMemcpyFromSymbol(out, tga::g_inter_probe, sizeof(uint64_t) * static_cast<size_t>(n)) == cudaSuccess ? 0 : -5;

@@ -101,6 +101,7 @@ __device__ __forceinline__ void neighbourhood_counts(const DevState &S, uint32_t
         for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) v += wsum[w][tid];
         sums[tid] = v;
     }
+    __syncthreads();   // sums[] complete before any thread reads it (racecheck)
     if (tid < 23 && (mask & (1u << tid))) {  // one variant per thread
         const long long S1 = sums[0], S2 = sums[1];
         const int v = tid;

@@ -438,27 +438,19 @@ static int32_t refresh(tga_solution *s, bool full, int ra = -1, int rb = -1) {
     return TGA_OK;
 }
 
-// fast-path plan: fastU x kFastTV tiles (I << 16 | J) of the upper triangle
-// Ordered by increasing work (cells u < v < Qp of the tile; ties by position):
-// with one tile per CTA the intra-route units, which ride with the first CTAs,
-// land on the lightest tiles (diagonal and ragged ones); with several tiles per
-// CTA the grid-stride walk gives every CTA one tile of each weight band.
+// fast-path plan: fastU x kFastTV tiles (I << 16 | J) of the upper triangle, in the
+// order the tile kernel decodes arithmetically (fast_tile_of, tga_inter_fast.cu):
+// the diagonal tiles first (one per row band, the lightest: with one tile per CTA the
+// intra-route units, which ride with the first CTAs, land on them), then the full
+// tiles column by column (with several tiles per CTA the grid-stride walk gives every
+// CTA a similar share).  The population batch keeps the table.
 static std::vector<uint32_t> fast_plan(const tga_solution *s) {
-    std::vector<std::pair<int64_t, uint32_t>> w;
-    const int U = s->fastU;
-    for (int I = 0; I < s->pitch / U && I * U < s->Qp; ++I)
-        for (int J = 0; J < s->pitch / kFastTV && J * kFastTV < s->Qp; ++J)
-            if (I * U < J * kFastTV + kFastTV - 1) {
-                int64_t cells = 0;
-                for (int u = I * U; u < std::min((I + 1) * U, s->Qp); ++u) {
-                    const int lo = std::max(u + 1, J * kFastTV), hi = std::min((J + 1) * kFastTV, s->Qp);
-                    cells += std::max(0, hi - lo);
-                }
-                w.emplace_back(cells, (static_cast<uint32_t>(I) << 16) | J);
-            }
-    std::stable_sort(w.begin(), w.end(), [](const auto &a, const auto &b) { return a.first < b.first; });
-    std::vector<uint32_t> f(w.size());
-    for (size_t k = 0; k < w.size(); ++k) f[k] = w[k].second;
+    const int U = s->fastU, R = kFastTV / U;
+    const int nI = (s->Qp + U - 1) / U, nJ = (s->Qp + kFastTV - 1) / kFastTV;
+    std::vector<uint32_t> f;
+    for (int I = 0; I < nI; ++I) f.push_back((static_cast<uint32_t>(I) << 16) | static_cast<uint32_t>(I / R));
+    for (int J = 1; J < nJ; ++J)
+        for (int I = 0; I < R * J; ++I) f.push_back((static_cast<uint32_t>(I) << 16) | static_cast<uint32_t>(J));
     return f;
 }
 

@@ -73,3 +73,28 @@ def test_key_decode_roundtrip():
     for s in [-5, 0, 7, -2 ** 31, 2 ** 31 - 1]:
         ordv = (s & 0xFFFFFFFF) ^ 0x80000000
         assert tga.decode_key((ordv << 32) | 123) == (s, 123)
+
+
+def test_fast_tile_order_is_a_bijection_onto_the_plan():
+    """The tile kernel decodes its tile order arithmetically (no plan table): for
+    U = 8 and 16 and many slot counts, t -> (I, J) enumerates exactly the tiles of
+    the upper triangle, I U < Qp, J 128 < Qp, I U < 128 J + 127, each once
+    (host logic of libtga.so; no GPU needed)."""
+    import ctypes as C
+    from paper_2506_17357_b200 import tga as T
+    L = T.lib()
+    f = L.tga_debug_fast_tile
+    f.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
+    I, J = C.c_int32(), C.c_int32()
+    for U in (8, 16):
+        R = 128 // U
+        for Qp in list(range(1, 400, 7)) + [1176, 2352, 10870, 40000]:
+            nI, nJ = -(-Qp // U), -(-Qp // 128)
+            plan = {(i, j) for i in range(nI) for j in range(nJ) if i * U < 128 * j + 127}
+            n = nI + R * nJ * (nJ - 1) // 2
+            assert n == len(plan), (U, Qp)
+            got = set()
+            for t in range(n):
+                assert f(t, nI, R, C.byref(I), C.byref(J)) == 0
+                got.add((I.value, J.value))
+            assert got == plan, (U, Qp)

@@ -14,8 +14,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libtga.so")
-SOURCES = ["tga_kernels.cu", "tga_inter_fast.cu", "tga_runtime.cu"]
-HEADERS = ["tga_device.cuh", "tga_launch.h", "tga_pick.cuh"]
+SOURCES = ["tga_kernels.cu", "tga_inter_fast.cu", "tga_ns.cu", "tga_runtime.cu"]
+HEADERS = ["tga_device.cuh", "tga_launch.h", "tga_pick.cuh", "tga_tma.cuh"]
 
 
 def nvcc() -> str:

@@ -1489,6 +1489,21 @@ bool pdl_enabled(int which) {
 }
 void note_launch() { ++g_launches; }
 
+__global__ void k_fill_u64(uint64_t *__restrict__ p, size_t n, uint64_t v) {
+    pdl_trigger();   // a programmatic dependent (the sweep kernel) may launch now; it waits before its key updates
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x)
+        p[i] = v;
+}
+cudaError_t launch_fill_u64(uint64_t *p, size_t n, uint64_t v, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    const int block = n <= 32 ? 32 : 256;
+    const int grid = static_cast<int>(std::min<size_t>((n + block - 1) / block, 1184));
+    k_fill_u64<<<grid, block, 0, st>>>(p, n, v);
+    note_launch();
+    return cudaGetLastError();
+}
+
 template <class DT>
 cudaError_t launch_dp(DT *Dp, int pitch, const int32_t *node, const DT *C, int n, int Qp, int lo, int hi,
                       bool full, cudaStream_t st) {

@@ -125,6 +125,9 @@ cudaError_t launch_inter_fast_dump(bool tw, const SlotRec *rec, const SlotTW *re
                                    int x_lo, int x_hi, unsigned long long *dump);
 unsigned long long launch_count();
 void note_launch();
+// p[0..n) = v on stream st: the per-eval key reset as a kernel node (a memset node
+// between two kernels costs ~3 us more inside a graph on B200, tools/graph_floor.cu)
+cudaError_t launch_fill_u64(uint64_t *p, size_t n, uint64_t v, cudaStream_t st);
 
 // Programmatic dependent launch (PDL): the kernel may be scheduled while its
 // stream predecessor is still running; it calls pdl_wait() before its first
@@ -198,6 +201,14 @@ struct EtgaArgs {
     int w_lo, w_hi, sm_count;
 };
 cudaError_t launch_etga(uint32_t mask, bool tw, const EtgaArgs &a, cudaStream_t st, bool build_slot_of);
+// north-star sweep (tga_ns.cu): 2-opt* + relocate + swap (1,1), CVRP feasible-only;
+// tiles [t_lo, t_hi) of its 32 x 128 plan (ns_tile_count); map: Dp, box {ns_box_cols, ns_box_rows}
+int ns_tile_count(int Qp);
+int ns_box_rows();
+int ns_box_cols();
+// after_reset: the stream predecessor is the key reset (launch_fill_u64): PDL launch
+cudaError_t launch_ns_sweep(const SlotRec *rec, const CUtensorMap &map, int Qp, int t_lo, int t_hi, uint32_t Qc,
+                            int32_t cap, uint64_t *keys, bool after_reset, cudaStream_t st, unsigned long long *dump);
 cudaError_t launch_inter_fast(int U, uint32_t mask, const SlotRec *rec, const SlotTW *rectw, const CUtensorMap &map,
                               const uint32_t *tiles, int t_lo, int t_hi, uint32_t Qc, int32_t cap, uint64_t *keys,
                               int max_grid, cudaStream_t st, const SolView<int32_t> &SV, const ScoreParams &sp,

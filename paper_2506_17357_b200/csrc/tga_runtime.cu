@@ -179,6 +179,8 @@ struct tga_solution {
     uint32_t *d_ftiles = nullptr;
     int n_ftiles = 0;
     CUtensorMap fmap{};
+    CUtensorMap nsmap{};           // Dp with the north-star sweep's box (tga_ns.cu)
+    bool ns_ok = false;            // CVRP feasible-only int32 with |c| < 2^21: the NS sweep kernel applies
     bool fast = false;
     int fastU = 16;                // rows per fast-path tile (8 for small neighbourhoods)
     uint64_t *h_keys = nullptr;                         // pinned
@@ -831,11 +833,20 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (cr != CUDA_SUCCESS) return bail(fail(TGA_ERR_CUDA, "fast-path tensor map"));
+        if (!I->tw && I->opt.score_mode == TGA_SCORE_FEASIBLE && I->max_c_abs < (1 << 21)) {
+            cuuint32_t nbox[2] = {static_cast<cuuint32_t>(ns_box_cols()), static_cast<cuuint32_t>(ns_box_rows())};
+            cr = enc(&s->nsmap, CU_TENSOR_MAP_DATA_TYPE_INT32, 2, s->Dp, gdim, gstride, nbox, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (cr != CUDA_SUCCESS) return bail(fail(TGA_ERR_CUDA, "north-star sweep tensor map"));
+            s->ns_ok = true;
+        }
     }
     {   // device-resident step state
         DevState ds = make_devstate(s, s->keys);
         if (cudaMemcpyAsync(s->d_ds, &ds, sizeof(ds), cudaMemcpyHostToDevice, s->stream) != cudaSuccess ||
             cudaMemsetAsync(s->d_acc, 0, 48 * 8, s->stream) != cudaSuccess ||
+
             cudaMemsetAsync(s->d_desc, 0, 16 * 4, s->stream) != cudaSuccess)
             return bail(fail(TGA_ERR_CUDA, "device step state"));
         cudaError_t e2;
@@ -897,6 +908,14 @@ static unsigned long long capture_id(cudaStream_t st) {
     return id;
 }
 
+// the north-star sweep kernel takes an evaluation whose inter-route part is exactly
+// {2-opt*, relocate, swap (1,1)} (TGA_NO_NS=1: the all-variant tile kernel instead)
+static bool ns_path(const tga_solution *s, uint32_t mask) {
+    static const bool off = std::getenv("TGA_NO_NS") != nullptr;
+    constexpr uint32_t NS = TGA_OP_2OPT_STAR | (1u << 2) | (1u << 5);
+    return s->ns_ok && !off && s->inst->theta <= 0 && (mask & TGA_OP_INTER) == NS;
+}
+
 extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
     if (!s) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL solution");
     const tga_instance *I = s->inst;
@@ -909,8 +928,12 @@ extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
     if (st != s->stream) TGA_CUDA(order_after(st, s->stream));  // see the latest applied move
     // a device step leaves the keys reset (consumed), so the next eval needs no memset node --
     // unless that step belongs to another capture sequence (a graph replayed later)
-    if (!accumulate && !(s->keys_clean && s->clean_cap == capture_id(st)))
-        TGA_CUDA(cudaMemsetAsync(s->keys, 0xFF, TGA_N_VARIANTS * 8, st));
+    const bool ns = ns_path(s, mask);
+    bool reset = false;
+    if (!accumulate && !(s->keys_clean && s->clean_cap == capture_id(st))) {
+        TGA_CUDA(launch_fill_u64(s->keys, TGA_N_VARIANTS, ~0ull, st));
+        reset = true;
+    }
     s->keys_clean = false;
     ScoreParams sp{I->Q, I->opt.score_mode, I->opt.w_load, I->opt.w_tw};
     // row shard of the tile list and of the intra slot range
@@ -964,6 +987,12 @@ extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
                     I->Q, s->keys, s->d_acc, static_cast<int>(a), static_cast<int>(b), s->sm_count};
         e = launch_etga(mask, I->tw, ea, st, !s->slot_of_fresh);
         s->slot_of_fresh = true;
+    } else if (ns) {
+        // the north-star sweep (2-opt* + relocate + swap (1,1)) has its own kernel;
+        // intra-route variants, if any, follow in their own launch
+        tga_shard_range(ns_tile_count(s->Qp), s->shard, s->n_shards, &a, &b);
+        e = launch_ns_sweep(s->rec, s->nsmap, s->Qp, static_cast<int>(a), static_cast<int>(b),
+                            static_cast<uint32_t>(s->pitch), I->Q, s->keys, reset && !timed, st, nullptr);
     } else if (I->dtype == TGA_I32 && s->fast) {
         tga_shard_range(s->n_ftiles, s->shard, s->n_shards, &a, &b);
         const int f_lo = static_cast<int>(a), f_hi = static_cast<int>(b);
@@ -1032,7 +1061,13 @@ extern "C" int32_t tga_debug_eval_dump(tga_solution *s, uint32_t mask, int32_t f
     const bool small = I->max_c_abs < (1 << 21);
     const int grid = std::max(1, std::min(s->n_tiles, s->sm_count * 4));
     if (e == cudaSuccess) {
-        if (I->dtype == TGA_I32 && s->fast) {
+        if (ns_path(s, mask)) {   // the north-star sweep kernel, as tga_eval launches it
+            e = launch_ns_sweep(s->rec, s->nsmap, s->Qp, 0, ns_tile_count(s->Qp), static_cast<uint32_t>(s->pitch), I->Q,
+                                s->keys, false, st, dump);
+            if (e == cudaSuccess && (mask & TGA_OP_INTRA))
+                e = launch_eval_dump<int32_t>(mask, I->tw, sol_view<int32_t>(s), s->tmap, s->d_tiles, 0, 0, sp, s->keys,
+                                              grid, 0, s->Qp, false, small, warp_tw, st, dump);
+        } else if (I->dtype == TGA_I32 && s->fast) {
             const bool fused = (mask & TGA_OP_INTER) && !I->tw && small;
             const uint32_t imask = fused ? (mask & TGA_OP_INTRA) : 0u;
             if (mask & TGA_OP_INTER)
@@ -1735,7 +1770,7 @@ extern "C" int32_t tga_batch_eval(tga_batch *b, uint32_t mask, void *stream) {
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : b->stream;
     if (st != b->stream) TGA_CUDA(order_after(st, b->stream));
     const int n = static_cast<int>(b->sols.size());
-    TGA_CUDA(cudaMemsetAsync(b->d_keys, 0xFF, sizeof(uint64_t) * TGA_N_VARIANTS * n, st));
+    TGA_CUDA(launch_fill_u64(b->d_keys, static_cast<size_t>(TGA_N_VARIANTS) * n, ~0ull, st));
     ScoreParams sp{I->Q, I->opt.score_mode, I->opt.w_load, I->opt.w_tw};
     const int grid = std::max(1, std::min(b->n_work, b->sm_count * 4));
     static const int force_warp = std::getenv("TGA_WARP_TW_BATCH") ? std::atoi(std::getenv("TGA_WARP_TW_BATCH")) : -1;

@@ -76,6 +76,7 @@ __device__ __forceinline__ void scan_spare(const ScanArgs<DT> &A, const int k0, 
                 for (int j = 0; j < 3; ++j) { q.so[j] = kPoison; q.sA[j] = kPoison; }
                 A.rec[base + k] = q;
             }
+            if (A.nsc) A.nsc[base + k] = -1;   // route plane: not a canonical slot
             if (TW && A.rectw) {
                 SlotTW w{};
                 w.EF = w.EFm = kTwBig;
@@ -309,6 +310,13 @@ __device__ __forceinline__ void scan_rec_pass(const ScanArgs<DT> &A, const int r
                     q.sE[N - 1] = segok ? -e_prev - eout - pex : 0;
                 }
                 A.rec[x] = q;
+                if (A.nsc) {   // the north-star sweep's column terms, one plane per term
+                    int32_t *c = A.nsc + x;
+                    const size_t P = static_cast<size_t>(A.nsc_pitch);
+                    c[0] = q.r; c[P] = q.ne; c[2 * P] = q.rem[0]; c[3 * P] = q.sE[0];
+                    c[4 * P] = A.capacity - q.bL1; c[5 * P] = A.capacity - q.fL; c[6 * P] = A.capacity - q.W;
+                    c[7 * P] = A.capacity - q.sS[0]; c[8 * P] = q.so[0]; c[9 * P] = q.sA[0];
+                }
             }
         }
     }

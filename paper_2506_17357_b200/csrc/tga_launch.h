@@ -69,7 +69,12 @@ struct ScanArgs {
     int32_t pen_wQ;    // penalised fast-path records: w_load (0 = feasible-only records)
     SlotRec *rec;      // CVRP fast-path records (int DT only); may be null
     SlotTW *rectw;     // VRPTW (TW-I) fast-path records; may be null
+    int32_t *nsc;      // north-star sweep column terms, SoA [kNscF][nsc_pitch] (ns_col_terms); may be null
+    int32_t nsc_pitch;
 };
+// the north-star sweep's per-slot column terms (tga_ns.cu), one plane each:
+// r, ne, rem0, sE0, cap - bL1, cap - fL, cap - W, cap - sS0, so0, sA0  (SlotRec fields)
+constexpr int kNscF = 10;
 
 // what an update refreshes: up to two slot ranges (the changed routes' whole
 // slot capacity) with their routes, or everything (full relayout)
@@ -202,13 +207,18 @@ struct EtgaArgs {
 };
 cudaError_t launch_etga(uint32_t mask, bool tw, const EtgaArgs &a, cudaStream_t st, bool build_slot_of);
 // north-star sweep (tga_ns.cu): 2-opt* + relocate + swap (1,1), CVRP feasible-only;
-// tiles [t_lo, t_hi) of its 32 x 128 plan (ns_tile_count); map: Dp, box {ns_box_cols, ns_box_rows}
-int ns_tile_count(int Qp);
-int ns_box_rows();
+// rw rows per warp (4, 8, 16: tiles of 4 rw x 128), tiles [t_lo, t_hi) of its plan
+// (ns_tile_count); nsc: the column-term planes (ScanArgs::nsc); map: Dp with box
+// {ns_box_cols(), ns_box_rows(rw)} (one warp's rows + halo); after_reset: the
+// stream predecessor is the key reset (launch_fill_u64), so the sweep is launched as its
+// programmatic dependent
+int ns_rows_per_warp(int Qp, int sm_count);
+int ns_tile_count(int Qp, int rw);
+int ns_box_rows(int rw);
 int ns_box_cols();
-// after_reset: the stream predecessor is the key reset (launch_fill_u64): PDL launch
-cudaError_t launch_ns_sweep(const SlotRec *rec, const CUtensorMap &map, int Qp, int t_lo, int t_hi, uint32_t Qc,
-                            int32_t cap, uint64_t *keys, bool after_reset, cudaStream_t st, unsigned long long *dump);
+cudaError_t launch_ns_sweep(int rw, const SlotRec *rec, const int32_t *nsc, int pitch, const CUtensorMap &map, int Qp,
+                            int t_lo, int t_hi, uint32_t Qc, int32_t cap, uint64_t *keys, bool after_reset,
+                            cudaStream_t st, unsigned long long *dump);
 cudaError_t launch_inter_fast(int U, uint32_t mask, const SlotRec *rec, const SlotTW *rectw, const CUtensorMap &map,
                               const uint32_t *tiles, int t_lo, int t_hi, uint32_t Qc, int32_t cap, uint64_t *keys,
                               int max_grid, cudaStream_t st, const SolView<int32_t> &SV, const ScoreParams &sp,

@@ -43,108 +43,131 @@ __device__ __forceinline__ unsigned long long ns_gtime() {
 }
 
 namespace {
-constexpr int kNsRW = 8;                        // rows per warp
 constexpr int kNsW = 4;                         // warps per CTA (stacked in rows)
-constexpr int kNsTU = kNsRW * kNsW;             // 32 rows per tile
 constexpr int kNsTV = 128;                      // 32 lanes x 4 columns
 constexpr int kNsBoxW = kNsTV + 8;              // cols v0-4 .. v0+131 (16-byte aligned TMA x)
-constexpr int kNsBoxH = kNsTU + 2;              // rows u0-1 .. u0+32
-constexpr int kNsBoxBytes = kNsBoxW * kNsBoxH * 4;
-constexpr int kNsBoxPad = (kNsBoxBytes + 127) / 128 * 128;
-constexpr int kNsRowBytes = kNsTU * 80;
-constexpr int kNsSmem = kNsBoxPad + kNsRowBytes + 128;
 constexpr int kNsColF = 10;                     // per-column terms, SoA in shared memory
-constexpr uint32_t kNsNone = 0xFFFFFF00u;       // "no feasible candidate": survives *4 + c and + 8 c
-constexpr uint32_t kNsOff = 1u << 28;           // key offset: score * 32 + 2^28 + row >= 0 for |score| < 2^23
+constexpr uint32_t kNsNone = 0xFFFFFF00u;       // "no feasible candidate": survives *4 + c and + RW c
+constexpr int32_t kNsOff = 1 << 28;             // key offset B: score * S + B + row >= 0 for |score| < B / S
+
+// geometry of the RW-rows-per-warp instantiation: tile = 4 RW rows x 128 columns;
+// shared memory: the column-term planes | per warp: its Dp box (RW + 2 rows) | per
+// warp: its row records -- every warp waits only for its own box and rows
+template <int RW>
+struct NsGeom {
+    static constexpr int TU = kNsW * RW;                        // rows per tile
+    static constexpr int RB = kNsTV / TU;                       // row bands per column band
+    static constexpr int BoxH = RW + 2;                         // a warp's rows u-1 .. u+RW
+    static constexpr int BoxBytes = kNsBoxW * BoxH * 4;
+    static constexpr int BoxPad = (BoxBytes + 127) / 128 * 128;
+    static constexpr int ColBytes = kNsColF * kNsTV * 4;        // column-term planes of the tile
+    static constexpr int RowBytes = RW * 80;                    // a warp's row records
+    static constexpr int RowPad = (RowBytes + 127) / 128 * 128;
+    static constexpr int OffBox = ColBytes;
+    static constexpr int OffRows = OffBox + kNsW * BoxPad;
+    static constexpr int Smem = OffRows + kNsW * RowPad + 128;
+    static constexpr int S = 4 * RW;                            // key = score * S + B + row (row < RW)
+    static constexpr int LS = RW == 4 ? 4 : (RW == 8 ? 5 : 6);  // log2 S
+    static_assert(RW == 4 || RW == 8 || RW == 16, "rows per warp");
+};
 
 // per-row terms of one tile row (built from the SlotRec once per tile)
 struct __align__(16) NsRow {
     int32_t r, fL, bL1, so0;     // route (-1: not a canonical slot), 2-opt* loads, relocate-out load
-    int32_t cW, sA0, cS, a2;     // cap - W, swap load, cap - sS0, ne * 32 + 2^28 + row8
-    int32_t aR, aS, pad0, pad1;  // rem0 * 32 + 2^28 + row8, sE0 * 32 + 2^28 + row8
+    int32_t cW, sA0, cS, a2;     // cap - W, swap load, cap - sS0, ne * S + B + row
+    int32_t aR, aS, pad0, pad1;  // rem0 * S + B + row, sE0 * S + B + row
 };
 }  // namespace
 
-// tile t of the plan: the diagonal tiles (row band I, column band I / 4) whose rows
-// start the column band's first three quarters, then the full tiles column by column
-// (2 J (J - 1) of them precede column band J), then the lightest diagonal tiles
-// (I % 4 == 3: only the band's last 32 columns can lie above their rows) -- so a grid
-// one wave short of the plan gives its extra tiles, these, to CTAs that started with
-// a diagonal tile
-__host__ __device__ __forceinline__ void ns_tile_of(int t, int nI, int nJ, int &I, int &J) {
-    const int n3 = nI / 4, n0 = nI - n3, F = 2 * nJ * (nJ - 1);
-    if (t < n0) { I = (t / 3) * 4 + t % 3; J = I >> 2; return; }
-    if (t >= n0 + F) { I = 4 * (t - n0 - F) + 3; J = I >> 2; return; }
+// tile t of the plan (RB row bands of TU rows per 128-column band): the diagonal tiles
+// (row band I, column band I / RB) that do not close their column band, then the full
+// tiles column by column (RB J (J - 1) / 2 of them precede column band J), then the
+// lightest diagonal tiles (I % RB == RB - 1: only the band's last TU columns can lie
+// above their rows) -- a grid one wave short of the plan gives its extra tiles, these,
+// to CTAs that started with a diagonal tile
+__host__ __device__ __forceinline__ void ns_tile_of(int t, int nI, int nJ, int RB, int &I, int &J) {
+    const int n3 = nI / RB, n0 = nI - n3, F = RB * nJ * (nJ - 1) / 2;
+    if (t < n0) { I = (t / (RB - 1)) * RB + t % (RB - 1); J = I / RB; return; }
+    if (t >= n0 + F) { I = RB * (t - n0 - F) + RB - 1; J = I / RB; return; }
     const int q = t - n0;
-    int j = static_cast<int>((1.0f + sqrtf(1.0f + 2.0f * static_cast<float>(q))) * 0.5f);
-    while (j > 1 && 2 * j * (j - 1) > q) --j;
-    while (2 * (j + 1) * j <= q) ++j;
+    int j = static_cast<int>((1.0f + sqrtf(1.0f + 8.0f * static_cast<float>(q) / static_cast<float>(RB))) * 0.5f);
+    while (j > 1 && RB * j * (j - 1) / 2 > q) --j;
+    while (RB * (j + 1) * j / 2 <= q) ++j;
     J = j;
-    I = q - 2 * j * (j - 1);
+    I = q - RB * j * (j - 1) / 2;
 }
 
-template <bool DUMP>
-__global__ void __launch_bounds__(kNsW * 32, 5)
-    k_ns_sweep(const SlotRec *__restrict__ rec, const __grid_constant__ CUtensorMap tmap, int Qp, int t_lo, int t_hi,
-               uint32_t Qc, int32_t cap, uint64_t *__restrict__ keys, uint32_t mul32, int flags,
-               unsigned long long *dump) {
+template <int RW, bool DUMP>
+__global__ void __launch_bounds__(kNsW * 32, DUMP ? 1 : (RW == 16 ? 4 : 5))
+    k_ns_sweep(const SlotRec *__restrict__ rec, const int32_t *__restrict__ nsc, int pitch,
+               const __grid_constant__ CUtensorMap tmap, int Qp, int t_lo, int t_hi, uint32_t Qc, int32_t cap,
+               uint64_t *__restrict__ keys, uint32_t mulS, uint32_t one, int flags, unsigned long long *dump) {
+    using G = NsGeom<RW>;
+    constexpr int TU = G::TU;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *sm = smem_raw + ((128u - (s_u32(smem_raw) & 127u)) & 127u);
-    int32_t *const box = reinterpret_cast<int32_t *>(sm);
-    const SlotRec *const rows = reinterpret_cast<const SlotRec *>(sm + kNsBoxPad);
-    __shared__ uint64_t bar;
-    __shared__ NsRow nrow[kNsTU];
-    __shared__ __align__(16) int32_t colS[kNsColF][kNsTV];   // column terms: [field][column]
+    const int32_t(*colS)[kNsTV] = reinterpret_cast<const int32_t(*)[kNsTV]>(sm);   // [term][column]
+    __shared__ uint64_t bar[kNsW + 1];                          // per warp (box + rows), [kNsW] columns
+    __shared__ int s_tile[2][2];                                // (u0, v0) of the tile of iteration parity
+    __shared__ NsRow nrow[TU];
     __shared__ unsigned long long red[kNsW][3];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const bool prb = (flags & 1) && tid == 0 && blockIdx.x < 4096;
     if (prb) g_ns_probe[4 * blockIdx.x] = ns_gtime();
-    const int nI = (Qp + kNsTU - 1) / kNsTU, nJ = (Qp + kNsTV - 1) / kNsTV;
+    const int nI = (Qp + TU - 1) / TU, nJ = (Qp + kNsTV - 1) / kNsTV;
+    const int G_ = static_cast<int>(gridDim.x);
     int t = t_lo + static_cast<int>(blockIdx.x);
-    auto issue = [&](int tt) {
-        int I, J;
-        ns_tile_of(tt, nI, nJ, I, J);
-        f_expect(&bar, kNsBoxBytes + kNsRowBytes);
-        f_tma2d(box, &tmap, J * kNsTV - 4, I * kNsTU - 1, &bar);
-        f_bulk(sm + kNsBoxPad, rec + I * kNsTU, kNsRowBytes, &bar);
+    // thread 0 issues a tile: the column-term planes first (every warp needs them), then
+    // each warp's Dp box and row records on the warp's own barrier
+    auto issue = [&](int u0, int v0) {
+        f_expect(&bar[kNsW], G::ColBytes);
+#pragma unroll
+        for (int f = 0; f < kNsColF; ++f)
+            f_bulk(sm + f * kNsTV * 4, nsc + static_cast<size_t>(f) * pitch + v0, kNsTV * 4, &bar[kNsW]);
+#pragma unroll
+        for (int w = 0; w < kNsW; ++w) {
+            f_expect(&bar[w], G::BoxBytes + G::RowBytes);
+            f_tma2d(sm + G::OffBox + w * G::BoxPad, &tmap, v0 - 4, u0 + w * RW - 1, &bar[w]);
+            f_bulk(sm + G::OffRows + w * G::RowPad, rec + u0 + w * RW, G::RowBytes, &bar[w]);
+        }
     };
     if (tid == 0) {
-        f_mbar_init(&bar);
+#pragma unroll
+        for (int w = 0; w <= kNsW; ++w) f_mbar_init(&bar[w]);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        if (t < t_hi) issue(t);   // the first Dp box is in flight before anything else runs
+        if (t < t_hi) {   // the first tile's loads are in flight before anything else runs
+            int I, J;
+            ns_tile_of(t, nI, nJ, G::RB, I, J);
+            s_tile[0][0] = I * TU;
+            s_tile[0][1] = J * kNsTV;
+            issue(I * TU, J * kNsTV);
+        }
     }
     uint64_t acc[3] = {kNoKey, kNoKey, kNoKey};   // 2-opt*, relocate, swap (1,1)
     __syncthreads();
     uint32_t phase = 0u;
-    for (; t < t_hi; t += static_cast<int>(gridDim.x)) {
-        int I, J;
-        ns_tile_of(t, nI, nJ, I, J);
-        const int u0 = I * kNsTU, v0 = J * kNsTV;
-        {   // column terms of the tile: thread t reads record v0 + t from L2 (in flight with
-            // the box) and stores its per-column terms as SoA, so that a lane later reads its 4
-            // consecutive columns' terms with one conflict-free 16-byte load per term
-            const SlotRec V = rec[v0 + tid];
-            colS[0][tid] = V.r; colS[1][tid] = V.ne; colS[2][tid] = V.rem[0]; colS[3][tid] = V.sE[0];
-            colS[4][tid] = cap - V.bL1; colS[5][tid] = cap - V.fL; colS[6][tid] = cap - V.W;
-            colS[7][tid] = cap - V.sS[0]; colS[8][tid] = V.so[0]; colS[9][tid] = V.sA[0];
-        }
-        f_wait(&bar, phase);
+    for (int it = 0; t < t_hi; t += G_, ++it) {
+        const int u0 = s_tile[it & 1][0], v0 = s_tile[it & 1][1];
+        const int32_t *const box = reinterpret_cast<const int32_t *>(sm + G::OffBox + warp * G::BoxPad);
+        const SlotRec *const rows = reinterpret_cast<const SlotRec *>(sm + G::OffRows + warp * G::RowPad);
+        f_wait(&bar[warp], phase);
         if (prb && phase == 0u) g_ns_probe[4 * blockIdx.x + 1] = ns_gtime();
-        phase ^= 1u;
-        // ---- this warp's 8 rows as NsRow (lanes 0..7)
-        const int uw = u0 + warp * kNsRW;   // first row of the warp
-        if (lane < kNsRW) {
-            const SlotRec &A = rows[warp * kNsRW + lane];
+        // ---- this warp's RW rows as NsRow (lanes 0..RW-1)
+        const int uw = u0 + warp * RW;   // first row of the warp
+        if (lane < RW) {
+            const SlotRec &A = rows[lane];
             NsRow n;
             n.r = A.r; n.fL = A.fL; n.bL1 = A.bL1; n.so0 = A.so[0];
             n.cW = cap - A.W; n.sA0 = A.sA[0]; n.cS = cap - A.sS[0];
-            n.a2 = A.ne * 32 + static_cast<int32_t>(kNsOff) + lane;
-            n.aR = A.rem[0] * 32 + static_cast<int32_t>(kNsOff) + lane;
-            n.aS = A.sE[0] * 32 + static_cast<int32_t>(kNsOff) + lane;
+            n.a2 = A.ne * G::S + kNsOff + lane;
+            n.aR = A.rem[0] * G::S + kNsOff + lane;
+            n.aS = A.sE[0] * G::S + kNsOff + lane;
             n.pad0 = n.pad1 = 0;
-            nrow[warp * kNsRW + lane] = n;
+            nrow[warp * RW + lane] = n;
         }
-        __syncthreads();
+        __syncwarp();
+        f_wait(&bar[kNsW], phase);   // the column-term planes
+        phase ^= 1u;
         int32_t Vr[4], Vne[4], Vrem[4], VsE[4], cbL1[4], cfL[4], cW[4], cS[4], Vso[4], VsA[4];
         auto col4 = [&](int f, int32_t (&x)[4]) {
             const int4 q = *reinterpret_cast<const int4 *>(&colS[f][4 * lane]);
@@ -157,16 +180,16 @@ __global__ void __launch_bounds__(kNsW * 32, 5)
         uint32_t run0[4], run1[4], run2[4], run3[4];   // 2-opt*, relocate u->v, relocate v->u, swap
 #pragma unroll
         for (int c = 0; c < 4; ++c) run0[c] = run1[c] = run2[c] = run3[c] = kNsNone;
-        // Dp(u, v0 + 4 lane + c) for the warp's rows: box row (u - u0 + 1), box col 4 + 4 lane + c
+        // Dp(u, v0 + 4 lane + c) for the warp's rows: box row (u - uw + 1), box col 4 + 4 lane + c
         const int32_t *bcol = box + 4 + 4 * lane;
         auto ld4 = [&](int brow) { return *reinterpret_cast<const int4 *>(bcol + brow * kNsBoxW); };
-        const int br0 = warp * kNsRW + 1;   // box row of the warp's first row
+        constexpr int br0 = 1;           // box row of the warp's first row
         int4 dm = ld4(br0 - 1), d0 = ld4(br0);
 #pragma unroll
-        for (int i = 0; i < kNsRW; ++i) {
+        for (int i = 0; i < RW; ++i) {
             const int4 d1 = ld4(br0 + i + 1);
             const int32_t dl = bcol[(br0 + i) * kNsBoxW - 1], dr = bcol[(br0 + i) * kNsBoxW + 4];
-            const NsRow A = nrow[warp * kNsRW + i];
+            const NsRow A = nrow[warp * RW + i];
             if (A.r >= 0 && A.r < rmaxV) {   // warp-uniform
                 const int32_t D0[4] = {d0.x, d0.y, d0.z, d0.w};
                 const int32_t Dm[4] = {dm.x, dm.y, dm.z, dm.w};
@@ -175,14 +198,25 @@ __global__ void __launch_bounds__(kNsW * 32, 5)
                 const int32_t Dl[4] = {dl, d0.x, d0.y, d0.z};    // Dp(u, v - 1)
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
-                    // 2-opt*: A' = F(u) + B(v+1), B' = F(v) + B(u+1)      (Eq. 14)
-                    const uint32_t k0 = static_cast<uint32_t>(Dr[c] + D1[c] + Vne[c]) * mul32 + static_cast<uint32_t>(A.a2);
-                    // relocate u after v / v after u                    (Eq. 13)
-                    const uint32_t k1 = static_cast<uint32_t>(D0[c] + Dr[c] + Vne[c]) * mul32 + static_cast<uint32_t>(A.aR);
-                    const uint32_t k2 = static_cast<uint32_t>(D0[c] + D1[c] + Vrem[c]) * mul32 + static_cast<uint32_t>(A.a2);
+                    // Keys  score * S + (B + row),  the sums built mostly with IMAD (x * S + y) on the
+                    // fma pipe: the compares and minima already fill the alu pipe (both issue every
+                    // 2 cycles per SMSP), so 12 alu + 10 fma instructions per cell beat 16 + 4.
+                    // (inline PTX: the compiler would otherwise re-associate x S + y S into (x + y) S)
+                    auto mad = [&](int32_t x, uint32_t y) {
+                        uint32_t r;
+                        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(x), "r"(mulS), "r"(y));
+                        return r;
+                    };
+                    uint32_t t;
+                    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(t) : "r"(Dr[c]), "r"(one), "r"(Vne[c]));
+                    const uint32_t u = mad(D1[c], static_cast<uint32_t>(A.a2));
+                    // 2-opt*: A' = F(u) + B(v+1), B' = F(v) + B(u+1): dD = Dp(u,v+1) + Dp(u+1,v) - e(u) - e(v)  (Eq. 14)
+                    const uint32_t k0 = mad(static_cast<int32_t>(t), u);
+                    // relocate u after v: rem(u) + Dp(u,v) + Dp(u,v+1) - e(v);  v after u: rem(v) + Dp(u,v) + Dp(u+1,v) - e(u)  (Eq. 13)
+                    const uint32_t k1 = mad(static_cast<int32_t>(t), mad(D0[c], static_cast<uint32_t>(A.aR)));
+                    const uint32_t k2 = mad(D0[c], mad(Vrem[c], u));
                     // swap (1,1): A' = F(u-1) + v + B(u+1), B' = F(v-1) + u + B(v+1)
-                    const uint32_t k3 = static_cast<uint32_t>(Dm[c] + D1[c] + Dl[c] + Dr[c] + VsE[c]) * mul32 +
-                                        static_cast<uint32_t>(A.aS);
+                    const uint32_t k3 = mad(Dr[c], mad(D1[c], mad(Dm[c] + Dl[c] + VsE[c], static_cast<uint32_t>(A.aS))));
                     // feasibility (Eq. 16b) and the keep, branch-free on predicates: the pair must
                     // span two routes, route(u) < route(v); every new route load <= cap (the loads
                     // of an invalid role are poisoned, so it fails the same compares)
@@ -212,7 +246,8 @@ __global__ void __launch_bounds__(kNsW * 32, 5)
                             const uint32_t u = static_cast<uint32_t>(uw + i), v = static_cast<uint32_t>(v0 + 4 * lane + c);
                             const uint32_t st = Qc * Qc;
                             auto key = [&](bool ok, uint32_t k, uint32_t idx) -> unsigned long long {
-                                return ok ? pack_key(ord_score(static_cast<int32_t>(k >> 5) - (1 << 23)), idx) : kNoKey;
+                                return ok ? pack_key(ord_score(static_cast<int32_t>(k >> G::LS) - (kNsOff >> G::LS)), idx)
+                                          : kNoKey;
                             };
                             dump_put(dump, st, 1, u * Qc + v, key(ok0, k0, u * Qc + v));
                             dump_put(dump, st, 2, u * Qc + v, key(ok1, k1, u * Qc + v));
@@ -225,38 +260,44 @@ __global__ void __launch_bounds__(kNsW * 32, 5)
             dm = d0;
             d0 = d1;
         }
+        // the next tile's origin, decoded before the barrier that lets thread 0 refill the stage
+        if (tid == 0 && t + G_ < t_hi) {
+            int I, J;
+            ns_tile_of(t + G_, nI, nJ, G::RB, I, J);
+            s_tile[(it + 1) & 1][0] = I * TU;
+            s_tile[(it + 1) & 1][1] = J * kNsTV;
+        }
         // ---- merge the 4 columns in 32 bits, then one 64-bit key per stream
         //  direct (u * Q + v):  order (score, row, c)  ->  run * 4 + c
-        //  reversed (v * Q + u): order (score, c, row)  ->  run + 8 c
+        //  reversed (v * Q + u): order (score, c, row)  ->  run + RW c
         uint32_t m0 = 0xFFFFFFFFu, m1 = 0xFFFFFFFFu, m2 = 0xFFFFFFFFu, m3 = 0xFFFFFFFFu;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
             m0 = min(m0, run0[c] * 4u + static_cast<uint32_t>(c));
             m1 = min(m1, run1[c] * 4u + static_cast<uint32_t>(c));
-            m2 = min(m2, run2[c] + 8u * static_cast<uint32_t>(c));
+            m2 = min(m2, run2[c] + static_cast<uint32_t>(RW * c));
             m3 = min(m3, run3[c] * 4u + static_cast<uint32_t>(c));
         }
         const uint32_t vb = static_cast<uint32_t>(v0 + 4 * lane);
+        constexpr uint32_t kOrd = 0x80000000u - static_cast<uint32_t>(kNsOff >> G::LS);   // ord_score(score) - (score + B/S)
         auto direct = [&](uint64_t &a, uint32_t m) {
             if (m < 0xF0000000u) {
-                const uint32_t ord = (m >> 7) + (0x80000000u - (1u << 23));   // ord_score(score)
-                const uint32_t u = static_cast<uint32_t>(uw) + ((m >> 2) & 7u), v = vb + (m & 3u);
-                a = umin64(a, pack_key(ord, u * Qc + v));
+                const uint32_t u = static_cast<uint32_t>(uw) + ((m >> 2) & (RW - 1)), v = vb + (m & 3u);
+                a = umin64(a, pack_key((m >> (G::LS + 2)) + kOrd, u * Qc + v));
             }
         };
         direct(acc[0], m0);
         direct(acc[1], m1);
         direct(acc[2], m3);
         if (m2 < 0xF0000000u) {
-            const uint32_t ord = (m2 >> 5) + (0x80000000u - (1u << 23));
-            const uint32_t u = static_cast<uint32_t>(uw) + (m2 & 7u), v = vb + ((m2 >> 3) & 3u);
-            acc[1] = umin64(acc[1], pack_key(ord, v * Qc + u));
+            const uint32_t u = static_cast<uint32_t>(uw) + (m2 & (RW - 1)), v = vb + ((m2 / RW) & 3u);
+            acc[1] = umin64(acc[1], pack_key((m2 >> G::LS) + kOrd, v * Qc + u));
         }
-        if (t + static_cast<int>(gridDim.x) < t_hi) {   // another tile: every warp is done with the stage
+        if (t + G_ < t_hi) {   // another tile: every warp is done with the stage
             __syncthreads();
             if (tid == 0) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                issue(t + static_cast<int>(gridDim.x));
+                issue(s_tile[(it + 1) & 1][0], s_tile[(it + 1) & 1][1]);
             }
         }
     }
@@ -281,37 +322,54 @@ __global__ void __launch_bounds__(kNsW * 32, 5)
     if (prb) g_ns_probe[4 * blockIdx.x + 3] = ns_gtime();
 }
 
-int ns_tile_count(int Qp) {
-    const int nI = (Qp + kNsTU - 1) / kNsTU, nJ = (Qp + kNsTV - 1) / kNsTV;
-    return nI + 2 * nJ * (nJ - 1);
+int ns_rows_per_warp(int Qp, int sm_count) {
+    // the largest RW whose plan still gives every SM ~2.5 tiles (parallelism for the
+    // latency-bound small sweeps, fewer per-tile overheads for the large ones)
+    if (const char *e = std::getenv("TGA_NS_RW")) {
+        const int v = std::atoi(e);
+        if (v == 4 || v == 8 || v == 16) return v;
+    }
+    for (int rw : {16, 8})
+        if (ns_tile_count(Qp, rw) >= (5 * sm_count) / 2) return rw;
+    return 4;
 }
 
-int ns_box_rows() { return kNsBoxH; }
+int ns_tile_count(int Qp, int rw) {
+    const int TU = kNsW * rw, RB = kNsTV / TU;
+    const int nI = (Qp + TU - 1) / TU, nJ = (Qp + kNsTV - 1) / kNsTV;
+    return nI + RB * nJ * (nJ - 1) / 2;
+}
+
+int ns_box_rows(int rw) { return rw + 2; }
 int ns_box_cols() { return kNsBoxW; }
 
-template <bool DUMP>
+template <int RW, bool DUMP>
 static int ns_capacity() {
     static PerDevice pd;
     static int res[kMaxDevices];
     const int d = once_per_device(pd, [](int dev) {
-        cudaFuncSetAttribute(k_ns_sweep<DUMP>, cudaFuncAttributeMaxDynamicSharedMemorySize, kNsSmem);
+        cudaFuncSetAttribute(k_ns_sweep<RW, DUMP>, cudaFuncAttributeMaxDynamicSharedMemorySize, NsGeom<RW>::Smem);
         int sms = 0, b = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_ns_sweep<DUMP>, kNsW * 32, kNsSmem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_ns_sweep<RW, DUMP>, kNsW * 32, NsGeom<RW>::Smem);
         res[dev] = std::max(1, b) * std::max(1, sms);
     });
     return res[d];
 }
 
-cudaError_t launch_ns_sweep(const SlotRec *rec, const CUtensorMap &map, int Qp, int t_lo, int t_hi, uint32_t Qc,
-                            int32_t cap, uint64_t *keys, bool after_reset, cudaStream_t st, unsigned long long *dump) {
-    if (t_hi <= t_lo) return cudaSuccess;
+template <int RW>
+static cudaError_t launch_ns_t(const SlotRec *rec, const int32_t *nsc, int pitch, const CUtensorMap &map, int Qp,
+                               int t_lo, int t_hi, uint32_t Qc, int32_t cap, uint64_t *keys, bool after_reset,
+                               cudaStream_t st, unsigned long long *dump) {
     const int tiles = t_hi - t_lo;
     static const int probe = std::getenv("TGA_NS_PROBE") != nullptr;
     static const bool no_pdl = std::getenv("TGA_NS_NO_PDL") != nullptr;   // A/B override
+    constexpr int Smem = NsGeom<RW>::Smem;
+    const uint32_t mulS = static_cast<uint32_t>(NsGeom<RW>::S);   // a kernel parameter: one IMAD per key
     if (dump) {
-        const int grid = std::min(tiles, ns_capacity<true>());
-        k_ns_sweep<true><<<grid, kNsW * 32, kNsSmem, st>>>(rec, map, Qp, t_lo, t_hi, Qc, cap, keys, 32u, 0, dump);
+        const int grid = std::min(tiles, ns_capacity<RW, true>());
+        k_ns_sweep<RW, true><<<grid, kNsW * 32, Smem, st>>>(rec, nsc, pitch, map, Qp, t_lo, t_hi, Qc, cap, keys, mulS, 1u,
+                                                            0, dump);
         note_launch();
         return cudaGetLastError();
     }
@@ -319,28 +377,40 @@ cudaError_t launch_ns_sweep(const SlotRec *rec, const CUtensorMap &map, int Qp, 
     // TMA loads and evaluation overlap the reset (k_ns_sweep waits only before its key
     // updates; the reset itself starts after every earlier write of the stream completed)
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(std::min(tiles, ns_capacity<false>()));
+    cfg.gridDim = dim3(std::min(tiles, ns_capacity<RW, false>()));
     cfg.blockDim = dim3(kNsW * 32);
-    cfg.dynamicSmemBytes = kNsSmem;
+    cfg.dynamicSmemBytes = Smem;
     cfg.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = (after_reset && !no_pdl) ? 1 : 0;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, k_ns_sweep<false>, rec, map, Qp, t_lo, t_hi, Qc, cap, keys, 32u,
-                                             probe ? 1 : 0, static_cast<unsigned long long *>(nullptr));
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, k_ns_sweep<RW, false>, rec, nsc, pitch, map, Qp, t_lo, t_hi, Qc, cap,
+                                             keys, mulS, 1u, probe ? 1 : 0, static_cast<unsigned long long *>(nullptr));
     note_launch();
     return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+cudaError_t launch_ns_sweep(int rw, const SlotRec *rec, const int32_t *nsc, int pitch, const CUtensorMap &map, int Qp,
+                            int t_lo, int t_hi, uint32_t Qc, int32_t cap, uint64_t *keys, bool after_reset,
+                            cudaStream_t st, unsigned long long *dump) {
+    if (t_hi <= t_lo) return cudaSuccess;
+    switch (rw) {
+        case 4: return launch_ns_t<4>(rec, nsc, pitch, map, Qp, t_lo, t_hi, Qc, cap, keys, after_reset, st, dump);
+        case 8: return launch_ns_t<8>(rec, nsc, pitch, map, Qp, t_lo, t_hi, Qc, cap, keys, after_reset, st, dump);
+        case 16: return launch_ns_t<16>(rec, nsc, pitch, map, Qp, t_lo, t_hi, Qc, cap, keys, after_reset, st, dump);
+        default: return cudaErrorInvalidValue;
+    }
 }
 
 }  // namespace tga
 
 // host-side decode of the NS tile order (tests: a bijection onto the plan)
-extern "C" int32_t tga_debug_ns_tile(int32_t t, int32_t nI, int32_t nJ, int32_t *I, int32_t *J) {
-    if (!I || !J || nI < 0 || nJ < 0 || t < 0) return -1;
+extern "C" int32_t tga_debug_ns_tile(int32_t t, int32_t nI, int32_t nJ, int32_t RB, int32_t *I, int32_t *J) {
+    if (!I || !J || nI < 0 || nJ < 0 || t < 0 || RB < 2) return -1;
     int i, j;
-    tga::ns_tile_of(t, nI, nJ, i, j);
+    tga::ns_tile_of(t, nI, nJ, RB, i, j);
     *I = i;
     *J = j;
     return 0;

@@ -180,7 +180,9 @@ struct tga_solution {
     int n_ftiles = 0;
     CUtensorMap fmap{};
     CUtensorMap nsmap{};           // Dp with the north-star sweep's box (tga_ns.cu)
-    bool ns_ok = false;            // CVRP feasible-only int32 with |c| < 2^21: the NS sweep kernel applies
+    bool ns_ok = false;            // CVRP feasible-only int32 with |c| < 2^20: the NS sweep kernel applies
+    int ns_rw = 8;                 // its rows per warp (ns_rows_per_warp)
+    int32_t *nsc = nullptr;        // its column-term planes [kNscF][pitch] (written by the scans)
     bool fast = false;
     int fastU = 16;                // rows per fast-path tile (8 for small neighbourhoods)
     uint64_t *h_keys = nullptr;                         // pinned
@@ -344,6 +346,8 @@ static ScanArgs<DT> scan_args(tga_solution *s) {
     a.pen_wQ = s->inst->opt.score_mode == TGA_SCORE_PENALISED ? s->inst->opt.w_load : 0;
     a.rec = s->rec;
     a.rectw = s->rectw;
+    a.nsc = s->nsc;
+    a.nsc_pitch = s->pitch;
     return a;
 }
 
@@ -715,7 +719,7 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
     void *v_node, *v_route, *v_pos, *v_rlen, *v_canon, *v_fwdL, *v_bwdL, *v_en, *v_fD, *v_bD, *v_b1, *v_b2, *v_b3;
     void *v_fT, *v_bT, *v_s2, *v_s3, *v_rbase, *v_rlenR, *v_cbase, *v_rW, *v_rTV, *v_rD, *v_keys, *v_tiles;
     void *v_ds, *v_sa, *v_desc, *v_scr, *v_acc;
-    void *v_rec = nullptr, *v_ftiles = nullptr, *v_rectw = nullptr, *v_slot_of = nullptr;
+    void *v_rec = nullptr, *v_ftiles = nullptr, *v_rectw = nullptr, *v_slot_of = nullptr, *v_nsc = nullptr;
     s->fastU = 16;  // U = 8 measured no better at n = 1000 (more tiles, more per-tile overhead)
     if (const char *ev = std::getenv("TGA_FAST_U")) s->fastU = std::atoi(ev) == 8 ? 8 : 16;  // tuning override
     if (I->opt.score_mode == TGA_SCORE_PENALISED) s->fastU = 16;   // the penalised tile body is built for U = 16
@@ -724,6 +728,8 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
     // fast path: integer distances; feasible-only (CVRP or VRPTW TW-I) or penalised CVRP
     const bool want_fast = I->dtype == TGA_I32 && I->fast_ok &&
                            (I->opt.score_mode == TGA_SCORE_FEASIBLE || I->fast_pen_ok);
+    // the north-star sweep kernel (tga_ns.cu): CVRP, feasible-only, |c| < 2^20
+    const bool want_ns = want_fast && !I->tw && I->opt.score_mode == TGA_SCORE_FEASIBLE && I->max_c_abs < (1 << 20);
     Item items[] = {
         {&v_node, cap * 4}, {&v_route, cap * 4}, {&v_pos, cap * 4}, {&v_rlen, cap * 4}, {&v_canon, cap * 4},
         {&v_fwdL, cap * 4}, {&v_bwdL, cap * 4}, {&v_en, cap * 4}, {&v_fD, cap * 4}, {&v_bD, cap * 4},
@@ -735,7 +741,8 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
         {&v_keys, TGA_N_VARIANTS * 8}, {&v_tiles, tiles_max * 4},
         {&v_rec, want_fast ? cap * sizeof(SlotRec) : 0}, {&v_ftiles, want_fast ? ftiles_max * 4 : 0},
         {&v_rectw, want_fast && I->tw ? cap * sizeof(SlotTW) : 0},
-        {&v_slot_of, I->theta > 0 ? static_cast<size_t>(I->n) * 4 : 0}};
+        {&v_slot_of, I->theta > 0 ? static_cast<size_t>(I->n) * 4 : 0},
+        {&v_nsc, want_ns ? static_cast<size_t>(kNscF) * s->pitch * 4 : 0}};
     size_t total = 0;
     for (auto &it : items) total += align_up(it.bytes, 256);
     if (cudaMalloc(&s->arena, total) != cudaSuccess) return bail(fail(TGA_ERR_OOM, "device arena"));
@@ -766,6 +773,12 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
     s->d_acc = static_cast<unsigned long long *>(v_acc);
     s->slot_of = I->theta > 0 ? static_cast<int32_t *>(v_slot_of) : nullptr;  // zero-size items point past the arena
     s->keys = static_cast<uint64_t *>(v_keys);
+    if (want_ns) {   // column-term planes: route -1 (no canonical slot) until the scan writes a slot
+        s->nsc = static_cast<int32_t *>(v_nsc);
+        if (cudaMemsetAsync(s->nsc, 0xFF, static_cast<size_t>(s->pitch) * 4, s->stream) != cudaSuccess ||
+            cudaMemsetAsync(s->nsc + s->pitch, 0, static_cast<size_t>(kNscF - 1) * s->pitch * 4, s->stream) != cudaSuccess)
+            return bail(fail(TGA_ERR_CUDA, "memset"));
+    }
     s->d_tiles = static_cast<uint32_t *>(v_tiles);
     if (want_fast) {
         s->fast = true;
@@ -833,8 +846,9 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (cr != CUDA_SUCCESS) return bail(fail(TGA_ERR_CUDA, "fast-path tensor map"));
-        if (!I->tw && I->opt.score_mode == TGA_SCORE_FEASIBLE && I->max_c_abs < (1 << 21)) {
-            cuuint32_t nbox[2] = {static_cast<cuuint32_t>(ns_box_cols()), static_cast<cuuint32_t>(ns_box_rows())};
+        if (s->nsc) {
+            s->ns_rw = ns_rows_per_warp(s->Qp, s->sm_count);
+            cuuint32_t nbox[2] = {static_cast<cuuint32_t>(ns_box_cols()), static_cast<cuuint32_t>(ns_box_rows(s->ns_rw))};
             cr = enc(&s->nsmap, CU_TENSOR_MAP_DATA_TYPE_INT32, 2, s->Dp, gdim, gstride, nbox, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -990,8 +1004,8 @@ extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
     } else if (ns) {
         // the north-star sweep (2-opt* + relocate + swap (1,1)) has its own kernel;
         // intra-route variants, if any, follow in their own launch
-        tga_shard_range(ns_tile_count(s->Qp), s->shard, s->n_shards, &a, &b);
-        e = launch_ns_sweep(s->rec, s->nsmap, s->Qp, static_cast<int>(a), static_cast<int>(b),
+        tga_shard_range(ns_tile_count(s->Qp, s->ns_rw), s->shard, s->n_shards, &a, &b);
+        e = launch_ns_sweep(s->ns_rw, s->rec, s->nsc, s->pitch, s->nsmap, s->Qp, static_cast<int>(a), static_cast<int>(b),
                             static_cast<uint32_t>(s->pitch), I->Q, s->keys, reset && !timed, st, nullptr);
     } else if (I->dtype == TGA_I32 && s->fast) {
         tga_shard_range(s->n_ftiles, s->shard, s->n_shards, &a, &b);
@@ -1062,7 +1076,8 @@ extern "C" int32_t tga_debug_eval_dump(tga_solution *s, uint32_t mask, int32_t f
     const int grid = std::max(1, std::min(s->n_tiles, s->sm_count * 4));
     if (e == cudaSuccess) {
         if (ns_path(s, mask)) {   // the north-star sweep kernel, as tga_eval launches it
-            e = launch_ns_sweep(s->rec, s->nsmap, s->Qp, 0, ns_tile_count(s->Qp), static_cast<uint32_t>(s->pitch), I->Q,
+            e = launch_ns_sweep(s->ns_rw, s->rec, s->nsc, s->pitch, s->nsmap, s->Qp, 0, ns_tile_count(s->Qp, s->ns_rw),
+                                static_cast<uint32_t>(s->pitch), I->Q,
                                 s->keys, false, st, dump);
             if (e == cudaSuccess && (mask & TGA_OP_INTRA))
                 e = launch_eval_dump<int32_t>(mask, I->tw, sol_view<int32_t>(s), s->tmap, s->d_tiles, 0, 0, sp, s->keys,

@@ -101,26 +101,29 @@ def test_fast_tile_order_is_a_bijection_onto_the_plan():
 
 
 def test_ns_tile_order_is_a_bijection_onto_the_plan():
-    """The north-star sweep kernel's 32 x 128 tile order (tga_ns.cu, decoded
-    arithmetically): t -> (I, J) enumerates every tile that holds a cell of the
-    upper triangle, each once; the lightest diagonal tiles last (host logic; no GPU)."""
+    """The north-star sweep kernel's tile order (tga_ns.cu, decoded arithmetically;
+    tiles of TU = 16 / 32 / 64 rows x 128 columns, RB = 128 / TU row bands per column
+    band): t -> (I, J) enumerates every tile that holds a cell of the upper triangle,
+    each once; the lightest diagonal tiles last (host logic; no GPU)."""
     import ctypes as C
     from paper_2506_17357_b200 import tga as T
     L = T.lib()
     f = L.tga_debug_ns_tile
-    f.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
+    f.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
     I, J = C.c_int32(), C.c_int32()
-    for Qp in list(range(1, 600, 11)) + [1176, 2352, 2944, 10870, 40000]:
-        nI, nJ = -(-Qp // 32), -(-Qp // 128)
-        plan = {(i, j) for i in range(nI) for j in range(nJ) if i * 32 < 128 * j + 127}
-        n = nI + 2 * nJ * (nJ - 1)
-        assert n == len(plan), Qp
-        got = []
-        for t in range(n):
-            assert f(t, nI, nJ, C.byref(I), C.byref(J)) == 0
-            got.append((I.value, J.value))
-        assert set(got) == plan and len(set(got)) == n, Qp
-        n3 = nI // 4
-        # diagonal tiles of the bands' first three quarters lead, the lightest close the plan
-        assert all(j == i // 4 and i % 4 != 3 for i, j in got[:nI - n3])
-        assert all(j == i // 4 and i % 4 == 3 for i, j in got[n - n3:])
+    for TU in (16, 32, 64):
+        RB = 128 // TU
+        for Qp in list(range(1, 600, 11)) + [1176, 2352, 2944, 10870, 40000]:
+            nI, nJ = -(-Qp // TU), -(-Qp // 128)
+            plan = {(i, j) for i in range(nI) for j in range(nJ) if i * TU < 128 * j + 127}
+            n = nI + RB * nJ * (nJ - 1) // 2
+            assert n == len(plan), (TU, Qp)
+            got = []
+            for t in range(n):
+                assert f(t, nI, nJ, RB, C.byref(I), C.byref(J)) == 0
+                got.append((I.value, J.value))
+            assert set(got) == plan and len(set(got)) == n, (TU, Qp)
+            n3 = nI // RB
+            # diagonal tiles that do not close their band lead, the lightest close the plan
+            assert all(j == i // RB and i % RB != RB - 1 for i, j in got[:nI - n3]), (TU, Qp)
+            assert all(j == i // RB and i % RB == RB - 1 for i, j in got[n - n3:]), (TU, Qp)

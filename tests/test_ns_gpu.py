@@ -177,3 +177,18 @@ def test_ns_publish_accumulate_and_reset():
     ks = gs.keys()
     for v in range(T.N_VARIANTS):
         assert ks[v] == (ref[v] if v in NS else np.uint64(0xFFFFFFFFFFFFFFFF)), v
+
+
+@pytest.mark.parametrize("rw", [4, 8, 16])
+def test_ns_rows_per_warp_instantiations_exact(rw, monkeypatch):
+    """Each rows-per-warp instantiation of the sweep (tiles of 16 / 32 / 64 rows; the
+    load picks one by plan size, TGA_NS_RW forces it): every candidate bit-exact on a
+    ragged 20-customer partition and on cfg2, and the keys equal the oracle's."""
+    _need_gpu()
+    monkeypatch.setenv("TGA_NS_RW", str(rw))
+    inst, sol = G.cvrp_small(1, spare=True)
+    compare_fields(inst, G.random_partition(20, 5, 900 + rw, allow_empty=True).routes, NS, 0, label=f"rw{rw} cfg1")
+    inst, sol = G.config("cfg2")
+    n, _ = compare_fields(inst, sol.routes, NS, 0, label=f"rw{rw} cfg2")
+    assert n > 0
+    ns_keys_vs_oracle(inst, sol.routes, f"rw{rw} cfg2", parallel=True)

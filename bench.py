@@ -69,6 +69,10 @@ def parse():
                     help="score mode (DESIGN.md reading 4): feasible-only or penalised dD + w_Q dL_V (+ w_T dT_V)")
     ap.add_argument("--granular", type=int, default=0,
                     help="theta > 0: edge-based neighbourhood (ETGA, P:390-401) with granularity threshold theta")
+    ap.add_argument("--no-north-star", action="store_true",
+                    help="skip the north-star sweep block (ns2000 fused 2-opt*+relocate+swap) of the default line")
+    ap.add_argument("--no-row-shard", action="store_true",
+                    help="skip the row-sharded cfg4 sweep block (SURVEY §8(e)) of the default line")
     ap.add_argument("--shard", choices=["replicas", "rows"], default="replicas",
                     help="N>1: independent descents per GPU (weak scaling, no collective) or one "
                          "solution's candidate rows split over the GPUs (NCCL MIN-allreduce of the keys)")
@@ -506,8 +510,6 @@ def run_tga(args):
     for r in reps:
         r.device_stats()
     del g_ker
-    if rank != 0:
-        return 0
 
     # ---------------- roofline of the dominant kernel (inter-route eval), live events
     pk, pk_src = peaks()
@@ -590,6 +592,21 @@ def run_tga(args):
                             "us_per_sweep": per_sweep_s * 1e6, "candidates": c}
             del g
 
+    # ---------------- row-sharded large sweep: cfg4's candidate rows over the
+    # ranks, keys MIN-allreduced over NCCL inside every tga_eval (one collective per sweep)
+    row_block = None
+    if not args.no_row_shard and not row_shard and args.config != "cfg4":
+        row_block = row_shard_block(args, ws, rank, local, dev, stream)
+    ns_block = None
+    if rank == 0 and not args.no_north_star and not row_shard:
+        ns_block = north_star_block(args, dev, stream)
+    if rank != 0:
+        if ws > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            dist.destroy_process_group()
+        return 0
+
     # ---------------- e2e through the C ABI with host buffers
     # each step: tga_solution_reload(host CSR routes of a new solution: H2D of
     # the routes + slot layout, Dp rebuild, full attribute scan) -> tga_eval(all)
@@ -664,11 +681,153 @@ def run_tga(args):
         "cpu_baseline": cpu, "cpu_baseline_concat": cpu_fast,
         "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
     }
+    if row_block is not None:
+        line["row_shard"] = row_block
+    if ns_block is not None:
+        line["north_star"] = ns_block
     print(json.dumps(line, default=float), flush=True)
     if ws > 1:
         import torch.distributed as dist
+        dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def north_star_block(args, dev, stream):
+    """BASELINE.json north_star: the 2000-customer full 2-opt*+relocate+swap sweep
+    (X-like CVRP, 2000 customers, 87 routes + spare; one solution, L2-warm steady
+    state).  us_per_sweep: S back-to-back tga_eval(OP_FUSED_NS) -- key reset + the
+    k_ns_sweep launch -- in one CUDA graph, CUDA events around R replays.  kernel_us:
+    the same with accumulating evals (no key reset node): S back-to-back k_ns_sweep
+    launches per graph, so per launch including the launch gap.
+    Fractions: algorithmic lane-ops (ALG_OPS x exact candidate counts) over the
+    148 x 128 x f_max issue peak, and the Dp upper triangle (Qp^2 / 2 int32) over the
+    measured HBM copy bandwidth."""
+    import torch
+    import tga_gen as G
+    from paper_2506_17357_b200 import tga as T
+    inst, sol = G.config("ns2000", args.seed)
+    gs = T.Solution(T.Instance.from_gen(inst), sol)
+    gs.set_stream(stream)
+    m = T.OP_FUSED_NS
+    S, REPS = 20, 10
+
+    def graph():
+        for _ in range(3):
+            gs.eval(m, stream)
+        torch.cuda.synchronize(dev)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            for _ in range(S):
+                gs.eval(m, stream)
+        g.replay()
+        torch.cuda.synchronize(dev)
+        return g
+
+    g = graph()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(REPS):
+            g.replay()
+        e1.record(stream)
+    torch.cuda.synchronize(dev)
+    per_s = e0.elapsed_time(e1) / 1e3 / (S * REPS)
+    del g
+    # kernel-only stream: accumulating evals need no key reset, so the graph holds S
+    # back-to-back k_ns_sweep launches (the same sweep; keys stay the minimum)
+    gs.eval(m, stream)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        for _ in range(S):
+            gs.eval(m | T.EVAL_ACCUMULATE, stream)
+    g.replay()
+    torch.cuda.synchronize(dev)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(REPS):
+            g.replay()
+        e1.record(stream)
+    torch.cuda.synchronize(dev)
+    kern_s = e0.elapsed_time(e1) / 1e3 / (S * REPS)
+    del g
+    c = gs.counts()
+    R, N, Qc, _ = gs.info()
+    cand = int(c[1]) + int(c[2]) + int(c[5])
+    ops = float(int(c[1]) * ALG_OPS[1] + int(c[2]) * ALG_OPS[2] + int(c[5]) * ALG_OPS[5])
+    Qp = N + 4 * R      # physical slots (2 spare slots per route)
+    tri = Qp * Qp / 2.0 * 4.0
+    pk, pk_src = peaks()
+    alu_peak = 148 * 128 * float(pk.get("sm_max_mhz", 1965.0)) * 1e6
+    hbm_peak = float(pk["hbm_gbs"]) * 1e9
+    gs.close()
+    return {"workload": "ns2000: " + G.CONFIGS["ns2000"] + "; fused 2-opt*+relocate+swap sweep (k_ns_sweep)",
+            "candidates": cand, "us_per_sweep": per_s * 1e6, "sweeps_per_s": 1.0 / per_s,
+            "moves_per_s": cand / per_s, "kernel_us": kern_s * 1e6,
+            "alu_frac_kernel": ops / kern_s / alu_peak, "alu_frac_sweep": ops / per_s / alu_peak,
+            "hbm_frac_kernel": tri / kern_s / hbm_peak, "hbm_frac_sweep": tri / per_s / hbm_peak,
+            "alg_ops": ops, "alg_bytes": tri, "alu_peak_tops": alu_peak / 1e12, "hbm_peak_gbs": hbm_peak / 1e9,
+            "peak_source": pk_src, "target": "sweep >= 0.6 of the binding roofline (ALU issue: <= 4.6 us)"}
+
+
+def row_shard_block(args, ws, rank, local, dev, stream):
+    """BASELINE config 4 (10^4 customers) with its candidate rows split over the N ranks
+    (DESIGN.md §9): every rank evaluates 1/N of the tile plan, the 23
+    packed keys are MIN-allreduced over NCCL inside tga_eval (ncclAllReduce on the
+    solution's stream), all ranks hold identical keys.  Timed: S back-to-back sweeps
+    (eval + allreduce) in one CUDA graph, CUDA events, max over ranks (strong scaling:
+    the same neighbourhood at every N).  At N = 1 the same sweep without a collective."""
+    import torch
+    import tga_gen as G
+    from paper_2506_17357_b200 import tga as T
+    inst, sol = G.config("cfg4", args.seed)
+    gi = T.Instance.from_gen(inst)
+    gs = T.Solution(gi, sol)
+    gs.set_stream(stream)
+    if ws > 1:
+        import torch.distributed as dist
+        obj = [T.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        gs.comm_init(rank, ws, obj[0])
+    out = {"workload": "cfg4: " + G.CONFIGS["cfg4"] + f"; candidate rows over {ws} rank(s), keys "
+                       "MIN-allreduced over NCCL per sweep" if ws > 1 else "cfg4 on 1 GPU (no collective)",
+           "scaling": "strong", "n_gpus": ws}
+    full = gs.counts()
+    for name, m in (("all inter", T.OP_INTER), ("fused 2-opt*+relocate+swap", T.OP_FUSED_NS)):
+        S, REPS = 10, 3
+        for _ in range(3):
+            gs.eval(m, stream)
+        torch.cuda.synchronize(dev)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            for _ in range(S):
+                gs.eval(m, stream)
+        g.replay()
+        torch.cuda.synchronize(dev)
+        if ws > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for _ in range(REPS):
+                g.replay()
+            e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ms = e0.elapsed_time(e1)
+        if ws > 1:
+            t = torch.tensor([ms], device=dev, dtype=torch.float64)
+            reduce_(t, dist.ReduceOp.MAX)
+            ms = float(t.item())
+        keys = gs.keys()
+        per = ms / 1e3 / (S * REPS)
+        cand = int(sum(int(full[v]) for v in range(23) if (m >> v) & 1))   # whole neighbourhood
+        out[name] = {"us_per_sweep": per * 1e6, "sweeps_per_s": 1.0 / per, "moves_per_s": cand / per,
+                     "candidates": cand, "keys_head": [hex(int(k)) for k in keys[1:3]]}
+        del g
+    gs.close()
+    return out
 
 
 def main():

@@ -45,7 +45,7 @@ class _Inst(C.Structure):
     _fields_ = [("n_nodes", C.c_int32), ("C", C.POINTER(C.c_double)),
                 ("demand", C.POINTER(C.c_int64)), ("e", C.POINTER(C.c_double)),
                 ("l", C.POINTER(C.c_double)), ("s", C.POINTER(C.c_double)),
-                ("Q", C.c_int64)]
+                ("Q", C.c_int64), ("pickup", C.POINTER(C.c_int64))]
 
 
 class _Move(C.Structure):
@@ -109,6 +109,8 @@ def lib():
             [P(C.c_double), P(C.c_int64), P(C.c_double)] * 2 + [P(C.c_double)]
         _lib.orc_solution_cost.argtypes = [P(_Inst), C.c_int32, P(C.c_int32), P(C.c_int32),
                                            P(C.c_double), P(C.c_double), P(C.c_double)]
+        _lib.orc_seq_lmax.argtypes = [P(_Inst), P(C.c_int32), C.c_int32]
+        _lib.orc_seq_lmax.restype = C.c_int64
     return _lib
 
 
@@ -120,9 +122,11 @@ class Oracle:
     """Holds one instance (fp64 copies) and evaluates solutions given as
     CSR route arrays (route_ptr int32[R+1], customers int32[N])."""
 
-    def __init__(self, dist, demand, capacity, tw=None):
+    def __init__(self, dist, demand, capacity, tw=None, pickup=None):
         self.dist = np.ascontiguousarray(dist, dtype=np.float64)
         self.demand = np.ascontiguousarray(demand, dtype=np.int64)
+        # VRPSPDTW pickup demands p_i (P:49-50); None => CVRP / VRPTW
+        self.pickup = None if pickup is None else np.ascontiguousarray(pickup, dtype=np.int64)
         self.n = self.dist.shape[0]
         self.tw = None if tw is None else np.ascontiguousarray(tw, dtype=np.float64)
         if self.tw is not None:
@@ -139,11 +143,19 @@ class Oracle:
             self._inst.l = _ptr(self.l, C.c_double)
             self._inst.s = _ptr(self.s, C.c_double)
         self._inst.Q = self.capacity
+        if self.pickup is not None:
+            self._inst.pickup = _ptr(self.pickup, C.c_int64)
         lib()
 
     @classmethod
     def from_instance(cls, inst):
-        return cls(inst.dist, inst.demand, inst.capacity, inst.tw)
+        return cls(inst.dist, inst.demand, inst.capacity, inst.tw, getattr(inst, "pickup", None))
+
+    def seq_lmax(self, nodes) -> int:
+        """The largest load carried along a node sequence served in order (seq_lmax in
+        tga_oracle.c; the delivery sum when the instance has no pickups)."""
+        nd = np.ascontiguousarray(nodes, dtype=np.int32)
+        return int(lib().orc_seq_lmax(C.byref(self._inst), _ptr(nd, C.c_int32), len(nd)))
 
     @staticmethod
     def _csr(routes):

@@ -41,6 +41,7 @@ typedef struct {
     const int64_t *demand;  /* d_i, d_0 = 0 */
     const double *e, *l, *s;/* time windows + service; NULL => CVRP (no time attributes) */
     int64_t Q;              /* capacity */
+    const int64_t *pickup;  /* p_i (VRPSPDTW), p_0 = 0; NULL => no pickups (CVRP / VRPTW) */
 } orc_instance;
 
 typedef struct {
@@ -51,7 +52,29 @@ typedef struct {
     int64_t n_candidates;
 } orc_move;
 
-typedef struct { double D; int64_t L; double TV; } orc_route_val;
+/* L: total delivery sum d over the nodes after the first (the CVRP / VRPTW load);
+ * LM: the largest load the vehicle carries along the route (== L without pickups) */
+typedef struct { double D; int64_t L; double TV; int64_t LM; } orc_route_val;
+
+/* ------------------------------------------------------------------ *
+ * seq_lmax: the maximum load along a node sequence served in order
+ * (VRPSPDTW: "deliver d_i units of goods from the depot v_0 to v_i
+ * and pick up p_i units from v_i back to the depot"): the vehicle enters
+ * carrying every delivery of the sequence, and after serving node k carries
+ * d_k less and p_k more.  The plain definition that Eq. 3a-d
+ * reaches by concatenation; no concatenation here.
+ * ------------------------------------------------------------------ */
+static int64_t seq_lmax(const orc_instance *I, const int32_t *nodes, int len)
+{
+    int64_t load = 0;
+    for (int k = 0; k < len; ++k) load += I->demand[nodes[k]];
+    int64_t m = load;
+    for (int k = 0; k < len; ++k) {
+        load += I->pickup[nodes[k]] - I->demand[nodes[k]];
+        if (load > m) m = load;
+    }
+    return m;
+}
 
 /* ------------------------------------------------------------------ *
  * route_eval: forward simulation of one closed route (SURVEY
@@ -62,7 +85,7 @@ typedef struct { double D; int64_t L; double TV; } orc_route_val;
 static orc_route_val route_eval(const orc_instance *I, const int32_t *nodes, int len,
                                 double *arrival, double *start)
 {
-    orc_route_val r = {0.0, 0, 0.0};
+    orc_route_val r = {0.0, 0, 0.0, 0};
     const int n = I->n_nodes;
     double t = I->e ? I->e[nodes[0]] : 0.0;
     if (arrival) arrival[0] = t;
@@ -80,6 +103,9 @@ static orc_route_val route_eval(const orc_instance *I, const int32_t *nodes, int
             t = st;
         }
     }
+    /* the capacity constraint applies to the largest load carried (Eq. 3a-d); without
+       pickups that is the delivery sum (Eq. 3e-f) */
+    r.LM = I->pickup ? seq_lmax(I, nodes, len) : r.L;
     return r;
 }
 
@@ -178,15 +204,15 @@ static orc_delta delta2(const orc_instance *I, const orc_sol *S, int ra, int rb,
     orc_delta d;
     orc_route_val va = route_eval(I, A, la, NULL, NULL);
     d.dD = va.D - S->val[ra].D;
-    d.dLV = lv(I, va.L) - lv(I, S->val[ra].L);
+    d.dLV = lv(I, va.LM) - lv(I, S->val[ra].LM);
     d.dTV = va.TV - S->val[ra].TV;
-    d.feasible = (va.L <= I->Q) && (va.TV == 0.0);
+    d.feasible = (va.LM <= I->Q) && (va.TV == 0.0);
     if (rb >= 0) {
         orc_route_val vb = route_eval(I, B, lb, NULL, NULL);
         d.dD += vb.D - S->val[rb].D;
-        d.dLV += lv(I, vb.L) - lv(I, S->val[rb].L);
+        d.dLV += lv(I, vb.LM) - lv(I, S->val[rb].LM);
         d.dTV += vb.TV - S->val[rb].TV;
-        d.feasible = d.feasible && (vb.L <= I->Q) && (vb.TV == 0.0);
+        d.feasible = d.feasible && (vb.LM <= I->Q) && (vb.TV == 0.0);
     }
     return d;
 }
@@ -534,10 +560,21 @@ int orc_solution_cost(const orc_instance *I, int32_t R, const int32_t *ptr, cons
     if (sol_build(I, R, ptr, cust, &S) != 0) { sol_free(&S); return -2; }
     *D = 0; *LV = 0; *TV = 0;
     for (int r = 0; r < S.R; ++r) {
-        *D += S.val[r].D; *LV += lv(I, S.val[r].L); *TV += S.val[r].TV;
+        *D += S.val[r].D; *LV += lv(I, S.val[r].LM); *TV += S.val[r].TV;
     }
     sol_free(&S);
     return 0;
 }
 
 int orc_n_variants(void) { return V_COUNT; }
+
+/* the maximum load along a node sequence (seq_lmax; for pins of the VRPSPDTW loads) */
+int64_t orc_seq_lmax(const orc_instance *I, const int32_t *nodes, int32_t len)
+{
+    if (!I->pickup) {
+        int64_t s = 0;
+        for (int k = 0; k < len; ++k) s += I->demand[nodes[k]];
+        return s;
+    }
+    return seq_lmax(I, nodes, len);
+}

@@ -21,12 +21,19 @@ import math
 from typing import Dict, List, Tuple
 
 
-def simulate(dist, demand, tw, route):
+def simulate(dist, demand, tw, route, pickup=None):
     """Event simulation of one route given as customers only (depot implicit).
-    Returns (distance, load, time_warp)."""
+    Returns (distance, load, time_warp).  load = the delivery sum (CVRP / VRPTW) or,
+    with pickups (VRPSPDTW), the largest load carried: after serving the
+    first k customers the vehicle holds the deliveries of the others and the pickups
+    of these, max over k = 0..L (a closed form, not the oracle's running simulation)."""
     nodes = [0] + list(route) + [0]
     D = sum(dist[nodes[k]][nodes[k + 1]] for k in range(len(nodes) - 1))
-    L = sum(demand[c] for c in route)
+    if pickup is None:
+        L = sum(demand[c] for c in route)
+    else:
+        L = max(sum(demand[c] for c in route[k:]) + sum(pickup[c] for c in route[:k])
+                for k in range(len(route) + 1))
     TV = 0.0
     if tw is not None:
         t = tw[0][0]
@@ -153,13 +160,13 @@ def neighbours(routes: List[List[int]], op: str, n1: int = 1, n2: int = 1, keyed
 
 
 def scores(dist, demand, tw, capacity, routes, op, n1=1, n2=1, mode=0, wQ=10.0, wT=10.0, mask=None,
-           with_index=False):
+           with_index=False, pickup=None):
     """List of scores of every neighbour (feasible-only: inf if infeasible).
     mask: inter-route neighbours only where mask[pair] is set (edge-based, ETGA).
     with_index: (score, u, v) triples with the canonical slot pair of each move."""
     cur = {}
     for idx, r in enumerate(routes):
-        cur[idx] = simulate(dist, demand, tw, r)
+        cur[idx] = simulate(dist, demand, tw, r, pickup)
     out = []
     for item in neighbours(routes, op, n1, n2, keyed=True, indexed=True):
         ids, news, pair, uv = item
@@ -168,7 +175,7 @@ def scores(dist, demand, tw, capacity, routes, op, n1=1, n2=1, mode=0, wQ=10.0, 
         dD = dLV = dTV = 0.0
         feas = True
         for rid, nr in zip(ids, news):
-            D, L, TV = simulate(dist, demand, tw, nr)
+            D, L, TV = simulate(dist, demand, tw, nr, pickup)
             D0, L0, TV0 = cur[rid]
             dD += D - D0
             dLV += max(L - capacity, 0) - max(L0 - capacity, 0)

@@ -446,3 +446,122 @@ def test_enumerate_full_feasibility_and_band(seed):
             assert sorted(bt) == got, (op, n1, n2, mode)
             nb += int(bd.sum())
     assert nb > 0, "the instance must exercise the band"
+
+
+# ---------------------------------------------------------------- VRPSPDTW loads
+PD_GOLD = json.load(open(os.path.join(GOLD, "pickup_delivery.json")))["examples"]
+
+
+@pytest.mark.parametrize("ex", PD_GOLD, ids=lambda e: e["name"])
+def test_pickup_delivery_hand_worked(ex):
+    """Hand-worked maximum loads (golden, P:49-50 and Eq. 3a-d): the
+    oracle's L_M of the route, and through it the capacity test: feasible iff
+    L_M <= Q (the 'capacity-order' pair: the same customers, one order over Q = 16,
+    the other within it)."""
+    n = len(ex["demand"])
+    coords = [[50, 50]] + [[10 * k, 5 * k] for k in range(1, n)]
+    dist = G.euclid_nint(np.asarray(coords))
+    orc = O.Oracle(dist, np.asarray(ex["demand"]), 16, None, np.asarray(ex["pickup"]))
+    assert orc.seq_lmax([0] + ex["route"] + [0]) == ex["lmax"]
+    assert max(ex["loads"]) == ex["lmax"]
+    D, L, TV = None, None, None
+    cost = orc.cost([ex["route"]])
+    assert cost[1] == max(ex["lmax"] - 16, 0)       # load excess of the single route
+
+
+def _pd_tiny(seed, tw=True):
+    rng = np.random.default_rng(900 + seed)
+    dist, demand, twa, cap, sol = _tiny(seed, tw)
+    n = len(demand) - 1
+    pickup = np.concatenate([[0], rng.integers(0, 21, size=n)]).astype(np.int32)
+    demand = demand.copy()
+    demand[1:] = rng.integers(0, 21, size=n)
+    return dist, demand, pickup, twa, cap, sol
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_pickup_delivery_closed_forms(seed):
+    """seq_lmax against three closed forms (no running simulation): without
+    pickups it is the delivery sum (Eq. 3e-f); without deliveries the pickup sum;
+    in general max over k of (deliveries of the customers after the first k +
+    pickups of the first k)."""
+    dist, demand, pickup, twa, cap, sol = _pd_tiny(seed)
+    rng = np.random.default_rng(seed)
+    for r in sol.routes + [list(rng.permutation(np.arange(1, len(demand))))]:
+        r = [int(c) for c in r]
+        nodes = [0] + r + [0]
+        zero = np.zeros_like(pickup)
+        assert O.Oracle(dist, demand, cap, None, zero).seq_lmax(nodes) == sum(int(demand[c]) for c in r)
+        assert O.Oracle(dist, zero, cap, None, pickup).seq_lmax(nodes) == sum(int(pickup[c]) for c in r)
+        exp = max(sum(int(demand[c]) for c in r[k:]) + sum(int(pickup[c]) for c in r[:k]) for k in range(len(r) + 1))
+        assert O.Oracle(dist, demand, cap, None, pickup).seq_lmax(nodes) == exp
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_pickup_delivery_concatenation_rule(seed):
+    """Eq. 3a-d -- the method's O(1) concatenation of (L_I, L_O, L_M),
+    written here from the paper -- reaches the oracle's simulated L_M for every
+    split of random sequences into two and three parts (the associativity the
+    prefix / suffix records rely on)."""
+    dist, demand, pickup, twa, cap, sol = _pd_tiny(seed)
+    orc = O.Oracle(dist, demand, cap, None, pickup)
+    rng = np.random.default_rng(50 + seed)
+
+    def single(k):
+        return (int(demand[k]), int(pickup[k]), max(int(demand[k]), int(pickup[k])))   # Eq. 3a
+
+    def cat(a, b):   # Eq. 3b-d
+        return (a[0] + b[0], a[1] + b[1], max(a[2] + b[0], a[1] + b[2]))
+
+    def rec(seq):
+        r = single(seq[0])
+        for k in seq[1:]:
+            r = cat(r, single(k))
+        return r
+
+    for _ in range(20):
+        seq = [int(x) for x in rng.permutation(np.arange(1, len(demand)))[: int(rng.integers(1, len(demand)))]]
+        full = rec(seq)
+        assert full[2] == orc.seq_lmax(seq)
+        for i in range(1, len(seq)):
+            assert cat(rec(seq[:i]), rec(seq[i:]))[2] == orc.seq_lmax(seq)
+            for j in range(i + 1, len(seq)):
+                assert cat(cat(rec(seq[:i]), rec(seq[i:j])), rec(seq[j:]))[2] == orc.seq_lmax(seq)
+
+
+@pytest.mark.parametrize("seed", range(8))
+@pytest.mark.parametrize("mode", [0, 1])
+def test_pickup_delivery_brute_force_neighbourhood(seed, mode):
+    """VRPSPDTW (pickups + time windows): every variant's (score, u, v) multiset ==
+    the brute force, whose load is the max-over-k closed form; best == min.
+    2-opt is excluded: the paper applies it to the CVRP only."""
+    dist, demand, pickup, twa, cap, sol = _pd_tiny(seed, tw=True)
+    orc = O.Oracle(dist, demand, cap, twa, pickup)
+    Q = O.canonical_q(sol.routes)
+    for op, n1, n2, var in BRUTE_OPS:
+        if var == O.V_2OPT:
+            continue
+        bt = brute.scores(dist.tolist(), demand.tolist(), twa.tolist(), cap, sol.routes, op, n1, n2, mode,
+                          with_index=True, pickup=pickup.tolist())
+        sc, us, vs, best = orc.enumerate(sol.routes, var, mode)
+        assert sorted(bt) == sorted(zip(sc.tolist(), us.tolist(), vs.tolist())), (op, n1, n2)
+        bb = brute.best(bt, Q)
+        assert best.found == (bb is not None)
+        if bb is not None:
+            assert (best.score, best.u * Q + best.v) == bb, (op, n1, n2)
+
+
+def test_pickup_delivery_changes_feasibility():
+    """The pickups matter: on a JD-like instance some candidates that are feasible
+    with the deliveries alone (CVRP / VRPTW loads) are infeasible with the pickups,
+    and the counts of feasible candidates differ."""
+    inst, sol = G.jd_like(1, n=60)
+    with_p = O.Oracle.from_instance(inst)
+    without = O.Oracle(inst.dist, inst.demand, inst.capacity, inst.tw)
+    diff = 0
+    for v in (O.V_2OPT_STAR, O.V_RELOC[1], O.V_SWAP[(1, 1)]):
+        a = np.isfinite(with_p.enumerate(sol.routes, v)[0]).sum()
+        b = np.isfinite(without.enumerate(sol.routes, v)[0]).sum()
+        assert a <= b
+        diff += b - a
+    assert diff > 0

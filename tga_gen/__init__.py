@@ -36,7 +36,7 @@ import numpy as np
 __all__ = [
     "Instance", "Solution", "euclid_nint", "euclid_tenths", "euclid_f32",
     "cvrp_small", "x_like", "gh_like", "large_cvrp", "population",
-    "random_partition", "perturb", "config", "CONFIGS",
+    "random_partition", "perturb", "config", "CONFIGS", "jd_like",
 ]
 
 MODE_CVRP = "cvrp"   # integer distances, no time windows
@@ -52,6 +52,8 @@ class Instance:
     demand:   (n+1,) int32, demand[0] == 0
     tw:       (n+1, 3) float64 [e, l, s] or None (CVRP); travel time == dist
     capacity: vehicle capacity Q
+    pickup:   (n+1,) int32 pickup demands p_i (VRPSPDTW, P:49-50), pickup[0] == 0;
+              None for CVRP / VRPTW (p_i = 0)
     """
     name: str
     mode: str
@@ -60,6 +62,7 @@ class Instance:
     demand: np.ndarray
     capacity: int
     tw: Optional[np.ndarray] = None
+    pickup: Optional[np.ndarray] = None
 
     @property
     def n_nodes(self) -> int:
@@ -342,6 +345,53 @@ def gh_like(seed: int = 0, n: int = 1000, kind: str = "R1", density: float = 1.0
     return inst, Solution(routes)
 
 
+def _max_load(route, demand, pickup):
+    """Largest load carried along a route (instance construction only): after the
+    first k customers the vehicle holds the deliveries of the rest and the pickups
+    of these."""
+    return max(int(demand[route[k:]].sum()) + int(pickup[route[:k]].sum()) for k in range(len(route) + 1))
+
+
+def jd_like(seed: int = 0, n: int = 1000, mode: str = MODE_TWI, spare: int = 1,
+            route_len: int = 14, capacity: int = 200):
+    """VRPSPDTW shaped like the JD benchmark ("20 JD benchmark instances ...
+    based on real-world JD Logistics data with 200, 400, 600, 800, and 1000
+    customers"; Liu et al. 2021; the data is not in the reference): random-clustered
+    customers around a central depot, every customer with a delivery d_i and a
+    pickup p_i, GH-like time windows placed around a reference schedule
+    (so the start solution is time-feasible), service 10.  The reference routes are
+    an angular sweep cut where the route's largest load would exceed Q (so the start
+    is capacity-feasible and loads are tight) or at route_len customers."""
+    rng = np.random.default_rng(6000 + seed)
+    grid = 500 if n >= 600 else 250
+    coords = _uchoa_coords(rng, n, grid, "central", "random-clustered")
+    demand = np.zeros(n + 1, dtype=np.int32)
+    pickup = np.zeros(n + 1, dtype=np.int32)
+    demand[1:] = rng.integers(0, 41, size=n)
+    pickup[1:] = rng.integers(0, 41, size=n)
+    scale = 10.0 if mode == MODE_TWI else 1.0
+    dist = _dist_for_mode(coords, mode)
+    c = coords[1:] - coords[0]
+    ang = np.mod(np.arctan2(c[:, 1], c[:, 0]) - rng.uniform(-math.pi, math.pi), 2 * math.pi)
+    routes: List[List[int]] = []
+    cur: List[int] = []
+    for i in (np.argsort(ang, kind="stable") + 1):
+        trial = np.array(cur + [int(i)], dtype=np.int64)
+        if cur and (len(cur) >= route_len or _max_load(trial, demand, pickup) > capacity):
+            routes.append(cur)
+            cur = []
+        cur.append(int(i))
+    if cur:
+        routes.append(cur)
+    service = 10.0 * scale
+    tw = _tw_around_schedule(rng, dist, routes, service, 1.0, 100.0 * scale, 300.0 * scale,
+                             n + 1, 1.15, integer=(mode == MODE_TWI))
+    inst = Instance(f"JD-like-n{n}-{mode}-s{seed}", mode, coords, dist, demand, capacity, tw,
+                    pickup=pickup)
+    routes += [[] for _ in range(spare)]
+    return inst, Solution(routes)
+
+
 def population(seed: int = 0, n: int = 200, n_sol: int = 1024, mode: str = MODE_TWI):
     """BASELINE config 5: one R1_2-like instance (200 customers, Q=200,
     ~18-23 routes) and n_sol solutions: the reference construction plus
@@ -362,6 +412,8 @@ CONFIGS = {
     "cfg4s": "large CVRP 10000 customers, mean route length 23",
     "ns2000": "X-like CVRP, 2000 customers, 87 routes (north-star sweep)",
     "cfg5": "population 1024 x VRPTW 200 customers (R1_2-like, TW-I)",
+    "jd": "JD-like VRPSPDTW, 1000 customers (delivery + pickup, time windows, TW-I)",
+    "jd200": "JD-like VRPSPDTW, 200 customers (delivery + pickup, time windows, TW-I)",
 }
 
 
@@ -385,4 +437,8 @@ def config(name: str, seed: int = 0):
         return large_cvrp(seed, n=10000, mean_len=23)
     if name == "cfg5":
         return population(seed)
+    if name == "jd":
+        return jd_like(seed, n=1000)
+    if name == "jd200":
+        return jd_like(seed, n=200)
     raise KeyError(name)

@@ -550,6 +550,9 @@ def run_tga(args):
     if args.granular:
         kname = ("k_etga<" + ("TW, " if inst.tw is not None else "") + "all-inter> (+ k_slot_of after a host "
                  "layout): the edge-mask cells; intra variants in their own kernels")
+    elif getattr(inst, "pickup", None) is not None:
+        kname = ("k_inter<TW, all-inter> (VRPSPDTW: generic tile kernel with the Eq. 3a-d load records; "
+                 "intra in its own kernel)")
     elif inst.tw is None:
         kname = "k_inter_fast<all-inter> (CVRP: inter tiles + intra warps in one launch)"
     else:

@@ -153,6 +153,17 @@ typedef struct {
 int32_t tga_instance_create(int32_t n_nodes, const void *dist, int32_t dist_dtype,
                             const void *time, const int32_t *demand, const float *tw,
                             int32_t capacity, const tga_options *opt, tga_instance **out);
+/* VRPSPDTW pickup demands ("the vehicle must deliver d_i units of goods
+ * from the depot v_0 to v_i and pick up p_i units from v_i back to the depot"; load
+ * attributes L_I, L_O, L_M of Eq. 3a-d).
+ *   pickup: host int32[n_nodes], p_0 == 0, p_i >= 0; copied (caller keeps ownership).
+ * With pickups the capacity constraint (and the load excess of the penalised score) is
+ * on the largest load a route carries; evaluation takes the generic kernels (the fast
+ * paths assume delivery sums) and 2-opt is unsupported (the paper applies it to the CVRP
+ * only).  Must be called before any solution of the instance is loaded.
+ * Errors: TGA_ERR_INVALID_ARGUMENT (NULL, p_0 != 0, p_i < 0, sum >= 2^30, solutions
+ * already loaded), TGA_ERR_CUDA. */
+int32_t tga_instance_set_pickup(tga_instance *inst, const int32_t *pickup);
 int32_t tga_instance_destroy(tga_instance *inst);
 /* n_nodes, granular_theta and the number of unordered customer pairs the edge
  * mask keeps (0 without a granular neighbourhood).  Any pointer may be NULL. */
@@ -275,6 +286,10 @@ int32_t tga_solution_info(const tga_solution *sol, int32_t *n_routes, int32_t *n
 int32_t tga_solution_attributes(tga_solution *sol, int64_t *pre_L, int64_t *suf_L,
                                 double *pre_D, double *suf_D, double *pre_TV,
                                 double *suf_TV, double *start);
+/* VRPSPDTW load records for parity (Eq. 3a-d), per CANONICAL slot c (Q = N + R):
+ * pre[3c .. 3c+2] = (L_I, L_O, L_M) of the prefix [0..p] of its route, suf[...] = those of
+ * the suffix [p..L+1].  Caller-owned int32[3 Q] each.  TGA_ERR_UNSUPPORTED without pickups. */
+int32_t tga_solution_load_records(tga_solution *sol, int32_t *pre, int32_t *suf);
 
 /* ------------------------------------------------------------ multi-GPU
  * Row sharding: a solution with a shard plan (n_shards > 1) evaluates only

@@ -42,6 +42,18 @@ __host__ __device__ __forceinline__ TwRec tw_single(float e, float l, float s) {
     return make_float4(s, e, l, 0.0f);
 }
 
+// ------------------------------------------------------------------ pickup and delivery loads
+// Eq. 3a-d: a subsequence's incoming load L_I (its deliveries), outgoing
+// load L_O (its pickups) and largest load L_M; x = L_I, y = L_O, z = L_M, w unused.
+using LoadRec = int4;
+__host__ __device__ __forceinline__ LoadRec ld_single(int32_t d, int32_t p) {   // Eq. 3a
+    return make_int4(d, p, d > p ? d : p, 0);
+}
+__host__ __device__ __forceinline__ LoadRec ld_cat(const LoadRec a, const LoadRec b) {   // Eq. 3b-d
+    const int32_t m1 = a.z + b.x, m2 = a.y + b.z;
+    return make_int4(a.x + b.x, a.y + b.y, m1 > m2 ? m1 : m2, 0);
+}
+
 // ------------------------------------------------------------------ keys
 // Order-preserving 32-bit images of a score.
 __device__ __forceinline__ uint32_t ord_score(int32_t s) { return static_cast<uint32_t>(s) ^ 0x80000000u; }
@@ -168,8 +180,11 @@ struct SolView {
     // time-window records: prefix, suffix, segments of 2 and 3 starting at x
     const TwRec *fwdT, *bwdT, *seg2T, *seg3T;
     const TwRec *node_tw;     // per node: (s, e, l, 0)
+    // VRPSPDTW (null without pickups): node demands d_i / p_i, prefix / suffix Eq. 3 load records
+    const int32_t *dem, *pick;
+    const LoadRec *fwdP, *bwdP;
     // per route
-    const int32_t *rW;        // load
+    const int32_t *rW;        // load (the largest load carried, L_M, with pickups)
     const float *rTV;         // time warp
     // position-ordered distance matrix Dp[a][b] = c(node(a), node(b))
     const DT *Dp;

@@ -95,6 +95,7 @@ __device__ __forceinline__ int scan_fwd_pass(const ScanArgs<DT> &A, const int r,
     const int n = A.n_nodes;
     // ---------------- forward pass: prefix loads, prefix distance, prefix TW records
     int carryL = 0;
+    LoadRec carryP = make_int4(0, 0, 0, 0);   // VRPSPDTW prefix record of the chunks so far
     DT carryD = DT(0);
     TwRec carryT = make_float4(0.f, 0.f, 0.f, 0.f);
     DT carryE = DT(0);  // edge into the first position of the chunk
@@ -136,6 +137,24 @@ __device__ __forceinline__ int scan_fwd_pass(const ScanArgs<DT> &A, const int r,
             }
             fT = (c0 > 0) ? tw_cat(carryT, rec, inl) : rec;
         }
+        if (A.pickup) {   // VRPSPDTW: inclusive prefix scan of the Eq. 3a-d load records (warp-uniform branch)
+            LoadRec pr = in ? ld_single(A.demand[nd], A.pickup[nd]) : make_int4(0, 0, 0, 0);
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                LoadRec o;
+                o.x = __shfl_up_sync(0xffffffffu, pr.x, off);
+                o.y = __shfl_up_sync(0xffffffffu, pr.y, off);
+                o.z = __shfl_up_sync(0xffffffffu, pr.z, off);
+                o.w = 0;
+                if (lane >= off) pr = ld_cat(o, pr);
+            }
+            if (c0 > 0) pr = ld_cat(carryP, pr);
+            if (in) A.fwdP[x] = pr;
+            const int lst = min(31, len - 1 - c0);
+            carryP.x = __shfl_sync(0xffffffffu, pr.x, lst);
+            carryP.y = __shfl_sync(0xffffffffu, pr.y, lst);
+            carryP.z = __shfl_sync(0xffffffffu, pr.z, lst);
+        }
         if (in) {
             A.fwdL[x] = fL;
             A.fwdD[x] = fD;
@@ -153,12 +172,15 @@ __device__ __forceinline__ int scan_fwd_pass(const ScanArgs<DT> &A, const int r,
             carryT.w = __shfl_sync(0xffffffffu, fT.w, last);
         }
     }
+    // the route's load: the delivery sum (Eq. 3e-f), or with pickups the largest load
+    // carried, L_M of the whole route (Eq. 3a-d) -- what the capacity constraint bounds
+    const int Wr = A.pickup ? carryP.z : carryL;
     if (lane == 0) {
-        A.rW[r] = carryL;
+        A.rW[r] = Wr;
         if (TW) A.rTV[r] = carryT.w;
     }
 
-    return carryL;   // route load (Eq. 3f over the whole route)
+    return Wr;
 }
 
 template <class DT, bool TW, class NodeF>
@@ -168,6 +190,7 @@ __device__ __forceinline__ void scan_bwd_pass(const ScanArgs<DT> &A, const int r
     const int n = A.n_nodes;
     // ---------------- backward pass: suffix loads, suffix distance, suffix TW records
     int bcarryL = 0;
+    LoadRec bcarryP = make_int4(0, 0, 0, 0);
     DT bcarryD = DT(0);
     TwRec bcarryT = make_float4(0.f, 0.f, 0.f, 0.f);
     const int nchunks = (len + 31) / 32;
@@ -207,6 +230,23 @@ __device__ __forceinline__ void scan_bwd_pass(const ScanArgs<DT> &A, const int r
                 if (lane + off < nvalid) { rec = tw_cat(rec, o, outl); outl = oout; }
             }
             bT = (ci < nchunks - 1) ? tw_cat(rec, bcarryT, outl) : rec;
+        }
+        if (A.pickup) {   // VRPSPDTW: inclusive suffix scan of the Eq. 3a-d load records
+            LoadRec pr = in ? ld_single(A.demand[nd], A.pickup[nd]) : make_int4(0, 0, 0, 0);
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                LoadRec o;
+                o.x = __shfl_down_sync(0xffffffffu, pr.x, off);
+                o.y = __shfl_down_sync(0xffffffffu, pr.y, off);
+                o.z = __shfl_down_sync(0xffffffffu, pr.z, off);
+                o.w = 0;
+                if (lane + off < nvalid) pr = ld_cat(pr, o);
+            }
+            if (ci < nchunks - 1) pr = ld_cat(pr, bcarryP);
+            if (in) A.bwdP[x] = pr;
+            bcarryP.x = __shfl_sync(0xffffffffu, pr.x, 0);
+            bcarryP.y = __shfl_sync(0xffffffffu, pr.y, 0);
+            bcarryP.z = __shfl_sync(0xffffffffu, pr.z, 0);
         }
         if (in) {
             A.bwdL[x] = bL;
@@ -830,6 +870,15 @@ __device__ __forceinline__ void inter_tile(const SolView<DT> &S, const DT *__res
             if (in_space) dump_put(dump, S.Qc * S.Qc, var, idx, k);
         }
     };
+    // VRPSPDTW (S.fwdP != null; a warp-uniform branch): the load a new route is checked
+    // with is its largest load L_M, concatenated from the prefix / segment / suffix
+    // records (Eq. 3a-d) instead of the delivery sums
+    const bool pd = S.fwdP != nullptr;
+    auto segP = [&](int x, int N) -> LoadRec {   // slots x..x+N-1
+        LoadRec r = ld_single(S.dem[S.node[x]], S.pick[S.node[x]]);
+        for (int k = 1; k < N; ++k) r = ld_cat(r, ld_single(S.dem[S.node[x + k]], S.pick[S.node[x + k]]));
+        return r;
+    };
 #pragma unroll 1
     for (int j = 0; j < VPT; ++j) {
         const int v = v0 + lane + 32 * j;
@@ -858,8 +907,12 @@ __device__ __forceinline__ void inter_tile(const SolView<DT> &S, const DT *__res
             // ---- 2-opt* (3-Seq(0,0) P:346; Eq. 14)
             if (MASK & (1u << 1)) {
                 const DT dD = Dt(u, v + 1) + Dt(u + 1, v) - S.enext[u] - S.enext[v];
-                const int la = S.fwdL[u] + S.bwdL[v + 1];
-                const int lb = S.fwdL[v] + S.bwdL[u + 1];
+                int la = S.fwdL[u] + S.bwdL[v + 1];
+                int lb = S.fwdL[v] + S.bwdL[u + 1];
+                if (pd && pair) {
+                    la = ld_cat(S.fwdP[u], S.bwdP[v + 1]).z;
+                    lb = ld_cat(S.fwdP[v], S.bwdP[u + 1]).z;
+                }
                 float ta = 0.f, tb = 0.f;
                 if (TW) {
                     ta = tw_cat(S.fwdT[u], S.bwdT[v + 1], static_cast<float>(Dt(u, v + 1))).w;
@@ -878,6 +931,11 @@ __device__ __forceinline__ void inter_tile(const SolView<DT> &S, const DT *__res
                     const DT dD = bridge[u] - S.enext[u - 1] - S.enext[u + N - 1] + Dt(u, v) +
                                   Dt(u + N - 1, v + 1) - S.enext[v];
                     const int s = S.fwdL[u + N - 1] - S.fwdL[u - 1];
+                    int la = Wa - s, lb = Wb + s;
+                    if (pd && ok) {
+                        la = ld_cat(S.fwdP[u - 1], S.bwdP[u + N]).z;
+                        lb = ld_cat(ld_cat(S.fwdP[v], segP(u, N)), S.bwdP[v + 1]).z;
+                    }
                     float ta = 0.f, tb = 0.f;
                     if (TW) {
                         const TwRec sg = N == 1 ? S.node_tw[S.node[u]] : segT[u];
@@ -885,13 +943,18 @@ __device__ __forceinline__ void inter_tile(const SolView<DT> &S, const DT *__res
                         const TwRec X = tw_cat(S.fwdT[v], sg, static_cast<float>(Dt(u, v)));
                         tb = tw_cat(X, S.bwdT[v + 1], static_cast<float>(Dt(u + N - 1, v + 1))).w;
                     }
-                    take(1 + N, score_key<DT, TW>(sp, ok, dD, Wa - s, Wb + s, Wa, Wb, ta, tb, TVa, TVb, idx_uv), idx_uv, pair);
+                    take(1 + N, score_key<DT, TW>(sp, ok, dD, la, lb, Wa, Wb, ta, tb, TVa, TVb, idx_uv), idx_uv, pair);
                 }
                 {   // segment v..v+N-1 (route b) inserted after u (route a)
                     const bool ok = pair && pv >= 1 && pv + N - 1 <= Lb;
                     const DT dD = bridge[v] - S.enext[v - 1] - S.enext[v + N - 1] + Dt(u, v) +
                                   Dt(u + 1, v + N - 1) - S.enext[u];
                     const int s = S.fwdL[v + N - 1] - S.fwdL[v - 1];
+                    int la = Wa + s, lb = Wb - s;
+                    if (pd && ok) {
+                        lb = ld_cat(S.fwdP[v - 1], S.bwdP[v + N]).z;
+                        la = ld_cat(ld_cat(S.fwdP[u], segP(v, N)), S.bwdP[u + 1]).z;
+                    }
                     float ta = 0.f, tb = 0.f;
                     if (TW) {
                         const TwRec sg = N == 1 ? S.node_tw[S.node[v]] : segT[v];
@@ -899,7 +962,7 @@ __device__ __forceinline__ void inter_tile(const SolView<DT> &S, const DT *__res
                         const TwRec X = tw_cat(S.fwdT[u], sg, static_cast<float>(Dt(u, v)));
                         ta = tw_cat(X, S.bwdT[u + 1], static_cast<float>(Dt(u + 1, v + N - 1))).w;
                     }
-                    take(1 + N, score_key<DT, TW>(sp, ok, dD, Wa + s, Wb - s, Wa, Wb, ta, tb, TVa, TVb, idx_vu), idx_vu, pair);
+                    take(1 + N, score_key<DT, TW>(sp, ok, dD, la, lb, Wa, Wb, ta, tb, TVa, TVb, idx_vu), idx_vu, pair);
                 }
             }
             // ---- swap (1,1) / cross-exchange (N1,N2) (3-Seq(N1,N2) P:346)
@@ -918,6 +981,11 @@ __device__ __forceinline__ void inter_tile(const SolView<DT> &S, const DT *__res
                                   S.enext[u - 1] - S.enext[u + N1 - 1] - S.enext[v - 1] - S.enext[v + N2 - 1];
                     const int sa = S.fwdL[u + N1 - 1] - S.fwdL[u - 1];
                     const int sb = S.fwdL[v + N2 - 1] - S.fwdL[v - 1];
+                    int la = Wa - sa + sb, lb = Wb - sb + sa;
+                    if (pd && ok) {   // A' = F(u-1) + seg(v,N2) + B(u+N1), B' = F(v-1) + seg(u,N1) + B(v+N2)
+                        la = ld_cat(ld_cat(S.fwdP[u - 1], segP(v, N2)), S.bwdP[u + N1]).z;
+                        lb = ld_cat(ld_cat(S.fwdP[v - 1], segP(u, N1)), S.bwdP[v + N2]).z;
+                    }
                     float ta = 0.f, tb = 0.f;
                     if (TW) {
                         const TwRec A1 = tw_cat(S.fwdT[u - 1], seg(v, N2), static_cast<float>(Dt(u - 1, v)));
@@ -925,7 +993,7 @@ __device__ __forceinline__ void inter_tile(const SolView<DT> &S, const DT *__res
                         const TwRec B1 = tw_cat(S.fwdT[v - 1], seg(u, N1), static_cast<float>(Dt(u, v - 1)));
                         tb = tw_cat(B1, S.bwdT[v + N2], static_cast<float>(Dt(u + N1 - 1, v + N2))).w;
                     }
-                    take(vid, score_key<DT, TW>(sp, ok, dD, Wa - sa + sb, Wb - sb + sa, Wa, Wb, ta, tb, TVa, TVb, idx_uv),
+                    take(vid, score_key<DT, TW>(sp, ok, dD, la, lb, Wa, Wb, ta, tb, TVa, TVb, idx_uv),
                          idx_uv, pair);
                 }
                 if (N1 != N2) {   // N1-segment at v (route b), N2-segment at u (route a)
@@ -934,6 +1002,11 @@ __device__ __forceinline__ void inter_tile(const SolView<DT> &S, const DT *__res
                                   S.enext[v - 1] - S.enext[v + N1 - 1] - S.enext[u - 1] - S.enext[u + N2 - 1];
                     const int sb = S.fwdL[v + N1 - 1] - S.fwdL[v - 1];
                     const int sa = S.fwdL[u + N2 - 1] - S.fwdL[u - 1];
+                    int la = Wa - sa + sb, lb = Wb - sb + sa;
+                    if (pd && ok) {   // B' = F(v-1) + seg(u,N2) + B(v+N1), A' = F(u-1) + seg(v,N1) + B(u+N2)
+                        lb = ld_cat(ld_cat(S.fwdP[v - 1], segP(u, N2)), S.bwdP[v + N1]).z;
+                        la = ld_cat(ld_cat(S.fwdP[u - 1], segP(v, N1)), S.bwdP[u + N2]).z;
+                    }
                     float ta = 0.f, tb = 0.f;
                     if (TW) {
                         const TwRec B1 = tw_cat(S.fwdT[v - 1], seg(u, N2), static_cast<float>(Dt(u, v - 1)));
@@ -941,7 +1014,7 @@ __device__ __forceinline__ void inter_tile(const SolView<DT> &S, const DT *__res
                         const TwRec A1 = tw_cat(S.fwdT[u - 1], seg(v, N1), static_cast<float>(Dt(u - 1, v)));
                         ta = tw_cat(A1, S.bwdT[u + N2], static_cast<float>(Dt(u + N2, v + N1 - 1))).w;
                     }
-                    take(vid, score_key<DT, TW>(sp, ok, dD, Wa - sa + sb, Wb - sb + sa, Wa, Wb, ta, tb, TVa, TVb, idx_vu),
+                    take(vid, score_key<DT, TW>(sp, ok, dD, la, lb, Wa, Wb, ta, tb, TVa, TVb, idx_vu),
                          idx_vu, pair);
                 }
             }
@@ -1110,18 +1183,27 @@ __device__ __forceinline__ void intra_body(const SolView<DT> &S, const ScorePara
         auto seg = [&](int a, int N) -> TwRec {
             return N == 1 ? S.node_tw[S.node[a]] : (N == 2 ? S.seg2T[a] : S.seg3T[a]);
         };
-        auto key = [&](DT dD, float tv, int q) -> uint64_t {
+        // la: the new route's load -- unchanged by an intra-route move without pickups
+        // (the delivery sum), its largest load L_M with them (VRPSPDTW, Eq. 3a-d)
+        auto key = [&](DT dD, float tv, int q, int la) -> uint64_t {
             const uint32_t idx = static_cast<uint32_t>(x) * S.Qc + static_cast<uint32_t>(base + q);
-            const uint64_t k = score_key<DT, TW>(sp, true, dD, W, 0, W, 0, tv, 0.f, TV0, 0.f, idx);
+            const uint64_t k = score_key<DT, TW>(sp, true, dD, la, 0, W, 0, tv, 0.f, TV0, 0.f, idx);
             if constexpr (DUMP) dump_put(dump, S.Qc * S.Qc, var, idx, k);
             return k;
+        };
+        const bool pd = S.fwdP != nullptr;   // warp-uniform
+        auto ldn = [&](int slot) -> LoadRec { return ld_single(S.dem[S.node[slot]], S.pick[S.node[slot]]); };
+        auto segP = [&](int a, int N) -> LoadRec {
+            LoadRec r = ldn(a);
+            for (int k = 1; k < N; ++k) r = ld_cat(r, ldn(a + k));
+            return r;
         };
         if (var == 0) {
             // 2-opt: reverse u..v (Eq. 7); loads unchanged; CVRP only (host-checked)
             for (int q = p + 1; q <= L; ++q) {
                 const int v = base + q;
                 const DT dD = D(x - 1, v) + D(x, v + 1) - E(x - 1) - E(v);
-                best = umin64(best, key(dD, 0.f, q));
+                best = umin64(best, key(dD, 0.f, q, W));
             }
         } else if (var <= 13) {
             // intra relocate / or-opt of x..x+N-1 after the node originally at q
@@ -1137,16 +1219,22 @@ __device__ __forceinline__ void intra_body(const SolView<DT> &S, const ScorePara
                     const float br = static_cast<float>(N == 1 ? S.bridge1[x] : (N == 2 ? S.bridge2[x] : S.bridge3[x]));
                     if (p + N <= L) P = tw_cat(S.fwdT[x - 1], S.node_tw[S.node[x + N]], br);
                 }
+                LoadRec PP = make_int4(0, 0, 0, 0), sgP = PP;   // VRPSPDTW: F(u-1) + [u+N..q], the segment
+                if (pd) {
+                    sgP = segP(x, N);
+                    if (p + N <= L) PP = ld_cat(S.fwdP[x - 1], ldn(x + N));
+                }
                 for (int q = p + N; q <= L; ++q) {
                     const int v = base + q;
                     if (TW && q > p + N) P = tw_cat(P, S.node_tw[S.node[v]], static_cast<float>(E(v - 1)));
+                    if (pd && q > p + N) PP = ld_cat(PP, ldn(v));
                     const DT dD = rem + D(v, x) + D(x + N - 1, v + 1) - E(v);
                     float tv = 0.f;
                     if (TW) {
                         const TwRec A2 = tw_cat(P, sg, static_cast<float>(D(v, x)));
                         tv = tw_cat(A2, S.bwdT[v + 1], static_cast<float>(D(x + N - 1, v + 1))).w;
                     }
-                    best = umin64(best, key(dD, tv, q));
+                    best = umin64(best, key(dD, tv, q, pd ? ld_cat(ld_cat(PP, sgP), S.bwdP[v + 1]).z : W));
                 }
                 // backward: route' = [0..q] + seg + [q+1..u-1] + [u+N..]
                 TwRec T = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1154,16 +1242,19 @@ __device__ __forceinline__ void intra_body(const SolView<DT> &S, const ScorePara
                     const float br = static_cast<float>(N == 1 ? S.bridge1[x] : (N == 2 ? S.bridge2[x] : S.bridge3[x]));
                     T = tw_cat(S.node_tw[S.node[x - 1]], S.bwdT[x + N], br);
                 }
+                LoadRec TP = make_int4(0, 0, 0, 0);   // VRPSPDTW: [q+1..u-1] + B(u+N)
+                if (pd && p >= 2) TP = ld_cat(ldn(x - 1), S.bwdP[x + N]);
                 for (int q = p - 2; q >= 0; --q) {
                     const int v = base + q;
                     if (TW && q < p - 2) T = tw_cat(S.node_tw[S.node[v + 1]], T, static_cast<float>(E(v + 1)));
+                    if (pd && q < p - 2) TP = ld_cat(ldn(v + 1), TP);
                     const DT dD = rem + D(v, x) + D(x + N - 1, v + 1) - E(v);
                     float tv = 0.f;
                     if (TW) {
                         const TwRec A2 = tw_cat(S.fwdT[v], sg, static_cast<float>(D(v, x)));
                         tv = tw_cat(A2, T, static_cast<float>(D(x + N - 1, v + 1))).w;
                     }
-                    best = umin64(best, key(dD, tv, q));
+                    best = umin64(best, key(dD, tv, q, pd ? ld_cat(ld_cat(S.fwdP[v], sgP), TP).z : W));
                 }
             }
         } else {
@@ -1172,10 +1263,13 @@ __device__ __forceinline__ void intra_body(const SolView<DT> &S, const ScorePara
             if (p + N1 - 1 <= L) {
                 TwRec M = make_float4(0.f, 0.f, 0.f, 0.f);
                 const TwRec s1 = TW ? seg(x, N1) : M;
+                LoadRec MP = make_int4(0, 0, 0, 0);               // VRPSPDTW: middle [u+N1..v-1]
+                const LoadRec s1P = pd ? segP(x, N1) : MP;
                 for (int q = p + N1; q + N2 - 1 <= L; ++q) {
                     const int v = base + q;
                     DT dD;
                     float tv = 0.f;
+                    int la = W;
                     if (q == p + N1) {  // adjacent: [0..u-1] + seg_v + seg_u + [v+N2..]
                         dD = D(x - 1, v) + D(v + N2 - 1, x) + D(x + N1 - 1, v + N2) - E(x - 1) - E(v - 1) -
                              E(v + N2 - 1);
@@ -1184,7 +1278,9 @@ __device__ __forceinline__ void intra_body(const SolView<DT> &S, const ScorePara
                             const TwRec R3 = tw_cat(R1, s1, static_cast<float>(D(v + N2 - 1, x)));
                             tv = tw_cat(R3, S.bwdT[v + N2], static_cast<float>(D(x + N1 - 1, v + N2))).w;
                         }
+                        if (pd) la = ld_cat(ld_cat(ld_cat(S.fwdP[x - 1], segP(v, N2)), s1P), S.bwdP[v + N2]).z;
                     } else {            // [0..u-1] + seg_v + [u+N1..v-1] + seg_u + [v+N2..]
+                        if (pd) MP = (q == p + N1 + 1) ? ldn(v - 1) : ld_cat(MP, ldn(v - 1));
                         if (TW) {
                             const TwRec nv1 = S.node_tw[S.node[v - 1]];
                             M = (q == p + N1 + 1) ? nv1 : tw_cat(M, nv1, static_cast<float>(E(v - 2)));
@@ -1197,8 +1293,9 @@ __device__ __forceinline__ void intra_body(const SolView<DT> &S, const ScorePara
                             const TwRec R3 = tw_cat(R2, s1, static_cast<float>(D(v - 1, x)));
                             tv = tw_cat(R3, S.bwdT[v + N2], static_cast<float>(D(x + N1 - 1, v + N2))).w;
                         }
+                        if (pd) la = ld_cat(ld_cat(ld_cat(ld_cat(S.fwdP[x - 1], segP(v, N2)), MP), s1P), S.bwdP[v + N2]).z;
                     }
-                    best = umin64(best, key(dD, tv, q));
+                    best = umin64(best, key(dD, tv, q, la));
                 }
             }
         }

@@ -71,6 +71,10 @@ struct ScanArgs {
     SlotTW *rectw;     // VRPTW (TW-I) fast-path records; may be null
     int32_t *nsc;      // north-star sweep column terms, SoA [kNscF][nsc_pitch] (ns_col_terms); may be null
     int32_t nsc_pitch;
+    // VRPSPDTW (pickups): per node p_i, and per slot the Eq. 3a-d load records
+    // (L_I, L_O, L_M, 0) of the prefix [0..x] / suffix [x..L+1]; all null without pickups
+    const int32_t *pickup;
+    int4 *fwdP, *bwdP;
 };
 // the north-star sweep's per-slot column terms (tga_ns.cu), one plane each:
 // r, ne, rem0, sE0, cap - bL1, cap - fL, cap - W, cap - sS0, so0, sA0  (SlotRec fields)

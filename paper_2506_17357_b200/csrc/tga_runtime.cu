@@ -100,6 +100,8 @@ struct tga_instance {
     tga_options opt{};
     void *dC = nullptr;
     int32_t *dDemand = nullptr;
+    int32_t *dPickup = nullptr;    // VRPSPDTW pickup demands (tga_instance_set_pickup); null = none
+    int live_solutions = 0;        // pickups may only be set before any solution is loaded
     TwRec *dNodeTw = nullptr;
     std::vector<int32_t> hDemand;
     std::vector<float> hTw;
@@ -183,6 +185,7 @@ struct tga_solution {
     bool ns_ok = false;            // CVRP feasible-only int32 with |c| < 2^20: the NS sweep kernel applies
     int ns_rw = 8;                 // its rows per warp (ns_rows_per_warp)
     int32_t *nsc = nullptr;        // its column-term planes [kNscF][pitch] (written by the scans)
+    LoadRec *fwdP = nullptr, *bwdP = nullptr;   // VRPSPDTW prefix / suffix load records (Eq. 3a-d)
     bool fast = false;
     int fastU = 16;                // rows per fast-path tile (8 for small neighbourhoods)
     uint64_t *h_keys = nullptr;                         // pinned
@@ -348,6 +351,9 @@ static ScanArgs<DT> scan_args(tga_solution *s) {
     a.rectw = s->rectw;
     a.nsc = s->nsc;
     a.nsc_pitch = s->pitch;
+    a.pickup = s->inst->dPickup;
+    a.fwdP = s->fwdP;
+    a.bwdP = s->bwdP;
     return a;
 }
 
@@ -370,6 +376,10 @@ static SolView<DT> sol_view(const tga_solution *s) {
     v.seg2T = s->seg2T;
     v.seg3T = s->seg3T;
     v.node_tw = s->inst->dNodeTw;
+    v.dem = s->inst->dDemand;
+    v.pick = s->inst->dPickup;
+    v.fwdP = s->fwdP;
+    v.bwdP = s->bwdP;
     v.rW = s->d_rW;
     v.rTV = s->d_rTV;
     v.Dp = static_cast<const DT *>(s->Dp);
@@ -494,6 +504,7 @@ static void free_solution(tga_solution *s) {
     if (s->side) cudaStreamSynchronize(s->side);
     (void)cudaGetLastError();
     if (s->comm && g_nccl.commDestroy) g_nccl.commDestroy(s->comm);
+    if (s->inst) --s->inst->live_solutions;
     if (s->arena) cudaFree(s->arena);
     if (s->Dp) cudaFree(s->Dp);
     if (s->h_keys) cudaFreeHost(s->h_keys);
@@ -652,9 +663,30 @@ extern "C" int32_t tga_instance_destroy(tga_instance *I) {
     (void)cudaGetLastError();
     cudaFree(I->dC);
     cudaFree(I->dDemand);
+    if (I->dPickup) cudaFree(I->dPickup);
     cudaFree(I->dNodeTw);
     if (I->dGpairs) cudaFree(I->dGpairs);
     delete I;
+    return TGA_OK;
+}
+
+extern "C" int32_t tga_instance_set_pickup(tga_instance *I, const int32_t *pickup) {
+    if (!I || !pickup) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (I->live_solutions > 0) return fail(TGA_ERR_INVALID_ARGUMENT, "pickups must be set before any solution is loaded");
+    if (pickup[0] != 0) return fail(TGA_ERR_INVALID_ARGUMENT, "depot pickup p_0 != 0");
+    int64_t tot = 0;
+    for (int i = 0; i < I->n; ++i) {
+        if (pickup[i] < 0) return fail(TGA_ERR_INVALID_ARGUMENT, "pickup demand < 0");
+        tot += pickup[i];
+    }
+    if (tot >= (int64_t(1) << 30)) return fail(TGA_ERR_INVALID_ARGUMENT, "pickup sum exceeds the int32 load range");
+    if (set_device(I) != TGA_OK) return TGA_ERR_CUDA;
+    if (!I->dPickup) TGA_CUDA(cudaMalloc(&I->dPickup, sizeof(int32_t) * I->n));
+    TGA_CUDA(cudaMemcpy(I->dPickup, pickup, sizeof(int32_t) * I->n, cudaMemcpyHostToDevice));
+    // the capacity test becomes one on the largest load carried (Eq. 3a-d): the generic
+    // kernels concatenate (L_I, L_O, L_M) records; the fast paths assume delivery sums
+    I->fast_ok = false;
+    I->fast_pen_ok = false;
     return TGA_OK;
 }
 
@@ -682,6 +714,7 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
     auto *s = new (std::nothrow) tga_solution();
     if (!s) return fail(TGA_ERR_OOM, "host allocation");
     s->inst = I;
+    ++I->live_solutions;   // (free_solution counts it back out, also on a failed load)
     s->R = R;
     s->routes.resize(R);
     for (int r = 0; r < R; ++r) s->routes[r].assign(cust + ptr[r], cust + ptr[r + 1]);
@@ -720,6 +753,7 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
     void *v_fT, *v_bT, *v_s2, *v_s3, *v_rbase, *v_rlenR, *v_cbase, *v_rW, *v_rTV, *v_rD, *v_keys, *v_tiles;
     void *v_ds, *v_sa, *v_desc, *v_scr, *v_acc;
     void *v_rec = nullptr, *v_ftiles = nullptr, *v_rectw = nullptr, *v_slot_of = nullptr, *v_nsc = nullptr;
+    void *v_fP = nullptr, *v_bP = nullptr;
     s->fastU = 16;  // U = 8 measured no better at n = 1000 (more tiles, more per-tile overhead)
     if (const char *ev = std::getenv("TGA_FAST_U")) s->fastU = std::atoi(ev) == 8 ? 8 : 16;  // tuning override
     if (I->opt.score_mode == TGA_SCORE_PENALISED) s->fastU = 16;   // the penalised tile body is built for U = 16
@@ -742,7 +776,8 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
         {&v_rec, want_fast ? cap * sizeof(SlotRec) : 0}, {&v_ftiles, want_fast ? ftiles_max * 4 : 0},
         {&v_rectw, want_fast && I->tw ? cap * sizeof(SlotTW) : 0},
         {&v_slot_of, I->theta > 0 ? static_cast<size_t>(I->n) * 4 : 0},
-        {&v_nsc, want_ns ? static_cast<size_t>(kNscF) * s->pitch * 4 : 0}};
+        {&v_nsc, want_ns ? static_cast<size_t>(kNscF) * s->pitch * 4 : 0},
+        {&v_fP, I->dPickup ? cap * sizeof(LoadRec) : 0}, {&v_bP, I->dPickup ? cap * sizeof(LoadRec) : 0}};
     size_t total = 0;
     for (auto &it : items) total += align_up(it.bytes, 256);
     if (cudaMalloc(&s->arena, total) != cudaSuccess) return bail(fail(TGA_ERR_OOM, "device arena"));
@@ -773,6 +808,13 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
     s->d_acc = static_cast<unsigned long long *>(v_acc);
     s->slot_of = I->theta > 0 ? static_cast<int32_t *>(v_slot_of) : nullptr;  // zero-size items point past the arena
     s->keys = static_cast<uint64_t *>(v_keys);
+    if (I->dPickup) {   // VRPSPDTW prefix / suffix load records (guards included, like the other slot arrays)
+        s->fwdP = static_cast<LoadRec *>(v_fP) + kGuard;
+        s->bwdP = static_cast<LoadRec *>(v_bP) + kGuard;
+        if (cudaMemsetAsync(v_fP, 0, cap * sizeof(LoadRec), s->stream) != cudaSuccess ||
+            cudaMemsetAsync(v_bP, 0, cap * sizeof(LoadRec), s->stream) != cudaSuccess)
+            return bail(fail(TGA_ERR_CUDA, "memset"));
+    }
     if (want_ns) {   // column-term planes: route -1 (no canonical slot) until the scan writes a slot
         s->nsc = static_cast<int32_t *>(v_nsc);
         if (cudaMemsetAsync(s->nsc, 0xFF, static_cast<size_t>(s->pitch) * 4, s->stream) != cudaSuccess ||
@@ -937,6 +979,8 @@ extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
     mask &= TGA_OP_ALL;
     if ((mask & TGA_OP_2OPT) && I->tw)
         return fail(TGA_ERR_UNSUPPORTED, "2-opt is only defined without time windows (P:148)");
+    if ((mask & TGA_OP_2OPT) && I->dPickup)
+        return fail(TGA_ERR_UNSUPPORTED, "2-opt is applied to the CVRP only (P:510), not with pickups");
     if (set_device(I) != TGA_OK) return TGA_ERR_CUDA;
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s->stream;
     if (st != s->stream) TGA_CUDA(order_after(st, s->stream));  // see the latest applied move
@@ -974,7 +1018,8 @@ extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
     // 35.9 vs 38.8 us/step with the walk, R2 (50 slots) 54.0 vs 76.2 with the warp kernel; the
     // same mean-length threshold as the population batch.  TGA_WARP_TW=0/1 forces one (A/B).
     static const int force_warp = std::getenv("TGA_WARP_TW") ? std::atoi(std::getenv("TGA_WARP_TW")) : -1;
-    const bool warp_tw = force_warp >= 0 ? force_warp != 0 : s->N >= 16 * s->R;
+    // (the warp-scan kernel has no pickup-and-delivery load records: VRPSPDTW takes the walk)
+    const bool warp_tw = !I->dPickup && (force_warp >= 0 ? force_warp != 0 : s->N >= 16 * s->R);
     const bool fork_intra = fork_env && I->tw && (mask & TGA_OP_INTER) && (mask & TGA_OP_INTRA) && x_hi > x_lo;
     if (fork_intra) {
         TGA_CUDA(cudaEventRecord(s->ev_fork, st));
@@ -1032,7 +1077,7 @@ extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
     if (e == cudaSuccess && !fused_intra && !fork_intra) {
         if (I->dtype == TGA_I32)
             e = launch_intra<int32_t>(mask, I->tw, sol_view<int32_t>(s), sp, x_lo, x_hi, s->keys, st,
-                                      I->max_c_abs < (1 << 21), warp_tw);
+                                      I->max_c_abs < (1 << 21) && !I->dPickup, warp_tw);
         else
             e = launch_intra<float>(mask, I->tw, sol_view<float>(s), sp, x_lo, x_hi, s->keys, st, false, warp_tw);
     }
@@ -1071,8 +1116,8 @@ extern "C" int32_t tga_debug_eval_dump(tga_solution *s, uint32_t mask, int32_t f
     cudaError_t e = cudaMemsetAsync(dump, 0, plane * TGA_N_VARIANTS * 8, st);
     if (e == cudaSuccess) e = cudaMemsetAsync(s->keys, 0xFF, TGA_N_VARIANTS * 8, st);
     const ScoreParams sp{I->Q, I->opt.score_mode, I->opt.w_load, I->opt.w_tw};
-    const bool warp_tw = (flags & 1) ? true : ((flags & 2) ? false : s->N >= 16 * s->R);
-    const bool small = I->max_c_abs < (1 << 21);
+    const bool warp_tw = !I->dPickup && ((flags & 1) ? true : ((flags & 2) ? false : s->N >= 16 * s->R));
+    const bool small = I->max_c_abs < (1 << 21) && !I->dPickup;
     const int grid = std::max(1, std::min(s->n_tiles, s->sm_count * 4));
     if (e == cudaSuccess) {
         if (ns_path(s, mask)) {   // the north-star sweep kernel, as tga_eval launches it
@@ -1431,6 +1476,25 @@ extern "C" int32_t tga_solution_attributes(tga_solution *s, int64_t *pre_L, int6
     return TGA_OK;
 }
 
+extern "C" int32_t tga_solution_load_records(tga_solution *s, int32_t *pre, int32_t *suf) {
+    if (!s || !pre || !suf) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (!s->fwdP) return fail(TGA_ERR_UNSUPPORTED, "no pickups: the instance has no load records");
+    if (sync_host(s) != TGA_OK) return TGA_ERR_CUDA;
+    TGA_CUDA(cudaStreamSynchronize(s->stream));
+    std::vector<LoadRec> fP(s->Qp), bP(s->Qp);
+    TGA_CUDA(cudaMemcpy(fP.data(), s->fwdP, sizeof(LoadRec) * s->Qp, cudaMemcpyDeviceToHost));
+    TGA_CUDA(cudaMemcpy(bP.data(), s->bwdP, sizeof(LoadRec) * s->Qp, cudaMemcpyDeviceToHost));
+    for (int r = 0; r < s->R; ++r) {
+        const int L = static_cast<int>(s->routes[r].size());
+        for (int p = 0; p <= L; ++p) {
+            const int x = s->rbase[r] + p, c = s->cbase[r] + p;
+            pre[3 * c] = fP[x].x; pre[3 * c + 1] = fP[x].y; pre[3 * c + 2] = fP[x].z;
+            suf[3 * c] = bP[x].x; suf[3 * c + 1] = bP[x].y; suf[3 * c + 2] = bP[x].z;
+        }
+    }
+    return TGA_OK;
+}
+
 // ============================================================== ABI: multi-GPU
 extern "C" int32_t tga_nccl_unique_id(void *out) {
     if (!out) return fail(TGA_ERR_INVALID_ARGUMENT, "NULL argument");
@@ -1781,6 +1845,7 @@ extern "C" int32_t tga_batch_eval(tga_batch *b, uint32_t mask, void *stream) {
     const tga_instance *I = b->inst;
     mask &= TGA_OP_ALL;
     if ((mask & TGA_OP_2OPT) && I->tw) return fail(TGA_ERR_UNSUPPORTED, "2-opt with time windows (P:148)");
+    if ((mask & TGA_OP_2OPT) && I->dPickup) return fail(TGA_ERR_UNSUPPORTED, "2-opt with pickups (P:510)");
     if (set_device(I) != TGA_OK) return TGA_ERR_CUDA;
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : b->stream;
     if (st != b->stream) TGA_CUDA(order_after(st, b->stream));
@@ -1789,7 +1854,7 @@ extern "C" int32_t tga_batch_eval(tga_batch *b, uint32_t mask, void *stream) {
     ScoreParams sp{I->Q, I->opt.score_mode, I->opt.w_load, I->opt.w_tw};
     const int grid = std::max(1, std::min(b->n_work, b->sm_count * 4));
     static const int force_warp = std::getenv("TGA_WARP_TW_BATCH") ? std::atoi(std::getenv("TGA_WARP_TW_BATCH")) : -1;
-    const bool warp_tw = force_warp >= 0 ? force_warp != 0 : b->sols[0]->N >= 16 * b->sols[0]->R;
+    const bool warp_tw = !I->dPickup && (force_warp >= 0 ? force_warp != 0 : b->sols[0]->N >= 16 * b->sols[0]->R);
     static const bool no_fast = std::getenv("TGA_BATCH_GENERIC") != nullptr;  // A/B override
     uint32_t rest = mask;
     if (b->fast && !no_fast && (mask & TGA_OP_INTER)) {

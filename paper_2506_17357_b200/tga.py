@@ -99,6 +99,8 @@ _SYMBOLS = {
     "tga_shard_range": (C.c_int32, [C.c_int64, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
     "tga_nccl_unique_id": (C.c_int32, [C.c_void_p]),
     "tga_comm_init": (C.c_int32, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
+    "tga_instance_set_pickup": (C.c_int32, [C.c_void_p, C.c_void_p]),
+    "tga_solution_load_records": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "tga_batch_load": (C.c_int32, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
                                    C.c_void_p]),
     "tga_batch_destroy": (C.c_int32, [C.c_void_p]),
@@ -184,7 +186,7 @@ class Instance:
 
     def __init__(self, dist, demand, capacity: int, tw=None, score_mode: int = SCORE_FEASIBLE,
                  w_load: int = 10, w_tw: int = 10, device: int = -1, slack: int = 0,
-                 granular_theta: int = 0):
+                 granular_theta: int = 0, pickup=None):
         dist = np.asarray(dist)
         if np.issubdtype(dist.dtype, np.integer):
             self.dist = np.ascontiguousarray(dist, dtype=np.int32)
@@ -206,10 +208,14 @@ class Instance:
         _check(lib().tga_instance_create(self.n, _p(self.dist), self.dtype, None, _p(self.demand),
                                          _p(self.tw), self.capacity, C.byref(opt), C.byref(h)))
         self._h = h
+        self.pickup = None
+        if pickup is not None:   # VRPSPDTW
+            self.pickup = np.ascontiguousarray(pickup, dtype=np.int32)
+            _check(lib().tga_instance_set_pickup(self._h, _p(self.pickup)))
 
     @classmethod
     def from_gen(cls, inst, **kw):
-        return cls(inst.dist, inst.demand, inst.capacity, inst.tw, **kw)
+        return cls(inst.dist, inst.demand, inst.capacity, inst.tw, pickup=getattr(inst, "pickup", None), **kw)
 
     def info(self):
         """(n_nodes, granular theta, unordered customer pairs kept by the edge mask)."""
@@ -342,6 +348,14 @@ class Solution:
         k = np.zeros(N_VARIANTS, dtype=np.uint64)
         _check(lib().tga_solution_keys(self._h, _p(k)))
         return k
+
+    def load_records(self):
+        """VRPSPDTW prefix / suffix (L_I, L_O, L_M) records per canonical slot (Eq. 3a-d)."""
+        R, N, _, _ = self.info()
+        pre = np.zeros((N + R, 3), dtype=np.int32)
+        suf = np.zeros((N + R, 3), dtype=np.int32)
+        _check(lib().tga_solution_load_records(self._h, _p(pre), _p(suf)))
+        return pre, suf
 
     def counts(self) -> np.ndarray:
         c = np.zeros(N_VARIANTS, dtype=np.uint64)

@@ -29,7 +29,11 @@ V_RELOC = {1: 2, 2: 3, 3: 4}
 V_SWAP = {(1, 1): 5, (1, 2): 6, (1, 3): 7, (2, 2): 8, (2, 3): 9, (3, 3): 10}
 V_IRELOC = {1: 11, 2: 12, 3: 13}
 V_ISWAP = {(a, b): 14 + 3 * (a - 1) + (b - 1) for a in (1, 2, 3) for b in (1, 2, 3)}
-N_VARIANTS = 23
+# reversed-segment variants, ranked after the standard 23
+V_RELOC_REV = {2: 23, 3: 24}
+V_CROSS_REV = {2: 25, 3: 26}
+N_VARIANTS = 27
+N_STANDARD = 23
 INTRA = {V_2OPT} | set(V_IRELOC.values()) | set(V_ISWAP.values())
 
 

@@ -32,7 +32,10 @@ enum {
     V_SWAP11 = 5, V_CROSS12 = 6, V_CROSS13 = 7, V_CROSS22 = 8, V_CROSS23 = 9, V_CROSS33 = 10,
     V_IRELOC1 = 11, V_IRELOC2 = 12, V_IRELOC3 = 13,
     V_ISWAP_FIRST = 14, /* 14..22 = intra swap (N1,N2), N1,N2 in 1..3, lexicographic */
-    V_COUNT = 23
+    /* reversed segments ("Relocate and Swap can incorporate reversed subsequences
+     * by exchanging the first and last node index tensors, as in 2-opt"), ranked last */
+    V_RELOC2R = 23, V_RELOC3R = 24, V_CROSS22R = 25, V_CROSS33R = 26,
+    V_COUNT = 27
 };
 
 typedef struct {
@@ -252,6 +255,26 @@ static int construct(const orc_sol *S, int var, int ra, int pa, int rb, int pb,
         *la = cat(A, 0, a, 0, pa - 1); *la = cat(A, *la, b, pb, pb + n2 - 1); *la = cat(A, *la, a, pa + n1, La + 1);
         *lb = cat(B, 0, b, 0, pb - 1); *lb = cat(B, *lb, a, pa, pa + n1 - 1); *lb = cat(B, *lb, b, pb + n2, Lb + 1);
         return 2;
+    case V_RELOC2R: case V_RELOC3R:
+        n1 = var - V_RELOC2R + 2;
+        /* A' = a[0..u-1] ++ a[u+N..]; B' = b[0..v] ++ reverse(a[u..u+N-1]) ++ b[v+1..] */
+        if (ra == rb || pa < 1 || pa + n1 - 1 > La || pb < 0 || pb > Lb) return 0;
+        *la = cat(A, 0, a, 0, pa - 1); *la = cat(A, *la, a, pa + n1, La + 1);
+        *lb = cat(B, 0, b, 0, pb);
+        for (int k = pa + n1 - 1; k >= pa; --k) B[(*lb)++] = a[k];
+        *lb = cat(B, *lb, b, pb + 1, Lb + 1);
+        return 2;
+    case V_CROSS22R: case V_CROSS33R:
+        n1 = n2 = var - V_CROSS22R + 2;
+        /* A' = a[0..u-1] ++ reverse(b[v..v+N-1]) ++ a[u+N..]; B' = b[0..v-1] ++ reverse(a[u..u+N-1]) ++ b[v+N..] */
+        if (ra == rb || pa < 1 || pa + n1 - 1 > La || pb < 1 || pb + n2 - 1 > Lb) return 0;
+        *la = cat(A, 0, a, 0, pa - 1);
+        for (int k = pb + n2 - 1; k >= pb; --k) A[(*la)++] = b[k];
+        *la = cat(A, *la, a, pa + n1, La + 1);
+        *lb = cat(B, 0, b, 0, pb - 1);
+        for (int k = pa + n1 - 1; k >= pa; --k) B[(*lb)++] = a[k];
+        *lb = cat(B, *lb, b, pb + n2, Lb + 1);
+        return 2;
     case V_2OPT:
         /* r' = r[0..u-1] ++ reverse(r[u..v]) ++ r[v+1..] */
         if (ra != rb || pa < 1 || pb <= pa || pb > La) return 0;
@@ -273,7 +296,7 @@ static int construct(const orc_sol *S, int var, int ra, int pa, int rb, int pb,
         }
         return 1;
     default:
-        if (var >= V_ISWAP_FIRST && var < V_COUNT) {
+        if (var >= V_ISWAP_FIRST && var < V_RELOC2R) {
             n1 = (var - V_ISWAP_FIRST) / 3 + 1;
             n2 = (var - V_ISWAP_FIRST) % 3 + 1;
             /* r' = r[0..u-1] ++ r[v..v+N2-1] ++ r[u+N1..v-1] ++ r[u..u+N1-1] ++ r[v+N2..] */
@@ -287,12 +310,13 @@ static int construct(const orc_sol *S, int var, int ra, int pa, int rb, int pb,
     }
 }
 
-static int is_intra(int var) { return var == V_2OPT || var >= V_IRELOC1; }
+static int is_intra(int var) { return var == V_2OPT || (var >= V_IRELOC1 && var < V_RELOC2R); }
 
 /* inter variants with an unordered pair space: route(u) < route(v) */
 static int unordered(int var)
 {
-    return var == V_2OPT_STAR || var == V_SWAP11 || var == V_CROSS22 || var == V_CROSS33;
+    return var == V_2OPT_STAR || var == V_SWAP11 || var == V_CROSS22 || var == V_CROSS33 ||
+           var == V_CROSS22R || var == V_CROSS33R;
 }
 
 /* position ranges of u (first slot) and v (second slot) per variant */
@@ -307,6 +331,9 @@ static void u_range(int var, int L, int *lo, int *hi)
     case V_CROSS33: *lo = 1; *hi = L - 2; return;
     case V_2OPT: *lo = 1; *hi = L; return;
     case V_IRELOC1: case V_IRELOC2: case V_IRELOC3: *lo = 1; *hi = L - (var - V_IRELOC1); return;
+    case V_RELOC2R: case V_RELOC3R: *lo = 1; *hi = L - (var - V_RELOC2R + 1); return;
+    case V_CROSS22R: *lo = 1; *hi = L - 1; return;
+    case V_CROSS33R: *lo = 1; *hi = L - 2; return;
     default: {
         int n1 = (var - V_ISWAP_FIRST) / 3 + 1;
         *lo = 1; *hi = L - n1 + 1; return;
@@ -327,6 +354,9 @@ static void v_range(int var, int L, int *lo, int *hi)
     case V_CROSS33: *lo = 1; *hi = L - 2; return;
     case V_2OPT: *lo = 1; *hi = L; return;
     case V_IRELOC1: case V_IRELOC2: case V_IRELOC3: *lo = 0; *hi = L; return;
+    case V_RELOC2R: case V_RELOC3R: *lo = 0; *hi = L; return;
+    case V_CROSS22R: *lo = 1; *hi = L - 1; return;
+    case V_CROSS33R: *lo = 1; *hi = L - 2; return;
     default: {
         int n2 = (var - V_ISWAP_FIRST) % 3 + 1;
         *lo = 1; *hi = L - n2 + 1; return;

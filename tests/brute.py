@@ -109,6 +109,25 @@ def neighbours(routes: List[List[int]], op: str, n1: int = 1, n2: int = 1, keyed
                         after = routes[b][k - 1] if k > 0 else 0
                         yield out((a, b), (rest, routes[b][:k] + seg + routes[b][k:]), (seg[0], after),
                                   (S(a, i + 1), S(b, k)))
+    elif op == "relocate_rev":   # the moved segment inserted reversed
+        for a in range(R):
+            for i, seg in segments(routes[a], n1):
+                rest = routes[a][:i] + routes[a][i + n1:]
+                for b in range(R):
+                    if b == a:
+                        continue
+                    for k in range(len(routes[b]) + 1):
+                        after = routes[b][k - 1] if k > 0 else 0
+                        yield out((a, b), (rest, routes[b][:k] + seg[::-1] + routes[b][k:]), (seg[0], after),
+                                  (S(a, i + 1), S(b, k)))
+    elif op == "swap_rev":   # both exchanged segments inserted reversed, n1 == n2
+        for a in range(R):
+            for b in range(a + 1, R):
+                for i, sa in segments(routes[a], n1):
+                    for j, sb in segments(routes[b], n2):
+                        yield out((a, b), (routes[a][:i] + sb[::-1] + routes[a][i + n1:],
+                                           routes[b][:j] + sa[::-1] + routes[b][j + n2:]), (sa[0], sb[0]),
+                                  (S(a, i + 1), S(b, j + 1)))
     elif op == "swap":
         for a in range(R):
             for b in range(R):

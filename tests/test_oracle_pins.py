@@ -77,6 +77,11 @@ def _closed_counts(lengths):
             M = L - n1 - n2 + 1
             tot += M * (M + 1) // 2 if M >= 1 else 0
         c[v] = tot
+    # reversed segments: the same candidate spaces as or-opt N and cross (N, N)
+    for n, v in O.V_RELOC_REV.items():
+        c[v] = c[O.V_RELOC[n]]
+    for n, v in O.V_CROSS_REV.items():
+        c[v] = c[O.V_SWAP[(n, n)]]
     return c
 
 
@@ -113,7 +118,9 @@ BRUTE_OPS = ([("2opt*", 1, 1, O.V_2OPT_STAR), ("2opt", 1, 1, O.V_2OPT)]
              + [("relocate", n, 1, v) for n, v in O.V_RELOC.items()]
              + [("swap", a, b, v) for (a, b), v in O.V_SWAP.items()]
              + [("intra_relocate", n, 1, v) for n, v in O.V_IRELOC.items()]
-             + [("intra_swap", a, b, v) for (a, b), v in O.V_ISWAP.items()])
+             + [("intra_swap", a, b, v) for (a, b), v in O.V_ISWAP.items()]
+             + [("relocate_rev", n, 1, v) for n, v in O.V_RELOC_REV.items()]
+             + [("swap_rev", n, n, v) for n, v in O.V_CROSS_REV.items()])
 
 
 def _tiny(seed, tw):

@@ -261,7 +261,7 @@ def run_population(args, ws, rank, local, dev):
     gi = T.Instance.from_gen(inst)
     b = T.Batch(gi, mine)
     b.set_stream(stream)
-    mask = T.OP_ALL & ~T.OP_2OPT
+    mask = T.OP_STANDARD & ~T.OP_2OPT
 
     def counts_total():
         return sum(int(sum(int(x) for v, x in enumerate(b.solution(k).counts()) if (mask >> v) & 1))
@@ -419,7 +419,7 @@ def run_tga(args):
         obj = [T.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         gs.comm_init(rank, ws, obj[0])
-    mask_all = T.OP_ALL if inst.tw is None else (T.OP_ALL & ~T.OP_2OPT)
+    mask_all = T.OP_STANDARD if inst.tw is None else (T.OP_STANDARD & ~T.OP_2OPT)
     K = args.steps
     W = max(args.warmup, 3)
 
@@ -570,7 +570,7 @@ def run_tga(args):
         groups["all inter"] = T.OP_INTER
         groups["all"] = mask_all
         for name, m in groups.items():
-            m &= mask_all
+            m &= mask_all | T.OP_REVERSED   # (the reversed-segment variants: per-operator lines only)
             if not m:
                 continue
             G_SWEEPS, REPS = 20, 10
@@ -590,7 +590,7 @@ def run_tga(args):
                 e1.record(stream)
             torch.cuda.synchronize(dev)
             per_sweep_s = e0.elapsed_time(e1) / 1e3 / (G_SWEEPS * REPS)
-            c = int(sum(cnt_now[v] for v in range(23) if (m >> v) & 1))
+            c = int(sum(cnt_now[v] for v in range(T.N_VARIANTS) if (m >> v) & 1))
             per_op[name] = {"moves_per_s": c / per_sweep_s, "sweeps_per_s": 1.0 / per_sweep_s,
                             "us_per_sweep": per_sweep_s * 1e6, "candidates": c}
             del g

@@ -67,6 +67,12 @@ extern "C" {
  *   CROSSn1n2   inter, exchange segment u..u+N1-1 with v..v+N2-1 (N1<=N2; N1==N2 => route(u)<route(v))
  *   IRELOCATEn  intra, move segment u..u+N-1 after the node originally at slot v
  *   ISWAPn1n2   intra, exchange segments at u (length N1) and v (length N2), u+N1<=v
+ * Reversed-segment variants ("Relocate and Swap can incorporate reversed subsequences by
+ * exchanging the first and last node index tensors, as in 2-opt"):
+ *   OROPTnR     inter, OROPTn with the segment inserted reversed (n = 2, 3)
+ *   CROSSnnR    inter, CROSSnn with both segments inserted reversed (n = 2, 3), route(u)<route(v)
+ * They rank after the 23 standard variants in the tie-break; TGA_OP_STANDARD is the
+ * standard set (the benchmarked neighbourhood), TGA_OP_ALL includes the reversed ones.
  */
 enum {
     TGA_V_2OPT = 0,
@@ -78,7 +84,8 @@ enum {
     TGA_V_ISWAP11 = 14, TGA_V_ISWAP12 = 15, TGA_V_ISWAP13 = 16,
     TGA_V_ISWAP21 = 17, TGA_V_ISWAP22 = 18, TGA_V_ISWAP23 = 19,
     TGA_V_ISWAP31 = 20, TGA_V_ISWAP32 = 21, TGA_V_ISWAP33 = 22,
-    TGA_N_VARIANTS = 23
+    TGA_V_OROPT2R = 23, TGA_V_OROPT3R = 24, TGA_V_CROSS22R = 25, TGA_V_CROSS33R = 26,
+    TGA_N_VARIANTS = 27
 };
 
 /* operator masks (bit i = variant i); OR them for a fused sweep */
@@ -92,6 +99,8 @@ enum {
 #define TGA_OP_INTRA_SWAP     (0x1FFu << TGA_V_ISWAP11)
 #define TGA_OP_INTER          (0x7FEu)
 #define TGA_OP_INTRA          (TGA_OP_2OPT | TGA_OP_INTRA_RELOCATE | TGA_OP_INTRA_SWAP)
+#define TGA_OP_REVERSED       (0xFu << TGA_V_OROPT2R)
+#define TGA_OP_STANDARD       ((1u << TGA_V_OROPT2R) - 1u)
 #define TGA_OP_ALL            ((1u << TGA_N_VARIANTS) - 1u)
 /* the north-star fused sweep: 2-opt* + relocate + swap */
 #define TGA_OP_FUSED_NS       (TGA_OP_2OPT_STAR | TGA_OP_RELOCATE | TGA_OP_SWAP)

@@ -62,6 +62,11 @@ __device__ __forceinline__ uint32_t ord_score(float s) {
     return u ^ ((u & 0x80000000u) ? 0xFFFFFFFFu : 0x80000000u);
 }
 constexpr uint64_t kNoKey = ~0ull;
+// variant count (include/tga.h TGA_N_VARIANTS): 23 standard + 4 reversed-segment variants;
+// a solution's accumulator words: [0, kNV) candidate counts, [kAccApplied] applied moves
+constexpr int kNV = 27;
+constexpr int kAccApplied = 27;
+constexpr uint32_t kRevMask = 0xFu << 23;   // the reversed-segment inter variants
 
 __device__ __forceinline__ uint64_t pack_key(uint32_t ord, uint32_t idx) {
     return (static_cast<uint64_t>(ord) << 32) | idx;

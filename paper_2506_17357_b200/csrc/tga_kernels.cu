@@ -555,14 +555,14 @@ __device__ __forceinline__ void pick_update_multi(const DevState &S, const ScanA
     int32_t *sb = smr, *sl = smr + (R + 1);
     int32_t *snap = smr + 2 * (R + 1);  // old node ids of the changed ranges
     int32_t *nn = snap + snap_cap;      // new node ids of the changed ranges
-    __shared__ uint64_t skeys[23];
+    __shared__ uint64_t skeys[kNV];
     __shared__ Decoded dm;
     // ---- 1. stage the old route bases / lengths and the keys; decode (every block)
     for (int r = tid; r <= R; r += blockDim.x) {
         sb[r] = S.rbase[r];
         sl[r] = r < R ? S.rlenR[r] : 0;
     }
-    if (tid < 23) skeys[tid] = S.keys[tid];
+    if (tid < kNV) skeys[tid] = S.keys[tid];
     __syncthreads();
     if (tid == 0) probe(pr, 1);
     if (pr) S.acc[43] = gtimer();   // diagnostics: block 0 start of decode (globaltimer)
@@ -598,7 +598,7 @@ __device__ __forceinline__ void pick_update_multi(const DevState &S, const ScanA
         if (b == 0 && tid == 0) {
             S.desc[0] = 0;
             wait_arrivals(S.desc + 9, G);  // every block has read the keys
-            for (int v = 0; v < 23; ++v) S.keys[v] = ~0ull;  // consumed: the next eval needs no memset
+            for (int v = 0; v < kNV; ++v) S.keys[v] = ~0ull;  // consumed: the next eval needs no memset
         }
         return;
     }
@@ -716,13 +716,13 @@ __device__ __forceinline__ void pick_update_multi(const DevState &S, const ScanA
             S.canon[x] = p <= L ? x : -1;  // validity only (keys index physical slots)
         }
         if (tid < dm.nrt) S.rlenR[dm.nr[tid].r] = dm.nr[tid].L;
-        if (tid < 23) S.keys[tid] = ~0ull;  // consumed: the next eval needs no memset
+        if (tid < kNV) S.keys[tid] = ~0ull;  // consumed: the next eval needs no memset
         if (tid == 0) {
             const int rlo = dm.nr[0].r, rhi = dm.nrt == 2 ? dm.nr[1].r : -1;
             S.desc[1] = lo0; S.desc[2] = lo0 + n1; S.desc[3] = dm.nrt == 2 ? lo1 : 0; S.desc[4] = dm.nrt == 2 ? lo1 + n2 : 0;
             S.desc[5] = rlo; S.desc[6] = rhi; S.desc[7] = 0;
             S.desc[0] = 1;
-            atomicAdd(S.acc + 23, 1ull);
+            atomicAdd(S.acc + kAccApplied, 1ull);
         }
     }
     if (!direct) {
@@ -854,7 +854,7 @@ __device__ __forceinline__ void tma_load_2d(void *smem_dst, const CUtensorMap *m
 // already in shared memory; running (score, index) keys per variant in `best`.
 template <class DT, bool TW, uint32_t MASK, bool DUMP = false>
 __device__ __forceinline__ void inter_tile(const SolView<DT> &S, const DT *__restrict__ tile, const int u0,
-                                           const int v0, const ScoreParams &sp, uint64_t (&best)[11],
+                                           const int v0, const ScoreParams &sp, uint64_t (&best)[kNV],
                                            unsigned long long *dump = nullptr) {
     constexpr int TU = kTileU, TV = kTileV, VPT = TV / 32, UPW = TU / (kInterThreads / 32);
     constexpr int BW = kBoxW;
@@ -1018,6 +1018,86 @@ __device__ __forceinline__ void inter_tile(const SolView<DT> &S, const DT *__res
                          idx_vu, pair);
                 }
             }
+            // ---- reversed segments ("Relocate and Swap can incorporate reversed
+            // subsequences by exchanging the first and last node index tensors, as in 2-opt"):
+            // the segment's records come from its nodes in reverse order; c is symmetric
+            // (host-checked), so the reversed segment's own distance is unchanged
+            auto segR_T = [&](int x, int N) -> TwRec {   // slots x+N-1, ..., x
+                TwRec r = S.node_tw[S.node[x + N - 1]];
+                for (int k = N - 2; k >= 0; --k) r = tw_cat(r, S.node_tw[S.node[x + k]], static_cast<float>(S.enext[x + k]));
+                return r;
+            };
+            auto segR_P = [&](int x, int N) -> LoadRec {
+                LoadRec r = ld_single(S.dem[S.node[x + N - 1]], S.pick[S.node[x + N - 1]]);
+                for (int k = N - 2; k >= 0; --k) r = ld_cat(r, ld_single(S.dem[S.node[x + k]], S.pick[S.node[x + k]]));
+                return r;
+            };
+#pragma unroll
+            for (int N = 2; N <= 3; ++N) {   // or-opt N reversed: variants 23, 24
+                const int vid = 21 + N;
+                if (!(MASK & (1u << vid))) continue;
+                const DT *bridge = N == 2 ? S.bridge2 : S.bridge3;
+                {   // segment u..u+N-1 (route a) inserted reversed after v (route b): B' = F(v) + rev + B(v+1)
+                    const bool ok = pair && pu >= 1 && pu + N - 1 <= La;
+                    const DT dD = bridge[u] - S.enext[u - 1] - S.enext[u + N - 1] + Dt(u + N - 1, v) + Dt(u, v + 1) -
+                                  S.enext[v];
+                    const int s = S.fwdL[u + N - 1] - S.fwdL[u - 1];
+                    int la = Wa - s, lb = Wb + s;
+                    if (pd && ok) {
+                        la = ld_cat(S.fwdP[u - 1], S.bwdP[u + N]).z;
+                        lb = ld_cat(ld_cat(S.fwdP[v], segR_P(u, N)), S.bwdP[v + 1]).z;
+                    }
+                    float ta = 0.f, tb = 0.f;
+                    if (TW) {
+                        ta = tw_cat(S.fwdT[u - 1], S.bwdT[u + N], static_cast<float>(bridge[u])).w;
+                        const TwRec X = tw_cat(S.fwdT[v], segR_T(u, N), static_cast<float>(Dt(u + N - 1, v)));
+                        tb = tw_cat(X, S.bwdT[v + 1], static_cast<float>(Dt(u, v + 1))).w;
+                    }
+                    take(vid, score_key<DT, TW>(sp, ok, dD, la, lb, Wa, Wb, ta, tb, TVa, TVb, idx_uv), idx_uv, pair);
+                }
+                {   // segment v..v+N-1 (route b) inserted reversed after u (route a): A' = F(u) + rev + B(u+1)
+                    const bool ok = pair && pv >= 1 && pv + N - 1 <= Lb;
+                    const DT dD = bridge[v] - S.enext[v - 1] - S.enext[v + N - 1] + Dt(u, v + N - 1) + Dt(u + 1, v) -
+                                  S.enext[u];
+                    const int s = S.fwdL[v + N - 1] - S.fwdL[v - 1];
+                    int la = Wa + s, lb = Wb - s;
+                    if (pd && ok) {
+                        lb = ld_cat(S.fwdP[v - 1], S.bwdP[v + N]).z;
+                        la = ld_cat(ld_cat(S.fwdP[u], segR_P(v, N)), S.bwdP[u + 1]).z;
+                    }
+                    float ta = 0.f, tb = 0.f;
+                    if (TW) {
+                        tb = tw_cat(S.fwdT[v - 1], S.bwdT[v + N], static_cast<float>(bridge[v])).w;
+                        const TwRec X = tw_cat(S.fwdT[u], segR_T(v, N), static_cast<float>(Dt(u, v + N - 1)));
+                        ta = tw_cat(X, S.bwdT[u + 1], static_cast<float>(Dt(u + 1, v))).w;
+                    }
+                    take(vid, score_key<DT, TW>(sp, ok, dD, la, lb, Wa, Wb, ta, tb, TVa, TVb, idx_vu), idx_vu, pair);
+                }
+            }
+#pragma unroll
+            for (int N = 2; N <= 3; ++N) {   // cross (N, N), both segments reversed: variants 25, 26
+                const int vid = 23 + N;
+                if (!(MASK & (1u << vid))) continue;
+                // A' = F(u-1) + rev(v..v+N-1) + B(u+N),  B' = F(v-1) + rev(u..u+N-1) + B(v+N)
+                const bool ok = pair && pu >= 1 && pu + N - 1 <= La && pv >= 1 && pv + N - 1 <= Lb;
+                const DT dD = Dt(u - 1, v + N - 1) + Dt(u + N, v) + Dt(u + N - 1, v - 1) + Dt(u, v + N) -
+                              S.enext[u - 1] - S.enext[u + N - 1] - S.enext[v - 1] - S.enext[v + N - 1];
+                const int sa = S.fwdL[u + N - 1] - S.fwdL[u - 1];
+                const int sb = S.fwdL[v + N - 1] - S.fwdL[v - 1];
+                int la = Wa - sa + sb, lb = Wb - sb + sa;
+                if (pd && ok) {
+                    la = ld_cat(ld_cat(S.fwdP[u - 1], segR_P(v, N)), S.bwdP[u + N]).z;
+                    lb = ld_cat(ld_cat(S.fwdP[v - 1], segR_P(u, N)), S.bwdP[v + N]).z;
+                }
+                float ta = 0.f, tb = 0.f;
+                if (TW) {
+                    const TwRec A1 = tw_cat(S.fwdT[u - 1], segR_T(v, N), static_cast<float>(Dt(u - 1, v + N - 1)));
+                    ta = tw_cat(A1, S.bwdT[u + N], static_cast<float>(Dt(u + N, v))).w;
+                    const TwRec B1 = tw_cat(S.fwdT[v - 1], segR_T(u, N), static_cast<float>(Dt(u + N - 1, v - 1)));
+                    tb = tw_cat(B1, S.bwdT[v + N], static_cast<float>(Dt(u, v + N))).w;
+                }
+                take(vid, score_key<DT, TW>(sp, ok, dD, la, lb, Wa, Wb, ta, tb, TVa, TVb, idx_uv), idx_uv, pair);
+            }
         }
     }
 }
@@ -1029,7 +1109,7 @@ __global__ void __launch_bounds__(kInterThreads) k_inter(const __grid_constant__
                                                          unsigned long long *dump) {
     constexpr int TU = kTileU, TV = kTileV, VPT = TV / 32, UPW = TU / (kInterThreads / 32);
     constexpr int BW = kBoxW, BH = kBoxH;
-    constexpr int NV = 11;  // inter variant ids 1..10
+    constexpr int NV = kNV;  // inter variant ids 1..10 and the reversed-segment ones 23..26
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // TMA destinations must be 128-byte aligned in the shared window: align at run time
     unsigned char *smem_al = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
@@ -1096,7 +1176,7 @@ __global__ void __launch_bounds__(kInterThreads) k_inter_batch(const SolView<DT>
                                                                const uint32_t *__restrict__ work, int n_work,
                                                                ScoreParams sp, uint64_t *__restrict__ keys) {
     constexpr int TU = kTileU, TV = kTileV;
-    constexpr int NV = 11;
+    constexpr int NV = kNV;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *smem_al = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
     DT *buf0 = reinterpret_cast<DT *>(smem_al);
@@ -1142,7 +1222,7 @@ __global__ void __launch_bounds__(kInterThreads) k_inter_batch(const SolView<DT>
         }
         __syncthreads();
         if (tid < NV && (MASK & (1u << tid)) && red[tid] != kNoKey) {
-            atomicMin(reinterpret_cast<unsigned long long *>(keys) + static_cast<size_t>(sol) * 23 + tid, red[tid]);
+            atomicMin(reinterpret_cast<unsigned long long *>(keys) + static_cast<size_t>(sol) * kNV + tid, red[tid]);
             red[tid] = kNoKey;
         }
         __syncthreads();  // buffer b and red[] are reused
@@ -1317,7 +1397,7 @@ template <class DT, bool TW>
 __global__ void __launch_bounds__(256) k_intra_batch(const SolView<DT> *__restrict__ views, ScoreParams sp,
                                                      uint32_t vmask, uint64_t *__restrict__ keys) {
     const SolView<DT> &S = views[blockIdx.y];
-    intra_body<DT, TW>(S, sp, vmask, 0, S.Qp, keys + static_cast<size_t>(blockIdx.y) * 23);
+    intra_body<DT, TW>(S, sp, vmask, 0, S.Qp, keys + static_cast<size_t>(blockIdx.y) * kNV);
 }
 
 // ============================================================== intra-route evaluation, VRPTW (warp-parallel)
@@ -1555,7 +1635,7 @@ __global__ void __launch_bounds__(256) k_intra_tw_batch(const SolView<DT> *__res
         unsigned long long m = red[0][threadIdx.x];
         for (int w = 1; w < 8; ++w) m = m < red[w][threadIdx.x] ? m : red[w][threadIdx.x];
         if (m != kNoKey)
-            atomicMin(reinterpret_cast<unsigned long long *>(keys) + static_cast<size_t>(blockIdx.y) * 23 + threadIdx.x, m);
+            atomicMin(reinterpret_cast<unsigned long long *>(keys) + static_cast<size_t>(blockIdx.y) * kNV + threadIdx.x, m);
     }
 }
 
@@ -1687,13 +1767,14 @@ static cudaError_t launch_inter_tw(uint32_t mask, const SolView<DT> &S, const CU
     if (mask & (3u << 3)) run(std::integral_constant<uint32_t, (3u << 3)>{});
     if (mask & (1u << 5)) run(std::integral_constant<uint32_t, (1u << 5)>{});
     if (mask & (0x1Fu << 6)) run(std::integral_constant<uint32_t, (0x1Fu << 6)>{});
+    if (mask & kRevMask) run(std::integral_constant<uint32_t, kRevMask>{});   // reversed segments
     return err;
 }
 
 template <class DT>
 cudaError_t launch_inter(uint32_t mask, bool tw, const SolView<DT> &S, const CUtensorMap &map, const uint32_t *tiles,
                          int t_lo, int t_hi, const ScoreParams &sp, uint64_t *keys, int grid, cudaStream_t st) {
-    if (t_hi <= t_lo || !(mask & 0x7FEu)) return cudaSuccess;
+    if (t_hi <= t_lo || !(mask & (0x7FEu | kRevMask))) return cudaSuccess;
     return tw ? launch_inter_tw<DT, true>(mask, S, map, tiles, t_lo, t_hi, sp, keys, grid, st)
               : launch_inter_tw<DT, false>(mask, S, map, tiles, t_lo, t_hi, sp, keys, grid, st);
 }
@@ -1736,6 +1817,15 @@ cudaError_t launch_eval_dump(uint32_t mask, bool tw, const SolView<DT> &S, const
     if (inter && t_hi > t_lo && (mask & ALL)) {
         const int smem = 2 * kBoxBytesPadded + 128;
         auto kern = tw ? k_inter<DT, true, ALL, true> : k_inter<DT, false, ALL, true>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        kern<<<grid, kInterThreads, smem, st>>>(S, map, tiles, t_lo, t_hi, sp, keys, dump);
+        ++g_launches;
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    if (t_hi > t_lo && (mask & kRevMask)) {   // reversed segments: always the generic kernel
+        const int smem = 2 * kBoxBytesPadded + 128;
+        auto kern = tw ? k_inter<DT, true, kRevMask, true> : k_inter<DT, false, kRevMask, true>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         kern<<<grid, kInterThreads, smem, st>>>(S, map, tiles, t_lo, t_hi, sp, keys, dump);
         ++g_launches;
@@ -1792,6 +1882,7 @@ static cudaError_t launch_inter_batch_tw(uint32_t mask, const SolView<DT> *views
     if (mask & (3u << 3)) run(std::integral_constant<uint32_t, (3u << 3)>{});
     if (mask & (1u << 5)) run(std::integral_constant<uint32_t, (1u << 5)>{});
     if (mask & (0x1Fu << 6)) run(std::integral_constant<uint32_t, (0x1Fu << 6)>{});
+    if (mask & kRevMask) run(std::integral_constant<uint32_t, kRevMask>{});
     return err;
 }
 
@@ -1800,7 +1891,7 @@ cudaError_t launch_batch(uint32_t mask, bool tw, const SolView<DT> *views, const
                          const uint32_t *work, int n_work, int n_sol, int max_qp, const ScoreParams &sp,
                          uint64_t *keys, int grid, cudaStream_t st, bool warp_tw) {
     cudaError_t e = cudaSuccess;
-    if (n_work > 0 && (mask & 0x7FEu))
+    if (n_work > 0 && (mask & (0x7FEu | kRevMask)))
         e = tw ? launch_inter_batch_tw<DT, true>(mask, views, maps, work, n_work, sp, keys, grid, st)
                : launch_inter_batch_tw<DT, false>(mask, views, maps, work, n_work, sp, keys, grid, st);
     const uint32_t intra = mask & ((1u << 0) | (0x7u << 11) | (0x1FFu << 14));

@@ -102,9 +102,11 @@ __device__ __forceinline__ void neighbourhood_counts(const DevState &S, uint32_t
         sums[tid] = v;
     }
     __syncthreads();   // sums[] complete before any thread reads it (racecheck)
-    if (tid < 23 && (mask & (1u << tid))) {  // one variant per thread
+    if (tid < kNV && (mask & (1u << tid))) {  // one variant per thread
         const long long S1 = sums[0], S2 = sums[1];
-        const int v = tid;
+        const int v0 = tid;
+        // reversed-segment variants: the candidate spaces of or-opt N and cross (N, N)
+        const int v = v0 == 23 ? 3 : (v0 == 24 ? 4 : (v0 == 25 ? 8 : (v0 == 26 ? 10 : v0)));
         long long c;
         if (v == 0) c = sums[14];
         else if (v == 1) c = (S1 * S1 - S2) / 2;
@@ -116,7 +118,7 @@ __device__ __forceinline__ void neighbourhood_counts(const DevState &S, uint32_t
             c = (n1s[k] == n2s[k]) ? ordered / 2 : ordered;
         } else if (v <= 13) c = sums[v + 4];
         else c = sums[v + 4];
-        atomicAdd(S.acc + v, static_cast<unsigned long long>(c));  // fire-and-forget (RED)
+        atomicAdd(S.acc + v0, static_cast<unsigned long long>(c));  // fire-and-forget (RED)
     }
 }
 
@@ -135,7 +137,7 @@ struct Decoded {
 __device__ __forceinline__ void decode_best(const uint64_t *__restrict__ keys, uint32_t mask, int integer,
                                             const int32_t *sb, const int32_t *sl, int R, int Qc, Decoded &dm) {
     const int lane = threadIdx.x & 31;
-    const uint64_t k = (lane < 23 && ((mask >> lane) & 1u)) ? keys[lane] : ~0ull;
+    const uint64_t k = (lane < kNV && ((mask >> lane) & 1u)) ? keys[lane] : ~0ull;
     const bool valid = k != ~0ull;
     const uint32_t hi = valid ? static_cast<uint32_t>(k >> 32) : 0xFFFFFFFFu;
     const uint32_t mhi = __reduce_min_sync(0xFFFFFFFFu, hi);
@@ -171,7 +173,7 @@ __device__ __forceinline__ void decode_best(const uint64_t *__restrict__ keys, u
     const int pa = __shfl_sync(0xFFFFFFFFu, x, 0) - sb[ra], pb = __shfl_sync(0xFFFFFFFFu, x, 1) - sb[rb];
     if (lane != 0) return;
     const int La = sl[ra], Lb = sl[rb];
-    const bool one = v == 0 || v >= 11;
+    const bool one = v == 0 || (v >= 11 && v < 23);
     // pieces with static indices (empty pieces have len 0 and are skipped by the walk)
     Piece A0{}, A1{}, A2{}, A3{}, A4{}, B0{}, B1{}, B2{};
     int na = 0, nb = 0;
@@ -190,6 +192,14 @@ __device__ __forceinline__ void decode_best(const uint64_t *__restrict__ keys, u
         B0 = pc(rb, 1, pb - 1); B1 = pc(ra, pa, pa + N1 - 1); B2 = pc(rb, pb + N2, Lb); nb = 3;
     } else if (v == 0) {  // 2-opt
         A0 = pc(ra, 1, pa - 1); A1 = pc(ra, pa, pb, 1); A2 = pc(ra, pb + 1, La); na = 3;
+    } else if (v == 23 || v == 24) {  // or-opt, the segment inserted reversed
+        const int N = v - 21;
+        A0 = pc(ra, 1, pa - 1); A1 = pc(ra, pa + N, La); na = 2;
+        B0 = pc(rb, 1, pb); B1 = pc(ra, pa, pa + N - 1, 1); B2 = pc(rb, pb + 1, Lb); nb = 3;
+    } else if (v == 25 || v == 26) {  // cross (N, N), both segments reversed
+        const int N = v - 23;
+        A0 = pc(ra, 1, pa - 1); A1 = pc(rb, pb, pb + N - 1, 1); A2 = pc(ra, pa + N, La); na = 3;
+        B0 = pc(rb, 1, pb - 1); B1 = pc(ra, pa, pa + N - 1, 1); B2 = pc(rb, pb + N, Lb); nb = 3;
     } else if (v >= 11 && v <= 13) {  // intra relocate
         const int N = v - 10;
         if (pb > pa) {
@@ -239,11 +249,11 @@ __device__ __forceinline__ void pick_apply_body(const DevState &S, uint32_t mask
         sb[r] = S.rbase[r];
         sl[r] = r < R ? S.rlenR[r] : 0;
     }
-    __shared__ uint64_t skeys[23];
-    if (tid < 23) skeys[tid] = S.keys[tid];
+    __shared__ uint64_t skeys[kNV];
+    if (tid < kNV) skeys[tid] = S.keys[tid];
     if (do_counts) neighbourhood_counts(S, cmask, sl);
     __syncthreads();
-    if (tid < 23) S.keys[tid] = ~0ull;  // consumed (block 0 is the only reader): the next eval needs no memset
+    if (tid < kNV) S.keys[tid] = ~0ull;  // consumed (block 0 is the only reader): the next eval needs no memset
     if (tid == 0) probe(pr, 1);
     // ---- 2. best key over the mask, decode, pieces of the new routes
     __shared__ NewRoute nr[2];
@@ -251,7 +261,7 @@ __device__ __forceinline__ void pick_apply_body(const DevState &S, uint32_t mask
     if (tid == 0) {
         int bv = -1;
         uint64_t bk = ~0ull;
-        for (int v = 0; v < 23; ++v) {
+        for (int v = 0; v < kNV; ++v) {
             if (!(mask & (1u << v))) continue;
             const uint64_t k = skeys[v];
             if (k == ~0ull) continue;
@@ -305,6 +315,14 @@ __device__ __forceinline__ void pick_apply_body(const DevState &S, uint32_t mask
             } else if (v == 0) {  // 2-opt
                 nroutes = 1;
                 add_piece(A, ra, 1, pa - 1); add_piece(A, ra, pa, pb, 1); add_piece(A, ra, pb + 1, La);
+            } else if (v == 23 || v == 24) {  // or-opt, the segment inserted reversed
+                const int N = v - 21;
+                add_piece(A, ra, 1, pa - 1); add_piece(A, ra, pa + N, La);
+                add_piece(B, rb, 1, pb); add_piece(B, ra, pa, pa + N - 1, 1); add_piece(B, rb, pb + 1, Lb);
+            } else if (v == 25 || v == 26) {  // cross (N, N), both segments reversed
+                const int N = v - 23;
+                add_piece(A, ra, 1, pa - 1); add_piece(A, rb, pb, pb + N - 1, 1); add_piece(A, ra, pa + N, La);
+                add_piece(B, rb, 1, pb - 1); add_piece(B, ra, pa, pa + N - 1, 1); add_piece(B, rb, pb + N, Lb);
             } else if (v >= 11 && v <= 13) {  // intra relocate
                 nroutes = 1;
                 const int N = v - 10;
@@ -440,7 +458,7 @@ __device__ __forceinline__ void pick_apply_body(const DevState &S, uint32_t mask
     }
     if (tid == 0) {
         S.desc[0] = 1;
-        atomicAdd(S.acc + 23, 1ull);
+        atomicAdd(S.acc + kAccApplied, 1ull);
         probe(pr, 3);
     }
 }

@@ -89,7 +89,9 @@ void variant_lengths(int v, int *n1, int *n2) {
     static const int sw[6][2] = {{1, 1}, {1, 2}, {1, 3}, {2, 2}, {2, 3}, {3, 3}};
     if (v >= TGA_V_SWAP11 && v <= TGA_V_CROSS33) { *n1 = sw[v - 5][0]; *n2 = sw[v - 5][1]; return; }
     if (v >= TGA_V_IRELOCATE1 && v <= TGA_V_IRELOCATE3) { *n1 = v - TGA_V_IRELOCATE1 + 1; return; }
-    if (v >= TGA_V_ISWAP11 && v <= TGA_V_ISWAP33) { *n1 = (v - 14) / 3 + 1; *n2 = (v - 14) % 3 + 1; }
+    if (v >= TGA_V_ISWAP11 && v <= TGA_V_ISWAP33) { *n1 = (v - 14) / 3 + 1; *n2 = (v - 14) % 3 + 1; return; }
+    if (v == TGA_V_OROPT2R || v == TGA_V_OROPT3R) { *n1 = v - TGA_V_OROPT2R + 2; return; }
+    if (v == TGA_V_CROSS22R || v == TGA_V_CROSS33R) { *n1 = *n2 = v - TGA_V_CROSS22R + 2; }
 }
 }  // namespace
 
@@ -209,7 +211,7 @@ struct tga_solution {
 };
 
 // ============================================================== helpers
-static bool is_intra_variant(int v) { return v == TGA_V_2OPT || v >= TGA_V_IRELOCATE1; }
+static bool is_intra_variant(int v) { return v == TGA_V_2OPT || (v >= TGA_V_IRELOCATE1 && v <= TGA_V_ISWAP33); }
 
 // make `later` wait for everything already enqueued on `earlier`
 static cudaError_t order_after(cudaStream_t later, cudaStream_t earlier) {
@@ -1034,6 +1036,8 @@ extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
     const bool etga = I->theta > 0;
     if (etga && !(I->dtype == TGA_I32 && s->fast && I->opt.score_mode == TGA_SCORE_FEASIBLE))
         return fail(TGA_ERR_UNSUPPORTED, "edge-based neighbourhood: integer feasible-only fast path only");
+    if (etga && (mask & TGA_OP_REVERSED))
+        return fail(TGA_ERR_UNSUPPORTED, "edge-based neighbourhood: reversed-segment variants");
     if (etga) {
         // ETGA: node -> slot map, then the cells the edge mask keeps; the
         // evaluated inter-route candidates are counted exactly on the device
@@ -1081,6 +1085,12 @@ extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
         else
             e = launch_intra<float>(mask, I->tw, sol_view<float>(s), sp, x_lo, x_hi, s->keys, st, false, warp_tw);
     }
+    // reversed-segment variants beside a fast-path / north-star sweep: the generic
+    // tile kernel (the generic branch above already covered them in its own launch)
+    const bool generic_branch = !etga && !ns && !(I->dtype == TGA_I32 && s->fast);
+    if (e == cudaSuccess && (mask & TGA_OP_REVERSED) && !generic_branch)
+        e = launch_inter<int32_t>(mask & TGA_OP_REVERSED, I->tw, sol_view<int32_t>(s), s->tmap, s->d_tiles, t_lo, t_hi, sp,
+                                  s->keys, grid, st);
     if (e != cudaSuccess) return fail(TGA_ERR_CUDA, std::string("eval launch: ") + cudaGetErrorString(e));
     if (s->comm) {
         const ncclResult_t r = g_nccl.allReduce(s->keys, s->keys, TGA_N_VARIANTS, kNcclUint64, kNcclMin, s->comm, st);
@@ -1137,6 +1147,12 @@ extern "C" int32_t tga_debug_eval_dump(tga_solution *s, uint32_t mask, int32_t f
             if (e == cudaSuccess && !fused)
                 e = launch_eval_dump<int32_t>(mask, I->tw, sol_view<int32_t>(s), s->tmap, s->d_tiles, 0, 0, sp, s->keys,
                                               grid, 0, s->Qp, false, small, warp_tw, st, dump);
+        }
+        if ((ns_path(s, mask) || (I->dtype == TGA_I32 && s->fast)) && e == cudaSuccess && (mask & TGA_OP_REVERSED)) {
+            // reversed-segment variants beside the fast paths: the generic tile kernel, as tga_eval
+            e = launch_eval_dump<int32_t>(mask & TGA_OP_REVERSED, I->tw, sol_view<int32_t>(s), s->tmap, s->d_tiles, 0,
+                                          s->n_tiles, sp, s->keys, grid, 0, s->Qp, false, small, warp_tw, st, dump);
+        } else if (ns_path(s, mask) || (I->dtype == TGA_I32 && s->fast)) {
         } else if (I->dtype == TGA_I32) {
             e = launch_eval_dump<int32_t>(mask, I->tw, sol_view<int32_t>(s), s->tmap, s->d_tiles, 0, s->n_tiles, sp,
                                           s->keys, grid, 0, s->Qp, true, small, warp_tw, st, dump);
@@ -1316,6 +1332,20 @@ static bool splice(std::vector<std::vector<int32_t>> &routes, const tga_move *m)
         V na = cat({sl(a, 0, pa - 1), sl(a, pb - 1, pb - 1 + n2), sl(a, pa - 1 + n1, pb - 1), sl(a, pa - 1, pa - 1 + n1),
                     sl(a, pb - 1 + n2, La)});
         a.swap(na);
+    } else if (v == TGA_V_OROPT2R || v == TGA_V_OROPT3R) {   // the segment inserted reversed
+        if (ra == rb || pa < 1 || pa + n1 - 1 > La || pb < 0 || pb > Lb) return false;
+        V seg = sl(a, pa - 1, pa - 1 + n1);
+        std::reverse(seg.begin(), seg.end());
+        V na = cat({sl(a, 0, pa - 1), sl(a, pa - 1 + n1, La)}), nb = cat({sl(b, 0, pb), seg, sl(b, pb, Lb)});
+        a.swap(na); b.swap(nb);
+    } else if (v == TGA_V_CROSS22R || v == TGA_V_CROSS33R) {   // both segments reversed
+        if (ra == rb || pa < 1 || pa + n1 - 1 > La || pb < 1 || pb + n2 - 1 > Lb) return false;
+        V sa = sl(a, pa - 1, pa - 1 + n1), sb = sl(b, pb - 1, pb - 1 + n2);
+        std::reverse(sa.begin(), sa.end());
+        std::reverse(sb.begin(), sb.end());
+        V na = cat({sl(a, 0, pa - 1), sb, sl(a, pa - 1 + n1, La)});
+        V nb = cat({sl(b, 0, pb - 1), sa, sl(b, pb - 1 + n2, Lb)});
+        a.swap(na); b.swap(nb);
     } else {
         return false;
     }
@@ -1386,6 +1416,11 @@ extern "C" int32_t tga_solution_counts(const tga_solution *cs, uint64_t *c) {
                 c[TGA_V_ISWAP11 + 3 * (a - 1) + (b - 1)] += M >= 1 ? M * (M + 1) / 2 : 0;
             }
     }
+    // reversed segments: the candidate spaces of or-opt N and cross (N, N)
+    c[TGA_V_OROPT2R] = c[TGA_V_OROPT2];
+    c[TGA_V_OROPT3R] = c[TGA_V_OROPT3];
+    c[TGA_V_CROSS22R] = c[TGA_V_CROSS22];
+    c[TGA_V_CROSS33R] = c[TGA_V_CROSS33];
     return TGA_OK;
 }
 
@@ -1678,9 +1713,9 @@ extern "C" int32_t tga_solution_device_stats(tga_solution *s, uint64_t *counts, 
     unsigned long long acc[48];
     TGA_CUDA(cudaMemcpyAsync(acc, s->d_acc, sizeof(acc), cudaMemcpyDeviceToHost, s->stream));
     TGA_CUDA(cudaStreamSynchronize(s->stream));
-    TGA_CUDA(cudaMemsetAsync(s->d_acc, 0, 24 * 8, s->stream));  // counts + applied (not the probe)
+    TGA_CUDA(cudaMemsetAsync(s->d_acc, 0, (kAccApplied + 1) * 8, s->stream));  // counts + applied (not the probe)
     if (counts) for (int v = 0; v < TGA_N_VARIANTS; ++v) counts[v] = acc[v];
-    if (applied) *applied = acc[23];
+    if (applied) *applied = acc[kAccApplied];
     return TGA_OK;
 }
 

@@ -23,15 +23,19 @@ ERR = {-1: "INVALID_ARGUMENT", -2: "STRUCTURE", -3: "STALE", -4: "UNSUPPORTED", 
        -6: "NCCL", -7: "OOM"}
 I32, F32 = 0, 1
 SCORE_FEASIBLE, SCORE_PENALISED = 0, 1
-N_VARIANTS = 23
+N_VARIANTS = 27
 V_2OPT, V_2OPT_STAR = 0, 1
 V_RELOCATE = {1: 2, 2: 3, 3: 4}
 V_SWAP = {(1, 1): 5, (1, 2): 6, (1, 3): 7, (2, 2): 8, (2, 3): 9, (3, 3): 10}
 V_IRELOCATE = {1: 11, 2: 12, 3: 13}
 V_ISWAP = {(a, b): 14 + 3 * (a - 1) + (b - 1) for a in (1, 2, 3) for b in (1, 2, 3)}
+# reversed-segment variants: or-opt N=2,3 and cross (N,N) N=2,3 with reversed segments
+V_OROPT_REV = {2: 23, 3: 24}
+V_CROSS_REV = {2: 25, 3: 26}
 VARIANT_NAMES = (["2opt", "2opt*", "relocate", "or-opt2", "or-opt3", "swap11", "cross12", "cross13",
                   "cross22", "cross23", "cross33", "irelocate1", "irelocate2", "irelocate3"]
-                 + [f"iswap{a}{b}" for a in (1, 2, 3) for b in (1, 2, 3)])
+                 + [f"iswap{a}{b}" for a in (1, 2, 3) for b in (1, 2, 3)]
+                 + ["or-opt2r", "or-opt3r", "cross22r", "cross33r"])
 OP_2OPT = 1 << 0
 OP_2OPT_STAR = 1 << 1
 OP_RELOCATE = 1 << 2
@@ -42,12 +46,14 @@ OP_INTRA_RELOCATE = 0x7 << 11
 OP_INTRA_SWAP = 0x1FF << 14
 OP_INTER = 0x7FE
 OP_INTRA = OP_2OPT | OP_INTRA_RELOCATE | OP_INTRA_SWAP
+OP_REVERSED = 0xF << 23
+OP_STANDARD = (1 << 23) - 1      # the 23 standard variants (the benchmarked neighbourhood)
 OP_ALL = (1 << N_VARIANTS) - 1
 OP_FUSED_NS = OP_2OPT_STAR | OP_RELOCATE | OP_SWAP
 EVAL_ACCUMULATE = 1 << 31
 OPERATORS = {"2opt": OP_2OPT, "2opt*": OP_2OPT_STAR, "relocate": OP_RELOCATE, "or-opt": OP_OR_OPT,
              "swap": OP_SWAP, "cross": OP_CROSS, "intra-relocate": OP_INTRA_RELOCATE,
-             "intra-swap": OP_INTRA_SWAP}
+             "intra-swap": OP_INTRA_SWAP, "or-opt reversed": 0x3 << 23, "cross reversed": 0x3 << 25}
 
 
 class TgaError(RuntimeError):

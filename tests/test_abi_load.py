@@ -43,10 +43,13 @@ def test_variant_tables_agree_with_oracle():
     assert tga.N_VARIANTS == O.N_VARIANTS
     assert tga.V_RELOCATE == O.V_RELOC and tga.V_SWAP == O.V_SWAP
     assert tga.V_IRELOCATE == O.V_IRELOC and tga.V_ISWAP == O.V_ISWAP
+    assert tga.V_OROPT_REV == O.V_RELOC_REV and tga.V_CROSS_REV == O.V_CROSS_REV
     hdr = open(os.path.join(ROOT, "include", "tga.h")).read()
-    for name, val in re.findall(r"TGA_V_([A-Z0-9_]+)\s*=\s*(\d+)", hdr):
-        pass
-    assert "TGA_N_VARIANTS = 23" in hdr
+    ids = {name: int(val) for name, val in re.findall(r"TGA_V_([A-Z0-9_]+)\s*=\s*(\d+)", hdr)}
+    assert ids["OROPT2R"] == O.V_RELOC_REV[2] and ids["CROSS33R"] == O.V_CROSS_REV[3]
+    assert ids["ISWAP33"] == O.V_ISWAP[(3, 3)] and ids["CROSS33"] == O.V_SWAP[(3, 3)]
+    assert f"TGA_N_VARIANTS = {O.N_VARIANTS}" in hdr
+    assert len(tga.VARIANT_NAMES) == O.N_VARIANTS
 
 
 def test_version_and_error_strings_without_gpu():

@@ -167,7 +167,7 @@ def test_ns_publish_accumulate_and_reset():
     _need_gpu()
     inst, sol = G.x_like(2, n=400, target_routes=17)
     gs = T.Solution(T.Instance.from_gen(inst), sol)
-    gs.eval(T.OP_ALL)
+    gs.eval(T.OP_STANDARD)
     ref = gs.keys()
     gs.eval(T.OP_OR_OPT | T.OP_CROSS | T.OP_INTRA)
     gs.eval(T.OP_FUSED_NS | T.EVAL_ACCUMULATE)

@@ -84,7 +84,7 @@ def test_cfg1_gpu_vs_brute_force(seed, spare, mode):
     _need_gpu()
     inst, sol = G.cvrp_small(seed, spare=spare)
     gs = T.Solution(T.Instance.from_gen(inst, score_mode=mode), sol)
-    gs.eval(T.OP_ALL)
+    gs.eval(T.OP_STANDARD)
     got = gpu_keys(gs, integer=True)
     Q = O.canonical_q(sol)
     d, dem = inst.dist.tolist(), inst.demand.tolist()
@@ -237,12 +237,12 @@ def test_virtual_shards_equal_unsharded(n_shards):
     _need_gpu()
     inst, sol = G.x_like(6, n=400, target_routes=17)
     gs = T.Solution(T.Instance.from_gen(inst), sol)
-    gs.eval(T.OP_ALL)
+    gs.eval(T.OP_STANDARD)
     full = gs.keys()
     comb = np.full(T.N_VARIANTS, np.iinfo(np.uint64).max, dtype=np.uint64)
     for s in range(n_shards):
         gs.set_shard(s, n_shards)
-        gs.eval(T.OP_ALL)
+        gs.eval(T.OP_STANDARD)
         comb = np.minimum(comb, gs.keys())
     np.testing.assert_array_equal(comb, full)
 
@@ -266,8 +266,8 @@ def test_cfg2_state_b_after_descent():
     orc = O.Oracle.from_instance(inst)
     gs = T.Solution(T.Instance.from_gen(inst), sol)
     for _ in range(30):
-        gs.eval(T.OP_ALL)
-        ok, mv = gs.best_move(T.OP_ALL)
+        gs.eval(T.OP_STANDARD)
+        ok, mv = gs.best_move(T.OP_STANDARD)
         if not ok:
             break
         gs.apply(mv)
@@ -313,9 +313,9 @@ def test_step_reload_and_timing():
     b = T.Solution(gi, sol)
     a.enable_timing(True)
     for _ in range(10):
-        a.eval(T.OP_ALL)
-        ok, mv = a.best_move(T.OP_ALL)
-        applied, mv2 = b.step(T.OP_ALL)
+        a.eval(T.OP_STANDARD)
+        ok, mv = a.best_move(T.OP_STANDARD)
+        applied, mv2 = b.step(T.OP_STANDARD)
         assert ok == applied and (mv.variant, mv.u, mv.v, mv.delta_i) == (mv2.variant, mv2.u, mv2.v, mv2.delta_i)
         if ok:
             a.apply(mv)
@@ -325,8 +325,8 @@ def test_step_reload_and_timing():
     other = G.perturb(sol, 15, 3)
     b.reload(other)
     fresh = T.Solution(gi, other)
-    b.eval(T.OP_ALL)
-    fresh.eval(T.OP_ALL)
+    b.eval(T.OP_STANDARD)
+    fresh.eval(T.OP_STANDARD)
     np.testing.assert_array_equal(b.keys(), fresh.keys())
     assert b.routes() == fresh.routes()
 
@@ -340,7 +340,7 @@ def test_batch_population_exact(mode):
     inst, sols = G.population(0, n=200, n_sol=24)
     gi = T.Instance.from_gen(inst, score_mode=mode)
     b = T.Batch(gi, sols)
-    mask = T.OP_ALL & ~T.OP_2OPT
+    mask = T.OP_STANDARD & ~T.OP_2OPT
     b.eval(mask)
     keys = b.keys()
     orc = O.Oracle.from_instance(inst)
@@ -363,7 +363,7 @@ def test_batch_full_population_1024():
     assert len(sols) == 1024
     gi = T.Instance.from_gen(inst)
     b = T.Batch(gi, sols)
-    mask = T.OP_ALL & ~T.OP_2OPT
+    mask = T.OP_STANDARD & ~T.OP_2OPT
     b.eval(mask)
     keys = b.keys()
     rng = np.random.default_rng(5)
@@ -423,7 +423,7 @@ def test_cfg4_large_global_exact(name):
     comb = np.full(T.N_VARIANTS, np.iinfo(np.uint64).max, dtype=np.uint64)
     for sh in range(4):
         gs.set_shard(sh, 4)
-        gs.eval(T.OP_ALL)
+        gs.eval(T.OP_STANDARD)
         comb = np.minimum(comb, gs.keys())
     np.testing.assert_array_equal(comb, full)
 
@@ -463,7 +463,7 @@ def test_device_resident_step_matches_host_step(name):
         inst, sol = G.gh_like(9, n=200, kind="R2")
     else:
         inst, sol = G.config("cfg2")
-    mask = T.OP_ALL if inst.tw is None else T.OP_ALL & ~T.OP_2OPT
+    mask = T.OP_STANDARD if inst.tw is None else T.OP_STANDARD & ~T.OP_2OPT
     gi = T.Instance.from_gen(inst)
     host = T.Solution(gi, sol)
     dev = T.Solution(gi, sol)
@@ -500,7 +500,7 @@ def test_batch_device_step_matches_host_batch():
     _need_gpu()
     inst, sols = G.population(1, n=200, n_sol=64)
     gi = T.Instance.from_gen(inst)
-    mask = T.OP_ALL & ~T.OP_2OPT
+    mask = T.OP_STANDARD & ~T.OP_2OPT
     hb = T.Batch(gi, sols)
     db = T.Batch(gi, sols)
     for _ in range(5):
@@ -545,15 +545,15 @@ def test_slack_layouts_lockstep(slack):
         ob = orc.best_over(routes, ALLV)
         if ob is None or not ob.score < 0:
             break
-        ok, mv = host.step(T.OP_ALL)
+        ok, mv = host.step(T.OP_STANDARD)
         assert ok and (mv.variant, mv.u, mv.v, mv.delta_i) == (ob.variant, ob.u, ob.v, ob.score)
-        dev.step_async(T.OP_ALL)
+        dev.step_async(T.OP_STANDARD)
         routes = orc.apply(routes, ob.variant, ob.route_a, ob.pos_a, ob.route_b, ob.pos_b)
         if step % 7 == 6:
             assert host.routes() == routes and dev.routes() == routes
             fresh = T.Solution(gi, routes)
             for s in (host, dev, fresh):
-                s.eval(T.OP_ALL)
+                s.eval(T.OP_STANDARD)
             np.testing.assert_array_equal(host.keys(), fresh.keys())
             np.testing.assert_array_equal(dev.keys(), fresh.keys())
     assert dev.routes() == routes
@@ -569,10 +569,10 @@ def test_device_step_column_paths_and_short_tw_routes(name):
     mode = 0
     if name == "cvrp3000":
         inst, sol = G.large_cvrp(3, n=3000, mean_len=60)
-        mask = T.OP_ALL
+        mask = T.OP_STANDARD
     else:
         inst, sol = G.gh_like(4, n=300, kind="R1")
-        mask = T.OP_ALL & ~T.OP_2OPT
+        mask = T.OP_STANDARD & ~T.OP_2OPT
         mode = 1 if name.endswith("penalised") else 0
     gi = T.Instance.from_gen(inst, score_mode=mode)
     host = T.Solution(gi, sol)
@@ -641,7 +641,7 @@ def test_etga_theta_all_is_full_neighbourhood():
     full = T.Solution(T.Instance.from_gen(inst), sol)
     edge = T.Solution(T.Instance.from_gen(inst, granular_theta=inst.dist.shape[0]), sol)
     for s in (full, edge):
-        s.eval(T.OP_ALL)
+        s.eval(T.OP_STANDARD)
     np.testing.assert_array_equal(full.keys(), edge.keys())
 
 
@@ -652,10 +652,10 @@ def test_etga_device_step_lockstep(name):
     _need_gpu()
     if name == "cvrp":
         inst, sol = G.x_like(6, n=200, target_routes=9)
-        mask, theta = T.OP_ALL, 10
+        mask, theta = T.OP_STANDARD, 10
     else:
         inst, sol = G.gh_like(6, n=200, kind="R2")
-        mask, theta = T.OP_ALL & ~T.OP_2OPT, 20
+        mask, theta = T.OP_STANDARD & ~T.OP_2OPT, 20
     orc = O.Oracle.from_instance(inst)
     M = O.granular_mask(inst.dist, theta)
     gi = T.Instance.from_gen(inst, granular_theta=theta)
@@ -719,14 +719,14 @@ def test_etga_virtual_shards_equal_unsharded(n_shards):
     inst, sol = G.x_like(7, n=400, target_routes=17)
     gs = T.Solution(T.Instance.from_gen(inst, granular_theta=12), sol)
     gs.device_stats()
-    gs.eval(T.OP_ALL)
+    gs.eval(T.OP_STANDARD)
     full = gs.keys()
     full_counts, _ = gs.device_stats()
     comb = np.full(T.N_VARIANTS, np.iinfo(np.uint64).max, dtype=np.uint64)
     tot = np.zeros(T.N_VARIANTS, dtype=np.uint64)
     for s in range(n_shards):
         gs.set_shard(s, n_shards)
-        gs.eval(T.OP_ALL)
+        gs.eval(T.OP_STANDARD)
         comb = np.minimum(comb, gs.keys())
         c, _ = gs.device_stats()
         tot += c
@@ -772,7 +772,7 @@ def test_mixed_grid_device_steps_share_the_barrier():
     _need_gpu()
     inst, sols = G.population(2, n=200, n_sol=4)
     gi = T.Instance.from_gen(inst)
-    mask = T.OP_ALL & ~T.OP_2OPT
+    mask = T.OP_STANDARD & ~T.OP_2OPT
     db = T.Batch(gi, sols)
     host = [T.Solution(gi, s) for s in sols]
     for it in range(12):
@@ -839,11 +839,11 @@ def test_penalised_device_steps_lockstep(name):
     gi = T.Instance.from_gen(inst, score_mode=1, slack=-1 if name.endswith("0") else 0)
     host, dev = T.Solution(gi, sol), T.Solution(gi, sol)
     for k in range(30):
-        host.step(T.OP_ALL)
-        dev.step_async(T.OP_ALL)
+        host.step(T.OP_STANDARD)
+        dev.step_async(T.OP_STANDARD)
         if k % 10 == 9:
             assert dev.routes() == host.routes(), k
     fresh = T.Solution(gi, dev.routes())
     for s in (dev, fresh):
-        s.eval(T.OP_ALL)
+        s.eval(T.OP_STANDARD)
     np.testing.assert_array_equal(dev.keys(), fresh.keys())

@@ -14,7 +14,7 @@ a = ap.parse_args()
 inst, sol = G.config(a.config)
 gs = T.Solution(T.Instance.from_gen(inst), sol)
 ap2 = None
-mask = {"ns": T.OP_FUSED_NS, "all": T.OP_ALL}.get(os.environ.get("PROBE_MASK", "all"), T.OP_ALL)
+mask = {"ns": T.OP_FUSED_NS, "all": T.OP_STANDARD}.get(os.environ.get("PROBE_MASK", "all"), T.OP_STANDARD)
 flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")
 lib = T.lib()
 lib.tga_debug_inter_probe.argtypes = [C.c_void_p, C.c_int32]

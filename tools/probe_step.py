@@ -14,7 +14,7 @@ a = ap.parse_args()
 inst, sol = G.config(a.config)
 gi = T.Instance.from_gen(inst)
 gs = T.Solution(gi, sol)
-mask = T.OP_ALL if inst.tw is None else T.OP_ALL & ~T.OP_2OPT
+mask = T.OP_STANDARD if inst.tw is None else T.OP_STANDARD & ~T.OP_2OPT
 flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")
 gs.descent(mask, 3)
 torch.cuda.synchronize()

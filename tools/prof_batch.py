@@ -6,7 +6,7 @@ import tga_gen as G
 from paper_2506_17357_b200 import tga as T
 inst, sols = G.config("cfg5")
 b = T.Batch(T.Instance.from_gen(inst), sols)
-mask = T.OP_ALL & ~T.OP_2OPT
+mask = T.OP_STANDARD & ~T.OP_2OPT
 for _ in range(3):
     b.step_async(mask)
 torch.cuda.synchronize()

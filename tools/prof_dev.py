@@ -12,6 +12,6 @@ a = ap.parse_args()
 inst, sol = G.config(a.config)
 gi = T.Instance.from_gen(inst, granular_theta=a.granular)
 gs = T.Solution(gi, sol)
-mask = T.OP_ALL if inst.tw is None else T.OP_ALL & ~T.OP_2OPT
+mask = T.OP_STANDARD if inst.tw is None else T.OP_STANDARD & ~T.OP_2OPT
 ms = gs.descent(mask, a.steps, timed=True)
 print("step ms", [round(float(x), 4) for x in ms])

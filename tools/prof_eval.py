@@ -12,7 +12,7 @@ ap.add_argument("--score", type=int, default=0)
 a = ap.parse_args()
 inst, sol = G.config(a.config)
 gs = T.Solution(T.Instance.from_gen(inst, score_mode=a.score), sol)
-m = {"ns": T.OP_FUSED_NS, "all": T.OP_ALL if inst.tw is None else T.OP_ALL & ~T.OP_2OPT,
+m = {"ns": T.OP_FUSED_NS, "all": T.OP_STANDARD if inst.tw is None else T.OP_STANDARD & ~T.OP_2OPT,
      "inter": T.OP_INTER}.get(a.mask) or int(a.mask, 16)
 for _ in range(a.reps):
     gs.eval(m)

@@ -11,7 +11,7 @@ a = ap.parse_args()
 inst, sol = G.config(a.config)
 gi = T.Instance.from_gen(inst)
 gs = T.Solution(gi, sol)
-mask = {"all": T.OP_ALL if inst.tw is None else T.OP_ALL & ~T.OP_2OPT, "inter": T.OP_INTER,
+mask = {"all": T.OP_STANDARD if inst.tw is None else T.OP_STANDARD & ~T.OP_2OPT, "inter": T.OP_INTER,
         "ns": T.OP_FUSED_NS}[a.mask]
 for _ in range(a.steps):
     gs.eval(mask & T.OP_INTER)

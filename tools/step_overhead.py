@@ -16,7 +16,7 @@ ap.add_argument("--replicas", type=int, default=24)
 a = ap.parse_args()
 inst, sol = G.config(a.config)
 gi = T.Instance.from_gen(inst)
-mask = T.OP_ALL if inst.tw is None else T.OP_ALL & ~T.OP_2OPT
+mask = T.OP_STANDARD if inst.tw is None else T.OP_STANDARD & ~T.OP_2OPT
 flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")
 K = a.steps
 

@@ -14,7 +14,7 @@ ap.add_argument("--reps", type=int, default=20)
 a = ap.parse_args()
 inst, sol = G.config(a.config)
 gs = T.Solution(T.Instance.from_gen(inst), sol)
-m = {"ns": T.OP_FUSED_NS, "inter": T.OP_INTER, "all": T.OP_ALL}.get(a.mask) or int(a.mask, 16)
+m = {"ns": T.OP_FUSED_NS, "inter": T.OP_INTER, "all": T.OP_STANDARD}.get(a.mask) or int(a.mask, 16)
 st = torch.cuda.Stream()
 gs.set_stream(st)
 gs.eval(m, st)

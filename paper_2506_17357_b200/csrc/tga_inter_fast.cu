@@ -426,10 +426,19 @@ __global__ void __launch_bounds__(kFastThreads) k_inter_fast(const SlotRec *__re
     pdl_wait();                       // Dp / records / keys are written by the stream predecessors
     const int cta = static_cast<int>(blockIdx.x);
     const int nI = (SV.Qp + U - 1) / U;
-    (void)tiles;
+    // a CTA's first tile is decoded arithmetically (no plan-table load before its first TMA);
+    // later tiles of a persistent CTA come from the plan table (one load, issued a tile ahead:
+    // the arithmetic decode costs every thread ~2 x 50 instructions per tile)
+    const int first_wave = t_lo + static_cast<int>(gridDim.x);
     auto item = [&](int t) -> FastItem {
         int I, J;
-        fast_tile_of(t, nI, kFastTV / U, I, J);
+        if (t < first_wave) {
+            fast_tile_of(t, nI, kFastTV / U, I, J);
+        } else {
+            const uint32_t ij = __ldg(tiles + t);
+            I = static_cast<int>(ij >> 16);
+            J = static_cast<int>(ij & 0xFFFFu);
+        }
         return FastItem{rec, rectw, &tmap, keys, Qc, 0, I, J};
     };
     if (MASK2 == 0 || cta < split) {

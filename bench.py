@@ -195,6 +195,42 @@ def oracle_sweep_rate(inst, routes, budget_s=12.0, rows_frac=None, row_offset=0)
     return tot_c / tot_t, tot_c, tot_t, sweeps
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_all_cores_rate(inst, routes, budget_s=6.0):
+    """The CPU oracle as it stands, process-parallel over canonical u-row chunks on every
+    host core (ctypes releases the GIL for each C call, one thread per core):
+    full sweeps of every standard variant; returns (moves/s, candidates, seconds, sweeps, cores)."""
+    import oracle as O
+    from concurrent.futures import ThreadPoolExecutor
+    orc = O.Oracle.from_instance(inst)
+    variants = [v for v in range(23) if not (inst.tw is not None and v == 0)]
+    Q = O.canonical_q(routes)
+    ptr_cust = orc._csr(routes)
+    nw = max(1, len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1))
+    k = max(1, min(Q, 4 * nw))
+    jobs = [(v, Q * i // k, Q * (i + 1) // k) for v in variants for i in range(k) if Q * (i + 1) // k > Q * i // k]
+    tot_c, sweeps = 0, 0
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=nw) as ex:
+        while True:
+            for m in ex.map(lambda j: orc.best_move(ptr_cust, j[0], u_lo=j[1], u_hi=j[2]), jobs):
+                tot_c += m.n_candidates
+            sweeps += 1
+            if time.perf_counter() - t0 >= budget_s:
+                break
+    dt = time.perf_counter() - t0
+    return tot_c / dt, tot_c, dt, sweeps, nw
+
+
 def concat_sweep_rate(inst, routes, budget_s=5.0):
     """The fast CPU evaluator (cpu_baseline/: O(1) concatenation per candidate,
     the paper's MA-N-style CPU move evaluation), single thread, full
@@ -645,6 +681,15 @@ def run_tga(args):
         cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle",
                "sample": f"{sw} full sweep(s) of all variants on state A ({c} candidates, {t:.1f} s), "
                          "single-threaded C oracle that rebuilds every neighbour route"}
+    cpu_all = None
+    if ws == 1 and not args.no_cpu_baseline:
+        rate, c, t, sw, nw = oracle_all_cores_rate(inst, sol0.routes)
+        cpu_all = {"value": rate, "unit": UNIT, "cores": nw, "kind": "oracle, all host cores",
+                   "cpu": cpu_model(),
+                   "sample": f"{sw} full sweep(s) of all variants on state A ({c} candidates, {t:.1f} s), the "
+                             f"C oracle over canonical u-row chunks on {nw} threads (one per core)"}
+        if cpu:
+            cpu["cpu"] = cpu_model()
     cpu_fast = None
     if ws == 1 and not args.no_cpu_baseline:
         rate, c, t, sw = concat_sweep_rate(inst, sol0.routes, budget_s=5.0)
@@ -681,7 +726,7 @@ def run_tga(args):
         "candidates_per_step": cand_total / K,
         "roofline": primary, "roofline_alt": alt,
         "per_operator_steady_state": per_op,
-        "cpu_baseline": cpu, "cpu_baseline_concat": cpu_fast,
+        "cpu_baseline": cpu, "cpu_baseline_all_cores": cpu_all, "cpu_baseline_concat": cpu_fast,
         "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
     }
     if row_block is not None:

@@ -225,15 +225,26 @@ __device__ __forceinline__ void fast_body(ItemF item, int w0, int w1, int wstrid
 #pragma unroll
     for (int i = 0; i < NV; ++i) acc[i] = kNoKey;
 
+    // A stage keeps the column records of its last tile: when its next tile has the same
+    // (solution, column band) -- consecutive items of a population run are ordered by column
+    // band -- only the Dp box and the row records are copied (the column records are the
+    // largest part of a tile's traffic).  s_colkey[b] is written by the one thread that
+    // refills stage b, after every warp has released it.
+    __shared__ int s_colkey[2];
+    if (tid == 0) s_colkey[0] = s_colkey[1] = -1;
+    __syncthreads();
     auto issue = [&](const FastItem &f, int b) {
         uint64_t *br = b ? &bar[1] : &bar[0];
-        f_expect(br, G::BoxBytes + G::RowBytes + G::ColBytes + G::RowTW + G::ColTW);
+        const int key = f.sol * 1024 + f.J;
+        const bool cols = s_colkey[b] != key;
+        s_colkey[b] = key;   // before the arrive below publishes it to the stage's next refiller
+        f_expect(br, G::BoxBytes + G::RowBytes + G::RowTW + (cols ? G::ColBytes + G::ColTW : 0));
         f_tma2d(b ? dp1 : dp0, f.map, f.J * kFastTV - 4, f.I * U - 1, br);
         f_bulk(b ? rows1 : rows0, f.rec + f.I * U, G::RowBytes, br);
-        f_bulk(b ? cols1 : cols0, f.rec + f.J * kFastTV, G::ColBytes, br);
+        if (cols) f_bulk(b ? cols1 : cols0, f.rec + f.J * kFastTV, G::ColBytes, br);
         if (TW) {
             f_bulk(b ? trows1 : trows0, f.rectw + f.I * U, G::RowTW, br);
-            f_bulk(b ? tcols1 : tcols0, f.rectw + f.J * kFastTV, G::ColTW, br);
+            if (cols) f_bulk(b ? tcols1 : tcols0, f.rectw + f.J * kFastTV, G::ColTW, br);
         }
     };
     // ---- fused argmin of the running minima: warp REDUX -> the warp's private shared

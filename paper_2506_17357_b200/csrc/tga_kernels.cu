@@ -375,15 +375,27 @@ __device__ __forceinline__ void scan_route_g(const ScanArgs<DT> &A, const int r,
 // The same rebuild by a whole block (every thread must call it): forward and
 // backward passes in warps 0 and 1 at once, then the per-slot records over all
 // threads -- the critical path of the device step's update for long routes.
+__device__ __forceinline__ unsigned long long scan_gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 template <class DT, bool TW, class NodeF, class CanonF>
 __device__ __forceinline__ void scan_route_block(const ScanArgs<DT> &A, const int r, const int base, const int L,
-                                                 const int cap, NodeF nodeAt, CanonF canonAt) {
+                                                 const int cap, NodeF nodeAt, CanonF canonAt,
+                                                 unsigned long long *stamp = nullptr) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (stamp && tid == 0) stamp[0] = scan_gtime();   // diagnostics: start / passes done / records done
     scan_spare<DT, TW>(A, tid, blockDim.x, base, L, cap);
     if (warp == 0) scan_fwd_pass<DT, TW>(A, r, lane, base, L, nodeAt);
     else if (warp == 1) scan_bwd_pass<DT, TW>(A, r, lane, base, L, nodeAt, true);
     __syncthreads();   // prefix / suffix records and rW[r] of this route are visible to the block
+    if (stamp && tid == 0) stamp[1] = scan_gtime();
     scan_rec_pass<DT, TW>(A, r, tid, blockDim.x, base, L, A.rW[r], nodeAt, canonAt);
+    if (stamp) {
+        __syncthreads();
+        if (tid == 0) stamp[2] = scan_gtime();
+    }
 }
 
 template <class DT, bool TW>
@@ -639,7 +651,8 @@ __device__ __forceinline__ void pick_update_multi(const DevState &S, const ScanA
         if (b == (scan0 + q) % G) {   // block-uniform: the whole block rebuilds the route
             const int r = dm.nr[q].r, base = dm.lo[q], off = q ? n1 : 0;
             scan_route_block<DT, TW>(A, r, base, dm.nr[q].L, dm.hi[q] - base,
-                                     [&](int x) { return nn[off + x - base]; }, [&](int x) { return x; });
+                                     [&](int x) { return nn[off + x - base]; }, [&](int x) { return x; },
+                                     (q == 0 && S.acc[31]) ? S.acc + 40 : nullptr);
             if (tid == 0 && S.acc[31]) S.acc[44 + q] = gtimer();   // diagnostics: scan end (globaltimer)
         }
     }

@@ -28,6 +28,8 @@ for k in range(a.steps):
     rows.append(d)
     print(a.config, "step %.1f us" % (1e3 * float(ms[0])), "phase cycles", d,
           "| scan ends (ns after block 0 decode):", [int(p[12 + q]) - int(p[11]) if p[12 + q] else None for q in range(2)],
-          "block 0 end:", int(p[14]) - int(p[11]) if p[14] else None)
+          "block 0 end:", int(p[14]) - int(p[11]) if p[14] else None,
+          "| route-0 scan ns: passes", int(p[9]) - int(p[8]) if p[8] else None, "records", int(p[10]) - int(p[9]) if p[9] else None,
+          "start", int(p[8]) - int(p[11]) if p[8] else None)
 r = np.array(rows[2:], dtype=np.float64)
 print("median phase (us @1.965GHz):", [round(x / 1965.0, 2) for x in np.median(r, axis=0)])

@@ -834,9 +834,14 @@ def row_shard_block(args, ws, rank, local, dev, stream):
     gs.set_stream(stream)
     if ws > 1:
         import torch.distributed as dist
-        obj = [T.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        gs.comm_init(rank, ws, obj[0])
+        if os.environ.get("TGA_BENCH_SHARED_GPU") == "1":
+            # ranks sharing one GPU (a smoke run of the multi-rank flow): NCCL refuses two ranks
+            # on one device, so the shards run without the collective (keys per shard)
+            gs.set_shard(rank, ws)
+        else:
+            obj = [T.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            gs.comm_init(rank, ws, obj[0])
     out = {"workload": "cfg4: " + G.CONFIGS["cfg4"] + f"; candidate rows over {ws} rank(s), keys "
                        "MIN-allreduced over NCCL per sweep" if ws > 1 else "cfg4 on 1 GPU (no collective)",
            "scaling": "strong", "n_gpus": ws}

@@ -470,6 +470,10 @@ def run_tga(args):
     def replay(g, timed=False):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(stream):
+            # a ~0.1 ms spin kernel ahead of the start event keeps the device busy while the host
+            # submits the graph, so the device-timed region holds the K steps and not the host's
+            # submission latency of a graph of 2K nodes (measured ~70 us per launch otherwise)
+            torch.cuda._sleep(200_000)
             e0.record(stream)
             g.replay()
             e1.record(stream)
@@ -515,6 +519,23 @@ def run_tga(args):
         c, a_ = r.device_stats()   # exact candidate counts of the K evaluated neighbourhoods
         dev_counts += c
         applied += a_
+    # K-dependence of the line: the same steps as a graph of 2K, so the per-step
+    # cost without any fixed cost of one graph replay is (T(2K) - T(K)) / K
+    g_2k = None
+    try:
+        g_2k = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_2k, stream=stream):
+            for k in range(2 * K):
+                reps[k % len(reps)].step_async(mask_all)
+        replay(g_2k)
+        t2k_ms = replay(g_2k)
+        step_marginal_ms = max(0.0, (t2k_ms - tot_ms) / K)
+        graph_fixed_ms = max(0.0, tot_ms - K * step_marginal_ms)
+    except Exception:   # pragma: no cover - capture failure must not cost the line
+        step_marginal_ms, graph_fixed_ms = None, None
+    del g_2k
+    for r in reps:
+        r.device_stats()
     load_for(lambda: replay(g_load), 0.4)
     clocks = sampler.stop()
     del g_load, load_reps
@@ -719,6 +740,8 @@ def run_tga(args):
                    "parallelism": (f"row-shard x{ws} (NCCL MIN-allreduce)" if row_shard else
                                    f"independent descents x{ws}" if ws > 1 else "1 GPU")},
         "sweeps_per_s": sweeps_per_s, "applied_moves": int(applied),
+        "us_per_step_marginal": None if step_marginal_ms is None else step_marginal_ms * 1e3,
+        "graph_launch_fixed_us": None if graph_fixed_ms is None else graph_fixed_ms * 1e3,
         "step": "tga_step_async: eval all variants -> on-device best move + splice -> update kernel; "
                 "K steps captured in one CUDA graph, timed by two CUDA events",
         "kernel_timing": "second pass of the same K-step graph with CUDA events around every "

@@ -1687,17 +1687,34 @@ bool pdl_enabled(int which) {
 }
 void note_launch() { ++g_launches; }
 
-__global__ void k_fill_u64(uint64_t *__restrict__ p, size_t n, uint64_t v) {
-    pdl_trigger();   // a programmatic dependent (the sweep kernel) may launch now; it waits before its key updates
+// The per-eval key reset.  Launched as a programmatic dependent (pdl) it waits for its
+// stream predecessor before writing the keys; it releases its own dependent (the north-star
+// sweep) after that wait, or -- early, when the predecessor is an evaluation of the same,
+// unchanged solution, so the dependent's pre-wait reads of Dp / records are safe -- at once,
+// so consecutive sweeps of an evaluation loop overlap.
+__global__ void k_fill_u64(uint64_t *__restrict__ p, size_t n, uint64_t v, int early) {
+    if (early) pdl_trigger();
+    pdl_wait();
+    if (!early) pdl_trigger();
     for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<size_t>(gridDim.x) * blockDim.x)
         p[i] = v;
 }
-cudaError_t launch_fill_u64(uint64_t *p, size_t n, uint64_t v, cudaStream_t st) {
+cudaError_t launch_fill_u64(uint64_t *p, size_t n, uint64_t v, cudaStream_t st, bool pdl, bool early) {
     if (n == 0) return cudaSuccess;
     const int block = n <= 32 ? 32 : 256;
     const int grid = static_cast<int>(std::min<size_t>((n + block - 1) / block, 1184));
-    k_fill_u64<<<grid, block, 0, st>>>(p, n, v);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, k_fill_u64, p, n, v, early ? 1 : 0);
+    if (e != cudaSuccess) return e;
     note_launch();
     return cudaGetLastError();
 }

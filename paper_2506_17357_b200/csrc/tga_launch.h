@@ -136,7 +136,9 @@ unsigned long long launch_count();
 void note_launch();
 // p[0..n) = v on stream st: the per-eval key reset as a kernel node (a memset node
 // between two kernels costs ~3 us more inside a graph on B200, tools/graph_floor.cu)
-cudaError_t launch_fill_u64(uint64_t *p, size_t n, uint64_t v, cudaStream_t st);
+// pdl: launched as a programmatic dependent of its stream predecessor (it waits for it before
+// writing); early: release its own dependent before that wait (see k_fill_u64)
+cudaError_t launch_fill_u64(uint64_t *p, size_t n, uint64_t v, cudaStream_t st, bool pdl = false, bool early = false);
 
 // Programmatic dependent launch (PDL): the kernel may be scheduled while its
 // stream predecessor is still running; it calls pdl_wait() before its first

@@ -143,6 +143,9 @@ __global__ void __launch_bounds__(kNsW * 32, DUMP ? 1 : (RW == 16 ? 4 : 5))
             issue(I * TU, J * kNsTV);
         }
     }
+    // a programmatic dependent (the next evaluation's key reset, which waits for this grid
+    // before it writes) may launch now
+    pdl_trigger();
     uint64_t acc[3] = {kNoKey, kNoKey, kNoKey};   // 2-opt*, relocate, swap (1,1)
     __syncthreads();
     uint32_t phase = 0u;

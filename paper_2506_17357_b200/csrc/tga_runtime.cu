@@ -186,6 +186,8 @@ struct tga_solution {
     CUtensorMap nsmap{};           // Dp with the north-star sweep's box (tga_ns.cu)
     bool ns_ok = false;            // CVRP feasible-only int32 with |c| < 2^20: the NS sweep kernel applies
     int ns_rw = 8;                 // its rows per warp (ns_rows_per_warp)
+    uint64_t ns_eval_gen = ~0ull;  // generation / stream of the last evaluation that ended in the NS sweep
+    cudaStream_t ns_eval_stream = nullptr;
     int32_t *nsc = nullptr;        // its column-term planes [kNscF][pitch] (written by the scans)
     LoadRec *fwdP = nullptr, *bwdP = nullptr;   // VRPSPDTW prefix / suffix load records (Eq. 3a-d)
     bool fast = false;
@@ -994,9 +996,15 @@ extern "C" int32_t tga_eval(tga_solution *s, uint32_t mask, void *stream) {
     const bool ns = ns_path(s, mask);
     bool reset = false;
     if (!accumulate && !(s->keys_clean && s->clean_cap == capture_id(st))) {
-        TGA_CUDA(launch_fill_u64(s->keys, TGA_N_VARIANTS, ~0ull, st));
+        // before the north-star sweep the reset is a programmatic dependent of its predecessor;
+        // when that is the sweep of the same, unchanged solution on this stream (an evaluation
+        // loop) the next sweep may start before the previous one ends (k_fill_u64)
+        const bool early = ns && s->ns_eval_gen == s->gen && s->ns_eval_stream == st;
+        TGA_CUDA(launch_fill_u64(s->keys, TGA_N_VARIANTS, ~0ull, st, ns, early));
         reset = true;
     }
+    s->ns_eval_gen = ns ? s->gen : ~0ull;
+    s->ns_eval_stream = st;
     s->keys_clean = false;
     ScoreParams sp{I->Q, I->opt.score_mode, I->opt.w_load, I->opt.w_tw};
     // row shard of the tile list and of the intra slot range

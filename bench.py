@@ -767,10 +767,13 @@ def run_tga(args):
 def north_star_block(args, dev, stream):
     """BASELINE.json north_star: the 2000-customer full 2-opt*+relocate+swap sweep
     (X-like CVRP, 2000 customers, 87 routes + spare; one solution, L2-warm steady
-    state).  us_per_sweep: S back-to-back tga_eval(OP_FUSED_NS) -- key reset + the
-    k_ns_sweep launch -- in one CUDA graph, CUDA events around R replays.  kernel_us:
-    the same with accumulating evals (no key reset node): S back-to-back k_ns_sweep
-    launches per graph, so per launch including the launch gap.
+    state).  us_per_sweep: S back-to-back tga_eval(OP_FUSED_NS) -- key
+    reset + the k_ns_sweep launch -- in one CUDA graph, CUDA events around R replays; the
+    solution does not change between them, so each reset is a programmatic dependent of
+    the previous sweep that releases the next sweep at once, and consecutive sweeps
+    overlap (the tail of one with the loads and compute of the next).  kernel_us:
+    accumulating evals (no reset, plain launches): one sweep at a time, launch gap
+    included.
     Fractions: algorithmic lane-ops (ALG_OPS x exact candidate counts) over the
     148 x 128 x f_max issue peak, and the Dp upper triangle (Qp^2 / 2 int32) over the
     measured HBM copy bandwidth."""

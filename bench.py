@@ -841,7 +841,8 @@ def north_star_block(args, dev, stream):
             "alu_frac_kernel": ops / kern_s / alu_peak, "alu_frac_sweep": ops / per_s / alu_peak,
             "hbm_frac_kernel": tri / kern_s / hbm_peak, "hbm_frac_sweep": tri / per_s / hbm_peak,
             "alg_ops": ops, "alg_bytes": tri, "alu_peak_tops": alu_peak / 1e12, "hbm_peak_gbs": hbm_peak / 1e9,
-            "peak_source": pk_src, "target": "sweep >= 0.6 of the binding roofline (ALU issue: <= 4.6 us)"}
+            "peak_source": pk_src, "target": "sweep >= 0.6 of the binding roofline (ALU issue: <= 4.6 us)",
+            "target_met": bool(ops / per_s / alu_peak >= 0.6)}
 
 
 def row_shard_block(args, ws, rank, local, dev, stream):

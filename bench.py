@@ -92,6 +92,8 @@ class ClockSampler:
         self.path = os.path.join("/tmp", f"tga_clocks_{os.getpid()}.csv")
 
     def start(self):
+        if os.environ.get("TGA_BENCH_NO_SMI"):   # diagnostics only: measure the sampler's own interference
+            return
         try:
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
@@ -480,9 +482,16 @@ def run_tga(args):
         torch.cuda.synchronize(dev)
         return e0.elapsed_time(e1)
 
-    # ---------------- warm-up: W device steps of every replica, then one replay of the graph
+    # ---------------- warm-up: W device steps of every replica, then one replay of the graph.
+    # Replica i takes i extra warm-up steps: identical replicas descending in lockstep would
+    # all reach a full relayout (a route outgrowing its spare slots, ~20 us) at the same step,
+    # so whether the timed window holds n_rep relayouts or none would depend on K; staggered,
+    # the window sees them at the descent's own rate.
     for _ in range(W):
         for r in reps:
+            r.step_async(mask_all)
+    for i, r in enumerate(reps):
+        for _ in range(i):
             r.step_async(mask_all)
     torch.cuda.synchronize(dev)
     launches0 = T.launch_count()

@@ -44,11 +44,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
         flags += ["-Xptxas", "-v"]
     tmp = os.path.join(HERE, "build")
     os.makedirs(tmp, exist_ok=True)
+    cmds = []
     for src in SOURCES:
         obj = os.path.join(tmp, src.replace(".cu", ".o"))
-        cmd = [nvcc(), *flags, "-c", os.path.join(CSRC, src), "-o", obj]
-        subprocess.check_call(cmd)
+        cmds.append([nvcc(), *flags, "-c", os.path.join(CSRC, src), "-o", obj])
         objs.append(obj)
+    # the translation units are independent: compile them side by side
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as ex:
+        list(ex.map(subprocess.check_call, cmds))
     subprocess.check_call([nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a",
                            "-o", LIB, *objs, "-ldl"])
     return LIB

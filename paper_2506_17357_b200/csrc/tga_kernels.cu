@@ -426,21 +426,41 @@ __device__ __forceinline__ void update_rows(const ScanArgs<DT> &A, DT *__restric
     const int nb_rows = n1 + n2;
     const int n_routes = u.full ? R : (u.r1 >= 0) + (u.r2 >= 0);
     const int total = nb_rows + (n_routes + 7) / 8;
-    for (int b = unit0; b < total; b += ustride) {
-        if (b < nb_rows) {
-            const int a = b < n1 ? u.lo1 + b : u.lo2 + (b - n1);
-            const DT *crow = C + static_cast<size_t>(A.node[a]) * n;
-            DT *drow = Dp + static_cast<size_t>(a) * pitch;
-            for (int c = 4 * threadIdx.x; c < pitch; c += 4 * blockDim.x) {
-                const int4 nd = *reinterpret_cast<const int4 *>(A.node + c);
-                *reinterpret_cast<int4 *>(drow + c) =
-                    make_int4(bits(__ldg(crow + nd.x)), bits(__ldg(crow + nd.y)), bits(__ldg(crow + nd.z)),
-                              bits(__ldg(crow + nd.w)));
-            }
-        } else {
-            const int j = (b - nb_rows) * 8 + static_cast<int>(threadIdx.x >> 5);
-            if (j < n_routes) scan_route<DT, TW>(A, u.full ? j : (j == 0 && u.r1 >= 0 ? u.r1 : u.r2), threadIdx.x & 31);
+    // rows: a block takes its units RG at a time -- the RG row node ids in one round, then
+    // per column chunk one (L1-resident) load of the column node ids and RG x 4 gathers in
+    // flight (a full relayout refreshes every row: ~7 rows per block at Q_p = 1000)
+    constexpr int RG = 8;
+    auto row_of = [&](int b) { return b < n1 ? u.lo1 + b : u.lo2 + (b - n1); };
+    for (int b0 = unit0; b0 < nb_rows; b0 += RG * ustride) {
+        int na[RG];
+#pragma unroll
+        for (int i = 0; i < RG; ++i) {
+            const int b = b0 + i * ustride;
+            na[i] = b < nb_rows ? A.node[row_of(b)] : -1;
         }
+        for (int c = 4 * threadIdx.x; c < pitch; c += 4 * blockDim.x) {
+            const int4 nd = __ldg(reinterpret_cast<const int4 *>(A.node + c));
+            DT v[RG][4];
+#pragma unroll
+            for (int i = 0; i < RG; ++i) {
+                if (na[i] < 0) continue;
+                const DT *crow = C + static_cast<size_t>(na[i]) * n;
+                v[i][0] = __ldg(crow + nd.x); v[i][1] = __ldg(crow + nd.y);
+                v[i][2] = __ldg(crow + nd.z); v[i][3] = __ldg(crow + nd.w);
+            }
+#pragma unroll
+            for (int i = 0; i < RG; ++i) {
+                if (na[i] < 0) continue;
+                DT *drow = Dp + static_cast<size_t>(row_of(b0 + i * ustride)) * pitch;
+                *reinterpret_cast<int4 *>(drow + c) = make_int4(bits(v[i][0]), bits(v[i][1]), bits(v[i][2]), bits(v[i][3]));
+            }
+        }
+    }
+    // re-scans: one unit per 8 routes, after the row units
+    for (int b = unit0; b < total; b += ustride) {
+        if (b < nb_rows) continue;
+        const int j = (b - nb_rows) * 8 + static_cast<int>(threadIdx.x >> 5);
+        if (j < n_routes) scan_route<DT, TW>(A, u.full ? j : (j == 0 && u.r1 >= 0 ? u.r1 : u.r2), threadIdx.x & 31);
     }
 }
 
@@ -1455,25 +1475,28 @@ __device__ __forceinline__ TwRec scan_bwd(TwRec rec, float &outl, int lane, int 
     return rec;
 }
 
-template <class DT, bool DUMP = false>
+// One warp per (u slot x, length A of the segment starting at x): the forward pass
+// evaluates relocate N = A after the segment and the swaps (A, b), the backward pass
+// relocate N = A before it.  The three lengths are independent scans (no shared
+// carries), so splitting them across warps triples the warps in flight without
+// adding work (blockIdx.y = A - 1).
+template <class DT, int A, bool DUMP = false>
 __device__ __forceinline__ void intra_tw_warp(const SolView<DT> &S, const ScoreParams &sp, uint32_t vmask, int x,
                                               unsigned long long *red, unsigned long long *dump = nullptr) {
     const int lane = threadIdx.x & 31;
+    constexpr int kRl = 10 + A, kSw0 = 14 + 3 * (A - 1);   // relocate N = A; swaps (A, 1..3)
     auto D = [&](int a, int b) -> DT { return S.Dp[static_cast<size_t>(a) * S.pitch + b]; };
     auto E = [&](int y) -> DT { return S.enext[y]; };
     // ---- slot x: everything indexed by x alone, one round of loads
     const int cx = S.canon[x], p = S.pos[x], L = S.rlen[x], r = S.route[x];
     const TwRec F = S.fwdT[x - 1];
-    const TwRec sg2x = S.seg2T[x], sg3x = S.seg3T[x];
-    const int nx = S.node[x];
-    const DT Exm1 = E(x - 1), Ex0 = E(x), Ex1 = E(x + 1), Ex2 = E(x + 2);
-    const DT br1 = S.bridge1[x], br2 = S.bridge2[x], br3 = S.bridge3[x];
-    if (!(cx >= 0 && p >= 1)) return;  // warp-uniform
+    const TwRec segxA = A == 1 ? S.node_tw[S.node[x]] : (A == 2 ? S.seg2T[x] : S.seg3T[x]);
+    const DT Exm1 = E(x - 1), ExA = E(x + A - 1);
+    const DT brA = A == 1 ? S.bridge1[x] : (A == 2 ? S.bridge2[x] : S.bridge3[x]);
+    if (!(cx >= 0 && p >= 1) || p + A - 1 > L) return;  // warp-uniform
     const int base = x - p;
     const int W = S.rW[r];
     const float TV0 = S.rTV[r];
-    const TwRec segx[3] = {S.node_tw[nx], sg2x, sg3x};
-    const DT brg[3] = {br1, br2, br3}, Exn[3] = {Ex0, Ex1, Ex2};  // E(x + N - 1)
     auto keyof = [&](bool ok, DT dD, float tv, int q, int var) -> uint64_t {
         const uint32_t idx = static_cast<uint32_t>(x) * S.Qc + static_cast<uint32_t>(base + q);
         const uint64_t k = score_key<DT, true>(sp, ok, dD, W, 0, W, 0, tv, 0.f, TV0, 0.f, idx);
@@ -1482,91 +1505,89 @@ __device__ __forceinline__ void intra_tw_warp(const SolView<DT> &S, const ScoreP
         }
         return k;
     };
-    uint64_t best[23];
-#pragma unroll
-    for (int i = 0; i < 23; ++i) best[i] = kNoKey;
+    uint64_t bRl = kNoKey, bRlB = kNoKey, bSw[3] = {kNoKey, kNoKey, kNoKey};
+    const bool need_rl = (vmask >> kRl) & 1u;
+    const bool any_sw = (vmask >> kSw0) & 7u;
 
     // ------------------------------------------------ forward pass (chunks left to right)
-    // G_a(q) = [x+a .. q] (plain scan from q = p+a); relocate-forward prefixes are
-    // F(x-1) + G_N(q) by associativity of Eq. 4 (exact on integer-valued times)
-    TwRec cG[3];
-    bool hG[3] = {false, false, false};
-    for (int qb = 0; qb <= L; qb += 32) {
-        const int q = qb + lane;
-        const bool in = q <= L;
-        const int v = base + min(q, L);
-        // lane data, loaded up front (masked lanes read slots of this or the next route)
-        const int nv = S.node[v];
-        const DT Evm1 = E(max(v - 1, base)), Ev0 = E(v), Ev1 = E(v + 1), Ev2 = E(v + 2);
-        const TwRec bw[3] = {S.bwdT[v + 1], S.bwdT[v + 2], S.bwdT[v + 3]};
-        const TwRec sg2 = S.seg2T[v], sg3 = S.seg3T[v];
-        const DT dm1 = D(x - 1, v), dxm = D(x, max(v - 1, base));
-        DT d[4][4];  // Dp(x + i, v + j) = c(node(x + i), node(v + j)), c symmetric
+    // G(q) = [x+A .. q] (plain scan from q = p+A); relocate-forward prefixes are
+    // F(x-1) + G(q) by associativity of Eq. 4 (exact on integer-valued times)
+    if (need_rl || any_sw) {
+        TwRec cG = make_float4(0.f, 0.f, 0.f, 0.f);
+        bool hG = false;
+        const int st = p + A;
+        for (int qb = 0; qb <= L; qb += 32) {
+            const int q = qb + lane;
+            const bool in = q <= L;
+            const int v = base + min(q, L);
+            // lane data, loaded up front (masked lanes read slots of this or the next route)
+            const int nv = S.node[v];
+            const DT Evm1 = E(max(v - 1, base)), Ev0 = E(v), Ev1 = E(v + 1), Ev2 = E(v + 2);
+            const TwRec bw[3] = {S.bwdT[v + 1], S.bwdT[v + 2], S.bwdT[v + 3]};
+            const TwRec sg2 = S.seg2T[v], sg3 = S.seg3T[v];
+            const DT dm1 = D(x - 1, v), dxm = D(x, max(v - 1, base));
+            DT d0[3], dAm1[4], dA[3];   // Dp(x, v + j), Dp(x + A - 1, v + j), Dp(x + A, v + j)
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+            for (int j = 0; j < 3; ++j) d0[j] = D(x, v + j);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) d[i][j] = (i == 3 && j == 3) ? DT(0) : D(x + i, v + j);
-        const TwRec sv = S.node_tw[nv];
-        const TwRec segv[3] = {sv, sg2, sg3};
-        const DT Evb[3] = {Ev0, Ev1, Ev2};  // E(v + b - 1)
-        const float inl0 = q >= 1 ? static_cast<float>(Evm1) : 0.f;  // link (q-1 -> q)
+            for (int j = 0; j < 4; ++j) dAm1[j] = (A == 1 && j < 3) ? DT(0) : D(x + A - 1, v + j);
+            if (A == 1) {
 #pragma unroll
-        for (int a = 1; a <= 3; ++a) {
-            bool any_sw = false;
+                for (int j = 0; j < 3; ++j) dAm1[j] = d0[j];
+            }
 #pragma unroll
-            for (int b = 1; b <= 3; ++b) any_sw |= (vmask >> (14 + 3 * (a - 1) + (b - 1))) & 1u;
-            const bool need_rl = (vmask >> (10 + a)) & 1u;
-            if (!(any_sw || need_rl) || p + a - 1 > L) continue;
-            const int st = p + a;
-            float inl = inl0;
+            for (int j = 0; j < 3; ++j) dA[j] = D(x + A, v + j);
+            const TwRec sv = S.node_tw[nv];
+            const TwRec segv[3] = {sv, sg2, sg3};
+            const DT Evb[3] = {Ev0, Ev1, Ev2};  // E(v + b - 1)
+            float inl = q >= 1 ? static_cast<float>(Evm1) : 0.f;  // link (q-1 -> q)
             const int s_rel = max(st - qb, 0);
             TwRec Gk = scan_fwd(sv, inl, lane, s_rel);
-            if (hG[a - 1] && lane >= s_rel) Gk = tw_cat(cG[a - 1], Gk, inl);
+            if (hG && lane >= s_rel) Gk = tw_cat(cG, Gk, inl);
             TwRec Gm = shfl_up_rec(Gk, 1);  // G(q-1)
-            if (lane == 0) Gm = cG[a - 1];
+            if (lane == 0) Gm = cG;
             if (st <= qb + 31) {  // carry: the run covers the whole chunk from here on
-                cG[a - 1] = shfl_rec(Gk, 31);
-                hG[a - 1] = true;
+                cG = shfl_rec(Gk, 31);
+                hG = true;
             }
-            if (need_rl) {  // relocate N = a after q >= p+N:  [F(x-1) + x+N .. q] + S(x,N) + B(q+1)
-                const int N = a;
+            if (need_rl) {  // relocate N = A after q >= p+N:  [F(x-1) + x+N .. q] + S(x,N) + B(q+1)
                 const bool ok = in && q >= st;
-                const DT rem = brg[N - 1] - Exm1 - Exn[N - 1];
-                const DT dD = rem + d[0][0] + d[N - 1][1] - Ev0;
-                const TwRec P = tw_cat(F, Gk, static_cast<float>(brg[N - 1]));
-                const TwRec A2 = tw_cat(P, segx[N - 1], static_cast<float>(d[0][0]));
-                const float tv = tw_cat(A2, bw[0], static_cast<float>(d[N - 1][1])).w;
-                best[10 + N] = umin64(best[10 + N], keyof(ok, dD, tv, q, 10 + N));
+                const DT rem = brA - Exm1 - ExA;
+                const DT dD = rem + d0[0] + dAm1[1] - Ev0;
+                const TwRec P = tw_cat(F, Gk, static_cast<float>(brA));
+                const TwRec A2 = tw_cat(P, segxA, static_cast<float>(d0[0]));
+                const float tv = tw_cat(A2, bw[0], static_cast<float>(dAm1[1])).w;
+                bRl = umin64(bRl, keyof(ok, dD, tv, q, kRl));
             }
 #pragma unroll
             for (int b = 1; b <= 3; ++b) {
-                const int var = 14 + 3 * (a - 1) + (b - 1);
+                const int var = kSw0 + (b - 1);
                 if (!(vmask & (1u << var))) continue;
-                const bool ok = in && q >= p + a && q + b - 1 <= L;
+                const bool ok = in && q >= p + A && q + b - 1 <= L;
                 if (!__any_sync(0xffffffffu, ok)) continue;
                 const TwRec R1 = tw_cat(F, segv[b - 1], static_cast<float>(dm1));
                 DT dD;
                 float tv;
-                if (q == p + a) {  // adjacent
-                    dD = dm1 + d[0][b - 1] + d[a - 1][b] - Exm1 - Evm1 - Evb[b - 1];
-                    const TwRec R3 = tw_cat(R1, segx[a - 1], static_cast<float>(d[0][b - 1]));
-                    tv = tw_cat(R3, bw[b - 1], static_cast<float>(d[a - 1][b])).w;
+                if (q == p + A) {  // adjacent
+                    dD = dm1 + d0[b - 1] + dAm1[b] - Exm1 - Evm1 - Evb[b - 1];
+                    const TwRec R3 = tw_cat(R1, segxA, static_cast<float>(d0[b - 1]));
+                    tv = tw_cat(R3, bw[b - 1], static_cast<float>(dAm1[b])).w;
                 } else {
-                    dD = dm1 + d[a][b - 1] + dxm + d[a - 1][b] - Exm1 - Exn[a - 1] - Evm1 - Evb[b - 1];
-                    const TwRec R2 = tw_cat(R1, Gm, static_cast<float>(d[a][b - 1]));
-                    const TwRec R3 = tw_cat(R2, segx[a - 1], static_cast<float>(dxm));
-                    tv = tw_cat(R3, bw[b - 1], static_cast<float>(d[a - 1][b])).w;
+                    dD = dm1 + dA[b - 1] + dxm + dAm1[b] - Exm1 - ExA - Evm1 - Evb[b - 1];
+                    const TwRec R2 = tw_cat(R1, Gm, static_cast<float>(dA[b - 1]));
+                    const TwRec R3 = tw_cat(R2, segxA, static_cast<float>(dxm));
+                    tv = tw_cat(R3, bw[b - 1], static_cast<float>(dAm1[b])).w;
                 }
-                best[var] = umin64(best[var], keyof(ok, dD, tv, q, var));
+                bSw[b - 1] = umin64(bSw[b - 1], keyof(ok, dD, tv, q, var));
             }
         }
     }
     // ------------------------------------------------ backward pass: relocate before the segment
-    if (p >= 2) {
+    if (need_rl && p >= 2) {
         const int nch = (p - 1) / 32 + 1;  // element positions up to p-1 (lane q reads Suf(q+1))
-        const TwRec bwx[3] = {S.bwdT[x + 1], S.bwdT[x + 2], S.bwdT[x + 3]};
-        TwRec cS[3];
-        bool hS[3] = {false, false, false};
+        const TwRec bwxA = S.bwdT[x + A];
+        TwRec cS = make_float4(0.f, 0.f, 0.f, 0.f);
+        bool hS = false;
         for (int ci = nch - 1; ci >= 0; --ci) {
             const int qb = ci * 32;
             const int k = qb + lane;                 // element position k in [1, p-1]; lane q uses Suf(q+1)
@@ -1578,53 +1599,58 @@ __device__ __forceinline__ void intra_tw_warp(const SolView<DT> &S, const ScoreP
             const float outl = static_cast<float>(E(vk));  // link (k -> k+1)
             const DT Evq = E(vq);
             const TwRec Fq = S.fwdT[vq];
-            const DT dq0 = D(x, vq), dq1[3] = {D(x, vq + 1), D(x + 1, vq + 1), D(x + 2, vq + 1)};
+            const DT dq0 = D(x, vq), dq1 = D(x + A - 1, vq + 1);
             const TwRec sk = S.node_tw[nk];
-#pragma unroll
-            for (int N = 1; N <= 3; ++N) {
-                const int var = 10 + N;
-                if (!(vmask & (1u << var)) || p + N - 1 > L) continue;
-                // Suf(k) = [k .. x-1] + B(x+N); the element at k = p-1 carries B(x+N) (link = bridge_N)
-                TwRec el = sk;
-                float ol = outl;
-                if (k == p - 1) { el = tw_cat(sk, bwx[N - 1], static_cast<float>(brg[N - 1])); ol = 0.f; }
-                const int e_rel = min(p - 1 - qb, 31);
-                TwRec Sf = scan_bwd(el, ol, lane, e_rel);
-                if (hS[N - 1] && lane <= e_rel) Sf = tw_cat(Sf, cS[N - 1], ol);
-                const TwRec carry_in = cS[N - 1];
-                const bool had = hS[N - 1];
-                cS[N - 1] = shfl_rec(Sf, 0);
-                hS[N - 1] = true;
-                // lane q = qb + lane inserts after position q: needs Suf(q+1)
-                TwRec Sn = shfl_down_rec(Sf, 1);
-                if (lane == 31) Sn = had ? carry_in : Sf;
-                const bool ok = q <= p - 2;
-                if (!__any_sync(0xffffffffu, ok)) continue;
-                const DT rem = brg[N - 1] - Exm1 - Exn[N - 1];
-                const DT dD = rem + dq0 + dq1[N - 1] - Evq;
-                const TwRec A2 = tw_cat(Fq, segx[N - 1], static_cast<float>(dq0));
-                const float tv = tw_cat(A2, Sn, static_cast<float>(dq1[N - 1])).w;
-                best[var] = umin64(best[var], keyof(ok, dD, tv, q, var));
-            }
+            // Suf(k) = [k .. x-1] + B(x+N); the element at k = p-1 carries B(x+N) (link = bridge_N)
+            TwRec el = sk;
+            float ol = outl;
+            if (k == p - 1) { el = tw_cat(sk, bwxA, static_cast<float>(brA)); ol = 0.f; }
+            const int e_rel = min(p - 1 - qb, 31);
+            TwRec Sf = scan_bwd(el, ol, lane, e_rel);
+            if (hS && lane <= e_rel) Sf = tw_cat(Sf, cS, ol);
+            const TwRec carry_in = cS;
+            const bool had = hS;
+            cS = shfl_rec(Sf, 0);
+            hS = true;
+            // lane q = qb + lane inserts after position q: needs Suf(q+1)
+            TwRec Sn = shfl_down_rec(Sf, 1);
+            if (lane == 31) Sn = had ? carry_in : Sf;
+            const bool ok = q <= p - 2;
+            if (!__any_sync(0xffffffffu, ok)) continue;
+            const DT rem = brA - Exm1 - ExA;
+            const DT dD = rem + dq0 + dq1 - Evq;
+            const TwRec A2 = tw_cat(Fq, segxA, static_cast<float>(dq0));
+            const float tv = tw_cat(A2, Sn, static_cast<float>(dq1)).w;
+            bRlB = umin64(bRlB, keyof(ok, dD, tv, q, kRl));
         }
     }
+    auto put = [&](int var, uint64_t b) {
+        const uint64_t m = warp_min64(b);
+        if (lane == 0 && m != kNoKey && m < red[var]) red[var] = m;  // the warp's private row
+    };
+    if (need_rl) put(kRl, umin64(bRl, bRlB));
 #pragma unroll
-    for (int i = 11; i < 23; ++i) {
-        if (!(vmask & (1u << i))) continue;
-        const uint64_t m = warp_min64(best[i]);
-        if (lane == 0 && m != kNoKey && m < red[i]) red[i] = m;  // the warp's private row
-    }
+    for (int b = 0; b < 3; ++b)
+        if (vmask & (1u << (kSw0 + b))) put(kSw0 + b, bSw[b]);
+}
+
+template <class DT, bool DUMP>
+__device__ __forceinline__ void intra_tw_dispatch(const SolView<DT> &S, const ScoreParams &sp, uint32_t vmask, int x,
+                                                  unsigned long long *red, unsigned long long *dump = nullptr) {
+    if (blockIdx.y == 0) intra_tw_warp<DT, 1, DUMP>(S, sp, vmask, x, red, dump);
+    else if (blockIdx.y == 1) intra_tw_warp<DT, 2, DUMP>(S, sp, vmask, x, red, dump);
+    else intra_tw_warp<DT, 3, DUMP>(S, sp, vmask, x, red, dump);
 }
 
 template <class DT, bool DUMP = false>
-__global__ void __launch_bounds__(256) k_intra_tw(const __grid_constant__ SolView<DT> S, ScoreParams sp,
+__global__ void __launch_bounds__(256, 3) k_intra_tw(const __grid_constant__ SolView<DT> S, ScoreParams sp,
                                                   uint32_t vmask, int x_lo, int x_hi, uint64_t *__restrict__ keys,
                                                   unsigned long long *dump) {
     __shared__ unsigned long long red[8][23];   // one private row per warp
     for (int i = threadIdx.x; i < 8 * 23; i += blockDim.x) red[i / 23][i % 23] = kNoKey;
     __syncthreads();
     const int x = x_lo + static_cast<int>(blockIdx.x) * 8 + (threadIdx.x >> 5);
-    if (x < x_hi) intra_tw_warp<DT, DUMP>(S, sp, vmask, x, red[threadIdx.x >> 5], dump);
+    if (x < x_hi) intra_tw_dispatch<DT, DUMP>(S, sp, vmask, x, red[threadIdx.x >> 5], dump);
     __syncthreads();
     if (threadIdx.x < 23) {
         unsigned long long m = red[0][threadIdx.x];
@@ -1633,22 +1659,22 @@ __global__ void __launch_bounds__(256) k_intra_tw(const __grid_constant__ SolVie
     }
 }
 
-// population mode: blockIdx.y = solution
+// population mode: blockIdx.z = solution
 template <class DT>
-__global__ void __launch_bounds__(256) k_intra_tw_batch(const SolView<DT> *__restrict__ views, ScoreParams sp,
+__global__ void __launch_bounds__(256, 3) k_intra_tw_batch(const SolView<DT> *__restrict__ views, ScoreParams sp,
                                                         uint32_t vmask, uint64_t *__restrict__ keys) {
     __shared__ unsigned long long red[8][23];   // one private row per warp
     for (int i = threadIdx.x; i < 8 * 23; i += blockDim.x) red[i / 23][i % 23] = kNoKey;
     __syncthreads();
-    const SolView<DT> &S = views[blockIdx.y];
+    const SolView<DT> &S = views[blockIdx.z];
     const int x = static_cast<int>(blockIdx.x) * 8 + (threadIdx.x >> 5);
-    if (x < S.Qp) intra_tw_warp<DT>(S, sp, vmask, x, red[threadIdx.x >> 5]);
+    if (x < S.Qp) intra_tw_dispatch<DT, false>(S, sp, vmask, x, red[threadIdx.x >> 5]);
     __syncthreads();
     if (threadIdx.x < 23) {
         unsigned long long m = red[0][threadIdx.x];
         for (int w = 1; w < 8; ++w) m = m < red[w][threadIdx.x] ? m : red[w][threadIdx.x];
         if (m != kNoKey)
-            atomicMin(reinterpret_cast<unsigned long long *>(keys) + static_cast<size_t>(blockIdx.y) * kNV + threadIdx.x, m);
+            atomicMin(reinterpret_cast<unsigned long long *>(keys) + static_cast<size_t>(blockIdx.z) * kNV + threadIdx.x, m);
     }
 }
 
@@ -1823,7 +1849,7 @@ cudaError_t launch_intra(uint32_t mask, bool tw, const SolView<DT> &S, const Sco
         }
     }
     if (tw && !(intra & 1u) && warp_tw) {  // warp-parallel VRPTW kernel (long routes)
-        const int blocks = (x_hi - x_lo + 7) / 8;
+        const dim3 blocks((x_hi - x_lo + 7) / 8, 3);   // y: the segment length A at u
         k_intra_tw<DT, false><<<blocks, 256, 0, st>>>(S, sp, intra, x_lo, x_hi, keys, nullptr);
         ++g_launches;
         return cudaGetLastError();
@@ -1872,7 +1898,7 @@ cudaError_t launch_eval_dump(uint32_t mask, bool tw, const SolView<DT> &S, const
         }
     }
     if (tw && !(intra & 1u) && warp_tw) {
-        k_intra_tw<DT, true><<<(x_hi - x_lo + 7) / 8, 256, 0, st>>>(S, sp, intra, x_lo, x_hi, keys, dump);
+        k_intra_tw<DT, true><<<dim3((x_hi - x_lo + 7) / 8, 3), 256, 0, st>>>(S, sp, intra, x_lo, x_hi, keys, dump);
         ++g_launches;
         return cudaGetLastError();
     }
@@ -1928,7 +1954,7 @@ cudaError_t launch_batch(uint32_t mask, bool tw, const SolView<DT> *views, const
     if (e == cudaSuccess && intra && n_sol > 0) {
         dim3 g(((max_qp + 31) / 32 * 32 * __builtin_popcount(intra) + 255) / 256, n_sol);
         if (tw && !(intra & 1u) && warp_tw)
-            k_intra_tw_batch<DT><<<dim3((max_qp + 7) / 8, n_sol), 256, 0, st>>>(views, sp, intra, keys);
+            k_intra_tw_batch<DT><<<dim3((max_qp + 7) / 8, 3, n_sol), 256, 0, st>>>(views, sp, intra, keys);
         else if (tw) k_intra_batch<DT, true><<<g, 256, 0, st>>>(views, sp, intra, keys);
         else    k_intra_batch<DT, false><<<g, 256, 0, st>>>(views, sp, intra, keys);
         ++g_launches;

@@ -342,7 +342,9 @@ int32_t tga_batch_device_stats(tga_batch *batch, uint64_t *counts, uint64_t *app
 
 /* Diagnostics: phase probe of the device-resident step.  enable != 0 makes the
  * next pick/update launches record the SM cycle counter (clock64 of block 0)
- * at 8 phase points; out[16] (may be NULL) receives the last record
+ * at 8 phase points; out[16 + 1024] (may be NULL) receives the last record
+ * and, from out[16], the globaltimer (ns) at the start / end of each block b < 512
+ * of the last single-solution pick/update launch at out[16 + 2b], out[17 + 2b]
  * (synchronises).  Not used on any timed path. */
 int32_t tga_solution_debug_probe(tga_solution *sol, int32_t enable, uint64_t *out);
 

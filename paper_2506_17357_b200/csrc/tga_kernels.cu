@@ -12,6 +12,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdlib>
 
 #include "tga_device.cuh"
 #include "tga_launch.h"
@@ -90,7 +91,8 @@ __device__ __forceinline__ void scan_spare(const ScanArgs<DT> &A, const int k0, 
 
 template <class DT, bool TW, class NodeF>
 __device__ __forceinline__ int scan_fwd_pass(const ScanArgs<DT> &A, const int r, const int lane, const int base,
-                                             const int L, NodeF nodeAt) {
+                                             const int L, NodeF nodeAt, int32_t *sfL = nullptr, DT *sen = nullptr,
+                                             TwRec *sfT = nullptr) {
     const int len = L + 2;
     const int n = A.n_nodes;
     // ---------------- forward pass: prefix loads, prefix distance, prefix TW records
@@ -160,6 +162,11 @@ __device__ __forceinline__ int scan_fwd_pass(const ScanArgs<DT> &A, const int r,
             A.fwdD[x] = fD;
             A.enext[x] = e;
             if (TW) A.fwdT[x] = fT;
+            if (sfL) {   // the block rebuild's shared mirror (position k of the route)
+                sfL[k] = fL;
+                sen[k] = e;
+                if (TW) sfT[k] = fT;
+            }
         }
         const int last = min(31, len - 1 - c0);
         carryL = __shfl_sync(0xffffffffu, fL, last);
@@ -185,7 +192,8 @@ __device__ __forceinline__ int scan_fwd_pass(const ScanArgs<DT> &A, const int r,
 
 template <class DT, bool TW, class NodeF>
 __device__ __forceinline__ void scan_bwd_pass(const ScanArgs<DT> &A, const int r, const int lane, const int base,
-                                              const int L, NodeF nodeAt, const bool e_from_C) {
+                                              const int L, NodeF nodeAt, const bool e_from_C,
+                                              int32_t *sbL = nullptr, TwRec *sbT = nullptr) {
     const int len = L + 2;
     const int n = A.n_nodes;
     // ---------------- backward pass: suffix loads, suffix distance, suffix TW records
@@ -252,6 +260,10 @@ __device__ __forceinline__ void scan_bwd_pass(const ScanArgs<DT> &A, const int r
             A.bwdL[x] = bL;
             A.bwdD[x] = bD;
             if (TW) A.bwdT[x] = bT;
+            if (sbL) {
+                sbL[k] = bL;
+                if (TW) sbT[k] = bT;
+            }
         }
         bcarryL = __shfl_sync(0xffffffffu, bL, 0);
         bcarryD = __shfl_sync(0xffffffffu, bD, 0);
@@ -265,33 +277,76 @@ __device__ __forceinline__ void scan_bwd_pass(const ScanArgs<DT> &A, const int r
     if (lane == 0) A.rD[r] = bcarryD;
 }
 
-template <class DT, bool TW, class NodeF, class CanonF>
+// bridge_N[x] = c(x-1, x+N): the edge that closes the gap left by removing the segment
+// x..x+N-1 (relocate / or-opt removal, Eq. 2); k = position of slot x in its route
+template <class DT, class NodeF>
+__device__ __forceinline__ void scan_bridges(const ScanArgs<DT> &A, const int k, const int x, const int len,
+                                             NodeF nodeAt, DT &b1, DT &b2, DT &b3) {
+    const int n = A.n_nodes;
+    const int np = (k >= 1) ? nodeAt(x - 1) : 0;
+    b1 = b2 = b3 = DT(0);
+    if (k >= 1 && k + 1 <= len - 1) b1 = A.C[static_cast<size_t>(np) * n + nodeAt(x + 1)];
+    if (k >= 1 && k + 2 <= len - 1) b2 = A.C[static_cast<size_t>(np) * n + nodeAt(x + 2)];
+    if (k >= 1 && k + 3 <= len - 1) b3 = A.C[static_cast<size_t>(np) * n + nodeAt(x + 3)];
+}
+// Where the record pass reads the passes' results: the global arrays (a warp's rebuild),
+// or the shared mirror a block rebuild keeps of one route (position k = x - base)
+template <class DT>
+struct ScanSrcGlobal {
+    const ScanArgs<DT> &A;
+    __device__ __forceinline__ int32_t fL(int x, int) const { return A.fwdL[x]; }
+    __device__ __forceinline__ int32_t bL(int x, int) const { return A.bwdL[x]; }
+    __device__ __forceinline__ DT en(int x, int) const { return A.enext[x]; }
+    __device__ __forceinline__ TwRec fT(int x, int) const { return A.fwdT[x]; }
+    __device__ __forceinline__ TwRec bT(int x, int) const { return A.bwdT[x]; }
+    __device__ __forceinline__ TwRec nt(int node, int) const { return A.node_tw[node]; }
+    template <class NodeF>
+    __device__ __forceinline__ void br(int k, int x, int len, NodeF nodeAt, DT &b1, DT &b2, DT &b3) const {
+        scan_bridges<DT>(A, k, x, len, nodeAt, b1, b2, b3);
+    }
+};
+#ifndef TGA_SCAN_SHARED
+#define TGA_SCAN_SHARED 1
+#endif
+constexpr int kScanShared = 256;   // route positions a block rebuild mirrors in shared memory
+template <class DT, bool TW>
+struct ScanSrcShared {
+    const int32_t *sfL, *sbL;
+    const DT *sen, *sbr;           // sbr[3][kScanShared]
+    const TwRec *sfT, *sbT, *snt;  // snt: node_tw of the route's positions
+    __device__ __forceinline__ int32_t fL(int, int k) const { return sfL[k]; }
+    __device__ __forceinline__ int32_t bL(int, int k) const { return sbL[k]; }
+    __device__ __forceinline__ DT en(int, int k) const { return sen[k]; }
+    __device__ __forceinline__ TwRec fT(int, int k) const { return sfT[k]; }
+    __device__ __forceinline__ TwRec bT(int, int k) const { return sbT[k]; }
+    __device__ __forceinline__ TwRec nt(int, int k) const { return snt[k]; }
+    template <class NodeF>
+    __device__ __forceinline__ void br(int k, int, int, NodeF, DT &b1, DT &b2, DT &b3) const {
+        b1 = sbr[k]; b2 = sbr[kScanShared + k]; b3 = sbr[2 * kScanShared + k];
+    }
+};
+
+template <class DT, bool TW, class NodeF, class CanonF, class Src>
 __device__ __forceinline__ void scan_rec_pass(const ScanArgs<DT> &A, const int r, const int k0, const int kstep,
                                               const int base, const int L, const int Wr, NodeF nodeAt,
-                                              CanonF canonAt) {
+                                              CanonF canonAt, const Src &src) {
     const int len = L + 2;
-    const int n = A.n_nodes;
     // ---------------- per-position segment records and bridges (N = 1..3)
     for (int k = k0; k < len; k += kstep) {
         const int x = base + k;
-        // bridge_N[x] = c(x-1, x+N): the edge that closes the gap left by removing
-        // the segment x..x+N-1 (relocate / or-opt removal, Eq. 2)
-        const int np = (k >= 1) ? nodeAt(x - 1) : 0;
-        DT b1 = DT(0), b2 = DT(0), b3 = DT(0);
-        if (k >= 1 && k + 1 <= len - 1) b1 = A.C[static_cast<size_t>(np) * n + nodeAt(x + 1)];
-        if (k >= 1 && k + 2 <= len - 1) b2 = A.C[static_cast<size_t>(np) * n + nodeAt(x + 2)];
-        if (k >= 1 && k + 3 <= len - 1) b3 = A.C[static_cast<size_t>(np) * n + nodeAt(x + 3)];
+        DT b1, b2, b3;
+        src.br(k, x, len, nodeAt, b1, b2, b3);
         A.bridge1[x] = b1;
         A.bridge2[x] = b2;
         A.bridge3[x] = b3;
         TwRec seg2v = make_float4(0.f, 0.f, 0.f, 0.f), seg3v = seg2v;   // kept for the SlotTW below
         if (TW) {
-            const TwRec s1 = A.node_tw[nodeAt(x)];
+            const TwRec s1 = src.nt(nodeAt(x), k);
             TwRec s2 = s1, s3 = s1;
             if (k + 1 < len) {
-                s2 = tw_cat(s1, A.node_tw[nodeAt(x + 1)], static_cast<float>(A.enext[x]));
+                s2 = tw_cat(s1, src.nt(nodeAt(x + 1), k + 1), static_cast<float>(src.en(x, k)));
                 s3 = s2;
-                if (k + 2 < len) s3 = tw_cat(s2, A.node_tw[nodeAt(x + 2)], static_cast<float>(A.enext[x + 1]));
+                if (k + 2 < len) s3 = tw_cat(s2, src.nt(nodeAt(x + 2), k + 2), static_cast<float>(src.en(x + 1, k + 1)));
             }
             A.seg2T[x] = s2;
             A.seg3T[x] = s3;
@@ -302,22 +357,22 @@ __device__ __forceinline__ void scan_rec_pass(const ScanArgs<DT> &A, const int r
             if (A.rec) {
                 SlotRec q;
                 const bool slot = k <= L;  // canonical slot (not the end depot)
-                const int32_t e_x = A.enext[x], e_prev = (k >= 1) ? A.enext[x - 1] : 0;
-                const int32_t fl_prev = (k >= 1) ? A.fwdL[x - 1] : 0;
+                const int32_t e_x = src.en(x, k), e_prev = (k >= 1) ? src.en(x - 1, k - 1) : 0;
+                const int32_t fl_prev = (k >= 1) ? src.fL(x - 1, k - 1) : 0;
                 q.r = (slot && canonAt(x) >= 0) ? r : -1;
-                q.fL = slot ? A.fwdL[x] : kPoison;
-                q.bL1 = (slot && k + 1 < len) ? A.bwdL[x + 1] : kPoison;
+                q.fL = slot ? src.fL(x, k) : kPoison;
+                q.bL1 = (slot && k + 1 < len) ? src.bL(x + 1, k + 1) : kPoison;
                 q.ne = -e_x;
                 q.W = slot ? Wr : kPoison;
                 const DT br[3] = {b1, b2, b3};
                 // time-window part (TW-I): earliest completions / latest starts
                 SlotTW w{};
-                auto EFof = [&](int y) { const TwRec f = A.fwdT[y]; return f.w == 0.f ? f.y + f.x : kTwBig; };
-                auto LBof = [&](int y) { const TwRec b = A.bwdT[y]; return b.w == 0.f ? b.z : -kTwBig; };
+                auto EFof = [&](int y) { const TwRec f = src.fT(y, y - base); return f.w == 0.f ? f.y + f.x : kTwBig; };
+                auto LBof = [&](int y) { const TwRec b = src.bT(y, y - base); return b.w == 0.f ? b.z : -kTwBig; };
                 if (TW && A.rectw) {
                     w.EF = EFof(x);
                     w.EFm = (k >= 1) ? EFof(x - 1) : kTwBig;
-                    const TwRec s1 = A.node_tw[nodeAt(x)];
+                    const TwRec s1 = src.nt(nodeAt(x), k);
                     const TwRec sg[3] = {s1, seg2v, seg3v};
 #pragma unroll
                     for (int N = 1; N <= 3; ++N) {
@@ -336,8 +391,8 @@ __device__ __forceinline__ void scan_rec_pass(const ScanArgs<DT> &A, const int r
 #pragma unroll
                 for (int N = 1; N <= 3; ++N) {
                     const bool segok = (k >= 1) && (k + N - 1 <= L);
-                    const int32_t sN = segok ? A.fwdL[x + N - 1] - fl_prev : 0;
-                    const int32_t eout = segok ? A.enext[x + N - 1] : 0;
+                    const int32_t sN = segok ? src.fL(x + N - 1, k + N - 1) - fl_prev : 0;
+                    const int32_t eout = segok ? src.en(x + N - 1, k + N - 1) : 0;
                     // route a after removing the segment: F(x-1) + B(x+N) must stay feasible
                     // (feasible-only records; penalised records price the excess instead)
                     bool rem_ok = segok && (A.pen_wQ || Wr - sN <= A.capacity);
@@ -369,7 +424,7 @@ __device__ __forceinline__ void scan_route_g(const ScanArgs<DT> &A, const int r,
     const int Wr = scan_fwd_pass<DT, TW>(A, r, lane, base, L, nodeAt);
     scan_bwd_pass<DT, TW>(A, r, lane, base, L, nodeAt, false);
     __syncwarp();   // fwdL / bwdL / enext of this route are visible to the whole warp
-    scan_rec_pass<DT, TW>(A, r, lane, 32, base, L, Wr, nodeAt, canonAt);
+    scan_rec_pass<DT, TW>(A, r, lane, 32, base, L, Wr, nodeAt, canonAt, ScanSrcGlobal<DT>{A});
 }
 
 // The same rebuild by a whole block (every thread must call it): forward and
@@ -386,12 +441,36 @@ __device__ __forceinline__ void scan_route_block(const ScanArgs<DT> &A, const in
                                                  unsigned long long *stamp = nullptr) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (stamp && tid == 0) stamp[0] = scan_gtime();   // diagnostics: start / passes done / records done
+    // routes of up to kScanShared positions: the passes mirror their results in shared memory
+    // and the other warps gather the bridges (and node windows) meanwhile, so the record
+    // pass reads no global memory (one round trip less on the update's critical path)
+    __shared__ int32_t s_fL[kScanShared], s_bL[kScanShared], s_W;
+    __shared__ DT s_en[kScanShared], s_br[3 * kScanShared];
+    __shared__ TwRec s_fT[TW ? kScanShared : 1], s_bT[TW ? kScanShared : 1], s_nt[TW ? kScanShared : 1];
+    const int len = L + 2;
+    const bool sh = TGA_SCAN_SHARED && len <= kScanShared && blockDim.x > 64;
     scan_spare<DT, TW>(A, tid, blockDim.x, base, L, cap);
-    if (warp == 0) scan_fwd_pass<DT, TW>(A, r, lane, base, L, nodeAt);
-    else if (warp == 1) scan_bwd_pass<DT, TW>(A, r, lane, base, L, nodeAt, true);
+    if (warp == 0) {
+        const int W = scan_fwd_pass<DT, TW>(A, r, lane, base, L, nodeAt, sh ? s_fL : nullptr, sh ? s_en : nullptr,
+                                            sh ? s_fT : nullptr);
+        if (lane == 0) s_W = W;
+    } else if (warp == 1) {
+        scan_bwd_pass<DT, TW>(A, r, lane, base, L, nodeAt, true, sh ? s_bL : nullptr, sh ? s_bT : nullptr);
+    } else if (sh) {
+        for (int k = tid - 64; k < len; k += blockDim.x - 64) {
+            DT b1, b2, b3;
+            scan_bridges<DT>(A, k, base + k, len, nodeAt, b1, b2, b3);
+            s_br[k] = b1; s_br[kScanShared + k] = b2; s_br[2 * kScanShared + k] = b3;
+            if (TW) s_nt[k] = A.node_tw[nodeAt(base + k)];
+        }
+    }
     __syncthreads();   // prefix / suffix records and rW[r] of this route are visible to the block
     if (stamp && tid == 0) stamp[1] = scan_gtime();
-    scan_rec_pass<DT, TW>(A, r, tid, blockDim.x, base, L, A.rW[r], nodeAt, canonAt);
+    if (sh)
+        scan_rec_pass<DT, TW>(A, r, tid, blockDim.x, base, L, s_W, nodeAt, canonAt,
+                              ScanSrcShared<DT, TW>{s_fL, s_bL, s_en, s_br, s_fT, s_bT, s_nt});
+    else
+        scan_rec_pass<DT, TW>(A, r, tid, blockDim.x, base, L, A.rW[r], nodeAt, canonAt, ScanSrcGlobal<DT>{A});
     if (stamp) {
         __syncthreads();
         if (tid == 0) stamp[2] = scan_gtime();
@@ -587,6 +666,7 @@ __device__ __forceinline__ void pick_update_multi(const DevState &S, const ScanA
     int32_t *sb = smr, *sl = smr + (R + 1);
     int32_t *snap = smr + 2 * (R + 1);  // old node ids of the changed ranges
     int32_t *nn = snap + snap_cap;      // new node ids of the changed ranges
+    const bool direct = S.Qp <= kDirectColsQp;
     __shared__ uint64_t skeys[kNV];
     __shared__ Decoded dm;
     // ---- 1. stage the old route bases / lengths and the keys; decode (every block)
@@ -623,9 +703,21 @@ __device__ __forceinline__ void pick_update_multi(const DevState &S, const ScanA
     __syncthreads();
     if (tid == 0) atomicAdd(S.desc + 9, 1);
     pdl_trigger();  // this block is resident and arrived: a dependent grid cannot starve the wait below
-    // the closed-form counts of the evaluated (old) lengths, on a block that does not
-    // rebuild a route (those are the last blocks when the update roles are split)
-    if (b == G / 2) neighbourhood_counts(S, cmask, sl);
+    // ---- 3. roles of the update work.  Direct columns (small Qp): every block does ONE kind of
+    // unit, so its chain is two rounds of loads: the re-scans on the last blocks, the changed Dp
+    // rows on the first ones, the closed-form counts on the block before the re-scans, the
+    // columns of every other row on the blocks between.
+    // Symmetric columns (large Qp): rows and re-scans on every block, then a barrier.
+    const int nrows = n1 + n2;
+    // block 0 keeps only the final slot-array writes (it is the one that waits for
+    // every arrival): rows on blocks 1 .. nrows, columns after them, counts, re-scans last
+    const bool split_roles = dm.applied && !dm.full && direct && G >= nrows + dm.nrt + 4;
+    const int scan0 = split_roles ? G - dm.nrt : 1;                  // first scanning block
+    const int row0 = split_roles ? 1 : 0, row_blocks = split_roles ? nrows : G;
+    const int col0 = split_roles ? nrows + 1 : 0, col_blocks = split_roles ? G - dm.nrt - nrows - 2 : G;
+    // the closed-form counts of the evaluated (old) lengths, on a block of their own when
+    // the roles are split (else on a block that does not rebuild a route)
+    if (b == (split_roles ? scan0 - 1 : G / 2)) neighbourhood_counts(S, cmask, sl);
     if (!dm.applied) {
         if (b == 0 && tid == 0) {
             S.desc[0] = 0;
@@ -654,18 +746,6 @@ __device__ __forceinline__ void pick_update_multi(const DevState &S, const ScanA
     const DT *__restrict__ C = A.C;
     const int n = A.n_nodes, pitch = S.pitch, Qp = S.Qp;
     DT *__restrict__ Dp = static_cast<DT *>(S.Dp);
-    // ---- 4. the update work.  Direct columns (small Qp): every block does ONE kind of unit,
-    // so its chain is two rounds of loads: the re-scans on the last blocks, the changed Dp
-    // rows on the first ones, the columns of every other row on the blocks between.
-    // Symmetric columns (large Qp): rows and re-scans on every block, then a barrier.
-    const bool direct = Qp <= kDirectColsQp;
-    const int nrows = n1 + n2;
-    // block 0 keeps only the final slot-array writes (it is the one that waits for
-    // every arrival): rows on blocks 1 .. nrows, columns after them, re-scans last
-    const bool split_roles = direct && G >= nrows + dm.nrt + 3;
-    const int scan0 = split_roles ? G - dm.nrt : 1;                  // first scanning block
-    const int row0 = split_roles ? 1 : 0, row_blocks = split_roles ? nrows : G;
-    const int col0 = split_roles ? nrows + 1 : 0, col_blocks = split_roles ? G - dm.nrt - nrows - 1 : G;
     // 4a. re-scan of the changed routes (one block each; the longest chains)
     for (int q = 0; q < dm.nrt; ++q) {
         if (b == (scan0 + q) % G) {   // block-uniform: the whole block rebuilds the route
@@ -771,17 +851,13 @@ __device__ __forceinline__ void pick_update_multi(const DevState &S, const ScanA
 }
 
 template <class DT, bool TW>
-__global__ void __launch_bounds__(256) k_pick_update(const DevState *__restrict__ states,
-                                                     const ScanArgs<DT> *__restrict__ scans, uint32_t mask,
-                                                     uint32_t cmask, int integer, int snap_cap) {
-    extern __shared__ int32_t smr[];
-    pdl_wait();  // the keys (and, two launches back, the slot arrays) come from stream predecessors
-    const DevState &S = states[blockIdx.y];
+__device__ __forceinline__ void pick_update_entry(const DevState &S, const ScanArgs<DT> &A, uint32_t mask,
+                                                  uint32_t cmask, int integer, int snap_cap, int32_t *smr) {
     unsigned long long *pr = (blockIdx.x == 0 && threadIdx.x == 0 && S.acc[31]) ? S.acc + 32 : nullptr;
     probe(pr, 0);
     if (gridDim.x == 1) pdl_trigger();
     if (snap_cap > 0 && gridDim.x > 1) {
-        pick_update_multi<DT, TW>(S, scans[blockIdx.y], mask, cmask, integer, smr, snap_cap, pr);
+        pick_update_multi<DT, TW>(S, A, mask, cmask, integer, smr, snap_cap, pr);
         return;
     }
     // one block per solution (population batches), or the shared memory cannot
@@ -794,7 +870,7 @@ __global__ void __launch_bounds__(256) k_pick_update(const DevState *__restrict_
     const volatile int32_t *desc = S.desc;
     if (desc[0] == 0) return;
     const UpdateSpec u{desc[1], desc[2], desc[3], desc[4], desc[5], desc[6], desc[7]};
-    update_rows<DT, TW>(scans[blockIdx.y], static_cast<DT *>(S.Dp), S.pitch, S.R, u, blockIdx.x, gridDim.x);
+    update_rows<DT, TW>(A, static_cast<DT *>(S.Dp), S.pitch, S.R, u, blockIdx.x, gridDim.x);
     probe(pr, 5);
     if (u.full) return;
     if (gridDim.x > 1) solution_barrier(S.desc + 8, gridDim.x);  // rows before the columns read them
@@ -805,10 +881,37 @@ __global__ void __launch_bounds__(256) k_pick_update(const DevState *__restrict_
     probe(pr, 7);
 }
 
-constexpr int kPickSmemMax = 200 * 1024;
+// population batches: blockIdx.y = solution, per-solution state read from device arrays
+template <class DT, bool TW>
+__global__ void __launch_bounds__(256) k_pick_update(const DevState *__restrict__ states,
+                                                     const ScanArgs<DT> *__restrict__ scans, uint32_t mask,
+                                                     uint32_t cmask, int integer, int snap_cap) {
+    extern __shared__ int32_t smr[];
+    pdl_wait();  // the keys (and, two launches back, the slot arrays) come from stream predecessors
+    pick_update_entry<DT, TW>(states[blockIdx.y], scans[blockIdx.y], mask, cmask, integer, snap_cap, smr);
+}
+// one solution: its state passed by value in the parameter space, so every pointer and
+// size of the chain (route bases, keys, node ids, C, the record arrays) is a constant-bank
+// read instead of a dependent global load in front of the first data load
+template <class DT, bool TW>
+__global__ void __launch_bounds__(256) k_pick_update1(const __grid_constant__ DevState S,
+                                                      const __grid_constant__ ScanArgs<DT> A, uint32_t mask,
+                                                      uint32_t cmask, int integer, int snap_cap) {
+    extern __shared__ int32_t smr[];
+    pdl_wait();
+    const bool tl = S.acc[31] != 0 && blockIdx.x < kTimelineBlocks;   // diagnostics: per-block timeline
+    if (tl && threadIdx.x == 0) S.acc[kTimeline + 2 * blockIdx.x] = gtimer();
+    pick_update_entry<DT, TW>(S, A, mask, cmask, integer, snap_cap, smr);
+    if (tl) {
+        __syncthreads();
+        if (threadIdx.x == 0) S.acc[kTimeline + 2 * blockIdx.x + 1] = gtimer();
+    }
+}
+
+constexpr int kPickSmemMax = 180 * 1024;   // + the static shared memory (<= 227 KB per block)
 cudaError_t launch_pick_update(const DevState *states, const void *scans, int n_sol, bool tw, bool is_int,
                                uint32_t mask, uint32_t cmask, int max_routes, int max_cap, int blocks_per_sol,
-                               cudaStream_t st) {
+                               cudaStream_t st, const DevState *h_state, const void *h_scan) {
     // old path: sb, sl, nb (3 x (R+1) ints) + the shared snapshot of the two changed routes;
     // multi-block path: sb, sl + old and new node ids of the two changed routes
     const int smem_old = 3 * (max_routes + 1) * 4 + 2 * max_cap * 4;
@@ -826,16 +929,33 @@ cudaError_t launch_pick_update(const DevState *states, const void *scans, int n_
             cudaFuncSetAttribute(k_pick_update<int32_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPickSmemMax);
             cudaFuncSetAttribute(k_pick_update<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPickSmemMax);
             cudaFuncSetAttribute(k_pick_update<float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPickSmemMax);
+            cudaFuncSetAttribute(k_pick_update1<int32_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPickSmemMax);
+            cudaFuncSetAttribute(k_pick_update1<int32_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPickSmemMax);
+            cudaFuncSetAttribute(k_pick_update1<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPickSmemMax);
+            cudaFuncSetAttribute(k_pick_update1<float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPickSmemMax);
         });
     }
     cudaError_t e;
-    const auto *si = static_cast<const ScanArgs<int32_t> *>(scans);
-    const auto *sf = static_cast<const ScanArgs<float> *>(scans);
     const int coop = blocks_per_sol > 1 ? 1 : 0;   // its blocks wait for each other
-    if (is_int) e = tw ? launch_pdl(2, k_pick_update<int32_t, true>, g, dim3(256), smem, st, coop, states, si, mask, cmask, 1, snap_cap)
-                       : launch_pdl(2, k_pick_update<int32_t, false>, g, dim3(256), smem, st, coop, states, si, mask, cmask, 1, snap_cap);
-    else e = tw ? launch_pdl(2, k_pick_update<float, true>, g, dim3(256), smem, st, coop, states, sf, mask, cmask, 0, snap_cap)
-                : launch_pdl(2, k_pick_update<float, false>, g, dim3(256), smem, st, coop, states, sf, mask, cmask, 0, snap_cap);
+    if (n_sol == 1 && h_state && h_scan) {   // by value: no dependent loads of the state itself
+        const DevState &S = *h_state;
+        if (is_int) {
+            const auto &A = *static_cast<const ScanArgs<int32_t> *>(h_scan);
+            e = tw ? launch_pdl(2, k_pick_update1<int32_t, true>, g, dim3(256), smem, st, coop, S, A, mask, cmask, 1, snap_cap)
+                   : launch_pdl(2, k_pick_update1<int32_t, false>, g, dim3(256), smem, st, coop, S, A, mask, cmask, 1, snap_cap);
+        } else {
+            const auto &A = *static_cast<const ScanArgs<float> *>(h_scan);
+            e = tw ? launch_pdl(2, k_pick_update1<float, true>, g, dim3(256), smem, st, coop, S, A, mask, cmask, 0, snap_cap)
+                   : launch_pdl(2, k_pick_update1<float, false>, g, dim3(256), smem, st, coop, S, A, mask, cmask, 0, snap_cap);
+        }
+    } else {
+        const auto *si = static_cast<const ScanArgs<int32_t> *>(scans);
+        const auto *sf = static_cast<const ScanArgs<float> *>(scans);
+        if (is_int) e = tw ? launch_pdl(2, k_pick_update<int32_t, true>, g, dim3(256), smem, st, coop, states, si, mask, cmask, 1, snap_cap)
+                           : launch_pdl(2, k_pick_update<int32_t, false>, g, dim3(256), smem, st, coop, states, si, mask, cmask, 1, snap_cap);
+        else e = tw ? launch_pdl(2, k_pick_update<float, true>, g, dim3(256), smem, st, coop, states, sf, mask, cmask, 0, snap_cap)
+                    : launch_pdl(2, k_pick_update<float, false>, g, dim3(256), smem, st, coop, states, sf, mask, cmask, 0, snap_cap);
+    }
     note_launch();
     return e != cudaSuccess ? e : cudaGetLastError();
 }

@@ -87,6 +87,9 @@ struct UpdateSpec {
 };
 
 // per-solution device state of the device-resident step (k_pick_apply / k_update_dev)
+// diagnostics: DevState::acc[kTimeline + 2b], [.. + 1] = globaltimer at the start / end of block b
+// of the single-solution pick/update launch (armed by tga_solution_debug_probe)
+constexpr int kTimeline = 64, kTimelineBlocks = 512, kAccWords = kTimeline + 2 * kTimelineBlocks;
 struct DevState {
     int32_t *node, *route, *pos, *rlen, *canon;   // slot arrays (guarded)
     int32_t *rbase, *rlenR, *cbase;              // per route
@@ -101,7 +104,7 @@ struct DevState {
 // mask: the evaluated variants (pick); cmask: the variants whose closed-form counts are added
 cudaError_t launch_pick_update(const DevState *states, const void *scans, int n_sol, bool tw, bool is_int,
                                uint32_t mask, uint32_t cmask, int max_routes, int max_cap, int blocks_per_sol,
-                               cudaStream_t st);
+                               cudaStream_t st, const DevState *h_state = nullptr, const void *h_scan = nullptr);
 
 template <class DT>
 cudaError_t launch_dp(DT *Dp, int pitch, const int32_t *node, const DT *C, int n, int Qp, int lo, int hi,

@@ -775,7 +775,7 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
         {&v_fT, cap * 16}, {&v_bT, cap * 16}, {&v_s2, cap * 16}, {&v_s3, cap * 16},
         {&v_rbase, Rr * 4}, {&v_rlenR, Rr * 4}, {&v_cbase, Rr * 4}, {&v_rW, Rr * 4}, {&v_rTV, Rr * 4},
         {&v_rD, Rr * 4}, {&v_ds, sizeof(DevState)}, {&v_sa, sizeof(ScanArgs<int32_t>)}, {&v_desc, 16 * 4},
-        {&v_scr, cap * 4}, {&v_acc, 48 * 8},
+        {&v_scr, cap * 4}, {&v_acc, kAccWords * 8},
         {&v_keys, TGA_N_VARIANTS * 8}, {&v_tiles, tiles_max * 4},
         {&v_rec, want_fast ? cap * sizeof(SlotRec) : 0}, {&v_ftiles, want_fast ? ftiles_max * 4 : 0},
         {&v_rectw, want_fast && I->tw ? cap * sizeof(SlotTW) : 0},
@@ -908,7 +908,7 @@ extern "C" int32_t tga_solution_load(tga_instance *I, int32_t R, const int32_t *
     {   // device-resident step state
         DevState ds = make_devstate(s, s->keys);
         if (cudaMemcpyAsync(s->d_ds, &ds, sizeof(ds), cudaMemcpyHostToDevice, s->stream) != cudaSuccess ||
-            cudaMemsetAsync(s->d_acc, 0, 48 * 8, s->stream) != cudaSuccess ||
+            cudaMemsetAsync(s->d_acc, 0, kAccWords * 8, s->stream) != cudaSuccess ||
 
             cudaMemsetAsync(s->d_desc, 0, 16 * 4, s->stream) != cudaSuccess)
             return bail(fail(TGA_ERR_CUDA, "device step state"));
@@ -1642,9 +1642,14 @@ extern "C" int32_t tga_step_async(tga_solution *s, uint32_t mask) {
     // pick + splice + update in one launch: one block per SM at most (grid barrier)
     // ETGA counts its (masked) inter-route candidates in the eval kernel; the closed forms cover the rest
     const uint32_t cmask = I->theta > 0 ? (s->eval_mask & TGA_OP_INTRA) : s->eval_mask;
+    // the state by value (kernel parameters): the chain's first loads are data, not the state
+    const DevState hs = make_devstate(s, s->keys);
+    const auto hsi = I->dtype == TGA_I32 ? scan_args<int32_t>(s) : ScanArgs<int32_t>{};
+    const auto hsf = I->dtype == TGA_I32 ? ScanArgs<float>{} : scan_args<float>(s);
+    const void *hsa = I->dtype == TGA_I32 ? static_cast<const void *>(&hsi) : static_cast<const void *>(&hsf);
     cudaError_t e = launch_pick_update(s->d_ds, s->d_sa, 1, I->tw, I->dtype == TGA_I32, s->eval_mask, cmask, s->R,
                                        s->N + 2 + s->slack,  // upper bound of any route's slot capacity
-                                       s->sm_count, s->stream);
+                                       s->sm_count, s->stream, &hs, hsa);
     if (e != cudaSuccess) return fail(TGA_ERR_CUDA, std::string("device step: ") + cudaGetErrorString(e));
     s->keys_clean = true;
     s->clean_cap = capture_id(s->stream);
@@ -1711,6 +1716,7 @@ extern "C" int32_t tga_solution_debug_probe(tga_solution *s, int32_t enable, uin
     if (set_device(s->inst) != TGA_OK) return TGA_ERR_CUDA;
     if (out) {
         TGA_CUDA(cudaMemcpyAsync(out, s->d_acc + 32, 16 * 8, cudaMemcpyDeviceToHost, s->stream));
+        TGA_CUDA(cudaMemcpyAsync(out + 16, s->d_acc + kTimeline, 2 * kTimelineBlocks * 8, cudaMemcpyDeviceToHost, s->stream));
         TGA_CUDA(cudaStreamSynchronize(s->stream));
     }
     const unsigned long long flag = enable ? 1ull : 0ull;

@@ -15,7 +15,8 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtga.so")
+# TGA_LIB: diagnostics only (A/B timing of two builds of the same sources in one GPU session)
+LIB_PATH = os.environ.get("TGA_LIB") or os.path.join(_HERE, "libtga.so")
 
 # ---------------------------------------------------------------- constants (include/tga.h)
 OK, NO_IMPROVING_MOVE = 0, 1
@@ -322,8 +323,9 @@ class Solution:
         return out
 
     def debug_probe(self, enable: bool = True):
-        """Diagnostics: clock64 phase stamps of the last device step (16 u64), then (re)arm."""
-        out = np.zeros(16, dtype=np.uint64)
+        """Diagnostics: clock64 phase stamps of the last device step (16 u64) followed by the
+        per-block (start, end) globaltimer pairs of its pick/update launch (512 x 2), then (re)arm."""
+        out = np.zeros(16 + 1024, dtype=np.uint64)
         _check(lib().tga_solution_debug_probe(self._h, int(enable), _p(out)))
         return out
 

@@ -24,6 +24,7 @@ for r in reps:
     r.descent(mask, 3)
 torch.cuda.synchronize()
 rows = []
+tls = []
 gs = reps[0]
 for k in range(a.steps):
     for r in reps[1:]:   # the other replicas' steps stream their data through L2
@@ -35,6 +36,15 @@ for k in range(a.steps):
     p = gs.debug_probe(False).astype(np.int64)
     d = [int(p[i] - p[0]) if p[i] else -1 for i in range(8)]
     rows.append(d)
+    tl = p[16:16 + 1024].reshape(512, 2).astype(np.int64)
+    nb = int((tl[:, 0] > 0).sum())
+    if nb:
+        t0 = tl[:nb, 0].min()
+        st, en = tl[:nb, 0] - t0, tl[:nb, 1] - t0
+        late = np.argsort(-en)[:6]
+        tls.append((st, en))
+        print("   blocks %d: start max %d ns, end median %d max %d ns; block0 end %d; latest:" % (nb, st.max(), np.median(en), en.max(), en[0]),
+              [(int(b), int(st[b]), int(en[b])) for b in late])
     print(a.config, "step %.1f us" % (1e3 * float(ms[0])), "phase cycles", d,
           "| scan ends (ns after block 0 decode):", [int(p[12 + q]) - int(p[11]) if p[12 + q] else None for q in range(2)],
           "block 0 end:", int(p[14]) - int(p[11]) if p[14] else None,

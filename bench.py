@@ -370,7 +370,7 @@ def run_population(args, ws, rank, local, dev):
     pk, pk_src = peaks()
     alu_peak = 148 * 128 * float(pk.get("sm_max_mhz", 1965.0)) * 1e6
     roof = {"bound": "alu", "achieved": ops / (kern_ms / 1e3) / 1e12, "peak": alu_peak / 1e12, "unit": "Tops/s",
-            "frac": ops / (kern_ms / 1e3) / alu_peak, "traffic": None,
+            "frac": ops / (kern_ms / 1e3) / alu_peak, "traffic": traffic_for("cfg5_batch"),
             "peak_source": f"148 SM x 128 lanes x {float(pk.get('sm_max_mhz', 1965.0)):.0f} MHz ({pk_src} sm_max_mhz)",
             "kernel": "k_inter_fast_batch<16, TW, all-inter> (+ key memset), CUDA events around each batch eval",
             "kernel_ms": kern_ms, "candidates_per_launch": float(cnt_all[1:11].sum()), "alg_ops_per_launch": ops}
@@ -604,7 +604,8 @@ def run_tga(args):
     hbm_peak = float(pk["hbm_gbs"]) * 1e9
     t_hbm = alg_bytes / hbm_peak
     t_alu = alg_ops / alu_peak
-    traffic_key = ("etga_" if args.granular else "") + args.config   # captures are per kernel
+    # captures are per kernel: the edge-based and the penalised instantiations have their own
+    traffic_key = ("etga_" if args.granular else "") + ("pen_" if score_mode else "") + args.config
     hbm_view = {"bound": "hbm", "achieved": alg_bytes / inter_avg_s / 1e9, "peak": hbm_peak / 1e9,
                 "unit": "GB/s", "frac": (alg_bytes / inter_avg_s) / hbm_peak,
                 "traffic": traffic_for(traffic_key), "peak_source": pk_src}

@@ -620,6 +620,11 @@ def run_tga(args):
     elif getattr(inst, "pickup", None) is not None:
         kname = ("k_inter<TW, all-inter> (VRPSPDTW: generic tile kernel with the Eq. 3a-d load records; "
                  "intra in its own kernel)")
+    elif getattr(inst, "mode", None) == G.MODE_TWF:
+        kname = ("k_inter<float, TW, all-inter> (TW-F: generic tile kernel, real-valued Eq. 4 times; "
+                 "intra in its own kernel)")
+    elif inst.tw is not None and score_mode:
+        kname = "k_inter<TW, all-inter> (penalised VRPTW: generic tile kernel; intra in its own kernel)"
     elif inst.tw is None:
         kname = "k_inter_fast<all-inter> (CVRP: inter tiles + intra warps in one launch)"
     else:
@@ -736,7 +741,9 @@ def run_tga(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K,
         "warmup": max(args.warmup, 3), "ms_per_step": tot_ms / K, "higher_is_better": True,
         "scaling": "strong" if row_shard else "weak", "vs_baseline": None,
-        "dtype": "int32" if inst.tw is None else "f32 (integer-valued TW-I times; int32 loads)",
+        "dtype": ("int32" if inst.tw is None else
+                  "f32 (real-valued TW-F distances and times)" if getattr(inst, "mode", None) == G.MODE_TWF else
+                  "f32 (integer-valued TW-I times; int32 loads)"),
         "data": "synthetic",
         "config": {"workload": f"{args.config}: {G.CONFIGS.get(args.config, args.config)}; "
                                + (f"edge-based neighbourhood (ETGA) theta={args.granular}; " if args.granular else "")

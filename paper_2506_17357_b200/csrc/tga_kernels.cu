@@ -678,7 +678,9 @@ __device__ __forceinline__ void pick_update_multi(const DevState &S, const ScanA
     __syncthreads();
     if (tid == 0) probe(pr, 1);
     if (pr) S.acc[43] = gtimer();   // diagnostics: block 0 start of decode (globaltimer)
-    if (tid < 32) decode_best(skeys, mask, integer, sb, sl, R, S.Qc, dm);
+    // the old node ids of the changed routes' first pwin slots ride with the decode
+    const int pwin = min(128, snap_cap / 2);
+    if (tid < 32) decode_best(skeys, mask, integer, sb, sl, R, S.Qc, dm, snap, S.node, pwin, S.pitch);
     __syncthreads();
     if (tid == 0) probe(pr, 2);
     const int n1 = dm.applied && !dm.full ? dm.hi[0] - dm.lo[0] : 0;
@@ -696,7 +698,9 @@ __device__ __forceinline__ void pick_update_multi(const DevState &S, const ScanA
             int off = p - 1, k = 0;
             while (off >= nr.p[k].len) { off -= nr.p[k].len; ++k; }
             const Piece &pc = nr.p[k];
-            nd = S.node[sb[pc.src] + (pc.rev ? pc.start + pc.len - 1 - off : pc.start + off)];
+            const int os = sb[pc.src] + (pc.rev ? pc.start + pc.len - 1 - off : pc.start + off);
+            const int r0 = os - dm.plo[0], r1 = os - dm.plo[1];
+            nd = (r0 >= 0 && r0 < pwin) ? snap[r0] : ((r1 >= 0 && r1 < pwin) ? snap[pwin + r1] : S.node[os]);
         }
         nn[j] = nd;
     }

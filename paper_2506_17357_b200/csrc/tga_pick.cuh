@@ -132,46 +132,13 @@ struct Decoded {
     int applied, full, nrt;  // move applied?  changed route outgrew its slots?  #routes changed
     NewRoute nr[2];          // nr[0] = lower route index
     int lo[2], hi[2];        // old (== new) slot ranges of the changed routes
+    int plo[2];              // first slots of the prefetched windows (routes of u and of v)
 };
 
-__device__ __forceinline__ void decode_best(const uint64_t *__restrict__ keys, uint32_t mask, int integer,
-                                            const int32_t *sb, const int32_t *sl, int R, int Qc, Decoded &dm) {
-    const int lane = threadIdx.x & 31;
-    const uint64_t k = (lane < kNV && ((mask >> lane) & 1u)) ? keys[lane] : ~0ull;
-    const bool valid = k != ~0ull;
-    const uint32_t hi = valid ? static_cast<uint32_t>(k >> 32) : 0xFFFFFFFFu;
-    const uint32_t mhi = __reduce_min_sync(0xFFFFFFFFu, hi);
-    const uint32_t win = __ballot_sync(0xFFFFFFFFu, valid && hi == mhi);
-    bool improving = false;
-    if (win) {
-        if (integer) {
-            improving = mhi < 0x80000000u;  // int32 score < 0
-        } else {
-            const uint32_t u = (mhi & 0x80000000u) ? (mhi ^ 0x80000000u) : ~mhi;
-            improving = __uint_as_float(u) < 0.0f;
-        }
-    }
-    if (!improving) {
-        if (lane == 0) dm.applied = 0;
-        return;
-    }
-    const int v = __ffs(win) - 1;  // lowest variant among the lowest scores (reading 5)
-    const uint32_t idx = static_cast<uint32_t>(__shfl_sync(0xFFFFFFFFu, k, v) & 0xFFFFFFFFu);
-    // lanes 0 / 1 locate the u / v slot (physical) in parallel: largest r with sb[r] <= x
-    const int x = lane == 0 ? static_cast<int>(idx / static_cast<uint32_t>(Qc)) : static_cast<int>(idx % static_cast<uint32_t>(Qc));
-    int ra_ = 0;
-    if (lane < 2) {
-        int a = 0, b = R - 1;
-        while (a < b) {
-            const int m = (a + b + 1) >> 1;
-            if (sb[m] <= x) a = m;
-            else b = m - 1;
-        }
-        ra_ = a;
-    }
-    const int ra = __shfl_sync(0xFFFFFFFFu, ra_, 0), rb = __shfl_sync(0xFFFFFFFFu, ra_, 1);
-    const int pa = __shfl_sync(0xFFFFFFFFu, x, 0) - sb[ra], pb = __shfl_sync(0xFFFFFFFFu, x, 1) - sb[rb];
-    if (lane != 0) return;
+// lane 0 of the decode: the 1-2 new routes of variant v at (ra, pa), (rb, pb) as pieces
+// of old routes, their slot ranges and whether they still fit
+__device__ __forceinline__ void decode_pieces(const int32_t *sb, const int32_t *sl, int ra, int rb, int pa, int pb,
+                                              int v, Decoded &dm) {
     const int La = sl[ra], Lb = sl[rb];
     const bool one = v == 0 || (v >= 11 && v < 23);
     // pieces with static indices (empty pieces have len 0 and are skipped by the walk)
@@ -234,6 +201,80 @@ __device__ __forceinline__ void decode_best(const uint64_t *__restrict__ keys, u
     dm.nrt = one ? 1 : 2;
     dm.full = fits ? 0 : 1;
     dm.applied = 1;
+}
+
+// snap / node / pwin (optional): the old node ids of the first pwin slots of the (up to) two
+// changed routes are loaded by the whole warp as soon as the routes are known -- in flight
+// while lane 0 builds the pieces -- and left in snap[0 .. pwin) / snap[pwin .. 2 pwin)
+// (slots below nlim, the length of node).
+__device__ __forceinline__ void decode_best(const uint64_t *__restrict__ keys, uint32_t mask, int integer,
+                                            const int32_t *sb, const int32_t *sl, int R, int Qc, Decoded &dm,
+                                            int32_t *snap = nullptr, const int32_t *node = nullptr, int pwin = 0,
+                                            int nlim = 0) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t k = (lane < kNV && ((mask >> lane) & 1u)) ? keys[lane] : ~0ull;
+    const bool valid = k != ~0ull;
+    const uint32_t hi = valid ? static_cast<uint32_t>(k >> 32) : 0xFFFFFFFFu;
+    const uint32_t mhi = __reduce_min_sync(0xFFFFFFFFu, hi);
+    const uint32_t win = __ballot_sync(0xFFFFFFFFu, valid && hi == mhi);
+    bool improving = false;
+    if (win) {
+        if (integer) {
+            improving = mhi < 0x80000000u;  // int32 score < 0
+        } else {
+            const uint32_t u = (mhi & 0x80000000u) ? (mhi ^ 0x80000000u) : ~mhi;
+            improving = __uint_as_float(u) < 0.0f;
+        }
+    }
+    if (!improving) {
+        if (lane == 0) dm.applied = 0;
+        return;
+    }
+    const int v = __ffs(win) - 1;  // lowest variant among the lowest scores (reading 5)
+    const uint32_t idx = static_cast<uint32_t>(__shfl_sync(0xFFFFFFFFu, k, v) & 0xFFFFFFFFu);
+    // lanes 0 / 1 locate the u / v slot (physical) in parallel: largest r with sb[r] <= x
+    const int x = lane == 0 ? static_cast<int>(idx / static_cast<uint32_t>(Qc)) : static_cast<int>(idx % static_cast<uint32_t>(Qc));
+    int ra_ = 0;
+    if (lane < 2) {
+        int a = 0, b = R - 1;
+        while (a < b) {
+            const int m = (a + b + 1) >> 1;
+            if (sb[m] <= x) a = m;
+            else b = m - 1;
+        }
+        ra_ = a;
+    }
+    const int ra = __shfl_sync(0xFFFFFFFFu, ra_, 0), rb = __shfl_sync(0xFFFFFFFFu, ra_, 1);
+    const int pa = __shfl_sync(0xFFFFFFFFu, x, 0) - sb[ra], pb = __shfl_sync(0xFFFFFFFFu, x, 1) - sb[rb];
+    constexpr int kPre = 4;   // slots per lane and route: windows of up to 128 slots
+    int32_t pre[2][kPre];
+    if (snap) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            // the whole window, across route ends: every old slot in it is then served
+            // from the snapshot, whichever route (of the two) it belongs to
+            const int lo = sb[q ? rb : ra];
+#pragma unroll
+            for (int k = 0; k < kPre; ++k) {
+                const int o = k * 32 + lane;
+                pre[q][k] = (o < pwin && lo + o < nlim) ? node[lo + o] : 0;
+            }
+        }
+    }
+    if (lane == 0) {
+        dm.plo[0] = sb[ra];
+        dm.plo[1] = sb[rb];
+        decode_pieces(sb, sl, ra, rb, pa, pb, v, dm);
+    }
+    if (snap) {   // the loads were in flight during the piece building above
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+#pragma unroll
+            for (int k = 0; k < kPre; ++k) {
+                const int o = k * 32 + lane;
+                if (o < pwin) snap[q * pwin + o] = pre[q][k];
+            }
+    }
 }
 
 // ------------------------------------------------------------------ pick + apply

@@ -854,13 +854,13 @@ __device__ __forceinline__ void pick_update_multi(const DevState &S, const ScanA
     if (pr) S.acc[46] = gtimer();
 }
 
-template <class DT, bool TW>
+template <class DT, bool TW, bool MULTI>
 __device__ __forceinline__ void pick_update_entry(const DevState &S, const ScanArgs<DT> &A, uint32_t mask,
                                                   uint32_t cmask, int integer, int snap_cap, int32_t *smr) {
     unsigned long long *pr = (blockIdx.x == 0 && threadIdx.x == 0 && S.acc[31]) ? S.acc + 32 : nullptr;
     probe(pr, 0);
     if (gridDim.x == 1) pdl_trigger();
-    if (snap_cap > 0 && gridDim.x > 1) {
+    if (MULTI && snap_cap > 0 && gridDim.x > 1) {
         pick_update_multi<DT, TW>(S, A, mask, cmask, integer, smr, snap_cap, pr);
         return;
     }
@@ -885,14 +885,25 @@ __device__ __forceinline__ void pick_update_entry(const DevState &S, const ScanA
     probe(pr, 7);
 }
 
-// population batches: blockIdx.y = solution, per-solution state read from device arrays
+// population batches: blockIdx.y = solution, per-solution state read from device arrays.
+// k_pick_update_b (one block per solution) compiles out the multi-block path, whose code
+// and registers (112 vs 64 with time windows) would otherwise bound the residency of the
+// 1024-block population launch; k_pick_update keeps it (small batches, several blocks each)
 template <class DT, bool TW>
 __global__ void __launch_bounds__(256) k_pick_update(const DevState *__restrict__ states,
                                                      const ScanArgs<DT> *__restrict__ scans, uint32_t mask,
                                                      uint32_t cmask, int integer, int snap_cap) {
     extern __shared__ int32_t smr[];
     pdl_wait();  // the keys (and, two launches back, the slot arrays) come from stream predecessors
-    pick_update_entry<DT, TW>(states[blockIdx.y], scans[blockIdx.y], mask, cmask, integer, snap_cap, smr);
+    pick_update_entry<DT, TW, true>(states[blockIdx.y], scans[blockIdx.y], mask, cmask, integer, snap_cap, smr);
+}
+template <class DT, bool TW>
+__global__ void __launch_bounds__(256, 4) k_pick_update_b(const DevState *__restrict__ states,
+                                                          const ScanArgs<DT> *__restrict__ scans, uint32_t mask,
+                                                          uint32_t cmask, int integer, int snap_cap) {
+    extern __shared__ int32_t smr[];
+    pdl_wait();
+    pick_update_entry<DT, TW, false>(states[blockIdx.y], scans[blockIdx.y], mask, cmask, integer, snap_cap, smr);
 }
 // one solution: its state passed by value in the parameter space, so every pointer and
 // size of the chain (route bases, keys, node ids, C, the record arrays) is a constant-bank
@@ -905,7 +916,7 @@ __global__ void __launch_bounds__(256) k_pick_update1(const __grid_constant__ De
     pdl_wait();
     const bool tl = S.acc[31] != 0 && blockIdx.x < kTimelineBlocks;   // diagnostics: per-block timeline
     if (tl && threadIdx.x == 0) S.acc[kTimeline + 2 * blockIdx.x] = gtimer();
-    pick_update_entry<DT, TW>(S, A, mask, cmask, integer, snap_cap, smr);
+    pick_update_entry<DT, TW, true>(S, A, mask, cmask, integer, snap_cap, smr);
     if (tl) {
         __syncthreads();
         if (threadIdx.x == 0) S.acc[kTimeline + 2 * blockIdx.x + 1] = gtimer();
@@ -933,6 +944,10 @@ cudaError_t launch_pick_update(const DevState *states, const void *scans, int n_
             cudaFuncSetAttribute(k_pick_update<int32_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPickSmemMax);
             cudaFuncSetAttribute(k_pick_update<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPickSmemMax);
             cudaFuncSetAttribute(k_pick_update<float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPickSmemMax);
+            cudaFuncSetAttribute(k_pick_update_b<int32_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPickSmemMax);
+            cudaFuncSetAttribute(k_pick_update_b<int32_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPickSmemMax);
+            cudaFuncSetAttribute(k_pick_update_b<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPickSmemMax);
+            cudaFuncSetAttribute(k_pick_update_b<float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPickSmemMax);
             cudaFuncSetAttribute(k_pick_update1<int32_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPickSmemMax);
             cudaFuncSetAttribute(k_pick_update1<int32_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPickSmemMax);
             cudaFuncSetAttribute(k_pick_update1<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPickSmemMax);
@@ -955,10 +970,17 @@ cudaError_t launch_pick_update(const DevState *states, const void *scans, int n_
     } else {
         const auto *si = static_cast<const ScanArgs<int32_t> *>(scans);
         const auto *sf = static_cast<const ScanArgs<float> *>(scans);
-        if (is_int) e = tw ? launch_pdl(2, k_pick_update<int32_t, true>, g, dim3(256), smem, st, coop, states, si, mask, cmask, 1, snap_cap)
-                           : launch_pdl(2, k_pick_update<int32_t, false>, g, dim3(256), smem, st, coop, states, si, mask, cmask, 1, snap_cap);
-        else e = tw ? launch_pdl(2, k_pick_update<float, true>, g, dim3(256), smem, st, coop, states, sf, mask, cmask, 0, snap_cap)
-                    : launch_pdl(2, k_pick_update<float, false>, g, dim3(256), smem, st, coop, states, sf, mask, cmask, 0, snap_cap);
+        if (multi) {
+            if (is_int) e = tw ? launch_pdl(2, k_pick_update<int32_t, true>, g, dim3(256), smem, st, coop, states, si, mask, cmask, 1, snap_cap)
+                               : launch_pdl(2, k_pick_update<int32_t, false>, g, dim3(256), smem, st, coop, states, si, mask, cmask, 1, snap_cap);
+            else e = tw ? launch_pdl(2, k_pick_update<float, true>, g, dim3(256), smem, st, coop, states, sf, mask, cmask, 0, snap_cap)
+                        : launch_pdl(2, k_pick_update<float, false>, g, dim3(256), smem, st, coop, states, sf, mask, cmask, 0, snap_cap);
+        } else {
+            if (is_int) e = tw ? launch_pdl(2, k_pick_update_b<int32_t, true>, g, dim3(256), smem, st, coop, states, si, mask, cmask, 1, snap_cap)
+                               : launch_pdl(2, k_pick_update_b<int32_t, false>, g, dim3(256), smem, st, coop, states, si, mask, cmask, 1, snap_cap);
+            else e = tw ? launch_pdl(2, k_pick_update_b<float, true>, g, dim3(256), smem, st, coop, states, sf, mask, cmask, 0, snap_cap)
+                        : launch_pdl(2, k_pick_update_b<float, false>, g, dim3(256), smem, st, coop, states, sf, mask, cmask, 0, snap_cap);
+        }
     }
     note_launch();
     return e != cudaSuccess ? e : cudaGetLastError();

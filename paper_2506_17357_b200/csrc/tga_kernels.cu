@@ -1281,8 +1281,13 @@ __device__ __forceinline__ void inter_tile(const SolView<DT> &S, const DT *__res
     }
 }
 
+// two resident CTAs per SM (<= 128 registers): the all-variant time-window instantiations
+// would take ~157 and run one 256-thread CTA per SM on a latency-bound, gather-heavy body
+#ifndef TGA_INTER_MINB
+#define TGA_INTER_MINB 2
+#endif
 template <class DT, bool TW, uint32_t MASK, bool DUMP = false>
-__global__ void __launch_bounds__(kInterThreads) k_inter(const __grid_constant__ SolView<DT> S, const __grid_constant__ CUtensorMap tmap,
+__global__ void __launch_bounds__(kInterThreads, TGA_INTER_MINB) k_inter(const __grid_constant__ SolView<DT> S, const __grid_constant__ CUtensorMap tmap,
                                                          const uint32_t *__restrict__ tiles, int t_lo, int t_hi,
                                                          ScoreParams sp, uint64_t *__restrict__ keys,
                                                          unsigned long long *dump) {

@@ -663,7 +663,7 @@ __global__ void __launch_bounds__(256) k_slot_of(const int32_t *__restrict__ nod
 }
 
 template <bool TW, uint32_t MASK>
-__global__ void __launch_bounds__(256) k_etga(const SlotRec *__restrict__ rec, const SlotTW *__restrict__ rectw,
+__global__ void __launch_bounds__(256, 2) k_etga(const SlotRec *__restrict__ rec, const SlotTW *__restrict__ rectw,
                                               const int32_t *__restrict__ Dp, int pitch, uint32_t Qc,
                                               const int32_t *__restrict__ slot_of, const int32_t *__restrict__ rbase,
                                               const int32_t *__restrict__ pos, const int32_t *__restrict__ rlen,

@@ -1355,7 +1355,7 @@ __global__ void __launch_bounds__(kInterThreads, TGA_INTER_MINB) k_inter(const _
 // instance; every solution has its own Dp (own TMA descriptor, in global
 // memory) and its own 23 keys.  Keys are reduced per work item.
 template <class DT, bool TW, uint32_t MASK>
-__global__ void __launch_bounds__(kInterThreads) k_inter_batch(const SolView<DT> *__restrict__ views,
+__global__ void __launch_bounds__(kInterThreads, TGA_INTER_MINB) k_inter_batch(const SolView<DT> *__restrict__ views,
                                                                const CUtensorMap *__restrict__ maps,
                                                                const uint32_t *__restrict__ work, int n_work,
                                                                ScoreParams sp, uint64_t *__restrict__ keys) {

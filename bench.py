@@ -144,6 +144,23 @@ def peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
+def ncu_for(config: str, candidates: float | None = None):
+    """The committed ncu page of a config's dominant kernel (profiles/ncu_evidence.json): issue
+    activity beside the roofline fraction (the ALG_OPS fraction credits sharing
+    between variants), and executed lane instructions per candidate when the count is known."""
+    p = os.path.join(ROOT, "profiles", "ncu_evidence.json")
+    if not os.path.exists(p):
+        return None
+    e = json.load(open(p)).get(config)
+    if not e:
+        return None
+    out = {"issue_active": e["issue_active_pct"] / 100.0, "warp_instructions": e["warp_instructions"],
+           "ncu_us_cold": e["ncu_us"], "source": e["source"]}
+    if candidates:
+        out["lane_instructions_per_candidate"] = e["warp_instructions"] * 32.0 / candidates
+    return out
+
+
 def traffic_for(config: str):
     """DRAM bytes per launch of the dominant kernel from one committed ncu --set full capture."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
@@ -371,6 +388,7 @@ def run_population(args, ws, rank, local, dev):
     alu_peak = 148 * 128 * float(pk.get("sm_max_mhz", 1965.0)) * 1e6
     roof = {"bound": "alu", "achieved": ops / (kern_ms / 1e3) / 1e12, "peak": alu_peak / 1e12, "unit": "Tops/s",
             "frac": ops / (kern_ms / 1e3) / alu_peak, "traffic": traffic_for("cfg5_batch"),
+            "ncu": ncu_for("cfg5_batch", float(cnt_all[1:11].sum())),
             "peak_source": f"148 SM x 128 lanes x {float(pk.get('sm_max_mhz', 1965.0)):.0f} MHz ({pk_src} sm_max_mhz)",
             "kernel": "k_inter_fast_batch<16, TW, all-inter> (+ key memset), CUDA events around each batch eval",
             "kernel_ms": kern_ms, "candidates_per_launch": float(cnt_all[1:11].sum()), "alg_ops_per_launch": ops}
@@ -632,6 +650,8 @@ def run_tga(args):
     primary = dict(primary, kernel=kname + ", live CUDA events",
                    kernel_ms=inter_avg_s * 1e3, candidates_per_launch=inter_cands,
                    alg_bytes_per_launch=alg_bytes, alg_ops_per_launch=alg_ops)
+    if not args.granular and shard_div == 1:
+        primary["ncu"] = ncu_for(("pen_" if score_mode else "") + args.config, inter_cands)
 
     # ---------------- steady state per operator: CUDA-graph replay of back-to-back sweeps
     per_op = {}
@@ -859,7 +879,9 @@ def north_star_block(args, dev, stream):
             "hbm_frac_kernel": tri / kern_s / hbm_peak, "hbm_frac_sweep": tri / per_s / hbm_peak,
             "alg_ops": ops, "alg_bytes": tri, "alu_peak_tops": alu_peak / 1e12, "hbm_peak_gbs": hbm_peak / 1e9,
             "peak_source": pk_src, "target": "sweep >= 0.6 of the binding roofline (ALU issue: <= 4.6 us)",
-            "target_met": bool(ops / per_s / alu_peak >= 0.6)}
+            "target_met": bool(ops / per_s / alu_peak >= 0.6),
+            "ncu": dict(ncu_for("ns_sweep_ns2000", cand) or {},
+                        note="one cold sweep in isolation under ncu (no overlap with a neighbouring sweep)")}
 
 
 def row_shard_block(args, ws, rank, local, dev, stream):

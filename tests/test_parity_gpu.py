@@ -277,9 +277,10 @@ def test_cfg2_state_b_after_descent():
 
 # ---------------------------------------------------------------- TW-F (real-valued)
 def test_real_valued_time_windows_tolerance():
-    """TW-F: fp32 GPU vs fp64 oracle.  Scores within 1e-4 relative; when the
-    oracle's best is separated from the runner-up by more than the band, the
-    index must match (readings 13, 17)."""
+    """TW-F: fp32 GPU vs fp64 oracle.  The GPU's best score within 1e-4 relative of the
+    oracle's; the candidate it picks is, in the oracle's enumeration, feasible and
+    within the same bar of the optimum; when the oracle's best is separated from the
+    runner-up by more than twice the bar, the index must match (readings 13, 17)."""
     _need_gpu()
     inst, sol = G.gh_like(1, n=200, kind="R2", mode="twf")
     orc = O.Oracle.from_instance(inst)
@@ -295,11 +296,16 @@ def test_real_valued_time_windows_tolerance():
             continue
         assert got[v] is not None
         s_gpu, idx_gpu = got[v]
-        tol = 1e-4 * max(1.0, abs(best.score))
-        assert abs(s_gpu - best.score) <= tol + 1e-3
+        tol = 1e-4 * max(1.0, abs(best.score))          # the north star's 1e-4 relative bar
+        assert abs(s_gpu - best.score) <= tol, (v, s_gpu, best.score)
+        # the GPU's chosen candidate, looked up in the oracle's enumeration: feasible, and
+        # scored by the oracle within the bar of the optimum
+        at = np.nonzero((us.astype(np.int64) * Q + vs) == idx_gpu)[0]
+        assert len(at) == 1, (v, idx_gpu)
+        assert np.isfinite(sc[at[0]]) and abs(sc[at[0]] - best.score) <= tol, (v, sc[at[0]], best.score)
         order = np.sort(sc[np.isfinite(sc)])
-        if len(order) > 1 and order[1] - order[0] > 10 * tol + 1e-2:
-            assert idx_gpu == best.u * Q + best.v
+        if len(order) > 1 and order[1] - order[0] > 2 * tol:
+            assert idx_gpu == best.u * Q + best.v, v
 
 
 # ---------------------------------------------------------------- step / reload / timing ABI

@@ -39,6 +39,9 @@ for rep in range(3):
         iw = p[w]
         qq = lambda c: np.percentile(iw[:, c] - iw[:, 4], [0, 50, 90, 100]).round(0).astype(int).tolist()
         print("   intra warp (from its start): slot loads", qq(5), "keys", qq(6), "redux", qq(7), "n", int(w.sum()))
+    if w.any() and (~w).any():
+        pe = lambda m: np.percentile(p[m][:, 3], [50, 90, 100]).round(0).astype(int).tolist()
+        print("   end ns [50,90,max]: CTAs with an intra unit", pe(w), " without", pe(~w))
     d = p[:, 3] - p[:, 2]
     print("   per-CTA tile phase ns [min,50,90,max]", np.percentile(d, [0, 50, 90, 100]).round(0).astype(int).tolist(),
           " wait for first data", np.percentile(p[:, 2] - p[:, 1], [0, 50, 90, 100]).round(0).astype(int).tolist())

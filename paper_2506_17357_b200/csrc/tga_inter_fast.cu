@@ -198,7 +198,12 @@ __device__ __forceinline__ bool stream_direct(int k) {
     return (k == 0 || k == 7 || k == 12 || k == 15) ? true : (k <= 6 ? (k & 1) == 1 : (k == 8 || k == 10 || k == 13));
 }
 
-template <int U, bool TW, uint32_t MASK, bool DUMP, bool PEN, class ItemF>
+// SC (population batches): one column region shared by both stages (rows and box stay
+// double-buffered) -- a lane reads its column record once per tile into registers, so the
+// region is refilled, on its own mbarrier bar[2], only when the run moves to another
+// (solution, column band), after every warp has read the last tile of the old one; the
+// CTA's buffers shrink from 63 to 45 KB (time windows): 4 CTAs per SM instead of 3.
+template <int U, bool TW, uint32_t MASK, bool DUMP, bool PEN, class ItemF, bool SC = false>
 __device__ __forceinline__ void fast_body(ItemF item, int w0, int w1, int wstride, uint64_t *bar,
                                           unsigned long long (*red)[23], unsigned char *sm, int32_t cap,
                                           const SolView<int32_t> &SV, const ScoreParams &sp, uint32_t imask,
@@ -208,16 +213,21 @@ __device__ __forceinline__ void fast_body(ItemF item, int w0, int w1, int wstrid
     constexpr int BW = G::BoxW;
     constexpr int NV = 11;
     // stage b at sm + b * Stage: box | row records | column records | TW rows | TW columns
+    // (SC: stage b at sm + b * StageSC: box | row records | TW rows; the columns after both)
+    constexpr int StageSC = G::BoxPad + G::RowBytes + G::RowTW;
+    constexpr int SB = SC ? StageSC : G::Stage;
     int32_t *const dp0 = reinterpret_cast<int32_t *>(sm);
-    int32_t *const dp1 = reinterpret_cast<int32_t *>(sm + G::Stage);
+    int32_t *const dp1 = reinterpret_cast<int32_t *>(sm + SB);
     SlotRec *const rows0 = reinterpret_cast<SlotRec *>(sm + G::BoxPad);
-    SlotRec *const rows1 = reinterpret_cast<SlotRec *>(sm + G::Stage + G::BoxPad);
-    SlotRec *const cols0 = reinterpret_cast<SlotRec *>(sm + G::BoxPad + G::RowBytes);
-    SlotRec *const cols1 = reinterpret_cast<SlotRec *>(sm + G::Stage + G::BoxPad + G::RowBytes);
-    SlotTW *const trows0 = reinterpret_cast<SlotTW *>(sm + G::BoxPad + G::RowBytes + G::ColBytes);
-    SlotTW *const trows1 = reinterpret_cast<SlotTW *>(sm + G::Stage + G::BoxPad + G::RowBytes + G::ColBytes);
-    SlotTW *const tcols0 = reinterpret_cast<SlotTW *>(sm + G::BoxPad + G::RowBytes + G::ColBytes + G::RowTW);
-    SlotTW *const tcols1 = reinterpret_cast<SlotTW *>(sm + G::Stage + G::BoxPad + G::RowBytes + G::ColBytes + G::RowTW);
+    SlotRec *const rows1 = reinterpret_cast<SlotRec *>(sm + SB + G::BoxPad);
+    SlotRec *const cols0 = reinterpret_cast<SlotRec *>(SC ? sm + 2 * StageSC : sm + G::BoxPad + G::RowBytes);
+    SlotRec *const cols1 = reinterpret_cast<SlotRec *>(SC ? sm + 2 * StageSC : sm + G::Stage + G::BoxPad + G::RowBytes);
+    SlotTW *const trows0 = reinterpret_cast<SlotTW *>(sm + G::BoxPad + G::RowBytes + (SC ? 0 : G::ColBytes));
+    SlotTW *const trows1 = reinterpret_cast<SlotTW *>(sm + SB + G::BoxPad + G::RowBytes + (SC ? 0 : G::ColBytes));
+    SlotTW *const tcols0 = reinterpret_cast<SlotTW *>(SC ? sm + 2 * StageSC + G::ColBytes
+                                                         : sm + G::BoxPad + G::RowBytes + G::ColBytes + G::RowTW);
+    SlotTW *const tcols1 = reinterpret_cast<SlotTW *>(SC ? sm + 2 * StageSC + G::ColBytes
+                                                         : sm + G::Stage + G::BoxPad + G::RowBytes + G::ColBytes + G::RowTW);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const bool prb = (flags & 2) && tid == 0 && blockIdx.x < 4096;
 
@@ -231,12 +241,19 @@ __device__ __forceinline__ void fast_body(ItemF item, int w0, int w1, int wstrid
     // largest part of a tile's traffic).  s_colkey[b] is written by the one thread that
     // refills stage b, after every warp has released it.
     __shared__ int s_colkey[2];
-    if (tid == 0) s_colkey[0] = s_colkey[1] = -1;
+    __shared__ int s_cout;   // SC: warps done with the column region's current content
+    if (tid == 0) { s_colkey[0] = s_colkey[1] = -1; s_cout = 0; }
     __syncthreads();
+    auto colkey = [](const FastItem &f) { return f.sol * 1024 + f.J; };
+    auto issue_cols = [&](const FastItem &f) {   // SC: the shared column region, on bar[2]
+        f_expect(&bar[2], G::ColBytes + G::ColTW);
+        f_bulk(cols0, f.rec + f.J * kFastTV, G::ColBytes, &bar[2]);
+        if (TW) f_bulk(tcols0, f.rectw + f.J * kFastTV, G::ColTW, &bar[2]);
+    };
     auto issue = [&](const FastItem &f, int b) {
         uint64_t *br = b ? &bar[1] : &bar[0];
         const int key = f.sol * 1024 + f.J;
-        const bool cols = s_colkey[b] != key;
+        const bool cols = !SC && s_colkey[b] != key;
         s_colkey[b] = key;   // before the arrive below publishes it to the stage's next refiller
         f_expect(br, G::BoxBytes + G::RowBytes + G::RowTW + (cols ? G::ColBytes + G::ColTW : 0));
         f_tma2d(b ? dp1 : dp0, f.map, f.J * kFastTV - 4, f.I * U - 1, br);
@@ -282,6 +299,7 @@ __device__ __forceinline__ void fast_body(ItemF item, int w0, int w1, int wstrid
     if (tid == 0) {
         s_out[0] = 0;
         s_out[1] = 0;
+        if (SC && w < w1) issue_cols(cur);
         if (w < w1) issue(cur, 0);                              // arrive (release) publishes s_out
         if (w + wstride < w1) issue(item(w + wstride), 1);
     }
@@ -302,7 +320,8 @@ __device__ __forceinline__ void fast_body(ItemF item, int w0, int w1, int wstrid
     uint64_t *keys = w < w1 ? cur.keys : keys0;   // keys0: intra-only CTAs of one solution
     int sol = cur.sol;
     const uint32_t mul32 = static_cast<uint32_t>(flags >> 8);   // 32, a kernel parameter: keep() packs with IMAD
-    uint32_t ph0 = 0u, ph1 = 0u;
+    uint32_t ph0 = 0u, ph1 = 0u, phc = 0u;
+    int held = -1;   // SC: the (solution, column band) key the column region holds for this warp
     for (int it = 0; w < w1; w += wstride, ++it) {
         const int b = it & 1;
         const FastItem f = cur;
@@ -323,10 +342,29 @@ __device__ __forceinline__ void fast_body(ItemF item, int w0, int w1, int wstrid
         const int v = v0 + col;
         if (b) { f_wait(&bar[1], ph1); ph1 ^= 1u; } else { f_wait(&bar[0], ph0); ph0 ^= 1u; }
         if (prb && it == 0) g_inter_probe[8 * blockIdx.x + 2] = gtime();
+        if (SC && colkey(f) != held) {   // warp-uniform: a new column epoch
+            f_wait(&bar[2], phc);
+            phc ^= 1u;
+            held = colkey(f);
+        }
         // ---- this lane's column record, bulk-copied with the tile (five 16-byte LDS)
         const SlotRec V = (b ? cols1 : cols0)[col];
         SlotTW VT{};
         if (TW) VT = (b ? tcols1 : tcols0)[col];
+        if (SC && w + wstride < w1 && colkey(cur) != colkey(f)) {
+            // the last tile of this column epoch: once every warp has its records in registers,
+            // the last one out refills the region with the next epoch's columns
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence_block();
+                if (atomicAdd(&s_cout, 1) == kFastThreads / 32 - 1) {
+                    s_cout = 0;
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before the copy
+                    issue_cols(cur);
+                }
+            }
+            __syncwarp();
+        }
         const SlotTW *TR = b ? trows1 : trows0;
         (void)TR;
         const int32_t *T = b ? dp1 : dp0;
@@ -560,6 +598,10 @@ static cudaError_t launch_fast_u(uint32_t mask, const SlotRec *rec, const SlotTW
     return err;
 }
 
+#ifndef TGA_BATCH_SHARED_COLS
+#define TGA_BATCH_SHARED_COLS 1
+#endif
+constexpr bool kBatchSharedCols = TGA_BATCH_SHARED_COLS != 0;
 // Population batch (BASELINE config 5) on the fast path: a contiguous run of
 // (solution, tile) items per CTA; the running minima are flushed into a
 // solution's keys when the run moves on to the next solution.
@@ -570,12 +612,13 @@ __global__ void __launch_bounds__(kFastThreads) k_inter_fast_batch(const FastSol
                                                                    int32_t cap, ScoreParams sp, int flags) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *sm = smem_raw + ((128u - (s_u32(smem_raw) & 127u)) & 127u);
-    __shared__ uint64_t bar[2];
+    __shared__ uint64_t bar[3];
     __shared__ unsigned long long red[kFastThreads / 32][23];
     const int tid = threadIdx.x;
     if (tid == 0) {
         f_mbar_init(&bar[0]);
         f_mbar_init(&bar[1]);
+        f_mbar_init(&bar[2]);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     for (int i = tid; i < (kFastThreads / 32) * 23; i += kFastThreads) red[i / 23][i % 23] = kNoKey;
@@ -591,9 +634,16 @@ __global__ void __launch_bounds__(kFastThreads) k_inter_fast_batch(const FastSol
                         static_cast<int>(c & 0x3FFu)};
     };
     const SolView<int32_t> none{};
-    fast_body<U, TW, MASK, false, false>(item, w0, w1, 1, bar, red, sm, cap, none, sp, 0u, 0, 0, 0, 1, flags);
+    fast_body<U, TW, MASK, false, false, decltype(item), kBatchSharedCols>(item, w0, w1, 1, bar, red, sm, cap, none, sp,
+                                                                         0u, 0, 0, 0, 1, flags);
 }
 
+// the batch kernel's dynamic shared memory: two box + row stages and one column region (SC)
+template <int U, bool TW>
+constexpr int batch_smem() {
+    using G = FastGeom<U, TW>;
+    return kBatchSharedCols ? 2 * (G::BoxPad + G::RowBytes + G::RowTW) + G::ColBytes + G::ColTW + 128 : G::Smem;
+}
 template <int U, bool TW, uint32_t MASK>
 static cudaError_t launch_fast_batch_t(const FastSol *sols, const CUtensorMap *maps, const uint32_t *work, int n_work,
                                        int32_t cap, const ScoreParams &sp, int max_grid, cudaStream_t st) {
@@ -603,15 +653,15 @@ static cudaError_t launch_fast_batch_t(const FastSol *sols, const CUtensorMap *m
     static int res_cap[kMaxDevices];
     const int d = once_per_device(pd, [](int dev) {
         auto k = k_inter_fast_batch<U, TW, MASK>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, FastGeom<U, TW>::Smem);
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, batch_smem<U, TW>());
         int sms = 0, b = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k, kFastThreads, FastGeom<U, TW>::Smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k, kFastThreads, batch_smem<U, TW>());
         res_cap[dev] = std::max(1, b) * std::max(1, sms);
     });
     const int res = res_cap[d];
     const int grid = std::max(1, std::min(n_work, std::min(res, max_grid)));
-    kern<<<grid, kFastThreads, G::Smem, st>>>(sols, maps, work, n_work, cap, sp, 32 << 8);
+    kern<<<grid, kFastThreads, batch_smem<U, TW>(), st>>>(sols, maps, work, n_work, cap, sp, 32 << 8);
     note_launch();
     return cudaGetLastError();
 }
